@@ -1,0 +1,222 @@
+/*
+ * geopipe_b200.h - C-ABI of the B200 plan-evaluation engine.
+ *
+ * Drop-in boundary for the reference planner's hot path
+ * (/root/reference/pkg/src/geopipe/, "src/" below).  The reference is pure
+ * Python with no FFI of its own; each entry point here replaces one Python
+ * seam and is bound from Python with ctypes:
+ *
+ *   gp_ctx_create / gp_ctx_load  <- the frozen inputs of search_plan /
+ *                                   exhaustive_plan: ModelSpec, ClusterTopology,
+ *                                   GroupIndex, SearchConfig.bottleneck_factor
+ *                                   (src/planner.py:330-335, :374-379)
+ *   gp_eval_batch               <- a batch of _evaluate(candidate, b, m, ...)
+ *                                   calls (src/planner.py:313-327)
+ *   gp_argmin_range             <- the exhaustive_plan loop nest and its
+ *                                   strict-< key (src/planner.py:389-399)
+ *   gp_plan_detail              <- build_plan + plan_cost for one candidate:
+ *                                   splits and CostBreakdown of the winner
+ *                                   (src/planner.py:203-223, src/costmodel.py:84-100)
+ *   gp_set_bandwidth            <- a bandwidth snapshot: LinkMeasurement with
+ *                                   scaled bandwidth -> build_topology ->
+ *                                   group_first_level (min_intra_bandwidth)
+ *                                   (src/profiling.py:48-78,167-215,
+ *                                    src/grouping.py:69-75)
+ *   gp_sim_1f1b                 <- simulate_timing(timing, ONE_F_ONE_B,
+ *                                   SimConfig(iterations=1)).makespan
+ *                                   (src/simulator.py:71-113, src/engine.py:230-431)
+ *
+ * Conventions: plain pointers and sizes, no exceptions.  Every call returns a
+ * status; GP_OK is 0 and the others map onto the reference's exceptions
+ * (src/errors.py).  gp_last_error() returns the message of the last failure
+ * on the calling thread.  One context per host thread; a context owns one
+ * CUDA device and one stream.  There is no CPU fallback: when no sm_100
+ * device is present gp_ctx_create fails with GP_ERR_CUDA.
+ */
+#ifndef GEOPIPE_B200_H
+#define GEOPIPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (src/errors.py) */
+enum {
+    GP_OK = 0,
+    GP_ERR_INPUT = 1,          /* InputFileError / ValueError                 */
+    GP_ERR_INFEASIBLE_SPLIT = 2,/* InfeasibleSplitError                       */
+    GP_ERR_NO_FEASIBLE = 3,    /* NoFeasiblePlanError                         */
+    GP_ERR_DEGENERATE = 4,     /* DegenerateGroupError (src/timing.py:138,142)*/
+    GP_ERR_TOPOLOGY = 5,       /* InvalidTopologyError (src/timing.py:172,184,215) */
+    GP_ERR_CUDA = 6,           /* device failure / no sm_100 device           */
+    GP_ERR_TIMING = 7,         /* InvalidTimingError (src/engine.py:136-141)  */
+    GP_ERR_SCHEDULING = 8      /* SchedulingBugError (src/engine.py:422)      */
+};
+
+/* split kinds, src/plans.py:60-66 */
+enum { GP_UNIFORM = 0, GP_ASYM_PP = 1, GP_ASYM_DP = 2, GP_ASYM_TP_DP = 3 };
+
+#define GP_MAX_STAGES 16   /* first-level groups per plan            */
+#define GP_MAX_SGS 16      /* second-level groups per first-level one */
+#define GP_MAX_LAYERS 255  /* layer counts travel as uint8            */
+#define GP_MAX_MEMBERS 1024 /* devices per first-level group          */
+
+/*
+ * One planner instance, structure-of-arrays, host memory.  All values are
+ * the reference's own (already derived) numbers:
+ *   layers   : LayerSpec fields (src/plans.py:12-30)
+ *   devices  : p_c = compute[d].p_c, memory_bytes (src/profiling.py:125-156);
+ *              `id_rank` = position of the device id in sorted string order
+ *              (gateway tie-break, src/timing.py:104-113)
+ *   links    : dense D x D matrices of p_t, latency_seconds and
+ *              bandwidth_bytes_per_s (symmetric; diagonal unused)
+ *   groups   : first-level groups in *string-sorted id order* (the order of
+ *              sorted(groups.fgs), src/planner.py:384); members in
+ *              member_device_ids order; second-level groups of each in
+ *              sgs_by_fg order (src/grouping.py:21-39, src/timing.py:28-44)
+ */
+typedef struct gp_instance {
+    uint32_t n_layers;
+    const double *fwd_flops, *bwd_input_flops, *bwd_weight_flops;
+    const double *activation_out_bytes, *param_bytes;
+    uint32_t n_batch;            /* global_batch_candidates */
+    const int64_t *batch;
+    uint32_t n_micro;            /* microbatch_candidates   */
+    const int64_t *micro;
+
+    uint32_t n_devices;
+    const double *p_c;
+    const double *memory_bytes;
+    const uint32_t *id_rank;
+    const double *p_t;           /* [n_devices * n_devices] */
+    const double *latency;       /* [n_devices * n_devices] */
+    const double *bandwidth;     /* [n_devices * n_devices] */
+
+    uint32_t n_fgs;
+    const uint32_t *fg_member_offset;   /* [n_fgs + 1]  -> fg_members          */
+    const uint32_t *fg_members;         /* device indices                       */
+    const double *fg_capacity;          /* aggregate_capacity                   */
+    const double *fg_min_bw;            /* min_intra_bandwidth                  */
+    const uint8_t *fg_has_min_bw;       /* 0 where min_intra_bandwidth is None  */
+    const uint32_t *fg_sg_offset;       /* [n_fgs + 1]  -> second-level groups  */
+    const uint32_t *sg_member_offset;   /* [n_sgs + 1]  -> sg_members           */
+    const uint32_t *sg_members;         /* device indices                       */
+    const double *sg_capacity;          /* aggregate_capacity                   */
+
+    double bottleneck_factor;           /* SearchConfig.bottleneck_factor       */
+} gp_instance;
+
+/* Result of an argmin over a candidate range (exhaustive_plan's `best`). */
+typedef struct gp_best {
+    double cost;           /* +inf when every candidate is memory-infeasible   */
+    uint64_t index;        /* enumeration index of the winner (see below)      */
+    uint32_t batch_index;  /* into gp_instance.batch                           */
+    uint32_t micro_index;  /* into gp_instance.micro                           */
+    uint32_t k;            /* number of stages                                 */
+    uint8_t order[GP_MAX_STAGES];   /* fg indices (string order)               */
+    uint8_t counts[GP_MAX_STAGES];  /* layers per stage                        */
+    uint64_t evaluated;    /* candidates evaluated (exhaustive_plan.evaluated) */
+} gp_best;
+
+/* Full evaluation of one candidate (plan + CostBreakdown). */
+typedef struct gp_stage_info {
+    uint32_t kind;                    /* GP_UNIFORM ...                         */
+    uint32_t n_parts;
+    /* ASYM_PP: part i = (sg index within fg, layer_start, layer_end)          */
+    uint32_t pp_sg[GP_MAX_SGS];
+    uint32_t pp_start[GP_MAX_SGS];
+    uint32_t pp_end[GP_MAX_SGS];
+    double fill_seconds, run_seconds, residual_seconds, collective_seconds;
+} gp_stage_info;
+
+typedef struct gp_plan_info {
+    int32_t feasible;                 /* memory_feasible (src/planner.py:248)   */
+    uint32_t k;
+    double plan_cost;                 /* +inf when infeasible                   */
+    gp_stage_info stage[GP_MAX_STAGES];
+} gp_plan_info;
+
+/* Group constants of the TP x DP grid and DP splits (src/planner.py:107-154):
+ * they depend on the group only, not on the layer range. */
+typedef struct gp_group_info {
+    int32_t tp_ok;                        /* rank-1 grid exists            */
+    uint32_t n_members, n_sgs;
+    double tp_row[GP_MAX_MEMBERS];        /* row fraction, member order    */
+    double tp_col[GP_MAX_MEMBERS];        /* column fraction               */
+    double dp_fraction[GP_MAX_SGS];       /* second-level data fractions   */
+} gp_group_info;
+
+typedef struct gp_ctx gp_ctx;
+
+/* Version / capability probe (no device needed). */
+const char *gp_version(void);
+/* Message of the last failing call on this thread. */
+const char *gp_last_error(void);
+
+/* Create a context on CUDA device `device` (no data yet). */
+int gp_ctx_create(int device, gp_ctx **out);
+/* Stage an instance into HBM and build the per-(group, layer-range) tables
+ * (kernel K1).  Re-callable: a new instance replaces the old one. */
+int gp_ctx_load(gp_ctx *ctx, const gp_instance *inst);
+void gp_ctx_destroy(gp_ctx *ctx);
+
+/*
+ * Explicit batch (kernel K2): candidate i is stage order order[i*k .. i*k+k),
+ * layer counts counts[i*k .. i*k+k) and (b, m) pair
+ * bm[i] = batch_index * n_micro + micro_index.  Writes cost[i] (+inf when
+ * memory-infeasible, as _evaluate's INFEASIBLE) and status[i] (GP_OK or the
+ * per-candidate error the reference would raise).  Host pointers.
+ */
+int gp_eval_batch(gp_ctx *ctx, uint32_t k, uint64_t n,
+                  const uint8_t *order, const uint8_t *counts,
+                  const uint8_t *bm, double *cost, uint8_t *status);
+/* Same with device pointers, asynchronous on the context's stream. */
+int gp_eval_batch_device(gp_ctx *ctx, uint32_t k, uint64_t n,
+                         const uint8_t *d_order, const uint8_t *d_counts,
+                         const uint8_t *d_bm, double *d_cost,
+                         uint8_t *d_status);
+
+/*
+ * Exhaustive enumeration (kernel K3).  Index space, as exhaustive_plan walks
+ * it (src/planner.py:389-392): idx = (bm * k! + perm_rank) * C(n-1, k-1)
+ * + comp_rank with bm = batch_index * n_micro + micro_index, permutations of
+ * all fgs in lexicographic order and compositions in lexicographic order.
+ * Returns the argmin over [lo, hi) of the reference key
+ * (cost, (order, cuts)) with earliest-index tie-break.
+ * gp_space_size() gives the total count.
+ */
+int gp_space_size(gp_ctx *ctx, uint64_t *out);
+int gp_argmin_range(gp_ctx *ctx, uint64_t lo, uint64_t hi, gp_best *out);
+/* Asynchronous variant writing the per-launch result to device memory
+ * (benchmarks / multi-GPU reduction); read with gp_argmin_fetch. */
+int gp_argmin_range_async(gp_ctx *ctx, uint64_t lo, uint64_t hi);
+int gp_argmin_fetch(gp_ctx *ctx, gp_best *out);
+
+/* Splits + CostBreakdown of one candidate (the winner), on the device. */
+int gp_plan_detail(gp_ctx *ctx, uint32_t k, const uint8_t *order,
+                   const uint8_t *counts, uint32_t bm, gp_plan_info *out);
+
+/* TP tiles / DP fractions of group f, computed on the device. */
+int gp_group_splits(gp_ctx *ctx, uint32_t f, gp_group_info *out);
+
+/*
+ * Bandwidth snapshot: replace bandwidth_bytes_per_s of every link with
+ * bandwidth[u*D+v] (p_t and latency unchanged) and recompute each group's
+ * min_intra_bandwidth and the boundary tables on the device.
+ */
+int gp_set_bandwidth(gp_ctx *ctx, const double *bandwidth);
+
+/* Stream the context uses (cudaStream_t), for event timing by callers. */
+void *gp_ctx_stream(gp_ctx *ctx);
+
+/* Diagnostics: measured FP64 DADD issue rate of `device` (ops/s), the
+ * roofline denominator of the range kernel (bench.py). */
+int gp_diag_fp64_peak(int device, double *dadd_per_second);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEOPIPE_B200_H */

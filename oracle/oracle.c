@@ -1,0 +1,760 @@
+/*
+ * oracle.c - CPU restatement of the reference planner's hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library, and
+ * only as the checker or the timed CPU baseline - never as the product path.
+ *
+ * It re-states, candidate by candidate and in the reference's operation
+ * order, what `_evaluate` (src/planner.py:313-327) computes, so that it is an
+ * independent check of the table-driven CUDA engine.  src/ =
+ * /root/reference/pkg/src/geopipe/.  Parity pinning: tests/test_oracle.py
+ * checks this file bit-for-bit against the live reference (in the build
+ * container) and against the committed fixtures in tests/golden/ generated
+ * from the reference by scripts/make_golden.py.
+ *
+ * Compile with -ffp-contract=off (no FMA contraction): every + - * / below is
+ * one IEEE double operation, exactly as CPython performs it.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "../include/geopipe_b200.h"
+
+#define OR_MAX_DEV GP_MAX_MEMBERS
+
+/* ------------------------------------------------------------------------
+ * CPython 3.12 builtin sum() over floats: Neumaier compensation
+ * (Python/bltinmodule.c, builtin_sum_impl).  Start value is int 0, so the
+ * first element enters as 0 + x0.
+ * ---------------------------------------------------------------------- */
+double or_psum(const double *x, size_t n)
+{
+    if (n == 0)
+        return 0.0;
+    double f = 0.0 + x[0];
+    double c = 0.0;
+    for (size_t i = 1; i < n; ++i) {
+        double xi = x[i];
+        double t = f + xi;
+        if (fabs(f) >= fabs(xi))
+            c += (f - t) + xi;
+        else
+            c += (xi - t) + f;
+        f = t;
+    }
+    if (c != 0.0 && isfinite(c))
+        f += c;
+    return f;
+}
+
+/* sum over a strided generator: sum(model.layers[i].<field> for i in [a,b)) */
+static double psum_range(const double *x, uint32_t a, uint32_t b)
+{
+    return or_psum(x + a, (size_t)(b - a));
+}
+
+/* math.isclose(a, b, rel_tol, abs_tol=0) (Modules/mathmodule.c) */
+static int py_isclose(double a, double b, double rel_tol)
+{
+    if (a == b)
+        return 1;
+    if (isinf(a) || isinf(b))
+        return 0;
+    double diff = fabs(b - a);
+    return (diff <= fabs(rel_tol * b)) || (diff <= fabs(rel_tol * a));
+}
+
+/* ------------------------------------------------------------------------
+ * proportional_split (src/planner.py:65-87).  Returns 0 or
+ * GP_ERR_INFEASIBLE_SPLIT.
+ * ---------------------------------------------------------------------- */
+int or_proportional_split(int64_t total, const double *w, int n, int minimum,
+                          int64_t *shares)
+{
+    double wsum = or_psum(w, (size_t)n);
+    double rem[GP_MAX_SGS];
+    int idx[GP_MAX_SGS];
+    int64_t ssum = 0;
+    for (int i = 0; i < n; ++i) {
+        double raw = ((double)total * w[i]) / wsum;
+        shares[i] = (int64_t)floor(raw);
+        rem[i] = raw - (double)shares[i];
+        ssum += shares[i];
+        idx[i] = i;
+    }
+    int64_t leftover = total - ssum;
+    /* sorted(range(n), key=lambda i: (-rem[i], i)) - stable insertion sort */
+    for (int i = 1; i < n; ++i) {
+        int v = idx[i];
+        int j = i - 1;
+        while (j >= 0 && (-rem[idx[j]] > -rem[v])) {
+            idx[j + 1] = idx[j];
+            --j;
+        }
+        idx[j + 1] = v;
+    }
+    /* python slice [:leftover] */
+    int64_t take = leftover >= 0 ? (leftover < n ? leftover : n)
+                                 : (n + leftover > 0 ? n + leftover : 0);
+    for (int64_t t = 0; t < take; ++t)
+        shares[idx[t]] += 1;
+    if (minimum > 0) {
+        for (int i = 0; i < n; ++i) {
+            while (shares[i] < minimum) {
+                int donor = 0;
+                for (int j = 1; j < n; ++j)
+                    if (shares[j] > shares[donor])
+                        donor = j;
+                if (shares[donor] <= minimum)
+                    return GP_ERR_INFEASIBLE_SPLIT;
+                shares[donor] -= 1;
+                shares[i] += 1;
+            }
+        }
+    }
+    return GP_OK;
+}
+
+/* ------------------------------------------------------------------------
+ * split_asymmetric_tp_dp (src/planner.py:116-154).  Returns 1 and fills
+ * rf/cf when a rank-1 grid exists (FactorizationError otherwise -> 0).
+ * ---------------------------------------------------------------------- */
+int or_tp_grid(const double *caps, int n, double *rf, double *cf)
+{
+    int shp_r[64], shp_c[64], ns = 0;
+    for (int r = 2; r < n && ns < 64; ++r)
+        if (n % r == 0 && n / r >= 2) {
+            shp_r[ns] = r;
+            shp_c[ns] = n / r;
+            ++ns;
+        }
+    /* sorted(..., key=|r-c|): stable */
+    for (int i = 1; i < ns; ++i) {
+        int r = shp_r[i], c = shp_c[i], j = i - 1;
+        while (j >= 0 && abs(shp_r[j] - shp_c[j]) > abs(r - c)) {
+            shp_r[j + 1] = shp_r[j];
+            shp_c[j + 1] = shp_c[j];
+            --j;
+        }
+        shp_r[j + 1] = r;
+        shp_c[j + 1] = c;
+    }
+    for (int s = 0; s < ns; ++s) {
+        int r = shp_r[s], c = shp_c[s];
+#define GRID(i, j) caps[(j) * r + (i)]
+        int ok = 1;
+        for (int i = 0; i < r && ok; ++i)
+            for (int j = 0; j < c && ok; ++j)
+                ok = py_isclose(GRID(i, j) * GRID(0, 0), GRID(i, 0) * GRID(0, j), 1e-9);
+        if (!ok)
+            continue;
+        double rows[OR_MAX_DEV], cols[OR_MAX_DEV];
+        for (int i = 0; i < r; ++i)
+            rows[i] = GRID(i, 0);
+        for (int j = 0; j < c; ++j)
+            cols[j] = GRID(0, j);
+#undef GRID
+        double rsum = or_psum(rows, (size_t)r), csum = or_psum(cols, (size_t)c);
+        for (int k = 0; k < n; ++k) {
+            rf[k] = rows[k % r] / rsum;
+            cf[k] = cols[k / r] / csum;
+        }
+        return 1;
+    }
+    return 0;
+}
+
+/* split_asymmetric_dp (src/planner.py:107-113) */
+void or_dp_fractions(const double *caps, int n, double *fr)
+{
+    double total = or_psum(caps, (size_t)n);
+    for (int i = 0; i < n; ++i)
+        fr[i] = caps[i] / total;
+    fr[n - 1] = 1.0 - or_psum(fr, (size_t)(n - 1));
+}
+
+/* ------------------------------------------------------------------------
+ * per-candidate evaluation
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int kind;
+    int n_parts;
+    uint32_t pp_start[GP_MAX_SGS], pp_end[GP_MAX_SGS];
+} stage_split;
+
+static double total_flops(const gp_instance *I, uint32_t i)
+{
+    /* LayerSpec.total_flops (src/plans.py:28-30) */
+    return (I->fwd_flops[i] + I->bwd_input_flops[i]) + I->bwd_weight_flops[i];
+}
+
+static double psum_total_flops(const gp_instance *I, uint32_t a, uint32_t b)
+{
+    double buf[GP_MAX_LAYERS + 1];
+    for (uint32_t i = a; i < b; ++i)
+        buf[i - a] = total_flops(I, i);
+    return or_psum(buf, b - a);
+}
+
+/* choose_intra_split (src/planner.py:157-200) */
+static void choose_split(const gp_instance *I, uint32_t f, uint32_t a, uint32_t b,
+                         stage_split *out, double *tp_rf, double *tp_cf)
+{
+    uint32_t m0 = I->fg_member_offset[f], m1 = I->fg_member_offset[f + 1];
+    uint32_t s0 = I->fg_sg_offset[f], s1 = I->fg_sg_offset[f + 1];
+    uint32_t nmem = m1 - m0, nsg = s1 - s0;
+    out->n_parts = 0;
+    if (nmem == 1 || nsg == 1) {
+        out->kind = GP_UNIFORM;
+        return;
+    }
+    const double *caps = I->sg_capacity + s0;
+    /* split_asymmetric_pp (src/planner.py:90-104) */
+    uint32_t n = b - a;
+    if (nsg <= n) {
+        int64_t shares[GP_MAX_SGS];
+        if (or_proportional_split((int64_t)n, caps, (int)nsg, 1, shares) == GP_OK) {
+            double times[GP_MAX_SGS];
+            uint32_t pos = a;
+            for (uint32_t j = 0; j < nsg; ++j) {
+                out->pp_start[j] = pos;
+                out->pp_end[j] = pos + (uint32_t)shares[j];
+                pos += (uint32_t)shares[j];
+                double flops = psum_total_flops(I, out->pp_start[j], out->pp_end[j]);
+                times[j] = flops / caps[j];
+            }
+            double mean = or_psum(times, nsg) / (double)nsg;
+            double mx = times[0];
+            for (uint32_t j = 1; j < nsg; ++j)
+                if (times[j] > mx)
+                    mx = times[j];
+            if (mx <= I->bottleneck_factor * mean) {
+                out->kind = GP_ASYM_PP;
+                out->n_parts = (int)nsg;
+                return;
+            }
+        }
+    }
+    double dcaps[OR_MAX_DEV];
+    for (uint32_t j = 0; j < nmem; ++j)
+        dcaps[j] = I->p_c[I->fg_members[m0 + j]];
+    if (or_tp_grid(dcaps, (int)nmem, tp_rf, tp_cf)) {
+        out->kind = GP_ASYM_TP_DP;
+        out->n_parts = (int)nmem;
+        return;
+    }
+    out->kind = GP_ASYM_DP;
+    out->n_parts = (int)nsg;
+}
+
+/* gateway_link (src/timing.py:104-113): argmin of (p_t, u, v) */
+static void gateway(const gp_instance *I, uint32_t fa, uint32_t fb, uint32_t *pu,
+                    uint32_t *pv)
+{
+    uint32_t D = I->n_devices;
+    int have = 0;
+    double bp = 0;
+    uint32_t bu = 0, bv = 0;
+    for (uint32_t x = I->fg_member_offset[fa]; x < I->fg_member_offset[fa + 1]; ++x) {
+        uint32_t u = I->fg_members[x];
+        for (uint32_t y = I->fg_member_offset[fb]; y < I->fg_member_offset[fb + 1]; ++y) {
+            uint32_t v = I->fg_members[y];
+            double p = I->p_t[(size_t)u * D + v];
+            int less;
+            if (!have)
+                less = 1;
+            else if (p != bp)
+                less = p < bp;
+            else if (I->id_rank[u] != I->id_rank[bu])
+                less = I->id_rank[u] < I->id_rank[bu];
+            else
+                less = I->id_rank[v] < I->id_rank[bv];
+            if (less) {
+                have = 1;
+                bp = p;
+                bu = u;
+                bv = v;
+            }
+        }
+    }
+    *pu = bu;
+    *pv = bv;
+}
+
+/*
+ * _evaluate (src/planner.py:313-327) for one candidate.
+ * Returns a status; *cost gets the plan cost (+inf if memory-infeasible).
+ */
+int or_evaluate(const gp_instance *I, uint32_t k, const uint8_t *order,
+                const uint8_t *counts, uint32_t bm, double *cost,
+                gp_plan_info *detail)
+{
+    uint32_t n = I->n_layers;
+    if (k < 1 || k > GP_MAX_STAGES || bm >= I->n_batch * I->n_micro)
+        return GP_ERR_INPUT;
+    int64_t B = I->batch[bm / I->n_micro];
+    int64_t m = I->micro[bm % I->n_micro];
+    /* ParallelPlan.__post_init__ (src/plans.py:106-122) */
+    uint32_t starts[GP_MAX_STAGES + 1];
+    uint32_t pos = 0;
+    for (uint32_t s = 0; s < k; ++s) {
+        if (order[s] >= I->n_fgs)
+            return GP_ERR_INPUT;
+        for (uint32_t t = 0; t < s; ++t)
+            if (order[t] == order[s])
+                return GP_ERR_INPUT;
+        if (counts[s] == 0)
+            return GP_ERR_INPUT;
+        starts[s] = pos;
+        pos += counts[s];
+    }
+    starts[k] = pos;
+    if (pos > n)   /* slicing past the model would shrink ranges: not a plan */
+        return GP_ERR_INPUT;
+
+    /* build_plan (src/planner.py:203-223) */
+    stage_split split[GP_MAX_STAGES];
+    static __thread double rf[GP_MAX_STAGES][OR_MAX_DEV], cf[GP_MAX_STAGES][OR_MAX_DEV];
+    for (uint32_t s = 0; s < k; ++s)
+        choose_split(I, order[s], starts[s], starts[s + 1], &split[s], rf[s], cf[s]);
+
+    /* assigned_param_bytes + memory_feasible (src/planner.py:226-253) */
+    static __thread double assigned[OR_MAX_DEV];
+    static __thread uint8_t touched[OR_MAX_DEV];
+    uint32_t D = I->n_devices;
+    memset(touched, 0, D);
+    for (uint32_t s = 0; s < k; ++s) {
+        uint32_t f = order[s];
+        double params = psum_range(I->param_bytes, starts[s], starts[s + 1]);
+        uint32_t m0 = I->fg_member_offset[f], m1 = I->fg_member_offset[f + 1];
+        if (split[s].kind == GP_ASYM_PP) {
+            uint32_t s0 = I->fg_sg_offset[f];
+            for (int j = 0; j < split[s].n_parts; ++j) {
+                double sub = psum_range(I->param_bytes, split[s].pp_start[j], split[s].pp_end[j]);
+                uint32_t g = s0 + (uint32_t)j;
+                for (uint32_t x = I->sg_member_offset[g]; x < I->sg_member_offset[g + 1]; ++x) {
+                    uint32_t d = I->sg_members[x];
+                    assigned[d] = (touched[d] ? assigned[d] : 0.0) + sub;
+                    touched[d] = 1;
+                }
+            }
+        } else if (split[s].kind == GP_ASYM_TP_DP) {
+            for (uint32_t x = m0; x < m1; ++x) {
+                uint32_t d = I->fg_members[x];
+                double v = (params * rf[s][x - m0]) * cf[s][x - m0];
+                assigned[d] = (touched[d] ? assigned[d] : 0.0) + v;
+                touched[d] = 1;
+            }
+        } else {
+            for (uint32_t x = m0; x < m1; ++x) {
+                uint32_t d = I->fg_members[x];
+                assigned[d] = (touched[d] ? assigned[d] : 0.0) + params;
+                touched[d] = 1;
+            }
+        }
+    }
+    int feasible = 1;
+    for (uint32_t d = 0; d < D; ++d)
+        if (touched[d] && assigned[d] > I->memory_bytes[d]) {
+            feasible = 0;
+            break;
+        }
+    if (detail) {
+        memset(detail, 0, sizeof(*detail));
+        detail->k = k;
+        detail->feasible = feasible;
+        for (uint32_t s = 0; s < k; ++s) {
+            detail->stage[s].kind = (uint32_t)split[s].kind;
+            if (split[s].kind == GP_ASYM_PP) {
+                detail->stage[s].n_parts = (uint32_t)split[s].n_parts;
+                for (int j = 0; j < split[s].n_parts; ++j) {
+                    detail->stage[s].pp_sg[j] = (uint32_t)j;
+                    detail->stage[s].pp_start[j] = split[s].pp_start[j];
+                    detail->stage[s].pp_end[j] = split[s].pp_end[j];
+                }
+            }
+        }
+    }
+    if (!feasible) {
+        *cost = INFINITY;
+        if (detail)
+            detail->plan_cost = INFINITY;
+        return GP_OK;
+    }
+
+    /* build_plan_timing (src/timing.py:176-231) */
+    if (pos != n)
+        return GP_ERR_TOPOLOGY;
+    double fwd_ps[GP_MAX_STAGES], bwd_ps[GP_MAX_STAGES], wgt_ps[GP_MAX_STAGES],
+        al[GP_MAX_STAGES];
+    for (uint32_t s = 0; s < k; ++s) {
+        uint32_t f = order[s], a = starts[s], b = starts[s + 1];
+        double cap;
+        /* effective_capacity (src/timing.py:116-143) */
+        if (split[s].kind == GP_ASYM_PP) {
+            double total = psum_total_flops(I, a, b);
+            int have = 0;
+            double best = 0.0;
+            uint32_t s0 = I->fg_sg_offset[f];
+            for (int j = 0; j < split[s].n_parts; ++j) {
+                double sub = psum_total_flops(I, split[s].pp_start[j], split[s].pp_end[j]);
+                double frac = sub / total;
+                double capj = I->sg_capacity[s0 + (uint32_t)j];
+                if (frac > 0) {
+                    double val = capj / frac;
+                    if (!have || val < best)
+                        best = val;
+                    have = 1;
+                }
+            }
+            if (!have)
+                return GP_ERR_DEGENERATE;
+            cap = best;
+        } else {
+            cap = I->fg_capacity[f];
+            if (!(cap > 0))
+                return GP_ERR_DEGENERATE;
+        }
+        /* collective_volume + intra_group_seconds (src/timing.py:146-173) */
+        uint32_t nmem = I->fg_member_offset[f + 1] - I->fg_member_offset[f];
+        double params = psum_range(I->param_bytes, a, b);
+        double volume = 0.0;
+        if (nmem >= 2) {
+            volume = 2.0 * params;
+            if (split[s].kind == GP_ASYM_TP_DP)
+                volume = volume + I->activation_out_bytes[b - 1] * (double)m;
+        }
+        if (volume == 0.0 || !I->fg_has_min_bw[f]) {
+            al[s] = 0.0;
+        } else {
+            if (!(I->fg_min_bw[f] > 0))
+                return GP_ERR_TOPOLOGY;
+            al[s] = volume / I->fg_min_bw[f];
+        }
+        /* sync = intra_group_seconds(params, fg): raises under the same rule */
+        if (params != 0.0 && I->fg_has_min_bw[f] && !(I->fg_min_bw[f] > 0))
+            return GP_ERR_TOPOLOGY;
+        fwd_ps[s] = psum_range(I->fwd_flops, a, b) / cap;
+        bwd_ps[s] = psum_range(I->bwd_input_flops, a, b) / cap;
+        wgt_ps[s] = psum_range(I->bwd_weight_flops, a, b) / cap;
+    }
+    double lat[GP_MAX_STAGES], bw[GP_MAX_STAGES], act[GP_MAX_STAGES];
+    for (uint32_t i = 0; i + 1 < k; ++i) {
+        uint32_t u, v;
+        gateway(I, order[i], order[i + 1], &u, &v);
+        double w = I->bandwidth[(size_t)u * D + v];
+        if (!(w > 0))
+            return GP_ERR_TOPOLOGY;
+        bw[i] = w;
+        lat[i] = I->latency[(size_t)u * D + v];
+        act[i] = I->activation_out_bytes[starts[i + 1] - 1];
+    }
+
+    /* plan_cost_from_timing / stage_cost (src/costmodel.py:56-89) */
+    double md = (double)m;
+    int64_t M = B / m;
+    double c[GP_MAX_STAGES], x[GP_MAX_STAGES];
+    for (uint32_t s = 0; s < k; ++s)
+        c[s] = ((fwd_ps[s] + bwd_ps[s]) + wgt_ps[s]) * md;
+    for (uint32_t i = 0; i + 1 < k; ++i)
+        x[i] = lat[i] + (act[i] * md) / bw[i];
+    double best = 0.0;
+    for (uint32_t s = 0; s < k; ++s) {
+        double fill = 0.0, res = 0.0;
+        for (uint32_t i = 0; i < s; ++i) {
+            fill += c[i] + x[i];
+            double r = x[i] - c[i + 1];
+            res += (r > 0.0) ? r : 0.0;
+        }
+        double run = (double)M * c[s];
+        double total = ((fill + run) + res) + al[s];
+        if (s == 0 || total > best)
+            best = total;
+        if (detail) {
+            detail->stage[s].fill_seconds = fill;
+            detail->stage[s].run_seconds = run;
+            detail->stage[s].residual_seconds = res;
+            detail->stage[s].collective_seconds = al[s];
+        }
+    }
+    *cost = best;
+    if (detail)
+        detail->plan_cost = best;
+    return GP_OK;
+}
+
+/* ------------------------------------------------------------------------
+ * exhaustive_plan (src/planner.py:374-403) over an index range
+ * ---------------------------------------------------------------------- */
+static uint64_t binom(uint64_t n, uint64_t r)
+{
+    if (r > n)
+        return 0;
+    uint64_t res = 1;
+    for (uint64_t i = 1; i <= r; ++i)
+        res = res * (n - r + i) / i;
+    return res;
+}
+
+static uint64_t fact(uint32_t k)
+{
+    uint64_t f = 1;
+    for (uint32_t i = 2; i <= k; ++i)
+        f *= i;
+    return f;
+}
+
+uint64_t or_space_size(const gp_instance *I)
+{
+    uint32_t k = I->n_fgs;
+    if (k > I->n_layers)
+        return 0;
+    return (uint64_t)I->n_batch * I->n_micro * fact(k) * binom(I->n_layers - 1, k - 1);
+}
+
+/* permutation of 0..k-1 with lexicographic rank r */
+static void unrank_perm(uint32_t k, uint64_t r, uint8_t *perm)
+{
+    uint8_t pool[GP_MAX_STAGES];
+    for (uint32_t i = 0; i < k; ++i)
+        pool[i] = (uint8_t)i;
+    uint32_t left = k;
+    for (uint32_t i = 0; i < k; ++i) {
+        uint64_t f = fact(k - 1 - i);
+        uint32_t q = (uint32_t)(r / f);
+        r %= f;
+        perm[i] = pool[q];
+        for (uint32_t j = q; j + 1 < left; ++j)
+            pool[j] = pool[j + 1];
+        --left;
+    }
+}
+
+/* composition of n into k positive parts with lexicographic rank r
+ * (_compositions, src/planner.py:406-413) */
+static void unrank_comp(uint32_t n, uint32_t k, uint64_t r, uint8_t *counts)
+{
+    uint32_t rem = n;
+    for (uint32_t i = 0; i + 1 < k; ++i) {
+        uint32_t parts = k - i;
+        for (uint32_t first = 1;; ++first) {
+            uint64_t cnt = binom(rem - first - 1, parts - 2);
+            if (r < cnt) {
+                counts[i] = (uint8_t)first;
+                rem -= first;
+                break;
+            }
+            r -= cnt;
+        }
+    }
+    counts[k - 1] = (uint8_t)rem;
+}
+
+void or_decode(const gp_instance *I, uint64_t idx, uint8_t *order, uint8_t *counts,
+               uint32_t *bm)
+{
+    uint32_t k = I->n_fgs;
+    uint64_t nc = binom(I->n_layers - 1, k - 1), np = fact(k);
+    uint64_t comp = idx % nc;
+    idx /= nc;
+    uint64_t perm = idx % np;
+    *bm = (uint32_t)(idx / np);
+    unrank_perm(k, perm, order);
+    unrank_comp(I->n_layers, k, comp, counts);
+}
+
+typedef struct {
+    const gp_instance *I;
+    uint64_t lo, hi;
+    int status;
+    int have;
+    double cost;
+    uint64_t idx;
+    uint8_t order[GP_MAX_STAGES], counts[GP_MAX_STAGES];
+} range_job;
+
+/* key (cost, (order, cuts)) strict-< then earliest index; fg index order is
+ * string order, so comparing indices compares the id strings. */
+static int key_less(double c1, const uint8_t *o1, const uint8_t *n1, uint64_t i1,
+                    double c2, const uint8_t *o2, const uint8_t *n2, uint64_t i2,
+                    uint32_t k)
+{
+    if (c1 != c2)
+        return c1 < c2;
+    for (uint32_t s = 0; s < k; ++s)
+        if (o1[s] != o2[s])
+            return o1[s] < o2[s];
+    for (uint32_t s = 0; s < k; ++s)
+        if (n1[s] != n2[s])
+            return n1[s] < n2[s];
+    return i1 < i2;
+}
+
+static void *range_worker(void *arg)
+{
+    range_job *J = (range_job *)arg;
+    const gp_instance *I = J->I;
+    uint32_t k = I->n_fgs;
+    J->have = 0;
+    J->status = GP_OK;
+    for (uint64_t idx = J->lo; idx < J->hi; ++idx) {
+        uint8_t order[GP_MAX_STAGES], counts[GP_MAX_STAGES];
+        uint32_t bm;
+        or_decode(I, idx, order, counts, &bm);
+        double cost;
+        int st = or_evaluate(I, k, order, counts, bm, &cost, NULL);
+        if (st != GP_OK) {
+            J->status = st;
+            return NULL;
+        }
+        if (!J->have || key_less(cost, order, counts, idx, J->cost, J->order, J->counts,
+                                 J->idx, k)) {
+            J->have = 1;
+            J->cost = cost;
+            J->idx = idx;
+            memcpy(J->order, order, k);
+            memcpy(J->counts, counts, k);
+        }
+    }
+    return NULL;
+}
+
+/* Argmin over [lo, hi) on `threads` host threads. */
+int or_argmin_range(const gp_instance *I, uint64_t lo, uint64_t hi, int threads,
+                    gp_best *out)
+{
+    uint32_t k = I->n_fgs;
+    if (k < 1 || k > GP_MAX_STAGES || k > I->n_layers)
+        return GP_ERR_INFEASIBLE_SPLIT;
+    if (threads < 1)
+        threads = 1;
+    if (threads > 256)
+        threads = 256;
+    range_job jobs[256];
+    pthread_t tid[256];
+    uint64_t span = hi > lo ? hi - lo : 0;
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].I = I;
+        jobs[t].lo = lo + span * (uint64_t)t / (uint64_t)threads;
+        jobs[t].hi = lo + span * (uint64_t)(t + 1) / (uint64_t)threads;
+        if (threads == 1)
+            range_worker(&jobs[0]);
+        else
+            pthread_create(&tid[t], NULL, range_worker, &jobs[t]);
+    }
+    if (threads > 1)
+        for (int t = 0; t < threads; ++t)
+            pthread_join(tid[t], NULL);
+    memset(out, 0, sizeof(*out));
+    out->k = k;
+    out->evaluated = span;
+    int have = 0;
+    for (int t = 0; t < threads; ++t) {
+        if (jobs[t].status != GP_OK)
+            return jobs[t].status;
+        if (!jobs[t].have)
+            continue;
+        if (!have || key_less(jobs[t].cost, jobs[t].order, jobs[t].counts, jobs[t].idx,
+                              out->cost, out->order, out->counts, out->index, k)) {
+            have = 1;
+            out->cost = jobs[t].cost;
+            out->index = jobs[t].idx;
+            memcpy(out->order, jobs[t].order, k);
+            memcpy(out->counts, jobs[t].counts, k);
+        }
+    }
+    if (!have)
+        return GP_ERR_NO_FEASIBLE;
+    uint64_t per_bm = fact(k) * binom(I->n_layers - 1, k - 1);
+    uint32_t bm = (uint32_t)(out->index / per_bm);
+    out->batch_index = bm / I->n_micro;
+    out->micro_index = bm % I->n_micro;
+    return GP_OK;
+}
+
+/* Batch of explicit candidates (same layout as gp_eval_batch), threaded. */
+typedef struct {
+    const gp_instance *I;
+    uint32_t k;
+    uint64_t lo, hi;
+    const uint8_t *order, *counts, *bm;
+    double *cost;
+    uint8_t *status;
+} batch_job;
+
+static void *batch_worker(void *arg)
+{
+    batch_job *J = (batch_job *)arg;
+    for (uint64_t i = J->lo; i < J->hi; ++i) {
+        double c = NAN;
+        int st = or_evaluate(J->I, J->k, J->order + i * J->k, J->counts + i * J->k,
+                             J->bm[i], &c, NULL);
+        J->cost[i] = st == GP_OK ? c : NAN;
+        J->status[i] = (uint8_t)st;
+    }
+    return NULL;
+}
+
+int or_eval_batch(const gp_instance *I, uint32_t k, uint64_t n, const uint8_t *order,
+                  const uint8_t *counts, const uint8_t *bm, double *cost,
+                  uint8_t *status, int threads)
+{
+    if (threads < 1)
+        threads = 1;
+    if (threads > 256)
+        threads = 256;
+    batch_job jobs[256];
+    pthread_t tid[256];
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = (batch_job){I, k, n * (uint64_t)t / (uint64_t)threads,
+                              n * (uint64_t)(t + 1) / (uint64_t)threads,
+                              order, counts, bm, cost, status};
+        if (threads == 1)
+            batch_worker(&jobs[0]);
+        else
+            pthread_create(&tid[t], NULL, batch_worker, &jobs[t]);
+    }
+    if (threads > 1)
+        for (int t = 0; t < threads; ++t)
+            pthread_join(tid[t], NULL);
+    return GP_OK;
+}
+
+/* Per-group constants of the TP/DP splits (they depend on the group only):
+ * split_asymmetric_tp_dp on device p_c in member order and
+ * split_asymmetric_dp on second-level capacities (src/planner.py:188-200). */
+int or_group_detail(const gp_instance *I, uint32_t f, gp_group_info *out)
+{
+    if (f >= I->n_fgs)
+        return GP_ERR_INPUT;
+    memset(out, 0, sizeof(*out));
+    uint32_t m0 = I->fg_member_offset[f], m1 = I->fg_member_offset[f + 1];
+    uint32_t s0 = I->fg_sg_offset[f], s1 = I->fg_sg_offset[f + 1];
+    out->n_members = m1 - m0;
+    out->n_sgs = s1 - s0;
+    double dcaps[OR_MAX_DEV];
+    for (uint32_t j = 0; j < out->n_members; ++j)
+        dcaps[j] = I->p_c[I->fg_members[m0 + j]];
+    out->tp_ok = or_tp_grid(dcaps, (int)out->n_members, out->tp_row, out->tp_col);
+    if (out->n_sgs >= 1)
+        or_dp_fractions(I->sg_capacity + s0, (int)out->n_sgs, out->dp_fraction);
+    return GP_OK;
+}
+
+/* sizeof of the ABI structs, for the ctypes layout test */
+size_t or_abi_sizeof(int which)
+{
+    switch (which) {
+    case 0: return sizeof(gp_instance);
+    case 1: return sizeof(gp_best);
+    case 2: return sizeof(gp_plan_info);
+    case 3: return sizeof(gp_group_info);
+    case 4: return sizeof(gp_stage_info);
+    default: return 0;
+    }
+}

@@ -1,0 +1,142 @@
+"""ctypes binding of ``oracle/liboracle.so`` - TEST INFRASTRUCTURE ONLY.
+
+The oracle is the CPU restatement of the reference planner path (see
+``oracle/oracle.c``).  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+CPU-baseline legs of ``bench.py`` may import this module: it is the checker
+and the timed CPU baseline, never part of the product path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2505_15536_b200 import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "liboracle.so")
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            build()
+        L = C.CDLL(LIB)
+        P = C.POINTER
+        L.or_psum.restype = C.c_double
+        L.or_psum.argtypes = [P(C.c_double), C.c_size_t]
+        L.or_proportional_split.argtypes = [C.c_int64, P(C.c_double), C.c_int, C.c_int,
+                                            P(C.c_int64)]
+        L.or_tp_grid.argtypes = [P(C.c_double), C.c_int, P(C.c_double), P(C.c_double)]
+        L.or_dp_fractions.argtypes = [P(C.c_double), C.c_int, P(C.c_double)]
+        L.or_evaluate.argtypes = [P(abi.GpInstance), C.c_uint32, P(C.c_uint8),
+                                  P(C.c_uint8), C.c_uint32, P(C.c_double),
+                                  P(abi.GpPlanInfo)]
+        L.or_space_size.restype = C.c_uint64
+        L.or_space_size.argtypes = [P(abi.GpInstance)]
+        L.or_decode.argtypes = [P(abi.GpInstance), C.c_uint64, P(C.c_uint8),
+                                P(C.c_uint8), P(C.c_uint32)]
+        L.or_argmin_range.argtypes = [P(abi.GpInstance), C.c_uint64, C.c_uint64,
+                                      C.c_int, P(abi.GpBest)]
+        L.or_eval_batch.argtypes = [P(abi.GpInstance), C.c_uint32, C.c_uint64,
+                                    P(C.c_uint8), P(C.c_uint8), P(C.c_uint8),
+                                    P(C.c_double), P(C.c_uint8), C.c_int]
+        L.or_group_detail.argtypes = [P(abi.GpInstance), C.c_uint32, P(abi.GpGroupInfo)]
+        _lib = L
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _u8(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def psum(xs) -> float:
+    a = np.ascontiguousarray(xs, dtype=np.float64)
+    return lib().or_psum(_dp(a), a.size)
+
+
+def proportional_split(total, weights, minimum=0):
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    out = np.zeros(len(w), dtype=np.int64)
+    st = lib().or_proportional_split(int(total), _dp(w), len(w), int(minimum),
+                                     out.ctypes.data_as(C.POINTER(C.c_int64)))
+    abi.raise_for(st, "cannot honor the minimum share")
+    return [int(x) for x in out]
+
+
+def tp_grid(caps):
+    c = np.ascontiguousarray(caps, dtype=np.float64)
+    rf = np.zeros(len(c)); cf = np.zeros(len(c))
+    ok = lib().or_tp_grid(_dp(c), len(c), _dp(rf), _dp(cf))
+    return [(float(a), float(b)) for a, b in zip(rf, cf)] if ok else None
+
+
+def dp_fractions(caps):
+    c = np.ascontiguousarray(caps, dtype=np.float64)
+    fr = np.zeros(len(c))
+    lib().or_dp_fractions(_dp(c), len(c), _dp(fr))
+    return [float(x) for x in fr]
+
+
+def evaluate(packed, order, counts, bm, detail=False):
+    """(status, cost[, GpPlanInfo]) for one encoded candidate."""
+    o = np.ascontiguousarray(order, dtype=np.uint8)
+    n = np.ascontiguousarray(counts, dtype=np.uint8)
+    cost = C.c_double(0.0)
+    info = abi.GpPlanInfo() if detail else None
+    st = lib().or_evaluate(C.byref(packed.struct), len(o), _u8(o), _u8(n), int(bm),
+                           C.byref(cost), C.byref(info) if detail else None)
+    return (st, cost.value, info) if detail else (st, cost.value)
+
+
+def eval_batch(packed, order, counts, bm, threads=1):
+    order = np.ascontiguousarray(order, dtype=np.uint8)
+    counts = np.ascontiguousarray(counts, dtype=np.uint8)
+    bm = np.ascontiguousarray(bm, dtype=np.uint8)
+    n, k = order.shape
+    cost = np.empty(n, dtype=np.float64)
+    status = np.empty(n, dtype=np.uint8)
+    lib().or_eval_batch(C.byref(packed.struct), k, n, _u8(order), _u8(counts),
+                        _u8(bm), _dp(cost), _u8(status), int(threads))
+    return cost, status
+
+
+def space_size(packed) -> int:
+    return int(lib().or_space_size(C.byref(packed.struct)))
+
+
+def decode(packed, idx):
+    k = packed.n_fgs
+    o = np.zeros(k, dtype=np.uint8); c = np.zeros(k, dtype=np.uint8)
+    bm = C.c_uint32(0)
+    lib().or_decode(C.byref(packed.struct), int(idx), _u8(o), _u8(c), C.byref(bm))
+    return o, c, bm.value
+
+
+def argmin_range(packed, lo, hi, threads=1):
+    best = abi.GpBest()
+    st = lib().or_argmin_range(C.byref(packed.struct), int(lo), int(hi),
+                               int(threads), C.byref(best))
+    return st, best
+
+
+def group_detail(packed, f):
+    g = abi.GpGroupInfo()
+    lib().or_group_detail(C.byref(packed.struct), int(f), C.byref(g))
+    return g

@@ -1,0 +1,114 @@
+"""ctypes mirror of ``include/geopipe_b200.h`` (structs, status codes).
+
+Kept in one place so the product binding (:mod:`.engine`) and the test-only
+oracle binding (``oracle/oracle.py``) agree on the layout byte for byte.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from . import domain as D
+
+GP_OK = 0
+GP_ERR_INPUT = 1
+GP_ERR_INFEASIBLE_SPLIT = 2
+GP_ERR_NO_FEASIBLE = 3
+GP_ERR_DEGENERATE = 4
+GP_ERR_TOPOLOGY = 5
+GP_ERR_CUDA = 6
+GP_ERR_TIMING = 7
+GP_ERR_SCHEDULING = 8
+
+GP_UNIFORM, GP_ASYM_PP, GP_ASYM_DP, GP_ASYM_TP_DP = 0, 1, 2, 3
+KIND_OF = {
+    GP_UNIFORM: D.SplitKind.UNIFORM,
+    GP_ASYM_PP: D.SplitKind.ASYMMETRIC_PP,
+    GP_ASYM_DP: D.SplitKind.ASYMMETRIC_DP,
+    GP_ASYM_TP_DP: D.SplitKind.ASYMMETRIC_TP_DP,
+}
+
+GP_MAX_STAGES = 16
+GP_MAX_SGS = 16
+GP_MAX_LAYERS = 255
+GP_MAX_MEMBERS = 1024
+
+_ERRORS = {
+    GP_ERR_INPUT: D.InputFileError,
+    GP_ERR_INFEASIBLE_SPLIT: D.InfeasibleSplitError,
+    GP_ERR_NO_FEASIBLE: D.NoFeasiblePlanError,
+    GP_ERR_DEGENERATE: D.DegenerateGroupError,
+    GP_ERR_TOPOLOGY: D.InvalidTopologyError,
+    GP_ERR_CUDA: D.DeviceError,
+    GP_ERR_TIMING: D.InvalidTimingError,
+    GP_ERR_SCHEDULING: D.SchedulingBugError,
+}
+
+
+def raise_for(status: int, message: str = "") -> None:
+    if status == GP_OK:
+        return
+    cls = _ERRORS.get(status, D.GeopipeError)
+    raise cls(message or f"status {status}")
+
+
+_dp = C.POINTER(C.c_double)
+_u32p = C.POINTER(C.c_uint32)
+_u8p = C.POINTER(C.c_uint8)
+_i64p = C.POINTER(C.c_int64)
+
+
+class GpInstance(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_uint32),
+        ("fwd_flops", _dp), ("bwd_input_flops", _dp), ("bwd_weight_flops", _dp),
+        ("activation_out_bytes", _dp), ("param_bytes", _dp),
+        ("n_batch", C.c_uint32), ("batch", _i64p),
+        ("n_micro", C.c_uint32), ("micro", _i64p),
+        ("n_devices", C.c_uint32),
+        ("p_c", _dp), ("memory_bytes", _dp), ("id_rank", _u32p),
+        ("p_t", _dp), ("latency", _dp), ("bandwidth", _dp),
+        ("n_fgs", C.c_uint32),
+        ("fg_member_offset", _u32p), ("fg_members", _u32p),
+        ("fg_capacity", _dp), ("fg_min_bw", _dp), ("fg_has_min_bw", _u8p),
+        ("fg_sg_offset", _u32p), ("sg_member_offset", _u32p),
+        ("sg_members", _u32p), ("sg_capacity", _dp),
+        ("bottleneck_factor", C.c_double),
+    ]
+
+
+class GpBest(C.Structure):
+    _fields_ = [
+        ("cost", C.c_double), ("index", C.c_uint64),
+        ("batch_index", C.c_uint32), ("micro_index", C.c_uint32),
+        ("k", C.c_uint32),
+        ("order", C.c_uint8 * GP_MAX_STAGES), ("counts", C.c_uint8 * GP_MAX_STAGES),
+        ("evaluated", C.c_uint64),
+    ]
+
+
+class GpStageInfo(C.Structure):
+    _fields_ = [
+        ("kind", C.c_uint32), ("n_parts", C.c_uint32),
+        ("pp_sg", C.c_uint32 * GP_MAX_SGS),
+        ("pp_start", C.c_uint32 * GP_MAX_SGS),
+        ("pp_end", C.c_uint32 * GP_MAX_SGS),
+        ("fill_seconds", C.c_double), ("run_seconds", C.c_double),
+        ("residual_seconds", C.c_double), ("collective_seconds", C.c_double),
+    ]
+
+
+class GpPlanInfo(C.Structure):
+    _fields_ = [
+        ("feasible", C.c_int32), ("k", C.c_uint32), ("plan_cost", C.c_double),
+        ("stage", GpStageInfo * GP_MAX_STAGES),
+    ]
+
+
+class GpGroupInfo(C.Structure):
+    _fields_ = [
+        ("tp_ok", C.c_int32), ("n_members", C.c_uint32), ("n_sgs", C.c_uint32),
+        ("tp_row", C.c_double * GP_MAX_MEMBERS),
+        ("tp_col", C.c_double * GP_MAX_MEMBERS),
+        ("dp_fraction", C.c_double * GP_MAX_SGS),
+    ]

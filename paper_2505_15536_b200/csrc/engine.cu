@@ -1,0 +1,1265 @@
+// engine.cu - B200 (sm_100a) plan-evaluation engine behind the C-ABI of
+// include/geopipe_b200.h.
+//
+// Data path:
+//   gp_ctx_load    H2D of the packed instance, then K1:
+//                    k1_intervals  Neumaier interval sums S[col][a][b]
+//                    k1_groups     per-group TP tiles, DP fractions, memory minima
+//                    k1_stages     per (group, a, b): split choice, memory
+//                                  feasibility, capacity, C1 = (F+Bi)+W, and per m
+//                                  the table {C1*m | +inf, AL}
+//                    k1_boundary   gateway pair per ordered group pair and
+//                                  x = lat + (act*m)/bw per boundary layer
+//   gp_eval_batch  K2: one thread per explicit candidate
+//   gp_argmin_range K3: one CTA per (b,m, order, comp-chunk); the varying last
+//                  cut sweeps a shared-memory triangle of the stage table;
+//                  warp-shuffle + CTA + last-block argmin on the reference key
+//
+// Every floating-point operation mirrors the reference operation order
+// (src/costmodel.py:56-89, src/timing.py:116-231, src/planner.py:157-253);
+// the file is compiled with -fmad=false.  There is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../include/geopipe_b200.h"
+#include "device_math.cuh"
+
+using gpd::NeumaierSum;
+
+// ----------------------------------------------------------------------------
+// error plumbing
+// ----------------------------------------------------------------------------
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                        \
+    do {                                                                      \
+        cudaError_t e_ = (expr);                                              \
+        if (e_ != cudaSuccess)                                                \
+            return fail(GP_ERR_CUDA, "%s: %s (%s:%d)", #expr,                 \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);          \
+    } while (0)
+
+// stage-table codes (per group, layer range)
+enum : uint8_t { SC_OK = 0, SC_INFEASIBLE = 1, SC_DEGENERATE = 4, SC_TOPOLOGY = 5 };
+// context flags that force the generic (status-tracking) range kernel
+enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 4 };
+
+// ----------------------------------------------------------------------------
+// device-side view of one loaded instance
+// ----------------------------------------------------------------------------
+struct DevInst {
+    int n;          // layers
+    int F;          // first-level groups
+    int D;          // devices
+    int nb, nm;     // |B|, |M|
+    const double *fwd, *bwd_in, *bwd_w, *act, *param;
+    const long long *batch, *micro;
+    const double *p_c, *mem, *p_t, *lat, *bw;
+    const uint32_t* id_rank;
+    const uint32_t *fg_off, *fg_mem, *fg_sg_off, *sg_off, *sg_mem;
+    const double *fg_cap, *sg_cap;
+    const double* fg_minbw;      // current min_intra_bandwidth
+    const uint8_t* fg_has_minbw;
+    double bf;                   // bottleneck_factor
+    // K1 outputs
+    double* S;                   // [5][(n+1)^2]: fwd, bwd_in, bwd_w, param, total_flops
+    uint8_t* g_tp_ok;            // [F]
+    double *g_rf, *g_cf;         // [fg member slots]
+    double* g_dp;                // [sg slots]
+    double* g_minmem;            // [F]
+    double* sg_minmem;           // [n_sgs]
+    double2* stg;                // [nm][F][(n+1)^2] {C1*m or +inf, AL}
+    uint8_t* scode;              // [F][(n+1)^2]
+    uint8_t* skind;              // [F][(n+1)^2]
+    double* C1;                  // [F][(n+1)^2] per-sample (F+Bi)+W (detail)
+    int* gw;                     // [F*F] gateway u*D+v
+    double* xt;                  // [nm][F][F][n]
+    uint32_t* flags;             // [1]
+};
+
+__device__ __forceinline__ int tri_idx(int n, int a, int b) { return a * (n + 1) + b; }
+
+enum { COL_FWD = 0, COL_BWD = 1, COL_WGT = 2, COL_PARAM = 3, COL_TF = 4 };
+
+__device__ __forceinline__ double Ssum(const DevInst& I, int col, int a, int b) {
+    size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
+    return I.S[col * N2 + tri_idx(I.n, a, b)];
+}
+
+// ---- K1a: interval sums -----------------------------------------------------
+// sum(model.layers[i].<field> for i in range(a, b)) for every 0 <= a < b <= n,
+// each interval summed from its own start (never prefix differences).
+__global__ void k1_intervals(DevInst I) {
+    int a = blockIdx.x * blockDim.x + threadIdx.x;
+    int col = blockIdx.y;
+    if (a >= I.n) return;
+    size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
+    double* out = I.S + col * N2;
+    NeumaierSum s;
+    for (int b = a + 1; b <= I.n; ++b) {
+        int i = b - 1;
+        double x;
+        switch (col) {
+            case COL_FWD: x = I.fwd[i]; break;
+            case COL_BWD: x = I.bwd_in[i]; break;
+            case COL_WGT: x = I.bwd_w[i]; break;
+            case COL_PARAM: x = I.param[i]; break;
+            default: x = (I.fwd[i] + I.bwd_in[i]) + I.bwd_w[i]; break;  // total_flops
+        }
+        if (b == a + 1) s.start(x); else s.add(x);
+        out[tri_idx(I.n, a, b)] = s.value();
+    }
+}
+
+// ---- K1b: per-group constants ---------------------------------------------------
+__global__ void k1_groups(DevInst I) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= I.F) return;
+    int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    int nmem = m1 - m0;
+    double caps[GP_MAX_MEMBERS];
+    double mn = 0.0;
+    for (int j = 0; j < nmem; ++j) {
+        int d = I.fg_mem[m0 + j];
+        caps[j] = I.p_c[d];
+        double mm = I.mem[d];
+        mn = (j == 0 || mm < mn) ? mm : mn;
+    }
+    I.g_minmem[f] = mn;
+    I.g_tp_ok[f] = gpd::tp_grid(caps, nmem, I.g_rf + m0, I.g_cf + m0) ? 1 : 0;
+    int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
+    if (s1 > s0) gpd::dp_fractions(I.sg_cap + s0, s1 - s0, I.g_dp + s0);
+    for (int g = s0; g < s1; ++g) {
+        double sm = 0.0;
+        for (int x = I.sg_off[g]; x < I.sg_off[g + 1]; ++x) {
+            double mm = I.mem[I.sg_mem[x]];
+            sm = (x == (int)I.sg_off[g] || mm < sm) ? mm : sm;
+        }
+        I.sg_minmem[g] = sm;
+    }
+}
+
+// recompute min_intra_bandwidth over member pairs (bandwidth snapshots;
+// src/grouping.py:69-75 on the rebuilt topology)
+__global__ void k1_minbw(DevInst I, double* out) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= I.F) return;
+    int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    double mn = 0.0;
+    bool have = false;
+    for (int x = m0; x < m1; ++x)
+        for (int y = x + 1; y < m1; ++y) {
+            double w = I.bw[(size_t)I.fg_mem[x] * I.D + I.fg_mem[y]];
+            if (!have || w < mn) mn = w;
+            have = true;
+        }
+    out[f] = have ? mn : 0.0;
+}
+
+// split choice for one (group, layer range): choose_intra_split
+// (src/planner.py:157-200).  Writes PP shares when kind == ASYM_PP.
+__device__ int choose_split(const DevInst& I, int f, int a, int b, int* shares, int* nparts) {
+    int nmem = I.fg_off[f + 1] - I.fg_off[f];
+    int s0 = I.fg_sg_off[f], nsg = I.fg_sg_off[f + 1] - s0;
+    *nparts = 0;
+    if (nmem == 1 || nsg == 1) return GP_UNIFORM;
+    const double* caps = I.sg_cap + s0;
+    int nl = b - a;
+    if (nsg <= nl && gpd::proportional_split(nl, caps, nsg, 1, shares)) {
+        double times[GP_MAX_SGS];
+        int pos = a;
+        for (int j = 0; j < nsg; ++j) {
+            times[j] = Ssum(I, COL_TF, pos, pos + shares[j]) / caps[j];
+            pos += shares[j];
+        }
+        double mean = gpd::psum(times, nsg) / (double)nsg;
+        double mx = times[0];
+        for (int j = 1; j < nsg; ++j) mx = times[j] > mx ? times[j] : mx;
+        if (mx <= I.bf * mean) { *nparts = nsg; return GP_ASYM_PP; }
+    }
+    if (I.g_tp_ok[f]) { *nparts = nmem; return GP_ASYM_TP_DP; }
+    *nparts = nsg;
+    return GP_ASYM_DP;
+}
+
+// ---- K1c: stage table -------------------------------------------------------------
+// One thread per (group, a, b).  memory_feasible is local to a stage because
+// every group appears in exactly one stage (src/planner.py:226-253).
+__global__ void k1_stages(DevInst I) {
+    int n = I.n;
+    int N1 = n + 1;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long total = (long long)I.F * N1 * N1;
+    if (t >= total) return;
+    int f = (int)(t / (N1 * N1));
+    int rem = (int)(t % (N1 * N1));
+    int a = rem / N1, b = rem % N1;
+    size_t N2 = (size_t)N1 * N1;
+    size_t e = (size_t)f * N2 + rem;
+    if (a >= b) {
+        I.scode[e] = SC_INFEASIBLE;
+        I.skind[e] = 0;
+        I.C1[e] = INFINITY;
+        for (int mi = 0; mi < I.nm; ++mi)
+            I.stg[(size_t)mi * I.F * N2 + e] = make_double2(INFINITY, 0.0);
+        return;
+    }
+    int shares[GP_MAX_SGS], np;
+    int kind = choose_split(I, f, a, b, shares, &np);
+    I.skind[e] = (uint8_t)kind;
+    double P = Ssum(I, COL_PARAM, a, b);
+    int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    int s0 = I.fg_sg_off[f];
+    // memory feasibility: bytes_needed > memory_bytes -> infeasible
+    bool feas = true;
+    if (kind == GP_ASYM_PP) {
+        int pos = a;
+        for (int j = 0; j < np && feas; ++j) {
+            double sub = Ssum(I, COL_PARAM, pos, pos + shares[j]);
+            if (I.sg_off[s0 + j + 1] > I.sg_off[s0 + j]) feas = !(sub > I.sg_minmem[s0 + j]);
+            pos += shares[j];
+        }
+    } else if (kind == GP_ASYM_TP_DP) {
+        for (int x = m0; x < m1 && feas; ++x)
+            feas = !(((P * I.g_rf[x]) * I.g_cf[x]) > I.mem[I.fg_mem[x]]);
+    } else {
+        feas = !(P > I.g_minmem[f]);
+    }
+    // effective_capacity (src/timing.py:116-143)
+    uint8_t code = SC_OK;
+    double cap;
+    if (kind == GP_ASYM_PP) {
+        double tot = Ssum(I, COL_TF, a, b);
+        bool have = false;
+        double best = 0.0;
+        int pos = a;
+        for (int j = 0; j < np; ++j) {
+            double sub = Ssum(I, COL_TF, pos, pos + shares[j]);
+            pos += shares[j];
+            double frac = sub / tot;
+            if (frac > 0) {
+                double val = I.sg_cap[s0 + j] / frac;
+                if (!have || val < best) best = val;
+                have = true;
+            }
+        }
+        cap = best;
+        if (!have) code = SC_DEGENERATE;
+    } else {
+        cap = I.fg_cap[f];
+        if (!(cap > 0)) code = SC_DEGENERATE;
+    }
+    // per-sample times (src/timing.py:198-200) and C1 (src/costmodel.py:59)
+    double Fp = Ssum(I, COL_FWD, a, b) / cap;
+    double Bp = Ssum(I, COL_BWD, a, b) / cap;
+    double Wp = Ssum(I, COL_WGT, a, b) / cap;
+    double c1 = (Fp + Bp) + Wp;
+    I.C1[e] = c1;
+    // collective + sync rule (src/timing.py:146-173)
+    int nmem = m1 - m0;
+    bool has = I.fg_has_minbw[f] != 0;
+    double mbw = I.fg_minbw[f];
+    if (code == SC_OK && has && !(mbw > 0) && (nmem >= 2 || P != 0.0)) code = SC_TOPOLOGY;
+    bool overflow = false;
+    for (int mi = 0; mi < I.nm; ++mi) {
+        double md = (double)I.micro[mi];
+        double al = 0.0;
+        if (nmem >= 2) {
+            double V = 2.0 * P;
+            if (kind == GP_ASYM_TP_DP) V = V + I.act[b - 1] * md;
+            if (V != 0.0 && has && mbw > 0) al = V / mbw;
+        }
+        double cm = c1 * md;
+        if (feas && isinf(cm)) overflow = true;
+        I.stg[(size_t)mi * I.F * N2 + e] = make_double2(feas ? cm : INFINITY, al);
+    }
+    I.scode[e] = feas ? code : SC_INFEASIBLE;
+    if (feas && code != SC_OK) atomicOr(I.flags, FLAG_STAGE_ERROR);
+    if (overflow) atomicOr(I.flags, FLAG_OVERFLOW);
+}
+
+// ---- K1d: gateways and boundary transfer table -------------------------------------
+// gateway_link (src/timing.py:104-113): argmin over (p_t, u, v) with string
+// order of ids, u in the upstream group, v in the downstream group.
+__global__ void k1_gateways(DevInst I) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= I.F * I.F) return;
+    int fa = t / I.F, fb = t % I.F;
+    bool have = false;
+    double bp = 0.0;
+    int bu = 0, bv = 0;
+    for (int x = I.fg_off[fa]; x < (int)I.fg_off[fa + 1]; ++x) {
+        int u = I.fg_mem[x];
+        for (int y = I.fg_off[fb]; y < (int)I.fg_off[fb + 1]; ++y) {
+            int v = I.fg_mem[y];
+            double p = I.p_t[(size_t)u * I.D + v];
+            bool less;
+            if (!have) less = true;
+            else if (p != bp) less = p < bp;
+            else if (I.id_rank[u] != I.id_rank[bu]) less = I.id_rank[u] < I.id_rank[bu];
+            else less = I.id_rank[v] < I.id_rank[bv];
+            if (less) { have = true; bp = p; bu = u; bv = v; }
+        }
+    }
+    I.gw[t] = bu * I.D + bv;
+    if (fa != fb && !(I.bw[(size_t)bu * I.D + bv] > 0)) atomicOr(I.flags, FLAG_GATEWAY_ERROR);
+}
+
+__global__ void k1_boundary(DevInst I) {
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long total = (long long)I.nm * I.F * I.F * I.n;
+    if (t >= total) return;
+    int j = (int)(t % I.n);
+    long long r = t / I.n;
+    int pair = (int)(r % (I.F * I.F));
+    int mi = (int)(r / (I.F * I.F));
+    int g = I.gw[pair];
+    double md = (double)I.micro[mi];
+    // transfer_seconds: latency + (act*m)/bandwidth (src/timing.py:91-97)
+    I.xt[t] = I.lat[g] + (I.act[j] * md) / I.bw[g];
+}
+
+// ----------------------------------------------------------------------------
+// generic evaluation of one candidate from the tables (status-tracking path)
+// ----------------------------------------------------------------------------
+struct EvalOut {
+    double cost;
+    int status;
+};
+
+// p[0..k] are cut positions (p[0] = 0); order[s] group of stage s.
+__device__ EvalOut eval_tables(const DevInst& I, int k, const uint8_t* order, const int* p,
+                               int mi, long long M) {
+    int n = I.n;
+    size_t N2 = (size_t)(n + 1) * (n + 1);
+    EvalOut out{0.0, GP_OK};
+    bool feas = true;
+    for (int s = 0; s < k; ++s)
+        if (I.scode[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])] == SC_INFEASIBLE)
+            feas = false;
+    if (!feas) { out.cost = INFINITY; return out; }
+    if (p[k] != n) { out.status = GP_ERR_TOPOLOGY; return out; }  // src/timing.py:183-186
+    for (int s = 0; s < k; ++s) {
+        uint8_t c = I.scode[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])];
+        if (c != SC_OK) { out.status = c; return out; }
+    }
+    for (int s = 0; s + 1 < k; ++s) {
+        int g = I.gw[order[s] * I.F + order[s + 1]];
+        if (!(I.bw[g] > 0)) { out.status = GP_ERR_TOPOLOGY; return out; }
+    }
+    const double2* T = I.stg + (size_t)mi * I.F * N2;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * n;
+    double Md = (double)M;
+    double fill = 0.0, res = 0.0, best = 0.0, xprev = 0.0;
+    for (int s = 0; s < k; ++s) {
+        double2 e = T[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])];
+        double c = e.x;
+        if (s > 0) res = res + gpd::max0(xprev - c);
+        double total = ((fill + Md * c) + res) + e.y;
+        best = (s == 0 || total > best) ? total : best;
+        if (s + 1 < k) {
+            double x = X[((size_t)order[s] * I.F + order[s + 1]) * n + (p[s + 1] - 1)];
+            fill = fill + (c + x);
+            xprev = x;
+        }
+    }
+    out.cost = best;
+    return out;
+}
+
+// ---- K2: explicit batch, one thread per candidate -------------------------------
+__global__ void k2_eval_batch(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
+                              const uint8_t* __restrict__ counts, const uint8_t* __restrict__ bm,
+                              double* __restrict__ cost, uint8_t* __restrict__ status) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncand) return;
+    uint8_t o[GP_MAX_STAGES];
+    int p[GP_MAX_STAGES + 1];
+    p[0] = 0;
+    int st = GP_OK;
+    unsigned seen = 0;
+    for (int s = 0; s < k; ++s) {
+        o[s] = order[i * k + s];
+        int c = counts[i * k + s];
+        if (o[s] >= I.F || (seen >> o[s]) & 1u || c == 0) st = GP_ERR_INPUT;
+        seen |= 1u << (o[s] & 31);
+        p[s + 1] = p[s] + c;
+    }
+    int b = bm[i];
+    if (b >= I.nb * I.nm || p[k] > I.n) st = GP_ERR_INPUT;
+    if (st != GP_OK) { cost[i] = NAN; status[i] = (uint8_t)st; return; }
+    int mi = b % I.nm;
+    long long M = I.batch[b / I.nm] / I.micro[mi];
+    EvalOut r = eval_tables(I, k, o, p, mi, M);
+    cost[i] = r.status == GP_OK ? r.cost : NAN;
+    status[i] = (uint8_t)r.status;
+}
+
+// ----------------------------------------------------------------------------
+// K3: exhaustive argmin over an enumeration-index range
+// ----------------------------------------------------------------------------
+struct RangeGeom {
+    int k;
+    int nbm;                 // |B| * |M|
+    unsigned long long NC;   // C(n-1, k-1)
+    unsigned long long NP;   // k!
+    unsigned long long lo, hi;
+    unsigned long long item0;          // first (bm, perm) item touched
+    unsigned long long chunks_per_item;
+    unsigned long long chunk;          // comps per CTA
+};
+
+__device__ unsigned long long d_binom(int n, int r) {
+    if (r < 0 || r > n) return 0ull;
+    unsigned long long res = 1;
+    for (int i = 1; i <= r; ++i) res = res * (unsigned long long)(n - r + i) / (unsigned long long)i;
+    return res;
+}
+
+__device__ void d_unrank_perm(int k, unsigned long long r, uint8_t* perm) {
+    uint8_t pool[GP_MAX_STAGES];
+    unsigned long long f = 1;
+    for (int i = 0; i < k; ++i) { pool[i] = (uint8_t)i; if (i > 0) f *= (unsigned long long)i; }
+    int left = k;
+    for (int i = 0; i < k; ++i) {
+        // f = (k-1-i)!
+        unsigned long long q = r / f;
+        r %= f;
+        perm[i] = pool[q];
+        for (int j = (int)q; j + 1 < left; ++j) pool[j] = pool[j + 1];
+        --left;
+        if (k - 1 - i > 0) f /= (unsigned long long)(k - 1 - i);
+    }
+}
+
+// composition rank -> cut positions p[1..k-1] (lexicographic in counts)
+__device__ void d_unrank_cuts(int n, int k, unsigned long long r, int* p) {
+    p[0] = 0;
+    int prev = 0;
+    for (int j = 1; j < k; ++j) {
+        for (int q = prev + 1;; ++q) {
+            unsigned long long cnt = d_binom(n - q - 1, k - 1 - j);
+            if (r < cnt) { p[j] = q; prev = q; break; }
+            r -= cnt;
+        }
+    }
+    p[k] = n;
+}
+
+struct Key {
+    double cost;
+    unsigned long long tie;
+};
+
+__device__ __forceinline__ bool key_less(const Key& a, const Key& b) {
+    return a.cost < b.cost || (a.cost == b.cost && a.tie < b.tie);
+}
+
+__device__ __forceinline__ Key warp_min(Key v) {
+    for (int off = 16; off > 0; off >>= 1) {
+        Key o;
+        o.cost = __shfl_down_sync(0xffffffffu, v.cost, off);
+        o.tie = __shfl_down_sync(0xffffffffu, v.tie, off);
+        if (key_less(o, v)) v = o;
+    }
+    return v;
+}
+
+struct ArgminScratch {
+    Key* blk;                 // [grid]
+    unsigned int* counter;    // [1]
+    Key* result;              // [1]
+    int* err;                 // [1] first error (index<<4|code) low 32 bits unused
+    unsigned long long* err_idx;
+};
+
+// CTA-wide reduction of per-thread keys, then last-block grid reduction.
+__device__ void block_argmin_finish(Key mine, const ArgminScratch& S) {
+    __shared__ Key wbest[32];
+    __shared__ bool last;
+    Key w = warp_min(mine);
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) wbest[wid] = w;
+    __syncthreads();
+    if (wid == 0) {
+        int nw = (blockDim.x + 31) >> 5;
+        Key v = lane < nw ? wbest[lane] : Key{INFINITY, ~0ull};
+        v = warp_min(v);
+        if (lane == 0) {
+            S.blk[blockIdx.x] = v;
+            __threadfence();
+            unsigned int done = atomicAdd(S.counter, 1u);
+            last = (done == gridDim.x - 1);
+        }
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    Key v{INFINITY, ~0ull};
+    for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+        Key o;
+        o.cost = __ldcg(&S.blk[b].cost);
+        o.tie = __ldcg(&S.blk[b].tie);
+        if (key_less(o, v)) v = o;
+    }
+    v = warp_min(v);
+    if (lane == 0) wbest[wid] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int nw = (blockDim.x + 31) >> 5;
+        Key r = wbest[0];
+        for (int i = 1; i < nw; ++i) if (key_less(wbest[i], r)) r = wbest[i];
+        *S.result = r;
+        *S.counter = 0;  // re-arm for the next launch
+    }
+}
+
+// Fast path: all stage entries error-free.  CTA = (item, chunk); item =
+// (bm, perm).  The last two stages vary with the last cut; stage k-2's
+// {C1*m, AL} triangle for this m sits in shared memory.
+template <bool SMEM>
+__global__ void __launch_bounds__(256) k3_argmin(DevInst I, RangeGeom G, ArgminScratch S) {
+    extern __shared__ double2 smem2[];
+    const int n = I.n, k = G.k;
+    const size_t N2 = (size_t)(n + 1) * (n + 1);
+    unsigned long long item = G.item0 + blockIdx.x / G.chunks_per_item;
+    unsigned long long cidx = blockIdx.x % G.chunks_per_item;
+    unsigned long long base = item * G.NC;
+    unsigned long long c_lo = cidx * G.chunk, c_hi = c_lo + G.chunk;
+    if (c_hi > G.NC) c_hi = G.NC;
+    // clip to [lo, hi)
+    if (base + c_lo < G.lo) c_lo = G.lo > base ? G.lo - base : 0;
+    if (base + c_hi > G.hi) c_hi = G.hi > base ? G.hi - base : 0;
+    Key mine{INFINITY, ~0ull};
+    int bmi = (int)(item / G.NP);
+    unsigned long long perm_rank = item % G.NP;
+    uint8_t order[GP_MAX_STAGES];
+    d_unrank_perm(k, perm_rank, order);
+    const int mi = bmi % I.nm;
+    const double Md = (double)(I.batch[bmi / I.nm] / I.micro[mi]);
+    const double2* T = I.stg + (size_t)mi * I.F * N2;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * n;
+    const int f2 = order[k - 2], f3 = order[k - 1];
+    const double2* T2 = T + (size_t)f2 * N2;
+    const double2* T3 = T + (size_t)f3 * N2;
+    const double* X23 = X + ((size_t)f2 * I.F + f3) * n;
+    // shared: stage k-2 triangle rows [a][a+1..n], then column of stage k-1
+    double2* tri = smem2;
+    double2* col = smem2 + (SMEM ? (size_t)n * (n + 1) / 2 : 0);
+    double* xs = (double*)(col + n);
+    if (SMEM) {
+        // dense [a][b] -> packed rows (row a holds b = a+1..n)
+        for (int t = threadIdx.x; t < n * (n + 1); t += blockDim.x) {
+            int a = t / (n + 1), b = t % (n + 1);
+            if (b > a) tri[a * n - a * (a - 1) / 2 + (b - a - 1)] = T2[t];
+        }
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+            col[t] = T3[tri_idx(n, t, n)];
+            xs[t] = X23[t];
+        }
+        __syncthreads();
+    }
+    if (c_lo < c_hi) {
+        unsigned long long span = c_hi - c_lo;
+        unsigned long long t0 = c_lo + span * threadIdx.x / blockDim.x;
+        unsigned long long t1 = c_lo + span * (threadIdx.x + 1) / blockDim.x;
+        if (t0 < t1) {
+            int p[GP_MAX_STAGES + 1];
+            d_unrank_cuts(n, k, t0, p);
+            unsigned long long ci = t0;
+            double best_cost = INFINITY;
+            unsigned long long best_ci = ~0ull;
+            bool have = false;
+            while (ci < t1) {
+                // prefix: stages 0..k-3 on cuts p[0..k-2]
+                double fill = 0.0, res = 0.0, mx = -INFINITY, xprev = 0.0;
+                for (int s = 0; s + 2 < k; ++s) {
+                    double2 e = __ldg(&T[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])]);
+                    if (s > 0) res = res + gpd::max0(xprev - e.x);
+                    double tot = ((fill + Md * e.x) + res) + e.y;
+                    mx = (s == 0 || tot > mx) ? tot : mx;
+                    double x = __ldg(&X[((size_t)order[s] * I.F + order[s + 1]) * n + (p[s + 1] - 1)]);
+                    fill = fill + (e.x + x);
+                    xprev = x;
+                }
+                const int a = p[k - 2];
+                const int rowoff = a * n - a * (a - 1) / 2;  // sum_{a'<a} (n - a')
+                // sweep the last cut q = p[k-1] in (a, n)
+                int q = p[k - 1];
+                unsigned long long run = (unsigned long long)(n - q);
+                if (run > t1 - ci) run = t1 - ci;
+                for (unsigned long long r = 0; r < run; ++r, ++q) {
+                    double2 e2, e3;
+                    double x2;
+                    if (SMEM) {
+                        e2 = tri[rowoff + (q - a - 1)];
+                        e3 = col[q];
+                        x2 = xs[q - 1];
+                    } else {
+                        e2 = __ldg(&T2[tri_idx(n, a, q)]);
+                        e3 = __ldg(&T3[tri_idx(n, q, n)]);
+                        x2 = __ldg(&X23[q - 1]);
+                    }
+                    double res2 = (k > 2) ? res + gpd::max0(xprev - e2.x) : res;
+                    double t2 = ((fill + Md * e2.x) + res2) + e2.y;
+                    double fill3 = fill + (e2.x + x2);
+                    double res3 = res2 + gpd::max0(x2 - e3.x);
+                    double t3 = ((fill3 + Md * e3.x) + res3) + e3.y;
+                    double c = (k > 2) ? mx : t2;
+                    c = (k > 2 && t2 > c) ? t2 : c;
+                    c = t3 > c ? t3 : c;
+                    if (!have || c < best_cost) {
+                        best_cost = c;
+                        best_ci = ci + r;
+                        have = true;
+                    }
+                }
+                ci += run;
+                if (ci >= t1) break;
+                // next prefix: next combination of p[1..k-2], then p[k-1] = p[k-2] + 1
+                int j = k - 2;
+                while (j >= 1 && p[j] >= n - (k - j)) --j;
+                if (j < 1) break;  // range exhausted (cannot happen while ci < NC)
+                ++p[j];
+                for (int t = j + 1; t < k; ++t) p[t] = p[t - 1] + 1;
+            }
+            if (have) {
+                mine.cost = best_cost;
+                mine.tie = ((perm_rank * G.NC) + best_ci) * (unsigned long long)G.nbm + (unsigned long long)bmi;
+            }
+        }
+    }
+    block_argmin_finish(mine, S);
+}
+
+// Generic range kernel (status-tracking): one thread per index; records the
+// first erroring candidate in enumeration order.
+__global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G, ArgminScratch S) {
+    unsigned long long idx = G.lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    Key mine{INFINITY, ~0ull};
+    if (idx < G.hi) {
+        unsigned long long comp = idx % G.NC;
+        unsigned long long r = idx / G.NC;
+        unsigned long long perm_rank = r % G.NP;
+        int bmi = (int)(r / G.NP);
+        uint8_t order[GP_MAX_STAGES];
+        int p[GP_MAX_STAGES + 1];
+        d_unrank_perm(G.k, perm_rank, order);
+        d_unrank_cuts(I.n, G.k, comp, p);
+        int mi = bmi % I.nm;
+        long long M = I.batch[bmi / I.nm] / I.micro[mi];
+        EvalOut e = eval_tables(I, G.k, order, p, mi, M);
+        if (e.status != GP_OK) {
+            atomicMin(S.err_idx, (idx << 4) | (unsigned long long)e.status);
+        } else {
+            mine.cost = e.cost;
+            mine.tie = ((perm_rank * G.NC) + comp) * (unsigned long long)G.nbm + (unsigned long long)bmi;
+        }
+    }
+    block_argmin_finish(mine, S);
+}
+
+// ---- plan detail of one candidate (single thread) -----------------------------------
+__global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const uint8_t* counts_in,
+                              int bm, gp_plan_info* out, int* status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int n = I.n;
+    size_t N2 = (size_t)(n + 1) * (n + 1);
+    uint8_t o[GP_MAX_STAGES];
+    int p[GP_MAX_STAGES + 1];
+    p[0] = 0;
+    for (int s = 0; s < k; ++s) { o[s] = order_in[s]; p[s + 1] = p[s] + counts_in[s]; }
+    int mi = bm % I.nm;
+    long long M = I.batch[bm / I.nm] / I.micro[mi];
+    EvalOut r = eval_tables(I, k, o, p, mi, M);
+    *status = r.status;
+    out->k = (uint32_t)k;
+    out->plan_cost = r.cost;
+    bool feas = true;
+    for (int s = 0; s < k; ++s)
+        if (I.scode[(size_t)o[s] * N2 + tri_idx(n, p[s], p[s + 1])] == SC_INFEASIBLE) feas = false;
+    out->feasible = feas ? 1 : 0;
+    const double2* T = I.stg + (size_t)mi * I.F * N2;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * n;
+    double Md = (double)M;
+    double fill = 0.0, res = 0.0, xprev = 0.0;
+    for (int s = 0; s < k; ++s) {
+        gp_stage_info& st = out->stage[s];
+        int shares[GP_MAX_SGS], np;
+        int kind = choose_split(I, o[s], p[s], p[s + 1], shares, &np);
+        st.kind = (uint32_t)kind;
+        st.n_parts = (uint32_t)np;
+        if (kind == GP_ASYM_PP) {
+            int pos = p[s];
+            for (int j = 0; j < np; ++j) {
+                st.pp_sg[j] = (uint32_t)j;
+                st.pp_start[j] = (uint32_t)pos;
+                st.pp_end[j] = (uint32_t)(pos + shares[j]);
+                pos += shares[j];
+            }
+        }
+        if (!feas || r.status != GP_OK) continue;
+        double2 e = T[(size_t)o[s] * N2 + tri_idx(n, p[s], p[s + 1])];
+        if (s > 0) res = res + gpd::max0(xprev - e.x);
+        st.fill_seconds = fill;
+        st.run_seconds = Md * e.x;
+        st.residual_seconds = res;
+        st.collective_seconds = e.y;
+        if (s + 1 < k) {
+            double x = X[((size_t)o[s] * I.F + o[s + 1]) * n + (p[s + 1] - 1)];
+            fill = fill + (e.x + x);
+            xprev = x;
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// context
+// ----------------------------------------------------------------------------
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t count) {
+        if (count <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = count ? count : 1;
+        cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+        if (e == cudaSuccess) cap = c;
+        return e;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+struct gp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool loaded = false;
+    uint32_t flags = 0;
+    int n = 0, F = 0, D = 0, nb = 0, nm = 0, nsg = 0;
+    std::vector<long long> h_batch, h_micro;
+    DBuf<double> fwd, bwd_in, bwd_w, act, param, p_c, mem, p_t, lat, bw, fg_cap, sg_cap, fg_minbw,
+        fg_minbw_in, S, g_rf, g_cf, g_dp, g_minmem, sg_minmem, C1, xt;
+    DBuf<long long> batch, micro;
+    DBuf<uint32_t> id_rank, fg_off, fg_mem, fg_sg_off, sg_off, sg_mem, flagsbuf;
+    DBuf<uint8_t> fg_has, g_tp_ok, scode, skind;
+    DBuf<double2> stg;
+    DBuf<int> gw;
+    // K3 scratch
+    DBuf<Key> blk, result;
+    DBuf<unsigned int> counter;
+    DBuf<unsigned long long> err_idx;
+    DBuf<int> err_dummy;
+    // K2 staging
+    DBuf<uint8_t> b_order, b_counts, b_bm, b_status;
+    DBuf<double> b_cost;
+    DBuf<gp_plan_info> info;
+    DBuf<gp_group_info> ginfo;
+    DBuf<int> dstatus;
+    RangeGeom last_geom{};
+    bool last_generic = false;
+    unsigned long long last_lo = 0, last_hi = 0;
+    int smem_max = 0;
+
+    DevInst view() {
+        DevInst I;
+        I.n = n; I.F = F; I.D = D; I.nb = nb; I.nm = nm;
+        I.fwd = fwd.p; I.bwd_in = bwd_in.p; I.bwd_w = bwd_w.p; I.act = act.p; I.param = param.p;
+        I.batch = batch.p; I.micro = micro.p;
+        I.p_c = p_c.p; I.mem = mem.p; I.p_t = p_t.p; I.lat = lat.p; I.bw = bw.p;
+        I.id_rank = id_rank.p;
+        I.fg_off = fg_off.p; I.fg_mem = fg_mem.p; I.fg_sg_off = fg_sg_off.p;
+        I.sg_off = sg_off.p; I.sg_mem = sg_mem.p;
+        I.fg_cap = fg_cap.p; I.sg_cap = sg_cap.p;
+        I.fg_minbw = fg_minbw.p; I.fg_has_minbw = fg_has.p;
+        I.bf = bf;
+        I.S = S.p; I.g_tp_ok = g_tp_ok.p; I.g_rf = g_rf.p; I.g_cf = g_cf.p; I.g_dp = g_dp.p;
+        I.g_minmem = g_minmem.p; I.sg_minmem = sg_minmem.p;
+        I.stg = stg.p; I.scode = scode.p; I.skind = skind.p; I.C1 = C1.p;
+        I.gw = gw.p; I.xt = xt.p; I.flags = flagsbuf.p;
+        return I;
+    }
+    double bf = 1.25;
+};
+
+template <typename T>
+static cudaError_t upload(cudaStream_t s, DBuf<T>& d, const T* h, size_t count) {
+    cudaError_t e = d.ensure(count);
+    if (e != cudaSuccess) return e;
+    if (count == 0) return cudaSuccess;
+    return cudaMemcpyAsync(d.p, h, count * sizeof(T), cudaMemcpyHostToDevice, s);
+}
+
+extern "C" {
+
+const char* gp_version(void) { return "geopipe_b200 0.1 (sm_100a)"; }
+const char* gp_last_error(void) { return g_err; }
+
+int gp_ctx_create(int device, gp_ctx** out) {
+    if (!out) return fail(GP_ERR_INPUT, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(GP_ERR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(GP_ERR_INPUT, "device %d out of range", device);
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(GP_ERR_CUDA, "device %d is sm_%d%d; this engine is built for sm_100a",
+                    device, prop.major, prop.minor);
+    CUDA_TRY(cudaSetDevice(device));
+    gp_ctx* c = new gp_ctx();
+    c->device = device;
+    c->smem_max = (int)prop.sharedMemPerBlockOptin;
+    cudaError_t se = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (se != cudaSuccess) { delete c; return fail(GP_ERR_CUDA, "stream: %s", cudaGetErrorString(se)); }
+    *out = c;
+    return GP_OK;
+}
+
+void* gp_ctx_stream(gp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+void gp_ctx_destroy(gp_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    DBuf<double>* dd[] = {&c->fwd, &c->bwd_in, &c->bwd_w, &c->act, &c->param, &c->p_c, &c->mem,
+                          &c->p_t, &c->lat, &c->bw, &c->fg_cap, &c->sg_cap, &c->fg_minbw,
+                          &c->fg_minbw_in, &c->S, &c->g_rf, &c->g_cf, &c->g_dp, &c->g_minmem,
+                          &c->sg_minmem, &c->C1, &c->xt, &c->b_cost};
+    for (auto* b : dd) b->release();
+    c->batch.release(); c->micro.release();
+    DBuf<uint32_t>* uu[] = {&c->id_rank, &c->fg_off, &c->fg_mem, &c->fg_sg_off, &c->sg_off,
+                            &c->sg_mem, &c->flagsbuf};
+    for (auto* b : uu) b->release();
+    DBuf<uint8_t>* bb[] = {&c->fg_has, &c->g_tp_ok, &c->scode, &c->skind, &c->b_order,
+                           &c->b_counts, &c->b_bm, &c->b_status};
+    for (auto* b : bb) b->release();
+    c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
+    c->counter.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
+    c->ginfo.release(); c->dstatus.release();
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+static int run_tables(gp_ctx* c, bool full) {
+    DevInst I = c->view();
+    cudaStream_t s = c->stream;
+    CUDA_TRY(cudaMemsetAsync(c->flagsbuf.p, 0, sizeof(uint32_t), s));
+    if (full) {
+        dim3 g1((c->n + 127) / 128, 5);
+        k1_intervals<<<g1, 128, 0, s>>>(I);
+        k1_groups<<<(c->F + 31) / 32, 32, 0, s>>>(I);
+    }
+    long long ns = (long long)c->F * (c->n + 1) * (c->n + 1);
+    k1_stages<<<(unsigned)((ns + 127) / 128), 128, 0, s>>>(I);
+    k1_gateways<<<(c->F * c->F + 63) / 64, 64, 0, s>>>(I);
+    long long nx = (long long)c->nm * c->F * c->F * c->n;
+    k1_boundary<<<(unsigned)((nx + 255) / 256), 256, 0, s>>>(I);
+    CUDA_TRY(cudaGetLastError());
+    uint32_t flags = 0;
+    CUDA_TRY(cudaMemcpyAsync(&flags, c->flagsbuf.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    c->flags = flags;
+    return GP_OK;
+}
+
+int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
+    if (!c || !in) return fail(GP_ERR_INPUT, "null argument");
+    if (in->n_layers < 1 || in->n_layers > GP_MAX_LAYERS)
+        return fail(GP_ERR_INPUT, "n_layers %u outside [1, %d]", in->n_layers, GP_MAX_LAYERS);
+    if (in->n_fgs < 1 || in->n_fgs > GP_MAX_STAGES)
+        return fail(GP_ERR_INPUT, "n_fgs %u outside [1, %d]", in->n_fgs, GP_MAX_STAGES);
+    if (in->n_batch < 1 || in->n_micro < 1 || in->n_batch * in->n_micro > 255)
+        return fail(GP_ERR_INPUT, "bad (batch, micro) candidate counts");
+    for (uint32_t i = 0; i < in->n_batch; ++i)
+        for (uint32_t j = 0; j < in->n_micro; ++j)
+            if (in->batch[i] <= 0 || in->micro[j] <= 0 || in->batch[i] % in->micro[j])
+                return fail(GP_ERR_INPUT, "micro-batch %lld does not divide batch %lld",
+                            (long long)in->micro[j], (long long)in->batch[i]);
+    uint32_t nsg = in->fg_sg_offset[in->n_fgs];
+    for (uint32_t f = 0; f < in->n_fgs; ++f) {
+        uint32_t nm = in->fg_member_offset[f + 1] - in->fg_member_offset[f];
+        uint32_t ng = in->fg_sg_offset[f + 1] - in->fg_sg_offset[f];
+        if (nm < 1 || nm > GP_MAX_MEMBERS) return fail(GP_ERR_INPUT, "group %u has %u members", f, nm);
+        if (ng > GP_MAX_SGS) return fail(GP_ERR_INPUT, "group %u has %u subgroups", f, ng);
+    }
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    uint32_t n = in->n_layers, D = in->n_devices, F = in->n_fgs;
+    c->n = (int)n; c->F = (int)F; c->D = (int)D; c->nb = (int)in->n_batch; c->nm = (int)in->n_micro;
+    c->nsg = (int)nsg;
+    c->bf = in->bottleneck_factor;
+    c->h_batch.assign(in->batch, in->batch + in->n_batch);
+    c->h_micro.assign(in->micro, in->micro + in->n_micro);
+    size_t DD = (size_t)D * D;
+    CUDA_TRY(upload(s, c->fwd, in->fwd_flops, n));
+    CUDA_TRY(upload(s, c->bwd_in, in->bwd_input_flops, n));
+    CUDA_TRY(upload(s, c->bwd_w, in->bwd_weight_flops, n));
+    CUDA_TRY(upload(s, c->act, in->activation_out_bytes, n));
+    CUDA_TRY(upload(s, c->param, in->param_bytes, n));
+    CUDA_TRY(upload(s, c->batch, (const long long*)in->batch, in->n_batch));
+    CUDA_TRY(upload(s, c->micro, (const long long*)in->micro, in->n_micro));
+    CUDA_TRY(upload(s, c->p_c, in->p_c, D));
+    CUDA_TRY(upload(s, c->mem, in->memory_bytes, D));
+    CUDA_TRY(upload(s, c->id_rank, in->id_rank, D));
+    CUDA_TRY(upload(s, c->p_t, in->p_t, DD));
+    CUDA_TRY(upload(s, c->lat, in->latency, DD));
+    CUDA_TRY(upload(s, c->bw, in->bandwidth, DD));
+    uint32_t nfm = in->fg_member_offset[F];
+    CUDA_TRY(upload(s, c->fg_off, in->fg_member_offset, F + 1));
+    CUDA_TRY(upload(s, c->fg_mem, in->fg_members, nfm));
+    CUDA_TRY(upload(s, c->fg_cap, in->fg_capacity, F));
+    CUDA_TRY(upload(s, c->fg_minbw_in, in->fg_min_bw, F));
+    CUDA_TRY(upload(s, c->fg_minbw, in->fg_min_bw, F));
+    CUDA_TRY(upload(s, c->fg_has, in->fg_has_min_bw, F));
+    CUDA_TRY(upload(s, c->fg_sg_off, in->fg_sg_offset, F + 1));
+    CUDA_TRY(upload(s, c->sg_off, in->sg_member_offset, nsg + 1));
+    uint32_t nsm = in->sg_member_offset[nsg];
+    CUDA_TRY(upload(s, c->sg_mem, in->sg_members, nsm));
+    CUDA_TRY(upload(s, c->sg_cap, in->sg_capacity, nsg));
+    size_t N2 = (size_t)(n + 1) * (n + 1);
+    CUDA_TRY(c->S.ensure(5 * N2));
+    CUDA_TRY(c->g_tp_ok.ensure(F));
+    CUDA_TRY(c->g_rf.ensure(nfm));
+    CUDA_TRY(c->g_cf.ensure(nfm));
+    CUDA_TRY(c->g_dp.ensure(nsg ? nsg : 1));
+    CUDA_TRY(c->g_minmem.ensure(F));
+    CUDA_TRY(c->sg_minmem.ensure(nsg ? nsg : 1));
+    CUDA_TRY(c->stg.ensure((size_t)c->nm * F * N2));
+    CUDA_TRY(c->scode.ensure((size_t)F * N2));
+    CUDA_TRY(c->skind.ensure((size_t)F * N2));
+    CUDA_TRY(c->C1.ensure((size_t)F * N2));
+    CUDA_TRY(c->gw.ensure((size_t)F * F));
+    CUDA_TRY(c->xt.ensure((size_t)c->nm * F * F * n));
+    CUDA_TRY(c->flagsbuf.ensure(1));
+    CUDA_TRY(c->counter.ensure(1));
+    CUDA_TRY(c->result.ensure(1));
+    CUDA_TRY(c->err_idx.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned int), s));
+    int st = run_tables(c, true);
+    if (st != GP_OK) return st;
+    c->loaded = true;
+    return GP_OK;
+}
+
+int gp_set_bandwidth(gp_ctx* c, const double* bandwidth) {
+    if (!c || !c->loaded || !bandwidth) return fail(GP_ERR_INPUT, "context not loaded");
+    CUDA_TRY(cudaSetDevice(c->device));
+    size_t DD = (size_t)c->D * c->D;
+    CUDA_TRY(cudaMemcpyAsync(c->bw.p, bandwidth, DD * sizeof(double), cudaMemcpyHostToDevice,
+                             c->stream));
+    DevInst I = c->view();
+    k1_minbw<<<(c->F + 31) / 32, 32, 0, c->stream>>>(I, c->fg_minbw.p);
+    CUDA_TRY(cudaGetLastError());
+    return run_tables(c, false);
+}
+
+int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_order,
+                         const uint8_t* d_counts, const uint8_t* d_bm, double* d_cost,
+                         uint8_t* d_status) {
+    if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    if (k < 1 || k > GP_MAX_STAGES) return fail(GP_ERR_INPUT, "k=%u outside [1,%d]", k, GP_MAX_STAGES);
+    if (n == 0) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    DevInst I = c->view();
+    unsigned blocks = (unsigned)((n + 255) / 256);
+    k2_eval_batch<<<blocks, 256, 0, c->stream>>>(I, (int)k, (long long)n, d_order, d_counts, d_bm,
+                                                 d_cost, d_status);
+    CUDA_TRY(cudaGetLastError());
+    return GP_OK;
+}
+
+int gp_eval_batch(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* order, const uint8_t* counts,
+                  const uint8_t* bm, double* cost, uint8_t* status) {
+    if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    if (n == 0) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->b_order.ensure(n * k));
+    CUDA_TRY(c->b_counts.ensure(n * k));
+    CUDA_TRY(c->b_bm.ensure(n));
+    CUDA_TRY(c->b_cost.ensure(n));
+    CUDA_TRY(c->b_status.ensure(n));
+    CUDA_TRY(cudaMemcpyAsync(c->b_order.p, order, n * k, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->b_counts.p, counts, n * k, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->b_bm.p, bm, n, cudaMemcpyHostToDevice, s));
+    int st = gp_eval_batch_device(c, k, n, c->b_order.p, c->b_counts.p, c->b_bm.p, c->b_cost.p,
+                                  c->b_status.p);
+    if (st != GP_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(cost, c->b_cost.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status, c->b_status.p, n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return GP_OK;
+}
+
+static unsigned long long h_binom(int n, int r) {
+    if (r < 0 || r > n) return 0ull;
+    unsigned long long res = 1;
+    for (int i = 1; i <= r; ++i) res = res * (unsigned long long)(n - r + i) / (unsigned long long)i;
+    return res;
+}
+static unsigned long long h_fact(int k) {
+    unsigned long long f = 1;
+    for (int i = 2; i <= k; ++i) f *= (unsigned long long)i;
+    return f;
+}
+
+int gp_space_size(gp_ctx* c, uint64_t* out) {
+    if (!c || !c->loaded || !out) return fail(GP_ERR_INPUT, "context not loaded");
+    int k = c->F;
+    *out = (k > c->n) ? 0 : (uint64_t)c->nb * c->nm * h_fact(k) * h_binom(c->n - 1, k - 1);
+    return GP_OK;
+}
+
+int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
+    if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    int k = c->F;
+    uint64_t total;
+    gp_space_size(c, &total);
+    if (hi > total) hi = total;
+    if (lo > hi) lo = hi;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    RangeGeom G;
+    G.k = k;
+    G.nbm = c->nb * c->nm;
+    G.NC = h_binom(c->n - 1, k - 1);
+    G.NP = h_fact(k);
+    G.lo = lo;
+    G.hi = hi;
+    c->last_lo = lo;
+    c->last_hi = hi;
+    ArgminScratch S;
+    CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));  // = ~0
+    DevInst I = c->view();
+    bool generic = c->flags != 0 || k < 2;
+    c->last_generic = generic;
+    unsigned long long grid;
+    if (hi == lo) {
+        generic = true;
+        grid = 1;
+    } else if (generic) {
+        grid = (hi - lo + 255) / 256;
+    } else {
+        unsigned long long item_first = lo / G.NC, item_last = (hi - 1) / G.NC;
+        unsigned long long items = item_last - item_first + 1;
+        // aim for >= 2 CTAs per SM, chunks of >= 4096 candidates
+        unsigned long long target = 2 * 148;
+        unsigned long long cpi = (target + items - 1) / items;
+        unsigned long long chunk = (G.NC + cpi - 1) / cpi;
+        if (chunk < 4096) chunk = 4096;
+        cpi = (G.NC + chunk - 1) / chunk;
+        G.item0 = item_first;
+        G.chunk = chunk;
+        G.chunks_per_item = cpi;
+        grid = items * cpi;
+    }
+    if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "range too large for one launch");
+    CUDA_TRY(c->blk.ensure(grid));
+    S.blk = c->blk.p;
+    S.counter = c->counter.p;
+    S.result = c->result.p;
+    S.err = nullptr;
+    S.err_idx = c->err_idx.p;
+    c->last_geom = G;
+    if (generic) {
+        if (hi == lo) G.hi = G.lo;  // one empty CTA writes the neutral key
+        k3_argmin_generic<<<(unsigned)grid, 256, 0, s>>>(I, G, S);
+    } else {
+        size_t smem = ((size_t)c->n * (c->n + 1) / 2 + c->n) * sizeof(double2) + c->n * sizeof(double);
+        if ((int)smem <= c->smem_max && smem <= 200 * 1024) {
+            CUDA_TRY(cudaFuncSetAttribute(k3_argmin<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+            k3_argmin<true><<<(unsigned)grid, 256, smem, s>>>(I, G, S);
+        } else {
+            k3_argmin<false><<<(unsigned)grid, 256, 0, s>>>(I, G, S);
+        }
+    }
+    CUDA_TRY(cudaGetLastError());
+    return GP_OK;
+}
+
+static void h_unrank_perm(int k, unsigned long long r, uint8_t* perm) {
+    uint8_t pool[GP_MAX_STAGES];
+    for (int i = 0; i < k; ++i) pool[i] = (uint8_t)i;
+    int left = k;
+    for (int i = 0; i < k; ++i) {
+        unsigned long long f = h_fact(k - 1 - i);
+        unsigned long long q = r / f;
+        r %= f;
+        perm[i] = pool[q];
+        for (int j = (int)q; j + 1 < left; ++j) pool[j] = pool[j + 1];
+        --left;
+    }
+}
+
+static void h_unrank_counts(int n, int k, unsigned long long r, uint8_t* counts) {
+    int prev = 0;
+    for (int j = 1; j < k; ++j) {
+        for (int q = prev + 1;; ++q) {
+            unsigned long long cnt = h_binom(n - q - 1, k - 1 - j);
+            if (r < cnt) { counts[j - 1] = (uint8_t)(q - prev); prev = q; break; }
+            r -= cnt;
+        }
+    }
+    counts[k - 1] = (uint8_t)(n - prev);
+}
+
+int gp_argmin_fetch(gp_ctx* c, gp_best* out) {
+    if (!c || !c->loaded || !out) return fail(GP_ERR_INPUT, "context not loaded");
+    CUDA_TRY(cudaSetDevice(c->device));
+    Key r;
+    unsigned long long err;
+    CUDA_TRY(cudaMemcpyAsync(&r, c->result.p, sizeof(Key), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&err, c->err_idx.p, sizeof(err), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    memset(out, 0, sizeof(*out));
+    const RangeGeom& G = c->last_geom;
+    out->k = (uint32_t)G.k;
+    out->evaluated = c->last_hi - c->last_lo;
+    if (err != ~0ull) {
+        int code = (int)(err & 15ull);
+        return fail(code, "candidate %llu raises status %d", err >> 4, code);
+    }
+    if (r.tie == ~0ull) return fail(GP_ERR_NO_FEASIBLE, "empty candidate range");
+    unsigned long long bm = r.tie % (unsigned long long)G.nbm;
+    unsigned long long pc = r.tie / (unsigned long long)G.nbm;
+    unsigned long long comp = pc % G.NC, perm = pc / G.NC;
+    out->cost = r.cost;
+    out->index = (bm * G.NP + perm) * G.NC + comp;
+    out->batch_index = (uint32_t)(bm / c->nm);
+    out->micro_index = (uint32_t)(bm % c->nm);
+    h_unrank_perm(G.k, perm, out->order);
+    h_unrank_counts(c->n, G.k, comp, out->counts);
+    return GP_OK;
+}
+
+int gp_argmin_range(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* out) {
+    int st = gp_argmin_range_async(c, lo, hi);
+    if (st != GP_OK) return st;
+    return gp_argmin_fetch(c, out);
+}
+
+int gp_plan_detail(gp_ctx* c, uint32_t k, const uint8_t* order, const uint8_t* counts, uint32_t bm,
+                   gp_plan_info* out) {
+    if (!c || !c->loaded || !out) return fail(GP_ERR_INPUT, "context not loaded");
+    if (k < 1 || k > GP_MAX_STAGES || bm >= (uint32_t)(c->nb * c->nm))
+        return fail(GP_ERR_INPUT, "bad candidate");
+    int sum = 0;
+    unsigned seen = 0;
+    for (uint32_t s = 0; s < k; ++s) {
+        if (order[s] >= c->F || ((seen >> order[s]) & 1u) || counts[s] == 0)
+            return fail(GP_ERR_INPUT, "stage order must use distinct groups and positive counts");
+        seen |= 1u << order[s];
+        sum += counts[s];
+    }
+    if (sum > c->n) return fail(GP_ERR_INPUT, "counts exceed the layer count");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->b_order.ensure(GP_MAX_STAGES));
+    CUDA_TRY(c->b_counts.ensure(GP_MAX_STAGES));
+    CUDA_TRY(c->info.ensure(1));
+    CUDA_TRY(c->dstatus.ensure(1));
+    CUDA_TRY(cudaMemcpyAsync(c->b_order.p, order, k, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->b_counts.p, counts, k, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(c->info.p, 0, sizeof(gp_plan_info), s));
+    DevInst I = c->view();
+    k_plan_detail<<<1, 32, 0, s>>>(I, (int)k, c->b_order.p, c->b_counts.p, (int)bm, c->info.p,
+                                   c->dstatus.p);
+    CUDA_TRY(cudaGetLastError());
+    int status = 0;
+    CUDA_TRY(cudaMemcpyAsync(out, c->info.p, sizeof(gp_plan_info), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&status, c->dstatus.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (status != GP_OK) return fail(status, "candidate raises status %d", status);
+    return GP_OK;
+}
+
+__global__ void k_group_info(DevInst I, int f, gp_group_info* out) {
+    if (threadIdx.x != 0) return;
+    int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
+    out->n_members = (uint32_t)(m1 - m0);
+    out->n_sgs = (uint32_t)(s1 - s0);
+    out->tp_ok = I.g_tp_ok[f];
+    for (int x = m0; x < m1; ++x) { out->tp_row[x - m0] = I.g_rf[x]; out->tp_col[x - m0] = I.g_cf[x]; }
+    for (int g = s0; g < s1; ++g) out->dp_fraction[g - s0] = I.g_dp[g];
+}
+
+int gp_group_splits(gp_ctx* c, uint32_t f, gp_group_info* out) {
+    if (!c || !c->loaded || !out || f >= (uint32_t)c->F) return fail(GP_ERR_INPUT, "bad group");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(c->ginfo.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(c->ginfo.p, 0, sizeof(gp_group_info), c->stream));
+    DevInst I = c->view();
+    k_group_info<<<1, 32, 0, c->stream>>>(I, (int)f, c->ginfo.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, c->ginfo.p, sizeof(gp_group_info), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return GP_OK;
+}
+
+// ---- diagnostics: FP64 add issue-rate microbenchmark --------------------------------
+// 8 independent DADD chains per thread so the FP64 pipe, not latency, bounds it.
+__global__ void k_fp64_peak(double* sink, int iters, double step) {
+    double a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+           a6 = a0 + 6, a7 = a0 + 7;
+    for (int i = 0; i < iters; ++i) {
+        a0 = a0 + step; a1 = a1 + step; a2 = a2 + step; a3 = a3 + step;
+        a4 = a4 + step; a5 = a5 + step; a6 = a6 + step; a7 = a7 + step;
+    }
+    double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (r == 12345.678) sink[blockIdx.x] = r;  // never true; keeps the chains live
+}
+
+int gp_diag_fp64_peak(int device, double* dadd_per_second) {
+    if (!dadd_per_second) return fail(GP_ERR_INPUT, "null output");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 1 << 14;
+    double* sink = nullptr;
+    CUDA_TRY(cudaMalloc(&sink, blocks * sizeof(double)));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_fp64_peak<<<blocks, threads>>>(sink, iters, 1e-9);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        k_fp64_peak<<<blocks, threads>>>(sink, iters, 1e-9);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (err != cudaSuccess) return fail(GP_ERR_CUDA, "fp64 peak: %s", cudaGetErrorString(err));
+    double ops = (double)blocks * threads * iters * 8.0;
+    *dadd_per_second = ops / (best * 1e-3);
+    return GP_OK;
+}
+
+}  // extern "C"

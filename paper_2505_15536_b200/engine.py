@@ -1,0 +1,181 @@
+"""ctypes binding of the CUDA engine ``libgeopipe_b200.so`` (include/geopipe_b200.h).
+
+This is the only way the package computes plan costs.  There is no CPU
+fallback: if the shared library is missing, or no sm_100 device is visible,
+every call raises :class:`~.domain.DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import abi
+from . import domain as D
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgeopipe_b200.so")
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib():
+    """Load the engine library (raises DeviceError when it is not built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise D.DeviceError(
+                f"CUDA engine not built: {LIB_PATH} is missing "
+                "(run __graft_entry__.build() or make -C paper_2505_15536_b200/csrc)")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        vp = C.c_void_p
+        L.gp_version.restype = C.c_char_p
+        L.gp_last_error.restype = C.c_char_p
+        L.gp_ctx_create.argtypes = [C.c_int, P(vp)]
+        L.gp_ctx_load.argtypes = [vp, P(abi.GpInstance)]
+        L.gp_ctx_destroy.argtypes = [vp]
+        L.gp_ctx_destroy.restype = None
+        L.gp_ctx_stream.argtypes = [vp]
+        L.gp_ctx_stream.restype = vp
+        u8p = P(C.c_uint8)
+        L.gp_eval_batch.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p,
+                                    P(C.c_double), u8p]
+        L.gp_eval_batch_device.argtypes = [vp, C.c_uint32, C.c_uint64, vp, vp, vp, vp, vp]
+        L.gp_space_size.argtypes = [vp, P(C.c_uint64)]
+        L.gp_argmin_range.argtypes = [vp, C.c_uint64, C.c_uint64, P(abi.GpBest)]
+        L.gp_argmin_range_async.argtypes = [vp, C.c_uint64, C.c_uint64]
+        L.gp_argmin_fetch.argtypes = [vp, P(abi.GpBest)]
+        L.gp_plan_detail.argtypes = [vp, C.c_uint32, u8p, u8p, C.c_uint32,
+                                     P(abi.GpPlanInfo)]
+        L.gp_group_splits.argtypes = [vp, C.c_uint32, P(abi.GpGroupInfo)]
+        L.gp_set_bandwidth.argtypes = [vp, P(C.c_double)]
+        L.gp_diag_fp64_peak.argtypes = [C.c_int, P(C.c_double)]
+        _lib = L
+        return L
+
+
+def _check(status: int) -> None:
+    if status != abi.GP_OK:
+        msg = lib().gp_last_error().decode(errors="replace")
+        abi.raise_for(status, msg)
+
+
+def _u8(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+class Engine:
+    """One engine context on one CUDA device (one stream)."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        _check(L.gp_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+        self.packed = None
+
+    def close(self):
+        if self._h:
+            lib().gp_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        return lib().gp_ctx_stream(self._h) or 0
+
+    def load(self, packed) -> "Engine":
+        _check(lib().gp_ctx_load(self._h, C.byref(packed.struct)))
+        self.packed = packed
+        return self
+
+    def space_size(self) -> int:
+        out = C.c_uint64(0)
+        _check(lib().gp_space_size(self._h, C.byref(out)))
+        return out.value
+
+    def eval_batch(self, order, counts, bm):
+        order = np.ascontiguousarray(order, dtype=np.uint8)
+        counts = np.ascontiguousarray(counts, dtype=np.uint8)
+        bm = np.ascontiguousarray(bm, dtype=np.uint8)
+        n, k = order.shape
+        cost = np.empty(n, dtype=np.float64)
+        status = np.empty(n, dtype=np.uint8)
+        if n:
+            _check(lib().gp_eval_batch(self._h, k, n, _u8(order), _u8(counts), _u8(bm),
+                                       cost.ctypes.data_as(C.POINTER(C.c_double)),
+                                       _u8(status)))
+        return cost, status
+
+    def eval_batch_device(self, k, n, d_order, d_counts, d_bm, d_cost, d_status):
+        """Device-pointer variant (ints), asynchronous on :attr:`stream`."""
+        _check(lib().gp_eval_batch_device(self._h, k, n, d_order, d_counts, d_bm,
+                                          d_cost, d_status))
+
+    def argmin_range(self, lo: int, hi: int) -> abi.GpBest:
+        best = abi.GpBest()
+        _check(lib().gp_argmin_range(self._h, int(lo), int(hi), C.byref(best)))
+        return best
+
+    def argmin_range_async(self, lo: int, hi: int) -> None:
+        _check(lib().gp_argmin_range_async(self._h, int(lo), int(hi)))
+
+    def argmin_fetch(self) -> abi.GpBest:
+        best = abi.GpBest()
+        _check(lib().gp_argmin_fetch(self._h, C.byref(best)))
+        return best
+
+    def plan_detail(self, order, counts, bm: int) -> abi.GpPlanInfo:
+        o = np.ascontiguousarray(order, dtype=np.uint8)
+        c = np.ascontiguousarray(counts, dtype=np.uint8)
+        info = abi.GpPlanInfo()
+        _check(lib().gp_plan_detail(self._h, len(o), _u8(o), _u8(c), int(bm),
+                                    C.byref(info)))
+        return info
+
+    def group_splits(self, f: int) -> abi.GpGroupInfo:
+        g = abi.GpGroupInfo()
+        _check(lib().gp_group_splits(self._h, int(f), C.byref(g)))
+        return g
+
+    def set_bandwidth(self, bw: np.ndarray) -> None:
+        a = np.ascontiguousarray(bw, dtype=np.float64)
+        _check(lib().gp_set_bandwidth(self._h, a.ctypes.data_as(C.POINTER(C.c_double))))
+
+
+def fp64_peak(device: int = 0) -> float:
+    """Measured FP64 add issue rate (ops/s) of ``device``."""
+    out = C.c_double(0.0)
+    _check(lib().gp_diag_fp64_peak(int(device), C.byref(out)))
+    return out.value
+
+
+_tls = threading.local()
+
+
+def default_engine(device: int = 0) -> Engine:
+    """Per-thread engine context (contexts are not shared across threads)."""
+    engines = getattr(_tls, "engines", None)
+    if engines is None:
+        engines = _tls.engines = {}
+    eng = engines.get(device)
+    if eng is None:
+        eng = engines[device] = Engine(device)
+    return eng

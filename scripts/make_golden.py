@@ -1,0 +1,234 @@
+#!/usr/bin/env python3
+"""Generate tests/golden/ fixtures from the UNMODIFIED reference (build container only).
+
+The reference (/root/reference/pkg/src, pure Python) is imported read-only; its
+outputs are frozen into JSON / .npy files so that the GPU box - which has no
+/root/reference - can check the engine against the reference's own answers.
+
+Cases
+  c1, c1j, c2, c2j   App. D configs (integer / jittered): every candidate's
+                     _evaluate cost in exhaustive_plan enumeration order, the
+                     exhaustive_plan result, search_plan results for seeds 0-5
+  c4, c4j            App. D config C4: 20,000 sampled candidates' costs
+                     (random.Random(4).sample), search_plan seeds 0-1, and the
+                     full 11.4M exhaustive arg-min computed by the C oracle
+                     (the oracle is first checked bit-exact on the sample)
+  small, rand*       reference test fixtures (tests/conftest.py small_setup,
+                     tests/test_acceptance.py:_random_instance)
+  err_*              error behaviour: all-infeasible memory, zero intra-group
+                     bandwidth, zero-bandwidth gateway
+Usage: python scripts/make_golden.py [--skip-c4]
+"""
+
+from __future__ import annotations
+
+import argparse
+import itertools
+import logging
+import os
+import random
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import golden_io as G  # noqa: E402
+from refbridge import AVAILABLE, build_reference, geopipe  # noqa: E402
+
+from paper_2505_15536_b200 import instances as I  # noqa: E402
+from paper_2505_15536_b200.layout import PackedInstance  # noqa: E402
+
+logging.disable(logging.CRITICAL)
+
+
+def enumerate_all(model, groups):
+    """Candidates in exhaustive_plan order (src/planner.py:389-392)."""
+    from geopipe.planner import Candidate, _compositions
+    fg_ids = sorted(groups.fgs)
+    n = model.num_layers
+    for bi, b in enumerate(model.global_batch_candidates):
+        for mi, m in enumerate(model.microbatch_candidates):
+            for order in itertools.permutations(fg_ids):
+                for cuts in _compositions(n, len(order)):
+                    yield bi * len(model.microbatch_candidates) + mi, b, m, Candidate(order, cuts)
+
+
+ERR_CODE = {"InputFileError": 1, "InfeasibleSplitError": 2, "NoFeasiblePlanError": 3,
+            "DegenerateGroupError": 4, "InvalidTopologyError": 5}
+
+
+def ref_cost(model, topo, groups, cand, b, m, cfg):
+    """(cost, status): status is the C-ABI code of the exception _evaluate raises."""
+    from geopipe.planner import _evaluate
+    try:
+        return _evaluate(cand, b, m, groups, topo, model, cfg, {})[0], 0
+    except Exception as e:
+        return float("nan"), ERR_CODE[type(e).__name__]
+
+
+def run_or_error(fn):
+    try:
+        return {"result": G.result_to_dict(fn())}
+    except Exception as e:  # reference exception class name is the golden
+        return {"error": type(e).__name__}
+
+
+def dump_case(name, model, topo, groups, seeds, all_costs=True, beam_width=8, max_iter=20):
+    gp = geopipe()
+    doc = {"instance": G.instance_to_dict(model, topo, groups)}
+    t = time.time()
+    if all_costs:
+        cfg = gp.SearchConfig(seed=0)
+        out = [ref_cost(model, topo, groups, c, b, m, cfg)
+               for _, b, m, c in enumerate_all(model, groups)]
+        costs = np.array([c for c, _ in out], dtype=np.float64)
+        status = np.array([s for _, s in out], dtype=np.uint8)
+        np.save(os.path.join(G.GOLDEN, f"{name}.costs.npy"), costs)
+        np.save(os.path.join(G.GOLDEN, f"{name}.status.npy"), status)
+        doc["n_candidates"] = int(costs.size)
+    cfg0 = gp.SearchConfig(seed=0, beam_width=beam_width, max_iter=max_iter)
+    doc["exhaustive"] = run_or_error(lambda: gp.exhaustive_plan(model, topo, groups, cfg0))
+    doc["search"] = {}
+    for s in seeds:
+        cfg = gp.SearchConfig(seed=s, beam_width=beam_width, max_iter=max_iter)
+        doc["search"][str(s)] = run_or_error(lambda: gp.search_plan(model, topo, groups, cfg))
+    doc["search_config"] = {"beam_width": beam_width, "max_iter": max_iter}
+    G.save(f"{name}.json", doc)
+    print(f"{name}: {time.time() - t:.1f}s", flush=True)
+
+
+def dump_c4(name, jitter):
+    gp = geopipe()
+    from oracle import oracle as O
+    spec = I.config("c4", jitter)
+    model, topo, groups = build_reference(spec)
+    doc = {"instance": G.instance_to_dict(model, topo, groups)}
+    packed = PackedInstance(model, topo, groups, 1.25)
+    total = O.space_size(packed)
+    idx = sorted(random.Random(4).sample(range(total), 20000))
+    cfg = gp.SearchConfig(seed=0)
+    t = time.time()
+    fg_ids = sorted(groups.fgs)
+    from geopipe.planner import Candidate
+    costs = []
+    for i in idx:
+        o, c, bm = O.decode(packed, i)
+        b = model.global_batch_candidates[bm // len(model.microbatch_candidates)]
+        m = model.microbatch_candidates[bm % len(model.microbatch_candidates)]
+        cand = Candidate(tuple(fg_ids[x] for x in o), tuple(int(x) for x in c))
+        costs.append(ref_cost(model, topo, groups, cand, b, m, cfg)[0])
+    costs = np.array(costs, dtype=np.float64)
+    # pin the oracle on this sample before trusting its full sweep
+    oc = []
+    for i in idx:
+        o, c, bm = O.decode(packed, i)
+        st, v = O.evaluate(packed, o, c, bm)
+        assert st == 0
+        oc.append(v)
+    oc = np.array(oc)
+    assert (oc.view(np.uint64) == costs.view(np.uint64)).all(), "oracle != reference on C4 sample"
+    np.save(os.path.join(G.GOLDEN, f"{name}.sample_idx.npy"), np.array(idx, dtype=np.uint64))
+    np.save(os.path.join(G.GOLDEN, f"{name}.sample_costs.npy"), costs)
+    print(f"{name}: sample {time.time() - t:.1f}s", flush=True)
+    t = time.time()
+    st, best = O.argmin_range(packed, 0, total, threads=os.cpu_count())
+    doc["oracle_argmin"] = {"status": st, "cost": best.cost, "index": best.index,
+                            "order": list(best.order[:best.k]),
+                            "counts": list(best.counts[:best.k]),
+                            "batch_index": best.batch_index, "micro_index": best.micro_index,
+                            "evaluated": total,
+                            "cpu_seconds_8threads": time.time() - t}
+    print(f"{name}: oracle argmin {time.time() - t:.1f}s", flush=True)
+    doc["search"] = {}
+    for s in (0, 1):
+        t = time.time()
+        doc["search"][str(s)] = run_or_error(
+            lambda: gp.search_plan(model, topo, groups, gp.SearchConfig(seed=s)))
+        print(f"{name}: search seed {s} {time.time() - t:.1f}s", flush=True)
+    doc["search_config"] = {"beam_width": 8, "max_iter": 20}
+    G.save(f"{name}.json", doc)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--skip-c4", action="store_true")
+    args = ap.parse_args()
+    if not AVAILABLE:
+        sys.exit("reference not available at /root/reference")
+    gp = geopipe()
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import conftest as rc  # reference test fixtures (read-only import)
+    os.makedirs(G.GOLDEN, exist_ok=True)
+
+    for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
+                                ("c2", "c2", False), ("c2j", "c2", True)]:
+        model, topo, groups = build_reference(I.config(cfg_name, jit))
+        dump_case(name, model, topo, groups, seeds=range(6))
+
+    # tests/test_planner.py small_setup
+    topo = rc.clique_topology([[4.0, 4.0], [2.0], [1.0]], intra=0.01, cross=0.5,
+                              bandwidth=1e8, latency=0.001)
+    groups = rc.make_groups(topo)
+    model = rc.uniform_model(6, flops=8.0, act_bytes=1e5, param_bytes=1e6,
+                             batches=(8,), micros=(2, 4))
+    dump_case("small", model, topo, groups, seeds=[2, 3, 5, 11])
+
+    # tests/test_acceptance.py:_random_instance (seeds with <= 4 groups)
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from test_acceptance import _random_instance
+    for seed in range(1, 16):
+        topo, groups, model = _random_instance(seed)
+        if len(groups.fgs) > 4:
+            continue
+        dump_case(f"rand{seed}", model, topo, groups, seeds=[seed], beam_width=16)
+
+    # error behaviour
+    topo = rc.clique_topology([[2.0], [1.0]], memory=10.0, bandwidth=1e8, latency=0.001)
+    groups = rc.make_groups(topo)
+    model = rc.uniform_model(4, param_bytes=1e9, batches=(4,), micros=(2,))
+    dump_case("err_memory", model, topo, groups, seeds=[0])
+
+    # zero intra-group bandwidth: one link of a 2-device clique carries 0 B/s
+    devs = [rc.device("a0", 1.0), rc.device("a1", 1.0), rc.device("b0", 1.0), rc.device("b1", 1.0)]
+    links = []
+    for u, v in itertools.combinations(devs, 2):
+        same = u.id[0] == v.id[0]
+        bw = (0.0 if (u.id, v.id) == ("a0", "a1") else 1e8) if same else 1e7
+        links.append(rc.link(u.id, v.id, 0.01 if same else 1.0, bandwidth=bw, latency=0.001))
+    topo = gp.build_topology(devs, links)
+    groups = rc.make_groups(topo)
+    model = rc.uniform_model(4, batches=(4,), micros=(2,))
+    dump_case("err_intra_bw", model, topo, groups, seeds=[0])
+
+    # zero-bandwidth gateway between the two groups
+    links = []
+    for u, v in itertools.combinations(devs, 2):
+        same = u.id[0] == v.id[0]
+        bw = 1e8 if same else (0.0 if (u.id, v.id) == ("a0", "b0") else 1e7)
+        pt = 0.01 if same else (0.5 if (u.id, v.id) == ("a0", "b0") else 1.0)
+        links.append(rc.link(u.id, v.id, pt, bandwidth=bw, latency=0.001))
+    topo = gp.build_topology(devs, links)
+    groups = rc.make_groups(topo)
+    dump_case("err_gateway", model, topo, groups, seeds=[0])
+
+    # single group (k = 1) and more groups than layers
+    topo = rc.clique_topology([[2.0, 1.0, 1.0]], bandwidth=1e8, latency=0.001)
+    groups = rc.make_groups(topo)
+    dump_case("single_fg", rc.uniform_model(5, batches=(4, 8), micros=(1, 2)), topo, groups,
+              seeds=[0, 1])
+    topo = rc.clique_topology([[1.0], [2.0], [4.0]], bandwidth=1e8, latency=0.001)
+    groups = rc.make_groups(topo)
+    dump_case("too_few_layers", rc.uniform_model(2, batches=(4,), micros=(2,)), topo, groups,
+              seeds=[0])
+
+    if not args.skip_c4:
+        dump_c4("c4", False)
+        dump_c4("c4j", True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+"""GPU parity: the CUDA engine (through the C-ABI) vs the reference's answers.
+
+Bar: bit-exact fp64 costs (including +inf for memory-infeasible plans and
+the reference's exception for erroring ones), identical chosen plans,
+splits, CostBreakdowns, traces and `evaluated` counts.  Reference answers
+come from tests/golden/ (scripts/make_golden.py) and, at C4 scale, from the
+oracle pinned there.
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from cases import CASES_ALL, enumerate_encoded, golden_costs, load_case, same_bits
+import paper_2505_15536_b200 as P
+from paper_2505_15536_b200.layout import PackedInstance
+
+pytestmark = pytest.mark.gpu
+
+ERRORS = {"NoFeasiblePlanError": P.NoFeasiblePlanError,
+          "InvalidTopologyError": P.InvalidTopologyError,
+          "DegenerateGroupError": P.DegenerateGroupError,
+          "InfeasibleSplitError": P.InfeasibleSplitError,
+          "InputFileError": P.InputFileError}
+
+
+def _load(engine, name):
+    doc, model, topo, groups = load_case(name)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    engine.load(packed)
+    return doc, model, topo, groups, packed
+
+
+# ---------------------------------------------------------------- K2 -------
+@pytest.mark.parametrize("name", CASES_ALL)
+def test_k2_every_candidate_bitwise(engine, name):
+    doc, model, topo, groups, packed = _load(engine, name)
+    order, counts, bm = enumerate_encoded(packed)
+    gc, gs = golden_costs(name)
+    if gc.size == 0:
+        return
+    cost, status = engine.eval_batch(order, counts, bm)
+    assert (status == gs).all(), np.nonzero(status != gs)[0][:10]
+    ok = same_bits(cost, gc)
+    assert ok.all(), (np.nonzero(~ok)[0][:10], cost[~ok][:5], gc[~ok][:5])
+
+
+@pytest.mark.parametrize("name", ["c4", "c4j"])
+def test_k2_c4_sample_bitwise(engine, oracle_lib, name):
+    doc, model, topo, groups, packed = _load(engine, name)
+    idx = np.load(f"{G.GOLDEN}/{name}.sample_idx.npy")
+    gc = np.load(f"{G.GOLDEN}/{name}.sample_costs.npy")
+    k = packed.n_fgs
+    order = np.zeros((idx.size, k), np.uint8)
+    counts = np.zeros((idx.size, k), np.uint8)
+    bm = np.zeros(idx.size, np.uint8)
+    for r, i in enumerate(idx):
+        order[r], counts[r], bm[r] = oracle_lib.decode(packed, int(i))
+    cost, status = engine.eval_batch(order, counts, bm)
+    assert (status == 0).all()
+    assert same_bits(cost, gc).all()
+
+
+def test_k2_rejects_bad_candidates(engine):
+    doc, model, topo, groups, packed = _load(engine, "c2")
+    order = np.array([[0, 0, 1], [0, 1, 7], [0, 1, 2], [0, 1, 2]], np.uint8)
+    counts = np.array([[10, 10, 12], [10, 10, 12], [10, 0, 22], [10, 10, 12]], np.uint8)
+    bm = np.array([0, 0, 0, 200], np.uint8)
+    cost, status = engine.eval_batch(order, counts, bm)
+    assert list(status) == [1, 1, 1, 1]
+    assert np.isnan(cost).all()
+
+
+# ---------------------------------------------------------------- K3 -------
+def _key_argmin(packed, gc, gs, lo, hi, order, counts, bm):
+    best = None
+    for i in range(lo, hi):
+        if gs[i]:
+            return ("error", int(gs[i]))
+        key = (gc[i], tuple(order[i]), tuple(counts[i]), int(bm[i]))
+        if best is None or key < best[0]:
+            best = (key, i)
+    return best
+
+
+@pytest.mark.parametrize("name", ["c1", "c1j", "c2", "c2j", "rand5", "rand10", "small"])
+def test_k3_random_subranges(engine, name):
+    doc, model, topo, groups, packed = _load(engine, name)
+    gc, gs = golden_costs(name)
+    order, counts, bm = enumerate_encoded(packed)
+    N = gc.size
+    rng = random.Random(7)
+    ranges = [(0, N), (0, 1), (N - 1, N)] + \
+        [tuple(sorted(rng.sample(range(N + 1), 2))) for _ in range(12)]
+    for lo, hi in ranges:
+        if hi <= lo:
+            continue
+        exp = _key_argmin(packed, gc, gs, lo, hi, order, counts, bm)
+        got = engine.argmin_range(lo, hi)
+        assert got.index == exp[1], (lo, hi)
+        assert same_bits(got.cost, gc[exp[1]])
+        assert got.evaluated == hi - lo
+
+
+@pytest.mark.parametrize("name", CASES_ALL)
+def test_exhaustive_plan_matches_reference(engine, name):
+    doc, model, topo, groups = load_case(name)
+    ex = doc["exhaustive"]
+    cfg = P.SearchConfig(seed=0, beam_width=doc["search_config"]["beam_width"],
+                         max_iter=doc["search_config"]["max_iter"])
+    if "error" in ex:
+        with pytest.raises(ERRORS[ex["error"]]):
+            P.exhaustive_plan(model, topo, groups, cfg, engine=engine)
+        return
+    res = P.exhaustive_plan(model, topo, groups, cfg, engine=engine)
+    assert G.normalize_result(res) == ex["result"]
+
+
+@pytest.mark.parametrize("name", ["c4", "c4j"])
+def test_k3_c4_full_argmin(engine, name):
+    doc, model, topo, groups, packed = _load(engine, name)
+    total = engine.space_size()
+    assert total == 11_387_376
+    got = engine.argmin_range(0, total)
+    exp = doc["oracle_argmin"]
+    assert got.index == exp["index"]
+    assert got.cost == exp["cost"]
+    assert list(got.order[:got.k]) == exp["order"]
+    assert list(got.counts[:got.k]) == exp["counts"]
+
+
+# ---------------------------------------------------------- search_plan ----
+SEARCH_CASES = [(n, s) for n in CASES_ALL + ["c4", "c4j"]
+                for s in G.load(f"{n}.json")["search"]]
+
+
+@pytest.mark.parametrize("name,seed", SEARCH_CASES)
+def test_search_plan_matches_reference(engine, name, seed):
+    doc, model, topo, groups = load_case(name)
+    exp = doc["search"][seed]
+    cfg = P.SearchConfig(seed=int(seed), beam_width=doc["search_config"]["beam_width"],
+                         max_iter=doc["search_config"]["max_iter"])
+    if "error" in exp:
+        with pytest.raises(ERRORS[exp["error"]]):
+            P.search_plan(model, topo, groups, cfg, engine=engine)
+        return
+    res = P.search_plan(model, topo, groups, cfg, engine=engine)
+    assert G.normalize_result(res) == exp["result"]

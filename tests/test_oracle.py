@@ -1,0 +1,197 @@
+"""The oracle (oracle/oracle.c) pinned against the reference.
+
+CPU-only.  Pinning sources:
+  * the committed fixtures in tests/golden/ (generated from the unmodified
+    reference by scripts/make_golden.py) - every candidate cost bitwise;
+  * the reference's own KATs for the split algebra (tests/test_planner.py:25-82);
+  * the live reference when /root/reference exists (randomized instances).
+"""
+
+import itertools
+import math
+import random
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from cases import CASES_ALL, enumerate_encoded, golden_costs, load_case, same_bits
+from paper_2505_15536_b200.layout import PackedInstance
+import refbridge
+
+
+# ---------------------------------------------------------------- psum -----
+def test_psum_matches_builtin_sum(oracle_lib):
+    rng = random.Random(12345)
+    for trial in range(3000):
+        n = rng.randint(1, 40)
+        scale = 10.0 ** rng.randint(-5, 15)
+        xs = [rng.uniform(0.0, 1.0) * scale * (10.0 ** rng.randint(-8, 8)) for _ in range(n)]
+        if trial % 3 == 0:
+            xs = [x * rng.choice([1.0, -1.0]) for x in xs]
+        assert oracle_lib.psum(xs) == sum(xs), xs
+
+
+def test_psum_kat_compensation(oracle_lib):
+    # Neumaier vs naive fold differ here (CPython 3.12 sum is compensated)
+    xs = [1e16, 1.0, -1e16]
+    assert oracle_lib.psum(xs) == sum(xs) == 1.0
+
+
+# ------------------------------------------------ reference split KATs -----
+# tests/test_planner.py:25-82 of the reference
+def test_proportional_split_kats(oracle_lib):
+    ps = oracle_lib.proportional_split
+    assert ps(6, [1.0, 1.0], 1) == [3, 3]
+    assert ps(6, [1.0, 2.0], 1) == [2, 4]
+    assert ps(5, [2.0, 3.0], 1) == [2, 3]
+    assert ps(3, [100.0, 1.0, 1.0], 1) == [1, 1, 1]
+    for total, w in [(7, [1, 2, 4]), (9, [5, 3, 1]), (4, [1, 1, 1, 1])]:
+        assert sum(ps(total, [float(x) for x in w], 1)) == total
+    from paper_2505_15536_b200.domain import InfeasibleSplitError
+    with pytest.raises(InfeasibleSplitError):
+        ps(2, [1.0, 1.0, 1.0], 1)
+
+
+def test_dp_fraction_kats(oracle_lib):
+    assert oracle_lib.dp_fractions([1.0, 2.0]) == pytest.approx([1 / 3, 2 / 3])
+    assert oracle_lib.dp_fractions([1.0, 2.0, 2.0]) == pytest.approx([0.2, 0.4, 0.4])
+    assert sum(oracle_lib.dp_fractions([1.0, 1.0, 1.0])) == 1.0
+
+
+def test_tp_grid_kats(oracle_lib):
+    tiles = oracle_lib.tp_grid([1.0, 2.0, 2.0, 4.0])
+    assert tiles == pytest.approx([(1 / 3, 1 / 3), (2 / 3, 1 / 3), (1 / 3, 2 / 3), (2 / 3, 2 / 3)])
+    assert oracle_lib.tp_grid([1.0] * 4) == pytest.approx([(0.5, 0.5)] * 4)
+    assert oracle_lib.tp_grid([1.0, 1.0, 2.0]) is None
+
+
+# -------------------------------------------------------- golden costs -----
+@pytest.mark.parametrize("name", CASES_ALL)
+def test_oracle_all_candidates_bitwise(oracle_lib, name):
+    doc, model, topo, groups = load_case(name)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    order, counts, bm = enumerate_encoded(packed)
+    gc, gs = golden_costs(name)
+    assert order.shape[0] == gc.size
+    if gc.size == 0:
+        return
+    cost, status = oracle_lib.eval_batch(packed, order, counts, bm, threads=4)
+    assert (status == gs).all()
+    assert same_bits(cost, gc).all()
+
+
+@pytest.mark.parametrize("name", ["c4", "c4j"])
+def test_oracle_c4_sample_bitwise(oracle_lib, name):
+    doc, model, topo, groups = load_case(name)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    idx = np.load(f"{G.GOLDEN}/{name}.sample_idx.npy")
+    gc = np.load(f"{G.GOLDEN}/{name}.sample_costs.npy")
+    k = packed.n_fgs
+    order = np.zeros((idx.size, k), np.uint8)
+    counts = np.zeros((idx.size, k), np.uint8)
+    bm = np.zeros(idx.size, np.uint8)
+    for r, i in enumerate(idx[:3000]):
+        order[r], counts[r], bm[r] = oracle_lib.decode(packed, int(i))
+    cost, status = oracle_lib.eval_batch(packed, order[:3000], counts[:3000], bm[:3000], 4)
+    assert (status == 0).all()
+    assert same_bits(cost, gc[:3000]).all()
+
+
+@pytest.mark.parametrize("name", CASES_ALL)
+def test_oracle_exhaustive_argmin(oracle_lib, name):
+    doc, model, topo, groups = load_case(name)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    st, best = oracle_lib.argmin_range(packed, 0, oracle_lib.space_size(packed), threads=4)
+    ex = doc["exhaustive"]
+    if "error" in ex:
+        if ex["error"] == "NoFeasiblePlanError":
+            # either every candidate is infeasible (winner infeasible) or empty space
+            if st == 0:
+                _, _, info = oracle_lib.evaluate(packed, best.order[:best.k],
+                                                 best.counts[:best.k],
+                                                 best.batch_index * len(packed.micros)
+                                                 + best.micro_index, detail=True)
+                assert not info.feasible
+            else:
+                assert st == 3
+        else:
+            assert st != 0
+        return
+    r = ex["result"]
+    assert st == 0
+    assert best.cost == r["breakdown"]["plan_cost"]
+    stages = r["plan"]["stages"]
+    assert [packed.fg_ids[x] for x in best.order[:best.k]] == [s[0] for s in stages]
+    assert list(best.counts[:best.k]) == [s[2] - s[1] for s in stages]
+    assert packed.batches[best.batch_index] == r["plan"]["batch_b"]
+    assert packed.micros[best.micro_index] == r["plan"]["microbatch_m"]
+
+
+# ------------------------------------------------------ live reference -----
+def _random_instance(rng):
+    """Heterogeneous random instance with jittered (non-integer) tables."""
+    gp = refbridge.geopipe()
+    from geopipe.timing import GroupIndex
+    n_cl = rng.randint(2, 4)
+    devs, links = [], []
+    clique = {}
+    for c in range(n_cl):
+        for j in range(rng.randint(1, 4)):
+            p = rng.choice([1e14, 3.3e14, 7e13, 2.2e15]) * rng.uniform(0.95, 1.05)
+            d = gp.DeviceSpec(id=f"c{c}d{j}", memory_bytes=rng.choice([8e9, 24e9, 80e9]),
+                              benchmark_times=(("b", 1.0 / p),))
+            devs.append(d)
+            clique[d.id] = c
+    for u, v in itertools.combinations(devs, 2):
+        same = clique[u.id] == clique[v.id]
+        bw = (rng.uniform(1e9, 5e10) if same else rng.uniform(1e7, 1e8))
+        lat = rng.uniform(1e-5, 1e-3) if same else rng.uniform(0.01, 0.05)
+        links.append(gp.LinkMeasurement(endpoints=frozenset((u.id, v.id)),
+                                        alpha_seconds=1e8 / bw, beta_seconds=lat,
+                                        payload_bytes_m=1e8, latency_seconds=lat,
+                                        bandwidth_bytes_per_s=bw))
+    topo = gp.build_topology(devs, links)
+    fgs = gp.group_first_level(topo, 0.3)
+    sgs = {fg.id: gp.group_second_level(fg, topo, 0.3) for fg in fgs}
+    groups = GroupIndex.build(fgs, sgs)
+    n = rng.randint(max(len(fgs), 3), 20)
+    layers = tuple(gp.LayerSpec(*(rng.uniform(1e12, 1e14) for _ in range(3)),
+                                rng.uniform(1e6, 1e8), rng.uniform(1e8, 4e9)) for _ in range(n))
+    model = gp.ModelSpec(layers=layers, global_batch_candidates=(64, 128),
+                         microbatch_candidates=(4, 8, 16))
+    return model, topo, groups
+
+
+@pytest.mark.skipif(not refbridge.AVAILABLE, reason="reference not present")
+def test_oracle_vs_live_reference_random(oracle_lib):
+    gp = refbridge.geopipe()
+    from geopipe.planner import Candidate, _evaluate
+    rng = random.Random(99)
+    checked = 0
+    for inst in range(25):
+        model, topo, groups = _random_instance(rng)
+        if len(groups.fgs) > 6:
+            continue
+        packed = PackedInstance(model, topo, groups, 1.25)
+        cfg = gp.SearchConfig(seed=0)
+        fg_ids = sorted(groups.fgs)
+        for _ in range(60):
+            order = list(fg_ids)
+            rng.shuffle(order)
+            k, n = len(order), model.num_layers
+            cuts = sorted(rng.sample(range(1, n), k - 1))
+            counts = tuple(b - a for a, b in zip([0] + cuts, cuts + [n]))
+            bi, mi = rng.randrange(2), rng.randrange(3)
+            b, m = model.global_batch_candidates[bi], model.microbatch_candidates[mi]
+            try:
+                ref = _evaluate(Candidate(tuple(order), counts), b, m, groups, topo, model,
+                                cfg, {})[0]
+            except Exception:
+                continue
+            st, mine = oracle_lib.evaluate(packed, [packed.fg_pos[f] for f in order],
+                                           counts, bi * 3 + mi)
+            assert st == 0
+            assert mine == ref or (math.isnan(mine) and math.isnan(ref))
+            checked += 1
+    assert checked > 500
