@@ -57,6 +57,9 @@ static int fail(int code, const char* fmt, ...) {
 enum : uint8_t { SC_OK = 0, SC_INFEASIBLE = 1, SC_DEGENERATE = 4, SC_TOPOLOGY = 5 };
 // context flags that force the generic (status-tracking) range kernel
 enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 4 };
+#define K3_THREADS 256
+#define K3_TILE 256
+#define BINOM_ROWS 257
 
 // ----------------------------------------------------------------------------
 // device-side view of one loaded instance
@@ -87,7 +90,10 @@ struct DevInst {
     uint8_t* skind;              // [F][(n+1)^2]
     double* C1;                  // [F][(n+1)^2] per-sample (F+Bi)+W (detail)
     int* gw;                     // [F*F] gateway u*D+v
-    double* xt;                  // [nm][F][F][n]
+    double* xt;                  // [nm][F][F][nxp] (rows padded to 16 B)
+    int nxp;                     // x row stride: n rounded up to even
+    double2* tpk;                // [nm][F][n(n+1)/2] packed rows a: b = a+1..n
+    double2* tcol;               // [nm][F][n+1] entry (q, n) at q
     uint32_t* flags;             // [1]
 };
 
@@ -214,8 +220,10 @@ __global__ void k1_stages(DevInst I) {
         I.scode[e] = SC_INFEASIBLE;
         I.skind[e] = 0;
         I.C1[e] = INFINITY;
-        for (int mi = 0; mi < I.nm; ++mi)
+        for (int mi = 0; mi < I.nm; ++mi) {
             I.stg[(size_t)mi * I.F * N2 + e] = make_double2(INFINITY, 0.0);
+            if (a == n && b == n) I.tcol[((size_t)mi * I.F + f) * (n + 1) + n] = make_double2(INFINITY, 0.0);
+        }
         return;
     }
     int shares[GP_MAX_SGS], np;
@@ -285,7 +293,11 @@ __global__ void k1_stages(DevInst I) {
         }
         double cm = c1 * md;
         if (feas && isinf(cm)) overflow = true;
-        I.stg[(size_t)mi * I.F * N2 + e] = make_double2(feas ? cm : INFINITY, al);
+        double2 v = make_double2(feas ? cm : INFINITY, al);
+        I.stg[(size_t)mi * I.F * N2 + e] = v;
+        size_t ntri = (size_t)n * (n + 1) / 2;
+        I.tpk[((size_t)mi * I.F + f) * ntri + (a * n - a * (a - 1) / 2) + (b - a - 1)] = v;
+        if (b == n) I.tcol[((size_t)mi * I.F + f) * (n + 1) + a] = v;
     }
     I.scode[e] = feas ? code : SC_INFEASIBLE;
     if (feas && code != SC_OK) atomicOr(I.flags, FLAG_STAGE_ERROR);
@@ -330,7 +342,7 @@ __global__ void k1_boundary(DevInst I) {
     int g = I.gw[pair];
     double md = (double)I.micro[mi];
     // transfer_seconds: latency + (act*m)/bandwidth (src/timing.py:91-97)
-    I.xt[t] = I.lat[g] + (I.act[j] * md) / I.bw[g];
+    I.xt[(size_t)r * I.nxp + j] = I.lat[g] + (I.act[j] * md) / I.bw[g];
 }
 
 // ----------------------------------------------------------------------------
@@ -362,7 +374,7 @@ __device__ EvalOut eval_tables(const DevInst& I, int k, const uint8_t* order, co
         if (!(I.bw[g] > 0)) { out.status = GP_ERR_TOPOLOGY; return out; }
     }
     const double2* T = I.stg + (size_t)mi * I.F * N2;
-    const double* X = I.xt + (size_t)mi * I.F * I.F * n;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
     double Md = (double)M;
     double fill = 0.0, res = 0.0, best = 0.0, xprev = 0.0;
     for (int s = 0; s < k; ++s) {
@@ -372,7 +384,7 @@ __device__ EvalOut eval_tables(const DevInst& I, int k, const uint8_t* order, co
         double total = ((fill + Md * c) + res) + e.y;
         best = (s == 0 || total > best) ? total : best;
         if (s + 1 < k) {
-            double x = X[((size_t)order[s] * I.F + order[s + 1]) * n + (p[s + 1] - 1)];
+            double x = X[((size_t)order[s] * I.F + order[s + 1]) * I.nxp + (p[s + 1] - 1)];
             fill = fill + (c + x);
             xprev = x;
         }
@@ -418,9 +430,11 @@ struct RangeGeom {
     unsigned long long NC;   // C(n-1, k-1)
     unsigned long long NP;   // k!
     unsigned long long lo, hi;
-    unsigned long long item0;          // first (bm, perm) item touched
-    unsigned long long chunks_per_item;
-    unsigned long long chunk;          // comps per CTA
+    unsigned long long item0;          // first item touched
+    unsigned long long chunks_per_item;  // CTAs sharing one item
+    unsigned long long chunk;          // (generic kernel: unused)
+    unsigned int* item_ctr;            // per-item tile counters (zeroed per launch)
+    const uint8_t* tiles;              // cut positions at every K3_TILE-th rank, or null
 };
 
 __device__ unsigned long long d_binom(int n, int r) {
@@ -528,122 +542,316 @@ __device__ void block_argmin_finish(Key mine, const ArgminScratch& S) {
     }
 }
 
-// Fast path: all stage entries error-free.  CTA = (item, chunk); item =
-// (bm, perm).  The last two stages vary with the last cut; stage k-2's
-// {C1*m, AL} triangle for this m sits in shared memory.
-template <bool SMEM>
-__global__ void __launch_bounds__(256) k3_argmin(DevInst I, RangeGeom G, ArgminScratch S) {
-    extern __shared__ double2 smem2[];
+// Fast path (all stage entries error-free, k >= 3).
+//
+// CTA = (item, chunk) with item = (bm, order); its comp ranks are split into
+// contiguous per-warp ranges and each warp sweeps its range in windows of 32
+// consecutive ranks (lane j takes rank r0 + j), so all lanes run the same
+// instruction stream.  A candidate = prefix cuts p[1..k-3] (stages 0..k-4,
+// folded once into per-lane scalars and refreshed only when a lane crosses
+// into the next prefix) plus the pair (a, q) = (p[k-2], p[k-1]) that bounds
+// the last three stages:
+//     stage k-3 = [p[k-3], a)   table T1 = {C1*m, AL} of group order[k-3]
+//     stage k-2 = [a, q)        table T2 of group order[k-2]
+//     stage k-1 = [q, n)        column of group order[k-1]
+// MODE 2: T1 and T2 triangles, the column and both boundary rows in shared
+// memory; MODE 1: T1 from L1/L2; MODE 0: everything from L1/L2.
+__device__ __forceinline__ int rowoff(int n, int a) { return a * n - a * (a - 1) / 2; }
+
+// lexicographic successor of the prefix cuts p[1..k-3] (p_j <= n - k + j)
+__device__ __forceinline__ bool next_prefix(int* p, int n, int k) {
+    int j = k - 3;
+    while (j >= 1 && p[j] >= n - k + j) --j;
+    if (j < 1) return false;
+    ++p[j];
+    for (int t = j + 1; t <= k - 3; ++t) p[t] = p[t - 1] + 1;
+    return true;
+}
+
+// advance (prefix, a, q) by s ranks; returns false past the last pair
+__device__ __forceinline__ bool advance_pair(int* p, int& a, int& q, int s, int n, int k,
+                                             bool& dirty) {
+    q += s;
+    while (q > n - 1) {
+        int o = q - (n - 1);
+        ++a;
+        if (a > n - 2) {
+            if (k < 4 || !next_prefix(p, n, k)) return false;
+            a = p[k - 3] + 1;
+            dirty = true;
+        }
+        q = a + o;
+    }
+    return true;
+}
+
+// max(0.0, x) as DSETP + 2 SEL (x > 0 ? x : +0.0, NaN -> +0.0 like Python)
+__device__ __forceinline__ double max0f(double x) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, 0d0000000000000000;\n\t"
+        "selp.f64 %0, %1, 0d0000000000000000, p;\n\t}" : "=d"(r) : "d"(x));
+    return r;
+}
+// a > b ? a : b (first-max; no NaNs occur)
+__device__ __forceinline__ double gtsel(double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+        : "=d"(r) : "d"(a), "d"(b));
+    return r;
+}
+
+// ---- TMA (bulk async copy) helpers ----------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
+// CTA group = item = (micro-batch index mi, order); chunks_per_item CTAs
+// share an item and pull K3_TILE-rank tiles of its composition space from a
+// per-item atomic counter (dynamic balance across warps and CTAs).  Every
+// candidate (order, cuts, m) is evaluated for all NB batch sizes at once:
+// the tables {C1*m, AL} and x depend on m only, and the fill / residual
+// chains do not depend on the batch size, so only the M*c terms and the
+// totals are per batch (tie order (cost, order, cuts, b) is kept by
+// scanning batch sizes innermost).
+//
+// Staging: one elected thread moves the packed stage-table triangles, the
+// last-stage column, stage 0's row and the boundary rows HBM/L2 -> shared
+// memory with bulk async copies (TMA, cp.async.bulk) on one mbarrier.
+template <int MODE, int NB>
+__global__ void __launch_bounds__(K3_THREADS, 2) k3_argmin(DevInst I, RangeGeom G, ArgminScratch S,
+                                                           const unsigned long long* __restrict__ binom) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = I.n, k = G.k;
-    const size_t N2 = (size_t)(n + 1) * (n + 1);
-    unsigned long long item = G.item0 + blockIdx.x / G.chunks_per_item;
-    unsigned long long cidx = blockIdx.x % G.chunks_per_item;
-    unsigned long long base = item * G.NC;
-    unsigned long long c_lo = cidx * G.chunk, c_hi = c_lo + G.chunk;
-    if (c_hi > G.NC) c_hi = G.NC;
-    // clip to [lo, hi)
-    if (base + c_lo < G.lo) c_lo = G.lo > base ? G.lo - base : 0;
-    if (base + c_hi > G.hi) c_hi = G.hi > base ? G.hi - base : 0;
-    Key mine{INFINITY, ~0ull};
-    int bmi = (int)(item / G.NP);
-    unsigned long long perm_rank = item % G.NP;
+    const int ntri = n * (n + 1) / 2;
+    const int KB = k + 1;  // binomial sub-table columns r = 0..k
+    const unsigned long long islot = blockIdx.x / G.chunks_per_item;
+    const unsigned long long item = G.item0 + islot;  // mi * NP + perm
+    const int mi = (int)(item / G.NP);
+    const unsigned long long perm_rank = item % G.NP;
+    // per-batch clip of [0, NC) against [lo, hi)
+    unsigned long long blo[NB], bhi[NB];
+    unsigned long long u_lo = ~0ull, u_hi = 0;
+    bool all_in = true;
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi) {
+        unsigned long long base = (((unsigned long long)bi * I.nm + mi) * G.NP + perm_rank) * G.NC;
+        unsigned long long l = 0, h = G.NC;
+        if (base + l < G.lo) l = G.lo - base < h ? G.lo - base : h;
+        if (base + h > G.hi) h = G.hi > base + l ? G.hi - base : l;
+        blo[bi] = l;
+        bhi[bi] = h;
+        if (l != 0 || h != G.NC) all_in = false;
+        if (l < h) { u_lo = l < u_lo ? l : u_lo; u_hi = h > u_hi ? h : u_hi; }
+    }
     uint8_t order[GP_MAX_STAGES];
     d_unrank_perm(k, perm_rank, order);
-    const int mi = bmi % I.nm;
-    const double Md = (double)(I.batch[bmi / I.nm] / I.micro[mi]);
+    double Mv[NB];
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[bi] / I.micro[mi]);
+    const size_t N2 = (size_t)(n + 1) * (n + 1);
     const double2* T = I.stg + (size_t)mi * I.F * N2;
-    const double* X = I.xt + (size_t)mi * I.F * I.F * n;
-    const int f2 = order[k - 2], f3 = order[k - 1];
-    const double2* T2 = T + (size_t)f2 * N2;
-    const double2* T3 = T + (size_t)f3 * N2;
-    const double* X23 = X + ((size_t)f2 * I.F + f3) * n;
-    // shared: stage k-2 triangle rows [a][a+1..n], then column of stage k-1
-    double2* tri = smem2;
-    double2* col = smem2 + (SMEM ? (size_t)n * (n + 1) / 2 : 0);
-    double* xs = (double*)(col + n);
-    if (SMEM) {
-        // dense [a][b] -> packed rows (row a holds b = a+1..n)
-        for (int t = threadIdx.x; t < n * (n + 1); t += blockDim.x) {
-            int a = t / (n + 1), b = t % (n + 1);
-            if (b > a) tri[a * n - a * (a - 1) / 2 + (b - a - 1)] = T2[t];
+    const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
+    const int f1 = order[k - 3], f2 = order[k - 2], f3 = order[k - 1];
+    const double2* P0 = I.tpk + ((size_t)mi * I.F + order[0]) * ntri;  // row 0 = first n
+    const double2* P1 = I.tpk + ((size_t)mi * I.F + f1) * ntri;
+    const double2* P2 = I.tpk + ((size_t)mi * I.F + f2) * ntri;
+    const double2* C3 = I.tcol + ((size_t)mi * I.F + f3) * (n + 1);
+    const double* X01 = X + ((size_t)order[0] * I.F + order[1]) * I.nxp;
+    const double* X12 = X + ((size_t)f1 * I.F + f2) * I.nxp;
+    const double* X23 = X + ((size_t)f2 * I.F + f3) * I.nxp;
+
+    // shared: mbarrier | binom | T2 | col | x12 | x23 | row0 | x01 | T1
+    uint64_t* bar = (uint64_t*)smem_raw;
+    unsigned long long* bn = (unsigned long long*)(smem_raw + 16);
+    unsigned char* tail = smem_raw + 16 + (((size_t)(n + 1) * KB * 8 + 15) & ~(size_t)15);
+    double2* tri2 = (double2*)tail;
+    double2* col3 = tri2 + (MODE >= 1 ? ntri : 0);
+    double* x12s = (double*)(col3 + (MODE >= 1 ? n + 1 : 0));
+    double* x23s = x12s + (MODE >= 1 ? I.nxp : 0);
+    double2* row0 = (double2*)(x23s + (MODE >= 1 ? I.nxp : 0));
+    double* x01s = (double*)(row0 + (MODE >= 1 ? n : 0));
+    double2* tri1 = (double2*)(x01s + (MODE >= 1 ? I.nxp : 0));
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        if (MODE >= 1) {
+            uint32_t bytes = (uint32_t)(ntri * 16 + (n + 1) * 16 + 3 * I.nxp * 8 + n * 16) +
+                             (MODE == 2 ? (uint32_t)ntri * 16 : 0u);
+            mbar_expect_tx(bar, bytes);
+            tma_bulk_g2s(tri2, P2, (uint32_t)ntri * 16, bar);
+            tma_bulk_g2s(col3, C3, (uint32_t)(n + 1) * 16, bar);
+            tma_bulk_g2s(x12s, X12, (uint32_t)I.nxp * 8, bar);
+            tma_bulk_g2s(x23s, X23, (uint32_t)I.nxp * 8, bar);
+            tma_bulk_g2s(row0, P0, (uint32_t)n * 16, bar);
+            tma_bulk_g2s(x01s, X01, (uint32_t)I.nxp * 8, bar);
+            if (MODE == 2) tma_bulk_g2s(tri1, P1, (uint32_t)ntri * 16, bar);
         }
-        for (int t = threadIdx.x; t < n; t += blockDim.x) {
-            col[t] = T3[tri_idx(n, t, n)];
-            xs[t] = X23[t];
-        }
-        __syncthreads();
     }
-    if (c_lo < c_hi) {
-        unsigned long long span = c_hi - c_lo;
-        unsigned long long t0 = c_lo + span * threadIdx.x / blockDim.x;
-        unsigned long long t1 = c_lo + span * (threadIdx.x + 1) / blockDim.x;
-        if (t0 < t1) {
-            int p[GP_MAX_STAGES + 1];
-            d_unrank_cuts(n, k, t0, p);
-            unsigned long long ci = t0;
-            double best_cost = INFINITY;
-            unsigned long long best_ci = ~0ull;
-            bool have = false;
-            while (ci < t1) {
-                // prefix: stages 0..k-3 on cuts p[0..k-2]
-                double fill = 0.0, res = 0.0, mx = -INFINITY, xprev = 0.0;
-                for (int s = 0; s + 2 < k; ++s) {
-                    double2 e = __ldg(&T[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])]);
-                    if (s > 0) res = res + gpd::max0(xprev - e.x);
-                    double tot = ((fill + Md * e.x) + res) + e.y;
-                    mx = (s == 0 || tot > mx) ? tot : mx;
-                    double x = __ldg(&X[((size_t)order[s] * I.F + order[s + 1]) * n + (p[s + 1] - 1)]);
-                    fill = fill + (e.x + x);
-                    xprev = x;
+    for (int t = threadIdx.x; t < (n + 1) * KB; t += blockDim.x)
+        bn[t] = binom[(t / KB) * (GP_MAX_STAGES + 1) + (t % KB)];
+    __syncthreads();
+    if (MODE >= 1) mbar_wait(bar, 0);
+
+    Key mine{INFINITY, ~0ull};
+    const int lane = threadIdx.x & 31;
+    double best_c = INFINITY;
+    unsigned long long best_t = ~0ull;  // rank * NB + bi
+    if (u_lo < u_hi) {
+        const unsigned long long tile_lo = u_lo / K3_TILE;
+        const unsigned long long ntiles = (u_hi + K3_TILE - 1) / K3_TILE - tile_lo;
+        int p[GP_MAX_STAGES + 1];
+        p[0] = 0;
+        for (;;) {
+            unsigned int t = 0;
+            if (lane == 0) t = atomicAdd(&G.item_ctr[islot], 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= ntiles) break;
+            const unsigned long long rank0 = (tile_lo + t) * K3_TILE;
+            // cut positions of rank0: precomputed tile table or ballot decode
+            if (G.tiles) {
+                const uint8_t* tp = G.tiles + (rank0 / K3_TILE) * 16;
+                for (int j = 1; j < k; ++j) p[j] = tp[j - 1];
+            } else {
+                // for cut j pick the smallest q with C(n-q-1, r+1) <
+                // C(n-lo, r+1) - rem (hockey stick), 32 candidates per ballot
+                unsigned long long rem = rank0;
+                int prev = 0;
+                for (int j = 1; j < k; ++j) {
+                    const int r = k - 1 - j, lo = prev + 1;
+                    const unsigned long long tot = bn[(n - lo) * KB + r + 1];
+                    const unsigned long long thr = tot - rem;
+                    int qsel = -1;
+                    for (int base = lo; qsel < 0; base += 32) {
+                        int qq = base + lane;
+                        bool ok = qq <= n - 1 - r && bn[(n - qq - 1) * KB + r + 1] < thr;
+                        unsigned m = __ballot_sync(0xffffffffu, ok);
+                        if (m) qsel = base + __ffs(m) - 1;
+                    }
+                    rem -= tot - bn[(n - qsel) * KB + r + 1];
+                    p[j] = qsel;
+                    prev = qsel;
                 }
-                const int a = p[k - 2];
-                const int rowoff = a * n - a * (a - 1) / 2;  // sum_{a'<a} (n - a')
-                // sweep the last cut q = p[k-1] in (a, n)
-                int q = p[k - 1];
-                unsigned long long run = (unsigned long long)(n - q);
-                if (run > t1 - ci) run = t1 - ci;
-                for (unsigned long long r = 0; r < run; ++r, ++q) {
-                    double2 e2, e3;
-                    double x2;
-                    if (SMEM) {
-                        e2 = tri[rowoff + (q - a - 1)];
-                        e3 = col[q];
-                        x2 = xs[q - 1];
+            }
+            int a = p[k - 2], q = p[k - 1];
+            bool dirty = true;
+            const int tlen = (int)((rank0 + K3_TILE <= u_hi ? K3_TILE : u_hi - rank0));
+            int rl = lane;  // rank within the tile
+            bool live = rl < tlen && advance_pair(p, a, q, lane, n, k, dirty);
+            double fill = 0.0, res = 0.0, xprev = 0.0;
+            double mx[NB];
+            int base1 = 0, base2 = 0, a_cached = -1;
+            while (__any_sync(0xffffffffu, live)) {
+                if (live) {
+                    if (dirty) {
+                        dirty = false;
+                        fill = 0.0; res = 0.0; xprev = 0.0;
+#pragma unroll
+                        for (int bi = 0; bi < NB; ++bi) mx[bi] = -INFINITY;
+                        for (int s = 0; s + 3 < k; ++s) {
+                            double2 e;
+                            double x;
+                            if (MODE >= 1 && s == 0) {
+                                e = row0[p[1] - 1];
+                                x = x01s[p[1] - 1];
+                            } else {
+                                e = __ldg(&T[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])]);
+                                x = __ldg(&X[((size_t)order[s] * I.F + order[s + 1]) * I.nxp + (p[s + 1] - 1)]);
+                            }
+                            if (s > 0) res = res + max0f(xprev - e.x);
+#pragma unroll
+                            for (int bi = 0; bi < NB; ++bi) {
+                                double tot = ((fill + Mv[bi] * e.x) + res) + e.y;
+                                mx[bi] = (s == 0) ? tot : gtsel(tot, mx[bi]);
+                            }
+                            fill = fill + (e.x + x);
+                            xprev = x;
+                        }
+                        const int pk3 = p[k - 3];
+                        base1 = rowoff(n, pk3) - pk3 - 1;
+                        a_cached = -1;
+                    }
+                    if (a != a_cached) {
+                        a_cached = a;
+                        base2 = rowoff(n, a) - a - 1;
+                    }
+                    double2 e1, e2, e3;
+                    double x1, x2;
+                    if (MODE == 2) e1 = tri1[base1 + a];
+                    else e1 = __ldg(&P1[base1 + a]);
+                    if (MODE >= 1) {
+                        e2 = tri2[base2 + q];
+                        e3 = col3[q];
+                        x1 = x12s[a - 1];
+                        x2 = x23s[q - 1];
                     } else {
-                        e2 = __ldg(&T2[tri_idx(n, a, q)]);
-                        e3 = __ldg(&T3[tri_idx(n, q, n)]);
+                        e2 = __ldg(&P2[base2 + q]);
+                        e3 = __ldg(&C3[q]);
+                        x1 = __ldg(&X12[a - 1]);
                         x2 = __ldg(&X23[q - 1]);
                     }
-                    double res2 = (k > 2) ? res + gpd::max0(xprev - e2.x) : res;
-                    double t2 = ((fill + Md * e2.x) + res2) + e2.y;
-                    double fill3 = fill + (e2.x + x2);
-                    double res3 = res2 + gpd::max0(x2 - e3.x);
-                    double t3 = ((fill3 + Md * e3.x) + res3) + e3.y;
-                    double c = (k > 2) ? mx : t2;
-                    c = (k > 2 && t2 > c) ? t2 : c;
-                    c = t3 > c ? t3 : c;
-                    if (!have || c < best_cost) {
-                        best_cost = c;
-                        best_ci = ci + r;
-                        have = true;
+                    // batch-independent chains (src/costmodel.py:68-81)
+                    const double res1 = (k > 3) ? res + max0f(xprev - e1.x) : res;
+                    const double fill2 = fill + (e1.x + x1);
+                    const double res2 = res1 + max0f(x1 - e2.x);
+                    const double fill3 = fill2 + (e2.x + x2);
+                    const double res3 = res2 + max0f(x2 - e3.x);
+                    const unsigned long long rabs = rank0 + rl;
+#pragma unroll
+                    for (int bi = 0; bi < NB; ++bi) {
+                        if (!all_in && (rabs < blo[bi] || rabs >= bhi[bi])) continue;
+                        double t1 = ((fill + Mv[bi] * e1.x) + res1) + e1.y;
+                        double t2 = ((fill2 + Mv[bi] * e2.x) + res2) + e2.y;
+                        double t3 = ((fill3 + Mv[bi] * e3.x) + res3) + e3.y;
+                        double c = (k > 3) ? gtsel(t1, mx[bi]) : t1;
+                        c = gtsel(t2, c);
+                        c = gtsel(t3, c);
+                        unsigned long long tk = rabs * NB + bi;
+                        if (c < best_c || (c == best_c && tk < best_t)) { best_c = c; best_t = tk; }
                     }
+                    rl += 32;
+                    live = rl < tlen && advance_pair(p, a, q, 32, n, k, dirty);
                 }
-                ci += run;
-                if (ci >= t1) break;
-                // next prefix: next combination of p[1..k-2], then p[k-1] = p[k-2] + 1
-                int j = k - 2;
-                while (j >= 1 && p[j] >= n - (k - j)) --j;
-                if (j < 1) break;  // range exhausted (cannot happen while ci < NC)
-                ++p[j];
-                for (int t = j + 1; t < k; ++t) p[t] = p[t - 1] + 1;
-            }
-            if (have) {
-                mine.cost = best_cost;
-                mine.tie = ((perm_rank * G.NC) + best_ci) * (unsigned long long)G.nbm + (unsigned long long)bmi;
             }
         }
     }
+    if (best_t != ~0ull) {
+        unsigned long long rr = best_t / NB, bi = best_t % NB;
+        mine.cost = best_c;
+        mine.tie = ((perm_rank * G.NC) + rr) * (unsigned long long)G.nbm +
+                   (unsigned long long)(bi * I.nm + mi);
+    }
     block_argmin_finish(mine, S);
+}
+
+// Tile table: cut positions p[1..k-1] (u8) of every K3_TILE-th composition
+// rank (16-byte records); depends on (n, k) only.
+__global__ void k_tiles(int n, int k, unsigned long long ntiles, uint8_t* out) {
+    unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    int p[GP_MAX_STAGES + 1];
+    d_unrank_cuts(n, k, t * K3_TILE, p);
+    for (int j = 1; j < 16; ++j) out[t * 16 + j - 1] = j < k ? (uint8_t)p[j] : 0;
+    out[t * 16 + 15] = 0;
 }
 
 // Generic range kernel (status-tracking): one thread per index; records the
@@ -694,7 +902,7 @@ __global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const u
         if (I.scode[(size_t)o[s] * N2 + tri_idx(n, p[s], p[s + 1])] == SC_INFEASIBLE) feas = false;
     out->feasible = feas ? 1 : 0;
     const double2* T = I.stg + (size_t)mi * I.F * N2;
-    const double* X = I.xt + (size_t)mi * I.F * I.F * n;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
     double Md = (double)M;
     double fill = 0.0, res = 0.0, xprev = 0.0;
     for (int s = 0; s < k; ++s) {
@@ -720,7 +928,7 @@ __global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const u
         st.residual_seconds = res;
         st.collective_seconds = e.y;
         if (s + 1 < k) {
-            double x = X[((size_t)o[s] * I.F + o[s + 1]) * n + (p[s + 1] - 1)];
+            double x = X[((size_t)o[s] * I.F + o[s + 1]) * I.nxp + (p[s + 1] - 1)];
             fill = fill + (e.x + x);
             xprev = x;
         }
@@ -756,6 +964,7 @@ struct gp_ctx {
     std::vector<long long> h_batch, h_micro;
     DBuf<double> fwd, bwd_in, bwd_w, act, param, p_c, mem, p_t, lat, bw, fg_cap, sg_cap, fg_minbw,
         fg_minbw_in, S, g_rf, g_cf, g_dp, g_minmem, sg_minmem, C1, xt;
+    DBuf<double2> tpk, tcol;
     DBuf<long long> batch, micro;
     DBuf<uint32_t> id_rank, fg_off, fg_mem, fg_sg_off, sg_off, sg_mem, flagsbuf;
     DBuf<uint8_t> fg_has, g_tp_ok, scode, skind;
@@ -776,6 +985,12 @@ struct gp_ctx {
     bool last_generic = false;
     unsigned long long last_lo = 0, last_hi = 0;
     int smem_max = 0;
+    int n_sms = 148;
+    int force_mode = -1;  // -1 auto; 0/1/2 fast-path variant; 3 generic kernel
+    DBuf<unsigned long long> binom;
+    DBuf<unsigned int> item_ctr;
+    DBuf<uint8_t> tiles;
+    bool tiles_ok = false;
 
     DevInst view() {
         DevInst I;
@@ -793,6 +1008,8 @@ struct gp_ctx {
         I.g_minmem = g_minmem.p; I.sg_minmem = sg_minmem.p;
         I.stg = stg.p; I.scode = scode.p; I.skind = skind.p; I.C1 = C1.p;
         I.gw = gw.p; I.xt = xt.p; I.flags = flagsbuf.p;
+        I.nxp = (n + 1) & ~1;
+        I.tpk = tpk.p; I.tcol = tcol.p;
         return I;
     }
     double bf = 1.25;
@@ -804,6 +1021,13 @@ static cudaError_t upload(cudaStream_t s, DBuf<T>& d, const T* h, size_t count) 
     if (e != cudaSuccess) return e;
     if (count == 0) return cudaSuccess;
     return cudaMemcpyAsync(d.p, h, count * sizeof(T), cudaMemcpyHostToDevice, s);
+}
+
+static unsigned long long h_binom(int n, int r) {
+    if (r < 0 || r > n) return 0ull;
+    unsigned long long res = 1;
+    for (int i = 1; i <= r; ++i) res = res * (unsigned long long)(n - r + i) / (unsigned long long)i;
+    return res;
 }
 
 extern "C" {
@@ -828,6 +1052,7 @@ int gp_ctx_create(int device, gp_ctx** out) {
     gp_ctx* c = new gp_ctx();
     c->device = device;
     c->smem_max = (int)prop.sharedMemPerBlockOptin;
+    c->n_sms = prop.multiProcessorCount;
     cudaError_t se = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (se != cudaSuccess) { delete c; return fail(GP_ERR_CUDA, "stream: %s", cudaGetErrorString(se)); }
     *out = c;
@@ -852,6 +1077,8 @@ void gp_ctx_destroy(gp_ctx* c) {
     DBuf<uint8_t>* bb[] = {&c->fg_has, &c->g_tp_ok, &c->scode, &c->skind, &c->b_order,
                            &c->b_counts, &c->b_bm, &c->b_status};
     for (auto* b : bb) b->release();
+    c->binom.release(); c->item_ctr.release(); c->tiles.release();
+    c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
     c->counter.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
     c->ginfo.release(); c->dstatus.release();
@@ -948,14 +1175,36 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     CUDA_TRY(c->skind.ensure((size_t)F * N2));
     CUDA_TRY(c->C1.ensure((size_t)F * N2));
     CUDA_TRY(c->gw.ensure((size_t)F * F));
-    CUDA_TRY(c->xt.ensure((size_t)c->nm * F * F * n));
+    CUDA_TRY(c->xt.ensure((size_t)c->nm * F * F * ((n + 1) & ~1u)));
+    CUDA_TRY(c->tpk.ensure((size_t)c->nm * F * ((size_t)n * (n + 1) / 2)));
+    CUDA_TRY(c->tcol.ensure((size_t)c->nm * F * (n + 1)));
     CUDA_TRY(c->flagsbuf.ensure(1));
     CUDA_TRY(c->counter.ensure(1));
     CUDA_TRY(c->result.ensure(1));
     CUDA_TRY(c->err_idx.ensure(1));
     CUDA_TRY(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned int), s));
+    if (!c->binom.p) {
+        // C(nn, r) for nn < 257, r <= GP_MAX_STAGES (composition unranking)
+        std::vector<unsigned long long> tab((size_t)BINOM_ROWS * (GP_MAX_STAGES + 1), 0ull);
+        for (int nn = 0; nn < BINOM_ROWS; ++nn)
+            for (int r = 0; r <= GP_MAX_STAGES; ++r) tab[(size_t)nn * (GP_MAX_STAGES + 1) + r] = h_binom(nn, r);
+        CUDA_TRY(upload(s, c->binom, tab.data(), tab.size()));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
     int st = run_tables(c, true);
     if (st != GP_OK) return st;
+    // K3 tile table for k = all groups (composition space depends on (n, k))
+    c->tiles_ok = false;
+    if ((int)F >= 3 && (int)F <= (int)n) {
+        unsigned long long NC = h_binom((int)n - 1, (int)F - 1);
+        unsigned long long ntiles = (NC + K3_TILE - 1) / K3_TILE;
+        if (ntiles <= (1ull << 22)) {
+            CUDA_TRY(c->tiles.ensure(ntiles * 16));
+            k_tiles<<<(unsigned)((ntiles + 127) / 128), 128, 0, s>>>((int)n, (int)F, ntiles, c->tiles.p);
+            CUDA_TRY(cudaGetLastError());
+            c->tiles_ok = true;
+        }
+    }
     c->loaded = true;
     return GP_OK;
 }
@@ -1010,12 +1259,6 @@ int gp_eval_batch(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* order, const
     return GP_OK;
 }
 
-static unsigned long long h_binom(int n, int r) {
-    if (r < 0 || r > n) return 0ull;
-    unsigned long long res = 1;
-    for (int i = 1; i <= r; ++i) res = res * (unsigned long long)(n - r + i) / (unsigned long long)i;
-    return res;
-}
 static unsigned long long h_fact(int k) {
     unsigned long long f = 1;
     for (int i = 2; i <= k; ++i) f *= (unsigned long long)i;
@@ -1050,28 +1293,61 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     ArgminScratch S;
     CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));  // = ~0
     DevInst I = c->view();
-    bool generic = c->flags != 0 || k < 2;
-    c->last_generic = generic;
+    bool generic = c->flags != 0 || k < 3 || c->force_mode == 3 || c->nb > 4;
     unsigned long long grid;
+    // fast-path kernel variant by shared-memory fit (see k3_argmin)
+    size_t ntri = (size_t)c->n * (c->n + 1) / 2;
+    size_t nxp = (size_t)((c->n + 1) & ~1);
+    size_t smem0 = 16 + (((size_t)(c->n + 1) * (k + 1) * 8 + 15) & ~(size_t)15);
+    size_t smem1 = smem0 + ntri * 16 + (c->n + 1) * 16 + 3 * nxp * 8 + (size_t)c->n * 16;
+    size_t smem2 = smem1 + ntri * 16;
+    int mode = smem2 <= (size_t)c->smem_max ? 2 : (smem1 <= (size_t)c->smem_max ? 1 : 0);
+    if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
+    size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
+    typedef void (*K3Fn)(DevInst, RangeGeom, ArgminScratch, const unsigned long long*);
+    static const K3Fn table[3][4] = {
+        {k3_argmin<0, 1>, k3_argmin<0, 2>, k3_argmin<0, 3>, k3_argmin<0, 4>},
+        {k3_argmin<1, 1>, k3_argmin<1, 2>, k3_argmin<1, 3>, k3_argmin<1, 4>},
+        {k3_argmin<2, 1>, k3_argmin<2, 2>, k3_argmin<2, 3>, k3_argmin<2, 4>}};
+    K3Fn kern = generic ? nullptr : table[mode][c->nb - 1];
     if (hi == lo) {
         generic = true;
         grid = 1;
     } else if (generic) {
         grid = (hi - lo + 255) / 256;
     } else {
-        unsigned long long item_first = lo / G.NC, item_last = (hi - 1) / G.NC;
-        unsigned long long items = item_last - item_first + 1;
-        // aim for >= 2 CTAs per SM, chunks of >= 4096 candidates
-        unsigned long long target = 2 * 148;
-        unsigned long long cpi = (target + items - 1) / items;
-        unsigned long long chunk = (G.NC + cpi - 1) / cpi;
-        if (chunk < 4096) chunk = 4096;
-        cpi = (G.NC + chunk - 1) / chunk;
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K3_THREADS, smem));
+        unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
+        // items = (micro index, order); a range inside one batch block touches
+        // a contiguous run of them, a wider range all of them
+        unsigned long long per_b = (unsigned long long)c->nm * G.NP;
+        unsigned long long blk_lo = lo / G.NC, blk_hi = (hi - 1) / G.NC;  // (bm, perm) blocks
+        unsigned long long item_first, items;
+        if (blk_lo / per_b == blk_hi / per_b) {
+            item_first = blk_lo % per_b;
+            items = blk_hi % per_b - item_first + 1;
+        } else {
+            item_first = 0;
+            items = per_b;
+        }
+        // CTAs per item: fill the resident slots, at most one per 8 tiles
+        unsigned long long tiles_per_item = (G.NC + K3_TILE - 1) / K3_TILE;
+        unsigned long long cpi = items >= resident ? 1 : resident / items;
+        unsigned long long cap = (tiles_per_item + 7) / 8;
+        if (cpi > cap) cpi = cap;
+        if (cpi < 1) cpi = 1;
         G.item0 = item_first;
-        G.chunk = chunk;
+        G.chunk = 0;
         G.chunks_per_item = cpi;
         grid = items * cpi;
+        CUDA_TRY(c->item_ctr.ensure(items));
+        CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
+        G.item_ctr = c->item_ctr.p;
+        G.tiles = c->tiles_ok ? c->tiles.p : nullptr;
     }
+    c->last_generic = generic;
     if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "range too large for one launch");
     CUDA_TRY(c->blk.ensure(grid));
     S.blk = c->blk.p;
@@ -1084,14 +1360,7 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
         if (hi == lo) G.hi = G.lo;  // one empty CTA writes the neutral key
         k3_argmin_generic<<<(unsigned)grid, 256, 0, s>>>(I, G, S);
     } else {
-        size_t smem = ((size_t)c->n * (c->n + 1) / 2 + c->n) * sizeof(double2) + c->n * sizeof(double);
-        if ((int)smem <= c->smem_max && smem <= 200 * 1024) {
-            CUDA_TRY(cudaFuncSetAttribute(k3_argmin<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-            k3_argmin<true><<<(unsigned)grid, 256, smem, s>>>(I, G, S);
-        } else {
-            k3_argmin<false><<<(unsigned)grid, 256, 0, s>>>(I, G, S);
-        }
+        kern<<<(unsigned)grid, K3_THREADS, smem, s>>>(I, G, S, c->binom.p);
     }
     CUDA_TRY(cudaGetLastError());
     return GP_OK;
@@ -1228,6 +1497,12 @@ __global__ void k_fp64_peak(double* sink, int iters, double step) {
     }
     double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
     if (r == 12345.678) sink[blockIdx.x] = r;  // never true; keeps the chains live
+}
+
+int gp_ctx_set_k3_mode(gp_ctx* c, int mode) {
+    if (!c || mode < -1 || mode > 3) return fail(GP_ERR_INPUT, "bad mode");
+    c->force_mode = mode;
+    return GP_OK;
 }
 
 int gp_diag_fp64_peak(int device, double* dadd_per_second) {

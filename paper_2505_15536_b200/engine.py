@@ -57,6 +57,7 @@ def lib():
         L.gp_group_splits.argtypes = [vp, C.c_uint32, P(abi.GpGroupInfo)]
         L.gp_set_bandwidth.argtypes = [vp, P(C.c_double)]
         L.gp_diag_fp64_peak.argtypes = [C.c_int, P(C.c_double)]
+        L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
         _lib = L
         return L
 
@@ -154,6 +155,10 @@ class Engine:
         g = abi.GpGroupInfo()
         _check(lib().gp_group_splits(self._h, int(f), C.byref(g)))
         return g
+
+    def set_k3_mode(self, mode: int) -> None:
+        """Force the exhaustive-kernel variant (-1 auto, 0/1/2, 3 generic)."""
+        _check(lib().gp_ctx_set_k3_mode(self._h, int(mode)))
 
     def set_bandwidth(self, bw: np.ndarray) -> None:
         a = np.ascontiguousarray(bw, dtype=np.float64)

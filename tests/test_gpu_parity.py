@@ -104,6 +104,39 @@ def test_k3_random_subranges(engine, name):
         assert got.evaluated == hi - lo
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("name", ["c1j", "c2", "c2j", "rand5", "rand10", "rand6", "small"])
+def test_k3_all_kernel_variants_agree(engine, name, mode):
+    doc, model, topo, groups, packed = _load(engine, name)
+    gc, gs = golden_costs(name)
+    order, counts, bm = enumerate_encoded(packed)
+    N = gc.size
+    rng = random.Random(mode)
+    ranges = [(0, N)] + [tuple(sorted(rng.sample(range(N + 1), 2))) for _ in range(6)]
+    try:
+        engine.set_k3_mode(mode)
+        for lo, hi in ranges:
+            if hi <= lo:
+                continue
+            exp = _key_argmin(packed, gc, gs, lo, hi, order, counts, bm)
+            got = engine.argmin_range(lo, hi)
+            assert got.index == exp[1], (mode, lo, hi)
+    finally:
+        engine.set_k3_mode(-1)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_k3_c4_variants(engine, mode):
+    doc, model, topo, groups, packed = _load(engine, "c4j")
+    try:
+        engine.set_k3_mode(mode)
+        got = engine.argmin_range(0, engine.space_size())
+    finally:
+        engine.set_k3_mode(-1)
+    assert got.index == doc["oracle_argmin"]["index"]
+    assert got.cost == doc["oracle_argmin"]["cost"]
+
+
 @pytest.mark.parametrize("name", CASES_ALL)
 def test_exhaustive_plan_matches_reference(engine, name):
     doc, model, topo, groups = load_case(name)
