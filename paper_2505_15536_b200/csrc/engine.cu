@@ -59,6 +59,10 @@ enum : uint8_t { SC_OK = 0, SC_INFEASIBLE = 1, SC_DEGENERATE = 4, SC_TOPOLOGY = 
 enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 4 };
 #define K3_THREADS 256
 #define K3_TILE 256
+#define K3_SEG 32
+#ifndef K3_MINB
+#define K3_MINB 3
+#endif
 #define BINOM_ROWS 257
 
 // ----------------------------------------------------------------------------
@@ -585,12 +589,12 @@ __device__ __forceinline__ bool advance_pair(int* p, int& a, int& q, int s, int 
     return true;
 }
 
-// max(0.0, x) as DSETP + 2 SEL (x > 0 ? x : +0.0, NaN -> +0.0 like Python)
+// max(0.0, x) = x > 0 ? x : +0.0 without the FP64 pipe: clear every bit
+// when the sign bit is set (-0.0 -> +0.0, negatives -> +0.0).  Exact for
+// every non-NaN x (NaN cannot occur: operands are finite or +inf).
 __device__ __forceinline__ double max0f(double x) {
-    double r;
-    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, 0d0000000000000000;\n\t"
-        "selp.f64 %0, %1, 0d0000000000000000, p;\n\t}" : "=d"(r) : "d"(x));
-    return r;
+    long long b = __double_as_longlong(x);
+    return __longlong_as_double(b & ~(b >> 63));
 }
 // a > b ? a : b (first-max; no NaNs occur)
 __device__ __forceinline__ double gtsel(double a, double b) {
@@ -639,7 +643,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // last-stage column, stage 0's row and the boundary rows HBM/L2 -> shared
 // memory with bulk async copies (TMA, cp.async.bulk) on one mbarrier.
 template <int MODE, int NB>
-__global__ void __launch_bounds__(K3_THREADS, 2) k3_argmin(DevInst I, RangeGeom G, ArgminScratch S,
+__global__ void __launch_bounds__(K3_THREADS, K3_MINB) k3_argmin(DevInst I, RangeGeom G, ArgminScratch S,
                                                            const unsigned long long* __restrict__ binom) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = I.n, k = G.k;
@@ -843,6 +847,218 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k3_argmin(DevInst I, RangeGeom 
     block_argmin_finish(mine, S);
 }
 
+// ---------------------------------------------------------------------------
+// K3 sweep (full items): the candidates of one (m, order) item are grouped
+// into RUNS = (prefix cuts p[1..k-3], a = p[k-2], a segment of <= K3_SEG
+// consecutive last cuts q).  A lane owns a run: the stages fixed by the run
+// (0..k-3) are folded once into per-lane scalars, then the lane walks q.
+// Runs are ordered by length (all full K3_SEG runs first, then the partial
+// ones grouped by length) so the 32 lanes of a warp walk in lock step, and
+// lanes of equal a read the same shared-memory row (broadcast).
+// A run group = {first run id, a | len << 16, rows, segs_per_row}; the run
+// id -> (group, prefix row, segment) map is a binary search in smem.
+// ---------------------------------------------------------------------------
+struct SweepGeom {
+    int k, nbm;
+    unsigned long long NC, NP;
+    unsigned long long item0;       // first (mi * NP + perm) item
+    unsigned long long cpi;         // CTAs per item
+    unsigned int W;                 // runs per item
+    int ngroups;
+    const uint4* groups;            // [ngroups]
+    unsigned int* item_ctr;         // per-item task counters
+    const uint8_t* prefixes;        // colex-ordered (k-3)-subsets, 16-byte records
+    int gsteps;                     // largest power of two <= ngroups
+};
+
+template <int MODE, int NB>
+__global__ void __launch_bounds__(K3_THREADS, 2) k3_sweep(DevInst I, SweepGeom G, ArgminScratch S,
+                                                          const unsigned long long* __restrict__ binom) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = I.n, k = G.k;
+    const int ntri = n * (n + 1) / 2;
+    const int KB = k + 1;
+    const unsigned long long islot = blockIdx.x / G.cpi;
+    const unsigned long long item = G.item0 + islot;
+    const int mi = (int)(item / G.NP);
+    const unsigned long long perm_rank = item % G.NP;
+    uint8_t order[GP_MAX_STAGES];
+    d_unrank_perm(k, perm_rank, order);
+    double Mv[NB];
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[bi] / I.micro[mi]);
+    const size_t N2 = (size_t)(n + 1) * (n + 1);
+    const double2* T = I.stg + (size_t)mi * I.F * N2;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
+    const int f1 = order[k - 3], f2 = order[k - 2], f3 = order[k - 1];
+    const double2* P0 = I.tpk + ((size_t)mi * I.F + order[0]) * ntri;
+    const double2* P1 = I.tpk + ((size_t)mi * I.F + f1) * ntri;
+    const double2* P2 = I.tpk + ((size_t)mi * I.F + f2) * ntri;
+    const double2* C3 = I.tcol + ((size_t)mi * I.F + f3) * (n + 1);
+    const double* X01 = X + ((size_t)order[0] * I.F + order[1]) * I.nxp;
+    const double* X12 = X + ((size_t)f1 * I.F + f2) * I.nxp;
+    const double* X23 = X + ((size_t)f2 * I.F + f3) * I.nxp;
+
+    // shared: mbarrier | binom | groups | T2 | col | x12 | x23 | row0 | x01 | T1
+    uint64_t* bar = (uint64_t*)smem_raw;
+    unsigned long long* bn = (unsigned long long*)(smem_raw + 16);
+    uint4* grp = (uint4*)(smem_raw + 16 + (((size_t)(n + 1) * KB * 8 + 15) & ~(size_t)15));
+    unsigned char* tail = (unsigned char*)(grp + G.ngroups);
+    double2* tri2 = (double2*)tail;
+    double2* col3 = tri2 + (MODE >= 1 ? ntri : 0);
+    double* x12s = (double*)(col3 + (MODE >= 1 ? n + 1 : 0));
+    double* x23s = x12s + (MODE >= 1 ? I.nxp : 0);
+    double2* row0 = (double2*)(x23s + (MODE >= 1 ? I.nxp : 0));
+    double* x01s = (double*)(row0 + (MODE >= 1 ? n : 0));
+    double2* tri1 = (double2*)(x01s + (MODE >= 1 ? I.nxp : 0));
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        if (MODE >= 1) {
+            uint32_t bytes = (uint32_t)(ntri * 16 + (n + 1) * 16 + 3 * I.nxp * 8 + n * 16) +
+                             (MODE == 2 ? (uint32_t)ntri * 16 : 0u);
+            mbar_expect_tx(bar, bytes);
+            tma_bulk_g2s(tri2, P2, (uint32_t)ntri * 16, bar);
+            tma_bulk_g2s(col3, C3, (uint32_t)(n + 1) * 16, bar);
+            tma_bulk_g2s(x12s, X12, (uint32_t)I.nxp * 8, bar);
+            tma_bulk_g2s(x23s, X23, (uint32_t)I.nxp * 8, bar);
+            tma_bulk_g2s(row0, P0, (uint32_t)n * 16, bar);
+            tma_bulk_g2s(x01s, X01, (uint32_t)I.nxp * 8, bar);
+            if (MODE == 2) tma_bulk_g2s(tri1, P1, (uint32_t)ntri * 16, bar);
+        }
+    }
+    for (int t = threadIdx.x; t < (n + 1) * KB; t += blockDim.x)
+        bn[t] = binom[(t / KB) * (GP_MAX_STAGES + 1) + (t % KB)];
+    for (int t = threadIdx.x; t < G.ngroups; t += blockDim.x) grp[t] = G.groups[t];
+    __syncthreads();
+    if (MODE >= 1) mbar_wait(bar, 0);
+
+    const int lane = threadIdx.x & 31;
+    double best_c = INFINITY;
+    unsigned long long best_t = ~0ull;  // R * NB + bi
+    for (;;) {
+        unsigned int t = 0;
+        if (lane == 0) t = atomicAdd(&G.item_ctr[islot], 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if ((unsigned long long)t * 32 >= G.W) break;
+        const unsigned int u = t * 32 + lane;
+        int len = 0, a = 0, q0 = 0;
+        double fill2 = 0.0, res1 = 0.0, x1 = 0.0;
+        double mx1[NB];
+        unsigned long long rpre = 0;  // comp rank of (prefix, a, q = a + 1)
+        if (u < G.W) {
+            // run id -> group (fixed-trip binary search), prefix row, segment
+            int gi = 0;
+            for (int step = G.gsteps; step > 0; step >>= 1) {
+                int mid = gi + step;
+                if (mid < G.ngroups && grp[mid].x <= u) gi = mid;
+            }
+            const uint4 g = grp[gi];
+            const unsigned int local = u - g.x;
+            a = (int)(g.y & 0xffffu);
+            len = (int)(g.y >> 16);
+            unsigned int row;
+            if (g.w) { row = local / g.w; q0 = a + 1 + (int)(local % g.w) * K3_SEG; }
+            else { row = local; q0 = n - len; }
+            // prefix cuts p[1..k-3]: colex row `row` (subsets of [1, a-1] come first)
+            int p[GP_MAX_STAGES + 1];
+            p[0] = 0;
+            if (k > 3) {
+                const uint8_t* pr = G.prefixes + (size_t)row * 16;
+                for (int j = 1; j <= k - 3; ++j) p[j] = pr[j - 1];
+            }
+            p[k - 2] = a;
+            // rank prefix: sum_j C(n - p[j-1] - 1, k - j) - C(n - p[j], k - j), j <= k-2
+            for (int j = 1; j <= k - 2; ++j)
+                rpre += bn[(n - p[j - 1] - 1) * KB + (k - j)] - bn[(n - p[j]) * KB + (k - j)];
+            // stages 0..k-4 (fixed by the prefix)
+            double fill = 0.0, res = 0.0, xprev = 0.0;
+            double mx[NB];
+#pragma unroll
+            for (int bi = 0; bi < NB; ++bi) mx[bi] = -INFINITY;
+            for (int s = 0; s + 3 < k; ++s) {
+                double2 e;
+                double x;
+                if (MODE >= 1 && s == 0) {
+                    e = row0[p[1] - 1];
+                    x = x01s[p[1] - 1];
+                } else {
+                    e = __ldg(&T[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])]);
+                    x = __ldg(&X[((size_t)order[s] * I.F + order[s + 1]) * I.nxp + (p[s + 1] - 1)]);
+                }
+                if (s > 0) res = res + max0f(xprev - e.x);
+#pragma unroll
+                for (int bi = 0; bi < NB; ++bi) {
+                    double tot = ((fill + Mv[bi] * e.x) + res) + e.y;
+                    mx[bi] = (s == 0) ? tot : gtsel(tot, mx[bi]);
+                }
+                fill = fill + (e.x + x);
+                xprev = x;
+            }
+            // stage k-3 = [p[k-3], a) (fixed by the run)
+            const int pk3 = p[k - 3];
+            double2 e1 = (MODE == 2) ? tri1[rowoff(n, pk3) - pk3 - 1 + a]
+                                     : __ldg(&P1[rowoff(n, pk3) - pk3 - 1 + a]);
+            x1 = (MODE >= 1) ? x12s[a - 1] : __ldg(&X12[a - 1]);
+            res1 = (k > 3) ? res + max0f(xprev - e1.x) : res;
+#pragma unroll
+            for (int bi = 0; bi < NB; ++bi) {
+                double t1 = ((fill + Mv[bi] * e1.x) + res1) + e1.y;
+                mx1[bi] = (k > 3) ? gtsel(t1, mx[bi]) : t1;
+            }
+            fill2 = fill + (e1.x + x1);
+        }
+        int lmax = len;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            int o = __shfl_xor_sync(0xffffffffu, lmax, off);
+            lmax = o > lmax ? o : lmax;
+        }
+        // walk q: per-run minimum with strict < (ranks increase with q, and
+        // with the batch index inside one q), merged into the lane's best
+        // under the full key (cost, rank, batch) when the run ends
+        const double2* e2p = (MODE >= 1 ? tri2 : P2) + (rowoff(n, a) - a - 1) + q0;
+        const double2* e3p = (MODE >= 1 ? col3 : C3) + q0;
+        const double* x2p = (MODE >= 1 ? x23s : X23) + (q0 - 1);
+        double run_c = INFINITY;
+        int run_i = -1, run_b = 0;
+        for (int i = 0; i < lmax; ++i) {
+            if (i < len) {
+                double2 e2, e3;
+                double x2;
+                if (MODE >= 1) { e2 = e2p[i]; e3 = e3p[i]; x2 = x2p[i]; }
+                else { e2 = __ldg(&e2p[i]); e3 = __ldg(&e3p[i]); x2 = __ldg(&x2p[i]); }
+                // stages k-2 = [a, q) and k-1 = [q, n) (src/costmodel.py:68-81)
+                const double res2 = res1 + max0f(x1 - e2.x);
+                const double fill3 = fill2 + (e2.x + x2);
+                const double res3 = res2 + max0f(x2 - e3.x);
+                double cmin = INFINITY;
+                int bmin = 0;
+#pragma unroll
+                for (int bi = 0; bi < NB; ++bi) {
+                    double t2 = ((fill2 + Mv[bi] * e2.x) + res2) + e2.y;
+                    double t3 = ((fill3 + Mv[bi] * e3.x) + res3) + e3.y;
+                    double c = gtsel(t2, mx1[bi]);
+                    c = gtsel(t3, c);
+                    if (bi == 0 || c < cmin) { cmin = c; bmin = bi; }
+                }
+                if (run_i < 0 || cmin < run_c) { run_c = cmin; run_i = i; run_b = bmin; }
+            }
+        }
+        if (run_i >= 0 && run_c <= best_c) {
+            unsigned long long tk = (rpre + (unsigned long long)(q0 + run_i - a - 1)) * NB + run_b;
+            if (run_c < best_c || tk < best_t) { best_c = run_c; best_t = tk; }
+        }
+    }
+    Key mine{INFINITY, ~0ull};
+    if (best_t != ~0ull) {
+        unsigned long long rr = best_t / NB, bi = best_t % NB;
+        mine.cost = best_c;
+        mine.tie = ((perm_rank * G.NC) + rr) * (unsigned long long)G.nbm +
+                   (unsigned long long)(bi * I.nm + mi);
+    }
+    block_argmin_finish(mine, S);
+}
+
 // Tile table: cut positions p[1..k-1] (u8) of every K3_TILE-th composition
 // rank (16-byte records); depends on (n, k) only.
 __global__ void k_tiles(int n, int k, unsigned long long ntiles, uint8_t* out) {
@@ -991,6 +1207,11 @@ struct gp_ctx {
     DBuf<unsigned int> item_ctr;
     DBuf<uint8_t> tiles;
     bool tiles_ok = false;
+    DBuf<uint4> groups;       // K3 sweep run groups
+    DBuf<uint8_t> prefixes;   // colex (k-3)-subsets for the sweep
+    int ngroups = 0;
+    unsigned int sweep_W = 0;
+    bool sweep_ok = false;
 
     DevInst view() {
         DevInst I;
@@ -1053,6 +1274,7 @@ int gp_ctx_create(int device, gp_ctx** out) {
     c->device = device;
     c->smem_max = (int)prop.sharedMemPerBlockOptin;
     c->n_sms = prop.multiProcessorCount;
+    if (const char* fm = getenv("GP_K3_MODE")) c->force_mode = atoi(fm);
     cudaError_t se = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (se != cudaSuccess) { delete c; return fail(GP_ERR_CUDA, "stream: %s", cudaGetErrorString(se)); }
     *out = c;
@@ -1077,7 +1299,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     DBuf<uint8_t>* bb[] = {&c->fg_has, &c->g_tp_ok, &c->scode, &c->skind, &c->b_order,
                            &c->b_counts, &c->b_bm, &c->b_status};
     for (auto* b : bb) b->release();
-    c->binom.release(); c->item_ctr.release(); c->tiles.release();
+    c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release();
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
     c->counter.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
@@ -1205,6 +1427,60 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
             c->tiles_ok = true;
         }
     }
+    // K3 sweep run groups (see k3_sweep): full K3_SEG runs by a, then partial
+    // runs grouped by length, longest first
+    c->sweep_ok = false;
+    if ((int)F >= 3 && (int)F <= (int)n) {
+        int k = (int)F, nn = (int)n;
+        std::vector<uint4> g;
+        unsigned long long start = 0;
+        for (int a = k - 2; a <= nn - 2; ++a) {
+            unsigned long long rows = h_binom(a - 1, k - 3);
+            int L = nn - 1 - a, nf = L / K3_SEG;
+            if (rows && nf) {
+                g.push_back(make_uint4((unsigned)start, (unsigned)a | ((unsigned)K3_SEG << 16),
+                                       (unsigned)rows, (unsigned)nf));
+                start += rows * nf;
+            }
+        }
+        for (int len = K3_SEG - 1; len >= 1; --len)
+            for (int a = k - 2; a <= nn - 2; ++a) {
+                int L = nn - 1 - a;
+                if (L % K3_SEG != len) continue;
+                unsigned long long rows = h_binom(a - 1, k - 3);
+                if (!rows) continue;
+                g.push_back(make_uint4((unsigned)start, (unsigned)a | ((unsigned)len << 16),
+                                       (unsigned)rows, 0u));
+                start += rows;
+            }
+        // colex list of (k-3)-subsets of [1, n-3]: the subsets of [1, a-1]
+        // are exactly its first C(a-1, k-3) entries
+        std::vector<uint8_t> pre;
+        unsigned long long npre = (k > 3) ? h_binom(nn - 3, k - 3) : 1;
+        bool pre_ok = npre <= (1ull << 22);
+        if (pre_ok && k > 3) {
+            int m = k - 3;
+            std::vector<int> cmb(m);
+            for (int i = 0; i < m; ++i) cmb[i] = i + 1;
+            pre.assign((size_t)npre * 16, 0);
+            for (unsigned long long r = 0; r < npre; ++r) {
+                for (int i = 0; i < m; ++i) pre[r * 16 + i] = (uint8_t)cmb[i];
+                // colex successor: smallest i with cmb[i] + 1 < cmb[i+1] (or last)
+                int i = 0;
+                while (i < m - 1 && cmb[i] + 1 == cmb[i + 1]) ++i;
+                ++cmb[i];
+                for (int j = 0; j < i; ++j) cmb[j] = j + 1;
+            }
+        }
+        if (pre_ok && start < (1ull << 31) && !g.empty()) {
+            if (k > 3) CUDA_TRY(upload(s, c->prefixes, pre.data(), pre.size()));
+            CUDA_TRY(upload(s, c->groups, g.data(), g.size()));
+            c->ngroups = (int)g.size();
+            c->sweep_W = (unsigned)start;
+            c->sweep_ok = true;
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
     c->loaded = true;
     return GP_OK;
 }
@@ -1272,6 +1548,67 @@ int gp_space_size(gp_ctx* c, uint64_t* out) {
     return GP_OK;
 }
 
+// Sweep launch over items [item_lo, item_hi) of (mi * k! + order).
+static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_lo,
+                        unsigned long long item_hi, int mode) {
+    cudaStream_t s = c->stream;
+    const int k = R.k, n = c->n;
+    size_t ntri = (size_t)n * (n + 1) / 2;
+    size_t nxp = (size_t)((n + 1) & ~1);
+    size_t smem0 = 16 + (((size_t)(n + 1) * (k + 1) * 8 + 15) & ~(size_t)15) + (size_t)c->ngroups * 16;
+    size_t smem1 = smem0 + ntri * 16 + (n + 1) * 16 + 3 * nxp * 8 + (size_t)n * 16;
+    size_t smem2 = smem1 + ntri * 16;
+    if (mode == 2 && smem2 > (size_t)c->smem_max) mode = 1;
+    if (mode == 1 && smem1 > (size_t)c->smem_max) mode = 0;
+    size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
+    typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*);
+    static const SwFn table[3][4] = {
+        {k3_sweep<0, 1>, k3_sweep<0, 2>, k3_sweep<0, 3>, k3_sweep<0, 4>},
+        {k3_sweep<1, 1>, k3_sweep<1, 2>, k3_sweep<1, 3>, k3_sweep<1, 4>},
+        {k3_sweep<2, 1>, k3_sweep<2, 2>, k3_sweep<2, 3>, k3_sweep<2, 4>}};
+    SwFn kern = table[mode][c->nb - 1];
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K3_THREADS, smem));
+    unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
+    unsigned long long items = item_hi - item_lo;
+    unsigned long long tasks = (c->sweep_W + 31) / 32;
+    unsigned long long cpi = items >= resident ? 1 : resident / items;
+    unsigned long long cap = (tasks + 7) / 8;
+    if (cpi > cap) cpi = cap;
+    if (cpi < 1) cpi = 1;
+    unsigned long long grid = items * cpi;
+    if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "item range too large for one launch");
+    SweepGeom G;
+    G.k = k;
+    G.nbm = R.nbm;
+    G.NC = R.NC;
+    G.NP = R.NP;
+    G.item0 = item_lo;
+    G.cpi = cpi;
+    G.W = c->sweep_W;
+    G.ngroups = c->ngroups;
+    G.groups = c->groups.p;
+    G.prefixes = c->prefixes.p;
+    G.gsteps = 1;
+    while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
+    CUDA_TRY(c->item_ctr.ensure(items));
+    CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
+    G.item_ctr = c->item_ctr.p;
+    CUDA_TRY(c->blk.ensure(grid));
+    ArgminScratch S;
+    S.blk = c->blk.p;
+    S.counter = c->counter.p;
+    S.result = c->result.p;
+    S.err = nullptr;
+    S.err_idx = c->err_idx.p;
+    c->last_geom = R;
+    DevInst I = c->view();
+    kern<<<(unsigned)grid, K3_THREADS, smem, s>>>(I, G, S, c->binom.p);
+    CUDA_TRY(cudaGetLastError());
+    return GP_OK;
+}
+
 int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
     int k = c->F;
@@ -1310,6 +1647,11 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
         {k3_argmin<1, 1>, k3_argmin<1, 2>, k3_argmin<1, 3>, k3_argmin<1, 4>},
         {k3_argmin<2, 1>, k3_argmin<2, 2>, k3_argmin<2, 3>, k3_argmin<2, 4>}};
     K3Fn kern = generic ? nullptr : table[mode][c->nb - 1];
+    if (!generic && lo == 0 && hi == total && hi > 0 && c->sweep_ok && c->force_mode != 4) {
+        c->last_generic = false;
+        CUDA_TRY(c->blk.ensure(1));
+        return launch_sweep(c, G, 0, (unsigned long long)c->nm * G.NP, mode);
+    }
     if (hi == lo) {
         generic = true;
         grid = 1;
@@ -1500,7 +1842,7 @@ __global__ void k_fp64_peak(double* sink, int iters, double step) {
 }
 
 int gp_ctx_set_k3_mode(gp_ctx* c, int mode) {
-    if (!c || mode < -1 || mode > 3) return fail(GP_ERR_INPUT, "bad mode");
+    if (!c || mode < -1 || mode > 4) return fail(GP_ERR_INPUT, "bad mode");
     c->force_mode = mode;
     return GP_OK;
 }

@@ -104,7 +104,7 @@ def test_k3_random_subranges(engine, name):
         assert got.evaluated == hi - lo
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("name", ["c1j", "c2", "c2j", "rand5", "rand10", "rand6", "small"])
 def test_k3_all_kernel_variants_agree(engine, name, mode):
     doc, model, topo, groups, packed = _load(engine, name)
@@ -125,7 +125,7 @@ def test_k3_all_kernel_variants_agree(engine, name, mode):
         engine.set_k3_mode(-1)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 def test_k3_c4_variants(engine, mode):
     doc, model, topo, groups, packed = _load(engine, "c4j")
     try:
