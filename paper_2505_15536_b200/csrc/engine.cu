@@ -60,6 +60,12 @@ enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 
 #define K3_THREADS 256
 #define K3_TILE 256
 #define K3_SEG 32
+#ifndef K3S_THREADS
+#define K3S_THREADS 256
+#endif
+#ifndef K3S_MINB
+#define K3S_MINB 2
+#endif
 #ifndef K3_MINB
 #define K3_MINB 3
 #endif
@@ -872,7 +878,7 @@ struct SweepGeom {
 };
 
 template <int MODE, int NB>
-__global__ void __launch_bounds__(K3_THREADS, 2) k3_sweep(DevInst I, SweepGeom G, ArgminScratch S,
+__global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, SweepGeom G, ArgminScratch S,
                                                           const unsigned long long* __restrict__ binom) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = I.n, k = G.k;
@@ -1569,12 +1575,12 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     SwFn kern = table[mode][c->nb - 1];
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K3_THREADS, smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K3S_THREADS, smem));
     unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
     unsigned long long items = item_hi - item_lo;
     unsigned long long tasks = (c->sweep_W + 31) / 32;
     unsigned long long cpi = items >= resident ? 1 : resident / items;
-    unsigned long long cap = (tasks + 7) / 8;
+    unsigned long long cap = (tasks + (K3S_THREADS / 32) - 1) / (K3S_THREADS / 32);
     if (cpi > cap) cpi = cap;
     if (cpi < 1) cpi = 1;
     unsigned long long grid = items * cpi;
@@ -1604,7 +1610,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     S.err_idx = c->err_idx.p;
     c->last_geom = R;
     DevInst I = c->view();
-    kern<<<(unsigned)grid, K3_THREADS, smem, s>>>(I, G, S, c->binom.p);
+    kern<<<(unsigned)grid, K3S_THREADS, smem, s>>>(I, G, S, c->binom.p);
     CUDA_TRY(cudaGetLastError());
     return GP_OK;
 }
