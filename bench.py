@@ -39,15 +39,17 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# FP64 ops per candidate in K3's inner loop (the last two stages vary with
-# the last cut; stages 0..k-3 are a prefix shared by the whole sweep):
-#   stage k-2: M*c, +fill, x-c, max0, +res, +res, +AL           = 7
-#   boundary k-2 -> k-1: c+x, fill+                             = 2
-#   stage k-1: x-c, max0, +res, M*c, +fill, +res, +AL           = 7
-#   max over three totals, compare with the incumbent           = 3
-K3_OPS_PER_CAND = 19
-# The reference's own per-candidate count (11k - 5) for C4.
-REF_OPS_PER_CAND_C4 = 39
+# Algorithmic FP64 ops per candidate in the reference's operation order
+# (11k - 5 = 39 for k = 4 stages): 6 per stage (C1*m, M*c,
+# three adds, max) + 5 per boundary (c+x, fill+, x-c', max0, res+).
+ALG_OPS_PER_CAND_C4 = 39
+# FP64 instructions the K3 sweep actually issues per candidate (SASS of the
+# inner loop, profiles/r1_k3_sweep.md): 27 per q-step for 2 candidates plus
+# the per-run prefix fold, amortised.
+K3_ISSUED_FP64_PER_CAND = 13.5
+# dram__bytes_read.sum + write of one K3 launch after an L2 flush (ncu,
+# profiles/r1_k3_sweep_ncu_raw.csv)
+K3_DRAM_BYTES = 725504
 
 
 def parse():
@@ -210,6 +212,8 @@ def main():
 
     # ---- device-resident throughput (value) --------------------------------
     for _ in range(max(3, args.warmup)):
+        with torch.cuda.stream(stream):
+            flush.zero_()
         eng.argmin_range_async(0, total)
     eng.argmin_fetch()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -272,7 +276,7 @@ def main():
         peak = fp64_peak(local)
         per_launch_ms = dev_ms_max / args.steps
         cand_rate_1gpu = total / (per_launch_ms * 1e-3)
-        achieved = K3_OPS_PER_CAND * cand_rate_1gpu
+        achieved = ALG_OPS_PER_CAND_C4 * cand_rate_1gpu
         line = {
             "metric": "candidate plans evaluated/sec", "value": value,
             "unit": "candidates/s", "n_gpus": world, "steps": args.steps,
@@ -291,10 +295,13 @@ def main():
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "gp_ctx_load + gp_argmin_range + gp_plan_detail (host buffers)"},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                         "ops_per_candidate": K3_OPS_PER_CAND,
-                         "peak_source": "FP64 DADD issue rate measured live (gp_diag_fp64_peak)",
-                         "reference_ops_per_candidate": REF_OPS_PER_CAND_C4},
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": K3_DRAM_BYTES,
+                         "algorithmic_ops_per_candidate": ALG_OPS_PER_CAND_C4,
+                         "issued_fp64_per_candidate": K3_ISSUED_FP64_PER_CAND,
+                         "issued_frac": K3_ISSUED_FP64_PER_CAND * cand_rate_1gpu / peak,
+                         "peak_source": "FP64 DADD issue rate measured live on this GPU "
+                                        "(gp_diag_fp64_peak); not in MEASURED_PEAKS.json",
+                         "kernel": "k3_sweep"},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "winners": winners[:8],
