@@ -195,6 +195,11 @@ int gp_argmin_range(gp_ctx *ctx, uint64_t lo, uint64_t hi, gp_best *out);
 int gp_argmin_range_async(gp_ctx *ctx, uint64_t lo, uint64_t hi);
 int gp_argmin_fetch(gp_ctx *ctx, gp_best *out);
 
+/* One-call exact re-plan: arg-min over [lo, hi) and the winner's splits +
+ * CostBreakdown, decoded on the device; a single device->host copy and one
+ * synchronisation.  `info` may be NULL. */
+int gp_solve(gp_ctx *ctx, uint64_t lo, uint64_t hi, gp_best *best, gp_plan_info *info);
+
 /* Splits + CostBreakdown of one candidate (the winner), on the device. */
 int gp_plan_detail(gp_ctx *ctx, uint32_t k, const uint8_t *order,
                    const uint8_t *counts, uint32_t bm, gp_plan_info *out);

@@ -120,14 +120,11 @@ __device__ __forceinline__ double Ssum(const DevInst& I, int col, int a, int b) 
 // sum(model.layers[i].<field> for i in range(a, b)) for every 0 <= a < b <= n,
 // each interval summed from its own start (never prefix differences).
 __global__ void k1_intervals(DevInst I) {
-    int a = blockIdx.x * blockDim.x + threadIdx.x;
-    int col = blockIdx.y;
-    if (a >= I.n) return;
-    size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
-    double* out = I.S + col * N2;
-    NeumaierSum s;
-    for (int b = a + 1; b <= I.n; ++b) {
-        int i = b - 1;
+    // one CTA per column; the column is staged in shared memory so the
+    // sequential Neumaier sweeps read on-chip values
+    __shared__ double col_s[GP_MAX_LAYERS + 1];
+    const int col = blockIdx.x;
+    for (int i = threadIdx.x; i < I.n; i += blockDim.x) {
         double x;
         switch (col) {
             case COL_FWD: x = I.fwd[i]; break;
@@ -136,8 +133,17 @@ __global__ void k1_intervals(DevInst I) {
             case COL_PARAM: x = I.param[i]; break;
             default: x = (I.fwd[i] + I.bwd_in[i]) + I.bwd_w[i]; break;  // total_flops
         }
-        if (b == a + 1) s.start(x); else s.add(x);
-        out[tri_idx(I.n, a, b)] = s.value();
+        col_s[i] = x;
+    }
+    __syncthreads();
+    size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
+    double* out = I.S + col * N2;
+    for (int a = threadIdx.x; a < I.n; a += blockDim.x) {
+        NeumaierSum sm;
+        for (int b = a + 1; b <= I.n; ++b) {
+            if (b == a + 1) sm.start(col_s[b - 1]); else sm.add(col_s[b - 1]);
+            out[tri_idx(I.n, a, b)] = sm.value();
+        }
     }
 }
 
@@ -318,27 +324,38 @@ __global__ void k1_stages(DevInst I) {
 // gateway_link (src/timing.py:104-113): argmin over (p_t, u, v) with string
 // order of ids, u in the upstream group, v in the downstream group.
 __global__ void k1_gateways(DevInst I) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= I.F * I.F) return;
-    int fa = t / I.F, fb = t % I.F;
+    // one warp per ordered pair (fa, fb); lanes scan member pairs, then a
+    // warp argmin on the key (p_t, rank(u), rank(v))
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= I.F * I.F) return;
+    const int fa = warp / I.F, fb = warp % I.F;
+    const int a0 = I.fg_off[fa], na = I.fg_off[fa + 1] - a0;
+    const int b0 = I.fg_off[fb], nbm = I.fg_off[fb + 1] - b0;
     bool have = false;
     double bp = 0.0;
-    int bu = 0, bv = 0;
-    for (int x = I.fg_off[fa]; x < (int)I.fg_off[fa + 1]; ++x) {
-        int u = I.fg_mem[x];
-        for (int y = I.fg_off[fb]; y < (int)I.fg_off[fb + 1]; ++y) {
-            int v = I.fg_mem[y];
-            double p = I.p_t[(size_t)u * I.D + v];
-            bool less;
-            if (!have) less = true;
-            else if (p != bp) less = p < bp;
-            else if (I.id_rank[u] != I.id_rank[bu]) less = I.id_rank[u] < I.id_rank[bu];
-            else less = I.id_rank[v] < I.id_rank[bv];
-            if (less) { have = true; bp = p; bu = u; bv = v; }
-        }
+    unsigned int bu = 0, bv = 0, ru = 0xffffffffu, rv = 0xffffffffu;
+    for (int t = lane; t < na * nbm; t += 32) {
+        const unsigned int u = I.fg_mem[a0 + t / nbm], v = I.fg_mem[b0 + t % nbm];
+        const double p = I.p_t[(size_t)u * I.D + v];
+        const unsigned int qu = I.id_rank[u], qv = I.id_rank[v];
+        bool less = !have || p < bp || (p == bp && (qu < ru || (qu == ru && qv < rv)));
+        if (less) { have = true; bp = p; bu = u; bv = v; ru = qu; rv = qv; }
     }
-    I.gw[t] = bu * I.D + bv;
-    if (fa != fb && !(I.bw[(size_t)bu * I.D + bv] > 0)) atomicOr(I.flags, FLAG_GATEWAY_ERROR);
+    for (int off = 16; off > 0; off >>= 1) {
+        const bool oh = __shfl_down_sync(0xffffffffu, have, off);
+        const double op = __shfl_down_sync(0xffffffffu, bp, off);
+        const unsigned int ou = __shfl_down_sync(0xffffffffu, bu, off);
+        const unsigned int ov = __shfl_down_sync(0xffffffffu, bv, off);
+        const unsigned int oru = __shfl_down_sync(0xffffffffu, ru, off);
+        const unsigned int orv = __shfl_down_sync(0xffffffffu, rv, off);
+        bool take = oh && (!have || op < bp || (op == bp && (oru < ru || (oru == ru && orv < rv))));
+        if (take) { have = true; bp = op; bu = ou; bv = ov; ru = oru; rv = orv; }
+    }
+    if (lane == 0) {
+        I.gw[warp] = (int)(bu * I.D + bv);
+        if (fa != fb && !(I.bw[(size_t)bu * I.D + bv] > 0)) atomicOr(I.flags, FLAG_GATEWAY_ERROR);
+    }
 }
 
 __global__ void k1_boundary(DevInst I) {
@@ -650,7 +667,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // memory with bulk async copies (TMA, cp.async.bulk) on one mbarrier.
 template <int MODE, int NB>
 __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k3_argmin(DevInst I, RangeGeom G, ArgminScratch S,
-                                                           const unsigned long long* __restrict__ binom) {
+                                                           const unsigned long long* __restrict__ binom,
+                                                           const uint32_t* skip_if_flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = I.n, k = G.k;
     const int ntri = n * (n + 1) / 2;
@@ -674,6 +692,7 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k3_argmin(DevInst I, Rang
         if (l != 0 || h != G.NC) all_in = false;
         if (l < h) { u_lo = l < u_lo ? l : u_lo; u_hi = h > u_hi ? h : u_hi; }
     }
+    if (skip_if_flags && *skip_if_flags) u_hi = 0;  // tables carry errors: generic kernel decides
     uint8_t order[GP_MAX_STAGES];
     d_unrank_perm(k, perm_rank, order);
     double Mv[NB];
@@ -879,7 +898,8 @@ struct SweepGeom {
 
 template <int MODE, int NB>
 __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, SweepGeom G, ArgminScratch S,
-                                                          const unsigned long long* __restrict__ binom) {
+                                                          const unsigned long long* __restrict__ binom,
+                                                          const uint32_t* skip_if_flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = I.n, k = G.k;
     const int ntri = n * (n + 1) / 2;
@@ -941,7 +961,8 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     const int lane = threadIdx.x & 31;
     double best_c = INFINITY;
     unsigned long long best_t = ~0ull;  // R * NB + bi
-    for (;;) {
+    const bool skip = skip_if_flags && *skip_if_flags;  // generic kernel decides
+    for (; !skip;) {
         unsigned int t = 0;
         if (lane == 0) t = atomicAdd(&G.item_ctr[islot], 1u);
         t = __shfl_sync(0xffffffffu, t, 0);
@@ -1078,10 +1099,15 @@ __global__ void k_tiles(int n, int k, unsigned long long ntiles, uint8_t* out) {
 
 // Generic range kernel (status-tracking): one thread per index; records the
 // first erroring candidate in enumeration order.
-__global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G, ArgminScratch S) {
-    unsigned long long idx = G.lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G, ArgminScratch S,
+                                                         const uint32_t* only_if_flags) {
+    // fix-up launch behind a fast-path kernel: do nothing unless the table
+    // build raised a flag (then this kernel's result replaces the fast one)
+    if (only_if_flags && *only_if_flags == 0u) return;
     Key mine{INFINITY, ~0ull};
-    if (idx < G.hi) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long idx = G.lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+         idx < G.hi; idx += stride) {
         unsigned long long comp = idx % G.NC;
         unsigned long long r = idx / G.NC;
         unsigned long long perm_rank = r % G.NP;
@@ -1096,23 +1122,18 @@ __global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G,
         if (e.status != GP_OK) {
             atomicMin(S.err_idx, (idx << 4) | (unsigned long long)e.status);
         } else {
-            mine.cost = e.cost;
-            mine.tie = ((perm_rank * G.NC) + comp) * (unsigned long long)G.nbm + (unsigned long long)bmi;
+            Key o{e.cost, ((perm_rank * G.NC) + comp) * (unsigned long long)G.nbm + (unsigned long long)bmi};
+            if (key_less(o, mine)) mine = o;
         }
     }
     block_argmin_finish(mine, S);
 }
 
 // ---- plan detail of one candidate (single thread) -----------------------------------
-__global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const uint8_t* counts_in,
-                              int bm, gp_plan_info* out, int* status) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void plan_detail_dev(const DevInst& I, int k, const uint8_t* o, const int* p, int bm,
+                                gp_plan_info* out, int* status) {
     int n = I.n;
     size_t N2 = (size_t)(n + 1) * (n + 1);
-    uint8_t o[GP_MAX_STAGES];
-    int p[GP_MAX_STAGES + 1];
-    p[0] = 0;
-    for (int s = 0; s < k; ++s) { o[s] = order_in[s]; p[s + 1] = p[s] + counts_in[s]; }
     int mi = bm % I.nm;
     long long M = I.batch[bm / I.nm] / I.micro[mi];
     EvalOut r = eval_tables(I, k, o, p, mi, M);
@@ -1157,6 +1178,52 @@ __global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const u
     }
 }
 
+__global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const uint8_t* counts_in,
+                              int bm, gp_plan_info* out, int* status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint8_t o[GP_MAX_STAGES];
+    int p[GP_MAX_STAGES + 1];
+    p[0] = 0;
+    for (int s = 0; s < k; ++s) { o[s] = order_in[s]; p[s + 1] = p[s] + counts_in[s]; }
+    plan_detail_dev(I, k, o, p, bm, out, status);
+}
+
+// Winner of the last arg-min -> decoded candidate + plan detail, on the
+// device (no host round trip between the arg-min and the breakdown).
+struct SolveOut {
+    Key key;
+    unsigned long long err;
+    int status;        // of the detail evaluation
+    uint32_t k, bm, pad;
+    uint8_t order[GP_MAX_STAGES];
+    uint8_t counts[GP_MAX_STAGES];
+    gp_plan_info info;
+};
+
+__global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned long long NP,
+                               int nbm, const Key* result, const unsigned long long* err,
+                               SolveOut* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    out->key = *result;
+    out->err = *err;
+    out->k = (uint32_t)k;
+    out->status = GP_OK;
+    if (out->err != ~0ull || out->key.tie == ~0ull) return;
+    unsigned long long t = out->key.tie;
+    int bm = (int)(t % (unsigned long long)nbm);
+    unsigned long long pc = t / (unsigned long long)nbm;
+    uint8_t o[GP_MAX_STAGES];
+    int p[GP_MAX_STAGES + 1];
+    d_unrank_perm(k, pc / NC, o);
+    d_unrank_cuts(I.n, k, pc % NC, p);
+    out->bm = (uint32_t)bm;
+    for (int s = 0; s < k; ++s) {
+        out->order[s] = o[s];
+        out->counts[s] = (uint8_t)(p[s + 1] - p[s]);
+    }
+    plan_detail_dev(I, k, o, p, bm, &out->info, &out->status);
+}
+
 // ----------------------------------------------------------------------------
 // context
 // ----------------------------------------------------------------------------
@@ -1175,6 +1242,12 @@ struct DBuf {
         return e;
     }
     void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+template <typename T>
+struct ArenaPtr {
+    T* p = nullptr;
+    void release() { p = nullptr; }
 };
 
 struct gp_ctx {
@@ -1203,11 +1276,23 @@ struct gp_ctx {
     DBuf<gp_plan_info> info;
     DBuf<gp_group_info> ginfo;
     DBuf<int> dstatus;
+    DBuf<SolveOut> dsolve;
+    SolveOut* h_solve = nullptr;  // pinned
     RangeGeom last_geom{};
     bool last_generic = false;
     unsigned long long last_lo = 0, last_hi = 0;
     int smem_max = 0;
     int n_sms = 148;
+    uint32_t* h_flags = nullptr;      // pinned
+    cudaEvent_t flags_ev = nullptr;
+    cudaEvent_t arena_ev = nullptr;
+    bool flags_known = false;
+    // raw instance arena: one pinned staging buffer -> one H2D copy
+    unsigned char* h_arena = nullptr;
+    size_t h_arena_cap = 0;
+    DBuf<unsigned char> arena;
+    int cache_n = -1, cache_k = -1;   // (n, k) of the enumeration helpers
+    size_t arena_bytes = 0;
     int force_mode = -1;  // -1 auto; 0/1/2 fast-path variant; 3 generic kernel
     DBuf<unsigned long long> binom;
     DBuf<unsigned int> item_ctr;
@@ -1281,6 +1366,13 @@ int gp_ctx_create(int device, gp_ctx** out) {
     c->smem_max = (int)prop.sharedMemPerBlockOptin;
     c->n_sms = prop.multiProcessorCount;
     if (const char* fm = getenv("GP_K3_MODE")) c->force_mode = atoi(fm);
+    if (cudaHostAlloc((void**)&c->h_flags, sizeof(uint32_t), cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc((void**)&c->h_solve, sizeof(SolveOut), cudaHostAllocDefault) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->flags_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->arena_ev, cudaEventDisableTiming) != cudaSuccess) {
+        gp_ctx_destroy(c);
+        return fail(GP_ERR_CUDA, "pinned flag / event allocation failed");
+    }
     cudaError_t se = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (se != cudaSuccess) { delete c; return fail(GP_ERR_CUDA, "stream: %s", cudaGetErrorString(se)); }
     *out = c;
@@ -1305,6 +1397,13 @@ void gp_ctx_destroy(gp_ctx* c) {
     DBuf<uint8_t>* bb[] = {&c->fg_has, &c->g_tp_ok, &c->scode, &c->skind, &c->b_order,
                            &c->b_counts, &c->b_bm, &c->b_status};
     for (auto* b : bb) b->release();
+    c->arena.release();
+    if (c->h_arena) cudaFreeHost(c->h_arena);
+    if (c->h_flags) cudaFreeHost(c->h_flags);
+    if (c->h_solve) cudaFreeHost(c->h_solve);
+    c->dsolve.release();
+    if (c->flags_ev) cudaEventDestroy(c->flags_ev);
+    if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release();
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
@@ -1319,21 +1418,32 @@ static int run_tables(gp_ctx* c, bool full) {
     cudaStream_t s = c->stream;
     CUDA_TRY(cudaMemsetAsync(c->flagsbuf.p, 0, sizeof(uint32_t), s));
     if (full) {
-        dim3 g1((c->n + 127) / 128, 5);
-        k1_intervals<<<g1, 128, 0, s>>>(I);
+        k1_intervals<<<5, 128, 0, s>>>(I);
         k1_groups<<<(c->F + 31) / 32, 32, 0, s>>>(I);
     }
     long long ns = (long long)c->F * (c->n + 1) * (c->n + 1);
     k1_stages<<<(unsigned)((ns + 127) / 128), 128, 0, s>>>(I);
-    k1_gateways<<<(c->F * c->F + 63) / 64, 64, 0, s>>>(I);
+    k1_gateways<<<(c->F * c->F * 32 + 127) / 128, 128, 0, s>>>(I);
     long long nx = (long long)c->nm * c->F * c->F * c->n;
     k1_boundary<<<(unsigned)((nx + 255) / 256), 256, 0, s>>>(I);
     CUDA_TRY(cudaGetLastError());
-    uint32_t flags = 0;
-    CUDA_TRY(cudaMemcpyAsync(&flags, c->flagsbuf.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    c->flags = flags;
+    // flags travel back asynchronously; kernels consult the device copy when
+    // the host copy is not known yet (no synchronisation on the load path)
+    CUDA_TRY(cudaMemcpyAsync(c->h_flags, c->flagsbuf.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(c->flags_ev, s));
+    c->flags_known = false;
     return GP_OK;
+}
+
+// host-side flags when the async read-back has landed; -1 when still pending
+static int known_flags(gp_ctx* c) {
+    if (c->flags_known) return (int)c->flags;
+    if (cudaEventQuery(c->flags_ev) == cudaSuccess) {
+        c->flags = *c->h_flags;
+        c->flags_known = true;
+        return (int)c->flags;
+    }
+    return -1;
 }
 
 int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
@@ -1365,31 +1475,68 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     c->h_batch.assign(in->batch, in->batch + in->n_batch);
     c->h_micro.assign(in->micro, in->micro + in->n_micro);
     size_t DD = (size_t)D * D;
-    CUDA_TRY(upload(s, c->fwd, in->fwd_flops, n));
-    CUDA_TRY(upload(s, c->bwd_in, in->bwd_input_flops, n));
-    CUDA_TRY(upload(s, c->bwd_w, in->bwd_weight_flops, n));
-    CUDA_TRY(upload(s, c->act, in->activation_out_bytes, n));
-    CUDA_TRY(upload(s, c->param, in->param_bytes, n));
-    CUDA_TRY(upload(s, c->batch, (const long long*)in->batch, in->n_batch));
-    CUDA_TRY(upload(s, c->micro, (const long long*)in->micro, in->n_micro));
-    CUDA_TRY(upload(s, c->p_c, in->p_c, D));
-    CUDA_TRY(upload(s, c->mem, in->memory_bytes, D));
-    CUDA_TRY(upload(s, c->id_rank, in->id_rank, D));
-    CUDA_TRY(upload(s, c->p_t, in->p_t, DD));
-    CUDA_TRY(upload(s, c->lat, in->latency, DD));
-    CUDA_TRY(upload(s, c->bw, in->bandwidth, DD));
     uint32_t nfm = in->fg_member_offset[F];
-    CUDA_TRY(upload(s, c->fg_off, in->fg_member_offset, F + 1));
-    CUDA_TRY(upload(s, c->fg_mem, in->fg_members, nfm));
-    CUDA_TRY(upload(s, c->fg_cap, in->fg_capacity, F));
-    CUDA_TRY(upload(s, c->fg_minbw_in, in->fg_min_bw, F));
-    CUDA_TRY(upload(s, c->fg_minbw, in->fg_min_bw, F));
-    CUDA_TRY(upload(s, c->fg_has, in->fg_has_min_bw, F));
-    CUDA_TRY(upload(s, c->fg_sg_off, in->fg_sg_offset, F + 1));
-    CUDA_TRY(upload(s, c->sg_off, in->sg_member_offset, nsg + 1));
     uint32_t nsm = in->sg_member_offset[nsg];
-    CUDA_TRY(upload(s, c->sg_mem, in->sg_members, nsm));
-    CUDA_TRY(upload(s, c->sg_cap, in->sg_capacity, nsg));
+    // arena layout: every array 16-byte aligned
+    struct Seg { const void* src; size_t bytes; size_t off; };
+    Seg seg[24];
+    int ns = 0;
+    size_t off = 0;
+    auto add = [&](const void* src, size_t bytes) {
+        seg[ns].src = src; seg[ns].bytes = bytes; seg[ns].off = off;
+        off += (bytes + 15) & ~(size_t)15;
+        return ns++;
+    };
+    const int i_fwd = add(in->fwd_flops, n * 8), i_bwd = add(in->bwd_input_flops, n * 8),
+              i_wgt = add(in->bwd_weight_flops, n * 8), i_act = add(in->activation_out_bytes, n * 8),
+              i_par = add(in->param_bytes, n * 8), i_b = add(in->batch, in->n_batch * 8),
+              i_m = add(in->micro, in->n_micro * 8), i_pc = add(in->p_c, D * 8),
+              i_mem = add(in->memory_bytes, D * 8), i_rank = add(in->id_rank, D * 4),
+              i_pt = add(in->p_t, DD * 8), i_lat = add(in->latency, DD * 8),
+              i_bw = add(in->bandwidth, DD * 8), i_foff = add(in->fg_member_offset, (F + 1) * 4),
+              i_fmem = add(in->fg_members, nfm * 4), i_fcap = add(in->fg_capacity, F * 8),
+              i_fbwi = add(in->fg_min_bw, F * 8), i_fbw = add(in->fg_min_bw, F * 8),
+              i_fhas = add(in->fg_has_min_bw, F), i_fsg = add(in->fg_sg_offset, (F + 1) * 4),
+              i_soff = add(in->sg_member_offset, (nsg + 1) * 4), i_smem = add(in->sg_members, nsm * 4),
+              i_scap = add(in->sg_capacity, nsg * 8);
+    if (c->arena_ev) CUDA_TRY(cudaEventSynchronize(c->arena_ev));  // last H2D done
+    if (off > c->h_arena_cap) {
+        if (c->h_arena) cudaFreeHost(c->h_arena);
+        c->h_arena = nullptr;
+        c->h_arena_cap = 0;
+        CUDA_TRY(cudaHostAlloc((void**)&c->h_arena, off, cudaHostAllocDefault));
+        c->h_arena_cap = off;
+    }
+    for (int i = 0; i < ns; ++i)
+        if (seg[i].bytes) memcpy(c->h_arena + seg[i].off, seg[i].src, seg[i].bytes);
+    CUDA_TRY(c->arena.ensure(off));
+    CUDA_TRY(cudaMemcpyAsync(c->arena.p, c->h_arena, off, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaEventRecord(c->arena_ev, s));
+    unsigned char* A = c->arena.p;
+    c->fwd.p = (double*)(A + seg[i_fwd].off);
+    c->bwd_in.p = (double*)(A + seg[i_bwd].off);
+    c->bwd_w.p = (double*)(A + seg[i_wgt].off);
+    c->act.p = (double*)(A + seg[i_act].off);
+    c->param.p = (double*)(A + seg[i_par].off);
+    c->batch.p = (long long*)(A + seg[i_b].off);
+    c->micro.p = (long long*)(A + seg[i_m].off);
+    c->p_c.p = (double*)(A + seg[i_pc].off);
+    c->mem.p = (double*)(A + seg[i_mem].off);
+    c->id_rank.p = (uint32_t*)(A + seg[i_rank].off);
+    c->p_t.p = (double*)(A + seg[i_pt].off);
+    c->lat.p = (double*)(A + seg[i_lat].off);
+    c->bw.p = (double*)(A + seg[i_bw].off);
+    c->fg_off.p = (uint32_t*)(A + seg[i_foff].off);
+    c->fg_mem.p = (uint32_t*)(A + seg[i_fmem].off);
+    c->fg_cap.p = (double*)(A + seg[i_fcap].off);
+    c->fg_minbw_in.p = (double*)(A + seg[i_fbwi].off);
+    c->fg_minbw.p = (double*)(A + seg[i_fbw].off);
+    c->fg_has.p = (uint8_t*)(A + seg[i_fhas].off);
+    c->fg_sg_off.p = (uint32_t*)(A + seg[i_fsg].off);
+    c->sg_off.p = (uint32_t*)(A + seg[i_soff].off);
+    c->sg_mem.p = (uint32_t*)(A + seg[i_smem].off);
+    c->sg_cap.p = (double*)(A + seg[i_scap].off);
+    c->arena_bytes = off;
     size_t N2 = (size_t)(n + 1) * (n + 1);
     CUDA_TRY(c->S.ensure(5 * N2));
     CUDA_TRY(c->g_tp_ok.ensure(F));
@@ -1410,6 +1557,7 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     CUDA_TRY(c->counter.ensure(1));
     CUDA_TRY(c->result.ensure(1));
     CUDA_TRY(c->err_idx.ensure(1));
+    CUDA_TRY(c->blk.ensure(4096));  // >= the generic fix-up grid (no realloc mid-stream)
     CUDA_TRY(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned int), s));
     if (!c->binom.p) {
         // C(nn, r) for nn < 257, r <= GP_MAX_STAGES (composition unranking)
@@ -1417,22 +1565,17 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
         for (int nn = 0; nn < BINOM_ROWS; ++nn)
             for (int r = 0; r <= GP_MAX_STAGES; ++r) tab[(size_t)nn * (GP_MAX_STAGES + 1) + r] = h_binom(nn, r);
         CUDA_TRY(upload(s, c->binom, tab.data(), tab.size()));
-        CUDA_TRY(cudaStreamSynchronize(s));
     }
     int st = run_tables(c, true);
     if (st != GP_OK) return st;
-    // K3 tile table for k = all groups (composition space depends on (n, k))
-    c->tiles_ok = false;
-    if ((int)F >= 3 && (int)F <= (int)n) {
-        unsigned long long NC = h_binom((int)n - 1, (int)F - 1);
-        unsigned long long ntiles = (NC + K3_TILE - 1) / K3_TILE;
-        if (ntiles <= (1ull << 22)) {
-            CUDA_TRY(c->tiles.ensure(ntiles * 16));
-            k_tiles<<<(unsigned)((ntiles + 127) / 128), 128, 0, s>>>((int)n, (int)F, ntiles, c->tiles.p);
-            CUDA_TRY(cudaGetLastError());
-            c->tiles_ok = true;
-        }
+    // enumeration helpers depend on (n, k) only: rebuild when those change
+    if (c->cache_n == (int)n && c->cache_k == (int)F) {
+        c->loaded = true;
+        return GP_OK;
     }
+    c->cache_n = (int)n;
+    c->cache_k = (int)F;
+    c->tiles_ok = false;  // K3 tile table: built lazily by the sub-range path
     // K3 sweep run groups (see k3_sweep): full K3_SEG runs by a, then partial
     // runs grouped by length, longest first
     c->sweep_ok = false;
@@ -1486,8 +1629,23 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
             c->sweep_ok = true;
         }
     }
-    CUDA_TRY(cudaStreamSynchronize(s));
     c->loaded = true;
+    return GP_OK;
+}
+
+static int ensure_tiles(gp_ctx* c) {
+    if (c->tiles_ok) return GP_OK;
+    int n = c->n, F = c->F;
+    if (F >= 3 && F <= n) {
+        unsigned long long NC = h_binom(n - 1, F - 1);
+        unsigned long long ntiles = (NC + K3_TILE - 1) / K3_TILE;
+        if (ntiles <= (1ull << 22)) {
+            CUDA_TRY(c->tiles.ensure(ntiles * 16));
+            k_tiles<<<(unsigned)((ntiles + 127) / 128), 128, 0, c->stream>>>(n, F, ntiles, c->tiles.p);
+            CUDA_TRY(cudaGetLastError());
+            c->tiles_ok = true;
+        }
+    }
     return GP_OK;
 }
 
@@ -1556,7 +1714,7 @@ int gp_space_size(gp_ctx* c, uint64_t* out) {
 
 // Sweep launch over items [item_lo, item_hi) of (mi * k! + order).
 static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_lo,
-                        unsigned long long item_hi, int mode) {
+                        unsigned long long item_hi, int mode, const uint32_t* dflags) {
     cudaStream_t s = c->stream;
     const int k = R.k, n = c->n;
     size_t ntri = (size_t)n * (n + 1) / 2;
@@ -1567,7 +1725,8 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     if (mode == 2 && smem2 > (size_t)c->smem_max) mode = 1;
     if (mode == 1 && smem1 > (size_t)c->smem_max) mode = 0;
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
-    typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*);
+    typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*,
+                         const uint32_t*);
     static const SwFn table[3][4] = {
         {k3_sweep<0, 1>, k3_sweep<0, 2>, k3_sweep<0, 3>, k3_sweep<0, 4>},
         {k3_sweep<1, 1>, k3_sweep<1, 2>, k3_sweep<1, 3>, k3_sweep<1, 4>},
@@ -1610,7 +1769,26 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     S.err_idx = c->err_idx.p;
     c->last_geom = R;
     DevInst I = c->view();
-    kern<<<(unsigned)grid, K3S_THREADS, smem, s>>>(I, G, S, c->binom.p);
+    kern<<<(unsigned)grid, K3S_THREADS, smem, s>>>(I, G, S, c->binom.p, dflags);
+    CUDA_TRY(cudaGetLastError());
+    return GP_OK;
+}
+
+// Generic status-tracking pass that runs only when the device flags are set.
+static int launch_fixup(gp_ctx* c, const RangeGeom& G) {
+    unsigned long long grid = (G.hi - G.lo + 255) / 256;
+    unsigned long long gmax = (unsigned long long)c->n_sms * 16;
+    if (grid > gmax) grid = gmax;
+    if (grid < 1) grid = 1;
+    CUDA_TRY(c->blk.ensure(grid));
+    ArgminScratch S;
+    S.blk = c->blk.p;
+    S.counter = c->counter.p;
+    S.result = c->result.p;
+    S.err = nullptr;
+    S.err_idx = c->err_idx.p;
+    DevInst I = c->view();
+    k3_argmin_generic<<<(unsigned)grid, 256, 0, c->stream>>>(I, G, S, c->flagsbuf.p);
     CUDA_TRY(cudaGetLastError());
     return GP_OK;
 }
@@ -1636,7 +1814,13 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     ArgminScratch S;
     CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));  // = ~0
     DevInst I = c->view();
-    bool generic = c->flags != 0 || k < 3 || c->force_mode == 3 || c->nb > 4;
+    // table flags (error entries, overflow) force the status-tracking kernel;
+    // while the async read-back is pending, launch the fast kernel with a
+    // device-side check plus a generic fix-up that runs only if flagged
+    const int fl = known_flags(c);
+    bool generic = fl > 0 || k < 3 || c->force_mode == 3 || c->nb > 4;
+    const bool pending = fl < 0 && !generic;
+    const uint32_t* dflags = pending ? c->flagsbuf.p : nullptr;
     unsigned long long grid;
     // fast-path kernel variant by shared-memory fit (see k3_argmin)
     size_t ntri = (size_t)c->n * (c->n + 1) / 2;
@@ -1647,7 +1831,8 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     int mode = smem2 <= (size_t)c->smem_max ? 2 : (smem1 <= (size_t)c->smem_max ? 1 : 0);
     if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
-    typedef void (*K3Fn)(DevInst, RangeGeom, ArgminScratch, const unsigned long long*);
+    typedef void (*K3Fn)(DevInst, RangeGeom, ArgminScratch, const unsigned long long*,
+                         const uint32_t*);
     static const K3Fn table[3][4] = {
         {k3_argmin<0, 1>, k3_argmin<0, 2>, k3_argmin<0, 3>, k3_argmin<0, 4>},
         {k3_argmin<1, 1>, k3_argmin<1, 2>, k3_argmin<1, 3>, k3_argmin<1, 4>},
@@ -1656,13 +1841,17 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     if (!generic && lo == 0 && hi == total && hi > 0 && c->sweep_ok && c->force_mode != 4) {
         c->last_generic = false;
         CUDA_TRY(c->blk.ensure(1));
-        return launch_sweep(c, G, 0, (unsigned long long)c->nm * G.NP, mode);
+        int st = launch_sweep(c, G, 0, (unsigned long long)c->nm * G.NP, mode, dflags);
+        if (st != GP_OK || !pending) return st;
+        return launch_fixup(c, G);
     }
     if (hi == lo) {
         generic = true;
         grid = 1;
     } else if (generic) {
         grid = (hi - lo + 255) / 256;
+        unsigned long long gmax = (unsigned long long)c->n_sms * 16;  // grid-stride
+        if (grid > gmax) grid = gmax;
     } else {
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
@@ -1693,6 +1882,8 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
         CUDA_TRY(c->item_ctr.ensure(items));
         CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
         G.item_ctr = c->item_ctr.p;
+        int ts = ensure_tiles(c);
+        if (ts != GP_OK) return ts;
         G.tiles = c->tiles_ok ? c->tiles.p : nullptr;
     }
     c->last_generic = generic;
@@ -1706,9 +1897,11 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     c->last_geom = G;
     if (generic) {
         if (hi == lo) G.hi = G.lo;  // one empty CTA writes the neutral key
-        k3_argmin_generic<<<(unsigned)grid, 256, 0, s>>>(I, G, S);
+        k3_argmin_generic<<<(unsigned)grid, 256, 0, s>>>(I, G, S, nullptr);
     } else {
-        kern<<<(unsigned)grid, K3_THREADS, smem, s>>>(I, G, S, c->binom.p);
+        kern<<<(unsigned)grid, K3_THREADS, smem, s>>>(I, G, S, c->binom.p, dflags);
+        CUDA_TRY(cudaGetLastError());
+        if (pending) return launch_fixup(c, G);
     }
     CUDA_TRY(cudaGetLastError());
     return GP_OK;
@@ -1773,6 +1966,41 @@ int gp_argmin_range(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* out) {
     int st = gp_argmin_range_async(c, lo, hi);
     if (st != GP_OK) return st;
     return gp_argmin_fetch(c, out);
+}
+
+int gp_solve(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* best, gp_plan_info* info) {
+    if (!c || !c->loaded || !best) return fail(GP_ERR_INPUT, "context not loaded");
+    int st = gp_argmin_range_async(c, lo, hi);
+    if (st != GP_OK) return st;
+    const RangeGeom& G = c->last_geom;
+    CUDA_TRY(c->dsolve.ensure(1));
+    DevInst I = c->view();
+    k_solve_detail<<<1, 32, 0, c->stream>>>(I, G.k, G.NC, G.NP, G.nbm, c->result.p, c->err_idx.p,
+                                            c->dsolve.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(c->h_solve, c->dsolve.p, sizeof(SolveOut), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const SolveOut& o = *c->h_solve;
+    memset(best, 0, sizeof(*best));
+    best->k = (uint32_t)G.k;
+    best->evaluated = c->last_hi - c->last_lo;
+    if (o.err != ~0ull) {
+        int code = (int)(o.err & 15ull);
+        return fail(code, "candidate %llu raises status %d", o.err >> 4, code);
+    }
+    if (o.key.tie == ~0ull) return fail(GP_ERR_NO_FEASIBLE, "empty candidate range");
+    unsigned long long bmv = o.key.tie % (unsigned long long)G.nbm;
+    unsigned long long pc = o.key.tie / (unsigned long long)G.nbm;
+    best->cost = o.key.cost;
+    best->index = (bmv * G.NP + pc / G.NC) * G.NC + pc % G.NC;
+    best->batch_index = (uint32_t)(bmv / c->nm);
+    best->micro_index = (uint32_t)(bmv % c->nm);
+    memcpy(best->order, o.order, sizeof(best->order));
+    memcpy(best->counts, o.counts, sizeof(best->counts));
+    if (info) *info = o.info;
+    if (o.status != GP_OK) return fail(o.status, "winner raises status %d", o.status);
+    return GP_OK;
 }
 
 int gp_plan_detail(gp_ctx* c, uint32_t k, const uint8_t* order, const uint8_t* counts, uint32_t bm,

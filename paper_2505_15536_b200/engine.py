@@ -54,6 +54,7 @@ def lib():
         L.gp_argmin_fetch.argtypes = [vp, P(abi.GpBest)]
         L.gp_plan_detail.argtypes = [vp, C.c_uint32, u8p, u8p, C.c_uint32,
                                      P(abi.GpPlanInfo)]
+        L.gp_solve.argtypes = [vp, C.c_uint64, C.c_uint64, P(abi.GpBest), P(abi.GpPlanInfo)]
         L.gp_group_splits.argtypes = [vp, C.c_uint32, P(abi.GpGroupInfo)]
         L.gp_set_bandwidth.argtypes = [vp, P(C.c_double)]
         L.gp_diag_fp64_peak.argtypes = [C.c_int, P(C.c_double)]
@@ -134,6 +135,13 @@ class Engine:
         best = abi.GpBest()
         _check(lib().gp_argmin_range(self._h, int(lo), int(hi), C.byref(best)))
         return best
+
+    def solve(self, lo: int, hi: int):
+        """Arg-min over [lo, hi) plus the winner's plan detail, one sync."""
+        best = abi.GpBest()
+        info = abi.GpPlanInfo()
+        _check(lib().gp_solve(self._h, int(lo), int(hi), C.byref(best), C.byref(info)))
+        return best, info
 
     def argmin_range_async(self, lo: int, hi: int) -> None:
         _check(lib().gp_argmin_range_async(self._h, int(lo), int(hi)))

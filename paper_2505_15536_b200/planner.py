@@ -127,9 +127,10 @@ def _engine_for(packed: PackedInstance, engine: Engine = None) -> Engine:
     return eng.load(packed)
 
 
-def assemble(packed: PackedInstance, eng: Engine, order_idx, counts, bm: int):
+def assemble(packed: PackedInstance, eng: Engine, order_idx, counts, bm: int, info=None):
     """(plan, breakdown|None, feasible) of one candidate, from gp_plan_detail."""
-    info = eng.plan_detail(order_idx, counts, bm)
+    if info is None:
+        info = eng.plan_detail(order_idx, counts, bm)
     b, m = packed.bm_pairs()[bm]
     stages = []
     pos = 0
@@ -181,12 +182,12 @@ def exhaustive_plan(model, topology, groups, config, engine: Engine = None) -> D
     total = eng.space_size()
     if total == 0:
         raise D.NoFeasiblePlanError("no feasible plan in exhaustive sweep")
-    best = eng.argmin_range(0, total)
+    best, info = eng.solve(0, total)
     k = best.k
     order = np.array(best.order[:k], dtype=np.uint8)
     counts = np.array(best.counts[:k], dtype=np.uint8)
     bm = best.batch_index * len(packed.micros) + best.micro_index
-    plan, breakdown, feasible = assemble(packed, eng, order, counts, bm)
+    plan, breakdown, feasible = assemble(packed, eng, order, counts, bm, info)
     if breakdown is None:
         raise D.NoFeasiblePlanError("no feasible plan in exhaustive sweep")
     return D.SearchResult(plan=plan, breakdown=breakdown,
