@@ -193,6 +193,12 @@ int gp_argmin_range(gp_ctx *ctx, uint64_t lo, uint64_t hi, gp_best *out);
 /* Asynchronous variant writing the per-launch result to device memory
  * (benchmarks / multi-GPU reduction); read with gp_argmin_fetch. */
 int gp_argmin_range_async(gp_ctx *ctx, uint64_t lo, uint64_t hi);
+/* Arg-min over the (micro-batch, stage order) items [item_lo, item_hi),
+ * item = micro_index * k! + order rank, all batch sizes and cuts included:
+ * the unit of multi-GPU sharding (the union over ranks of disjoint item
+ * ranges is the whole exhaustive space).  Read with gp_argmin_fetch; the
+ * returned index is the global enumeration index. */
+int gp_argmin_items_async(gp_ctx *ctx, uint64_t item_lo, uint64_t item_hi);
 int gp_argmin_fetch(gp_ctx *ctx, gp_best *out);
 
 /* One-call exact re-plan: arg-min over [lo, hi) and the winner's splits +

@@ -462,6 +462,9 @@ struct RangeGeom {
     unsigned long long chunk;          // (generic kernel: unused)
     unsigned int* item_ctr;            // per-item tile counters (zeroed per launch)
     const uint8_t* tiles;              // cut positions at every K3_TILE-th rank, or null
+    int items_mode;                    // generic kernel: [lo, hi) indexes (b, item, comp)
+    unsigned long long it_lo, it_span; // item range of items_mode
+    int nm;                            // |M| (items_mode decode)
 };
 
 __device__ unsigned long long d_binom(int n, int r) {
@@ -1106,8 +1109,14 @@ __global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G,
     if (only_if_flags && *only_if_flags == 0u) return;
     Key mine{INFINITY, ~0ull};
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long idx = G.lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-         idx < G.hi; idx += stride) {
+    for (unsigned long long t = G.lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+         t < G.hi; t += stride) {
+        unsigned long long idx = t;
+        if (G.items_mode) {  // t = (b * span + item offset) * NC + comp
+            unsigned long long comp0 = t % G.NC, r0 = t / G.NC;
+            unsigned long long item = G.it_lo + r0 % G.it_span, b = r0 / G.it_span;
+            idx = ((b * G.nm + item / G.NP) * G.NP + item % G.NP) * G.NC + comp0;
+        }
         unsigned long long comp = idx % G.NC;
         unsigned long long r = idx / G.NC;
         unsigned long long perm_rank = r % G.NP;
@@ -1809,6 +1818,12 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     G.NP = h_fact(k);
     G.lo = lo;
     G.hi = hi;
+    G.items_mode = 0;
+    G.it_lo = 0;
+    G.it_span = 1;
+    G.nm = c->nm;
+    G.item_ctr = nullptr;
+    G.tiles = nullptr;
     c->last_lo = lo;
     c->last_hi = hi;
     ArgminScratch S;
@@ -1966,6 +1981,58 @@ int gp_argmin_range(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* out) {
     int st = gp_argmin_range_async(c, lo, hi);
     if (st != GP_OK) return st;
     return gp_argmin_fetch(c, out);
+}
+
+int gp_argmin_items_async(gp_ctx* c, uint64_t item_lo, uint64_t item_hi) {
+    if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    const int k = c->F;
+    uint64_t total;
+    gp_space_size(c, &total);
+    const unsigned long long NP = h_fact(k), NC = h_binom(c->n - 1, k - 1);
+    const unsigned long long n_items = total ? (unsigned long long)c->nm * NP : 0;
+    if (item_hi > n_items) item_hi = n_items;
+    if (item_lo > item_hi) item_lo = item_hi;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    RangeGeom G;
+    memset(&G, 0, sizeof(G));
+    G.k = k;
+    G.nbm = c->nb * c->nm;
+    G.NC = NC;
+    G.NP = NP;
+    G.nm = c->nm;
+    G.items_mode = 1;
+    G.it_lo = item_lo;
+    G.it_span = item_hi > item_lo ? item_hi - item_lo : 1;
+    G.lo = 0;
+    G.hi = (unsigned long long)c->nb * (item_hi - item_lo) * NC;
+    c->last_lo = 0;
+    c->last_hi = G.hi;
+    c->last_geom = G;
+    CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));
+    const int fl = known_flags(c);
+    const bool generic = fl > 0 || k < 3 || c->force_mode == 3 || c->force_mode == 4 ||
+                         c->nb > 4 || !c->sweep_ok || G.hi == 0;
+    if (!generic) {
+        int mode = c->force_mode >= 0 && c->force_mode <= 2 ? c->force_mode : 2;
+        const uint32_t* dflags = fl < 0 ? c->flagsbuf.p : nullptr;
+        int st = launch_sweep(c, G, item_lo, item_hi, mode, dflags);
+        if (st != GP_OK || fl >= 0) return st;
+        return launch_fixup(c, G);
+    }
+    unsigned long long grid = G.hi ? (G.hi + 255) / 256 : 1;
+    unsigned long long gmax = (unsigned long long)c->n_sms * 16;
+    if (grid > gmax) grid = gmax;
+    ArgminScratch S;
+    S.blk = c->blk.p;
+    S.counter = c->counter.p;
+    S.result = c->result.p;
+    S.err = nullptr;
+    S.err_idx = c->err_idx.p;
+    DevInst I = c->view();
+    k3_argmin_generic<<<(unsigned)grid, 256, 0, s>>>(I, G, S, nullptr);
+    CUDA_TRY(cudaGetLastError());
+    return GP_OK;
 }
 
 int gp_solve(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* best, gp_plan_info* info) {
