@@ -149,6 +149,26 @@ typedef struct gp_group_info {
     double dp_fraction[GP_MAX_SGS];       /* second-level data fractions   */
 } gp_group_info;
 
+/*
+ * One pipeline timing (PlanTiming, src/timing.py:47-101) for the 1F1B
+ * simulator: per-stage seconds per sample and closing costs, per-boundary
+ * gateway link and bytes per sample.  Boundary arrays use n_stages-1 slots.
+ */
+typedef struct gp_timing {
+    uint32_t n_stages;                 /* S, 1..GP_MAX_STAGES            */
+    uint32_t pad;
+    int64_t batch, microbatch;         /* PlanTiming.batch / .microbatch */
+    double fwd[GP_MAX_STAGES];         /* StageTiming.fwd_per_sample     */
+    double bwd[GP_MAX_STAGES];         /* .bwd_per_sample                */
+    double wgt[GP_MAX_STAGES];         /* .wgt_per_sample                */
+    double sync[GP_MAX_STAGES];        /* .sync_seconds                  */
+    double opt[GP_MAX_STAGES];         /* .opt_seconds                   */
+    double lat[GP_MAX_STAGES];         /* BoundaryTiming.latency_seconds */
+    double bw[GP_MAX_STAGES];          /* .bandwidth_bytes_per_s         */
+    double act[GP_MAX_STAGES];         /* .act_bytes_per_sample          */
+    double grad[GP_MAX_STAGES];        /* .grad_bytes_per_sample         */
+} gp_timing;
+
 typedef struct gp_ctx gp_ctx;
 
 /* Version / capability probe (no device needed). */
@@ -219,6 +239,18 @@ int gp_group_splits(gp_ctx *ctx, uint32_t f, gp_group_info *out);
  * min_intra_bandwidth and the boundary tables on the device.
  */
 int gp_set_bandwidth(gp_ctx *ctx, const double *bandwidth);
+
+/*
+ * 1F1B makespans (kernel K5): makespan[i] = simulate_timing(timings[i],
+ * Policy.ONE_F_ONE_B, CONSTANT_TRACE, adapter_enabled=False,
+ * SimConfig(iterations)).makespan; status[i] = GP_OK or GP_ERR_SCHEDULING /
+ * GP_ERR_TIMING.  Host pointers; the context need not be loaded.
+ */
+int gp_sim_1f1b(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t iterations,
+                double *makespan, uint8_t *status);
+/* Same with device pointers, asynchronous on the context's stream. */
+int gp_sim_1f1b_device(gp_ctx *ctx, const gp_timing *d_timings, uint64_t n,
+                       uint32_t iterations, double *d_makespan, uint8_t *d_status);
 
 /* Stream the context uses (cudaStream_t), for event timing by callers. */
 void *gp_ctx_stream(gp_ctx *ctx);

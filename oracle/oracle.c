@@ -758,3 +758,296 @@ size_t or_abi_sizeof(int which)
     default: return 0;
     }
 }
+
+/* ------------------------------------------------------------------------
+ * PipelineEngine.run for Policy.ONE_F_ONE_B, constant trace, no adapter,
+ * synchronous iterations (src/engine.py:125-431, src/nettrace.py:57-76).
+ * A direct restatement with the reference's data structures: per
+ * (stage, iteration) pools, FIFO link queues, a (time, seq) binary heap.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int64_t fwd_avail, fwd_taken, fwd_done, bwd_avail, bwd_taken, bwd_done;
+    int64_t wq_head, wq_tail, w_done;   /* w_queue as a FIFO of sizes */
+    int64_t *wq;                        /* sizes */
+    int sync_done, opt_done, activated;
+} sim_pool;
+
+typedef struct {
+    double t;
+    uint64_t seq;
+    int kind;           /* 0 op, 1 transfer */
+    int s, op, it;      /* op: stage, op kind (0 F,1 B,2 W,3 S,4 O), iteration */
+    int64_t size;       /* also transfer size; for transfers s=boundary, op=dir */
+} sim_ev;
+
+typedef struct {
+    sim_ev *h;
+    int n, cap;
+} sim_heap;
+
+static int ev_less(const sim_ev *a, const sim_ev *b)
+{
+    return a->t < b->t || (a->t == b->t && a->seq < b->seq);
+}
+
+static void heap_push(sim_heap *H, sim_ev e)
+{
+    if (H->n == H->cap) {
+        H->cap = H->cap ? 2 * H->cap : 64;
+        H->h = (sim_ev *)realloc(H->h, sizeof(sim_ev) * (size_t)H->cap);
+    }
+    int i = H->n++;
+    H->h[i] = e;
+    while (i > 0) {
+        int p = (i - 1) / 2;
+        if (!ev_less(&H->h[i], &H->h[p]))
+            break;
+        sim_ev t = H->h[i];
+        H->h[i] = H->h[p];
+        H->h[p] = t;
+        i = p;
+    }
+}
+
+static sim_ev heap_pop(sim_heap *H)
+{
+    sim_ev top = H->h[0];
+    H->h[0] = H->h[--H->n];
+    int i = 0;
+    for (;;) {
+        int l = 2 * i + 1, r = l + 1, m = i;
+        if (l < H->n && ev_less(&H->h[l], &H->h[m]))
+            m = l;
+        if (r < H->n && ev_less(&H->h[r], &H->h[m]))
+            m = r;
+        if (m == i)
+            break;
+        sim_ev t = H->h[i];
+        H->h[i] = H->h[m];
+        H->h[m] = t;
+        i = m;
+    }
+    return top;
+}
+
+typedef struct {
+    int64_t *q_size;
+    int *q_it;
+    int64_t head, tail;
+    int busy;
+} sim_link;
+
+int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
+{
+    const int S = (int)T->n_stages;
+    if (S < 1 || S > GP_MAX_STAGES || iterations < 1)
+        return GP_ERR_TIMING;
+    const int64_t B = T->batch, m = T->microbatch;
+    const int64_t per_it = B / (m > 0 ? m : 1) + 2;
+    sim_pool *pools = (sim_pool *)calloc((size_t)S * iterations, sizeof(sim_pool));
+    for (int i = 0; i < S * iterations; ++i)
+        pools[i].wq = (int64_t *)calloc((size_t)per_it + 1, sizeof(int64_t));
+#define POOL(s, it) (&pools[(s) * iterations + (it)])
+    int cur[GP_MAX_STAGES], busy[GP_MAX_STAGES], closed_cnt = 0;
+    int *stages_closed = (int *)calloc((size_t)iterations, sizeof(int));
+    sim_link links[2 * GP_MAX_STAGES];
+    const int64_t lcap = per_it * iterations + 1;
+    for (int l = 0; l < 2 * (S - 1); ++l) {
+        links[l].q_size = (int64_t *)calloc((size_t)lcap, sizeof(int64_t));
+        links[l].q_it = (int *)calloc((size_t)lcap, sizeof(int));
+        links[l].head = links[l].tail = 0;
+        links[l].busy = 0;
+    }
+    (void)closed_cnt;
+    sim_heap H = {NULL, 0, 0};
+    uint64_t seq = 0;
+    for (int s = 0; s < S; ++s) {
+        cur[s] = 0;
+        busy[s] = 0;
+        POOL(s, 0)->activated = 1;
+        if (s == 0)
+            POOL(s, 0)->fwd_avail = B;
+    }
+
+    /* try_start_link (src/engine.py:276-289) */
+#define TRY_START(tnow, bnd, dir)                                                          \
+    do {                                                                                   \
+        sim_link *L_ = &links[2 * (bnd) + (dir)];                                           \
+        if (!L_->busy && L_->head < L_->tail) {                                            \
+            int64_t sz_ = L_->q_size[L_->head];                                            \
+            int it_ = L_->q_it[L_->head];                                                  \
+            L_->head++;                                                                    \
+            L_->busy = 1;                                                                  \
+            double per_ = (dir) == 0 ? T->act[bnd] : T->grad[bnd];                         \
+            double bw_ = T->bw[bnd] * 1.0;                                                 \
+            double end_ = ((tnow) + (per_ * (double)sz_) / bw_) + T->lat[bnd];            \
+            sim_ev e_ = {end_, seq++, 1, (bnd), (dir), it_, sz_};                          \
+            heap_push(&H, e_);                                                             \
+        }                                                                                  \
+    } while (0)
+
+    double now = 0.0;
+    int first = 1;
+    for (;;) {
+        /* dispatch(now) (src/engine.py:335-341) */
+        int progress = 1;
+        while (progress) {
+            progress = 0;
+            for (int s = 0; s < S; ++s) {
+                if (busy[s])
+                    continue;
+                int it = cur[s];
+                if (it >= iterations)
+                    continue;
+                sim_pool *p = POOL(s, it);
+                /* _ready_op (src/engine.py:157-215), ONE_F_ONE_B */
+                int best_pr = 100, best_k = -1;
+                int64_t best_sz = 0;
+                int64_t size = m;
+                int64_t fwd_rem = B - p->fwd_taken;
+                if (fwd_rem > 0) {
+                    int64_t chunk = size < fwd_rem ? size : fwd_rem;
+                    if (p->fwd_avail - p->fwd_taken >= chunk) {
+                        int64_t quota = (int64_t)(S - s) * m;
+                        int pr = -1;
+                        if (p->fwd_taken < quota)
+                            pr = 1;
+                        else if (p->fwd_taken + chunk <= quota + p->bwd_done)
+                            pr = 2;
+                        if (pr >= 0 && pr < best_pr) {
+                            best_pr = pr;
+                            best_k = 0;
+                            best_sz = chunk;
+                        }
+                    }
+                }
+                int64_t bwd_rem = B - p->bwd_taken;
+                if (bwd_rem > 0) {
+                    int64_t chunk = size < bwd_rem ? size : bwd_rem;
+                    int64_t av = (p->bwd_avail < p->fwd_done ? p->bwd_avail : p->fwd_done) - p->bwd_taken;
+                    if (s == S - 1)
+                        av = p->fwd_done - p->bwd_taken;
+                    if (av >= chunk && 2 < best_pr) {
+                        best_pr = 2;
+                        best_k = 1;
+                        best_sz = chunk;
+                    }
+                }
+                if (p->wq_head < p->wq_tail && 0 < best_pr) {
+                    best_pr = 0;
+                    best_k = 2;
+                    best_sz = p->wq[p->wq_head];
+                }
+                if (p->w_done == B && p->wq_head == p->wq_tail && !p->sync_done && 8 < best_pr) {
+                    best_pr = 8;
+                    best_k = 3;
+                    best_sz = 0;
+                }
+                if (p->sync_done && !p->opt_done && 9 < best_pr) {
+                    best_pr = 9;
+                    best_k = 4;
+                    best_sz = 0;
+                }
+                if (best_k < 0)
+                    continue;
+                double dur;
+                switch (best_k) {
+                case 0: dur = T->fwd[s] * (double)best_sz; p->fwd_taken += best_sz; break;
+                case 1: dur = T->bwd[s] * (double)best_sz; p->bwd_taken += best_sz; break;
+                case 2: dur = T->wgt[s] * (double)best_sz; p->wq_head++; break;
+                case 3: dur = T->sync[s]; break;
+                default: dur = T->opt[s]; break;
+                }
+                busy[s] = 1;
+                sim_ev e = {now + dur, seq++, 0, s, best_k, it, best_sz};
+                heap_push(&H, e);
+                progress = 1;
+            }
+        }
+        if (H.n == 0)
+            break;
+        (void)first;
+        sim_ev e = heap_pop(&H);
+        now = e.t;
+        if (e.kind == 0) {
+            /* finish_op (src/engine.py:343-378) */
+            int s = e.s, it = e.it;
+            sim_pool *p = POOL(s, it);
+            busy[s] = 0;
+            if (e.op == 0) {
+                p->fwd_done += e.size;
+                if (s < S - 1) {
+                    sim_link *L = &links[2 * s + 0];
+                    L->q_size[L->tail] = e.size;
+                    L->q_it[L->tail] = it;
+                    L->tail++;
+                    TRY_START(now, s, 0);
+                }
+            } else if (e.op == 1) {
+                p->bwd_done += e.size;
+                p->wq[p->wq_tail++] = e.size;
+                if (s > 0) {
+                    sim_link *L = &links[2 * (s - 1) + 1];
+                    L->q_size[L->tail] = e.size;
+                    L->q_it[L->tail] = it;
+                    L->tail++;
+                    TRY_START(now, s - 1, 1);
+                }
+            } else if (e.op == 2) {
+                p->w_done += e.size;
+            } else if (e.op == 3) {
+                p->sync_done = 1;
+            } else {
+                p->opt_done = 1;
+                stages_closed[it] += 1;
+                cur[s] = it + 1;
+                if (it + 1 < iterations) {
+                    sim_pool *q = POOL(s, it + 1);
+                    if (!q->activated) {
+                        q->activated = 1;
+                        if (s == 0)
+                            q->fwd_avail = B;
+                    }
+                }
+            }
+        } else {
+            /* finish_transfer (src/engine.py:380-396) */
+            int bnd = e.s, dir = e.op;
+            links[2 * bnd + dir].busy = 0;
+            if (dir == 0)
+                POOL(bnd + 1, e.it)->fwd_avail += e.size;
+            else
+                POOL(bnd, e.it)->bwd_avail += e.size;
+            TRY_START(now, bnd, dir);
+        }
+    }
+    int status = GP_OK;
+    for (int s = 0; s < S; ++s)
+        if (cur[s] < iterations)
+            status = GP_ERR_SCHEDULING;
+    *makespan_out = now;
+    for (int i = 0; i < S * iterations; ++i)
+        free(pools[i].wq);
+    free(pools);
+    free(stages_closed);
+    for (int l = 0; l < 2 * (S - 1); ++l) {
+        free(links[l].q_size);
+        free(links[l].q_it);
+    }
+    free(H.h);
+#undef POOL
+#undef TRY_START
+    return status;
+}
+
+int or_sim_batch(const gp_timing *T, uint64_t n, int iterations, double *makespan,
+                 uint8_t *status)
+{
+    for (uint64_t i = 0; i < n; ++i) {
+        double ms = NAN;
+        int st = or_sim_1f1b(&T[i], iterations, &ms);
+        makespan[i] = ms;
+        status[i] = (uint8_t)st;
+    }
+    return GP_OK;
+}

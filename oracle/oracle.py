@@ -54,6 +54,9 @@ def lib():
                                     P(C.c_uint8), P(C.c_uint8), P(C.c_uint8),
                                     P(C.c_double), P(C.c_uint8), C.c_int]
         L.or_group_detail.argtypes = [P(abi.GpInstance), C.c_uint32, P(abi.GpGroupInfo)]
+        L.or_sim_1f1b.argtypes = [P(abi.GpTiming), C.c_int, P(C.c_double)]
+        L.or_sim_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, P(C.c_double),
+                                   P(C.c_uint8)]
         _lib = L
     return _lib
 
@@ -140,3 +143,11 @@ def group_detail(packed, f):
     g = abi.GpGroupInfo()
     lib().or_group_detail(C.byref(packed.struct), int(f), C.byref(g))
     return g
+
+
+def sim_batch(packed_timings, n, iterations=1):
+    """(makespans, status) of gp_timing records (simulate.pack_timings)."""
+    ms = np.empty(n, dtype=np.float64)
+    st = np.empty(n, dtype=np.uint8)
+    lib().or_sim_batch(packed_timings, n, int(iterations), _dp(ms), _u8(st))
+    return ms, st

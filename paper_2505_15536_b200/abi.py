@@ -112,3 +112,15 @@ class GpGroupInfo(C.Structure):
         ("tp_col", C.c_double * GP_MAX_MEMBERS),
         ("dp_fraction", C.c_double * GP_MAX_SGS),
     ]
+
+
+class GpTiming(C.Structure):
+    _fields_ = [
+        ("n_stages", C.c_uint32), ("pad", C.c_uint32),
+        ("batch", C.c_int64), ("microbatch", C.c_int64),
+        ("fwd", C.c_double * GP_MAX_STAGES), ("bwd", C.c_double * GP_MAX_STAGES),
+        ("wgt", C.c_double * GP_MAX_STAGES), ("sync", C.c_double * GP_MAX_STAGES),
+        ("opt", C.c_double * GP_MAX_STAGES), ("lat", C.c_double * GP_MAX_STAGES),
+        ("bw", C.c_double * GP_MAX_STAGES), ("act", C.c_double * GP_MAX_STAGES),
+        ("grad", C.c_double * GP_MAX_STAGES),
+    ]

@@ -59,6 +59,8 @@ def lib():
         L.gp_group_splits.argtypes = [vp, C.c_uint32, P(abi.GpGroupInfo)]
         L.gp_set_bandwidth.argtypes = [vp, P(C.c_double)]
         L.gp_diag_fp64_peak.argtypes = [C.c_int, P(C.c_double)]
+        L.gp_sim_1f1b.argtypes = [vp, vp, C.c_uint64, C.c_uint32, P(C.c_double), u8p]
+        L.gp_sim_1f1b_device.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
         _lib = L
         return L
@@ -169,6 +171,16 @@ class Engine:
         g = abi.GpGroupInfo()
         _check(lib().gp_group_splits(self._h, int(f), C.byref(g)))
         return g
+
+    def sim_1f1b(self, packed_timings, n: int, iterations: int = 1):
+        """(makespans, status) for gp_timing records (simulate.pack_timings)."""
+        ms = np.empty(n, dtype=np.float64)
+        st = np.empty(n, dtype=np.uint8)
+        if n:
+            _check(lib().gp_sim_1f1b(self._h, C.cast(packed_timings, C.c_void_p), n,
+                                     int(iterations),
+                                     ms.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
+        return ms, st
 
     def set_k3_mode(self, mode: int) -> None:
         """Force the exhaustive-kernel variant (-1 auto, 0/1/2, 3 generic)."""

@@ -153,9 +153,52 @@ def dump_c4(name, jitter):
     G.save(f"{name}.json", doc)
 
 
+def timing_to_dict(t):
+    return {"batch": t.batch, "microbatch": t.microbatch,
+            "stages": [[st.fwd_per_sample, st.bwd_per_sample, st.wgt_per_sample,
+                        st.sync_seconds, st.opt_seconds] for st in t.stages],
+            "boundaries": [[b.latency_seconds, b.bandwidth_bytes_per_s,
+                            b.act_bytes_per_sample, b.grad_bytes_per_sample]
+                           for b in t.boundaries]}
+
+
+def dump_sim():
+    """1F1B makespans (simulate_timing, ONE_F_ONE_B) of random and plan timings."""
+    gp = geopipe()
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from test_schedule import random_timing
+    from test_acceptance import _random_instance
+    rng = random.Random(2024)
+    cases = [random_timing(rng) for _ in range(1500)]
+    # timings of real plans: winners and random candidates of the golden configs
+    for seed in range(100, 130):
+        topo, groups, model = _random_instance(seed)
+        res = gp.search_plan(model, topo, groups, gp.SearchConfig(seed=seed))
+        cases.append(gp.build_plan_timing(res.plan, topo, model, groups))
+    for cfg_name, jit in [("c1", False), ("c2", True), ("c4", False)]:
+        model, topo, groups = build_reference(I.config(cfg_name, jit))
+        res = gp.search_plan(model, topo, groups, gp.SearchConfig(seed=0))
+        for opt in (0.0, 0.25):
+            cases.append(gp.build_plan_timing(res.plan, topo, model, groups, opt_seconds=opt))
+    out = {"timings": [timing_to_dict(t) for t in cases], "makespan": {}}
+    t0 = time.time()
+    for it in (1, 2, 3):
+        ms = []
+        for t in cases:
+            try:
+                ms.append(gp.simulate_timing(t, gp.Policy.ONE_F_ONE_B,
+                                             config=gp.SimConfig(iterations=it)).makespan)
+            except Exception as e:
+                ms.append(type(e).__name__)
+        out["makespan"][str(it)] = ms
+    G.save("sim.json", out)
+    print(f"sim: {len(cases)} timings x 3 iteration counts, {time.time() - t0:.1f}s", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c4", action="store_true")
+    ap.add_argument("--only-sim", action="store_true")
     args = ap.parse_args()
     if not AVAILABLE:
         sys.exit("reference not available at /root/reference")
@@ -163,6 +206,9 @@ def main():
     sys.path.insert(0, "/root/reference/pkg/tests")
     import conftest as rc  # reference test fixtures (read-only import)
     os.makedirs(G.GOLDEN, exist_ok=True)
+    dump_sim()
+    if args.only_sim:
+        return
 
     for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
                                 ("c2", "c2", False), ("c2j", "c2", True)]:

@@ -1,0 +1,103 @@
+"""1F1B makespan (K5) vs the reference's discrete-event engine.
+
+Goldens: tests/golden/sim.json = simulate_timing(t, ONE_F_ONE_B,
+SimConfig(iterations=1|2|3)).makespan of 1,500 random timings
+(tests/test_schedule.py:random_timing) and of real plan timings
+(build_plan_timing of search_plan winners, incl. C1/C2/C4).
+"""
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from paper_2505_15536_b200 import simulate as SM
+
+SIM = G.load("sim.json")
+
+
+def _timing(d):
+    stages = tuple(SM.StageTiming(f, b, w, sy, sy, op, 1.0) for f, b, w, sy, op in d["stages"])
+    bounds = tuple(SM.BoundaryTiming(f"{i}-{i + 1}", lat, bw, act, grad)
+                   for i, (lat, bw, act, grad) in enumerate(d["boundaries"]))
+    return SM.PlanTiming(stages, bounds, d["batch"], d["microbatch"])
+
+
+TIMINGS = [_timing(d) for d in SIM["timings"]]
+
+
+def _expected(it):
+    ms = SIM["makespan"][str(it)]
+    return np.array([m if not isinstance(m, str) else np.nan for m in ms]), \
+        np.array([0 if not isinstance(m, str) else 8 for m in ms], np.uint8)
+
+
+def _random_timings(n, seed):
+    rng = random.Random(seed)
+    out = []
+    for _ in range(n):
+        S = rng.randint(1, 6)
+        micro = rng.choice([1, 2, 4, 8])
+        out.append(SM.make_timing(
+            fwd=[rng.uniform(0.2, 2.0) for _ in range(S)],
+            bwd=[rng.uniform(0.2, 2.0) for _ in range(S)],
+            wgt=[rng.uniform(0.05, 1.0) for _ in range(S)],
+            transfer=[rng.uniform(0.05, 2.5) for _ in range(S - 1)],
+            microbatch=micro, micro_count=rng.randint(1, 12),
+            sync=[rng.uniform(0.0, 0.5) for _ in range(S)],
+            opt=[rng.uniform(0.0, 0.3) for _ in range(S)],
+            latency=rng.uniform(0.0, 0.2)))
+    return out
+
+
+@pytest.mark.parametrize("it", [1, 2, 3])
+def test_oracle_sim_matches_reference(oracle_lib, it):
+    arr = SM.pack_timings(TIMINGS)
+    ms, st = oracle_lib.sim_batch(arr, len(TIMINGS), it)
+    exp, est = _expected(it)
+    assert (st == est).all()
+    assert (ms.view(np.uint64) == exp.view(np.uint64)).all()
+
+
+def test_reference_schedule_kats(oracle_lib):
+    # tests/test_schedule.py:97-104 (single stage, 1F1B): 2*(1+2+0.5)+0.25+0.75
+    t = SM.make_timing(fwd=[1.0], bwd=[2.0], wgt=[0.5], transfer=[], microbatch=1,
+                       micro_count=2, sync=[0.25], opt=[0.75])
+    ms, st = oracle_lib.sim_batch(SM.pack_timings([t]), 1, 1)
+    assert st[0] == 0 and ms[0] == pytest.approx(2 * (1 + 2 + 0.5) + 0.25 + 0.75)
+    # tests/test_schedule.py:115-120: three iterations take three times as long
+    t = SM.make_timing(fwd=[1.0, 1.0], bwd=[1.0, 1.0], wgt=[0.5, 0.5], transfer=[0.3],
+                       microbatch=1, micro_count=3)
+    one, _ = oracle_lib.sim_batch(SM.pack_timings([t]), 1, 1)
+    three, _ = oracle_lib.sim_batch(SM.pack_timings([t]), 1, 3)
+    assert three[0] == pytest.approx(3 * one[0])
+
+
+def test_pack_rejects_inconsistent_timing():
+    from paper_2505_15536_b200 import domain as D
+    bad = SM.PlanTiming(TIMINGS[0].stages, TIMINGS[0].boundaries + TIMINGS[0].boundaries[:1]
+                        if TIMINGS[0].boundaries else (SM.BoundaryTiming("x", 0, 1, 1, 1),),
+                        4, 2)
+    with pytest.raises(D.InvalidTimingError):
+        SM.pack_timings([bad])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("it", [1, 2, 3])
+def test_k5_matches_reference(engine, it):
+    ms = SM.simulate_makespans(TIMINGS, it, engine=engine)
+    exp, _ = _expected(it)
+    assert (ms.view(np.uint64) == exp.view(np.uint64)).all()
+
+
+@pytest.mark.gpu
+def test_k5_matches_oracle_large(engine, oracle_lib):
+    tims = _random_timings(20000, 11)
+    arr = SM.pack_timings(tims)
+    for it in (1, 2):
+        ms, st = engine.sim_1f1b(arr, len(tims), it)
+        oms, ost = oracle_lib.sim_batch(arr, len(tims), it)
+        assert (st == ost).all()
+        assert (ms.view(np.uint64) == oms.view(np.uint64)).all()
