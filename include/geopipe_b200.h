@@ -252,6 +252,16 @@ int gp_sim_1f1b(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t iter
 int gp_sim_1f1b_device(gp_ctx *ctx, const gp_timing *d_timings, uint64_t n,
                        uint32_t iterations, double *d_makespan, uint8_t *d_status);
 
+/*
+ * 1F1B makespans of explicit candidates (same encoding as gp_eval_batch):
+ * simulate(build_plan(...), ..., Policy.ONE_F_ONE_B,
+ * SimConfig(iterations, opt_seconds)).makespan (src/simulator.py:116-128).
+ * status GP_ERR_NO_FEASIBLE marks memory-infeasible plans.
+ */
+int gp_sim_candidates(gp_ctx *ctx, uint32_t k, uint64_t n, const uint8_t *order,
+                      const uint8_t *counts, const uint8_t *bm, uint32_t iterations,
+                      double opt_seconds, double *makespan, uint8_t *status);
+
 /* Stream the context uses (cudaStream_t), for event timing by callers. */
 void *gp_ctx_stream(gp_ctx *ctx);
 

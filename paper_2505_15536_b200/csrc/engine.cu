@@ -99,6 +99,7 @@ struct DevInst {
     uint8_t* scode;              // [F][(n+1)^2]
     uint8_t* skind;              // [F][(n+1)^2]
     double* C1;                  // [F][(n+1)^2] per-sample (F+Bi)+W (detail)
+    double4* fbws;               // [F][(n+1)^2] {F, Bi, W per sample, sync seconds} (K5)
     int* gw;                     // [F*F] gateway u*D+v
     double* xt;                  // [nm][F][F][nxp] (rows padded to 16 B)
     int nxp;                     // x row stride: n rounded up to even
@@ -236,6 +237,7 @@ __global__ void k1_stages(DevInst I) {
         I.scode[e] = SC_INFEASIBLE;
         I.skind[e] = 0;
         I.C1[e] = INFINITY;
+        I.fbws[e] = make_double4(NAN, NAN, NAN, NAN);
         for (int mi = 0; mi < I.nm; ++mi) {
             I.stg[(size_t)mi * I.F * N2 + e] = make_double2(INFINITY, 0.0);
             if (a == n && b == n) I.tcol[((size_t)mi * I.F + f) * (n + 1) + n] = make_double2(INFINITY, 0.0);
@@ -297,6 +299,9 @@ __global__ void k1_stages(DevInst I) {
     int nmem = m1 - m0;
     bool has = I.fg_has_minbw[f] != 0;
     double mbw = I.fg_minbw[f];
+    // StageTiming.sync_seconds = intra_group_seconds(params, fg) (src/timing.py:195)
+    double sync = (P == 0.0 || !has) ? 0.0 : (mbw > 0 ? P / mbw : NAN);
+    I.fbws[e] = make_double4(Fp, Bp, Wp, sync);
     if (code == SC_OK && has && !(mbw > 0) && (nmem >= 2 || P != 0.0)) code = SC_TOPOLOGY;
     bool overflow = false;
     for (int mi = 0; mi < I.nm; ++mi) {
@@ -1417,6 +1422,57 @@ __device__ int sim_1f1b_dev(const gp_timing& T, int iterations, double* makespan
     return GP_OK;
 }
 
+// 1F1B makespan of explicit candidates: the PlanTiming of build_plan_timing
+// (src/timing.py:176-231) assembled from the stage / boundary tables.
+__global__ void k5_sim_candidates(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
+                                  const uint8_t* __restrict__ counts, const uint8_t* __restrict__ bm,
+                                  int iterations, double opt_seconds, double* __restrict__ makespan,
+                                  uint8_t* __restrict__ status) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncand) return;
+    uint8_t o[GP_MAX_STAGES];
+    int p[GP_MAX_STAGES + 1];
+    p[0] = 0;
+    int st = GP_OK;
+    unsigned seen = 0;
+    for (int s = 0; s < k; ++s) {
+        o[s] = order[i * k + s];
+        int c = counts[i * k + s];
+        if (o[s] >= I.F || (seen >> o[s]) & 1u || c == 0) st = GP_ERR_INPUT;
+        seen |= 1u << (o[s] & 31);
+        p[s + 1] = p[s] + c;
+    }
+    int b = bm[i];
+    if (b >= I.nb * I.nm || p[k] > I.n) st = GP_ERR_INPUT;
+    int mi = b % I.nm;
+    if (st == GP_OK) {
+        long long M = I.batch[b / I.nm] / I.micro[mi];
+        EvalOut r = eval_tables(I, k, o, p, mi, M);  // feasibility + errors, as _evaluate
+        st = r.status;
+        if (st == GP_OK && isinf(r.cost)) st = GP_ERR_NO_FEASIBLE;  // memory-infeasible plan
+    }
+    if (st != GP_OK) { makespan[i] = NAN; status[i] = (uint8_t)st; return; }
+    const size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
+    gp_timing T;
+    T.n_stages = (uint32_t)k;
+    T.batch = I.batch[b / I.nm];
+    T.microbatch = I.micro[mi];
+    for (int s = 0; s < k; ++s) {
+        double4 v = I.fbws[(size_t)o[s] * N2 + tri_idx(I.n, p[s], p[s + 1])];
+        T.fwd[s] = v.x; T.bwd[s] = v.y; T.wgt[s] = v.z; T.sync[s] = v.w; T.opt[s] = opt_seconds;
+        if (s + 1 < k) {
+            int g = I.gw[o[s] * I.F + o[s + 1]];
+            T.lat[s] = I.lat[g];
+            T.bw[s] = I.bw[g];
+            T.act[s] = T.grad[s] = I.act[p[s + 1] - 1];
+        }
+    }
+    double ms = NAN;
+    st = sim_1f1b_dev(T, iterations, &ms);
+    makespan[i] = ms;
+    status[i] = (uint8_t)st;
+}
+
 __global__ void k5_sim_1f1b(const gp_timing* __restrict__ T, long long n, int iterations,
                             double* __restrict__ makespan, uint8_t* __restrict__ status) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1460,12 +1516,18 @@ struct gp_ctx {
     uint32_t flags = 0;
     int n = 0, F = 0, D = 0, nb = 0, nm = 0, nsg = 0;
     std::vector<long long> h_batch, h_micro;
-    DBuf<double> fwd, bwd_in, bwd_w, act, param, p_c, mem, p_t, lat, bw, fg_cap, sg_cap, fg_minbw,
-        fg_minbw_in, S, g_rf, g_cf, g_dp, g_minmem, sg_minmem, C1, xt;
+    // raw instance arrays live in the arena (one allocation, one H2D copy)
+    ArenaPtr<double> fwd, bwd_in, bwd_w, act, param, p_c, mem, p_t, lat, bw, fg_cap, sg_cap,
+        fg_minbw, fg_minbw_in;
+    ArenaPtr<long long> batch, micro;
+    ArenaPtr<uint32_t> id_rank, fg_off, fg_mem, fg_sg_off, sg_off, sg_mem;
+    ArenaPtr<uint8_t> fg_has;
+    // derived tables
+    DBuf<double> S, g_rf, g_cf, g_dp, g_minmem, sg_minmem, C1, xt;
+    DBuf<double4> fbws;
     DBuf<double2> tpk, tcol;
-    DBuf<long long> batch, micro;
-    DBuf<uint32_t> id_rank, fg_off, fg_mem, fg_sg_off, sg_off, sg_mem, flagsbuf;
-    DBuf<uint8_t> fg_has, g_tp_ok, scode, skind;
+    DBuf<uint32_t> flagsbuf;
+    DBuf<uint8_t> g_tp_ok, scode, skind;
     DBuf<double2> stg;
     DBuf<int> gw;
     // K3 scratch
@@ -1524,7 +1586,7 @@ struct gp_ctx {
         I.bf = bf;
         I.S = S.p; I.g_tp_ok = g_tp_ok.p; I.g_rf = g_rf.p; I.g_cf = g_cf.p; I.g_dp = g_dp.p;
         I.g_minmem = g_minmem.p; I.sg_minmem = sg_minmem.p;
-        I.stg = stg.p; I.scode = scode.p; I.skind = skind.p; I.C1 = C1.p;
+        I.stg = stg.p; I.scode = scode.p; I.skind = skind.p; I.C1 = C1.p; I.fbws = fbws.p;
         I.gw = gw.p; I.xt = xt.p; I.flags = flagsbuf.p;
         I.nxp = (n + 1) & ~1;
         I.tpk = tpk.p; I.tcol = tcol.p;
@@ -1591,17 +1653,13 @@ void gp_ctx_destroy(gp_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    DBuf<double>* dd[] = {&c->fwd, &c->bwd_in, &c->bwd_w, &c->act, &c->param, &c->p_c, &c->mem,
-                          &c->p_t, &c->lat, &c->bw, &c->fg_cap, &c->sg_cap, &c->fg_minbw,
-                          &c->fg_minbw_in, &c->S, &c->g_rf, &c->g_cf, &c->g_dp, &c->g_minmem,
-                          &c->sg_minmem, &c->C1, &c->xt, &c->b_cost};
+    DBuf<double>* dd[] = {&c->S, &c->g_rf, &c->g_cf, &c->g_dp, &c->g_minmem, &c->sg_minmem,
+                          &c->C1, &c->xt, &c->b_cost};
     for (auto* b : dd) b->release();
-    c->batch.release(); c->micro.release();
-    DBuf<uint32_t>* uu[] = {&c->id_rank, &c->fg_off, &c->fg_mem, &c->fg_sg_off, &c->sg_off,
-                            &c->sg_mem, &c->flagsbuf};
-    for (auto* b : uu) b->release();
-    DBuf<uint8_t>* bb[] = {&c->fg_has, &c->g_tp_ok, &c->scode, &c->skind, &c->b_order,
-                           &c->b_counts, &c->b_bm, &c->b_status};
+    c->fbws.release();
+    c->flagsbuf.release();
+    DBuf<uint8_t>* bb[] = {&c->g_tp_ok, &c->scode, &c->skind, &c->b_order, &c->b_counts,
+                           &c->b_bm, &c->b_status};
     for (auto* b : bb) b->release();
     c->arena.release();
     if (c->h_arena) cudaFreeHost(c->h_arena);
@@ -1755,6 +1813,7 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     CUDA_TRY(c->scode.ensure((size_t)F * N2));
     CUDA_TRY(c->skind.ensure((size_t)F * N2));
     CUDA_TRY(c->C1.ensure((size_t)F * N2));
+    CUDA_TRY(c->fbws.ensure((size_t)F * N2));
     CUDA_TRY(c->gw.ensure((size_t)F * F));
     CUDA_TRY(c->xt.ensure((size_t)c->nm * F * F * ((n + 1) & ~1u)));
     CUDA_TRY(c->tpk.ensure((size_t)c->nm * F * ((size_t)n * (n + 1) / 2)));
@@ -2365,6 +2424,34 @@ int gp_sim_1f1b(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t iterat
     if (st != GP_OK) return st;
     CUDA_TRY(cudaMemcpyAsync(makespan, c->s_ms.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return GP_OK;
+}
+
+int gp_sim_candidates(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* order,
+                      const uint8_t* counts, const uint8_t* bm, uint32_t iterations,
+                      double opt_seconds, double* makespan, uint8_t* status) {
+    if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    if (k < 1 || k > GP_MAX_STAGES) return fail(GP_ERR_INPUT, "k=%u outside [1,%d]", k, GP_MAX_STAGES);
+    if (n == 0) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->b_order.ensure(n * k));
+    CUDA_TRY(c->b_counts.ensure(n * k));
+    CUDA_TRY(c->b_bm.ensure(n));
+    CUDA_TRY(c->b_cost.ensure(n));
+    CUDA_TRY(c->b_status.ensure(n));
+    CUDA_TRY(cudaMemcpyAsync(c->b_order.p, order, n * k, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->b_counts.p, counts, n * k, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->b_bm.p, bm, n, cudaMemcpyHostToDevice, s));
+    DevInst I = c->view();
+    k5_sim_candidates<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(I, (int)k, (long long)n, c->b_order.p,
+                                                                 c->b_counts.p, c->b_bm.p,
+                                                                 (int)iterations, opt_seconds,
+                                                                 c->b_cost.p, c->b_status.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(makespan, c->b_cost.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status, c->b_status.p, n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return GP_OK;
 }

@@ -61,6 +61,8 @@ def lib():
         L.gp_diag_fp64_peak.argtypes = [C.c_int, P(C.c_double)]
         L.gp_sim_1f1b.argtypes = [vp, vp, C.c_uint64, C.c_uint32, P(C.c_double), u8p]
         L.gp_sim_1f1b_device.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp]
+        L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
+                                        C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
         _lib = L
         return L
@@ -180,6 +182,20 @@ class Engine:
             _check(lib().gp_sim_1f1b(self._h, C.cast(packed_timings, C.c_void_p), n,
                                      int(iterations),
                                      ms.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
+        return ms, st
+
+    def sim_candidates(self, order, counts, bm, iterations: int = 1, opt_seconds: float = 0.0):
+        """1F1B makespans of explicit candidates of the loaded instance."""
+        order = np.ascontiguousarray(order, dtype=np.uint8)
+        counts = np.ascontiguousarray(counts, dtype=np.uint8)
+        bm = np.ascontiguousarray(bm, dtype=np.uint8)
+        n, k = order.shape
+        ms = np.empty(n, dtype=np.float64)
+        st = np.empty(n, dtype=np.uint8)
+        if n:
+            _check(lib().gp_sim_candidates(self._h, k, n, _u8(order), _u8(counts), _u8(bm),
+                                           int(iterations), float(opt_seconds),
+                                           ms.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
         return ms, st
 
     def set_k3_mode(self, mode: int) -> None:

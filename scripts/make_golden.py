@@ -195,6 +195,36 @@ def dump_sim():
     print(f"sim: {len(cases)} timings x 3 iteration counts, {time.time() - t0:.1f}s", flush=True)
 
 
+def dump_sim_candidates():
+    """simulate(build_plan(candidate), ONE_F_ONE_B) makespans of candidates."""
+    gp = geopipe()
+    from geopipe.planner import build_plan, memory_feasible
+    out = {}
+    t0 = time.time()
+    for name, cfg_name, jit, nsample in [("c1", "c1", False, None), ("c2j", "c2", True, 600),
+                                         ("c4", "c4", False, 300)]:
+        model, topo, groups = build_reference(I.config(cfg_name, jit))
+        allc = list(enumerate_all(model, groups))
+        rng = random.Random(17)
+        idx = range(len(allc)) if nsample is None else sorted(rng.sample(range(len(allc)), nsample))
+        rows = []
+        for i in idx:
+            bm, b, m, cand = allc[i]
+            plan = build_plan(cand, b, m, groups, topo, model, 1.25)
+            if not memory_feasible(plan, model, groups, topo):
+                rows.append([i, "infeasible", "infeasible"])
+                continue
+            vals = []
+            for it, opt in ((1, 0.0), (2, 0.5)):
+                r = gp.simulate(plan, topo, model, groups, gp.Policy.ONE_F_ONE_B,
+                                config=gp.SimConfig(iterations=it, opt_seconds=opt))
+                vals.append(r.makespan)
+            rows.append([i] + vals)
+        out[name] = rows
+    G.save("sim_cands.json", out)
+    print(f"sim candidates: {time.time() - t0:.1f}s", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c4", action="store_true")
@@ -207,6 +237,7 @@ def main():
     import conftest as rc  # reference test fixtures (read-only import)
     os.makedirs(G.GOLDEN, exist_ok=True)
     dump_sim()
+    dump_sim_candidates()
     if args.only_sim:
         return
 

@@ -101,3 +101,27 @@ def test_k5_matches_oracle_large(engine, oracle_lib):
         oms, ost = oracle_lib.sim_batch(arr, len(tims), it)
         assert (st == ost).all()
         assert (ms.view(np.uint64) == oms.view(np.uint64)).all()
+
+
+SIMC = G.load("sim_cands.json")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c2j", "c4"])
+def test_k5_candidates_match_reference_simulate(engine, oracle_lib, name):
+    from cases import load_case
+    from paper_2505_15536_b200.layout import PackedInstance
+    doc, model, topo, groups = load_case(name)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    engine.load(packed)
+    rows = SIMC[name]
+    dec = [oracle_lib.decode(packed, r[0]) for r in rows]
+    order = np.stack([d[0] for d in dec]); counts = np.stack([d[1] for d in dec])
+    bm = np.array([d[2] for d in dec], np.uint8)
+    for col, (it, opt) in enumerate(((1, 0.0), (2, 0.5))):
+        ms, st = engine.sim_candidates(order, counts, bm, it, opt)
+        for r, m_, s_ in zip(rows, ms, st):
+            if r[1 + col] == "infeasible":
+                assert s_ == 3
+            else:
+                assert s_ == 0 and m_ == r[1 + col], (r, m_)
