@@ -262,6 +262,17 @@ int gp_sim_candidates(gp_ctx *ctx, uint32_t k, uint64_t n, const uint8_t *order,
                       const uint8_t *counts, const uint8_t *bm, uint32_t iterations,
                       double opt_seconds, double *makespan, uint8_t *status);
 
+/*
+ * Batched re-plan over bandwidth snapshots (kernel K6 + K3): for snapshot i,
+ * bandwidth[i*D*D ..] replaces every link's bandwidth_bytes_per_s (p_t and
+ * latency unchanged) and out[i] receives exhaustive_plan's arg-min on that
+ * topology (min_intra_bandwidth re-derived as group_first_level would).
+ * status[i] = GP_OK or the error exhaustive_plan would raise.  The loaded
+ * instance is left unchanged.
+ */
+int gp_replan_snapshots(gp_ctx *ctx, const double *bandwidth, uint32_t n_snap, gp_best *out,
+                        int32_t *status);
+
 /* Stream the context uses (cudaStream_t), for event timing by callers. */
 void *gp_ctx_stream(gp_ctx *ctx);
 

@@ -100,6 +100,7 @@ struct DevInst {
     uint8_t* skind;              // [F][(n+1)^2]
     double* C1;                  // [F][(n+1)^2] per-sample (F+Bi)+W (detail)
     double4* fbws;               // [F][(n+1)^2] {F, Bi, W per sample, sync seconds} (K5)
+    double* vtab;                // [nm][F][ntri] collective volume V (0 if no collective) (K6)
     int* gw;                     // [F*F] gateway u*D+v
     double* xt;                  // [nm][F][F][nxp] (rows padded to 16 B)
     int nxp;                     // x row stride: n rounded up to even
@@ -314,6 +315,8 @@ __global__ void k1_stages(DevInst I) {
         }
         double cm = c1 * md;
         if (feas && isinf(cm)) overflow = true;
+        I.vtab[((size_t)mi * I.F + f) * ((size_t)n * (n + 1) / 2) + (a * n - a * (a - 1) / 2) + (b - a - 1)] =
+            nmem >= 2 ? (kind == GP_ASYM_TP_DP ? 2.0 * P + I.act[b - 1] * md : 2.0 * P) : 0.0;
         double2 v = make_double2(feas ? cm : INFINITY, al);
         I.stg[(size_t)mi * I.F * N2 + e] = v;
         size_t ntri = (size_t)n * (n + 1) / 2;
@@ -537,7 +540,11 @@ struct ArgminScratch {
 };
 
 // CTA-wide reduction of per-thread keys, then last-block grid reduction.
-__device__ void block_argmin_finish(Key mine, const ArgminScratch& S) {
+// Reduction over a group of `nblk` CTAs (the whole grid, or one snapshot's
+// CTAs): CTA `bidx` of the group writes its key; the last one to finish
+// reduces the group's keys into *S.result and re-arms the counter.
+__device__ void block_argmin_finish(Key mine, const ArgminScratch& S, unsigned int nblk,
+                                    unsigned int bidx) {
     __shared__ Key wbest[32];
     __shared__ bool last;
     Key w = warp_min(mine);
@@ -549,17 +556,17 @@ __device__ void block_argmin_finish(Key mine, const ArgminScratch& S) {
         Key v = lane < nw ? wbest[lane] : Key{INFINITY, ~0ull};
         v = warp_min(v);
         if (lane == 0) {
-            S.blk[blockIdx.x] = v;
+            S.blk[bidx] = v;
             __threadfence();
             unsigned int done = atomicAdd(S.counter, 1u);
-            last = (done == gridDim.x - 1);
+            last = (done == nblk - 1);
         }
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
     Key v{INFINITY, ~0ull};
-    for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    for (unsigned int b = threadIdx.x; b < nblk; b += blockDim.x) {
         Key o;
         o.cost = __ldcg(&S.blk[b].cost);
         o.tie = __ldcg(&S.blk[b].tie);
@@ -575,6 +582,10 @@ __device__ void block_argmin_finish(Key mine, const ArgminScratch& S) {
         *S.result = r;
         *S.counter = 0;  // re-arm for the next launch
     }
+}
+
+__device__ __forceinline__ void block_argmin_finish(Key mine, const ArgminScratch& S) {
+    block_argmin_finish(mine, S, gridDim.x, blockIdx.x);
 }
 
 // Fast path (all stage entries error-free, k >= 3).
@@ -902,6 +913,12 @@ struct SweepGeom {
     unsigned int* item_ctr;         // per-item task counters
     const uint8_t* prefixes;        // colex-ordered (k-3)-subsets, 16-byte records
     int gsteps;                     // largest power of two <= ngroups
+    // snapshot batches (K6): tables and results per snapshot
+    unsigned int items;             // items per snapshot in this launch
+    const double2* tpk;             // packed triangles of snapshot 0
+    const double2* tcol;
+    const double* xt;
+    unsigned long long s_tpk, s_tcol, s_xt;  // per-snapshot strides (elements)
 };
 
 template <int MODE, int NB>
@@ -912,7 +929,9 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     const int n = I.n, k = G.k;
     const int ntri = n * (n + 1) / 2;
     const int KB = k + 1;
-    const unsigned long long islot = blockIdx.x / G.cpi;
+    const unsigned int per_snap = G.items * (unsigned int)G.cpi;
+    const unsigned int snap = blockIdx.x / per_snap, local = blockIdx.x % per_snap;
+    const unsigned long long islot = local / G.cpi;
     const unsigned long long item = G.item0 + islot;
     const int mi = (int)(item / G.NP);
     const unsigned long long perm_rank = item % G.NP;
@@ -921,14 +940,13 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     double Mv[NB];
 #pragma unroll
     for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[bi] / I.micro[mi]);
-    const size_t N2 = (size_t)(n + 1) * (n + 1);
-    const double2* T = I.stg + (size_t)mi * I.F * N2;
-    const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
+    const double2* TPm = G.tpk + snap * G.s_tpk + (size_t)mi * I.F * ntri;
+    const double* X = G.xt + snap * G.s_xt + (size_t)mi * I.F * I.F * I.nxp;
     const int f1 = order[k - 3], f2 = order[k - 2], f3 = order[k - 1];
-    const double2* P0 = I.tpk + ((size_t)mi * I.F + order[0]) * ntri;
-    const double2* P1 = I.tpk + ((size_t)mi * I.F + f1) * ntri;
-    const double2* P2 = I.tpk + ((size_t)mi * I.F + f2) * ntri;
-    const double2* C3 = I.tcol + ((size_t)mi * I.F + f3) * (n + 1);
+    const double2* P0 = TPm + (size_t)order[0] * ntri;
+    const double2* P1 = TPm + (size_t)f1 * ntri;
+    const double2* P2 = TPm + (size_t)f2 * ntri;
+    const double2* C3 = G.tcol + snap * G.s_tcol + ((size_t)mi * I.F + f3) * (n + 1);
     const double* X01 = X + ((size_t)order[0] * I.F + order[1]) * I.nxp;
     const double* X12 = X + ((size_t)f1 * I.F + f2) * I.nxp;
     const double* X23 = X + ((size_t)f2 * I.F + f3) * I.nxp;
@@ -969,10 +987,10 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     const int lane = threadIdx.x & 31;
     double best_c = INFINITY;
     unsigned long long best_t = ~0ull;  // R * NB + bi
-    const bool skip = skip_if_flags && *skip_if_flags;  // generic kernel decides
+    const bool skip = skip_if_flags && skip_if_flags[snap];  // generic kernel decides
     for (; !skip;) {
         unsigned int t = 0;
-        if (lane == 0) t = atomicAdd(&G.item_ctr[islot], 1u);
+        if (lane == 0) t = atomicAdd(&G.item_ctr[(size_t)snap * G.items + islot], 1u);
         t = __shfl_sync(0xffffffffu, t, 0);
         if ((unsigned long long)t * 32 >= G.W) break;
         const unsigned int u = t * 32 + lane;
@@ -1017,7 +1035,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
                     e = row0[p[1] - 1];
                     x = x01s[p[1] - 1];
                 } else {
-                    e = __ldg(&T[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])]);
+                    e = __ldg(&TPm[(size_t)order[s] * ntri + rowoff(n, p[s]) + (p[s + 1] - p[s] - 1)]);
                     x = __ldg(&X[((size_t)order[s] * I.F + order[s + 1]) * I.nxp + (p[s + 1] - 1)]);
                 }
                 if (s > 0) res = res + max0f(xprev - e.x);
@@ -1091,7 +1109,11 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
         mine.tie = ((perm_rank * G.NC) + rr) * (unsigned long long)G.nbm +
                    (unsigned long long)(bi * I.nm + mi);
     }
-    block_argmin_finish(mine, S);
+    ArgminScratch Ss = S;
+    Ss.blk = S.blk + (size_t)snap * per_snap;
+    Ss.counter = S.counter + snap;
+    Ss.result = S.result + snap;
+    block_argmin_finish(mine, Ss, per_snap, local);
 }
 
 // Tile table: cut positions p[1..k-1] (u8) of every K3_TILE-th composition
@@ -1236,6 +1258,87 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
         out->counts[s] = (uint8_t)(p[s + 1] - p[s]);
     }
     plan_detail_dev(I, k, o, p, bm, &out->info, &out->status);
+}
+
+// ----------------------------------------------------------------------------
+// K6: bandwidth-snapshot re-plan.  A snapshot rescales link bandwidths only
+// (p_t, grouping, gateway pairs, splits and memory feasibility are
+// unchanged - SURVEY.md CS4), so per snapshot the engine re-derives
+//   min_intra_bandwidth per group            (src/grouping.py:69-75)
+//   AL = V / min_bw per stage-table entry     (src/timing.py:146-173)
+//   x = lat + (act*m)/bw per gateway/boundary (src/timing.py:91-97, 209-225)
+// into per-snapshot copies of the packed tables, then one K3 sweep launch
+// covers every (snapshot, item) with a per-snapshot arg-min.
+// ----------------------------------------------------------------------------
+struct SnapGeom {
+    int nsnap;
+    const double* bw;            // [nsnap][D*D]
+    double* mbw;                 // [nsnap][F]
+    uint32_t* flags;             // [nsnap]
+    double2* tpk;                // [nsnap][nm][F][ntri]
+    double2* tcol;               // [nsnap][nm][F][n+1]
+    double* xt;                  // [nsnap][nm][F][F][nxp]
+    unsigned long long s_tpk, s_tcol, s_xt;
+};
+
+__global__ void k6_minbw(DevInst I, SnapGeom Z) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= Z.nsnap * I.F) return;
+    const int sn = t / I.F, f = t % I.F;
+    const double* bw = Z.bw + (size_t)sn * I.D * I.D;
+    const int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    double mn = 0.0;
+    bool have = false;
+    for (int x = m0; x < m1; ++x)
+        for (int y = x + 1; y < m1; ++y) {
+            double w = bw[(size_t)I.fg_mem[x] * I.D + I.fg_mem[y]];
+            if (!have || w < mn) mn = w;
+            have = true;
+        }
+    Z.mbw[(size_t)sn * I.F + f] = have ? mn : 0.0;
+    if (I.fg_has_minbw[f] && !(mn > 0)) atomicOr(&Z.flags[sn], FLAG_STAGE_ERROR);
+    if (f == 0)
+        for (int pr = 0; pr < I.F * I.F; ++pr) {
+            const int fa = pr / I.F, fb = pr % I.F;
+            if (fa != fb && !(bw[I.gw[pr]] > 0)) atomicOr(&Z.flags[sn], FLAG_GATEWAY_ERROR);
+        }
+}
+
+__global__ void k6_patch(DevInst I, SnapGeom Z) {
+    const int n = I.n;
+    const long long ntri = (long long)n * (n + 1) / 2;
+    const long long per_snap_tri = (long long)I.nm * I.F * ntri;
+    const long long per_snap_x = (long long)I.nm * I.F * I.F * n;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int sn = blockIdx.y;
+    const double* mbw = Z.mbw + (size_t)sn * I.F;
+    if (t < per_snap_tri) {
+        const int f = (int)((t / ntri) % I.F);
+        const int mi = (int)(t / (ntri * I.F));
+        const int e = (int)(t % ntri);
+        // packed entry e -> (a, b): row a holds n - a entries
+        int a = 0, off = e;
+        while (off >= n - a) { off -= n - a; ++a; }
+        const int b = a + 1 + off;
+        double2 v = I.tpk[t];
+        const double V = I.vtab[t];
+        const double mb = mbw[f];
+        v.y = (V != 0.0 && I.fg_has_minbw[f] && mb > 0) ? V / mb : 0.0;
+        Z.tpk[sn * Z.s_tpk + t] = v;
+        if (b == n) Z.tcol[sn * Z.s_tcol + ((size_t)mi * I.F + f) * (n + 1) + a] = v;
+        if (a == 0 && b == 1)
+            Z.tcol[sn * Z.s_tcol + ((size_t)mi * I.F + f) * (n + 1) + n] = make_double2(INFINITY, 0.0);
+    } else if (t < per_snap_tri + per_snap_x) {
+        const long long u = t - per_snap_tri;
+        const int j = (int)(u % n);
+        const long long r = u / n;  // mi * F * F + pair
+        const int pair = (int)(r % (I.F * I.F));
+        const int mi = (int)(r / (I.F * I.F));
+        const int g = I.gw[pair];
+        const double md = (double)I.micro[mi];
+        const double bw = Z.bw[(size_t)sn * I.D * I.D + g];
+        Z.xt[sn * Z.s_xt + (size_t)r * I.nxp + j] = I.lat[g] + (I.act[j] * md) / bw;
+    }
 }
 
 // ----------------------------------------------------------------------------
@@ -1525,6 +1628,7 @@ struct gp_ctx {
     // derived tables
     DBuf<double> S, g_rf, g_cf, g_dp, g_minmem, sg_minmem, C1, xt;
     DBuf<double4> fbws;
+    DBuf<double> vtab;
     DBuf<double2> tpk, tcol;
     DBuf<uint32_t> flagsbuf;
     DBuf<uint8_t> g_tp_ok, scode, skind;
@@ -1543,6 +1647,12 @@ struct gp_ctx {
     DBuf<int> dstatus;
     DBuf<SolveOut> dsolve;
     DBuf<gp_timing> s_tim;       // K5 staging
+    // K6 snapshot batch buffers
+    DBuf<double> z_bw, z_mbw, z_xt;
+    DBuf<uint32_t> z_flags;
+    DBuf<double2> z_tpk, z_tcol;
+    DBuf<Key> z_res;
+    DBuf<unsigned int> z_cnt;
     DBuf<double> s_ms;
     DBuf<uint8_t> s_st;
     SolveOut* h_solve = nullptr;  // pinned
@@ -1586,7 +1696,7 @@ struct gp_ctx {
         I.bf = bf;
         I.S = S.p; I.g_tp_ok = g_tp_ok.p; I.g_rf = g_rf.p; I.g_cf = g_cf.p; I.g_dp = g_dp.p;
         I.g_minmem = g_minmem.p; I.sg_minmem = sg_minmem.p;
-        I.stg = stg.p; I.scode = scode.p; I.skind = skind.p; I.C1 = C1.p; I.fbws = fbws.p;
+        I.stg = stg.p; I.scode = scode.p; I.skind = skind.p; I.C1 = C1.p; I.fbws = fbws.p; I.vtab = vtab.p;
         I.gw = gw.p; I.xt = xt.p; I.flags = flagsbuf.p;
         I.nxp = (n + 1) & ~1;
         I.tpk = tpk.p; I.tcol = tcol.p;
@@ -1657,6 +1767,7 @@ void gp_ctx_destroy(gp_ctx* c) {
                           &c->C1, &c->xt, &c->b_cost};
     for (auto* b : dd) b->release();
     c->fbws.release();
+    c->vtab.release();
     c->flagsbuf.release();
     DBuf<uint8_t>* bb[] = {&c->g_tp_ok, &c->scode, &c->skind, &c->b_order, &c->b_counts,
                            &c->b_bm, &c->b_status};
@@ -1665,6 +1776,8 @@ void gp_ctx_destroy(gp_ctx* c) {
     if (c->h_arena) cudaFreeHost(c->h_arena);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->h_solve) cudaFreeHost(c->h_solve);
+    c->z_bw.release(); c->z_mbw.release(); c->z_xt.release(); c->z_flags.release();
+    c->z_tpk.release(); c->z_tcol.release(); c->z_res.release(); c->z_cnt.release();
     c->dsolve.release(); c->s_tim.release(); c->s_ms.release(); c->s_st.release();
     if (c->flags_ev) cudaEventDestroy(c->flags_ev);
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
@@ -1814,6 +1927,7 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     CUDA_TRY(c->skind.ensure((size_t)F * N2));
     CUDA_TRY(c->C1.ensure((size_t)F * N2));
     CUDA_TRY(c->fbws.ensure((size_t)F * N2));
+    CUDA_TRY(c->vtab.ensure((size_t)c->nm * F * ((size_t)n * (n + 1) / 2)));
     CUDA_TRY(c->gw.ensure((size_t)F * F));
     CUDA_TRY(c->xt.ensure((size_t)c->nm * F * F * ((n + 1) & ~1u)));
     CUDA_TRY(c->tpk.ensure((size_t)c->nm * F * ((size_t)n * (n + 1) / 2)));
@@ -2020,6 +2134,11 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     G.ngroups = c->ngroups;
     G.groups = c->groups.p;
     G.prefixes = c->prefixes.p;
+    G.items = (unsigned int)items;
+    G.tpk = c->tpk.p;
+    G.tcol = c->tcol.p;
+    G.xt = c->xt.p;
+    G.s_tpk = G.s_tcol = G.s_xt = 0;
     G.gsteps = 1;
     while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
     CUDA_TRY(c->item_ctr.ensure(items));
@@ -2425,6 +2544,150 @@ int gp_sim_1f1b(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t iterat
     CUDA_TRY(cudaMemcpyAsync(makespan, c->s_ms.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    return GP_OK;
+}
+
+int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_best* out,
+                        int32_t* status) {
+    if (!c || !c->loaded || !bandwidth || !out || !status) return fail(GP_ERR_INPUT, "bad arguments");
+    if (n_snap == 0) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    const int k = c->F, n = c->n;
+    uint64_t total;
+    gp_space_size(c, &total);
+    const unsigned long long NP = h_fact(k), NC = h_binom(n - 1, k - 1);
+    const unsigned long long items = (unsigned long long)c->nm * NP;
+    const size_t DD = (size_t)c->D * c->D;
+    const size_t ntri = (size_t)n * (n + 1) / 2, nxp = (size_t)((n + 1) & ~1);
+    const size_t s_tpk = (size_t)c->nm * c->F * ntri, s_tcol = (size_t)c->nm * c->F * (n + 1);
+    const size_t s_xt = (size_t)c->nm * c->F * c->F * nxp;
+    int fl_sync = known_flags(c);
+    if (fl_sync < 0) {  // base tables must be error-free for the per-snapshot fast path
+        CUDA_TRY(cudaEventSynchronize(c->flags_ev));
+        fl_sync = known_flags(c);
+    }
+    const bool fast = k >= 3 && c->sweep_ok && c->nb <= 4 && total > 0 && c->force_mode != 3 &&
+                      c->force_mode != 4;
+    // batch size: keep the per-snapshot tables around 256 MB
+    size_t per = (s_tpk + s_tcol) * 16 + s_xt * 8 + DD * 8;
+    uint32_t SB = (uint32_t)((256ull << 20) / (per ? per : 1));
+    if (SB < 1) SB = 1;
+    if (SB > 4096) SB = 4096;
+    if (SB > n_snap) SB = n_snap;
+    std::vector<uint32_t> h_fl(SB);
+    std::vector<Key> h_res(SB);
+    std::vector<uint32_t> slow;
+    for (uint32_t b0 = 0; b0 < n_snap; b0 += SB) {
+        const uint32_t nb = (n_snap - b0) < SB ? (n_snap - b0) : SB;
+        if (!(fast && fl_sync == 0)) {
+            for (uint32_t i = 0; i < nb; ++i) slow.push_back(b0 + i);
+            continue;
+        }
+        CUDA_TRY(c->z_bw.ensure((size_t)SB * DD));
+        CUDA_TRY(c->z_mbw.ensure((size_t)SB * c->F));
+        CUDA_TRY(c->z_flags.ensure(SB));
+        CUDA_TRY(c->z_tpk.ensure((size_t)SB * s_tpk));
+        CUDA_TRY(c->z_tcol.ensure((size_t)SB * s_tcol));
+        CUDA_TRY(c->z_xt.ensure((size_t)SB * s_xt));
+        CUDA_TRY(c->z_res.ensure(SB));
+        CUDA_TRY(c->z_cnt.ensure(SB));
+        CUDA_TRY(cudaMemcpyAsync(c->z_bw.p, bandwidth + (size_t)b0 * DD, (size_t)nb * DD * 8,
+                                 cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemsetAsync(c->z_flags.p, 0, nb * sizeof(uint32_t), s));
+        CUDA_TRY(cudaMemsetAsync(c->z_cnt.p, 0, nb * sizeof(unsigned int), s));
+        SnapGeom Z;
+        Z.nsnap = (int)nb;
+        Z.bw = c->z_bw.p; Z.mbw = c->z_mbw.p; Z.flags = c->z_flags.p;
+        Z.tpk = c->z_tpk.p; Z.tcol = c->z_tcol.p; Z.xt = c->z_xt.p;
+        Z.s_tpk = s_tpk; Z.s_tcol = s_tcol; Z.s_xt = s_xt;
+        DevInst I = c->view();
+        k6_minbw<<<(unsigned)((nb * c->F + 127) / 128), 128, 0, s>>>(I, Z);
+        const long long work = (long long)(s_tpk + (size_t)c->nm * c->F * c->F * n);
+        dim3 pg((unsigned)((work + 255) / 256), nb);
+        k6_patch<<<pg, 256, 0, s>>>(I, Z);
+        CUDA_TRY(cudaGetLastError());
+        // sweep over (snapshot, item)
+        size_t smem0 = 16 + (((size_t)(n + 1) * (k + 1) * 8 + 15) & ~(size_t)15) + (size_t)c->ngroups * 16;
+        size_t smem1 = smem0 + ntri * 16 + (n + 1) * 16 + 3 * nxp * 8 + (size_t)n * 16;
+        size_t smem2 = smem1 + ntri * 16;
+        int mode = smem2 <= (size_t)c->smem_max ? 2 : (smem1 <= (size_t)c->smem_max ? 1 : 0);
+        if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
+        size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
+        typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*,
+                             const uint32_t*);
+        static const SwFn table[3][4] = {
+            {k3_sweep<0, 1>, k3_sweep<0, 2>, k3_sweep<0, 3>, k3_sweep<0, 4>},
+            {k3_sweep<1, 1>, k3_sweep<1, 2>, k3_sweep<1, 3>, k3_sweep<1, 4>},
+            {k3_sweep<2, 1>, k3_sweep<2, 2>, k3_sweep<2, 3>, k3_sweep<2, 4>}};
+        SwFn kern = table[mode][c->nb - 1];
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K3S_THREADS, smem));
+        unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
+        unsigned long long cpi = (items * nb) >= resident ? 1 : resident / (items * nb);
+        unsigned long long tasks = (c->sweep_W + 31) / 32;
+        unsigned long long cap = (tasks + (K3S_THREADS / 32) - 1) / (K3S_THREADS / 32);
+        if (cpi > cap) cpi = cap;
+        if (cpi < 1) cpi = 1;
+        unsigned long long grid = (unsigned long long)nb * items * cpi;
+        if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "snapshot batch too large");
+        SweepGeom G;
+        G.k = k; G.nbm = c->nb * c->nm; G.NC = NC; G.NP = NP; G.item0 = 0; G.cpi = cpi;
+        G.W = c->sweep_W; G.ngroups = c->ngroups; G.groups = c->groups.p;
+        G.prefixes = c->prefixes.p;
+        G.gsteps = 1;
+        while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
+        G.items = (unsigned int)items;
+        G.tpk = c->z_tpk.p; G.tcol = c->z_tcol.p; G.xt = c->z_xt.p;
+        G.s_tpk = s_tpk; G.s_tcol = s_tcol; G.s_xt = s_xt;
+        CUDA_TRY(c->item_ctr.ensure((size_t)nb * items));
+        CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, (size_t)nb * items * sizeof(unsigned int), s));
+        G.item_ctr = c->item_ctr.p;
+        CUDA_TRY(c->blk.ensure(grid > 4096 ? grid : 4096));
+        ArgminScratch S;
+        S.blk = c->blk.p;
+        S.counter = c->z_cnt.p;
+        S.result = c->z_res.p;
+        S.err = nullptr;
+        S.err_idx = c->err_idx.p;
+        kern<<<(unsigned)grid, K3S_THREADS, smem, s>>>(I, G, S, c->binom.p, c->z_flags.p);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(h_res.data(), c->z_res.p, nb * sizeof(Key), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(h_fl.data(), c->z_flags.p, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (uint32_t i = 0; i < nb; ++i) {
+            gp_best& o = out[b0 + i];
+            memset(&o, 0, sizeof(o));
+            o.k = (uint32_t)k;
+            o.evaluated = total;
+            if (h_fl[i]) { slow.push_back(b0 + i); continue; }
+            const Key& r = h_res[i];
+            if (r.tie == ~0ull) { status[b0 + i] = GP_ERR_NO_FEASIBLE; continue; }
+            const int nbm = c->nb * c->nm;
+            unsigned long long bmv = r.tie % (unsigned long long)nbm, pc = r.tie / (unsigned long long)nbm;
+            o.cost = r.cost;
+            o.index = (bmv * NP + pc / NC) * NC + pc % NC;
+            o.batch_index = (uint32_t)(bmv / c->nm);
+            o.micro_index = (uint32_t)(bmv % c->nm);
+            h_unrank_perm(k, pc / NC, o.order);
+            h_unrank_counts(n, k, pc % NC, o.counts);
+            status[b0 + i] = GP_OK;
+        }
+    }
+    if (!slow.empty()) {
+        // exact status-tracking path, one snapshot at a time on the context
+        std::vector<double> base((size_t)DD);
+        CUDA_TRY(cudaMemcpyAsync(base.data(), c->bw.p, DD * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (uint32_t sn : slow) {
+            int st = gp_set_bandwidth(c, bandwidth + (size_t)sn * DD);
+            if (st == GP_OK) st = gp_argmin_range(c, 0, total, &out[sn]);
+            status[sn] = st;
+        }
+        int st = gp_set_bandwidth(c, base.data());
+        if (st != GP_OK) return st;
+    }
     return GP_OK;
 }
 

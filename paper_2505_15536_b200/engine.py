@@ -61,6 +61,8 @@ def lib():
         L.gp_diag_fp64_peak.argtypes = [C.c_int, P(C.c_double)]
         L.gp_sim_1f1b.argtypes = [vp, vp, C.c_uint64, C.c_uint32, P(C.c_double), u8p]
         L.gp_sim_1f1b_device.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp]
+        L.gp_replan_snapshots.argtypes = [vp, P(C.c_double), C.c_uint32, P(abi.GpBest),
+                                          P(C.c_int32)]
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
@@ -197,6 +199,19 @@ class Engine:
                                            int(iterations), float(opt_seconds),
                                            ms.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
         return ms, st
+
+    def replan_snapshots(self, bandwidths: np.ndarray):
+        """Exhaustive arg-min per bandwidth snapshot (bandwidths [S, D, D]).
+
+        Returns (bests, status): a ctypes array of GpBest and int32 codes."""
+        bw = np.ascontiguousarray(bandwidths, dtype=np.float64)
+        n = bw.shape[0]
+        out = (abi.GpBest * max(1, n))()
+        st = np.zeros(n, dtype=np.int32)
+        if n:
+            _check(lib().gp_replan_snapshots(self._h, bw.ctypes.data_as(C.POINTER(C.c_double)), n,
+                                             out, st.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out, st
 
     def set_k3_mode(self, mode: int) -> None:
         """Force the exhaustive-kernel variant (-1 auto, 0/1/2, 3 generic)."""

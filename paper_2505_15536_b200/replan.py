@@ -1,0 +1,83 @@
+"""Re-planning over bandwidth-fluctuation snapshots.
+
+The reference has no single entry point for this: the Dynamic Environment
+Adapter's re-plan is composed from its APIs - rebuild every
+``LinkMeasurement`` with the base alpha/beta/payload/latency and a scaled
+``bandwidth_bytes_per_s`` (src/profiling.py:48-78), ``build_topology``
+(:167-215), regroup (membership is unchanged because p_t does not depend on
+bandwidth; ``min_intra_bandwidth`` is re-derived, src/grouping.py:69-75), then
+``exhaustive_plan`` (src/planner.py:374-403).  Here the whole batch of
+snapshots is one engine call (gp_replan_snapshots): per-snapshot tables are
+patched on the device and one K3 sweep covers every (snapshot, item).
+"""
+
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import abi
+from . import domain as D
+from .engine import Engine, default_engine
+from .layout import PackedInstance
+from .planner import assemble
+
+
+def bandwidth_matrices(packed: PackedInstance,
+                       multipliers: Sequence[Dict[Tuple[str, str], float]]) -> np.ndarray:
+    """[S, D, D] bandwidths: base link bandwidth x per-pair multiplier
+    (keys are (u, v) with u < v), in the packed device order."""
+    ids = packed.device_ids
+    Dn = len(ids)
+    base = packed.bw
+    out = np.empty((len(multipliers), Dn, Dn), dtype=np.float64)
+    for s, mult in enumerate(multipliers):
+        m = np.ones((Dn, Dn))
+        for (u, v), f in mult.items():
+            i, j = packed.dev_index[u], packed.dev_index[v]
+            m[i, j] = m[j, i] = f
+        out[s] = base * m
+    return out
+
+
+def replan_snapshots(model, topology, groups, config, bandwidths: np.ndarray,
+                     engine: Optional[Engine] = None, detail: bool = False):
+    """Exact re-plan per snapshot.
+
+    Returns a list with, per snapshot, either a SearchResult (``detail=True``:
+    plan, splits and CostBreakdown, as ``exhaustive_plan`` on the rebuilt
+    topology returns them) or the tuple ``(cost, order_ids, counts, b, m)``;
+    snapshots whose re-plan raises carry the exception instance instead.
+    """
+    packed = PackedInstance(model, topology, groups, config.bottleneck_factor)
+    eng = (engine or default_engine()).load(packed)
+    bests, status = eng.replan_snapshots(bandwidths)
+    out: List = []
+    k = packed.n_fgs
+    nm = len(packed.micros)
+    for i in range(bandwidths.shape[0]):
+        st = int(status[i])
+        if st != abi.GP_OK:
+            cls = abi._ERRORS.get(st, D.GeopipeError)
+            out.append(cls(f"snapshot {i}: status {st}"))
+            continue
+        b = bests[i]
+        order = [int(x) for x in b.order[:k]]
+        counts = [int(x) for x in b.counts[:k]]
+        bm = b.batch_index * nm + b.micro_index
+        if not detail:
+            out.append((b.cost, [packed.fg_ids[f] for f in order], counts,
+                        packed.batches[b.batch_index], packed.micros[b.micro_index]))
+            continue
+        eng.set_bandwidth(bandwidths[i])
+        plan, breakdown, feasible = assemble(packed, eng, np.array(order, np.uint8),
+                                             np.array(counts, np.uint8), bm)
+        if breakdown is None:
+            out.append(D.NoFeasiblePlanError(f"snapshot {i}: no feasible plan"))
+        else:
+            out.append(D.SearchResult(plan=plan, breakdown=breakdown, best_cost_trace=[b.cost],
+                                      evaluated=int(b.evaluated)))
+    if detail:
+        eng.set_bandwidth(packed.bw)
+    return out

@@ -225,6 +225,33 @@ def dump_sim_candidates():
     print(f"sim candidates: {time.time() - t0:.1f}s", flush=True)
 
 
+def dump_snapshots():
+    """C3: exhaustive re-plan of C2 per bandwidth snapshot (App. D recipe).
+
+    Each snapshot is rebuilt with the reference's own constructors and
+    grouping (CS4 composition); the arg-min comes from the pinned oracle,
+    itself checked against the reference's exhaustive_plan on 3 snapshots."""
+    from oracle import oracle as O
+    gp = geopipe()
+    spec = I.config("c2")
+    out = {"config": "c2", "snapshots": []}
+    t0 = time.time()
+    for j in range(200):
+        mult = I.snapshot_multipliers(spec, j)
+        model, topo, groups = build_reference(spec, mult)
+        packed = PackedInstance(model, topo, groups, 1.25)
+        st, best = O.argmin_range(packed, 0, O.space_size(packed), threads=os.cpu_count())
+        rec = {"j": j, "status": st, "cost": best.cost, "index": best.index,
+               "min_bw": {f: groups.fgs[f].min_intra_bandwidth for f in sorted(groups.fgs)}}
+        if j < 3:
+            r = gp.exhaustive_plan(model, topo, groups, gp.SearchConfig(seed=0))
+            assert r.breakdown.plan_cost == best.cost, (j, r.breakdown.plan_cost, best.cost)
+            rec["reference"] = G.result_to_dict(r)
+        out["snapshots"].append(rec)
+    G.save("c3_snapshots.json", out)
+    print(f"snapshots: {time.time() - t0:.1f}s", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c4", action="store_true")
@@ -236,10 +263,15 @@ def main():
     sys.path.insert(0, "/root/reference/pkg/tests")
     import conftest as rc  # reference test fixtures (read-only import)
     os.makedirs(G.GOLDEN, exist_ok=True)
+    ap_only = args.only_sim
+    if ap_only:
+        dump_sim()
+        dump_sim_candidates()
+        dump_snapshots()
+        return
     dump_sim()
     dump_sim_candidates()
-    if args.only_sim:
-        return
+    dump_snapshots()
 
     for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
                                 ("c2", "c2", False), ("c2j", "c2", True)]:
