@@ -29,6 +29,8 @@ from __future__ import annotations
 
 import argparse
 import json
+
+import numpy as np
 import os
 import statistics
 import subprocess
@@ -60,6 +62,7 @@ def parse():
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     return ap.parse_args()
 
 
@@ -139,6 +142,110 @@ def cpu_baseline(total, threads, target_s=10.0):
     st, best = O.argmin_range(packed, 0, n, threads=threads)
     dt = time.perf_counter() - t
     return n / dt, n, dt
+
+
+def extra_sections(eng, packed, total, local, args, world):
+    """Secondary measurements of the other kernels (each self-timed on the
+    engine stream with CUDA events; inputs device-resident unless noted)."""
+    import torch
+    from paper_2505_15536_b200 import instances, replan, simulate
+    from paper_2505_15536_b200.engine import Engine
+    from paper_2505_15536_b200.enumeration import decode_indices, composition_table
+    from paper_2505_15536_b200.layout import PackedInstance
+    out = {}
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+
+    def timed(fn, reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        fn()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+        for _ in range(reps):
+            fn()
+        with torch.cuda.stream(stream):
+            ev[1].record(stream)
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / reps
+
+    # ---- K2: explicit batch of 10^6 sampled C4 candidates (BASELINE configs[3])
+    N = 1_000_000
+    rng = np.random.default_rng(4)
+    idx = rng.choice(total, size=N, replace=False)
+    order, counts, bm = decode_indices(80, 4, idx, composition_table(80, 4))
+    d_o = torch.from_numpy(np.ascontiguousarray(order)).to(dev)
+    d_c = torch.from_numpy(np.ascontiguousarray(counts)).to(dev)
+    d_b = torch.from_numpy(np.ascontiguousarray(bm)).to(dev)
+    d_cost = torch.empty(N, dtype=torch.float64, device=dev)
+    d_st = torch.empty(N, dtype=torch.uint8, device=dev)
+    ms = timed(lambda: eng.eval_batch_device(4, N, d_o.data_ptr(), d_c.data_ptr(), d_b.data_ptr(),
+                                             d_cost.data_ptr(), d_st.data_ptr()), 20)
+    bytes_per = 2 * 4 + 1 + 8 + 1
+    hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6536.0
+    out["k2_explicit_batch"] = {
+        "candidates": N, "ms_per_launch": ms, "candidates_per_s": N / (ms * 1e-3),
+        "roofline": {"bound": "hbm", "bytes_per_candidate": bytes_per,
+                     "achieved_gbs": N * bytes_per / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
+                     "frac": N * bytes_per / (ms * 1e-3) / 1e9 / hbm},
+        "note": "inputs L2-resident across reps (18 MB); order/counts/bm u8 in, cost f64 + status u8 out"}
+
+    # ---- K5: 1F1B makespans of 10^5 of those C4 candidates
+    NS = 100_000
+    t0 = time.perf_counter()
+    msk, stk = eng.sim_candidates(order[:NS], counts[:NS], bm[:NS], 1, 0.0)
+    el = time.perf_counter() - t0
+    out["k5_sim_1f1b"] = {"simulations": NS, "host_call_s": el, "simulations_per_s": NS / el,
+                          "feasible": int((stk == 0).sum()),
+                          "note": "C4 candidates, iterations=1; includes H2D/D2H of the batch"}
+
+    # ---- K6: C3 - 10^4 bandwidth snapshots of C2, exact re-plan each
+    spec = instances.config("c2")
+    m2, t2, g2 = instances.build(spec)
+    p2 = PackedInstance(m2, t2, g2, 1.25)
+    nsnap = 10_000
+    bws = replan.bandwidth_matrices(p2, [instances.snapshot_multipliers(spec, j)
+                                         for j in range(nsnap)])
+    e2 = Engine(local).load(p2)
+    e2.replan_snapshots(bws[:64])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    b2, s2 = e2.replan_snapshots(bws)
+    el = time.perf_counter() - t0
+    lat = []
+    for j in range(20):
+        t1 = time.perf_counter()
+        e2.replan_snapshots(bws[j:j + 1])
+        lat.append(time.perf_counter() - t1)
+    c2_total = e2.space_size()
+    out["k6_snapshot_replan"] = {
+        "snapshots": nsnap, "candidates_per_snapshot": c2_total, "host_call_s": el,
+        "snapshots_per_s": nsnap / el, "candidates_per_s": nsnap * c2_total / el,
+        "single_snapshot_latency_ms_p50": statistics.median(lat) * 1e3,
+        "ok": int((s2 == 0).sum()),
+        "note": "C3 recipe (App. D) on C2; bandwidth matrices H2D inside the call"}
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        for j in range(5):
+            m3, t3, g3 = instances.build(spec, instances.snapshot_multipliers(spec, j))
+            p3 = PackedInstance(m3, t3, g3, 1.25)
+            O.argmin_range(p3, 0, c2_total, threads=args.cpu_threads or os.cpu_count())
+        out["k6_snapshot_replan"]["cpu_port_ms_per_snapshot"] = (time.perf_counter() - t0) / 5 * 1e3
+    e2.close()
+
+    # ---- drop-in search_plan (beam, host RNG driver + K2 batches) on C4
+    from paper_2505_15536_b200 import SearchConfig, search_plan
+    model, topo, groups = instances.load("c4")
+    search_plan(model, topo, groups, SearchConfig(seed=0), engine=eng)
+    t0 = time.perf_counter()
+    r = search_plan(model, topo, groups, SearchConfig(seed=0), engine=eng)
+    out["search_plan_c4"] = {"seconds": time.perf_counter() - t0, "evaluated": r.evaluated,
+                             "note": "reference Python driver (RNG, sort) on the host, one "
+                                     "K2 batch per beam iteration across all (b, m) passes"}
+    eng.load(packed)
+    return out
 
 
 def run_reference(args):
@@ -312,6 +419,8 @@ def main():
                 "sample": f"first {n} candidates of the C4 exhaustive range, "
                           f"{dt:.1f} s on {threads} host threads (oracle/oracle.c)"}
             line["cpu_replan_s_extrapolated"] = total / rate
+        if not args.no_extra:
+            line["extra"] = extra_sections(eng, packed, total, local, args, world)
         print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:
