@@ -429,6 +429,48 @@ __device__ EvalOut eval_tables(const DevInst& I, int k, const uint8_t* order, co
 }
 
 // ---- K2: explicit batch, one thread per candidate -------------------------------
+// max(0.0, x) = x > 0 ? x : +0.0 without the FP64 pipe: clear every bit
+// when the sign bit is set (-0.0 -> +0.0, negatives -> +0.0).  Exact for
+// every non-NaN x (NaN cannot occur: operands are finite or +inf).
+__device__ __forceinline__ double max0f(double x) {
+    long long b = __double_as_longlong(x);
+    return __longlong_as_double(b & ~(b >> 63));
+}
+// a > b ? a : b (first-max; no NaNs occur)
+__device__ __forceinline__ double gtsel(double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+        : "=d"(r) : "d"(a), "d"(b));
+    return r;
+}
+
+// Fast per-candidate evaluation when the tables carry no error entries:
+// infeasible stages are +inf in the table, so the cost needs only the K stage
+// entries and K-1 boundary values - all loads issued before any arithmetic.
+template <int K>
+__device__ __forceinline__ double eval_fast(const DevInst& I, const uint8_t* o, const int* p,
+                                            int mi, double Md) {
+    const size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
+    const double2* T = I.stg + (size_t)mi * I.F * N2;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
+    double2 e[K];
+    double x[K];
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        e[s] = __ldg(&T[(size_t)o[s] * N2 + tri_idx(I.n, p[s], p[s + 1])]);
+        if (s + 1 < K) x[s] = __ldg(&X[((size_t)o[s] * I.F + o[s + 1]) * I.nxp + (p[s + 1] - 1)]);
+    }
+    double fill = 0.0, res = 0.0, best = 0.0;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        if (s > 0) res = res + max0f(x[s - 1] - e[s].x);
+        const double total = ((fill + Md * e[s].x) + res) + e[s].y;
+        best = (s == 0 || total > best) ? total : best;
+        if (s + 1 < K) fill = fill + (e[s].x + x[s]);
+    }
+    return best;
+}
+
 __global__ void k2_eval_batch(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
                               const uint8_t* __restrict__ counts, const uint8_t* __restrict__ bm,
                               double* __restrict__ cost, uint8_t* __restrict__ status) {
@@ -451,6 +493,20 @@ __global__ void k2_eval_batch(DevInst I, int k, long long ncand, const uint8_t* 
     if (st != GP_OK) { cost[i] = NAN; status[i] = (uint8_t)st; return; }
     int mi = b % I.nm;
     long long M = I.batch[b / I.nm] / I.micro[mi];
+    if (*I.flags == 0u && p[k] == I.n && k >= 2 && k <= 6) {
+        const double Md = (double)M;
+        double c;
+        switch (k) {
+            case 2: c = eval_fast<2>(I, o, p, mi, Md); break;
+            case 3: c = eval_fast<3>(I, o, p, mi, Md); break;
+            case 4: c = eval_fast<4>(I, o, p, mi, Md); break;
+            case 5: c = eval_fast<5>(I, o, p, mi, Md); break;
+            default: c = eval_fast<6>(I, o, p, mi, Md); break;
+        }
+        cost[i] = c;
+        status[i] = GP_OK;
+        return;
+    }
     EvalOut r = eval_tables(I, k, o, p, mi, M);
     cost[i] = r.status == GP_OK ? r.cost : NAN;
     status[i] = (uint8_t)r.status;
@@ -631,20 +687,7 @@ __device__ __forceinline__ bool advance_pair(int* p, int& a, int& q, int s, int 
     return true;
 }
 
-// max(0.0, x) = x > 0 ? x : +0.0 without the FP64 pipe: clear every bit
-// when the sign bit is set (-0.0 -> +0.0, negatives -> +0.0).  Exact for
-// every non-NaN x (NaN cannot occur: operands are finite or +inf).
-__device__ __forceinline__ double max0f(double x) {
-    long long b = __double_as_longlong(x);
-    return __longlong_as_double(b & ~(b >> 63));
-}
-// a > b ? a : b (first-max; no NaNs occur)
-__device__ __forceinline__ double gtsel(double a, double b) {
-    double r;
-    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}"
-        : "=d"(r) : "d"(a), "d"(b));
-    return r;
-}
+
 
 // ---- TMA (bulk async copy) helpers ----------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
