@@ -962,6 +962,7 @@ struct SweepGeom {
     const double2* tcol;
     const double* xt;
     unsigned long long s_tpk, s_tcol, s_xt;  // per-snapshot strides (elements)
+    const unsigned long long* bnk;  // C(nn, r), nn <= n, r <= k: contiguous [n+1][k+1]
 };
 
 template <int MODE, int NB>
@@ -1007,11 +1008,17 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     double* x01s = (double*)(row0 + (MODE >= 1 ? n : 0));
     double2* tri1 = (double2*)(x01s + (MODE >= 1 ? I.nxp : 0));
     if (threadIdx.x == 0) {
+        // every table this CTA reads arrives by bulk async copy on one mbarrier
+        const uint32_t bn_bytes = (uint32_t)(((size_t)(n + 1) * KB * 8 + 15) & ~(size_t)15);
+        uint32_t bytes = bn_bytes + (uint32_t)G.ngroups * 16;
+        if (MODE >= 1)
+            bytes += (uint32_t)(ntri * 16 + (n + 1) * 16 + 3 * I.nxp * 8 + n * 16) +
+                     (MODE == 2 ? (uint32_t)ntri * 16 : 0u);
         mbar_init(bar, 1);
+        mbar_expect_tx(bar, bytes);
+        tma_bulk_g2s(bn, G.bnk, bn_bytes, bar);
+        tma_bulk_g2s(grp, G.groups, (uint32_t)G.ngroups * 16, bar);
         if (MODE >= 1) {
-            uint32_t bytes = (uint32_t)(ntri * 16 + (n + 1) * 16 + 3 * I.nxp * 8 + n * 16) +
-                             (MODE == 2 ? (uint32_t)ntri * 16 : 0u);
-            mbar_expect_tx(bar, bytes);
             tma_bulk_g2s(tri2, P2, (uint32_t)ntri * 16, bar);
             tma_bulk_g2s(col3, C3, (uint32_t)(n + 1) * 16, bar);
             tma_bulk_g2s(x12s, X12, (uint32_t)I.nxp * 8, bar);
@@ -1021,21 +1028,20 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
             if (MODE == 2) tma_bulk_g2s(tri1, P1, (uint32_t)ntri * 16, bar);
         }
     }
-    for (int t = threadIdx.x; t < (n + 1) * KB; t += blockDim.x)
-        bn[t] = binom[(t / KB) * (GP_MAX_STAGES + 1) + (t % KB)];
-    for (int t = threadIdx.x; t < G.ngroups; t += blockDim.x) grp[t] = G.groups[t];
     __syncthreads();
-    if (MODE >= 1) mbar_wait(bar, 0);
+    mbar_wait(bar, 0);
 
     const int lane = threadIdx.x & 31;
     double best_c = INFINITY;
     unsigned long long best_t = ~0ull;  // R * NB + bi
     const bool skip = skip_if_flags && skip_if_flags[snap];  // generic kernel decides
+    unsigned int* const ctr = &G.item_ctr[(size_t)snap * G.items + islot];
+    unsigned int t_next = 0;
+    if (lane == 0 && !skip) t_next = atomicAdd(ctr, 1u);
     for (; !skip;) {
-        unsigned int t = 0;
-        if (lane == 0) t = atomicAdd(&G.item_ctr[(size_t)snap * G.items + islot], 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
+        const unsigned int t = __shfl_sync(0xffffffffu, t_next, 0);
         if ((unsigned long long)t * 32 >= G.W) break;
+        if (lane == 0) t_next = atomicAdd(ctr, 1u);  // next task, latency hidden by this one
         const unsigned int u = t * 32 + lane;
         int len = 0, a = 0, q0 = 0;
         double fill2 = 0.0, res1 = 0.0, x1 = 0.0;
@@ -1721,6 +1727,7 @@ struct gp_ctx {
     bool tiles_ok = false;
     DBuf<uint4> groups;       // K3 sweep run groups
     DBuf<uint8_t> prefixes;   // colex (k-3)-subsets for the sweep
+    DBuf<unsigned long long> bnk;  // binomial sub-table [n+1][k+1] (TMA-staged)
     int ngroups = 0;
     unsigned int sweep_W = 0;
     bool sweep_ok = false;
@@ -1824,7 +1831,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     c->dsolve.release(); c->s_tim.release(); c->s_ms.release(); c->s_st.release();
     if (c->flags_ev) cudaEventDestroy(c->flags_ev);
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
-    c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release();
+    c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release();
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
     c->counter.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
@@ -2045,6 +2052,10 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
         }
         if (pre_ok && start < (1ull << 31) && !g.empty()) {
             if (k > 3) CUDA_TRY(upload(s, c->prefixes, pre.data(), pre.size()));
+            std::vector<unsigned long long> bk((size_t)(nn + 1) * (k + 1) + 2, 0ull);
+            for (int a = 0; a <= nn; ++a)
+                for (int r = 0; r <= k; ++r) bk[(size_t)a * (k + 1) + r] = h_binom(a, r);
+            CUDA_TRY(upload(s, c->bnk, bk.data(), bk.size()));
             CUDA_TRY(upload(s, c->groups, g.data(), g.size()));
             c->ngroups = (int)g.size();
             c->sweep_W = (unsigned)start;
@@ -2177,6 +2188,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     G.ngroups = c->ngroups;
     G.groups = c->groups.p;
     G.prefixes = c->prefixes.p;
+    G.bnk = c->bnk.p;
     G.items = (unsigned int)items;
     G.tpk = c->tpk.p;
     G.tcol = c->tcol.p;
@@ -2679,6 +2691,7 @@ int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_
         G.k = k; G.nbm = c->nb * c->nm; G.NC = NC; G.NP = NP; G.item0 = 0; G.cpi = cpi;
         G.W = c->sweep_W; G.ngroups = c->ngroups; G.groups = c->groups.p;
         G.prefixes = c->prefixes.p;
+        G.bnk = c->bnk.p;
         G.gsteps = 1;
         while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
         G.items = (unsigned int)items;

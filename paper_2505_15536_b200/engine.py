@@ -17,7 +17,7 @@ from . import abi
 from . import domain as D
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgeopipe_b200.so")
+LIB_PATH = os.environ.get("GP_ENGINE_LIB") or os.path.join(HERE, "libgeopipe_b200.so")
 
 _lib = None
 _lib_lock = threading.Lock()
