@@ -226,6 +226,12 @@ int gp_argmin_fetch(gp_ctx *ctx, gp_best *out);
  * synchronisation.  `info` may be NULL. */
 int gp_solve(gp_ctx *ctx, uint64_t lo, uint64_t hi, gp_best *best, gp_plan_info *info);
 
+/* Full exact re-plan of an instance in one call: H2D of the instance, table
+ * build, exhaustive arg-min and winner detail, replayed as one CUDA graph for
+ * every instance of the same shape (layers, devices, group structure,
+ * (b, m) candidates).  Equivalent to gp_ctx_load + gp_solve(0, total). */
+int gp_replan(gp_ctx *ctx, const gp_instance *inst, gp_best *best, gp_plan_info *info);
+
 /* Splits + CostBreakdown of one candidate (the winner), on the device. */
 int gp_plan_detail(gp_ctx *ctx, uint32_t k, const uint8_t *order,
                    const uint8_t *counts, uint32_t bm, gp_plan_info *out);

@@ -121,11 +121,10 @@ __device__ __forceinline__ double Ssum(const DevInst& I, int col, int a, int b) 
 // ---- K1a: interval sums -----------------------------------------------------
 // sum(model.layers[i].<field> for i in range(a, b)) for every 0 <= a < b <= n,
 // each interval summed from its own start (never prefix differences).
-__global__ void k1_intervals(DevInst I) {
+__device__ void k1_intervals_block(const DevInst& I, int col) {
     // one CTA per column; the column is staged in shared memory so the
     // sequential Neumaier sweeps read on-chip values
     __shared__ double col_s[GP_MAX_LAYERS + 1];
-    const int col = blockIdx.x;
     for (int i = threadIdx.x; i < I.n; i += blockDim.x) {
         double x;
         switch (col) {
@@ -149,33 +148,57 @@ __global__ void k1_intervals(DevInst I) {
     }
 }
 
+__global__ void k1_intervals(DevInst I) { k1_intervals_block(I, blockIdx.x); }
+
 // ---- K1b: per-group constants ---------------------------------------------------
-__global__ void k1_groups(DevInst I) {
-    int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= I.F) return;
-    int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
-    int nmem = m1 - m0;
-    double caps[GP_MAX_MEMBERS];
-    double mn = 0.0;
-    for (int j = 0; j < nmem; ++j) {
-        int d = I.fg_mem[m0 + j];
-        caps[j] = I.p_c[d];
-        double mm = I.mem[d];
-        mn = (j == 0 || mm < mn) ? mm : mn;
+__device__ __forceinline__ double block_min128(double v, double* red) {
+    // exact min over a 128-thread block (min is order-independent)
+    for (int off = 16; off > 0; off >>= 1) {
+        double o = __shfl_down_sync(0xffffffffu, v, off);
+        v = o < v ? o : v;
     }
-    I.g_minmem[f] = mn;
-    I.g_tp_ok[f] = gpd::tp_grid(caps, nmem, I.g_rf + m0, I.g_cf + m0) ? 1 : 0;
-    int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
-    if (s1 > s0) gpd::dp_fractions(I.sg_cap + s0, s1 - s0, I.g_dp + s0);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = red[w] < r ? red[w] : r;
+    return r;
+}
+
+// one 128-thread block per group: members loaded in parallel into shared
+// memory, then the (sequential) factorisation runs on-chip
+__device__ void k1_group_block(const DevInst& I, int f) {
+    __shared__ double caps[GP_MAX_MEMBERS];
+    __shared__ double red[4];
+    const int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    const int nmem = m1 - m0;
+    double mn = INFINITY;
+    for (int j = threadIdx.x; j < nmem; j += blockDim.x) {
+        const int d = I.fg_mem[m0 + j];
+        caps[j] = I.p_c[d];
+        const double mm = I.mem[d];
+        mn = mm < mn ? mm : mn;
+    }
+    mn = block_min128(mn, red);
+    if (threadIdx.x == 0) {
+        I.g_minmem[f] = mn;
+        I.g_tp_ok[f] = gpd::tp_grid(caps, nmem, I.g_rf + m0, I.g_cf + m0) ? 1 : 0;
+        const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
+        if (s1 > s0) gpd::dp_fractions(I.sg_cap + s0, s1 - s0, I.g_dp + s0);
+    }
+    const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
     for (int g = s0; g < s1; ++g) {
-        double sm = 0.0;
-        for (int x = I.sg_off[g]; x < I.sg_off[g + 1]; ++x) {
-            double mm = I.mem[I.sg_mem[x]];
-            sm = (x == (int)I.sg_off[g] || mm < sm) ? mm : sm;
+        double sm = INFINITY;
+        for (int x = I.sg_off[g] + threadIdx.x; x < (int)I.sg_off[g + 1]; x += blockDim.x) {
+            const double mm = I.mem[I.sg_mem[x]];
+            sm = mm < sm ? mm : sm;
         }
-        I.sg_minmem[g] = sm;
+        sm = block_min128(sm, red);
+        if (threadIdx.x == 0) I.sg_minmem[g] = I.sg_off[g + 1] > I.sg_off[g] ? sm : 0.0;
     }
 }
+
+__global__ void k1_groups(DevInst I) { k1_group_block(I, blockIdx.x); }
 
 // recompute min_intra_bandwidth over member pairs (bandwidth snapshots;
 // src/grouping.py:69-75 on the rebuilt topology)
@@ -223,10 +246,9 @@ __device__ int choose_split(const DevInst& I, int f, int a, int b, int* shares, 
 // ---- K1c: stage table -------------------------------------------------------------
 // One thread per (group, a, b).  memory_feasible is local to a stage because
 // every group appears in exactly one stage (src/planner.py:226-253).
-__global__ void k1_stages(DevInst I) {
+__device__ void k1_stage_t(const DevInst& I, long long t) {
     int n = I.n;
     int N1 = n + 1;
-    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     long long total = (long long)I.F * N1 * N1;
     if (t >= total) return;
     int f = (int)(t / (N1 * N1));
@@ -328,15 +350,14 @@ __global__ void k1_stages(DevInst I) {
     if (overflow) atomicOr(I.flags, FLAG_OVERFLOW);
 }
 
+__global__ void k1_stages(DevInst I) { k1_stage_t(I, (long long)blockIdx.x * blockDim.x + threadIdx.x); }
+
 // ---- K1d: gateways and boundary transfer table -------------------------------------
 // gateway_link (src/timing.py:104-113): argmin over (p_t, u, v) with string
 // order of ids, u in the upstream group, v in the downstream group.
-__global__ void k1_gateways(DevInst I) {
+__device__ void k1_gateway_warp(const DevInst& I, int warp, int lane) {
     // one warp per ordered pair (fa, fb); lanes scan member pairs, then a
     // warp argmin on the key (p_t, rank(u), rank(v))
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= I.F * I.F) return;
     const int fa = warp / I.F, fb = warp % I.F;
     const int a0 = I.fg_off[fa], na = I.fg_off[fa + 1] - a0;
     const int b0 = I.fg_off[fb], nbm = I.fg_off[fb + 1] - b0;
@@ -366,8 +387,29 @@ __global__ void k1_gateways(DevInst I) {
     }
 }
 
+__global__ void k1_gateways(DevInst I) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (warp < I.F * I.F) k1_gateway_warp(I, warp, threadIdx.x & 31);
+}
+
+// K1 phase 1 in one launch: blocks [0,5) interval sums, [5, 5+F) group
+// constants, the rest gateways (one warp per ordered group pair)
+__device__ void k1_intervals_block(const DevInst& I, int col);
+__device__ void k1_gateway_warp(const DevInst& I, int warp, int lane);
+
+__global__ void __launch_bounds__(128) k1_phase1(DevInst I) {
+    const int b = blockIdx.x;
+    if (b < 5) { k1_intervals_block(I, b); return; }
+    if (b < 5 + I.F) { k1_group_block(I, b - 5); return; }
+    const int warp = (b - 5 - I.F) * 4 + (threadIdx.x >> 5);
+    if (warp < I.F * I.F) k1_gateway_warp(I, warp, threadIdx.x & 31);
+}
+
+__device__ void k1_boundary_t(const DevInst& I, long long t);
 __global__ void k1_boundary(DevInst I) {
-    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    k1_boundary_t(I, (long long)blockIdx.x * blockDim.x + threadIdx.x);
+}
+__device__ void k1_boundary_t(const DevInst& I, long long t) {
     long long total = (long long)I.nm * I.F * I.F * I.n;
     if (t >= total) return;
     int j = (int)(t % I.n);
@@ -378,6 +420,13 @@ __global__ void k1_boundary(DevInst I) {
     double md = (double)I.micro[mi];
     // transfer_seconds: latency + (act*m)/bandwidth (src/timing.py:91-97)
     I.xt[(size_t)r * I.nxp + j] = I.lat[g] + (I.act[j] * md) / I.bw[g];
+}
+
+// K1 phase 2 in one launch: stage table entries, then boundary x entries
+__global__ void k1_phase2(DevInst I, long long n_stage) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_stage) k1_stage_t(I, t);
+    else k1_boundary_t(I, t - n_stage);
 }
 
 // ----------------------------------------------------------------------------
@@ -1263,14 +1312,16 @@ __device__ void plan_detail_dev(const DevInst& I, int k, const uint8_t* o, const
     }
 }
 
+__device__ void plan_detail_warp(const DevInst& I, int k, const uint8_t* o, const int* p, int bm,
+                                 gp_plan_info* out, int* status);
+
 __global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const uint8_t* counts_in,
                               int bm, gp_plan_info* out, int* status) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
     uint8_t o[GP_MAX_STAGES];
     int p[GP_MAX_STAGES + 1];
     p[0] = 0;
     for (int s = 0; s < k; ++s) { o[s] = order_in[s]; p[s + 1] = p[s] + counts_in[s]; }
-    plan_detail_dev(I, k, o, p, bm, out, status);
+    plan_detail_warp(I, k, o, p, bm, out, status);
 }
 
 // Winner of the last arg-min -> decoded candidate + plan detail, on the
@@ -1285,28 +1336,137 @@ struct SolveOut {
     gp_plan_info info;
 };
 
+// Warp version of plan_detail_dev: lane s prepares stage s (split choice and
+// table loads in parallel), lane 0 runs the short Eq. 1 chain.
+__device__ void plan_detail_warp(const DevInst& I, int k, const uint8_t* o, const int* p, int bm,
+                                 gp_plan_info* out, int* status) {
+    const int lane = threadIdx.x & 31;
+    const int n = I.n;
+    const size_t N2 = (size_t)(n + 1) * (n + 1);
+    const int mi = bm % I.nm;
+    const long long M = I.batch[bm / I.nm] / I.micro[mi];
+    const double2* T = I.stg + (size_t)mi * I.F * N2;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
+    double2 e = make_double2(0.0, 0.0);
+    double x = 0.0;
+    uint8_t code = SC_OK;
+    bool gw_bad = false;
+    if (lane < k) {
+        const int s = lane;
+        gp_stage_info& st = out->stage[s];
+        int shares[GP_MAX_SGS], np;
+        const int kind = choose_split(I, o[s], p[s], p[s + 1], shares, &np);
+        st.kind = (uint32_t)kind;
+        st.n_parts = (uint32_t)np;
+        if (kind == GP_ASYM_PP) {
+            int pos = p[s];
+            for (int j = 0; j < np; ++j) {
+                st.pp_sg[j] = (uint32_t)j;
+                st.pp_start[j] = (uint32_t)pos;
+                st.pp_end[j] = (uint32_t)(pos + shares[j]);
+                pos += shares[j];
+            }
+        }
+        const size_t ei = (size_t)o[s] * N2 + tri_idx(n, p[s], p[s + 1]);
+        e = T[ei];
+        code = I.scode[ei];
+        if (s + 1 < k) {
+            x = X[((size_t)o[s] * I.F + o[s + 1]) * I.nxp + (p[s + 1] - 1)];
+            gw_bad = !(I.bw[I.gw[o[s] * I.F + o[s + 1]]] > 0);
+        }
+    }
+    const unsigned infeas = __ballot_sync(0xffffffffu, lane < k && code == SC_INFEASIBLE);
+    const unsigned errs = __ballot_sync(0xffffffffu, lane < k && code != SC_OK && code != SC_INFEASIBLE);
+    const unsigned gbad = __ballot_sync(0xffffffffu, gw_bad);
+    const int first_err = errs ? __shfl_sync(0xffffffffu, (int)code, __ffs(errs) - 1) : 0;
+    // lane 0: the sequential chain; stage values arrive by shuffles
+    double fill = 0.0, res = 0.0, xprev = 0.0, best = 0.0;
+    int st = GP_OK;
+    const bool feas = infeas == 0u;
+    if (!feas) best = INFINITY;
+    else if (p[k] != n) st = GP_ERR_TOPOLOGY;
+    else if (errs) st = first_err;
+    else if (gbad) st = GP_ERR_TOPOLOGY;
+    const double Md = (double)M;
+    for (int s = 0; s < k; ++s) {
+        const double cx = __shfl_sync(0xffffffffu, e.x, s);
+        const double cy = __shfl_sync(0xffffffffu, e.y, s);
+        const double xs = __shfl_sync(0xffffffffu, x, s);
+        if (!feas || st != GP_OK) continue;
+        if (s > 0) res = res + gpd::max0(xprev - cx);
+        const double run = Md * cx;
+        const double total = ((fill + run) + res) + cy;
+        best = (s == 0 || total > best) ? total : best;
+        if (lane == 0) {
+            out->stage[s].fill_seconds = fill;
+            out->stage[s].run_seconds = run;
+            out->stage[s].residual_seconds = res;
+            out->stage[s].collective_seconds = cy;
+        }
+        if (s + 1 < k) {
+            fill = fill + (cx + xs);
+            xprev = xs;
+        }
+    }
+    if (lane == 0) {
+        out->k = (uint32_t)k;
+        out->feasible = feas ? 1 : 0;
+        out->plan_cost = best;
+        *status = st;
+    }
+}
+
 __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned long long NP,
                                int nbm, const Key* result, const unsigned long long* err,
-                               SolveOut* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    out->key = *result;
-    out->err = *err;
-    out->k = (uint32_t)k;
-    out->status = GP_OK;
-    if (out->err != ~0ull || out->key.tie == ~0ull) return;
-    unsigned long long t = out->key.tie;
-    int bm = (int)(t % (unsigned long long)nbm);
-    unsigned long long pc = t / (unsigned long long)nbm;
+                               const unsigned long long* __restrict__ binom, SolveOut* out) {
+    // one warp: decode the arg-min key (cut positions by a 32-wide ballot
+    // over the hockey-stick counts), then the warp plan detail
+    const int lane = threadIdx.x & 31;
+    const Key key = *result;
+    const unsigned long long e = *err;
+    if (lane == 0) {
+        out->key = key;
+        out->err = e;
+        out->k = (uint32_t)k;
+        out->status = GP_OK;
+    }
+    if (e != ~0ull || key.tie == ~0ull) return;
+    const int n = I.n;
+    const unsigned long long t = key.tie;
+    const int bm = (int)(t % (unsigned long long)nbm);
+    const unsigned long long pc = t / (unsigned long long)nbm;
     uint8_t o[GP_MAX_STAGES];
     int p[GP_MAX_STAGES + 1];
     d_unrank_perm(k, pc / NC, o);
-    d_unrank_cuts(I.n, k, pc % NC, p);
-    out->bm = (uint32_t)bm;
-    for (int s = 0; s < k; ++s) {
-        out->order[s] = o[s];
-        out->counts[s] = (uint8_t)(p[s + 1] - p[s]);
+    p[0] = 0;
+    unsigned long long rem = pc % NC;
+    int prev = 0;
+    auto C = [&](int nn, int r) -> unsigned long long {
+        return (r < 0 || nn < 0) ? 0ull : binom[(size_t)nn * (GP_MAX_STAGES + 1) + r];
+    };
+    for (int j = 1; j < k; ++j) {
+        const int r = k - 1 - j, lo = prev + 1;
+        const unsigned long long tot = C(n - lo, r + 1), thr = tot - rem;
+        int qsel = -1;
+        for (int base = lo; qsel < 0; base += 32) {
+            const int qq = base + lane;
+            const bool ok = qq <= n - 1 - r && C(n - qq - 1, r + 1) < thr;
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (m) qsel = base + __ffs(m) - 1;
+        }
+        rem -= tot - C(n - qsel, r + 1);
+        p[j] = qsel;
+        prev = qsel;
     }
-    plan_detail_dev(I, k, o, p, bm, &out->info, &out->status);
+    p[k] = n;
+    if (lane == 0) {
+        out->bm = (uint32_t)bm;
+        for (int s = 0; s < k; ++s) {
+            out->order[s] = o[s];
+            out->counts[s] = (uint8_t)(p[s + 1] - p[s]);
+        }
+    }
+    plan_detail_warp(I, k, o, p, bm, &out->info, &out->status);
 }
 
 // ----------------------------------------------------------------------------
@@ -1638,12 +1798,17 @@ __global__ void k5_sim_1f1b(const gp_timing* __restrict__ T, long long n, int it
 // ----------------------------------------------------------------------------
 // context
 // ----------------------------------------------------------------------------
+// bumped on every device (re)allocation: a captured CUDA graph is only
+// replayed while the buffers it was captured with are still in place
+static unsigned long long g_alloc_gen = 0;
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t cap = 0;
     cudaError_t ensure(size_t count) {
         if (count <= cap && p) return cudaSuccess;
+        __atomic_add_fetch(&g_alloc_gen, 1ull, __ATOMIC_RELAXED);
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
@@ -1719,6 +1884,13 @@ struct gp_ctx {
     size_t h_arena_cap = 0;
     DBuf<unsigned char> arena;
     int cache_n = -1, cache_k = -1;   // (n, k) of the enumeration helpers
+    // gp_replan: CUDA graph of H2D + K1 + K3 + detail + D2H for one shape
+    cudaGraphExec_t graph_exec = nullptr;
+    unsigned long long graph_key[10] = {0};
+    unsigned long long graph_gen = 0;
+    RangeGeom graph_geom{};
+    unsigned long long graph_lo = 0, graph_hi = 0;
+    bool capturing = false;
     size_t arena_bytes = 0;
     int force_mode = -1;  // -1 auto; 0/1/2 fast-path variant; 3 generic kernel
     DBuf<unsigned long long> binom;
@@ -1831,6 +2003,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     c->dsolve.release(); c->s_tim.release(); c->s_ms.release(); c->s_st.release();
     if (c->flags_ev) cudaEventDestroy(c->flags_ev);
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release();
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
@@ -1845,14 +2018,16 @@ static int run_tables(gp_ctx* c, bool full) {
     cudaStream_t s = c->stream;
     CUDA_TRY(cudaMemsetAsync(c->flagsbuf.p, 0, sizeof(uint32_t), s));
     if (full) {
-        k1_intervals<<<5, 128, 0, s>>>(I);
-        k1_groups<<<(c->F + 31) / 32, 32, 0, s>>>(I);
+        // interval sums + group constants + gateways (independent) in one launch
+        const int gw_blocks = (c->F * c->F + 3) / 4;
+        k1_phase1<<<5 + c->F + gw_blocks, 128, 0, s>>>(I);
+    } else {
+        k1_gateways<<<(c->F * c->F * 32 + 127) / 128, 128, 0, s>>>(I);
     }
+    // stage table + boundary table in one launch
     long long ns = (long long)c->F * (c->n + 1) * (c->n + 1);
-    k1_stages<<<(unsigned)((ns + 127) / 128), 128, 0, s>>>(I);
-    k1_gateways<<<(c->F * c->F * 32 + 127) / 128, 128, 0, s>>>(I);
     long long nx = (long long)c->nm * c->F * c->F * c->n;
-    k1_boundary<<<(unsigned)((nx + 255) / 256), 256, 0, s>>>(I);
+    k1_phase2<<<(unsigned)((ns + nx + 127) / 128), 128, 0, s>>>(I, ns);
     CUDA_TRY(cudaGetLastError());
     // flags travel back asynchronously; kernels consult the device copy when
     // the host copy is not known yet (no synchronisation on the load path)
@@ -1864,6 +2039,7 @@ static int run_tables(gp_ctx* c, bool full) {
 
 // host-side flags when the async read-back has landed; -1 when still pending
 static int known_flags(gp_ctx* c) {
+    if (c->capturing) return -1;  // graph: device-side dispatch
     if (c->flags_known) return (int)c->flags;
     if (cudaEventQuery(c->flags_ev) == cudaSuccess) {
         c->flags = *c->h_flags;
@@ -2465,19 +2641,24 @@ int gp_argmin_items_async(gp_ctx* c, uint64_t item_lo, uint64_t item_hi) {
     return GP_OK;
 }
 
-int gp_solve(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* best, gp_plan_info* info) {
-    if (!c || !c->loaded || !best) return fail(GP_ERR_INPUT, "context not loaded");
+// arg-min + on-device winner detail + D2H of the SolveOut record (no sync)
+static int enqueue_solve(gp_ctx* c, uint64_t lo, uint64_t hi) {
     int st = gp_argmin_range_async(c, lo, hi);
     if (st != GP_OK) return st;
     const RangeGeom& G = c->last_geom;
     CUDA_TRY(c->dsolve.ensure(1));
     DevInst I = c->view();
     k_solve_detail<<<1, 32, 0, c->stream>>>(I, G.k, G.NC, G.NP, G.nbm, c->result.p, c->err_idx.p,
-                                            c->dsolve.p);
+                                            c->binom.p, c->dsolve.p);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(c->h_solve, c->dsolve.p, sizeof(SolveOut), cudaMemcpyDeviceToHost,
                              c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return GP_OK;
+}
+
+// decode the SolveOut record that landed in pinned memory
+static int finish_solve(gp_ctx* c, gp_best* best, gp_plan_info* info) {
+    const RangeGeom& G = c->last_geom;
     const SolveOut& o = *c->h_solve;
     memset(best, 0, sizeof(*best));
     best->k = (uint32_t)G.k;
@@ -2498,6 +2679,122 @@ int gp_solve(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* best, gp_plan_info* i
     if (info) *info = o.info;
     if (o.status != GP_OK) return fail(o.status, "winner raises status %d", o.status);
     return GP_OK;
+}
+
+int gp_solve(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* best, gp_plan_info* info) {
+    if (!c || !c->loaded || !best) return fail(GP_ERR_INPUT, "context not loaded");
+    int st = enqueue_solve(c, lo, hi);
+    if (st != GP_OK) return st;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return finish_solve(c, best, info);
+}
+
+// shape of an instance: everything the arena layout and the launch geometry
+// depend on (a CUDA graph captured for one shape replays for any instance of
+// the same shape)
+static void instance_shape(const gp_instance* in, unsigned long long* key) {
+    key[0] = in->n_layers; key[1] = in->n_devices; key[2] = in->n_fgs;
+    key[3] = in->n_batch; key[4] = in->n_micro;
+    key[5] = in->fg_member_offset[in->n_fgs];
+    key[6] = in->fg_sg_offset[in->n_fgs];
+    key[7] = in->sg_member_offset[in->fg_sg_offset[in->n_fgs]];
+    unsigned long long h = 1469598103934665603ull;  // group structure (CSR offsets)
+    for (uint32_t f = 0; f <= in->n_fgs; ++f) {
+        h = (h ^ in->fg_member_offset[f]) * 1099511628211ull;
+        h = (h ^ in->fg_sg_offset[f]) * 1099511628211ull;
+    }
+    for (uint32_t g = 0; g <= in->fg_sg_offset[in->n_fgs]; ++g)
+        h = (h ^ in->sg_member_offset[g]) * 1099511628211ull;
+    for (uint32_t i = 0; i < in->n_batch; ++i) h = (h ^ (unsigned long long)in->batch[i]) * 1099511628211ull;
+    for (uint32_t i = 0; i < in->n_micro; ++i) h = (h ^ (unsigned long long)in->micro[i]) * 1099511628211ull;
+    key[8] = h;
+}
+
+int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* info) {
+    if (!c || !in || !best) return fail(GP_ERR_INPUT, "null argument");
+    unsigned long long key[10];
+    instance_shape(in, key);
+    memcpy(&key[9], &in->bottleneck_factor, sizeof(double));
+    const bool same = c->graph_exec && memcmp(key, c->graph_key, sizeof(key)) == 0 &&
+                      c->graph_gen == __atomic_load_n(&g_alloc_gen, __ATOMIC_RELAXED);
+    cudaStream_t s = c->stream;
+    if (!same) {
+        // first instance of this shape: regular load (allocations, helpers),
+        // then capture H2D + K1 + K3 + detail + D2H as one graph
+        int st = gp_ctx_load(c, in);
+        if (st != GP_OK) return st;
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+        uint64_t total;
+        gp_space_size(c, &total);
+        // make every buffer the graph touches exist before capturing
+        CUDA_TRY(c->dsolve.ensure(1));
+        CUDA_TRY(c->item_ctr.ensure((size_t)c->nm * h_fact(c->F) + 1));
+        c->capturing = true;
+        CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        cudaError_t ce = cudaMemcpyAsync(c->arena.p, c->h_arena, c->arena_bytes,
+                                         cudaMemcpyHostToDevice, s);
+        int st2 = ce == cudaSuccess ? GP_OK : fail(GP_ERR_CUDA, "capture: %s", cudaGetErrorString(ce));
+        if (st2 == GP_OK) {
+            DevInst I = c->view();
+            cudaMemsetAsync(c->flagsbuf.p, 0, sizeof(uint32_t), s);
+            const int gw_blocks = (c->F * c->F + 3) / 4;
+            k1_phase1<<<5 + c->F + gw_blocks, 128, 0, s>>>(I);
+            long long ns = (long long)c->F * (c->n + 1) * (c->n + 1);
+            long long nx = (long long)c->nm * c->F * c->F * c->n;
+            k1_phase2<<<(unsigned)((ns + nx + 127) / 128), 128, 0, s>>>(I, ns);
+            cudaMemcpyAsync(c->h_flags, c->flagsbuf.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+            cudaEventRecord(c->flags_ev, s);
+            c->flags_known = false;
+            st2 = enqueue_solve(c, 0, total);
+        }
+        cudaGraph_t g = nullptr;
+        cudaError_t ee = cudaStreamEndCapture(s, &g);
+        c->capturing = false;
+        if (st2 != GP_OK) { if (g) cudaGraphDestroy(g); return st2; }
+        if (ee != cudaSuccess) return fail(GP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ee));
+        ee = cudaGraphInstantiate(&c->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ee != cudaSuccess) { c->graph_exec = nullptr; return fail(GP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ee)); }
+        memcpy(c->graph_key, key, sizeof(key));
+        c->graph_gen = __atomic_load_n(&g_alloc_gen, __ATOMIC_RELAXED);
+        c->graph_geom = c->last_geom;
+        c->graph_lo = c->last_lo;
+        c->graph_hi = c->last_hi;
+    } else {
+        // same shape: refill the pinned arena in place (same offsets)
+        if (c->arena_ev) CUDA_TRY(cudaEventSynchronize(c->arena_ev));
+        const uint32_t n = in->n_layers, D = in->n_devices, F = in->n_fgs;
+        const size_t DD = (size_t)D * D;
+        const uint32_t nsg = in->fg_sg_offset[F];
+        const void* src[23] = {in->fwd_flops, in->bwd_input_flops, in->bwd_weight_flops,
+                               in->activation_out_bytes, in->param_bytes, in->batch, in->micro,
+                               in->p_c, in->memory_bytes, in->id_rank, in->p_t, in->latency,
+                               in->bandwidth, in->fg_member_offset, in->fg_members, in->fg_capacity,
+                               in->fg_min_bw, in->fg_min_bw, in->fg_has_min_bw, in->fg_sg_offset,
+                               in->sg_member_offset, in->sg_members, in->sg_capacity};
+        const size_t bytes[23] = {n * 8ull, n * 8ull, n * 8ull, n * 8ull, n * 8ull,
+                                  in->n_batch * 8ull, in->n_micro * 8ull, D * 8ull, D * 8ull,
+                                  D * 4ull, DD * 8, DD * 8, DD * 8, (F + 1) * 4ull,
+                                  in->fg_member_offset[F] * 4ull, F * 8ull, F * 8ull, F * 8ull,
+                                  (size_t)F, (F + 1) * 4ull, (nsg + 1) * 4ull,
+                                  in->sg_member_offset[nsg] * 4ull, nsg * 8ull};
+        size_t off = 0;
+        for (int i = 0; i < 23; ++i) {
+            if (bytes[i]) memcpy(c->h_arena + off, src[i], bytes[i]);
+            off += (bytes[i] + 15) & ~(size_t)15;
+        }
+        c->bf = in->bottleneck_factor;
+        c->last_geom = c->graph_geom;
+        c->last_lo = c->graph_lo;
+        c->last_hi = c->graph_hi;
+    }
+    CUDA_TRY(cudaGraphLaunch(c->graph_exec, s));
+    CUDA_TRY(cudaEventRecord(c->arena_ev, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    c->flags_known = false;
+    c->loaded = true;
+    return finish_solve(c, best, info);
 }
 
 int gp_plan_detail(gp_ctx* c, uint32_t k, const uint8_t* order, const uint8_t* counts, uint32_t bm,

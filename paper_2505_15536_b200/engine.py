@@ -56,6 +56,7 @@ def lib():
         L.gp_plan_detail.argtypes = [vp, C.c_uint32, u8p, u8p, C.c_uint32,
                                      P(abi.GpPlanInfo)]
         L.gp_solve.argtypes = [vp, C.c_uint64, C.c_uint64, P(abi.GpBest), P(abi.GpPlanInfo)]
+        L.gp_replan.argtypes = [vp, P(abi.GpInstance), P(abi.GpBest), P(abi.GpPlanInfo)]
         L.gp_group_splits.argtypes = [vp, C.c_uint32, P(abi.GpGroupInfo)]
         L.gp_set_bandwidth.argtypes = [vp, P(C.c_double)]
         L.gp_diag_fp64_peak.argtypes = [C.c_int, P(C.c_double)]
@@ -148,6 +149,15 @@ class Engine:
         best = abi.GpBest()
         info = abi.GpPlanInfo()
         _check(lib().gp_solve(self._h, int(lo), int(hi), C.byref(best), C.byref(info)))
+        return best, info
+
+    def replan(self, packed):
+        """Load + exhaustive arg-min + winner detail in one call (CUDA graph
+        replayed for every instance of the same shape)."""
+        best = abi.GpBest()
+        info = abi.GpPlanInfo()
+        _check(lib().gp_replan(self._h, C.byref(packed.struct), C.byref(best), C.byref(info)))
+        self.packed = packed
         return best, info
 
     def argmin_range_async(self, lo: int, hi: int) -> None:

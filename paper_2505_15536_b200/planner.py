@@ -178,11 +178,9 @@ def assemble(packed: PackedInstance, eng: Engine, order_idx, counts, bm: int, in
 def exhaustive_plan(model, topology, groups, config, engine: Engine = None) -> D.SearchResult:
     """GPU replacement for ``exhaustive_plan`` (src/planner.py:374-403)."""
     packed = PackedInstance(model, topology, groups, config.bottleneck_factor)
-    eng = _engine_for(packed, engine)
-    total = eng.space_size()
-    if total == 0:
-        raise D.NoFeasiblePlanError("no feasible plan in exhaustive sweep")
-    best, info = eng.solve(0, total)
+    eng = engine if engine is not None else default_engine()
+    best, info = eng.replan(packed)   # H2D + K1 + K3 + detail as one CUDA graph
+    total = int(best.evaluated)
     k = best.k
     order = np.array(best.order[:k], dtype=np.uint8)
     counts = np.array(best.counts[:k], dtype=np.uint8)

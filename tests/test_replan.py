@@ -71,3 +71,15 @@ def test_k6_variants(engine, mode):
         engine.set_k3_mode(-1)
     for j in range(20):
         assert bests[j].index == SNAP["snapshots"][j]["index"]
+
+
+@pytest.mark.gpu
+def test_graph_replan_over_same_shape_instances(engine):
+    """gp_replan replays one captured CUDA graph for every same-shape instance."""
+    spec = I.config("c2")
+    for j in list(range(12)) + [0, 5]:
+        m2, t2, g2 = I.build(spec, I.snapshot_multipliers(spec, j))
+        best, info = engine.replan(PackedInstance(m2, t2, g2, 1.25))
+        assert best.cost == SNAP["snapshots"][j]["cost"], j
+        assert best.index == SNAP["snapshots"][j]["index"], j
+        assert info.plan_cost == best.cost
