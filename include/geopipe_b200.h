@@ -210,6 +210,10 @@ int gp_eval_batch_device(gp_ctx *ctx, uint32_t k, uint64_t n,
  */
 int gp_space_size(gp_ctx *ctx, uint64_t *out);
 int gp_argmin_range(gp_ctx *ctx, uint64_t lo, uint64_t hi, gp_best *out);
+/* Same result as gp_argmin_range over the whole space, by exact
+ * branch-and-bound with min-max DP bounds (kernel K4): for large stage
+ * counts where enumeration explodes.  Read with gp_argmin_fetch. */
+int gp_argmin_bnb_async(gp_ctx *ctx);
 /* Asynchronous variant writing the per-launch result to device memory
  * (benchmarks / multi-GPU reduction); read with gp_argmin_fetch. */
 int gp_argmin_range_async(gp_ctx *ctx, uint64_t lo, uint64_t hi);

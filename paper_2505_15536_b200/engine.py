@@ -53,6 +53,7 @@ def lib():
         L.gp_argmin_range_async.argtypes = [vp, C.c_uint64, C.c_uint64]
         L.gp_argmin_fetch.argtypes = [vp, P(abi.GpBest)]
         L.gp_argmin_items_async.argtypes = [vp, C.c_uint64, C.c_uint64]
+        L.gp_argmin_bnb_async.argtypes = [vp]
         L.gp_plan_detail.argtypes = [vp, C.c_uint32, u8p, u8p, C.c_uint32,
                                      P(abi.GpPlanInfo)]
         L.gp_solve.argtypes = [vp, C.c_uint64, C.c_uint64, P(abi.GpBest), P(abi.GpPlanInfo)]
@@ -166,6 +167,11 @@ class Engine:
     def argmin_items(self, item_lo: int, item_hi: int) -> abi.GpBest:
         """Arg-min over (micro-batch, order) items [item_lo, item_hi)."""
         _check(lib().gp_argmin_items_async(self._h, int(item_lo), int(item_hi)))
+        return self.argmin_fetch()
+
+    def argmin_bnb(self) -> abi.GpBest:
+        """Exhaustive arg-min by exact branch-and-bound (K4)."""
+        _check(lib().gp_argmin_bnb_async(self._h))
         return self.argmin_fetch()
 
     def argmin_fetch(self) -> abi.GpBest:

@@ -35,6 +35,8 @@ from .layout import PackedInstance
 log = logging.getLogger(__name__)
 
 INFEASIBLE = math.inf
+# exhaustive spaces above this many candidates go to the K4 branch-and-bound
+BNB_THRESHOLD = 500_000_000
 
 
 # --------------------------------------------------------------------------
@@ -179,7 +181,16 @@ def exhaustive_plan(model, topology, groups, config, engine: Engine = None) -> D
     """GPU replacement for ``exhaustive_plan`` (src/planner.py:374-403)."""
     packed = PackedInstance(model, topology, groups, config.bottleneck_factor)
     eng = engine if engine is not None else default_engine()
-    best, info = eng.replan(packed)   # H2D + K1 + K3 + detail as one CUDA graph
+    k, n = packed.n_fgs, packed.n_layers
+    space = (len(packed.batches) * len(packed.micros) * math.factorial(k) *
+             math.comb(n - 1, k - 1)) if k <= n else 0
+    if space > BNB_THRESHOLD:
+        # large spaces: exact branch-and-bound with DP bounds (K4), same winner
+        eng.load(packed)
+        best = eng.argmin_bnb()
+        info = None
+    else:
+        best, info = eng.replan(packed)   # H2D + K1 + K3 + detail as one CUDA graph
     total = int(best.evaluated)
     k = best.k
     order = np.array(best.order[:k], dtype=np.uint8)

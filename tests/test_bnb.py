@@ -1,0 +1,82 @@
+"""K4 branch-and-bound == exhaustive arg-min (same cost, same winner index)."""
+
+import random
+
+import pytest
+
+from cases import CASES_ALL, load_case
+from paper_2505_15536_b200 import instances as I
+from paper_2505_15536_b200.layout import PackedInstance
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", CASES_ALL + ["c4", "c4j"])
+def test_bnb_equals_exhaustive_golden(engine, name):
+    doc, model, topo, groups = load_case(name)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    engine.load(packed)
+    total = engine.space_size()
+    if total == 0:
+        return
+    try:
+        ex = engine.argmin_range(0, total)
+    except Exception as e:
+        with pytest.raises(type(e)):
+            engine.argmin_bnb()
+        return
+    bb = engine.argmin_bnb()
+    assert bb.cost == ex.cost
+    assert bb.index == ex.index
+
+
+def _many_group_instance(k, n, seed, jitter=True):
+    rng = random.Random(seed)
+    regions = []
+    for r in range(k):
+        tiers = [[(rng.choice([3.5e13, 7.1e13, 1.65e14, 9.89e14]), rng.choice([8e9, 24e9, 80e9]))]
+                 * rng.randint(1, 2)]
+        if rng.random() < 0.5:
+            tiers.append([(rng.choice([2.0e13, 3.12e14]), 24e9)])
+        regions.append(tiers)
+    layers = I.transformer_layers(n, 2048, 5504, 1024, 32000, d_kv=2048,
+                                  jitter_seed=seed if jitter else None)
+    spec = I.InstanceSpec(f"k{k}", layers, (64, 128), (8, 16), regions,
+                          intra_bw=[rng.uniform(1e9, 5e10) for _ in range(k)],
+                          intra_lat=[rng.uniform(1e-5, 1e-3) for _ in range(k)],
+                          cross_bw=1.25e7, cross_lat=0.03, jitter_seed=seed)
+    return I.build(spec)
+
+
+@pytest.mark.parametrize("k,n,seed", [(5, 20, 1), (5, 24, 2), (6, 16, 3), (6, 20, 4), (6, 40, 5),
+                                      (7, 20, 11), (7, 24, 12), (8, 16, 13)])
+def test_bnb_equals_sweep_many_groups(engine, k, n, seed):
+    model, topo, groups = _many_group_instance(k, n, seed)
+    assert len(groups.fgs) == k
+    packed = PackedInstance(model, topo, groups, 1.25)
+    engine.load(packed)
+    total = engine.space_size()
+    ex = engine.argmin_range(0, total)
+    bb = engine.argmin_bnb()
+    assert bb.cost == ex.cost
+    assert bb.index == ex.index
+
+
+@pytest.mark.parametrize("name", ["c1j", "c2", "c2j", "small", "rand10", "err_memory", "c4"])
+def test_exhaustive_plan_via_bnb_matches_reference(engine, name, monkeypatch):
+    import golden_io as G
+    import paper_2505_15536_b200 as P
+    from paper_2505_15536_b200 import planner as PL
+    monkeypatch.setattr(PL, "BNB_THRESHOLD", 0)
+    doc, model, topo, groups = load_case(name)
+    cfg = P.SearchConfig(seed=0)
+    if "error" in doc.get("exhaustive", {}):
+        with pytest.raises(P.GeopipeError):
+            P.exhaustive_plan(model, topo, groups, cfg, engine=engine)
+        return
+    res = P.exhaustive_plan(model, topo, groups, cfg, engine=engine)
+    if "exhaustive" in doc:
+        assert G.normalize_result(res) == doc["exhaustive"]["result"]
+    else:
+        exp = doc["oracle_argmin"]
+        assert res.breakdown.plan_cost == exp["cost"]
