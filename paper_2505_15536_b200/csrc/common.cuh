@@ -1,0 +1,326 @@
+// common.cuh - shared device-side pieces of the engine: error plumbing,
+// the device view of a loaded instance (DevInst), arg-min keys and their
+// warp / CTA / grid reduction, exact scalar helpers, enumeration decode,
+// and the TMA bulk-copy + mbarrier primitives.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../include/geopipe_b200.h"
+#include "device_math.cuh"
+
+using gpd::NeumaierSum;
+
+// ----------------------------------------------------------------------------
+// error plumbing
+// ----------------------------------------------------------------------------
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                        \
+    do {                                                                      \
+        cudaError_t e_ = (expr);                                              \
+        if (e_ != cudaSuccess)                                                \
+            return fail(GP_ERR_CUDA, "%s: %s (%s:%d)", #expr,                 \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);          \
+    } while (0)
+
+// stage-table codes (per group, layer range)
+enum : uint8_t { SC_OK = 0, SC_INFEASIBLE = 1, SC_DEGENERATE = 4, SC_TOPOLOGY = 5 };
+// context flags that force the generic (status-tracking) range kernel
+enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 4 };
+#define K3_THREADS 256
+#define K3_TILE 256
+#define K3_SEG 32
+#ifndef K3S_THREADS
+#define K3S_THREADS 256
+#endif
+#ifndef K3S_MINB
+#define K3S_MINB 2
+#endif
+#ifndef K3_MINB
+#define K3_MINB 3
+#endif
+#define BINOM_ROWS 257
+
+// ----------------------------------------------------------------------------
+// device-side view of one loaded instance
+// ----------------------------------------------------------------------------
+struct DevInst {
+    int n;          // layers
+    int F;          // first-level groups
+    int D;          // devices
+    int nb, nm;     // |B|, |M|
+    const double *fwd, *bwd_in, *bwd_w, *act, *param;
+    const long long *batch, *micro;
+    const double *p_c, *mem, *p_t, *lat, *bw;
+    const uint32_t* id_rank;
+    const uint32_t *fg_off, *fg_mem, *fg_sg_off, *sg_off, *sg_mem;
+    const double *fg_cap, *sg_cap;
+    const double* fg_minbw;      // current min_intra_bandwidth
+    const uint8_t* fg_has_minbw;
+    double bf;                   // bottleneck_factor
+    // K1 outputs
+    double* S;                   // [5][(n+1)^2]: fwd, bwd_in, bwd_w, param, total_flops
+    uint8_t* g_tp_ok;            // [F]
+    double *g_rf, *g_cf;         // [fg member slots]
+    double* g_dp;                // [sg slots]
+    double* g_minmem;            // [F]
+    double* sg_minmem;           // [n_sgs]
+    double2* stg;                // [nm][F][(n+1)^2] {C1*m or +inf, AL}
+    uint8_t* scode;              // [F][(n+1)^2]
+    uint8_t* skind;              // [F][(n+1)^2]
+    double* C1;                  // [F][(n+1)^2] per-sample (F+Bi)+W (detail)
+    double4* fbws;               // [F][(n+1)^2] {F, Bi, W per sample, sync seconds} (K5)
+    double* vtab;                // [nm][F][ntri] collective volume V (0 if no collective) (K6)
+    int* gw;                     // [F*F] gateway u*D+v
+    double* xt;                  // [nm][F][F][nxp] (rows padded to 16 B)
+    int nxp;                     // x row stride: n rounded up to even
+    double2* tpk;                // [nm][F][n(n+1)/2] packed rows a: b = a+1..n
+    double2* tcol;               // [nm][F][n+1] entry (q, n) at q
+    uint32_t* flags;             // [1]
+};
+
+__device__ __forceinline__ int tri_idx(int n, int a, int b) { return a * (n + 1) + b; }
+
+enum { COL_FWD = 0, COL_BWD = 1, COL_WGT = 2, COL_PARAM = 3, COL_TF = 4 };
+
+__device__ __forceinline__ double Ssum(const DevInst& I, int col, int a, int b) {
+    size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
+    return I.S[col * N2 + tri_idx(I.n, a, b)];
+}
+
+
+// max(0.0, x) = x > 0 ? x : +0.0 without the FP64 pipe: clear every bit
+// when the sign bit is set (-0.0 -> +0.0, negatives -> +0.0).  Exact for
+// every non-NaN x (NaN cannot occur: operands are finite or +inf).
+__device__ __forceinline__ double max0f(double x) {
+    long long b = __double_as_longlong(x);
+    return __longlong_as_double(b & ~(b >> 63));
+}
+// a > b ? a : b (first-max; no NaNs occur)
+__device__ __forceinline__ double gtsel(double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+        : "=d"(r) : "d"(a), "d"(b));
+    return r;
+}
+
+
+// ----------------------------------------------------------------------------
+// K3: exhaustive argmin over an enumeration-index range
+// ----------------------------------------------------------------------------
+struct RangeGeom {
+    int k;
+    int nbm;                 // |B| * |M|
+    unsigned long long NC;   // C(n-1, k-1)
+    unsigned long long NP;   // k!
+    unsigned long long lo, hi;
+    unsigned long long item0;          // first item touched
+    unsigned long long chunks_per_item;  // CTAs sharing one item
+    unsigned long long chunk;          // (generic kernel: unused)
+    unsigned int* item_ctr;            // per-item tile counters (zeroed per launch)
+    const uint8_t* tiles;              // cut positions at every K3_TILE-th rank, or null
+    int items_mode;                    // generic kernel: [lo, hi) indexes (b, item, comp)
+    unsigned long long it_lo, it_span; // item range of items_mode
+    int nm;                            // |M| (items_mode decode)
+};
+
+__device__ unsigned long long d_binom(int n, int r) {
+    if (r < 0 || r > n) return 0ull;
+    unsigned long long res = 1;
+    for (int i = 1; i <= r; ++i) res = res * (unsigned long long)(n - r + i) / (unsigned long long)i;
+    return res;
+}
+
+__device__ void d_unrank_perm(int k, unsigned long long r, uint8_t* perm) {
+    uint8_t pool[GP_MAX_STAGES];
+    unsigned long long f = 1;
+    for (int i = 0; i < k; ++i) { pool[i] = (uint8_t)i; if (i > 0) f *= (unsigned long long)i; }
+    int left = k;
+    for (int i = 0; i < k; ++i) {
+        // f = (k-1-i)!
+        unsigned long long q = r / f;
+        r %= f;
+        perm[i] = pool[q];
+        for (int j = (int)q; j + 1 < left; ++j) pool[j] = pool[j + 1];
+        --left;
+        if (k - 1 - i > 0) f /= (unsigned long long)(k - 1 - i);
+    }
+}
+
+// composition rank -> cut positions p[1..k-1] (lexicographic in counts)
+__device__ void d_unrank_cuts(int n, int k, unsigned long long r, int* p) {
+    p[0] = 0;
+    int prev = 0;
+    for (int j = 1; j < k; ++j) {
+        for (int q = prev + 1;; ++q) {
+            unsigned long long cnt = d_binom(n - q - 1, k - 1 - j);
+            if (r < cnt) { p[j] = q; prev = q; break; }
+            r -= cnt;
+        }
+    }
+    p[k] = n;
+}
+
+struct Key {
+    double cost;
+    unsigned long long tie;
+};
+
+__device__ __forceinline__ bool key_less(const Key& a, const Key& b) {
+    return a.cost < b.cost || (a.cost == b.cost && a.tie < b.tie);
+}
+
+__device__ __forceinline__ Key warp_min(Key v) {
+    for (int off = 16; off > 0; off >>= 1) {
+        Key o;
+        o.cost = __shfl_down_sync(0xffffffffu, v.cost, off);
+        o.tie = __shfl_down_sync(0xffffffffu, v.tie, off);
+        if (key_less(o, v)) v = o;
+    }
+    return v;
+}
+
+struct ArgminScratch {
+    Key* blk;                 // [grid]
+    unsigned int* counter;    // [1]
+    Key* result;              // [1]
+    int* err;                 // [1] first error (index<<4|code) low 32 bits unused
+    unsigned long long* err_idx;
+};
+
+// CTA-wide reduction of per-thread keys, then last-block grid reduction.
+// Reduction over a group of `nblk` CTAs (the whole grid, or one snapshot's
+// CTAs): CTA `bidx` of the group writes its key; the last one to finish
+// reduces the group's keys into *S.result and re-arms the counter.
+__device__ void block_argmin_finish(Key mine, const ArgminScratch& S, unsigned int nblk,
+                                    unsigned int bidx) {
+    __shared__ Key wbest[32];
+    __shared__ bool last;
+    Key w = warp_min(mine);
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) wbest[wid] = w;
+    __syncthreads();
+    if (wid == 0) {
+        int nw = (blockDim.x + 31) >> 5;
+        Key v = lane < nw ? wbest[lane] : Key{INFINITY, ~0ull};
+        v = warp_min(v);
+        if (lane == 0) {
+            S.blk[bidx] = v;
+            __threadfence();
+            unsigned int done = atomicAdd(S.counter, 1u);
+            last = (done == nblk - 1);
+        }
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    Key v{INFINITY, ~0ull};
+    for (unsigned int b = threadIdx.x; b < nblk; b += blockDim.x) {
+        Key o;
+        o.cost = __ldcg(&S.blk[b].cost);
+        o.tie = __ldcg(&S.blk[b].tie);
+        if (key_less(o, v)) v = o;
+    }
+    v = warp_min(v);
+    if (lane == 0) wbest[wid] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int nw = (blockDim.x + 31) >> 5;
+        Key r = wbest[0];
+        for (int i = 1; i < nw; ++i) if (key_less(wbest[i], r)) r = wbest[i];
+        *S.result = r;
+        *S.counter = 0;  // re-arm for the next launch
+    }
+}
+
+__device__ __forceinline__ void block_argmin_finish(Key mine, const ArgminScratch& S) {
+    block_argmin_finish(mine, S, gridDim.x, blockIdx.x);
+}
+
+
+// packed triangle: row a of a stage table holds b = a+1..n
+__device__ __forceinline__ int rowoff(int n, int a) { return a * n - a * (a - 1) / 2; }
+
+// lexicographic successor of the prefix cuts p[1..k-3] (p_j <= n - k + j)
+__device__ __forceinline__ bool next_prefix(int* p, int n, int k) {
+    int j = k - 3;
+    while (j >= 1 && p[j] >= n - k + j) --j;
+    if (j < 1) return false;
+    ++p[j];
+    for (int t = j + 1; t <= k - 3; ++t) p[t] = p[t - 1] + 1;
+    return true;
+}
+
+// advance (prefix, a, q) by s ranks; returns false past the last pair
+__device__ __forceinline__ bool advance_pair(int* p, int& a, int& q, int s, int n, int k,
+                                             bool& dirty) {
+    q += s;
+    while (q > n - 1) {
+        int o = q - (n - 1);
+        ++a;
+        if (a > n - 2) {
+            if (k < 4 || !next_prefix(p, n, k)) return false;
+            a = p[k - 3] + 1;
+            dirty = true;
+        }
+        q = a + o;
+    }
+    return true;
+}
+
+
+
+
+// ---- TMA (bulk async copy) helpers ----------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
+// CTA group = item = (micro-batch index mi, order); chunks_per_item CTAs
+// share an item and pull K3_TILE-rank tiles of its composition space from a
+// per-item atomic counter (dynamic balance across warps and CTAs).  Every
+// candidate (order, cuts, m) is evaluated for all NB batch sizes at once:
+// the tables {C1*m, AL} and x depend on m only, and the fill / residual
+// chains do not depend on the batch size, so only the M*c terms and the
+// totals are per batch (tie order (cost, order, cuts, b) is kept by
+// scanning batch sizes innermost).
+//
+// Staging: one elected thread moves the packed stage-table triangles, the
+// last-stage column, stage 0's row and the boundary rows HBM/L2 -> shared
+// memory with bulk async copies (TMA, cp.async.bulk) on one mbarrier.

@@ -1,0 +1,162 @@
+// detail.cuh - winner plan detail (splits + CostBreakdown) and on-device key decode.
+#pragma once
+#include "k2_eval.cuh"
+
+// ---- plan detail of one candidate (single thread) -----------------------------------
+__device__ void plan_detail_warp(const DevInst& I, int k, const uint8_t* o, const int* p, int bm,
+                                 gp_plan_info* out, int* status);
+
+__global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const uint8_t* counts_in,
+                              int bm, gp_plan_info* out, int* status) {
+    uint8_t o[GP_MAX_STAGES];
+    int p[GP_MAX_STAGES + 1];
+    p[0] = 0;
+    for (int s = 0; s < k; ++s) { o[s] = order_in[s]; p[s + 1] = p[s] + counts_in[s]; }
+    plan_detail_warp(I, k, o, p, bm, out, status);
+}
+
+// Winner of the last arg-min -> decoded candidate + plan detail, on the
+// device (no host round trip between the arg-min and the breakdown).
+struct SolveOut {
+    Key key;
+    unsigned long long err;
+    int status;        // of the detail evaluation
+    uint32_t k, bm, pad;
+    uint8_t order[GP_MAX_STAGES];
+    uint8_t counts[GP_MAX_STAGES];
+    gp_plan_info info;
+};
+
+// Warp version of plan_detail_dev: lane s prepares stage s (split choice and
+// table loads in parallel), lane 0 runs the short Eq. 1 chain.
+__device__ void plan_detail_warp(const DevInst& I, int k, const uint8_t* o, const int* p, int bm,
+                                 gp_plan_info* out, int* status) {
+    const int lane = threadIdx.x & 31;
+    const int n = I.n;
+    const size_t N2 = (size_t)(n + 1) * (n + 1);
+    const int mi = bm % I.nm;
+    const long long M = I.batch[bm / I.nm] / I.micro[mi];
+    const double2* T = I.stg + (size_t)mi * I.F * N2;
+    const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
+    double2 e = make_double2(0.0, 0.0);
+    double x = 0.0;
+    uint8_t code = SC_OK;
+    bool gw_bad = false;
+    if (lane < k) {
+        const int s = lane;
+        gp_stage_info& st = out->stage[s];
+        int shares[GP_MAX_SGS], np;
+        const int kind = choose_split(I, o[s], p[s], p[s + 1], shares, &np);
+        st.kind = (uint32_t)kind;
+        st.n_parts = (uint32_t)np;
+        if (kind == GP_ASYM_PP) {
+            int pos = p[s];
+            for (int j = 0; j < np; ++j) {
+                st.pp_sg[j] = (uint32_t)j;
+                st.pp_start[j] = (uint32_t)pos;
+                st.pp_end[j] = (uint32_t)(pos + shares[j]);
+                pos += shares[j];
+            }
+        }
+        const size_t ei = (size_t)o[s] * N2 + tri_idx(n, p[s], p[s + 1]);
+        e = T[ei];
+        code = I.scode[ei];
+        if (s + 1 < k) {
+            x = X[((size_t)o[s] * I.F + o[s + 1]) * I.nxp + (p[s + 1] - 1)];
+            gw_bad = !(I.bw[I.gw[o[s] * I.F + o[s + 1]]] > 0);
+        }
+    }
+    const unsigned infeas = __ballot_sync(0xffffffffu, lane < k && code == SC_INFEASIBLE);
+    const unsigned errs = __ballot_sync(0xffffffffu, lane < k && code != SC_OK && code != SC_INFEASIBLE);
+    const unsigned gbad = __ballot_sync(0xffffffffu, gw_bad);
+    const int first_err = errs ? __shfl_sync(0xffffffffu, (int)code, __ffs(errs) - 1) : 0;
+    // lane 0: the sequential chain; stage values arrive by shuffles
+    double fill = 0.0, res = 0.0, xprev = 0.0, best = 0.0;
+    int st = GP_OK;
+    const bool feas = infeas == 0u;
+    if (!feas) best = INFINITY;
+    else if (p[k] != n) st = GP_ERR_TOPOLOGY;
+    else if (errs) st = first_err;
+    else if (gbad) st = GP_ERR_TOPOLOGY;
+    const double Md = (double)M;
+    for (int s = 0; s < k; ++s) {
+        const double cx = __shfl_sync(0xffffffffu, e.x, s);
+        const double cy = __shfl_sync(0xffffffffu, e.y, s);
+        const double xs = __shfl_sync(0xffffffffu, x, s);
+        if (!feas || st != GP_OK) continue;
+        if (s > 0) res = res + gpd::max0(xprev - cx);
+        const double run = Md * cx;
+        const double total = ((fill + run) + res) + cy;
+        best = (s == 0 || total > best) ? total : best;
+        if (lane == 0) {
+            out->stage[s].fill_seconds = fill;
+            out->stage[s].run_seconds = run;
+            out->stage[s].residual_seconds = res;
+            out->stage[s].collective_seconds = cy;
+        }
+        if (s + 1 < k) {
+            fill = fill + (cx + xs);
+            xprev = xs;
+        }
+    }
+    if (lane == 0) {
+        out->k = (uint32_t)k;
+        out->feasible = feas ? 1 : 0;
+        out->plan_cost = best;
+        *status = st;
+    }
+}
+
+__global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned long long NP,
+                               int nbm, const Key* result, const unsigned long long* err,
+                               const unsigned long long* __restrict__ binom, SolveOut* out) {
+    // one warp: decode the arg-min key (cut positions by a 32-wide ballot
+    // over the hockey-stick counts), then the warp plan detail
+    const int lane = threadIdx.x & 31;
+    const Key key = *result;
+    const unsigned long long e = *err;
+    if (lane == 0) {
+        out->key = key;
+        out->err = e;
+        out->k = (uint32_t)k;
+        out->status = GP_OK;
+    }
+    if (e != ~0ull || key.tie == ~0ull) return;
+    const int n = I.n;
+    const unsigned long long t = key.tie;
+    const int bm = (int)(t % (unsigned long long)nbm);
+    const unsigned long long pc = t / (unsigned long long)nbm;
+    uint8_t o[GP_MAX_STAGES];
+    int p[GP_MAX_STAGES + 1];
+    d_unrank_perm(k, pc / NC, o);
+    p[0] = 0;
+    unsigned long long rem = pc % NC;
+    int prev = 0;
+    auto C = [&](int nn, int r) -> unsigned long long {
+        return (r < 0 || nn < 0) ? 0ull : binom[(size_t)nn * (GP_MAX_STAGES + 1) + r];
+    };
+    for (int j = 1; j < k; ++j) {
+        const int r = k - 1 - j, lo = prev + 1;
+        const unsigned long long tot = C(n - lo, r + 1), thr = tot - rem;
+        int qsel = -1;
+        for (int base = lo; qsel < 0; base += 32) {
+            const int qq = base + lane;
+            const bool ok = qq <= n - 1 - r && C(n - qq - 1, r + 1) < thr;
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (m) qsel = base + __ffs(m) - 1;
+        }
+        rem -= tot - C(n - qsel, r + 1);
+        p[j] = qsel;
+        prev = qsel;
+    }
+    p[k] = n;
+    if (lane == 0) {
+        out->bm = (uint32_t)bm;
+        for (int s = 0; s < k; ++s) {
+            out->order[s] = o[s];
+            out->counts[s] = (uint8_t)(p[s + 1] - p[s]);
+        }
+    }
+    plan_detail_warp(I, k, o, p, bm, &out->info, &out->status);
+}
+

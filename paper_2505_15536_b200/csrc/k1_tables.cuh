@@ -1,0 +1,305 @@
+// k1_tables.cuh - K1: per-load table build (interval sums, group constants, stage and boundary tables).
+#pragma once
+#include "common.cuh"
+
+// ---- K1a: interval sums -----------------------------------------------------
+// sum(model.layers[i].<field> for i in range(a, b)) for every 0 <= a < b <= n,
+// each interval summed from its own start (never prefix differences).
+__device__ void k1_intervals_block(const DevInst& I, int col) {
+    // one CTA per column; the column is staged in shared memory so the
+    // sequential Neumaier sweeps read on-chip values
+    __shared__ double col_s[GP_MAX_LAYERS + 1];
+    for (int i = threadIdx.x; i < I.n; i += blockDim.x) {
+        double x;
+        switch (col) {
+            case COL_FWD: x = I.fwd[i]; break;
+            case COL_BWD: x = I.bwd_in[i]; break;
+            case COL_WGT: x = I.bwd_w[i]; break;
+            case COL_PARAM: x = I.param[i]; break;
+            default: x = (I.fwd[i] + I.bwd_in[i]) + I.bwd_w[i]; break;  // total_flops
+        }
+        col_s[i] = x;
+    }
+    __syncthreads();
+    size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
+    double* out = I.S + col * N2;
+    for (int a = threadIdx.x; a < I.n; a += blockDim.x) {
+        NeumaierSum sm;
+        for (int b = a + 1; b <= I.n; ++b) {
+            if (b == a + 1) sm.start(col_s[b - 1]); else sm.add(col_s[b - 1]);
+            out[tri_idx(I.n, a, b)] = sm.value();
+        }
+    }
+}
+
+// ---- K1b: per-group constants ---------------------------------------------------
+__device__ __forceinline__ double block_min128(double v, double* red) {
+    // exact min over a 128-thread block (min is order-independent)
+    for (int off = 16; off > 0; off >>= 1) {
+        double o = __shfl_down_sync(0xffffffffu, v, off);
+        v = o < v ? o : v;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = red[w] < r ? red[w] : r;
+    return r;
+}
+
+// one 128-thread block per group: members loaded in parallel into shared
+// memory, then the (sequential) factorisation runs on-chip
+__device__ void k1_group_block(const DevInst& I, int f) {
+    __shared__ double caps[GP_MAX_MEMBERS];
+    __shared__ double red[4];
+    const int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    const int nmem = m1 - m0;
+    double mn = INFINITY;
+    for (int j = threadIdx.x; j < nmem; j += blockDim.x) {
+        const int d = I.fg_mem[m0 + j];
+        caps[j] = I.p_c[d];
+        const double mm = I.mem[d];
+        mn = mm < mn ? mm : mn;
+    }
+    mn = block_min128(mn, red);
+    if (threadIdx.x == 0) {
+        I.g_minmem[f] = mn;
+        I.g_tp_ok[f] = gpd::tp_grid(caps, nmem, I.g_rf + m0, I.g_cf + m0) ? 1 : 0;
+        const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
+        if (s1 > s0) gpd::dp_fractions(I.sg_cap + s0, s1 - s0, I.g_dp + s0);
+    }
+    const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
+    for (int g = s0; g < s1; ++g) {
+        double sm = INFINITY;
+        for (int x = I.sg_off[g] + threadIdx.x; x < (int)I.sg_off[g + 1]; x += blockDim.x) {
+            const double mm = I.mem[I.sg_mem[x]];
+            sm = mm < sm ? mm : sm;
+        }
+        sm = block_min128(sm, red);
+        if (threadIdx.x == 0) I.sg_minmem[g] = I.sg_off[g + 1] > I.sg_off[g] ? sm : 0.0;
+    }
+}
+
+// recompute min_intra_bandwidth over member pairs (bandwidth snapshots;
+// src/grouping.py:69-75 on the rebuilt topology)
+__global__ void k1_minbw(DevInst I, double* out) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= I.F) return;
+    int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    double mn = 0.0;
+    bool have = false;
+    for (int x = m0; x < m1; ++x)
+        for (int y = x + 1; y < m1; ++y) {
+            double w = I.bw[(size_t)I.fg_mem[x] * I.D + I.fg_mem[y]];
+            if (!have || w < mn) mn = w;
+            have = true;
+        }
+    out[f] = have ? mn : 0.0;
+}
+
+// split choice for one (group, layer range): choose_intra_split
+// (src/planner.py:157-200).  Writes PP shares when kind == ASYM_PP.
+__device__ int choose_split(const DevInst& I, int f, int a, int b, int* shares, int* nparts) {
+    int nmem = I.fg_off[f + 1] - I.fg_off[f];
+    int s0 = I.fg_sg_off[f], nsg = I.fg_sg_off[f + 1] - s0;
+    *nparts = 0;
+    if (nmem == 1 || nsg == 1) return GP_UNIFORM;
+    const double* caps = I.sg_cap + s0;
+    int nl = b - a;
+    if (nsg <= nl && gpd::proportional_split(nl, caps, nsg, 1, shares)) {
+        double times[GP_MAX_SGS];
+        int pos = a;
+        for (int j = 0; j < nsg; ++j) {
+            times[j] = Ssum(I, COL_TF, pos, pos + shares[j]) / caps[j];
+            pos += shares[j];
+        }
+        double mean = gpd::psum(times, nsg) / (double)nsg;
+        double mx = times[0];
+        for (int j = 1; j < nsg; ++j) mx = times[j] > mx ? times[j] : mx;
+        if (mx <= I.bf * mean) { *nparts = nsg; return GP_ASYM_PP; }
+    }
+    if (I.g_tp_ok[f]) { *nparts = nmem; return GP_ASYM_TP_DP; }
+    *nparts = nsg;
+    return GP_ASYM_DP;
+}
+
+// ---- K1c: stage table -------------------------------------------------------------
+// One thread per (group, a, b).  memory_feasible is local to a stage because
+// every group appears in exactly one stage (src/planner.py:226-253).
+__device__ void k1_stage_t(const DevInst& I, long long t) {
+    int n = I.n;
+    int N1 = n + 1;
+    long long total = (long long)I.F * N1 * N1;
+    if (t >= total) return;
+    int f = (int)(t / (N1 * N1));
+    int rem = (int)(t % (N1 * N1));
+    int a = rem / N1, b = rem % N1;
+    size_t N2 = (size_t)N1 * N1;
+    size_t e = (size_t)f * N2 + rem;
+    if (a >= b) {
+        I.scode[e] = SC_INFEASIBLE;
+        I.skind[e] = 0;
+        I.C1[e] = INFINITY;
+        I.fbws[e] = make_double4(NAN, NAN, NAN, NAN);
+        for (int mi = 0; mi < I.nm; ++mi) {
+            I.stg[(size_t)mi * I.F * N2 + e] = make_double2(INFINITY, 0.0);
+            if (a == n && b == n) I.tcol[((size_t)mi * I.F + f) * (n + 1) + n] = make_double2(INFINITY, 0.0);
+        }
+        return;
+    }
+    int shares[GP_MAX_SGS], np;
+    int kind = choose_split(I, f, a, b, shares, &np);
+    I.skind[e] = (uint8_t)kind;
+    double P = Ssum(I, COL_PARAM, a, b);
+    int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
+    int s0 = I.fg_sg_off[f];
+    // memory feasibility: bytes_needed > memory_bytes -> infeasible
+    bool feas = true;
+    if (kind == GP_ASYM_PP) {
+        int pos = a;
+        for (int j = 0; j < np && feas; ++j) {
+            double sub = Ssum(I, COL_PARAM, pos, pos + shares[j]);
+            if (I.sg_off[s0 + j + 1] > I.sg_off[s0 + j]) feas = !(sub > I.sg_minmem[s0 + j]);
+            pos += shares[j];
+        }
+    } else if (kind == GP_ASYM_TP_DP) {
+        for (int x = m0; x < m1 && feas; ++x)
+            feas = !(((P * I.g_rf[x]) * I.g_cf[x]) > I.mem[I.fg_mem[x]]);
+    } else {
+        feas = !(P > I.g_minmem[f]);
+    }
+    // effective_capacity (src/timing.py:116-143)
+    uint8_t code = SC_OK;
+    double cap;
+    if (kind == GP_ASYM_PP) {
+        double tot = Ssum(I, COL_TF, a, b);
+        bool have = false;
+        double best = 0.0;
+        int pos = a;
+        for (int j = 0; j < np; ++j) {
+            double sub = Ssum(I, COL_TF, pos, pos + shares[j]);
+            pos += shares[j];
+            double frac = sub / tot;
+            if (frac > 0) {
+                double val = I.sg_cap[s0 + j] / frac;
+                if (!have || val < best) best = val;
+                have = true;
+            }
+        }
+        cap = best;
+        if (!have) code = SC_DEGENERATE;
+    } else {
+        cap = I.fg_cap[f];
+        if (!(cap > 0)) code = SC_DEGENERATE;
+    }
+    // per-sample times (src/timing.py:198-200) and C1 (src/costmodel.py:59)
+    double Fp = Ssum(I, COL_FWD, a, b) / cap;
+    double Bp = Ssum(I, COL_BWD, a, b) / cap;
+    double Wp = Ssum(I, COL_WGT, a, b) / cap;
+    double c1 = (Fp + Bp) + Wp;
+    I.C1[e] = c1;
+    // collective + sync rule (src/timing.py:146-173)
+    int nmem = m1 - m0;
+    bool has = I.fg_has_minbw[f] != 0;
+    double mbw = I.fg_minbw[f];
+    // StageTiming.sync_seconds = intra_group_seconds(params, fg) (src/timing.py:195)
+    double sync = (P == 0.0 || !has) ? 0.0 : (mbw > 0 ? P / mbw : NAN);
+    I.fbws[e] = make_double4(Fp, Bp, Wp, sync);
+    if (code == SC_OK && has && !(mbw > 0) && (nmem >= 2 || P != 0.0)) code = SC_TOPOLOGY;
+    bool overflow = false;
+    for (int mi = 0; mi < I.nm; ++mi) {
+        double md = (double)I.micro[mi];
+        double al = 0.0;
+        if (nmem >= 2) {
+            double V = 2.0 * P;
+            if (kind == GP_ASYM_TP_DP) V = V + I.act[b - 1] * md;
+            if (V != 0.0 && has && mbw > 0) al = V / mbw;
+        }
+        double cm = c1 * md;
+        if (feas && isinf(cm)) overflow = true;
+        I.vtab[((size_t)mi * I.F + f) * ((size_t)n * (n + 1) / 2) + (a * n - a * (a - 1) / 2) + (b - a - 1)] =
+            nmem >= 2 ? (kind == GP_ASYM_TP_DP ? 2.0 * P + I.act[b - 1] * md : 2.0 * P) : 0.0;
+        double2 v = make_double2(feas ? cm : INFINITY, al);
+        I.stg[(size_t)mi * I.F * N2 + e] = v;
+        size_t ntri = (size_t)n * (n + 1) / 2;
+        I.tpk[((size_t)mi * I.F + f) * ntri + (a * n - a * (a - 1) / 2) + (b - a - 1)] = v;
+        if (b == n) I.tcol[((size_t)mi * I.F + f) * (n + 1) + a] = v;
+    }
+    I.scode[e] = feas ? code : SC_INFEASIBLE;
+    if (feas && code != SC_OK) atomicOr(I.flags, FLAG_STAGE_ERROR);
+    if (overflow) atomicOr(I.flags, FLAG_OVERFLOW);
+}
+
+// ---- K1d: gateways and boundary transfer table -------------------------------------
+// gateway_link (src/timing.py:104-113): argmin over (p_t, u, v) with string
+// order of ids, u in the upstream group, v in the downstream group.
+__device__ void k1_gateway_warp(const DevInst& I, int warp, int lane) {
+    // one warp per ordered pair (fa, fb); lanes scan member pairs, then a
+    // warp argmin on the key (p_t, rank(u), rank(v))
+    const int fa = warp / I.F, fb = warp % I.F;
+    const int a0 = I.fg_off[fa], na = I.fg_off[fa + 1] - a0;
+    const int b0 = I.fg_off[fb], nbm = I.fg_off[fb + 1] - b0;
+    bool have = false;
+    double bp = 0.0;
+    unsigned int bu = 0, bv = 0, ru = 0xffffffffu, rv = 0xffffffffu;
+    for (int t = lane; t < na * nbm; t += 32) {
+        const unsigned int u = I.fg_mem[a0 + t / nbm], v = I.fg_mem[b0 + t % nbm];
+        const double p = I.p_t[(size_t)u * I.D + v];
+        const unsigned int qu = I.id_rank[u], qv = I.id_rank[v];
+        bool less = !have || p < bp || (p == bp && (qu < ru || (qu == ru && qv < rv)));
+        if (less) { have = true; bp = p; bu = u; bv = v; ru = qu; rv = qv; }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const bool oh = __shfl_down_sync(0xffffffffu, have, off);
+        const double op = __shfl_down_sync(0xffffffffu, bp, off);
+        const unsigned int ou = __shfl_down_sync(0xffffffffu, bu, off);
+        const unsigned int ov = __shfl_down_sync(0xffffffffu, bv, off);
+        const unsigned int oru = __shfl_down_sync(0xffffffffu, ru, off);
+        const unsigned int orv = __shfl_down_sync(0xffffffffu, rv, off);
+        bool take = oh && (!have || op < bp || (op == bp && (oru < ru || (oru == ru && orv < rv))));
+        if (take) { have = true; bp = op; bu = ou; bv = ov; ru = oru; rv = orv; }
+    }
+    if (lane == 0) {
+        I.gw[warp] = (int)(bu * I.D + bv);
+        if (fa != fb && !(I.bw[(size_t)bu * I.D + bv] > 0)) atomicOr(I.flags, FLAG_GATEWAY_ERROR);
+    }
+}
+
+__global__ void k1_gateways(DevInst I) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (warp < I.F * I.F) k1_gateway_warp(I, warp, threadIdx.x & 31);
+}
+
+// K1 phase 1 in one launch: blocks [0,5) interval sums, [5, 5+F) group
+// constants, the rest gateways (one warp per ordered group pair)
+__device__ void k1_intervals_block(const DevInst& I, int col);
+__device__ void k1_gateway_warp(const DevInst& I, int warp, int lane);
+
+__global__ void __launch_bounds__(128) k1_phase1(DevInst I) {
+    const int b = blockIdx.x;
+    if (b < 5) { k1_intervals_block(I, b); return; }
+    if (b < 5 + I.F) { k1_group_block(I, b - 5); return; }
+    const int warp = (b - 5 - I.F) * 4 + (threadIdx.x >> 5);
+    if (warp < I.F * I.F) k1_gateway_warp(I, warp, threadIdx.x & 31);
+}
+
+__device__ void k1_boundary_t(const DevInst& I, long long t) {
+    long long total = (long long)I.nm * I.F * I.F * I.n;
+    if (t >= total) return;
+    int j = (int)(t % I.n);
+    long long r = t / I.n;
+    int pair = (int)(r % (I.F * I.F));
+    int mi = (int)(r / (I.F * I.F));
+    int g = I.gw[pair];
+    double md = (double)I.micro[mi];
+    // transfer_seconds: latency + (act*m)/bandwidth (src/timing.py:91-97)
+    I.xt[(size_t)r * I.nxp + j] = I.lat[g] + (I.act[j] * md) / I.bw[g];
+}
+
+// K1 phase 2 in one launch: stage table entries, then boundary x entries
+__global__ void k1_phase2(DevInst I, long long n_stage) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_stage) k1_stage_t(I, t);
+    else k1_boundary_t(I, t - n_stage);
+}
+
