@@ -169,6 +169,19 @@ typedef struct gp_timing {
     double grad[GP_MAX_STAGES];        /* .grad_bytes_per_sample         */
 } gp_timing;
 
+/* schedule policies (src/engine.py:48-52) */
+enum { GP_POLICY_GPIPE = 0, GP_POLICY_1F1B = 1, GP_POLICY_ZB_ORIGINAL = 2, GP_POLICY_ZB_COMPACT = 3 };
+
+#define GP_MAX_BREAKPOINTS 32
+/* NetworkTrace (src/nettrace.py:12-45) restricted to the plan's boundary
+ * links "b-(b+1)": per boundary b, n_points[b] breakpoints (t, multiplier)
+ * sorted by strictly increasing t; the multiplier before the first one is 1. */
+typedef struct gp_trace {
+    uint32_t n_points[GP_MAX_STAGES];
+    double t[GP_MAX_STAGES][GP_MAX_BREAKPOINTS];
+    double mult[GP_MAX_STAGES][GP_MAX_BREAKPOINTS];
+} gp_trace;
+
 typedef struct gp_ctx gp_ctx;
 
 /* Version / capability probe (no device needed). */
@@ -258,6 +271,16 @@ int gp_set_bandwidth(gp_ctx *ctx, const double *bandwidth);
  */
 int gp_sim_1f1b(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t iterations,
                 double *makespan, uint8_t *status);
+/*
+ * Makespans under any schedule policy and network trace:
+ * simulate_timing(timings[i], policy, trace, adapter_enabled=False,
+ * SimConfig(iterations)).makespan with trace = traces[trace_index[i]]
+ * (constant trace when traces is NULL / n_traces == 0; trace_index NULL
+ * means trace 0 for every timing).  Host pointers.
+ */
+int gp_simulate(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t policy,
+                uint32_t iterations, const gp_trace *traces, uint32_t n_traces,
+                const uint32_t *trace_index, double *makespan, uint8_t *status);
 /* Same with device pointers, asynchronous on the context's stream. */
 int gp_sim_1f1b_device(gp_ctx *ctx, const gp_timing *d_timings, uint64_t n,
                        uint32_t iterations, double *d_makespan, uint8_t *d_status);

@@ -760,8 +760,9 @@ size_t or_abi_sizeof(int which)
 }
 
 /* ------------------------------------------------------------------------
- * PipelineEngine.run for Policy.ONE_F_ONE_B, constant trace, no adapter,
- * synchronous iterations (src/engine.py:125-431, src/nettrace.py:57-76).
+ * PipelineEngine.run for any Policy, any NetworkTrace on the boundary links,
+ * no adapter, synchronous iterations (src/engine.py:125-431,
+ * src/nettrace.py:12-76).
  * A direct restatement with the reference's data structures: per
  * (stage, iteration) pools, FIFO link queues, a (time, seq) binary heap.
  * ---------------------------------------------------------------------- */
@@ -837,7 +838,52 @@ typedef struct {
     int busy;
 } sim_link;
 
+/* NetworkTrace.multiplier (src/nettrace.py:36-43): bisect_right - 1 */
+static double trace_mult(const gp_trace *tr, int link, double t)
+{
+    if (!tr)
+        return 1.0;
+    int np = (int)tr->n_points[link];
+    int idx = -1;
+    for (int i = 0; i < np; ++i)
+        if (tr->t[link][i] <= t)
+            idx = i;
+    return idx < 0 ? 1.0 : tr->mult[link][idx];
+}
+
+/* transfer_end_time (src/nettrace.py:57-76) */
+static double transfer_end(double start, double bytes, double base_bw, double latency,
+                           const gp_trace *tr, int link)
+{
+    double t = start, remaining = bytes;
+    if (tr) {
+        int np = (int)tr->n_points[link];
+        for (int i = 0; i < np; ++i) {
+            double bp_t = tr->t[link][i];
+            if (!(bp_t > start))
+                continue;
+            double bw = base_bw * trace_mult(tr, link, t);
+            double span = bp_t - t;
+            if (remaining <= bw * span)
+                return (t + remaining / bw) + latency;
+            remaining -= bw * span;
+            t = bp_t;
+        }
+    }
+    double bw = base_bw * trace_mult(tr, link, t);
+    return (t + remaining / bw) + latency;
+}
+
+int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
+           double *makespan_out);
+
 int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
+{
+    return or_sim(T, GP_POLICY_1F1B, iterations, NULL, makespan_out);
+}
+
+int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
+           double *makespan_out)
 {
     const int S = (int)T->n_stages;
     if (S < 1 || S > GP_MAX_STAGES || iterations < 1)
@@ -879,8 +925,8 @@ int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
             L_->head++;                                                                    \
             L_->busy = 1;                                                                  \
             double per_ = (dir) == 0 ? T->act[bnd] : T->grad[bnd];                         \
-            double bw_ = T->bw[bnd] * 1.0;                                                 \
-            double end_ = ((tnow) + (per_ * (double)sz_) / bw_) + T->lat[bnd];            \
+            double end_ = transfer_end((tnow), per_ * (double)sz_, T->bw[bnd], T->lat[bnd], \
+                                       trace, (bnd));                                      \
             sim_ev e_ = {end_, seq++, 1, (bnd), (dir), it_, sz_};                          \
             heap_push(&H, e_);                                                             \
         }                                                                                  \
@@ -900,7 +946,8 @@ int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
                 if (it >= iterations)
                     continue;
                 sim_pool *p = POOL(s, it);
-                /* _ready_op (src/engine.py:157-215), ONE_F_ONE_B */
+                /* _ready_op (src/engine.py:157-215): candidates F, B, W, SYNC, OPT
+                 * in this order; the lowest priority wins, the earliest on ties */
                 int best_pr = 100, best_k = -1;
                 int64_t best_sz = 0;
                 int64_t size = m;
@@ -908,12 +955,16 @@ int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
                 if (fwd_rem > 0) {
                     int64_t chunk = size < fwd_rem ? size : fwd_rem;
                     if (p->fwd_avail - p->fwd_taken >= chunk) {
-                        int64_t quota = (int64_t)(S - s) * m;
                         int pr = -1;
-                        if (p->fwd_taken < quota)
-                            pr = 1;
-                        else if (p->fwd_taken + chunk <= quota + p->bwd_done)
-                            pr = 2;
+                        if (policy == GP_POLICY_ZB_COMPACT || policy == GP_POLICY_GPIPE) {
+                            pr = policy == GP_POLICY_ZB_COMPACT ? 0 : 1;
+                        } else {
+                            int64_t quota = (int64_t)(S - s) * m;
+                            if (p->fwd_taken < quota)
+                                pr = policy == GP_POLICY_ZB_ORIGINAL ? 0 : 1;
+                            else if (p->fwd_taken + chunk <= quota + p->bwd_done)
+                                pr = policy == GP_POLICY_ZB_ORIGINAL ? 3 : 2;
+                        }
                         if (pr >= 0 && pr < best_pr) {
                             best_pr = pr;
                             best_k = 0;
@@ -922,21 +973,26 @@ int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
                     }
                 }
                 int64_t bwd_rem = B - p->bwd_taken;
-                if (bwd_rem > 0) {
+                int gate = policy != GP_POLICY_GPIPE || p->fwd_done == B;
+                if (bwd_rem > 0 && gate) {
                     int64_t chunk = size < bwd_rem ? size : bwd_rem;
                     int64_t av = (p->bwd_avail < p->fwd_done ? p->bwd_avail : p->fwd_done) - p->bwd_taken;
                     if (s == S - 1)
                         av = p->fwd_done - p->bwd_taken;
-                    if (av >= chunk && 2 < best_pr) {
-                        best_pr = 2;
+                    int pr = (policy == GP_POLICY_ZB_COMPACT || policy == GP_POLICY_ZB_ORIGINAL) ? 1 : 2;
+                    if (av >= chunk && pr < best_pr) {
+                        best_pr = pr;
                         best_k = 1;
                         best_sz = chunk;
                     }
                 }
-                if (p->wq_head < p->wq_tail && 0 < best_pr) {
-                    best_pr = 0;
-                    best_k = 2;
-                    best_sz = p->wq[p->wq_head];
+                if (p->wq_head < p->wq_tail) {
+                    int pr = (policy == GP_POLICY_GPIPE || policy == GP_POLICY_1F1B) ? 0 : 2;
+                    if (pr < best_pr) {
+                        best_pr = pr;
+                        best_k = 2;
+                        best_sz = p->wq[p->wq_head];
+                    }
                 }
                 if (p->w_done == B && p->wq_head == p->wq_tail && !p->sync_done && 8 < best_pr) {
                     best_pr = 8;
@@ -1046,6 +1102,20 @@ int or_sim_batch(const gp_timing *T, uint64_t n, int iterations, double *makespa
     for (uint64_t i = 0; i < n; ++i) {
         double ms = NAN;
         int st = or_sim_1f1b(&T[i], iterations, &ms);
+        makespan[i] = ms;
+        status[i] = (uint8_t)st;
+    }
+    return GP_OK;
+}
+
+int or_sim_policy_batch(const gp_timing *T, uint64_t n, int policy, int iterations,
+                        const gp_trace *traces, const uint32_t *trace_index, double *makespan,
+                        uint8_t *status)
+{
+    for (uint64_t i = 0; i < n; ++i) {
+        double ms = NAN;
+        const gp_trace *tr = traces ? &traces[trace_index ? trace_index[i] : 0] : NULL;
+        int st = or_sim(&T[i], policy, iterations, tr, &ms);
         makespan[i] = ms;
         status[i] = (uint8_t)st;
     }

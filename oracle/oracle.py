@@ -57,6 +57,9 @@ def lib():
         L.or_sim_1f1b.argtypes = [P(abi.GpTiming), C.c_int, P(C.c_double)]
         L.or_sim_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, P(C.c_double),
                                    P(C.c_uint8)]
+        L.or_sim_policy_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, C.c_int,
+                                          P(abi.GpTrace), P(C.c_uint32), P(C.c_double),
+                                          P(C.c_uint8)]
         _lib = L
     return _lib
 
@@ -150,4 +153,17 @@ def sim_batch(packed_timings, n, iterations=1):
     ms = np.empty(n, dtype=np.float64)
     st = np.empty(n, dtype=np.uint8)
     lib().or_sim_batch(packed_timings, n, int(iterations), _dp(ms), _u8(st))
+    return ms, st
+
+
+def sim_policy_batch(packed_timings, n, policy, iterations=1, traces=None, trace_index=None):
+    """(makespans, status) under ``policy`` (abi.POLICY_CODE) and traces."""
+    ms = np.empty(n, dtype=np.float64)
+    st = np.empty(n, dtype=np.uint8)
+    ti = None
+    if trace_index is not None:
+        ti = np.ascontiguousarray(trace_index, dtype=np.uint32)
+    lib().or_sim_policy_batch(packed_timings, n, int(policy), int(iterations), traces,
+                              ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
+                              _dp(ms), _u8(st))
     return ms, st

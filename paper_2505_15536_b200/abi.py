@@ -124,3 +124,16 @@ class GpTiming(C.Structure):
         ("bw", C.c_double * GP_MAX_STAGES), ("act", C.c_double * GP_MAX_STAGES),
         ("grad", C.c_double * GP_MAX_STAGES),
     ]
+
+
+GP_POLICY_GPIPE, GP_POLICY_1F1B, GP_POLICY_ZB_ORIGINAL, GP_POLICY_ZB_COMPACT = 0, 1, 2, 3
+POLICY_CODE = {"gpipe": 0, "1f1b": 1, "zb_original": 2, "zb_compact": 3}
+GP_MAX_BREAKPOINTS = 32
+
+
+class GpTrace(C.Structure):
+    _fields_ = [
+        ("n_points", C.c_uint32 * GP_MAX_STAGES),
+        ("t", (C.c_double * GP_MAX_BREAKPOINTS) * GP_MAX_STAGES),
+        ("mult", (C.c_double * GP_MAX_BREAKPOINTS) * GP_MAX_STAGES),
+    ]

@@ -100,6 +100,8 @@ struct gp_ctx {
     DBuf<SolveOut> dsolve;
     DBuf<unsigned long long> gbest;  // K4 shared incumbent
     DBuf<gp_timing> s_tim;       // K5 staging
+    DBuf<gp_trace> s_traces;
+    DBuf<uint32_t> s_tidx;
     // K6 snapshot batch buffers
     DBuf<double> z_bw, z_mbw, z_xt;
     DBuf<uint32_t> z_flags;
@@ -239,7 +241,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     if (c->h_solve) cudaFreeHost(c->h_solve);
     c->z_bw.release(); c->z_mbw.release(); c->z_xt.release(); c->z_flags.release();
     c->z_tpk.release(); c->z_tcol.release(); c->z_res.release(); c->z_cnt.release();
-    c->dsolve.release(); c->gbest.release(); c->s_tim.release(); c->s_ms.release(); c->s_st.release();
+    c->dsolve.release(); c->gbest.release(); c->s_tim.release(); c->s_traces.release(); c->s_tidx.release(); c->s_ms.release(); c->s_st.release();
     if (c->flags_ev) cudaEventDestroy(c->flags_ev);
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
@@ -1154,10 +1156,55 @@ int gp_sim_1f1b_device(gp_ctx* c, const gp_timing* d_timings, uint64_t n, uint32
     if (!c) return fail(GP_ERR_INPUT, "null context");
     if (n == 0) return GP_OK;
     CUDA_TRY(cudaSetDevice(c->device));
-    k5_sim_1f1b<<<(unsigned)((n + 127) / 128), 128, 0, c->stream>>>(d_timings, (long long)n,
-                                                                   (int)iterations, d_makespan,
-                                                                   d_status);
+    k5_sim_1f1b<<<(unsigned)((n + 127) / 128), 128, 0, c->stream>>>(
+        d_timings, (long long)n, GP_POLICY_1F1B, (int)iterations, nullptr, nullptr, d_makespan,
+        d_status);
     CUDA_TRY(cudaGetLastError());
+    return GP_OK;
+}
+
+int gp_simulate(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy,
+                uint32_t iterations, const gp_trace* traces, uint32_t n_traces,
+                const uint32_t* trace_index, double* makespan, uint8_t* status) {
+    if (!c) return fail(GP_ERR_INPUT, "null context");
+    if (policy > GP_POLICY_ZB_COMPACT) return fail(GP_ERR_INPUT, "unknown policy %u", policy);
+    if (n == 0) return GP_OK;
+    if (traces && n_traces == 0) traces = nullptr;
+    if (traces && trace_index)
+        for (uint64_t i = 0; i < n; ++i)
+            if (trace_index[i] >= n_traces) return fail(GP_ERR_INPUT, "trace index out of range");
+    if (traces)
+        for (uint32_t t = 0; t < n_traces; ++t)
+            for (int b = 0; b < GP_MAX_STAGES; ++b)
+                if (traces[t].n_points[b] > GP_MAX_BREAKPOINTS)
+                    return fail(GP_ERR_INPUT, "trace %u link %d: too many breakpoints", t, b);
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->s_tim.ensure(n));
+    CUDA_TRY(c->s_ms.ensure(n));
+    CUDA_TRY(c->s_st.ensure(n));
+    CUDA_TRY(cudaMemcpyAsync(c->s_tim.p, timings, n * sizeof(gp_timing), cudaMemcpyHostToDevice, s));
+    gp_trace* d_tr = nullptr;
+    uint32_t* d_ti = nullptr;
+    if (traces) {
+        CUDA_TRY(c->s_traces.ensure(n_traces));
+        CUDA_TRY(cudaMemcpyAsync(c->s_traces.p, traces, n_traces * sizeof(gp_trace),
+                                 cudaMemcpyHostToDevice, s));
+        d_tr = c->s_traces.p;
+        if (trace_index) {
+            CUDA_TRY(c->s_tidx.ensure(n));
+            CUDA_TRY(cudaMemcpyAsync(c->s_tidx.p, trace_index, n * sizeof(uint32_t),
+                                     cudaMemcpyHostToDevice, s));
+            d_ti = c->s_tidx.p;
+        }
+    }
+    k5_sim_1f1b<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(c->s_tim.p, (long long)n, (int)policy,
+                                                           (int)iterations, d_tr, d_ti, c->s_ms.p,
+                                                           c->s_st.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(makespan, c->s_ms.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return GP_OK;
 }
 

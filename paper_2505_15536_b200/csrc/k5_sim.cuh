@@ -41,7 +41,37 @@ __device__ __forceinline__ SimPool& sim_pool(SimPool* P, int s, int it) {
     return p;
 }
 
-__device__ int sim_1f1b_dev(const gp_timing& T, int iterations, double* makespan) {
+// NetworkTrace.multiplier (src/nettrace.py:36-43): last breakpoint <= t
+__device__ __forceinline__ double trace_mult(const gp_trace* tr, int link, double t) {
+    const int np = (int)tr->n_points[link];
+    double m = 1.0;
+    for (int i = 0; i < np; ++i)
+        if (tr->t[link][i] <= t) m = tr->mult[link][i];
+    return m;
+}
+
+// transfer_end_time (src/nettrace.py:57-76)
+__device__ double transfer_end(double start, double bytes, double base_bw, double latency,
+                               const gp_trace* tr, int link) {
+    double t = start, remaining = bytes;
+    if (tr) {
+        const int np = (int)tr->n_points[link];
+        for (int i = 0; i < np; ++i) {
+            const double bp_t = tr->t[link][i];
+            if (!(bp_t > start)) continue;
+            const double bw = base_bw * trace_mult(tr, link, t);
+            const double span = bp_t - t;
+            if (remaining <= bw * span) return (t + remaining / bw) + latency;
+            remaining -= bw * span;
+            t = bp_t;
+        }
+    }
+    const double bw = base_bw * (tr ? trace_mult(tr, link, t) : 1.0);
+    return (t + remaining / bw) + latency;
+}
+
+__device__ int sim_dev(const gp_timing& T, int policy, int iterations, const gp_trace* trace,
+                       double* makespan) {
     const int S = (int)T.n_stages;
     if (S < 1 || S > GP_MAX_STAGES || iterations < 1 || T.microbatch <= 0) return GP_ERR_TIMING;
     const long long B = T.batch, m = T.microbatch;
@@ -75,9 +105,8 @@ __device__ int sim_1f1b_dev(const gp_timing& T, int iterations, double* makespan
         const long long sz = chunk_size(j);
         const int it = (int)(j / nchunk);
         const double per = dir == 0 ? T.act[bnd] : T.grad[bnd];
-        const double bw = T.bw[bnd] * 1.0;  // base * multiplier(1.0)
         SimEv& e = ev[nev++];
-        e.t = (tnow + (per * (double)sz) / bw) + T.lat[bnd];
+        e.t = transfer_end(tnow, per * (double)sz, T.bw[bnd], T.lat[bnd], trace, bnd);
         e.seq = seq++;
         e.code = (int)(1u << 31) | (bnd << 20) | (dir << 16) | it;
         e.size = (int)sz;
@@ -93,29 +122,38 @@ __device__ int sim_1f1b_dev(const gp_timing& T, int iterations, double* makespan
                 const int it = cur[s];
                 if (it >= iterations) continue;
                 SimPool& p = sim_pool(P, s, it);
-                // _ready_op (src/engine.py:157-215), ONE_F_ONE_B priorities
+                // _ready_op (src/engine.py:157-215): candidates F, B, W, SYNC,
+                // OPT in this order; lowest priority wins, earliest on ties
+                const bool zbc = policy == GP_POLICY_ZB_COMPACT, zbo = policy == GP_POLICY_ZB_ORIGINAL;
+                const bool gpipe = policy == GP_POLICY_GPIPE;
                 int best_pr = 100, best_k = -1;
                 long long best_sz = 0;
                 const long long fwd_rem = B - p.fwd_taken;
                 if (fwd_rem > 0) {
                     const long long chunk = m < fwd_rem ? m : fwd_rem;
                     if (p.fwd_avail - p.fwd_taken >= chunk) {
-                        const long long quota = (long long)(S - s) * m;
                         int pr = -1;
-                        if (p.fwd_taken < quota) pr = 1;
-                        else if (p.fwd_taken + chunk <= quota + p.bwd_done) pr = 2;
+                        if (zbc || gpipe) {
+                            pr = zbc ? 0 : 1;
+                        } else {
+                            const long long quota = (long long)(S - s) * m;
+                            if (p.fwd_taken < quota) pr = zbo ? 0 : 1;
+                            else if (p.fwd_taken + chunk <= quota + p.bwd_done) pr = zbo ? 3 : 2;
+                        }
                         if (pr >= 0) { best_pr = pr; best_k = 0; best_sz = chunk; }
                     }
                 }
                 const long long bwd_rem = B - p.bwd_taken;
-                if (bwd_rem > 0) {
+                if (bwd_rem > 0 && (!gpipe || p.fwd_done == B)) {
                     const long long chunk = m < bwd_rem ? m : bwd_rem;
                     long long av = (p.bwd_avail < p.fwd_done ? p.bwd_avail : p.fwd_done) - p.bwd_taken;
                     if (s == S - 1) av = p.fwd_done - p.bwd_taken;
-                    if (av >= chunk && 2 < best_pr) { best_pr = 2; best_k = 1; best_sz = chunk; }
+                    const int pr = (zbc || zbo) ? 1 : 2;
+                    if (av >= chunk && pr < best_pr) { best_pr = pr; best_k = 1; best_sz = chunk; }
                 }
-                if (p.wq_head < p.wq_tail && 0 < best_pr) {
-                    best_pr = 0; best_k = 2; best_sz = chunk_size(p.wq_head);
+                if (p.wq_head < p.wq_tail) {
+                    const int pr = (gpipe || policy == GP_POLICY_1F1B) ? 0 : 2;
+                    if (pr < best_pr) { best_pr = pr; best_k = 2; best_sz = chunk_size(p.wq_head); }
                 }
                 if (p.w_done == B && p.wq_head == p.wq_tail && !(p.flags & 1) && 8 < best_pr) {
                     best_pr = 8; best_k = 3; best_sz = 0;
@@ -232,17 +270,19 @@ __global__ void k5_sim_candidates(DevInst I, int k, long long ncand, const uint8
         }
     }
     double ms = NAN;
-    st = sim_1f1b_dev(T, iterations, &ms);
+    st = sim_dev(T, GP_POLICY_1F1B, iterations, nullptr, &ms);
     makespan[i] = ms;
     status[i] = (uint8_t)st;
 }
 
-__global__ void k5_sim_1f1b(const gp_timing* __restrict__ T, long long n, int iterations,
+__global__ void k5_sim_1f1b(const gp_timing* __restrict__ T, long long n, int policy, int iterations,
+                            const gp_trace* __restrict__ traces, const uint32_t* __restrict__ tidx,
                             double* __restrict__ makespan, uint8_t* __restrict__ status) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double ms = NAN;
-    int st = sim_1f1b_dev(T[i], iterations, &ms);
+    const gp_trace* tr = traces ? traces + (tidx ? tidx[i] : 0u) : nullptr;
+    int st = sim_dev(T[i], policy, iterations, tr, &ms);
     makespan[i] = ms;
     status[i] = (uint8_t)st;
 }

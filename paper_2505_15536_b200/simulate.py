@@ -1,11 +1,14 @@
-"""Batched 1F1B pipeline-time simulation (K5) - the makespan of the reference's
+"""Batched pipeline-time simulation (K5) - the makespan of the reference's
 discrete-event engine.
 
 ``simulate_makespans(timings, iterations)`` returns, for every timing,
 ``simulate_timing(timing, Policy.ONE_F_ONE_B, CONSTANT_TRACE,
 adapter_enabled=False, config=SimConfig(iterations=...)).makespan``
 (src/simulator.py:71-113 -> PipelineEngine.run, src/engine.py:230-431), bit
-for bit, computed by one GPU thread per timing.  Timings are the reference's
+for bit, computed by one GPU thread per timing;
+``simulate_makespans_policy`` does the same for GPIPE / 1F1B / ZB_ORIGINAL /
+ZB_COMPACT under per-timing NetworkTrace breakpoints (src/nettrace.py:12-76),
+e.g. to rank candidate plans by simulated makespan under bandwidth drops.  Timings are the reference's
 ``PlanTiming`` objects (or the mirrors below); ``make_timing`` mirrors the
 reference fixture builder (src/schedule.py:27-74).
 """
@@ -96,6 +99,46 @@ def pack_timings(timings: Sequence) -> "C.Array":
             r.act[b] = bt.act_bytes_per_sample
             r.grad[b] = bt.grad_bytes_per_sample
     return arr
+
+
+def pack_traces(traces: Sequence, n_boundaries: int = abi.GP_MAX_STAGES) -> "C.Array":
+    """NetworkTrace objects (``breakpoints: {link_id: ((t, mult), ...)}``) ->
+    gp_trace records; link "b-(b+1)" of boundary b (src/timing.py:219)."""
+    arr = (abi.GpTrace * max(1, len(traces)))()
+    for i, tr in enumerate(traces):
+        bps = getattr(tr, "breakpoints", tr) or {}
+        for link, points in bps.items():
+            try:
+                a, b = (int(x) for x in str(link).split("-"))
+            except ValueError:
+                continue  # links that are not stage boundaries never apply
+            if b != a + 1 or not 0 <= a < abi.GP_MAX_STAGES:
+                continue
+            if len(points) > abi.GP_MAX_BREAKPOINTS:
+                raise D.InputFileError(f"trace link {link}: more than "
+                                       f"{abi.GP_MAX_BREAKPOINTS} breakpoints")
+            arr[i].n_points[a] = len(points)
+            for j, (t, mult) in enumerate(points):
+                arr[i].t[a][j] = float(t)
+                arr[i].mult[a][j] = float(mult)
+    return arr
+
+
+def simulate_makespans_policy(timings: Sequence, policy: str = "1f1b", iterations: int = 1,
+                              traces: Sequence = (), trace_index=None, engine=None) -> np.ndarray:
+    """Makespans of ``simulate_timing(t, policy, trace, adapter_enabled=False,
+    SimConfig(iterations))`` for every timing (traces[trace_index[i]], or the
+    constant trace when ``traces`` is empty)."""
+    from .engine import default_engine
+    eng = engine if engine is not None else default_engine()
+    code = abi.POLICY_CODE[getattr(policy, "value", policy)]
+    arr = pack_timings(timings)
+    tr = pack_traces(traces) if traces else None
+    ms, st = eng.simulate(arr, len(timings), code, iterations, tr, len(traces), trace_index)
+    bad = np.nonzero(st)[0]
+    if bad.size:
+        abi.raise_for(int(st[bad[0]]), f"timing {int(bad[0])} failed to simulate")
+    return ms
 
 
 def simulate_makespans(timings: Sequence, iterations: int = 1, engine=None) -> np.ndarray:

@@ -195,6 +195,40 @@ def dump_sim():
     print(f"sim: {len(cases)} timings x 3 iteration counts, {time.time() - t0:.1f}s", flush=True)
 
 
+def dump_sim_policies():
+    """makespans under all four policies with random breakpoint traces."""
+    gp = geopipe()
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from test_schedule import random_timing
+    rng = random.Random(77)
+    cases = [random_timing(rng) for _ in range(400)]
+    traces = []
+    for t in cases:
+        bps = {}
+        for b in range(t.num_stages - 1):
+            if rng.random() < 0.75:
+                pts = sorted(set(round(rng.uniform(0.0, 25.0), 3) for _ in range(rng.randint(1, 8))))
+                bps[f"{b}-{b + 1}"] = [[x, rng.choice([0.25, 0.4, 0.5, 0.6, 0.8, 1.0, 1.5, 2.0])]
+                                       for x in pts]
+        traces.append(bps)
+    out = {"timings": [timing_to_dict(t) for t in cases], "traces": traces, "makespan": {}}
+    t0 = time.time()
+    for pol in gp.Policy:
+        for it in (1, 2):
+            ms = []
+            for t, bps in zip(cases, traces):
+                tr = gp.NetworkTrace(breakpoints={k: tuple(tuple(p) for p in v)
+                                                  for k, v in bps.items()})
+                try:
+                    ms.append(gp.simulate_timing(t, pol, tr,
+                                                 config=gp.SimConfig(iterations=it)).makespan)
+                except Exception as e:
+                    ms.append(type(e).__name__)
+            out["makespan"][f"{pol.value}:{it}"] = ms
+    G.save("sim_policies.json", out)
+    print(f"sim policies: {time.time() - t0:.1f}s", flush=True)
+
+
 def dump_sim_candidates():
     """simulate(build_plan(candidate), ONE_F_ONE_B) makespans of candidates."""
     gp = geopipe()
@@ -265,11 +299,13 @@ def main():
     os.makedirs(G.GOLDEN, exist_ok=True)
     ap_only = args.only_sim
     if ap_only:
+        dump_sim_policies()
         dump_sim()
         dump_sim_candidates()
         dump_snapshots()
         return
     dump_sim()
+    dump_sim_policies()
     dump_sim_candidates()
     dump_snapshots()
 

@@ -125,3 +125,47 @@ def test_k5_candidates_match_reference_simulate(engine, oracle_lib, name):
                 assert s_ == 3
             else:
                 assert s_ == 0 and m_ == r[1 + col], (r, m_)
+
+
+# ---------------------------------------------------------------- policies --
+POL = G.load("sim_policies.json")
+POL_TIMINGS = [_timing(d) for d in POL["timings"]]
+
+
+def _pol_expected(key):
+    ms = POL["makespan"][key]
+    return np.array([m if not isinstance(m, str) else np.nan for m in ms])
+
+
+@pytest.mark.parametrize("key", sorted(POL["makespan"]))
+def test_oracle_policies_and_traces(oracle_lib, key):
+    from paper_2505_15536_b200 import abi
+    pol, it = key.split(":")
+    arr = SM.pack_timings(POL_TIMINGS)
+    tr = SM.pack_traces(POL["traces"])
+    ms, st = oracle_lib.sim_policy_batch(arr, len(POL_TIMINGS), abi.POLICY_CODE[pol], int(it), tr,
+                                         np.arange(len(POL_TIMINGS)))
+    exp = _pol_expected(key)
+    assert (st == 0).all()
+    assert (ms.view(np.uint64) == exp.view(np.uint64)).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", sorted(POL["makespan"]))
+def test_k5_policies_and_traces(engine, key):
+    pol, it = key.split(":")
+    ms = SM.simulate_makespans_policy(POL_TIMINGS, pol, int(it), POL["traces"],
+                                      np.arange(len(POL_TIMINGS)), engine=engine)
+    exp = _pol_expected(key)
+    assert (ms.view(np.uint64) == exp.view(np.uint64)).all()
+
+
+@pytest.mark.gpu
+def test_k5_constant_trace_policies_match_oracle(engine, oracle_lib):
+    from paper_2505_15536_b200 import abi
+    tims = _random_timings(5000, 21)
+    arr = SM.pack_timings(tims)
+    for pol, code in abi.POLICY_CODE.items():
+        ms = SM.simulate_makespans_policy(tims, pol, 2, engine=engine)
+        oms, ost = oracle_lib.sim_policy_batch(arr, len(tims), code, 2)
+        assert (ms.view(np.uint64) == oms.view(np.uint64)).all(), pol
