@@ -176,11 +176,15 @@ static cudaError_t upload(cudaStream_t s, DBuf<T>& d, const T* h, size_t count) 
     return cudaMemcpyAsync(d.p, h, count * sizeof(T), cudaMemcpyHostToDevice, s);
 }
 
+// C(n, r), saturating at UINT64_MAX (exact whenever the true value fits)
 static unsigned long long h_binom(int n, int r) {
     if (r < 0 || r > n) return 0ull;
-    unsigned long long res = 1;
-    for (int i = 1; i <= r; ++i) res = res * (unsigned long long)(n - r + i) / (unsigned long long)i;
-    return res;
+    unsigned __int128 res = 1;
+    for (int i = 1; i <= r; ++i) {
+        res = res * (unsigned __int128)(n - r + i) / (unsigned __int128)i;
+        if (res > (unsigned __int128)~0ull) return ~0ull;
+    }
+    return (unsigned long long)res;
 }
 
 extern "C" {
@@ -558,7 +562,15 @@ static unsigned long long h_fact(int k) {
 int gp_space_size(gp_ctx* c, uint64_t* out) {
     if (!c || !c->loaded || !out) return fail(GP_ERR_INPUT, "context not loaded");
     int k = c->F;
-    *out = (k > c->n) ? 0 : (uint64_t)c->nb * c->nm * h_fact(k) * h_binom(c->n - 1, k - 1);
+    if (k > c->n) { *out = 0; return GP_OK; }
+    unsigned __int128 v = (unsigned __int128)c->nb * c->nm * h_fact(k);
+    const unsigned long long nc = h_binom(c->n - 1, k - 1);
+    v *= nc;
+    if (nc == ~0ull || v > (unsigned __int128)~0ull) {
+        *out = ~0ull;
+        return fail(GP_ERR_INPUT, "candidate space of %d groups x %d layers exceeds 2^64", k, c->n);
+    }
+    *out = (uint64_t)v;
     return GP_OK;
 }
 
@@ -653,7 +665,7 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
     int k = c->F;
     uint64_t total;
-    gp_space_size(c, &total);
+    { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
     if (hi > total) hi = total;
     if (lo > hi) lo = hi;
     CUDA_TRY(cudaSetDevice(c->device));
@@ -834,7 +846,7 @@ int gp_argmin_bnb_async(gp_ctx* c) {
     if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
     const int k = c->F, n = c->n;
     uint64_t total;
-    gp_space_size(c, &total);
+    { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
     int fl = known_flags(c);
     if (fl < 0) {
         CUDA_TRY(cudaEventSynchronize(c->flags_ev));
@@ -875,7 +887,7 @@ int gp_argmin_items_async(gp_ctx* c, uint64_t item_lo, uint64_t item_hi) {
     if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
     const int k = c->F;
     uint64_t total;
-    gp_space_size(c, &total);
+    { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
     const unsigned long long NP = h_fact(k), NC = h_binom(c->n - 1, k - 1);
     const unsigned long long n_items = total ? (unsigned long long)c->nm * NP : 0;
     if (item_hi > n_items) item_hi = n_items;
@@ -1008,7 +1020,8 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
         CUDA_TRY(cudaStreamSynchronize(s));
         if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
         uint64_t total;
-        gp_space_size(c, &total);
+        st = gp_space_size(c, &total);
+        if (st != GP_OK) return st;
         // make every buffer the graph touches exist before capturing
         CUDA_TRY(c->dsolve.ensure(1));
         CUDA_TRY(c->item_ctr.ensure((size_t)c->nm * h_fact(c->F) + 1));
@@ -1234,7 +1247,7 @@ int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_
     cudaStream_t s = c->stream;
     const int k = c->F, n = c->n;
     uint64_t total;
-    gp_space_size(c, &total);
+    { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
     const unsigned long long NP = h_fact(k), NC = h_binom(n - 1, k - 1);
     const unsigned long long items = (unsigned long long)c->nm * NP;
     const size_t DD = (size_t)c->D * c->D;

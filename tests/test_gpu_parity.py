@@ -181,3 +181,17 @@ def test_search_plan_matches_reference(engine, name, seed):
         return
     res = P.search_plan(model, topo, groups, cfg, engine=engine)
     assert G.normalize_result(res) == exp["result"]
+
+
+def test_space_overflow_is_an_error(engine):
+    """16 groups x 255 layers: the space exceeds 2^64 -> InputFileError, not wraparound."""
+    from paper_2505_15536_b200 import instances as I
+    import paper_2505_15536_b200 as P
+    regions = [[[(1e14 * (1 + r), 80e9)]] for r in range(16)]
+    layers = I.transformer_layers(255, 1024, 4096, 512, 32000, d_kv=1024)
+    spec = I.InstanceSpec("huge", layers, (64,), (8,), regions, intra_bw=[1e9] * 16,
+                          intra_lat=[1e-4] * 16, cross_bw=1e8, cross_lat=0.01)
+    model, topo, groups = I.build(spec)
+    engine.load(PackedInstance(model, topo, groups, 1.25))
+    with pytest.raises(P.InputFileError):
+        engine.space_size()
