@@ -182,6 +182,28 @@ typedef struct gp_trace {
     double mult[GP_MAX_STAGES][GP_MAX_BREAKPOINTS];
 } gp_trace;
 
+/* SimConfig knobs beyond the iteration count (src/simulator.py:21-28,
+ * src/adapter.py:127-130): the DynamicBatchAdapter and asynchronous
+ * iterations (src/engine.py:297-314). */
+typedef struct gp_sim_options {
+    uint32_t adapter;             /* adapter_enabled                         */
+    uint32_t async_iterations;    /* SimConfig.async_iterations              */
+    double degrade_factor;        /* AdapterConfig.degrade_factor (1.2)      */
+    double recover_factor;        /* AdapterConfig.recover_factor (1.05)     */
+} gp_sim_options;
+
+/* Per-timing SimReport ingredients (src/simulator.py:84-113): the host
+ * derives throughput, steady_throughput and bubble_fractions from these
+ * exactly as simulate_timing does. */
+typedef struct gp_sim_report {
+    double makespan;
+    double busy[GP_MAX_STAGES];   /* sum(op.end - op.start) per stage        */
+    uint32_t adapter_actions;     /* len(adapter.actions)                    */
+    uint32_t n_ops;               /* ops over all stages                     */
+    uint32_t n_transfers;         /* len(result.transfers)                   */
+    uint32_t pad;
+} gp_sim_report;
+
 typedef struct gp_ctx gp_ctx;
 
 /* Version / capability probe (no device needed). */
@@ -281,6 +303,18 @@ int gp_sim_1f1b(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t iter
 int gp_simulate(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t policy,
                 uint32_t iterations, const gp_trace *traces, uint32_t n_traces,
                 const uint32_t *trace_index, double *makespan, uint8_t *status);
+/*
+ * Full simulate_timing(timings[i], policy, trace, opts->adapter,
+ * SimConfig(iterations, async_iterations, AdapterConfig(...))) reports:
+ * report[i] as above and, when iteration_ends is not NULL,
+ * iteration_ends[i*iterations + j] = result.iteration_ends[j].  Host
+ * pointers.  Per-timing queues live in device scratch sized by the largest
+ * batch (chunks shrink to one sample under the adapter).
+ */
+int gp_simulate_report(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t policy,
+                       uint32_t iterations, const gp_trace *traces, uint32_t n_traces,
+                       const uint32_t *trace_index, const gp_sim_options *opts,
+                       gp_sim_report *report, double *iteration_ends, uint8_t *status);
 /* Same with device pointers, asynchronous on the context's stream. */
 int gp_sim_1f1b_device(gp_ctx *ctx, const gp_timing *d_timings, uint64_t n,
                        uint32_t iterations, double *d_makespan, uint8_t *d_status);

@@ -770,7 +770,7 @@ typedef struct {
     int64_t fwd_avail, fwd_taken, fwd_done, bwd_avail, bwd_taken, bwd_done;
     int64_t wq_head, wq_tail, w_done;   /* w_queue as a FIFO of sizes */
     int64_t *wq;                        /* sizes */
-    int sync_done, opt_done, activated;
+    int sync_done, opt_done, activated, first_bwd;
 } sim_pool;
 
 typedef struct {
@@ -779,7 +779,111 @@ typedef struct {
     int kind;           /* 0 op, 1 transfer */
     int s, op, it;      /* op: stage, op kind (0 F,1 B,2 W,3 S,4 O), iteration */
     int64_t size;       /* also transfer size; for transfers s=boundary, op=dir */
+    double t0;          /* transfer start (adapter latency samples) */
 } sim_ev;
+
+/* ---- DynamicBatchAdapter (src/adapter.py:18-224) ---------------------- */
+#define AD_WINDOW 20
+typedef struct {
+    double samples[AD_WINDOW]; /* deque(maxlen=20): ring, oldest at head */
+    int head, len;
+    double baseline;
+    int64_t count, since;
+    int degraded, exists;
+} ad_window;
+
+typedef struct {
+    int64_t configured, current[GP_MAX_STAGES];
+    int phase[GP_MAX_STAGES];   /* 0 FILL, 1 RUN, 2 DRAIN */
+    ad_window win[2 * GP_MAX_STAGES];
+    double degrade, recover;
+    uint32_t actions;           /* len(adapter.actions): _apply with a change */
+} ad_state;
+
+static void ad_apply(ad_state *A, int s, int64_t size)
+{
+    if (size != A->current[s]) {
+        A->actions++;
+        A->current[s] = size;
+    }
+}
+
+static void ad_record(ad_window *w, double lat, int freeze)
+{
+    if (w->len < AD_WINDOW) {
+        w->samples[(w->head + w->len) % AD_WINDOW] = lat;
+        w->len++;
+    } else {
+        w->samples[w->head] = lat;
+        w->head = (w->head + 1) % AD_WINDOW;
+    }
+    w->count += 1;
+    w->since += 1;
+    if (!freeze) {
+        if (w->count == 1)
+            w->baseline = lat;
+        else
+            w->baseline += 0.05 * (lat - w->baseline);
+    }
+}
+
+/* detect_fluctuation: 0 STABLE, 1 DEGRADED, 2 RECOVERED */
+static int ad_detect(const ad_window *w, int reduced, double degrade, double recover)
+{
+    if (w->len != AD_WINDOW || w->baseline <= 0)
+        return 0;
+    double buf[AD_WINDOW];
+    for (int i = 0; i < w->len; ++i)
+        buf[i] = w->samples[(w->head + i) % AD_WINDOW];
+    double mean = or_psum(buf, (size_t)w->len) / (double)w->len;
+    if (mean > degrade * w->baseline)
+        return 1;
+    if (reduced && mean < recover * w->baseline)
+        return 2;
+    return 0;
+}
+
+static int64_t ad_adjust(int64_t current, int64_t configured, int signal, int phase)
+{
+    if (phase == 2)
+        return current / 2 > 1 ? current / 2 : 1;
+    if (signal == 1)
+        return current / 2 > 1 ? current / 2 : 1;
+    if (signal == 2)
+        return current * 2 < configured ? current * 2 : configured;
+    return current;
+}
+
+static void ad_iteration_start(ad_state *A, int S, int s)
+{
+    A->phase[s] = 0;
+    int poor = 0;
+    for (int b = s - 1; b <= s; ++b)
+        for (int d = 0; d < 2; ++d)
+            if (b >= 0 && b < S - 1 && A->win[2 * b + d].exists && A->win[2 * b + d].degraded)
+                poor = 1;
+    ad_apply(A, s, poor ? (A->configured / 2 > 1 ? A->configured / 2 : 1) : A->configured);
+}
+
+static void ad_transfer_complete(ad_state *A, int boundary, int dir, double raw, int64_t size)
+{
+    int producer = dir == 0 ? boundary : boundary + 1;
+    ad_window *w = &A->win[2 * boundary + dir];
+    w->exists = 1;
+    int reduced = A->current[producer] < A->configured;
+    ad_record(w, raw / (double)size, reduced);
+    if (w->since < AD_WINDOW)
+        return;
+    int sig = ad_detect(w, reduced, A->degrade, A->recover);
+    if (sig == 0)
+        return;
+    w->degraded = sig == 1;
+    int64_t ns = ad_adjust(A->current[producer], A->configured, sig, A->phase[producer]);
+    if (ns != A->current[producer]) {
+        w->since = 0;
+        ad_apply(A, producer, ns);
+    }
+}
 
 typedef struct {
     sim_ev *h;
@@ -874,22 +978,53 @@ static double transfer_end(double start, double bytes, double base_bw, double la
     return (t + remaining / bw) + latency;
 }
 
+int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
+                const gp_sim_options *opts, gp_sim_report *rep, double *iter_ends,
+                double *makespan_out);
+
 int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
-           double *makespan_out);
+           double *makespan_out)
+{
+    return or_sim_full(T, policy, iterations, trace, NULL, NULL, NULL, makespan_out);
+}
 
 int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
 {
     return or_sim(T, GP_POLICY_1F1B, iterations, NULL, makespan_out);
 }
 
-int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
-           double *makespan_out)
+/* PipelineEngine.run (src/engine.py:230-431) with every option: policy,
+ * trace, DynamicBatchAdapter hooks (src/adapter.py:167-224) and
+ * asynchronous iterations (:297-314); rep / iter_ends may be NULL. */
+int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
+                const gp_sim_options *opts, gp_sim_report *rep, double *iter_ends,
+                double *makespan_out)
 {
     const int S = (int)T->n_stages;
     if (S < 1 || S > GP_MAX_STAGES || iterations < 1)
         return GP_ERR_TIMING;
+    const int adapter = opts ? (int)opts->adapter : 0;
+    const int async_it = opts ? (int)opts->async_iterations : 0;
     const int64_t B = T->batch, m = T->microbatch;
-    const int64_t per_it = B / (m > 0 ? m : 1) + 2;
+    const int64_t per_it = B + 2;  /* chunks can shrink to 1 sample with the adapter */
+    ad_state A;
+    memset(&A, 0, sizeof(A));
+    A.configured = m;
+    A.degrade = opts ? opts->degrade_factor : 1.2;
+    A.recover = opts ? opts->recover_factor : 1.05;
+    double busy_f[GP_MAX_STAGES], busy_c[GP_MAX_STAGES];
+    int64_t busy_n[GP_MAX_STAGES];
+    uint32_t n_ops = 0, n_xfer = 0;
+    for (int s = 0; s < S; ++s) {
+        busy_f[s] = busy_c[s] = 0.0;
+        busy_n[s] = 0;
+    }
+    if (iter_ends)
+        for (int i = 0; i < iterations; ++i)
+            iter_ends[i] = 0.0;
+    for (int s = 0; s < S; ++s)
+        A.current[s] = m;
+    int64_t *it_fwd_done = (int64_t *)calloc((size_t)iterations, sizeof(int64_t));
     sim_pool *pools = (sim_pool *)calloc((size_t)S * iterations, sizeof(sim_pool));
     for (int i = 0; i < S * iterations; ++i)
         pools[i].wq = (int64_t *)calloc((size_t)per_it + 1, sizeof(int64_t));
@@ -907,12 +1042,22 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
     (void)closed_cnt;
     sim_heap H = {NULL, 0, 0};
     uint64_t seq = 0;
+    /* activate (src/engine.py:259-267) */
+#define ACTIVATE(s_, it_)                                                                  \
+    do {                                                                                   \
+        sim_pool *q_ = POOL((s_), (it_));                                                  \
+        if (!q_->activated) {                                                              \
+            q_->activated = 1;                                                             \
+            if ((s_) == 0)                                                                 \
+                q_->fwd_avail = B;                                                         \
+            if (adapter)                                                                   \
+                ad_iteration_start(&A, S, (s_));                                           \
+        }                                                                                  \
+    } while (0)
     for (int s = 0; s < S; ++s) {
         cur[s] = 0;
         busy[s] = 0;
-        POOL(s, 0)->activated = 1;
-        if (s == 0)
-            POOL(s, 0)->fwd_avail = B;
+        ACTIVATE(s, 0);
     }
 
     /* try_start_link (src/engine.py:276-289) */
@@ -927,7 +1072,7 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
             double per_ = (dir) == 0 ? T->act[bnd] : T->grad[bnd];                         \
             double end_ = transfer_end((tnow), per_ * (double)sz_, T->bw[bnd], T->lat[bnd], \
                                        trace, (bnd));                                      \
-            sim_ev e_ = {end_, seq++, 1, (bnd), (dir), it_, sz_};                          \
+            sim_ev e_ = {end_, seq++, 1, (bnd), (dir), it_, sz_, (tnow)};                  \
             heap_push(&H, e_);                                                             \
         }                                                                                  \
     } while (0)
@@ -950,7 +1095,7 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
                  * in this order; the lowest priority wins, the earliest on ties */
                 int best_pr = 100, best_k = -1;
                 int64_t best_sz = 0;
-                int64_t size = m;
+                int64_t size = adapter ? A.current[s] : m;
                 int64_t fwd_rem = B - p->fwd_taken;
                 if (fwd_rem > 0) {
                     int64_t chunk = size < fwd_rem ? size : fwd_rem;
@@ -1004,6 +1149,24 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
                     best_k = 4;
                     best_sz = 0;
                 }
+                if (best_k < 0 && async_it && p->fwd_taken == B && it + 1 < iterations) {
+                    /* asynchronous iterations: the next iteration's forwards may
+                     * start before this one's optimizer step (src/engine.py:297-314) */
+                    ACTIVATE(s, it + 1);  /* may resize the stage (on_iteration_start) */
+                    size = adapter ? A.current[s] : m;
+                    sim_pool *nx = POOL(s, it + 1);
+                    int64_t remaining = B - nx->fwd_taken;
+                    int64_t chunk = size < remaining ? size : remaining;
+                    if (remaining > 0 && nx->fwd_avail - nx->fwd_taken >= chunk) {
+                        nx->fwd_taken += chunk;
+                        busy[s] = 1;
+                        sim_ev e = {now + T->fwd[s] * (double)chunk, seq++, 0, s, 0, it + 1, chunk, now};
+                        heap_push(&H, e);
+                        n_ops++;
+                        progress = 1;
+                    }
+                    continue;
+                }
                 if (best_k < 0)
                     continue;
                 double dur;
@@ -1015,8 +1178,9 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
                 default: dur = T->opt[s]; break;
                 }
                 busy[s] = 1;
-                sim_ev e = {now + dur, seq++, 0, s, best_k, it, best_sz};
+                sim_ev e = {now + dur, seq++, 0, s, best_k, it, best_sz, now};
                 heap_push(&H, e);
+                n_ops++;
                 progress = 1;
             }
         }
@@ -1030,6 +1194,19 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
             int s = e.s, it = e.it;
             sim_pool *p = POOL(s, it);
             busy[s] = 0;
+            {   /* busy[s] = sum(op.end - op.start) in op order (CPython 3.12 sum) */
+                double x = now - e.t0;
+                if (busy_n[s]++ == 0) {
+                    busy_f[s] = 0.0 + x;
+                } else {
+                    double t = busy_f[s] + x;
+                    if (fabs(busy_f[s]) >= fabs(x))
+                        busy_c[s] += (busy_f[s] - t) + x;
+                    else
+                        busy_c[s] += (x - t) + busy_f[s];
+                    busy_f[s] = t;
+                }
+            }
             if (e.op == 0) {
                 p->fwd_done += e.size;
                 if (s < S - 1) {
@@ -1039,9 +1216,20 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
                     L->tail++;
                     TRY_START(now, s, 0);
                 }
+                it_fwd_done[it] += e.size;
+                if (adapter && it_fwd_done[it] == (int64_t)S * B)
+                    for (int q = 0; q < S; ++q) {  /* on_drain: halve every stage once */
+                        A.phase[q] = 2;
+                        ad_apply(&A, q, ad_adjust(A.current[q], A.configured, 0, 2));
+                    }
             } else if (e.op == 1) {
                 p->bwd_done += e.size;
                 p->wq[p->wq_tail++] = e.size;
+                if (!p->first_bwd) {
+                    p->first_bwd = 1;
+                    if (adapter)
+                        A.phase[s] = 1;  /* on_run_phase */
+                }
                 if (s > 0) {
                     sim_link *L = &links[2 * (s - 1) + 1];
                     L->q_size[L->tail] = e.size;
@@ -1056,15 +1244,11 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
             } else {
                 p->opt_done = 1;
                 stages_closed[it] += 1;
+                if (stages_closed[it] == S && iter_ends)
+                    iter_ends[it] = now;
                 cur[s] = it + 1;
-                if (it + 1 < iterations) {
-                    sim_pool *q = POOL(s, it + 1);
-                    if (!q->activated) {
-                        q->activated = 1;
-                        if (s == 0)
-                            q->fwd_avail = B;
-                    }
-                }
+                if (it + 1 < iterations)
+                    ACTIVATE(s, it + 1);
             }
         } else {
             /* finish_transfer (src/engine.py:380-396) */
@@ -1074,6 +1258,9 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
                 POOL(bnd + 1, e.it)->fwd_avail += e.size;
             else
                 POOL(bnd, e.it)->bwd_avail += e.size;
+            n_xfer++;
+            if (adapter)
+                ad_transfer_complete(&A, bnd, dir, now - e.t0, e.size);
             TRY_START(now, bnd, dir);
         }
     }
@@ -1082,10 +1269,20 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
         if (cur[s] < iterations)
             status = GP_ERR_SCHEDULING;
     *makespan_out = now;
+    if (rep) {
+        memset(rep, 0, sizeof(*rep));
+        rep->makespan = now;
+        for (int s = 0; s < S; ++s)
+            rep->busy[s] = (busy_c[s] != 0.0 && isfinite(busy_c[s])) ? busy_f[s] + busy_c[s] : busy_f[s];
+        rep->adapter_actions = A.actions;
+        rep->n_ops = n_ops;
+        rep->n_transfers = n_xfer;
+    }
     for (int i = 0; i < S * iterations; ++i)
         free(pools[i].wq);
     free(pools);
     free(stages_closed);
+    free(it_fwd_done);
     for (int l = 0; l < 2 * (S - 1); ++l) {
         free(links[l].q_size);
         free(links[l].q_it);
@@ -1093,6 +1290,7 @@ int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace
     free(H.h);
 #undef POOL
 #undef TRY_START
+#undef ACTIVATE
     return status;
 }
 
@@ -1117,6 +1315,24 @@ int or_sim_policy_batch(const gp_timing *T, uint64_t n, int policy, int iteratio
         const gp_trace *tr = traces ? &traces[trace_index ? trace_index[i] : 0] : NULL;
         int st = or_sim(&T[i], policy, iterations, tr, &ms);
         makespan[i] = ms;
+        status[i] = (uint8_t)st;
+    }
+    return GP_OK;
+}
+
+/* simulate_timing reports (src/simulator.py:71-113) for a batch of timings. */
+int or_sim_report_batch(const gp_timing *T, uint64_t n, int policy, int iterations,
+                        const gp_trace *traces, const uint32_t *trace_index,
+                        const gp_sim_options *opts, gp_sim_report *reports, double *iter_ends,
+                        uint8_t *status)
+{
+    for (uint64_t i = 0; i < n; ++i) {
+        double ms = NAN;
+        const gp_trace *tr = traces ? &traces[trace_index ? trace_index[i] : 0] : NULL;
+        int st = or_sim_full(&T[i], policy, iterations, tr, opts, &reports[i],
+                             iter_ends ? iter_ends + i * (uint64_t)iterations : NULL, &ms);
+        if (st != GP_OK)
+            reports[i].makespan = NAN;
         status[i] = (uint8_t)st;
     }
     return GP_OK;

@@ -60,6 +60,9 @@ def lib():
         L.or_sim_policy_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, C.c_int,
                                           P(abi.GpTrace), P(C.c_uint32), P(C.c_double),
                                           P(C.c_uint8)]
+        L.or_sim_report_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, C.c_int,
+                                          P(abi.GpTrace), P(C.c_uint32), P(abi.GpSimOptions),
+                                          P(abi.GpSimReport), P(C.c_double), P(C.c_uint8)]
         _lib = L
     return _lib
 
@@ -167,3 +170,21 @@ def sim_policy_batch(packed_timings, n, policy, iterations=1, traces=None, trace
                               ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
                               _dp(ms), _u8(st))
     return ms, st
+
+
+def sim_reports(packed_timings, n, policy, iterations=1, traces=None, trace_index=None,
+                adapter=False, async_iterations=False, degrade=1.2, recover=1.05):
+    """(GpSimReport array, iteration_ends[n, iterations], status) of
+    simulate_timing with every SimConfig option."""
+    opts = abi.GpSimOptions(int(bool(adapter)), int(bool(async_iterations)),
+                            float(degrade), float(recover))
+    reps = (abi.GpSimReport * max(1, n))()
+    ends = np.zeros((n, iterations), dtype=np.float64)
+    st = np.empty(n, dtype=np.uint8)
+    ti = None
+    if trace_index is not None:
+        ti = np.ascontiguousarray(trace_index, dtype=np.uint32)
+    lib().or_sim_report_batch(packed_timings, n, int(policy), int(iterations), traces,
+                              ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
+                              C.byref(opts), reps, _dp(ends), _u8(st))
+    return reps, ends, st

@@ -137,3 +137,18 @@ class GpTrace(C.Structure):
         ("t", (C.c_double * GP_MAX_BREAKPOINTS) * GP_MAX_STAGES),
         ("mult", (C.c_double * GP_MAX_BREAKPOINTS) * GP_MAX_STAGES),
     ]
+
+
+class GpSimOptions(C.Structure):
+    _fields_ = [
+        ("adapter", C.c_uint32), ("async_iterations", C.c_uint32),
+        ("degrade_factor", C.c_double), ("recover_factor", C.c_double),
+    ]
+
+
+class GpSimReport(C.Structure):
+    _fields_ = [
+        ("makespan", C.c_double), ("busy", C.c_double * GP_MAX_STAGES),
+        ("adapter_actions", C.c_uint32), ("n_ops", C.c_uint32),
+        ("n_transfers", C.c_uint32), ("pad", C.c_uint32),
+    ]

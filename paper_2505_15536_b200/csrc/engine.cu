@@ -110,6 +110,10 @@ struct gp_ctx {
     DBuf<unsigned int> z_cnt;
     DBuf<double> s_ms;
     DBuf<uint8_t> s_st;
+    DBuf<gp_sim_report> s_rep;  // K5 full reports
+    DBuf<double> s_ends;
+    DBuf<uint32_t> s_wq;         // K5 full queue scratch
+    DBuf<unsigned long long> s_lq;
     SolveOut* h_solve = nullptr;  // pinned
     RangeGeom last_geom{};
     bool last_generic = false;
@@ -246,6 +250,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     c->z_bw.release(); c->z_mbw.release(); c->z_xt.release(); c->z_flags.release();
     c->z_tpk.release(); c->z_tcol.release(); c->z_res.release(); c->z_cnt.release();
     c->dsolve.release(); c->gbest.release(); c->s_tim.release(); c->s_traces.release(); c->s_tidx.release(); c->s_ms.release(); c->s_st.release();
+    c->s_rep.release(); c->s_ends.release(); c->s_wq.release(); c->s_lq.release();
     if (c->flags_ev) cudaEventDestroy(c->flags_ev);
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
@@ -1176,13 +1181,9 @@ int gp_sim_1f1b_device(gp_ctx* c, const gp_timing* d_timings, uint64_t n, uint32
     return GP_OK;
 }
 
-int gp_simulate(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy,
-                uint32_t iterations, const gp_trace* traces, uint32_t n_traces,
-                const uint32_t* trace_index, double* makespan, uint8_t* status) {
-    if (!c) return fail(GP_ERR_INPUT, "null context");
-    if (policy > GP_POLICY_ZB_COMPACT) return fail(GP_ERR_INPUT, "unknown policy %u", policy);
-    if (n == 0) return GP_OK;
-    if (traces && n_traces == 0) traces = nullptr;
+// Validation shared by the trace-taking simulators.
+static int check_traces(const gp_trace* traces, uint32_t n_traces, const uint32_t* trace_index,
+                        uint64_t n) {
     if (traces && trace_index)
         for (uint64_t i = 0; i < n; ++i)
             if (trace_index[i] >= n_traces) return fail(GP_ERR_INPUT, "trace index out of range");
@@ -1191,6 +1192,17 @@ int gp_simulate(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy
             for (int b = 0; b < GP_MAX_STAGES; ++b)
                 if (traces[t].n_points[b] > GP_MAX_BREAKPOINTS)
                     return fail(GP_ERR_INPUT, "trace %u link %d: too many breakpoints", t, b);
+    return GP_OK;
+}
+
+int gp_simulate(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy,
+                uint32_t iterations, const gp_trace* traces, uint32_t n_traces,
+                const uint32_t* trace_index, double* makespan, uint8_t* status) {
+    if (!c) return fail(GP_ERR_INPUT, "null context");
+    if (policy > GP_POLICY_ZB_COMPACT) return fail(GP_ERR_INPUT, "unknown policy %u", policy);
+    if (n == 0) return GP_OK;
+    if (traces && n_traces == 0) traces = nullptr;
+    { int st_ = check_traces(traces, n_traces, trace_index, n); if (st_ != GP_OK) return st_; }
     CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t s = c->stream;
     CUDA_TRY(c->s_tim.ensure(n));
@@ -1216,6 +1228,88 @@ int gp_simulate(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy
                                                            c->s_st.p);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(makespan, c->s_ms.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return GP_OK;
+}
+
+int gp_simulate_report(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy,
+                       uint32_t iterations, const gp_trace* traces, uint32_t n_traces,
+                       const uint32_t* trace_index, const gp_sim_options* opts,
+                       gp_sim_report* report, double* iteration_ends, uint8_t* status) {
+    if (!c || !timings || !report || !status) return fail(GP_ERR_INPUT, "bad arguments");
+    if (policy > GP_POLICY_ZB_COMPACT) return fail(GP_ERR_INPUT, "unknown policy %u", policy);
+    if (iterations < 1 || iterations > 0xffff) return fail(GP_ERR_INPUT, "iterations out of range");
+    if (n == 0) return GP_OK;
+    if (traces && n_traces == 0) traces = nullptr;
+    { int st_ = check_traces(traces, n_traces, trace_index, n); if (st_ != GP_OK) return st_; }
+    gp_sim_options opt{0u, 0u, 1.2, 1.05};
+    if (opts) opt = *opts;
+    // queue capacities from the largest timing of the batch
+    long long bmax = 1;
+    int smax = 1;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (timings[i].batch > bmax) bmax = timings[i].batch;
+        if ((int)timings[i].n_stages > smax && timings[i].n_stages <= GP_MAX_STAGES)
+            smax = (int)timings[i].n_stages;
+    }
+    if (bmax > 0x7fffffffll / 2 - 2) return fail(GP_ERR_INPUT, "batch too large");
+    const int wcap = (int)bmax + 1, lcap = (int)(2 * bmax + 2);
+    const size_t nlinks = (size_t)2 * (smax > 1 ? smax - 1 : 1);
+    const size_t per = (size_t)smax * SIMF_SLOTS * wcap * sizeof(uint32_t) + 8 +
+                       nlinks * lcap * sizeof(unsigned long long) +
+                       (size_t)smax * SIMF_SLOTS * sizeof(SimFPool) + nlinks * sizeof(AdWindow);
+    uint64_t chunk = (uint64_t)((1ull << 30) / per);  // <= 1 GiB of queue scratch per launch
+    if (chunk < 1) chunk = 1;
+    if (chunk > n) chunk = n;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->s_tim.ensure(n));
+    CUDA_TRY(c->s_st.ensure(n));
+    CUDA_TRY(c->s_rep.ensure(n));
+    if (iteration_ends) CUDA_TRY(c->s_ends.ensure(n * (uint64_t)iterations));
+    CUDA_TRY(c->s_wq.ensure(chunk * (per / sizeof(uint32_t) + 1)));  // queues, pools, windows
+    CUDA_TRY(cudaMemcpyAsync(c->s_tim.p, timings, n * sizeof(gp_timing), cudaMemcpyHostToDevice, s));
+    if (iteration_ends)
+        CUDA_TRY(cudaMemsetAsync(c->s_ends.p, 0, n * (uint64_t)iterations * sizeof(double), s));
+    gp_trace* d_tr = nullptr;
+    uint32_t* d_ti = nullptr;
+    if (traces) {
+        CUDA_TRY(c->s_traces.ensure(n_traces));
+        CUDA_TRY(cudaMemcpyAsync(c->s_traces.p, traces, n_traces * sizeof(gp_trace),
+                                 cudaMemcpyHostToDevice, s));
+        d_tr = c->s_traces.p;
+        if (trace_index) {
+            CUDA_TRY(c->s_tidx.ensure(n));
+            CUDA_TRY(cudaMemcpyAsync(c->s_tidx.p, trace_index, n * sizeof(uint32_t),
+                                     cudaMemcpyHostToDevice, s));
+            d_ti = c->s_tidx.p;
+        }
+    }
+    for (uint64_t i0 = 0; i0 < n; i0 += chunk) {
+        const uint64_t nc = (n - i0) < chunk ? (n - i0) : chunk;
+        SimScratch sc;
+        sc.n = (long long)nc;
+        sc.wcap = wcap;
+        sc.lcap = lcap;
+        sc.wq = c->s_wq.p;
+        // link FIFOs after the W queues, 8-byte aligned (wcap words per queue)
+        size_t wwords = (size_t)smax * SIMF_SLOTS * wcap * nc;
+        wwords = (wwords + 1) & ~(size_t)1;
+        sc.lq = reinterpret_cast<unsigned long long*>(c->s_wq.p + wwords);
+        sc.pools = reinterpret_cast<SimFPool*>(sc.lq + nlinks * lcap * nc);
+        sc.win = reinterpret_cast<AdWindow*>(sc.pools + (size_t)smax * SIMF_SLOTS * nc);
+        sc.smax = smax;
+        k5_sim_full<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
+            c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, d_tr,
+            d_ti ? d_ti + i0 : nullptr, opt, sc, c->s_rep.p + i0,
+            iteration_ends ? c->s_ends.p + i0 * iterations : nullptr, c->s_st.p + i0);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaMemcpyAsync(report, c->s_rep.p, n * sizeof(gp_sim_report), cudaMemcpyDeviceToHost, s));
+    if (iteration_ends)
+        CUDA_TRY(cudaMemcpyAsync(iteration_ends, c->s_ends.p, n * (uint64_t)iterations * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return GP_OK;

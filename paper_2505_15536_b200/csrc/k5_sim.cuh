@@ -70,6 +70,53 @@ __device__ double transfer_end(double start, double bytes, double base_bw, doubl
     return (t + remaining / bw) + latency;
 }
 
+// _ready_op (src/engine.py:157-215): candidates F, B, W, SYNC, OPT in this
+// order; the lowest priority wins, the earliest on ties.  `size` is the
+// stage's current micro-batch (the adapter's, or m), `m` the configured one
+// that sets the warm-up quota.  Returns the op kind (-1: none) and its size.
+__device__ __forceinline__ int ready_op(int policy, int S, int s, long long B, long long m,
+                                        long long size, long long fwd_avail, long long fwd_taken,
+                                        long long fwd_done, long long bwd_avail, long long bwd_taken,
+                                        long long bwd_done, long long w_done, bool wq_any,
+                                        long long wq_head_size, bool sync_done, bool opt_done,
+                                        long long* out_size) {
+    const bool zbc = policy == GP_POLICY_ZB_COMPACT, zbo = policy == GP_POLICY_ZB_ORIGINAL;
+    const bool gpipe = policy == GP_POLICY_GPIPE;
+    int best_pr = 100, best_k = -1;
+    long long best_sz = 0;
+    const long long fwd_rem = B - fwd_taken;
+    if (fwd_rem > 0) {
+        const long long chunk = size < fwd_rem ? size : fwd_rem;
+        if (fwd_avail - fwd_taken >= chunk) {
+            int pr = -1;
+            if (zbc || gpipe) {
+                pr = zbc ? 0 : 1;
+            } else {
+                const long long quota = (long long)(S - s) * m;
+                if (fwd_taken < quota) pr = zbo ? 0 : 1;
+                else if (fwd_taken + chunk <= quota + bwd_done) pr = zbo ? 3 : 2;
+            }
+            if (pr >= 0) { best_pr = pr; best_k = 0; best_sz = chunk; }
+        }
+    }
+    const long long bwd_rem = B - bwd_taken;
+    if (bwd_rem > 0 && (!gpipe || fwd_done == B)) {
+        const long long chunk = size < bwd_rem ? size : bwd_rem;
+        long long av = (bwd_avail < fwd_done ? bwd_avail : fwd_done) - bwd_taken;
+        if (s == S - 1) av = fwd_done - bwd_taken;
+        const int pr = (zbc || zbo) ? 1 : 2;
+        if (av >= chunk && pr < best_pr) { best_pr = pr; best_k = 1; best_sz = chunk; }
+    }
+    if (wq_any) {
+        const int pr = (gpipe || policy == GP_POLICY_1F1B) ? 0 : 2;
+        if (pr < best_pr) { best_pr = pr; best_k = 2; best_sz = wq_head_size; }
+    }
+    if (w_done == B && !wq_any && !sync_done && 8 < best_pr) { best_pr = 8; best_k = 3; best_sz = 0; }
+    if (sync_done && !opt_done && 9 < best_pr) { best_pr = 9; best_k = 4; best_sz = 0; }
+    *out_size = best_sz;
+    return best_k;
+}
+
 __device__ int sim_dev(const gp_timing& T, int policy, int iterations, const gp_trace* trace,
                        double* makespan) {
     const int S = (int)T.n_stages;
@@ -122,43 +169,12 @@ __device__ int sim_dev(const gp_timing& T, int policy, int iterations, const gp_
                 const int it = cur[s];
                 if (it >= iterations) continue;
                 SimPool& p = sim_pool(P, s, it);
-                // _ready_op (src/engine.py:157-215): candidates F, B, W, SYNC,
-                // OPT in this order; lowest priority wins, earliest on ties
-                const bool zbc = policy == GP_POLICY_ZB_COMPACT, zbo = policy == GP_POLICY_ZB_ORIGINAL;
-                const bool gpipe = policy == GP_POLICY_GPIPE;
-                int best_pr = 100, best_k = -1;
-                long long best_sz = 0;
-                const long long fwd_rem = B - p.fwd_taken;
-                if (fwd_rem > 0) {
-                    const long long chunk = m < fwd_rem ? m : fwd_rem;
-                    if (p.fwd_avail - p.fwd_taken >= chunk) {
-                        int pr = -1;
-                        if (zbc || gpipe) {
-                            pr = zbc ? 0 : 1;
-                        } else {
-                            const long long quota = (long long)(S - s) * m;
-                            if (p.fwd_taken < quota) pr = zbo ? 0 : 1;
-                            else if (p.fwd_taken + chunk <= quota + p.bwd_done) pr = zbo ? 3 : 2;
-                        }
-                        if (pr >= 0) { best_pr = pr; best_k = 0; best_sz = chunk; }
-                    }
-                }
-                const long long bwd_rem = B - p.bwd_taken;
-                if (bwd_rem > 0 && (!gpipe || p.fwd_done == B)) {
-                    const long long chunk = m < bwd_rem ? m : bwd_rem;
-                    long long av = (p.bwd_avail < p.fwd_done ? p.bwd_avail : p.fwd_done) - p.bwd_taken;
-                    if (s == S - 1) av = p.fwd_done - p.bwd_taken;
-                    const int pr = (zbc || zbo) ? 1 : 2;
-                    if (av >= chunk && pr < best_pr) { best_pr = pr; best_k = 1; best_sz = chunk; }
-                }
-                if (p.wq_head < p.wq_tail) {
-                    const int pr = (gpipe || policy == GP_POLICY_1F1B) ? 0 : 2;
-                    if (pr < best_pr) { best_pr = pr; best_k = 2; best_sz = chunk_size(p.wq_head); }
-                }
-                if (p.w_done == B && p.wq_head == p.wq_tail && !(p.flags & 1) && 8 < best_pr) {
-                    best_pr = 8; best_k = 3; best_sz = 0;
-                }
-                if ((p.flags & 1) && !(p.flags & 2) && 9 < best_pr) { best_pr = 9; best_k = 4; best_sz = 0; }
+                long long best_sz;
+                const int best_k = ready_op(policy, S, s, B, m, m, p.fwd_avail, p.fwd_taken,
+                                            p.fwd_done, p.bwd_avail, p.bwd_taken, p.bwd_done,
+                                            p.w_done, p.wq_head < p.wq_tail,
+                                            p.wq_head < p.wq_tail ? chunk_size(p.wq_head) : 0,
+                                            (p.flags & 1) != 0, (p.flags & 2) != 0, &best_sz);
                 if (best_k < 0) continue;
                 double dur;
                 switch (best_k) {
@@ -287,3 +303,329 @@ __global__ void k5_sim_1f1b(const gp_timing* __restrict__ T, long long n, int po
     status[i] = (uint8_t)st;
 }
 
+
+// ----------------------------------------------------------------------------
+// K5 full: PipelineEngine.run with every SimConfig option
+// (src/engine.py:230-431): any policy and trace, the DynamicBatchAdapter
+// hooks (src/adapter.py:133-224) and asynchronous iterations (:297-314),
+// producing the SimReport ingredients (src/simulator.py:84-113).
+//
+// Under the adapter chunk sizes are data-dependent, so the W queues and the
+// link FIFOs hold explicit sizes in per-timing scratch (global memory,
+// interleaved by timing so neighbouring threads' same-index entries share
+// sectors).  Pools: four tagged iteration slots per stage (asynchronous
+// iterations keep at most three iterations of a stage live: a stage's
+// iteration it+2 forwards need its optimizer step of it, which needs every
+// stage's backward of it).  A slot or queue overflow is reported, never
+// silently overwritten.
+// ----------------------------------------------------------------------------
+#define SIMF_SLOTS 4
+#define AD_WINDOW 20
+
+struct SimFPool {
+    long long fwd_avail, fwd_taken, fwd_done, bwd_avail, bwd_taken, bwd_done, w_done;
+    int it_tag, wq_head, wq_tail;
+    int flags;          // bit0 sync_done, bit1 opt_done, bit2 activated, bit3 first_bwd_done
+};
+
+struct SimFEv {
+    double t, t0;       // t0: start (op duration / transfer latency samples)
+    unsigned long long seq;
+    int code;           // kind<<31 | s<<20 | op<<16 | slot<<14 ... iteration kept separately
+    int it;
+    long long size;
+};
+
+// MonitorWindow (src/adapter.py:37-58): ring of the last 20 per-sample
+// latencies (oldest at head), EMA baseline frozen while reduced.
+struct AdWindow {
+    double samples[AD_WINDOW];
+    double baseline;
+    long long count, since;
+    int head, len, degraded, exists;
+};
+
+struct SimScratch {
+    uint32_t* wq;               // [S*SLOTS*wcap][n]   W queue sizes
+    unsigned long long* lq;     // [2*(S-1)*lcap][n]   link FIFOs: it<<32 | size
+    SimFPool* pools;            // [n][smax*SLOTS]     iteration pools
+    AdWindow* win;              // [n][2*(smax-1)]     adapter monitor windows
+    long long n;                // timings in this launch (interleave stride)
+    int wcap, lcap, smax;
+};
+
+__device__ __forceinline__ long long ad_halve(long long v) { return v / 2 > 1 ? v / 2 : 1; }
+
+__device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp_trace* trace,
+                        const gp_sim_options& opt, SimScratch sc, long long tid,
+                        gp_sim_report* rep, double* iter_ends) {
+    const int S = (int)T.n_stages;
+    if (S < 1 || S > GP_MAX_STAGES || iterations < 1 || T.microbatch <= 0) return GP_ERR_TIMING;
+    const long long B = T.batch, m = T.microbatch;
+    if (B + 1 > sc.wcap || 2 * B + 2 > sc.lcap) return GP_ERR_INPUT;
+    const bool adapter = opt.adapter != 0, async_it = opt.async_iterations != 0;
+    if (S > sc.smax) return GP_ERR_INPUT;
+    SimFPool* P = sc.pools + tid * (long long)(sc.smax * SIMF_SLOTS);
+    for (int i = 0; i < SIMF_SLOTS * S; ++i) P[i].it_tag = -1;
+    bool overflow = false;
+    auto pool = [&](int s, int it) -> SimFPool& {
+        SimFPool& p = P[s * SIMF_SLOTS + (it & (SIMF_SLOTS - 1))];
+        if (p.it_tag != it) {
+            if (p.it_tag >= 0 && !(p.flags & 2)) overflow = true;  // live iteration evicted
+            p.fwd_avail = p.fwd_taken = p.fwd_done = p.bwd_avail = p.bwd_taken = p.bwd_done = 0;
+            p.w_done = 0;
+            p.wq_head = p.wq_tail = 0;
+            p.flags = 0;
+            p.it_tag = it;
+        }
+        return p;
+    };
+    auto wq_at = [&](int s, int it, int j) -> uint32_t& {
+        const long long q = (long long)(s * SIMF_SLOTS + (it & (SIMF_SLOTS - 1))) * sc.wcap + j;
+        return sc.wq[q * sc.n + tid];
+    };
+    auto lq_at = [&](int l, long long j) -> unsigned long long& {
+        const long long q = (long long)l * sc.lcap + (j % sc.lcap);
+        return sc.lq[q * sc.n + tid];
+    };
+    // per-iteration counters (iteration_fwd_done, stages_closed), tagged ring
+    long long it_fwd[SIMF_SLOTS];
+    int it_closed[SIMF_SLOTS], it_tag[SIMF_SLOTS];
+    for (int i = 0; i < SIMF_SLOTS; ++i) { it_fwd[i] = 0; it_closed[i] = 0; it_tag[i] = -1; }
+    auto it_slot = [&](int it) -> int {
+        const int k = it & (SIMF_SLOTS - 1);
+        if (it_tag[k] != it) {
+            if (it_tag[k] >= 0 && it_closed[k] != S) overflow = true;
+            it_tag[k] = it; it_fwd[k] = 0; it_closed[k] = 0;
+        }
+        return k;
+    };
+    // adapter state (src/adapter.py:91-150)
+    long long cur_sz[GP_MAX_STAGES];
+    int phase[GP_MAX_STAGES];  // 0 FILL, 1 RUN, 2 DRAIN
+    AdWindow* W = sc.win + tid * (long long)(2 * (sc.smax > 1 ? sc.smax - 1 : 1));
+    unsigned actions = 0;
+    for (int s = 0; s < S; ++s) { cur_sz[s] = m; phase[s] = 0; }
+    for (int l = 0; l < 2 * (S - 1); ++l) {
+        W[l].head = W[l].len = 0; W[l].baseline = 0.0; W[l].count = W[l].since = 0;
+        W[l].degraded = W[l].exists = 0;
+    }
+    auto ad_apply = [&](int s, long long size) {
+        if (size != cur_sz[s]) { ++actions; cur_sz[s] = size; }
+    };
+    auto activate = [&](int s, int it) {  // src/engine.py:259-267
+        SimFPool& q = pool(s, it);
+        if (q.flags & 4) return;
+        q.flags |= 4;
+        if (s == 0) q.fwd_avail = B;
+        if (adapter) {  // on_iteration_start (src/adapter.py:200-211)
+            phase[s] = 0;
+            bool poor = false;
+            for (int b = s - 1; b <= s; ++b)
+                for (int d = 0; d < 2; ++d)
+                    if (b >= 0 && b < S - 1 && W[2 * b + d].exists && W[2 * b + d].degraded) poor = true;
+            ad_apply(s, poor ? ad_halve(m) : m);
+        }
+    };
+    auto on_transfer = [&](int bnd, int dir, double raw, long long size) {
+        // on_transfer_complete (src/adapter.py:167-198)
+        const int producer = dir == 0 ? bnd : bnd + 1;
+        AdWindow& w = W[2 * bnd + dir];
+        w.exists = 1;
+        const bool reduced = cur_sz[producer] < m;
+        const double lat = raw / (double)size;  // record_transfer (:61-74)
+        if (w.len < AD_WINDOW) { w.samples[(w.head + w.len) % AD_WINDOW] = lat; ++w.len; }
+        else { w.samples[w.head] = lat; w.head = (w.head + 1) % AD_WINDOW; }
+        ++w.count; ++w.since;
+        if (!reduced) {
+            if (w.count == 1) w.baseline = lat;
+            else w.baseline += 0.05 * (lat - w.baseline);
+        }
+        if (w.since < AD_WINDOW) return;
+        // detect_fluctuation (:77-88)
+        if (w.len != AD_WINDOW || w.baseline <= 0) return;
+        NeumaierSum acc;
+        acc.start(w.samples[w.head]);
+        for (int i = 1; i < AD_WINDOW; ++i) acc.add(w.samples[(w.head + i) % AD_WINDOW]);
+        const double mean = acc.value() / (double)AD_WINDOW;
+        int sig = 0;
+        if (mean > opt.degrade_factor * w.baseline) sig = 1;
+        else if (reduced && mean < opt.recover_factor * w.baseline) sig = 2;
+        if (sig == 0) return;
+        w.degraded = sig == 1;
+        // adjust (:105-113)
+        const long long c = cur_sz[producer];
+        long long ns = c;
+        if (phase[producer] == 2 || sig == 1) ns = ad_halve(c);
+        else ns = c * 2 < m ? c * 2 : m;
+        if (ns != c) { w.since = 0; ad_apply(producer, ns); }
+    };
+
+    int cur[GP_MAX_STAGES];
+    bool busy[GP_MAX_STAGES];
+    long long l_head[2 * GP_MAX_STAGES], l_tail[2 * GP_MAX_STAGES];
+    bool l_busy[2 * GP_MAX_STAGES];
+    NeumaierSum bsum[GP_MAX_STAGES];
+    int bn[GP_MAX_STAGES];
+    unsigned n_ops = 0, n_xfer = 0;
+    SimFEv ev[3 * GP_MAX_STAGES];
+    int nev = 0;
+    unsigned long long seq = 0;
+    for (int l = 0; l < 2 * (S - 1); ++l) { l_head[l] = l_tail[l] = 0; l_busy[l] = false; }
+    if (iter_ends)
+        for (int i = 0; i < iterations; ++i) iter_ends[i] = 0.0;
+    for (int s = 0; s < S; ++s) {
+        cur[s] = 0;
+        busy[s] = false;
+        bn[s] = 0;
+        activate(s, 0);
+    }
+    auto push_op = [&](double tnow, double dur, int s, int k, int it, long long size) {
+        SimFEv& e = ev[nev++];
+        e.t = tnow + dur; e.t0 = tnow; e.seq = seq++;
+        e.code = (s << 20) | (k << 16);
+        e.it = it; e.size = size;
+        ++n_ops;
+    };
+    auto try_start = [&](double tnow, int bnd, int dir) {  // src/engine.py:276-289
+        const int l = 2 * bnd + dir;
+        if (l_busy[l] || l_head[l] >= l_tail[l]) return;
+        const unsigned long long v = lq_at(l, l_head[l]++);
+        l_busy[l] = true;
+        const long long sz = (long long)(v & 0xffffffffull);
+        const double per = dir == 0 ? T.act[bnd] : T.grad[bnd];
+        SimFEv& e = ev[nev++];
+        e.t = transfer_end(tnow, per * (double)sz, T.bw[bnd], T.lat[bnd], trace, bnd);
+        e.t0 = tnow; e.seq = seq++;
+        e.code = (int)(1u << 31) | (bnd << 20) | (dir << 16);
+        e.it = (int)(v >> 32); e.size = sz;
+    };
+    auto enqueue = [&](double tnow, int bnd, int dir, long long size, int it) {
+        const int l = 2 * bnd + dir;
+        if (l_tail[l] - l_head[l] >= sc.lcap) { overflow = true; return; }
+        lq_at(l, l_tail[l]++) = ((unsigned long long)(unsigned)it << 32) | (unsigned long long)size;
+        try_start(tnow, bnd, dir);
+    };
+    double now = 0.0;
+    while (!overflow) {
+        bool progress = true;
+        while (progress) {  // dispatch (src/engine.py:335-341)
+            progress = false;
+            for (int s = 0; s < S; ++s) {
+                if (busy[s]) continue;
+                const int it = cur[s];
+                if (it >= iterations) continue;
+                SimFPool& p = pool(s, it);
+                const bool wq_any = p.wq_head < p.wq_tail;
+                long long size = adapter ? cur_sz[s] : m, best_sz;
+                const int k = ready_op(policy, S, s, B, m, size, p.fwd_avail, p.fwd_taken, p.fwd_done,
+                                       p.bwd_avail, p.bwd_taken, p.bwd_done, p.w_done, wq_any,
+                                       wq_any ? (long long)wq_at(s, it, p.wq_head) : 0,
+                                       (p.flags & 1) != 0, (p.flags & 2) != 0, &best_sz);
+                if (k < 0) {
+                    if (async_it && p.fwd_taken == B && it + 1 < iterations) {
+                        activate(s, it + 1);  // may resize the stage
+                        size = adapter ? cur_sz[s] : m;
+                        SimFPool& nx = pool(s, it + 1);
+                        const long long rem = B - nx.fwd_taken;
+                        const long long chunk = size < rem ? size : rem;
+                        if (rem > 0 && nx.fwd_avail - nx.fwd_taken >= chunk) {
+                            nx.fwd_taken += chunk;
+                            busy[s] = true;
+                            push_op(now, T.fwd[s] * (double)chunk, s, 0, it + 1, chunk);
+                            progress = true;
+                        }
+                    }
+                    continue;
+                }
+                double dur;
+                switch (k) {
+                    case 0: dur = T.fwd[s] * (double)best_sz; p.fwd_taken += best_sz; break;
+                    case 1: dur = T.bwd[s] * (double)best_sz; p.bwd_taken += best_sz; break;
+                    case 2: dur = T.wgt[s] * (double)best_sz; p.wq_head++; break;
+                    case 3: dur = T.sync[s]; break;
+                    default: dur = T.opt[s]; break;
+                }
+                busy[s] = true;
+                push_op(now, dur, s, k, it, best_sz);
+                progress = true;
+            }
+        }
+        if (nev == 0 || overflow) break;
+        int bi = 0;
+        for (int i = 1; i < nev; ++i)
+            if (ev[i].t < ev[bi].t || (ev[i].t == ev[bi].t && ev[i].seq < ev[bi].seq)) bi = i;
+        const SimFEv e = ev[bi];
+        ev[bi] = ev[--nev];
+        now = e.t;
+        const int it = e.it, sb = (e.code >> 20) & 0x7ff, op = (e.code >> 16) & 0xf;
+        if (e.code >= 0) {  // finish_op (src/engine.py:343-378)
+            const int s = sb;
+            SimFPool& p = pool(s, it);
+            busy[s] = false;
+            const double x = now - e.t0;
+            if (bn[s]++ == 0) bsum[s].start(x); else bsum[s].add(x);
+            if (op == 0) {
+                p.fwd_done += e.size;
+                if (s < S - 1) enqueue(now, s, 0, e.size, it);
+                const int ks = it_slot(it);
+                it_fwd[ks] += e.size;
+                if (adapter && it_fwd[ks] == (long long)S * B)
+                    for (int q = 0; q < S; ++q) { phase[q] = 2; ad_apply(q, ad_halve(cur_sz[q])); }
+            } else if (op == 1) {
+                p.bwd_done += e.size;
+                if (p.wq_tail >= sc.wcap) { overflow = true; break; }
+                wq_at(s, it, p.wq_tail++) = (uint32_t)e.size;
+                if (!(p.flags & 8)) { p.flags |= 8; if (adapter) phase[s] = 1; }
+                if (s > 0) enqueue(now, s - 1, 1, e.size, it);
+            } else if (op == 2) {
+                p.w_done += e.size;
+            } else if (op == 3) {
+                p.flags |= 1;
+            } else {
+                p.flags |= 2;
+                const int ks = it_slot(it);
+                if (++it_closed[ks] == S && iter_ends) iter_ends[it] = now;
+                cur[s] = it + 1;
+                if (it + 1 < iterations) activate(s, it + 1);
+            }
+        } else {  // finish_transfer (src/engine.py:380-396)
+            l_busy[2 * sb + op] = false;
+            if (op == 0) pool(sb + 1, it).fwd_avail += e.size;
+            else pool(sb, it).bwd_avail += e.size;
+            ++n_xfer;
+            if (adapter) on_transfer(sb, op, now - e.t0, e.size);
+            try_start(now, sb, op);
+        }
+    }
+    if (overflow) return GP_ERR_CUDA;  // capacity bound broken: never a silent result
+    rep->makespan = now;
+    for (int s = 0; s < GP_MAX_STAGES; ++s) rep->busy[s] = s < S && bn[s] ? bsum[s].value() : 0.0;
+    rep->adapter_actions = actions;
+    rep->n_ops = n_ops;
+    rep->n_transfers = n_xfer;
+    rep->pad = 0;
+    for (int s = 0; s < S; ++s)
+        if (cur[s] < iterations) return GP_ERR_SCHEDULING;
+    return GP_OK;
+}
+
+__global__ void k5_sim_full(const gp_timing* __restrict__ T, long long n, int policy, int iterations,
+                            const gp_trace* __restrict__ traces, const uint32_t* __restrict__ tidx,
+                            gp_sim_options opt, SimScratch sc, gp_sim_report* __restrict__ rep,
+                            double* __restrict__ iter_ends, uint8_t* __restrict__ status) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const gp_trace* tr = traces ? traces + (tidx ? tidx[i] : 0u) : nullptr;
+    gp_sim_report r;
+    int st = sim_full(T[i], policy, iterations, tr, opt, sc, i, &r,
+                      iter_ends ? iter_ends + i * (long long)iterations : nullptr);
+    if (st != GP_OK && st != GP_ERR_SCHEDULING) {
+        r.makespan = NAN;
+        for (int s = 0; s < GP_MAX_STAGES; ++s) r.busy[s] = 0.0;
+        r.adapter_actions = r.n_ops = r.n_transfers = r.pad = 0;
+    }
+    if (st == GP_ERR_SCHEDULING) r.makespan = NAN;
+    rep[i] = r;
+    status[i] = (uint8_t)st;
+}

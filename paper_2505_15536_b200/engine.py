@@ -65,6 +65,9 @@ def lib():
         L.gp_sim_1f1b_device.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp]
         L.gp_simulate.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp, C.c_uint32,
                                   P(C.c_uint32), P(C.c_double), u8p]
+        L.gp_simulate_report.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp,
+                                         C.c_uint32, P(C.c_uint32), P(abi.GpSimOptions),
+                                         P(abi.GpSimReport), P(C.c_double), u8p]
         L.gp_replan_snapshots.argtypes = [vp, P(C.c_double), C.c_uint32, P(abi.GpBest),
                                           P(C.c_int32)]
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
@@ -219,6 +222,28 @@ class Engine:
                 int(n_traces), ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
                 ms.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
         return ms, st
+
+    def simulate_report(self, packed_timings, n: int, policy: int, iterations: int = 1,
+                        packed_traces=None, n_traces: int = 0, trace_index=None,
+                        adapter: bool = False, async_iterations: bool = False,
+                        degrade: float = 1.2, recover: float = 1.05):
+        """(GpSimReport array, iteration_ends[n, iterations], status): the
+        full simulate_timing event engine with every SimConfig option."""
+        opts = abi.GpSimOptions(int(bool(adapter)), int(bool(async_iterations)),
+                                float(degrade), float(recover))
+        reps = (abi.GpSimReport * max(1, n))()
+        ends = np.zeros((n, iterations), dtype=np.float64)
+        st = np.empty(n, dtype=np.uint8)
+        ti = None
+        if trace_index is not None:
+            ti = np.ascontiguousarray(trace_index, dtype=np.uint32)
+        if n:
+            _check(lib().gp_simulate_report(
+                self._h, C.cast(packed_timings, C.c_void_p), n, int(policy), int(iterations),
+                C.cast(packed_traces, C.c_void_p) if packed_traces is not None else None,
+                int(n_traces), ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
+                C.byref(opts), reps, ends.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
+        return reps, ends, st
 
     def sim_candidates(self, order, counts, bm, iterations: int = 1, opt_seconds: float = 0.0):
         """1F1B makespans of explicit candidates of the loaded instance."""

@@ -8,7 +8,10 @@ adapter_enabled=False, config=SimConfig(iterations=...)).makespan``
 for bit, computed by one GPU thread per timing;
 ``simulate_makespans_policy`` does the same for GPIPE / 1F1B / ZB_ORIGINAL /
 ZB_COMPACT under per-timing NetworkTrace breakpoints (src/nettrace.py:12-76),
-e.g. to rank candidate plans by simulated makespan under bandwidth drops.  Timings are the reference's
+e.g. to rank candidate plans by simulated makespan under bandwidth drops;
+``simulate_timings`` / ``simulate_timing`` run the full engine (adapter,
+asynchronous iterations) and return the scalar fields of ``SimReport``
+(src/simulator.py:31-113).  Timings are the reference's
 ``PlanTiming`` objects (or the mirrors below); ``make_timing`` mirrors the
 reference fixture builder (src/schedule.py:27-74).
 """
@@ -155,3 +158,98 @@ def simulate_makespans(timings: Sequence, iterations: int = 1, engine=None) -> n
 
 def simulate_timing_makespan(timing, iterations: int = 1, engine=None) -> float:
     return float(simulate_makespans([timing], iterations, engine)[0])
+
+
+@dataclass(frozen=True)
+class AdapterConfig:
+    """Mirror of src/adapter.py:127-130."""
+    degrade_factor: float = 1.2
+    recover_factor: float = 1.05
+
+
+@dataclass(frozen=True)
+class SimConfig:
+    """Mirror of src/simulator.py:21-28 (the reference's object works too)."""
+    iterations: int = 3
+    warmup_iterations: int = 1
+    opt_seconds: float = 0.0
+    async_iterations: bool = False
+    adapter: AdapterConfig = AdapterConfig()
+    seed: int = 0
+
+
+@dataclass(frozen=True)
+class SimSummary:
+    """The scalar fields of SimReport (src/simulator.py:31-43), computed as
+    simulate_timing does; per-op / per-transfer lists are not materialised,
+    only their counts."""
+    makespan: float
+    throughput: float
+    steady_throughput: float
+    bubble_fractions: Tuple[float, ...]
+    iteration_ends: Tuple[float, ...]
+    adapter_action_count: int
+    transfer_count: int
+    op_count: int
+    policy: str
+    adapter_enabled: bool
+    total_samples: int
+
+
+def simulate_timings(timings: Sequence, policy="1f1b", traces: Sequence = (), trace_index=None,
+                     adapter_enabled: bool = False, config=None, engine=None):
+    """``simulate_timing(t, policy, traces[trace_index[i]], adapter_enabled,
+    config)`` for every timing, batched on the GPU (one thread per timing).
+    Raises the reference's exceptions (SchedulingBugError for a stalled
+    engine, InvalidTimingError for malformed timings)."""
+    from .engine import default_engine
+    eng = engine if engine is not None else default_engine()
+    config = config if config is not None else SimConfig()
+    pol = getattr(policy, "value", policy)
+    code = abi.POLICY_CODE[pol]
+    arr = pack_timings(timings)
+    tr = pack_traces(traces) if traces else None
+    its = int(config.iterations)
+    ad = getattr(config, "adapter", None)
+    reps, ends, st = eng.simulate_report(
+        arr, len(timings), code, its, tr, len(traces), trace_index, adapter=adapter_enabled,
+        async_iterations=bool(getattr(config, "async_iterations", False)),
+        degrade=getattr(ad, "degrade_factor", 1.2), recover=getattr(ad, "recover_factor", 1.05))
+    bad = np.nonzero(st)[0]
+    if bad.size:
+        i = int(bad[0])
+        if int(st[i]) == abi.GP_ERR_CUDA:
+            raise D.DeviceError(f"timing {i}: simulator queue capacity exceeded")
+        abi.raise_for(int(st[i]), f"timing {i}: event loop stalled with work remaining"
+                      if int(st[i]) == abi.GP_ERR_SCHEDULING else f"timing {i} failed to simulate")
+    out = []
+    warm = min(int(config.warmup_iterations), its - 1)
+    for i, t in enumerate(timings):
+        r = reps[i]
+        makespan = float(r.makespan)
+        it_ends = tuple(float(x) for x in ends[i])
+        total = int(t.batch) * its
+        steady_samples = int(t.batch) * (its - warm)
+        steady_start = it_ends[warm - 1] if warm > 0 else 0.0
+        busy = [float(r.busy[s]) for s in range(len(t.stages))]
+        out.append(SimSummary(
+            makespan=makespan,
+            throughput=total / makespan,
+            steady_throughput=steady_samples / (makespan - steady_start),
+            bubble_fractions=tuple((makespan - b) / makespan for b in busy),
+            iteration_ends=it_ends,
+            adapter_action_count=int(r.adapter_actions),
+            transfer_count=int(r.n_transfers),
+            op_count=int(r.n_ops),
+            policy=pol,
+            adapter_enabled=bool(adapter_enabled),
+            total_samples=total,
+        ))
+    return out
+
+
+def simulate_timing(timing, policy="1f1b", trace=None, adapter_enabled: bool = False,
+                    config=None, engine=None) -> SimSummary:
+    """Single-timing form of :func:`simulate_timings` (src/simulator.py:71-77)."""
+    traces = (trace,) if trace is not None else ()
+    return simulate_timings([timing], policy, traces, None, adapter_enabled, config, engine)[0]

@@ -229,6 +229,52 @@ def dump_sim_policies():
     print(f"sim policies: {time.time() - t0:.1f}s", flush=True)
 
 
+def dump_sim_reports():
+    """simulate_timing reports with the adapter and asynchronous iterations:
+    makespan, throughput, steady_throughput, bubble_fractions, iteration_ends
+    and the action / transfer / op counts, under degrading traces."""
+    gp = geopipe()
+    rng = random.Random(91)
+    cases, traces = [], []
+    for _ in range(160):
+        S = rng.randint(1, 5)
+        micro = rng.choice([1, 2, 4, 8])
+        cases.append(gp.make_timing(
+            fwd=[rng.uniform(0.2, 2.0) for _ in range(S)], bwd=[rng.uniform(0.2, 2.0) for _ in range(S)],
+            wgt=[rng.uniform(0.05, 1.0) for _ in range(S)],
+            transfer=[rng.uniform(0.05, 2.5) for _ in range(S - 1)], microbatch=micro,
+            micro_count=rng.randint(1, 16), sync=[rng.uniform(0, 0.5) for _ in range(S)],
+            opt=[rng.uniform(0, 0.3) for _ in range(S)], latency=rng.uniform(0.0, 0.2)))
+        bps = {}
+        for b in range(S - 1):
+            if rng.random() < 0.8:
+                pts = sorted(set(round(rng.uniform(0.0, 60.0), 3) for _ in range(rng.randint(1, 6))))
+                bps[f"{b}-{b + 1}"] = [[x, rng.choice([0.25, 0.4, 0.5, 0.6, 1.0])] for x in pts]
+        traces.append(bps)
+    out = {"timings": [timing_to_dict(t) for t in cases], "traces": traces, "reports": {}}
+    t0 = time.time()
+    combos = [(ad, asy, pol.value, it, 1.2, 1.05) for ad in (0, 1) for asy in (0, 1)
+              for pol in gp.Policy for it in (1, 3)]
+    combos += [(1, 0, "zb_compact", 3, 1.1, 1.02), (1, 1, "1f1b", 4, 1.5, 1.2)]
+    for ad, asy, pol, it, deg, rec in combos:
+        cfg = gp.SimConfig(iterations=it, async_iterations=bool(asy),
+                           adapter=gp.AdapterConfig(degrade_factor=deg, recover_factor=rec))
+        rows = []
+        for t, bps in zip(cases, traces):
+            tr = gp.NetworkTrace(breakpoints={k: tuple(tuple(p) for p in v) for k, v in bps.items()})
+            try:
+                r = gp.simulate_timing(t, gp.Policy(pol), tr, adapter_enabled=bool(ad), config=cfg)
+            except Exception as e:
+                rows.append(type(e).__name__)
+                continue
+            rows.append([r.makespan, r.throughput, r.steady_throughput, list(r.bubble_fractions),
+                         list(r.iteration_ends), len(r.adapter_actions), len(r.transfers),
+                         sum(len(o) for o in r.schedule.ops)])
+        out["reports"][f"{ad}:{asy}:{pol}:{it}:{deg}:{rec}"] = rows
+    G.save("sim_reports.json", out)
+    print(f"sim reports: {time.time() - t0:.1f}s", flush=True)
+
+
 def dump_sim_candidates():
     """simulate(build_plan(candidate), ONE_F_ONE_B) makespans of candidates."""
     gp = geopipe()
@@ -290,6 +336,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c4", action="store_true")
     ap.add_argument("--only-sim", action="store_true")
+    ap.add_argument("--only", default=None, help="run one dump_* function, e.g. sim_reports")
     args = ap.parse_args()
     if not AVAILABLE:
         sys.exit("reference not available at /root/reference")
@@ -297,8 +344,12 @@ def main():
     sys.path.insert(0, "/root/reference/pkg/tests")
     import conftest as rc  # reference test fixtures (read-only import)
     os.makedirs(G.GOLDEN, exist_ok=True)
+    if args.only:
+        globals()["dump_" + args.only]()
+        return
     ap_only = args.only_sim
     if ap_only:
+        dump_sim_reports()
         dump_sim_policies()
         dump_sim()
         dump_sim_candidates()
@@ -306,6 +357,7 @@ def main():
         return
     dump_sim()
     dump_sim_policies()
+    dump_sim_reports()
     dump_sim_candidates()
     dump_snapshots()
 

@@ -169,3 +169,115 @@ def test_k5_constant_trace_policies_match_oracle(engine, oracle_lib):
         ms = SM.simulate_makespans_policy(tims, pol, 2, engine=engine)
         oms, ost = oracle_lib.sim_policy_batch(arr, len(tims), code, 2)
         assert (ms.view(np.uint64) == oms.view(np.uint64)).all(), pol
+
+
+# ------------------------------------------------- adapter / async reports --
+REP = G.load("sim_reports.json")
+REP_TIMINGS = [_timing(d) for d in REP["timings"]]
+
+
+def _rep_key(key):
+    ad, asy, pol, it, deg, rec = key.split(":")
+    return bool(int(ad)), bool(int(asy)), pol, int(it), float(deg), float(rec)
+
+
+def _bits(x):
+    return np.array(x, dtype=np.float64).view(np.uint64)
+
+
+def test_report_golden_exercises_the_adapter():
+    acts = sum(r[5] for k, rows in REP["reports"].items() if k.startswith("1:")
+               for r in rows if not isinstance(r, str))
+    stalls = sum(isinstance(r, str) for rows in REP["reports"].values() for r in rows)
+    assert acts > 1000 and stalls > 0
+
+
+@pytest.mark.parametrize("key", sorted(REP["reports"]))
+def test_oracle_reports_match_reference(oracle_lib, key):
+    from paper_2505_15536_b200 import abi
+    ad, asy, pol, it, deg, rec = _rep_key(key)
+    arr = SM.pack_timings(REP_TIMINGS)
+    tr = SM.pack_traces(REP["traces"])
+    reps, ends, st = oracle_lib.sim_reports(arr, len(REP_TIMINGS), abi.POLICY_CODE[pol], it, tr,
+                                            np.arange(len(REP_TIMINGS)), adapter=ad,
+                                            async_iterations=asy, degrade=deg, recover=rec)
+    for i, row in enumerate(REP["reports"][key]):
+        if isinstance(row, str):
+            assert row == "SchedulingBugError" and st[i] == abi.GP_ERR_SCHEDULING
+            continue
+        r = reps[i]
+        assert st[i] == 0
+        assert _bits(r.makespan) == _bits(row[0])
+        assert (_bits(ends[i]) == _bits(row[4])).all()
+        S = len(row[3])
+        bub = [(r.makespan - r.busy[s]) / r.makespan for s in range(S)]
+        assert (_bits(bub) == _bits(row[3])).all()
+        assert (r.adapter_actions, r.n_transfers, r.n_ops) == tuple(row[5:8])
+
+
+def _check_summaries(out, rows):
+    for o, row in zip(out, rows):
+        assert _bits(o.makespan) == _bits(row[0])
+        assert _bits(o.throughput) == _bits(row[1])
+        assert _bits(o.steady_throughput) == _bits(row[2])
+        assert (_bits(o.bubble_fractions) == _bits(row[3])).all()
+        assert (_bits(o.iteration_ends) == _bits(row[4])).all()
+        assert (o.adapter_action_count, o.transfer_count, o.op_count) == tuple(row[5:8])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", sorted(REP["reports"]))
+def test_k5_full_reports_match_reference(engine, key):
+    ad, asy, pol, it, deg, rec = _rep_key(key)
+    cfg = SM.SimConfig(iterations=it, async_iterations=asy,
+                       adapter=SM.AdapterConfig(deg, rec))
+    rows = REP["reports"][key]
+    ok = [i for i, r in enumerate(rows) if not isinstance(r, str)]
+    out = SM.simulate_timings([REP_TIMINGS[i] for i in ok], pol, [REP["traces"][i] for i in ok],
+                              np.arange(len(ok)), adapter_enabled=ad, config=cfg, engine=engine)
+    _check_summaries(out, [rows[i] for i in ok])
+    for i, r in enumerate(rows):
+        if isinstance(r, str):
+            with pytest.raises(SM.D.SchedulingBugError):
+                SM.simulate_timing(REP_TIMINGS[i], pol, REP["traces"][i], ad, cfg, engine=engine)
+
+
+@pytest.mark.gpu
+def test_k5_full_matches_oracle_large(engine, oracle_lib):
+    """10^4 random timings x random degrading traces, adapter + async, 3
+    iterations: device reports equal the oracle's bit for bit."""
+    from paper_2505_15536_b200 import abi
+    rng = random.Random(5)
+    tims = _random_timings(10000, 33)
+    traces = []
+    for t in tims:
+        bps = {}
+        for b in range(len(t.stages) - 1):
+            if rng.random() < 0.8:
+                pts = sorted(set(round(rng.uniform(0.0, 60.0), 3) for _ in range(rng.randint(1, 6))))
+                bps[f"{b}-{b + 1}"] = [[x, rng.choice([0.25, 0.5, 0.6, 1.0, 1.5])] for x in pts]
+        traces.append(bps)
+    arr = SM.pack_timings(tims)
+    tr = SM.pack_traces(traces)
+    idx = np.arange(len(tims))
+    for pol, code in abi.POLICY_CODE.items():
+        for ad, asy in ((True, False), (True, True), (False, True)):
+            reps, ends, st = engine.simulate_report(arr, len(tims), code, 3, tr, len(traces), idx,
+                                                    adapter=ad, async_iterations=asy)
+            oreps, oends, ost = oracle_lib.sim_reports(arr, len(tims), code, 3, tr, idx,
+                                                       adapter=ad, async_iterations=asy)
+            assert (st == ost).all(), (pol, ad, asy)
+            okm = st == 0
+            a = np.frombuffer(reps, dtype=np.uint8).reshape(len(tims), -1)
+            b = np.frombuffer(oreps, dtype=np.uint8).reshape(len(tims), -1)
+            assert (a[okm] == b[okm]).all(), (pol, ad, asy)
+            assert (ends.view(np.uint64)[okm] == oends.view(np.uint64)[okm]).all()
+
+
+@pytest.mark.gpu
+def test_k5_full_without_options_equals_fast_path(engine):
+    tims = _random_timings(3000, 8)
+    for pol in ("gpipe", "1f1b", "zb_original", "zb_compact"):
+        fast = SM.simulate_makespans_policy(tims, pol, 2, engine=engine)
+        full = SM.simulate_timings(tims, pol, config=SM.SimConfig(iterations=2), engine=engine)
+        assert (np.array([o.makespan for o in full]).view(np.uint64) == fast.view(np.uint64)).all()
