@@ -315,6 +315,26 @@ int gp_simulate_report(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32
                        uint32_t iterations, const gp_trace *traces, uint32_t n_traces,
                        const uint32_t *trace_index, const gp_sim_options *opts,
                        gp_sim_report *report, double *iteration_ends, uint8_t *status);
+/*
+ * Two-level device grouping per topology snapshot (kernel K7):
+ * group_first_level(topology, threshold_net) and group_second_level(fg,
+ * topology, threshold_compute) for every first-level group
+ * (src/grouping.py:146-228).  Devices are given in string-sorted id order
+ * (ClusterTopology.device_ids): p_t[s*D*D + u*D + v] is snapshot s's link
+ * metric, bandwidth (may be NULL) its bytes/s for min_intra_bandwidth, p_c
+ * shared.  Outputs, stride D per snapshot: fg_of[d] = index of d's group in
+ * the reference's fg{i} order; sg_of[d] = index of its subgroup within the
+ * group (fg{i}.sg{j}); fg_intra / fg_capacity / fg_min_bw per group
+ * (intra_metric, aggregate_capacity, min_intra_bandwidth; NaN where the
+ * reference has None); sg_capacity per subgroup in group-major order.
+ * GP_ERR_INPUT for D == 0 (EmptyClusterError) or a threshold outside (0, 1).
+ */
+int gp_group_snapshots(gp_ctx *ctx, uint32_t D, uint32_t n_snap, const double *p_t,
+                       const double *bandwidth, const double *p_c, double threshold_net,
+                       double threshold_compute, uint16_t *fg_of, uint16_t *sg_of,
+                       uint32_t *n_fg, uint32_t *n_sg, double *fg_intra, double *fg_capacity,
+                       double *fg_min_bw, double *sg_capacity);
+
 /* Same with device pointers, asynchronous on the context's stream. */
 int gp_sim_1f1b_device(gp_ctx *ctx, const gp_timing *d_timings, uint64_t n,
                        uint32_t iterations, double *d_makespan, uint8_t *d_status);

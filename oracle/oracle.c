@@ -1337,3 +1337,338 @@ int or_sim_report_batch(const gp_timing *T, uint64_t n, int policy, int iteratio
     }
     return GP_OK;
 }
+
+/* ========================================================================
+ * Two-level grouping (src/grouping.py): greedy agglomerative merging.
+ * Devices are identified by their rank in string-sorted id order (the
+ * order of ClusterTopology.device_ids, src/profiling.py:191), so tuples of
+ * sorted ids compare like arrays of ranks.
+ * ====================================================================== */
+typedef struct {
+    int n;
+    int *m;                 /* sorted member ranks */
+} og_group;
+
+typedef struct {
+    double key;
+    int a, b;               /* group ids */
+    uint64_t cnt;
+} og_entry;
+
+typedef struct {
+    int level;              /* 1: network (p_t), 2: compute (p_c) */
+    int D;
+    const double *pt, *pc;
+} og_ctx;
+
+static int og_tuple_cmp(const og_group *x, const og_group *y)
+{
+    int n = x->n < y->n ? x->n : y->n;
+    for (int i = 0; i < n; ++i)
+        if (x->m[i] != y->m[i])
+            return x->m[i] < y->m[i] ? -1 : 1;
+    return x->n < y->n ? -1 : (x->n > y->n ? 1 : 0);
+}
+
+/* group_pair_metric (src/grouping.py:54-60): mean of p_t over u in a, v in b */
+static double og_pair_metric(const og_ctx *c, const og_group *a, const og_group *b)
+{
+    size_t n = (size_t)a->n * b->n, k = 0;
+    double *v = (double *)malloc(n * sizeof(double));
+    for (int i = 0; i < a->n; ++i)
+        for (int j = 0; j < b->n; ++j)
+            v[k++] = c->pt[(size_t)a->m[i] * c->D + b->m[j]];
+    double r = or_psum(v, n) / (double)n;
+    free(v);
+    return r;
+}
+
+/* _mean_intra_pt (:63-67); returns 0 and leaves *out for singletons */
+static int og_mean_intra(const og_ctx *c, const og_group *g, double *out)
+{
+    if (g->n < 2)
+        return 0;
+    size_t n = (size_t)g->n * (g->n - 1) / 2, k = 0;
+    double *v = (double *)malloc(n * sizeof(double));
+    for (int i = 0; i < g->n; ++i)
+        for (int j = i + 1; j < g->n; ++j)
+            v[k++] = c->pt[(size_t)g->m[i] * c->D + g->m[j]];
+    *out = or_psum(v, n) / (double)n;
+    free(v);
+    return 1;
+}
+
+static double og_mean_pc(const og_ctx *c, const og_group *g)
+{
+    double *v = (double *)malloc((size_t)g->n * sizeof(double));
+    for (int i = 0; i < g->n; ++i)
+        v[i] = c->pc[g->m[i]];
+    double r = or_psum(v, (size_t)g->n) / (double)g->n;
+    free(v);
+    return r;
+}
+
+/* _relative_spread (:78-82) */
+static double og_spread(const double *v, int n)
+{
+    double top = v[0], bot = v[0];
+    for (int i = 1; i < n; ++i) {
+        if (v[i] > top)
+            top = v[i];
+        if (v[i] < bot)
+            bot = v[i];
+    }
+    if (top == 0)
+        return 0.0;
+    return (top - bot) / top;
+}
+
+static double og_pair_key(const og_ctx *c, const og_group *a, const og_group *b)
+{
+    if (c->level == 1)
+        return og_pair_metric(c, a, b);
+    double v[2] = {og_mean_pc(c, a), og_mean_pc(c, b)};
+    return og_spread(v, 2);
+}
+
+static int og_less(const og_entry *x, const og_entry *y, const og_group *G)
+{
+    if (x->key != y->key)
+        return x->key < y->key;
+    int c = og_tuple_cmp(&G[x->a], &G[y->a]);
+    if (c)
+        return c < 0;
+    c = og_tuple_cmp(&G[x->b], &G[y->b]);
+    if (c)
+        return c < 0;
+    return x->cnt < y->cnt;
+}
+
+typedef struct {
+    og_entry *h;
+    size_t n, cap;
+} og_heap;
+
+static void og_push(og_heap *H, og_entry e, const og_group *G)
+{
+    if (H->n == H->cap) {
+        H->cap = H->cap ? 2 * H->cap : 1024;
+        H->h = (og_entry *)realloc(H->h, H->cap * sizeof(og_entry));
+    }
+    size_t i = H->n++;
+    while (i > 0) {
+        size_t p = (i - 1) / 2;
+        if (!og_less(&e, &H->h[p], G))
+            break;
+        H->h[i] = H->h[p];
+        i = p;
+    }
+    H->h[i] = e;
+}
+
+static og_entry og_pop(og_heap *H, const og_group *G)
+{
+    og_entry top = H->h[0], last = H->h[--H->n];
+    size_t i = 0;
+    for (;;) {
+        size_t l = 2 * i + 1, r = l + 1, s = i;
+        const og_entry *best = &last;
+        if (l < H->n && og_less(&H->h[l], best, G)) {
+            s = l;
+            best = &H->h[l];
+        }
+        if (r < H->n && og_less(&H->h[r], best, G))
+            s = r;
+        if (s == i)
+            break;
+        H->h[i] = H->h[s];
+        i = s;
+    }
+    if (H->n)
+        H->h[i] = last;
+    return top;
+}
+
+/* _agglomerate (src/grouping.py:85-143) over the (sorted) items; writes the
+ * index of each item's final group in sorted(alive) order to group_of[i]
+ * and returns the number of groups. */
+static int og_agglomerate(const og_ctx *c, const int *items, int n, double thr, int *group_of)
+{
+    int cap = 2 * n + 1, ng = 0;
+    og_group *G = (og_group *)calloc((size_t)cap, sizeof(og_group));
+    char *alive = (char *)calloc((size_t)cap, 1);
+    double *intra = (double *)calloc((size_t)cap, sizeof(double));
+    char *has_intra = (char *)calloc((size_t)cap, 1);
+    int *order = (int *)malloc((size_t)cap * sizeof(int));  /* alive in insertion order */
+    int n_order = 0;
+    for (int i = 0; i < n; ++i) {
+        G[ng].n = 1;
+        G[ng].m = (int *)malloc(sizeof(int));
+        G[ng].m[0] = items[i];
+        alive[ng] = 1;
+        order[n_order++] = ng;
+        ng++;
+    }
+    og_heap H = {NULL, 0, 0};
+    uint64_t cnt = 0;
+    for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j) {
+            og_entry e = {og_pair_key(c, &G[i], &G[j]), i, j, cnt++};
+            og_push(&H, e, G);
+        }
+    while (H.n) {
+        og_entry e = og_pop(&H, G);
+        if (!alive[e.a] || !alive[e.b])
+            continue;
+        const og_group *a = &G[e.a], *b = &G[e.b];
+        double vals[3];
+        int nv;
+        if (c->level == 1) {
+            double cross = og_pair_metric(c, a, b);
+            double va, vb;
+            if (!has_intra[e.a])
+                has_intra[e.a] = (char)og_mean_intra(c, a, &intra[e.a]) | 2;
+            if (!has_intra[e.b])
+                has_intra[e.b] = (char)og_mean_intra(c, b, &intra[e.b]) | 2;
+            va = (has_intra[e.a] & 1) ? intra[e.a] : cross;
+            vb = (has_intra[e.b] & 1) ? intra[e.b] : cross;
+            vals[0] = va;
+            vals[1] = vb;
+            vals[2] = cross;
+            nv = 3;
+        } else {
+            vals[0] = og_mean_pc(c, a);
+            vals[1] = og_mean_pc(c, b);
+            nv = 2;
+        }
+        if (og_spread(vals, nv) >= thr)
+            continue;
+        alive[e.a] = alive[e.b] = 0;
+        og_group *mg = &G[ng];
+        mg->n = a->n + b->n;
+        mg->m = (int *)malloc((size_t)mg->n * sizeof(int));
+        {   /* tuple(sorted(a + b)) */
+            int i = 0, j = 0, k = 0;
+            while (i < a->n || j < b->n)
+                mg->m[k++] = (j >= b->n || (i < a->n && a->m[i] < b->m[j])) ? a->m[i++] : b->m[j++];
+        }
+        int mid = ng++;
+        /* push_pairs(merged) over alive groups in dict order, then insert */
+        int w = 0;
+        for (int q = 0; q < n_order; ++q)
+            if (alive[order[q]])
+                order[w++] = order[q];
+        n_order = w;
+        for (int q = 0; q < n_order; ++q) {
+            int o = order[q];
+            int x = mid, y = o;
+            if (og_tuple_cmp(&G[y], &G[x]) < 0) {
+                x = o;
+                y = mid;
+            }
+            og_entry ne = {og_pair_key(c, &G[x], &G[y]), x, y, cnt++};
+            og_push(&H, ne, G);
+        }
+        alive[mid] = 1;
+        order[n_order++] = mid;
+    }
+    /* sorted(alive): by tuple order */
+    int na = 0;
+    for (int q = 0; q < ng; ++q)
+        if (alive[q])
+            order[na++] = q;
+    for (int i = 1; i < na; ++i) {  /* insertion sort, na is small */
+        int v = order[i], j = i - 1;
+        while (j >= 0 && og_tuple_cmp(&G[order[j]], &G[v]) > 0) {
+            order[j + 1] = order[j];
+            --j;
+        }
+        order[j + 1] = v;
+    }
+    for (int gi = 0; gi < na; ++gi) {
+        const og_group *g = &G[order[gi]];
+        for (int t = 0; t < g->n; ++t)
+            for (int i = 0; i < n; ++i)
+                if (items[i] == g->m[t])
+                    group_of[i] = gi;
+    }
+    for (int q = 0; q < ng; ++q)
+        free(G[q].m);
+    free(G);
+    free(alive);
+    free(intra);
+    free(has_intra);
+    free(order);
+    free(H.h);
+    return na;
+}
+
+/* group_first_level + group_second_level (src/grouping.py:146-228) for one
+ * topology given in rank order: fg_of[d], sg_of[d] (index within the FG),
+ * per FG (index f < *n_fg): intra_metric (NaN for singletons),
+ * aggregate_capacity, min_intra_bandwidth (NaN for singletons); per SG in
+ * FG-major order: aggregate_capacity.  Returns GP_OK / GP_ERR_INPUT. */
+int or_group_hierarchy(int D, const double *pt, const double *bw, const double *pc,
+                       double thr_net, double thr_comp, uint16_t *fg_of, uint16_t *sg_of,
+                       uint32_t *n_fg, uint32_t *n_sg, double *fg_intra, double *fg_cap,
+                       double *fg_minbw, double *sg_cap)
+{
+    if (D < 1)
+        return GP_ERR_INPUT;  /* EmptyClusterError */
+    if (!(thr_net > 0 && thr_net < 1) || !(thr_comp > 0 && thr_comp < 1))
+        return GP_ERR_INPUT;  /* ValueError */
+    og_ctx c1 = {1, D, pt, pc};
+    int *items = (int *)malloc((size_t)D * sizeof(int));
+    int *gof = (int *)malloc((size_t)D * sizeof(int));
+    for (int d = 0; d < D; ++d)
+        items[d] = d;
+    int nf = og_agglomerate(&c1, items, D, thr_net, gof);
+    *n_fg = (uint32_t)nf;
+    uint32_t sg_base = 0;
+    int *mem = (int *)malloc((size_t)D * sizeof(int));
+    int *sgo = (int *)malloc((size_t)D * sizeof(int));
+    double *tmp = (double *)malloc(((size_t)D * D / 2 + D + 1) * sizeof(double));
+    for (int f = 0; f < nf; ++f) {
+        int nm = 0;
+        for (int d = 0; d < D; ++d)
+            if (gof[d] == f)
+                mem[nm++] = d;
+        for (int i = 0; i < nm; ++i)
+            fg_of[mem[i]] = (uint16_t)f;
+        og_group g = {nm, mem};
+        double v;
+        fg_intra[f] = og_mean_intra(&c1, &g, &v) ? v : NAN;
+        for (int i = 0; i < nm; ++i)
+            tmp[i] = pc[mem[i]];
+        fg_cap[f] = or_psum(tmp, (size_t)nm);
+        if (nm < 2) {
+            fg_minbw[f] = NAN;
+        } else {
+            double mb = INFINITY;
+            for (int i = 0; i < nm; ++i)
+                for (int j = i + 1; j < nm; ++j)
+                    if (bw[(size_t)mem[i] * D + mem[j]] < mb)
+                        mb = bw[(size_t)mem[i] * D + mem[j]];
+            fg_minbw[f] = mb;
+        }
+        og_ctx c2 = {2, D, pt, pc};
+        int ns = og_agglomerate(&c2, mem, nm, thr_comp, sgo);
+        for (int i = 0; i < nm; ++i)
+            sg_of[mem[i]] = (uint16_t)sgo[i];
+        for (int sgi = 0; sgi < ns; ++sgi) {
+            int k = 0;
+            for (int i = 0; i < nm; ++i)
+                if (sgo[i] == sgi)
+                    tmp[k++] = pc[mem[i]];
+            sg_cap[sg_base + sgi] = or_psum(tmp, (size_t)k);
+        }
+        sg_base += (uint32_t)ns;
+    }
+    *n_sg = sg_base;
+    free(items);
+    free(gof);
+    free(mem);
+    free(sgo);
+    free(tmp);
+    return GP_OK;
+}

@@ -63,6 +63,10 @@ def lib():
         L.or_sim_report_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, C.c_int,
                                           P(abi.GpTrace), P(C.c_uint32), P(abi.GpSimOptions),
                                           P(abi.GpSimReport), P(C.c_double), P(C.c_uint8)]
+        L.or_group_hierarchy.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(C.c_double),
+                                         C.c_double, C.c_double, P(C.c_uint16), P(C.c_uint16),
+                                         P(C.c_uint32), P(C.c_uint32), P(C.c_double),
+                                         P(C.c_double), P(C.c_double), P(C.c_double)]
         _lib = L
     return _lib
 
@@ -188,3 +192,25 @@ def sim_reports(packed_timings, n, policy, iterations=1, traces=None, trace_inde
                               ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
                               C.byref(opts), reps, _dp(ends), _u8(st))
     return reps, ends, st
+
+
+def group_hierarchy(pt, bw, pc, thr_net=0.3, thr_comp=0.3):
+    """(status, grouping.Hierarchy) of group_first_level + group_second_level
+    for one topology in rank order (grouping.topology_arrays)."""
+    from paper_2505_15536_b200.grouping import Hierarchy
+    pt = np.ascontiguousarray(pt, dtype=np.float64)
+    bw = np.ascontiguousarray(bw, dtype=np.float64)
+    pc = np.ascontiguousarray(pc, dtype=np.float64)
+    n = len(pc)
+    fg_of = np.zeros(n, np.uint16); sg_of = np.zeros(n, np.uint16)
+    nf = C.c_uint32(0); ns = C.c_uint32(0)
+    fi = np.zeros(max(n, 1)); fc = np.zeros(max(n, 1)); fb = np.zeros(max(n, 1))
+    sc = np.zeros(max(n, 1))
+    u16 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint16))
+    st = lib().or_group_hierarchy(n, _dp(pt), _dp(bw), _dp(pc), float(thr_net), float(thr_comp),
+                                  u16(fg_of), u16(sg_of), C.byref(nf), C.byref(ns), _dp(fi),
+                                  _dp(fc), _dp(fb), _dp(sc))
+    if st:
+        return st, None
+    return st, Hierarchy(fg_of, sg_of, fi[:nf.value].copy(), fc[:nf.value].copy(),
+                         fb[:nf.value].copy(), sc[:ns.value].copy())

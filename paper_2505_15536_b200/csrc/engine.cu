@@ -32,6 +32,7 @@
 #include "k4_bnb.cuh"
 #include "k6_snapshots.cuh"
 #include "k5_sim.cuh"
+#include "k7_grouping.cuh"
 
 // ----------------------------------------------------------------------------
 // context
@@ -113,6 +114,7 @@ struct gp_ctx {
     DBuf<gp_sim_report> s_rep;  // K5 full reports
     DBuf<double> s_ends;
     DBuf<uint32_t> s_wq;         // K5 full queue scratch
+    DBuf<uint8_t> g_buf;         // K7 inputs, outputs and scratch
     DBuf<unsigned long long> s_lq;
     SolveOut* h_solve = nullptr;  // pinned
     RangeGeom last_geom{};
@@ -250,7 +252,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     c->z_bw.release(); c->z_mbw.release(); c->z_xt.release(); c->z_flags.release();
     c->z_tpk.release(); c->z_tcol.release(); c->z_res.release(); c->z_cnt.release();
     c->dsolve.release(); c->gbest.release(); c->s_tim.release(); c->s_traces.release(); c->s_tidx.release(); c->s_ms.release(); c->s_st.release();
-    c->s_rep.release(); c->s_ends.release(); c->s_wq.release(); c->s_lq.release();
+    c->s_rep.release(); c->s_ends.release(); c->g_buf.release(); c->s_wq.release(); c->s_lq.release();
     if (c->flags_ev) cudaEventDestroy(c->flags_ev);
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
@@ -1545,3 +1547,70 @@ int gp_diag_fp64_peak(int device, double* dadd_per_second) {
 }
 
 }  // extern "C"
+
+// ----------------------------------------------------------------------------
+// K7: device grouping per topology snapshot
+// ----------------------------------------------------------------------------
+extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_t,
+                                  const double* bandwidth, const double* p_c, double threshold_net,
+                                  double threshold_compute, uint16_t* fg_of, uint16_t* sg_of,
+                                  uint32_t* n_fg, uint32_t* n_sg, double* fg_intra,
+                                  double* fg_capacity, double* fg_min_bw, double* sg_capacity) {
+    if (!c || !p_t || !p_c || !fg_of || !sg_of || !n_fg || !n_sg || !fg_intra || !fg_capacity ||
+        !fg_min_bw || !sg_capacity)
+        return fail(GP_ERR_INPUT, "bad arguments");
+    if (D == 0) return fail(GP_ERR_INPUT, "topology has no devices");
+    if (D > GP_MAX_MEMBERS) return fail(GP_ERR_INPUT, "%u devices exceed %d", D, GP_MAX_MEMBERS);
+    if (!(threshold_net > 0 && threshold_net < 1) || !(threshold_compute > 0 && threshold_compute < 1))
+        return fail(GP_ERR_INPUT, "threshold must lie in (0, 1)");
+    if (n_snap == 0) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    const size_t DD = (size_t)D * D;
+    const size_t per_scr = k7_scratch_bytes((int)D);
+    // snapshots per launch: scratch <= 512 MiB
+    uint32_t SB = (uint32_t)((512ull << 20) / per_scr);
+    if (SB < 1) SB = 1;
+    if (SB > n_snap) SB = n_snap;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t o_pt = 0, o_bw = o_pt + al(SB * DD * 8), o_pc = o_bw + al(bandwidth ? SB * DD * 8 : 8);
+    const size_t o_u16 = o_pc + al((size_t)D * 8), o_cnt = o_u16 + al((size_t)SB * D * 2 * 2);
+    const size_t o_dbl = o_cnt + al((size_t)SB * 2 * 4), o_scr = o_dbl + al((size_t)SB * D * 4 * 8);
+    const size_t total = o_scr + SB * per_scr;
+    CUDA_TRY(c->g_buf.ensure(total));
+    uint8_t* b = c->g_buf.p;
+    const size_t smem = k7_smem_bytes((int)D);
+    CUDA_TRY(cudaFuncSetAttribute(k7_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaMemcpyAsync(b + o_pc, p_c, (size_t)D * 8, cudaMemcpyHostToDevice, s));
+    for (uint32_t s0 = 0; s0 < n_snap; s0 += SB) {
+        const uint32_t nb = (n_snap - s0) < SB ? (n_snap - s0) : SB;
+        CUDA_TRY(cudaMemcpyAsync(b + o_pt, p_t + (size_t)s0 * DD, nb * DD * 8, cudaMemcpyHostToDevice, s));
+        if (bandwidth)
+            CUDA_TRY(cudaMemcpyAsync(b + o_bw, bandwidth + (size_t)s0 * DD, nb * DD * 8,
+                                     cudaMemcpyHostToDevice, s));
+        uint16_t* d_fg = reinterpret_cast<uint16_t*>(b + o_u16);
+        uint16_t* d_sg = d_fg + (size_t)SB * D;
+        uint32_t* d_nf = reinterpret_cast<uint32_t*>(b + o_cnt);
+        uint32_t* d_ns = d_nf + SB;
+        double* d_dbl = reinterpret_cast<double*>(b + o_dbl);
+        double *d_fi = d_dbl, *d_fc = d_fi + (size_t)SB * D, *d_fb = d_fc + (size_t)SB * D,
+               *d_sc = d_fb + (size_t)SB * D;
+        k7_group<<<nb, K7_THREADS, smem, s>>>(
+            (int)D, reinterpret_cast<const double*>(b + o_pt),
+            bandwidth ? reinterpret_cast<const double*>(b + o_bw) : nullptr, (long long)DD,
+            (long long)DD, reinterpret_cast<const double*>(b + o_pc), threshold_net,
+            threshold_compute, b + o_scr, per_scr, d_fg, d_sg, d_nf, d_ns, d_fi, d_fc, d_fb, d_sc);
+        CUDA_TRY(cudaGetLastError());
+        const size_t o = (size_t)s0 * D;
+        CUDA_TRY(cudaMemcpyAsync(fg_of + o, d_fg, (size_t)nb * D * 2, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(sg_of + o, d_sg, (size_t)nb * D * 2, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(n_fg + s0, d_nf, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(n_sg + s0, d_ns, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(fg_intra + o, d_fi, (size_t)nb * D * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(fg_capacity + o, d_fc, (size_t)nb * D * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(fg_min_bw + o, d_fb, (size_t)nb * D * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(sg_capacity + o, d_sc, (size_t)nb * D * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));  // staging buffers are reused by the next batch
+    }
+    return GP_OK;
+}

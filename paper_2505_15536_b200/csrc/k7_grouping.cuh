@@ -1,0 +1,384 @@
+// k7_grouping.cuh - K7: two-level device grouping (group_first_level +
+// group_second_level, src/grouping.py:85-228), one CTA per topology snapshot.
+#pragma once
+#include "common.cuh"
+
+// ----------------------------------------------------------------------------
+// The reference merges greedily from a heap of (key, a, b, counter) entries.
+// Every live pair of groups has exactly one entry, pushed when the younger of
+// the two groups was created, and its key depends only on the two member
+// sets, so the heap pops the live pair with the smallest (key, a, b) where
+// groups compare as sorted tuples of ids.  Live groups are disjoint, so the
+// tuple order is the order of their smallest member; each group therefore
+// lives in the slot of its smallest member (device rank, or local index for
+// the second level), and the pop is an arg-min over (key, slot a, slot b).
+//
+// Instead of a heap the CTA keeps, per slot a, the best live pair (a, b > a)
+// of its row (row minima in shared memory); a pop is a CTA arg-min over the
+// row minima.  After a merge of b into a, only rows that pointed at a or b
+// are rescanned; the others compare against their new pair (c, a).
+// A pair that fails the merge predicate is dropped for good, as the
+// reference's discarded heap entry is.
+//
+// Keys and merge values are the reference's sums (CPython 3.12 sum, i.e.
+// Neumaier) over the reference's operand order, computed by one thread each:
+// group_pair_metric runs u over the first group's sorted members and v over
+// the second's (:54-60); _mean_intra_pt runs over combinations of the sorted
+// members (:63-67); mean_pc over the members (:203-204).
+// ----------------------------------------------------------------------------
+#define K7_THREADS 256
+
+struct K7Shared {
+    double* rowkey;     // [n] best live key of row a
+    double* intra;      // [n] level 1: _mean_intra_pt cache; level 2: mean_pc
+    int16_t* rowarg;    // [n] its partner b (-1: row empty)
+    int16_t* cnt;       // [n] members of the group in slot a (0: dead slot)
+    uint8_t* has;       // [n] intra cache valid (bit0) / singleton (bit1)
+};
+
+struct K7Global {
+    double* key;        // [n*n] pair keys, row a < column b
+    uint8_t* live;      // [n*n] pair still in the heap
+    uint16_t* mem;      // [n*n] members (device ranks) of slot a at mem[a*n ..]
+    uint16_t* tmp;      // [n]   merge buffer
+};
+
+__device__ __forceinline__ bool k7_less(double k1, int a1, int b1, double k2, int a2, int b2) {
+    if (k1 != k2) return k1 < k2;
+    if (a1 != a2) return a1 < a2;
+    return b1 < b2;
+}
+
+// pair key of slots x < y (level 1: group_pair_metric; level 2:
+// _relative_spread of the two mean p_c)
+__device__ double k7_pair_key(int level, const K7Global& g, const K7Shared& sh, int n,
+                              const double* __restrict__ pt, int D, int x, int y) {
+    if (level == 2) {
+        const double va = sh.intra[x], vb = sh.intra[y];
+        const double top = va >= vb ? va : vb, bot = va <= vb ? va : vb;
+        if (top == 0) return 0.0;
+        return (top - bot) / top;
+    }
+    const uint16_t* mx = g.mem + (size_t)x * n;
+    const uint16_t* my = g.mem + (size_t)y * n;
+    const int nx = sh.cnt[x], ny = sh.cnt[y];
+    NeumaierSum s;
+    bool first = true;
+    for (int i = 0; i < nx; ++i) {
+        const double* row = pt + (size_t)mx[i] * D;
+        for (int j = 0; j < ny; ++j) {
+            const double v = row[my[j]];
+            if (first) { s.start(v); first = false; } else s.add(v);
+        }
+    }
+    return s.value() / (double)((long long)nx * ny);
+}
+
+// _mean_intra_pt of slot a (level 1) or mean p_c (level 2), one thread
+__device__ void k7_group_value(int level, const K7Global& g, const K7Shared& sh, int n,
+                               const double* __restrict__ pt, const double* __restrict__ pc, int D,
+                               int a) {
+    const uint16_t* m = g.mem + (size_t)a * n;
+    const int c = sh.cnt[a];
+    if (level == 2) {
+        NeumaierSum s;
+        s.start(pc[m[0]]);
+        for (int i = 1; i < c; ++i) s.add(pc[m[i]]);
+        sh.intra[a] = s.value() / (double)c;
+        sh.has[a] = 1;
+        return;
+    }
+    if (c < 2) { sh.has[a] = 2; return; }
+    NeumaierSum s;
+    bool first = true;
+    for (int i = 0; i < c; ++i)
+        for (int j = i + 1; j < c; ++j) {
+            const double v = pt[(size_t)m[i] * D + m[j]];
+            if (first) { s.start(v); first = false; } else s.add(v);
+        }
+    sh.intra[a] = s.value() / (double)((long long)c * (c - 1) / 2);
+    sh.has[a] = 1;
+}
+
+// full rescan of row a by one thread
+__device__ __forceinline__ void k7_scan_row(const K7Global& g, const K7Shared& sh, int n, int a) {
+    double bk = 0.0;
+    int bb = -1;
+    const double* kr = g.key + (size_t)a * n;
+    const uint8_t* lr = g.live + (size_t)a * n;
+    for (int b = a + 1; b < n; ++b)
+        if (lr[b] && sh.cnt[b] && (bb < 0 || kr[b] < bk)) { bk = kr[b]; bb = b; }
+    sh.rowkey[a] = bk;
+    sh.rowarg[a] = (int16_t)bb;
+}
+
+// CTA arg-min over the row minima: returns (a, b) in s_ab, or a = -1
+__device__ void k7_pop(const K7Shared& sh, int n, int* s_ab, double* s_red, int* s_ia) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    double bk = 0.0;
+    int ba = -1, bb = -1;
+    for (int a = tid; a < n; a += blockDim.x) {
+        const int b = sh.rowarg[a];
+        if (sh.cnt[a] == 0 || b < 0) continue;
+        const double k = sh.rowkey[a];
+        if (ba < 0 || k7_less(k, a, b, bk, ba, bb)) { bk = k; ba = a; bb = b; }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double k2 = __shfl_down_sync(0xffffffffu, bk, o);
+        const int a2 = __shfl_down_sync(0xffffffffu, ba, o);
+        const int b2 = __shfl_down_sync(0xffffffffu, bb, o);
+        if (a2 >= 0 && (ba < 0 || k7_less(k2, a2, b2, bk, ba, bb))) { bk = k2; ba = a2; bb = b2; }
+    }
+    if (lane == 0) { s_red[wid] = bk; s_ia[2 * wid] = ba; s_ia[2 * wid + 1] = bb; }
+    __syncthreads();
+    if (tid == 0) {
+        double k = 0.0;
+        int a = -1, b = -1;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            const int a2 = s_ia[2 * w], b2 = s_ia[2 * w + 1];
+            if (a2 >= 0 && (a < 0 || k7_less(s_red[w], a2, b2, k, a, b))) { k = s_red[w]; a = a2; b = b2; }
+        }
+        s_ab[0] = a;
+        s_ab[1] = b;
+    }
+    __syncthreads();
+}
+
+// _agglomerate over n items (device ranks items[i], sorted): on return
+// group_of[i] = index of the item's group in sorted(alive) order; returns
+// the number of groups.  All threads of the CTA call it.
+__device__ int k7_agglomerate(int level, int n, const uint16_t* items, const double* __restrict__ pt,
+                              const double* __restrict__ pc, int D, double thr, const K7Global& g,
+                              const K7Shared& sh, uint16_t* group_of, int* s_ab, double* s_red,
+                              int* s_ia) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int a = tid; a < n; a += nt) {
+        sh.cnt[a] = 1;
+        g.mem[(size_t)a * n] = items[a];
+        sh.has[a] = 0;
+    }
+    __syncthreads();
+    if (level == 2)
+        for (int a = tid; a < n; a += nt) k7_group_value(2, g, sh, n, pt, pc, D, a);
+    __syncthreads();
+    for (long long p = tid; p < (long long)n * n; p += nt) {
+        const int a = (int)(p / n), b = (int)(p % n);
+        if (b > a) {
+            g.key[p] = k7_pair_key(level, g, sh, n, pt, D, a, b);
+            g.live[p] = 1;
+        }
+    }
+    __syncthreads();
+    for (int a = tid; a < n; a += nt) k7_scan_row(g, sh, n, a);
+    __syncthreads();
+    for (;;) {
+        k7_pop(sh, n, s_ab, s_red, s_ia);
+        const int a = s_ab[0], b = s_ab[1];
+        if (a < 0) break;
+        // merge predicate (merge_values + _relative_spread, :154-180, :203-210)
+        if (tid == 0) {
+            double v0, v1, v2 = 0.0;
+            int nv;
+            if (level == 1) {
+                const double cross = g.key[(size_t)a * n + b];
+                if (!sh.has[a]) k7_group_value(1, g, sh, n, pt, pc, D, a);
+                if (!sh.has[b]) k7_group_value(1, g, sh, n, pt, pc, D, b);
+                v0 = (sh.has[a] & 1) ? sh.intra[a] : cross;
+                v1 = (sh.has[b] & 1) ? sh.intra[b] : cross;
+                v2 = cross;
+                nv = 3;
+            } else {
+                v0 = sh.intra[a];
+                v1 = sh.intra[b];
+                nv = 2;
+            }
+            double top = v0, bot = v0;
+            if (v1 > top) top = v1;
+            if (v1 < bot) bot = v1;
+            if (nv == 3) { if (v2 > top) top = v2; if (v2 < bot) bot = v2; }
+            const double spread = top == 0 ? 0.0 : (top - bot) / top;
+            if (spread >= thr) {
+                g.live[(size_t)a * n + b] = 0;  // discarded permanently
+                k7_scan_row(g, sh, n, a);
+                s_ab[2] = 0;
+            } else {
+                // merged = tuple(sorted(a + b)) into slot a
+                const uint16_t* ma = g.mem + (size_t)a * n;
+                const uint16_t* mb = g.mem + (size_t)b * n;
+                const int na = sh.cnt[a], nb = sh.cnt[b];
+                int i = 0, j = 0, k = 0;
+                while (i < na || j < nb)
+                    g.tmp[k++] = (j >= nb || (i < na && ma[i] < mb[j])) ? ma[i++] : mb[j++];
+                uint16_t* md = g.mem + (size_t)a * n;
+                for (int q = 0; q < k; ++q) md[q] = g.tmp[q];
+                sh.cnt[a] = (int16_t)k;
+                sh.cnt[b] = 0;
+                g.live[(size_t)a * n + b] = 0;
+                sh.has[a] = 0;
+                s_ab[2] = 1;
+            }
+        }
+        __syncthreads();
+        if (!s_ab[2]) continue;
+        if (level == 2 && tid == 0) k7_group_value(2, g, sh, n, pt, pc, D, a);
+        __syncthreads();
+        // pairs of the merged group with every other live group; drop b's
+        for (int c = tid; c < n; c += nt) {
+            if (c == a || sh.cnt[c] == 0) continue;
+            const int x = c < a ? c : a, y = c < a ? a : c;
+            g.key[(size_t)x * n + y] = k7_pair_key(level, g, sh, n, pt, D, x, y);
+            g.live[(size_t)x * n + y] = 1;
+            if (c < b) g.live[(size_t)c * n + b] = 0;
+        }
+        __syncthreads();
+        // row minima: rows that pointed at a or b rescan; rows c < a compare
+        // against their new pair (c, a); row a rescans
+        for (int c = tid; c < n; c += nt) {
+            if (sh.cnt[c] == 0) continue;
+            const int r = sh.rowarg[c];
+            if (c == a || r == a || r == b) {
+                k7_scan_row(g, sh, n, c);
+            } else if (c < a) {
+                const double k = g.key[(size_t)c * n + a];
+                if (r < 0 || k7_less(k, c, a, sh.rowkey[c], c, r)) {
+                    sh.rowkey[c] = k;
+                    sh.rowarg[c] = (int16_t)a;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // sorted(alive): slot order; group index = rank among live slots
+    if (tid == 0) {
+        int gi = 0;
+        for (int a = 0; a < n; ++a) {
+            if (sh.cnt[a] == 0) continue;
+            const uint16_t* m = g.mem + (size_t)a * n;
+            for (int q = 0; q < sh.cnt[a]; ++q) {
+                // members are device ranks; map back to local item index
+                int lo = 0, hi = n - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (items[mid] < m[q]) lo = mid + 1; else hi = mid;
+                }
+                group_of[lo] = (uint16_t)gi;
+            }
+            ++gi;
+        }
+        s_ab[3] = gi;
+    }
+    __syncthreads();
+    return s_ab[3];
+}
+
+// One CTA per snapshot.  Outputs (stride D per snapshot): fg_of, sg_of,
+// fg_intra / fg_cap / fg_minbw per FG, sg_cap per SG (FG-major); n_fg, n_sg.
+__global__ void __launch_bounds__(K7_THREADS)
+k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw_all,
+         long long pt_stride, long long bw_stride, const double* __restrict__ pc, double thr_net,
+         double thr_comp, uint8_t* __restrict__ scratch, size_t scratch_per, uint16_t* fg_of_all,
+         uint16_t* sg_of_all, uint32_t* n_fg, uint32_t* n_sg, double* fg_intra_all,
+         double* fg_cap_all, double* fg_minbw_all, double* sg_cap_all) {
+    extern __shared__ __align__(16) uint8_t k7_smem[];
+    __shared__ int s_ab[4];
+    __shared__ double s_red[K7_THREADS / 32];
+    __shared__ int s_ia[2 * (K7_THREADS / 32)];
+    const int snap = blockIdx.x, tid = threadIdx.x;
+    const double* pt = pt_all + (size_t)snap * pt_stride;
+    const double* bw = bw_all ? bw_all + (size_t)snap * bw_stride : nullptr;
+    uint8_t* base = scratch + (size_t)snap * scratch_per;
+    K7Global g;
+    g.key = reinterpret_cast<double*>(base);
+    g.mem = reinterpret_cast<uint16_t*>(base + (size_t)D * D * 8);
+    g.tmp = g.mem + (size_t)D * D;
+    g.live = reinterpret_cast<uint8_t*>(g.tmp + D);
+    K7Shared sh;
+    sh.rowkey = reinterpret_cast<double*>(k7_smem);
+    sh.intra = sh.rowkey + D;
+    sh.rowarg = reinterpret_cast<int16_t*>(sh.intra + D);
+    sh.cnt = sh.rowarg + D;
+    uint16_t* items = reinterpret_cast<uint16_t*>(sh.cnt + D);
+    uint16_t* gof = items + D;          // level-1 group of each device
+    uint16_t* sgo = gof + D;            // level-2 group of each FG member
+    sh.has = reinterpret_cast<uint8_t*>(sgo + D);
+    uint16_t* fg_of = fg_of_all + (size_t)snap * D;
+    uint16_t* sg_of = sg_of_all + (size_t)snap * D;
+    double* fg_intra = fg_intra_all + (size_t)snap * D;
+    double* fg_cap = fg_cap_all + (size_t)snap * D;
+    double* fg_minbw = fg_minbw_all + (size_t)snap * D;
+    double* sg_cap = sg_cap_all + (size_t)snap * D;
+
+    for (int d = tid; d < D; d += blockDim.x) items[d] = (uint16_t)d;
+    __syncthreads();
+    const int nf = k7_agglomerate(1, D, items, pt, pc, D, thr_net, g, sh, gof, s_ab, s_red, s_ia);
+    for (int d = tid; d < D; d += blockDim.x) fg_of[d] = gof[d];
+    __syncthreads();
+    int sg_base = 0;
+    for (int f = 0; f < nf; ++f) {
+        // members of FG f in rank order
+        if (tid == 0) {
+            int k = 0;
+            for (int d = 0; d < D; ++d)
+                if (gof[d] == f) items[k++] = (uint16_t)d;
+            s_ab[0] = k;
+        }
+        __syncthreads();
+        const int nm = s_ab[0];
+        __syncthreads();
+        // FG statistics (group_first_level, :176-188)
+        if (tid == 0) {
+            NeumaierSum s;
+            s.start(pc[items[0]]);
+            for (int i = 1; i < nm; ++i) s.add(pc[items[i]]);
+            fg_cap[f] = s.value();
+            if (nm < 2) {
+                fg_intra[f] = NAN;
+                fg_minbw[f] = NAN;
+            } else {
+                NeumaierSum t;
+                bool first = true;
+                double mb = INFINITY;
+                for (int i = 0; i < nm; ++i)
+                    for (int j = i + 1; j < nm; ++j) {
+                        const size_t e = (size_t)items[i] * D + items[j];
+                        if (first) { t.start(pt[e]); first = false; } else t.add(pt[e]);
+                        if (bw && bw[e] < mb) mb = bw[e];
+                    }
+                fg_intra[f] = t.value() / (double)((long long)nm * (nm - 1) / 2);
+                fg_minbw[f] = bw ? mb : NAN;
+            }
+        }
+        // second level over the FG's members (local slots 0..nm-1)
+        const int ns = k7_agglomerate(2, nm, items, pt, pc, D, thr_comp, g, sh, sgo, s_ab, s_red,
+                                      s_ia);
+        for (int i = tid; i < nm; i += blockDim.x) sg_of[items[i]] = sgo[i];
+        __syncthreads();
+        if (tid == 0) {
+            for (int q = 0; q < ns; ++q) {
+                NeumaierSum s;
+                bool first = true;
+                for (int i = 0; i < nm; ++i)
+                    if (sgo[i] == q) {
+                        const double v = pc[items[i]];
+                        if (first) { s.start(v); first = false; } else s.add(v);
+                    }
+                sg_cap[sg_base + q] = s.value();
+            }
+        }
+        sg_base += ns;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        n_fg[snap] = (uint32_t)nf;
+        n_sg[snap] = (uint32_t)sg_base;
+    }
+}
+
+__host__ __forceinline__ size_t k7_scratch_bytes(int D) {
+    size_t b = (size_t)D * D * 8 + (size_t)D * D * 2 + (size_t)D * 2 + (size_t)D * D;
+    return (b + 255) & ~(size_t)255;
+}
+
+__host__ __forceinline__ size_t k7_smem_bytes(int D) {
+    return (size_t)D * 8 * 2 + (size_t)D * 2 * 5 + (size_t)D + 16;
+}

@@ -65,6 +65,10 @@ class InvalidTimingError(GeopipeError):
     """Timing vectors inconsistent with the stage count (src/errors.py:53)."""
 
 
+class EmptyClusterError(GeopipeError):
+    """Grouping was asked to run on a topology with no devices."""
+
+
 class SchedulingBugError(GeopipeError):
     """The 1F1B event loop stalled (src/errors.py:57-62)."""
 

@@ -68,6 +68,11 @@ def lib():
         L.gp_simulate_report.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp,
                                          C.c_uint32, P(C.c_uint32), P(abi.GpSimOptions),
                                          P(abi.GpSimReport), P(C.c_double), u8p]
+        u16p = P(C.c_uint16)
+        L.gp_group_snapshots.argtypes = [vp, C.c_uint32, C.c_uint32, P(C.c_double),
+                                         P(C.c_double), P(C.c_double), C.c_double, C.c_double,
+                                         u16p, u16p, P(C.c_uint32), P(C.c_uint32), P(C.c_double),
+                                         P(C.c_double), P(C.c_double), P(C.c_double)]
         L.gp_replan_snapshots.argtypes = [vp, P(C.c_double), C.c_uint32, P(abi.GpBest),
                                           P(C.c_int32)]
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
@@ -244,6 +249,30 @@ class Engine:
                 int(n_traces), ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
                 C.byref(opts), reps, ends.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
         return reps, ends, st
+
+    def group_snapshots(self, p_t, bandwidth, p_c, threshold_net=0.3, threshold_compute=0.3):
+        """K7 grouping of ``p_t[n_snap, D, D]`` (rank order); returns the raw
+        arrays (fg_of, sg_of, n_fg, n_sg, fg_intra, fg_cap, fg_min_bw, sg_cap)."""
+        p_t = np.ascontiguousarray(p_t, dtype=np.float64)
+        if p_t.ndim == 2:
+            p_t = p_t[None]
+        ns, D = p_t.shape[0], p_t.shape[1]
+        bw = None
+        if bandwidth is not None:
+            bw = np.ascontiguousarray(np.broadcast_to(bandwidth, p_t.shape), dtype=np.float64)
+        pc = np.ascontiguousarray(p_c, dtype=np.float64)
+        fg_of = np.zeros((ns, D), np.uint16); sg_of = np.zeros((ns, D), np.uint16)
+        nf = np.zeros(ns, np.uint32); nsg = np.zeros(ns, np.uint32)
+        fi, fc, fb, sc = (np.zeros((ns, D)) for _ in range(4))
+        P = C.POINTER
+        dp = lambda a: a.ctypes.data_as(P(C.c_double))
+        u16 = lambda a: a.ctypes.data_as(P(C.c_uint16))
+        u32 = lambda a: a.ctypes.data_as(P(C.c_uint32))
+        _check(lib().gp_group_snapshots(self._h, D, ns, dp(p_t), dp(bw) if bw is not None else None,
+                                        dp(pc), float(threshold_net), float(threshold_compute),
+                                        u16(fg_of), u16(sg_of), u32(nf), u32(nsg), dp(fi), dp(fc),
+                                        dp(fb), dp(sc)))
+        return fg_of, sg_of, nf, nsg, fi, fc, fb, sc
 
     def sim_candidates(self, order, counts, bm, iterations: int = 1, opt_seconds: float = 0.0):
         """1F1B makespans of explicit candidates of the loaded instance."""

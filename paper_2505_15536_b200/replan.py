@@ -81,3 +81,45 @@ def replan_snapshots(model, topology, groups, config, bandwidths: np.ndarray,
     if detail:
         eng.set_bandwidth(packed.bw)
     return out
+
+
+def snapshot_topology(topology, p_t: np.ndarray, bandwidth: Optional[np.ndarray] = None):
+    """The topology with every link's p_t (and bandwidth) replaced by the
+    snapshot's ``[D, D]`` matrices in string-sorted id order; latency kept."""
+    ids = sorted(d.id for d in topology.devices)
+    pos = {d: i for i, d in enumerate(ids)}
+    links = {}
+    for key, info in topology.links.items():
+        u, v = tuple(key)
+        i, j = pos[u], pos[v]
+        links[key] = D.LinkInfo(
+            metric=D.CommMetric(p_t=float(p_t[i, j])), latency_seconds=info.latency_seconds,
+            bandwidth_bytes_per_s=float(bandwidth[i, j]) if bandwidth is not None
+            else info.bandwidth_bytes_per_s)
+    return D.ClusterTopology(devices=topology.devices, compute=topology.compute, links=links)
+
+
+def replan_regrouped(model, topology, config, p_t_snapshots, bandwidth_snapshots=None,
+                     threshold_net: float = 0.3, threshold_compute: float = 0.3,
+                     engine: Optional[Engine] = None):
+    """Re-plan per snapshot when p_t changes too:
+    every snapshot is regrouped on the GPU (K7, group_first_level +
+    group_second_level) and then re-planned exactly (exhaustive_plan through
+    the engine).  Returns one SearchResult - or the exception the reference
+    would raise - per snapshot, plus the GroupIndex used."""
+    from .grouping import regroup_snapshots
+    from .planner import exhaustive_plan
+    eng = engine or default_engine()
+    pts = np.asarray(p_t_snapshots, dtype=np.float64)
+    bws = None if bandwidth_snapshots is None else np.asarray(bandwidth_snapshots, np.float64)
+    groupings = regroup_snapshots(topology, pts, bws, threshold_net, threshold_compute,
+                                  engine=eng)
+    out = []
+    for s, (_, _, gi) in enumerate(groupings):
+        topo_s = snapshot_topology(topology, pts[s], None if bws is None else
+                                   np.broadcast_to(bws, pts.shape)[s])
+        try:
+            out.append((exhaustive_plan(model, topo_s, gi, config, engine=eng), gi))
+        except D.GeopipeError as e:
+            out.append((e, gi))
+    return out

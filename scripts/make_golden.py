@@ -360,6 +360,8 @@ def main():
     dump_sim_reports()
     dump_sim_candidates()
     dump_snapshots()
+    dump_grouping()
+    dump_regroup_replan()
 
     for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
                                 ("c2", "c2", False), ("c2j", "c2", True)]:
@@ -425,6 +427,74 @@ def main():
     if not args.skip_c4:
         dump_c4("c4", False)
         dump_c4("c4j", True)
+
+
+
+
+def dump_grouping():
+    """group_first_level / group_second_level of the reference on the
+    topologies of tests/grouping_cases.py (rebuilt as reference objects)."""
+    gp = geopipe()
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import grouping_cases as GC
+    from geopipe.profiling import ClusterTopology, CommMetric, ComputeMetric, LinkInfo
+    out = {}
+    t0 = time.time()
+    for name in GC.names():
+        pt, bw, pc, tn, tc = GC.build(name)
+        n = len(pc)
+        ids = [f"d{i:04d}" for i in range(n)]  # string order == rank order
+        devices = tuple(gp.DeviceSpec(id=i, memory_bytes=1e12, benchmark_times=(("b", 1.0),))
+                        for i in ids)
+        compute = {ids[i]: ComputeMetric(p_c=float(pc[i])) for i in range(n)}
+        links = {frozenset((ids[i], ids[j])): LinkInfo(metric=CommMetric(p_t=float(pt[i, j])),
+                                                        latency_seconds=0.0,
+                                                        bandwidth_bytes_per_s=float(bw[i, j]))
+                 for i in range(n) for j in range(i + 1, n)}
+        topo = ClusterTopology(devices=devices, compute=compute, links=links)
+        fgs = gp.group_first_level(topo, tn)
+        rank = {d: i for i, d in enumerate(ids)}
+        rows = []
+        for fg in fgs:
+            sgs = gp.group_second_level(fg, topo, tc)
+            rows.append([[rank[d] for d in fg.member_device_ids], fg.intra_metric,
+                         fg.aggregate_capacity, fg.min_intra_bandwidth,
+                         [[[rank[d] for d in sg.member_device_ids], sg.aggregate_capacity]
+                          for sg in sgs]])
+        out[name] = rows
+    G.save("grouping.json", out)
+    print(f"grouping: {time.time() - t0:.1f}s", flush=True)
+
+
+def dump_regroup_replan():
+    """exhaustive_plan of the reference on C2 with per-snapshot p_t
+    (tests/grouping_cases.py c2snap*), regrouped by the reference."""
+    gp = geopipe()
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import grouping_cases as GC
+    from geopipe.profiling import ClusterTopology, CommMetric, LinkInfo
+    from geopipe.timing import GroupIndex
+    spec = I.config("c2")
+    model, topo, _ = build_reference(spec)
+    ids = sorted(d.id for d in topo.devices)
+    pos = {d: i for i, d in enumerate(ids)}
+    out = {}
+    t0 = time.time()
+    for s in range(4):
+        pt, _, _, tn, tc = GC.build(f"c2snap{s}")
+        links = {}
+        for key, info in topo.links.items():
+            u, v = tuple(key)
+            links[key] = LinkInfo(metric=CommMetric(p_t=float(pt[pos[u], pos[v]])),
+                                  latency_seconds=info.latency_seconds,
+                                  bandwidth_bytes_per_s=info.bandwidth_bytes_per_s)
+        t2 = ClusterTopology(devices=topo.devices, compute=topo.compute, links=links)
+        fgs = gp.group_first_level(t2, tn)
+        groups = GroupIndex.build(fgs, {fg.id: gp.group_second_level(fg, t2, tc) for fg in fgs})
+        r = run_or_error(lambda: gp.exhaustive_plan(model, t2, groups, gp.SearchConfig(seed=0)))
+        out[f"c2snap{s}"] = r
+    G.save("regroup_replan.json", out)
+    print(f"regroup re-plan: {time.time() - t0:.1f}s", flush=True)
 
 
 if __name__ == "__main__":
