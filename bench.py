@@ -241,6 +241,77 @@ def extra_sections(eng, packed, total, local, args, world):
         out["k6_snapshot_replan"]["cpu_port_ms_per_snapshot"] = (time.perf_counter() - t0) / 5 * 1e3
     e2.close()
 
+    # ---- K7: regroup C4 (64 devices) per p_t snapshot
+    from paper_2505_15536_b200 import grouping as GR
+    _, t4, _ = instances.load("c4")
+    ids4, pt4, bw4, pc4 = GR.topology_arrays(t4)
+    spec4 = instances.config("c4")
+    reg = np.array([{i: r for i, r, _, _, _ in spec4.devices()}[d] for d in ids4])
+    nreg = int(reg.max()) + 1
+    rng7 = np.random.default_rng(7)
+    n7 = 1000
+    fac = np.where(rng7.random((n7, nreg, nreg)) < 0.5, rng7.uniform(1.0, 3.0, (n7, nreg, nreg)), 1.0)
+    fac = np.triu(fac) + np.triu(fac, 1).transpose(0, 2, 1)
+    pts = pt4[None] * fac[:, reg][:, :, reg]
+    GR.group_hierarchies(pts[:8], bw4, pc4, engine=eng)
+    t0 = time.perf_counter()
+    hs = GR.group_hierarchies(pts, bw4, pc4, engine=eng)
+    el = time.perf_counter() - t0
+    lat = []
+    for j in range(20):
+        t1 = time.perf_counter()
+        GR.group_hierarchies(pts[j:j + 1], bw4, pc4, engine=eng)
+        lat.append(time.perf_counter() - t1)
+    out["k7_regroup"] = {
+        "snapshots": n7, "devices": int(len(ids4)), "host_call_s": el,
+        "snapshots_per_s": n7 / el, "single_snapshot_latency_ms_p50": statistics.median(lat) * 1e3,
+        "groups_seen": sorted({len(h.fg_capacity) for h in hs}),
+        "note": "group_first_level + group_second_level per C4 p_t snapshot, one CTA each; "
+                "p_t matrices H2D inside the call; the Python reference takes ~50 ms per "
+                "grouping at 64 devices (SURVEY §8(f))"}
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        for j in range(20):
+            O.group_hierarchy(pts[j], bw4, pc4)
+        out["k7_regroup"]["cpu_port_ms_per_snapshot"] = (time.perf_counter() - t0) / 20 * 1e3
+
+    # ---- K5 full: adapter + asynchronous iterations under degrading traces
+    rng5 = np.random.default_rng(5)
+    n5 = 100_000
+    S5 = rng5.integers(2, 6, n5)
+    tims = []
+    for i in range(n5):
+        S = int(S5[i])
+        tims.append(simulate.make_timing(
+            fwd=list(rng5.uniform(0.2, 2.0, S)), bwd=list(rng5.uniform(0.2, 2.0, S)),
+            wgt=list(rng5.uniform(0.05, 1.0, S)), transfer=list(rng5.uniform(0.05, 2.5, S - 1)),
+            microbatch=int(rng5.choice([2, 4, 8])), micro_count=int(rng5.integers(4, 17)),
+            sync=list(rng5.uniform(0.0, 0.5, S)), opt=list(rng5.uniform(0.0, 0.3, S)),
+            latency=float(rng5.uniform(0.0, 0.2))))
+    traces = [{f"{b}-{b + 1}": [[float(t), float(m)] for t, m in
+                                zip(np.sort(rng5.uniform(0, 60, 4)), rng5.choice([0.25, 0.5, 1.0], 4))]
+               for b in range(4)} for _ in range(64)]
+    arr5 = simulate.pack_timings(tims)
+    tr5 = simulate.pack_traces(traces)
+    ti5 = np.arange(n5) % 64
+    eng.simulate_report(arr5, 1000, 3, 3, tr5, 64, ti5[:1000], adapter=True, async_iterations=True)
+    t0 = time.perf_counter()
+    reps5, _, st5 = eng.simulate_report(arr5, n5, 3, 3, tr5, 64, ti5, adapter=True,
+                                        async_iterations=True)
+    el = time.perf_counter() - t0
+    out["k5_full_adapter"] = {
+        "simulations": n5, "host_call_s": el, "simulations_per_s": n5 / el,
+        "ok": int((st5 == 0).sum()),
+        "adapter_actions": int(sum(r.adapter_actions for r in reps5)),
+        "note": "ZB_COMPACT, 3 iterations, DynamicBatchAdapter on, asynchronous iterations, "
+                "64 breakpoint traces; one thread per simulation; includes H2D/D2H"}
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        O.sim_reports(arr5, 5000, 3, 3, tr5, ti5[:5000], adapter=True, async_iterations=True)
+        out["k5_full_adapter"]["cpu_port_simulations_per_s_1thread"] = 5000 / (time.perf_counter() - t0)
+
     # ---- K4: exact re-plan of spaces far beyond enumeration (k = 8 groups)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from test_bnb import _many_group_instance

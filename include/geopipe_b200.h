@@ -192,6 +192,42 @@ typedef struct gp_sim_options {
     double recover_factor;        /* AdapterConfig.recover_factor (1.05)     */
 } gp_sim_options;
 
+/* One executed operation (PipeOp, src/engine.py:55-64); kinds F, B, W,
+ * SYNC, OPT = 0..4 (OpKind "F","B","W","S","O"). */
+typedef struct gp_op {
+    double start, end;
+    int32_t size;
+    int32_t microbatch_id;        /* -1 for None (sync / optimizer step)     */
+    uint32_t iteration;
+    uint8_t kind, stage;
+    uint16_t pad;
+} gp_op;
+
+/* One finished transfer (TransferRecord, src/engine.py:67-76); link_id is
+ * the plan's boundary link, direction 0 "fwd", 1 "bwd". */
+typedef struct gp_transfer {
+    double start, end;
+    int32_t size, microbatch_id;
+    uint32_t iteration;
+    uint8_t boundary, direction;
+    uint16_t pad;
+} gp_transfer;
+
+/* One validate_schedule violation (src/schedule.py:95-171); the message
+ * text is formatted by the host from these fields.  Codes:
+ * 0 op ends before it starts (stage, kind); 1 ops overlap (stage, t);
+ * 2 F before its activation arrives; 3 B before F ends; 4 B before its
+ * gradient arrives; 5 W before B ends (stage, microbatch, iteration);
+ * 6 not one sync and one optimizer; 7 sync before last weight update;
+ * 8 optimizer before sync ends (stage, iteration). */
+typedef struct gp_violation {
+    double t;
+    uint32_t iteration;
+    int32_t microbatch_id;
+    uint8_t code, stage, kind, pad;
+    uint32_t pad2;
+} gp_violation;
+
 /* Per-timing SimReport ingredients (src/simulator.py:84-113): the host
  * derives throughput, steady_throughput and bubble_fractions from these
  * exactly as simulate_timing does. */
@@ -334,6 +370,37 @@ int gp_group_snapshots(gp_ctx *ctx, uint32_t D, uint32_t n_snap, const double *p
                        double threshold_compute, uint16_t *fg_of, uint16_t *sg_of,
                        uint32_t *n_fg, uint32_t *n_sg, double *fg_intra, double *fg_capacity,
                        double *fg_min_bw, double *sg_capacity);
+
+/*
+ * The schedules themselves (generate_schedule / SimReport.schedule and
+ * .transfers): timing i writes its ops, in per-stage start order
+ * interleaved by start, to ops[op_offset[i] ..] and its transfers, in
+ * completion order, to transfers[xfer_offset[i] ..] (transfers / offsets
+ * may be NULL).  Offsets come from gp_simulate_report's n_ops /
+ * n_transfers; a timing whose counts disagree reports GP_ERR_INPUT.
+ */
+int gp_simulate_schedule(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t policy,
+                         uint32_t iterations, const gp_trace *traces, uint32_t n_traces,
+                         const uint32_t *trace_index, const gp_sim_options *opts,
+                         const uint64_t *op_offset, gp_op *ops, const uint64_t *xfer_offset,
+                         gp_transfer *transfers, uint8_t *status);
+
+/*
+ * validate_schedule(schedule_i, timings[i], tol) and the per-stage busy sums
+ * of bubble_fraction (src/schedule.py:95-182) for a batch of schedules:
+ * schedule i = ops[op_offset[i] .. op_offset[i+1]) (stage field decides the
+ * stage list; order within a stage is list order), makespan[i].  Writes
+ * n_violations[i] and the first max_violations records to
+ * violations[i*max_violations ..]; busy[i*GP_MAX_STAGES + s] =
+ * sum(op.end - op.start) over stage s (may be NULL).  Micro-batch ids must
+ * be dense per (stage, iteration, kind) in list order, as the engine
+ * produces them (else status GP_ERR_INPUT).
+ */
+int gp_validate_schedules(gp_ctx *ctx, const gp_timing *timings, uint64_t n,
+                          const uint64_t *op_offset, const gp_op *ops, const double *makespan,
+                          uint32_t iterations, double tol, uint32_t max_violations,
+                          gp_violation *violations, uint32_t *n_violations, double *busy,
+                          uint8_t *status);
 
 /* Same with device pointers, asynchronous on the context's stream. */
 int gp_sim_1f1b_device(gp_ctx *ctx, const gp_timing *d_timings, uint64_t n,

@@ -761,8 +761,8 @@ size_t or_abi_sizeof(int which)
 
 /* ------------------------------------------------------------------------
  * PipelineEngine.run for any Policy, any NetworkTrace on the boundary links,
- * no adapter, synchronous iterations (src/engine.py:125-431,
- * src/nettrace.py:12-76).
+ * optionally the DynamicBatchAdapter and asynchronous iterations
+ * (src/engine.py:125-431, src/nettrace.py:12-76, src/adapter.py:133-224).
  * A direct restatement with the reference's data structures: per
  * (stage, iteration) pools, FIFO link queues, a (time, seq) binary heap.
  * ---------------------------------------------------------------------- */
@@ -770,6 +770,8 @@ typedef struct {
     int64_t fwd_avail, fwd_taken, fwd_done, bwd_avail, bwd_taken, bwd_done;
     int64_t wq_head, wq_tail, w_done;   /* w_queue as a FIFO of sizes */
     int64_t *wq;                        /* sizes */
+    int64_t *wq_id;                     /* micro-batch ids */
+    int64_t fwd_next_id, bwd_next_id;
     int sync_done, opt_done, activated, first_bwd;
 } sim_pool;
 
@@ -779,7 +781,8 @@ typedef struct {
     int kind;           /* 0 op, 1 transfer */
     int s, op, it;      /* op: stage, op kind (0 F,1 B,2 W,3 S,4 O), iteration */
     int64_t size;       /* also transfer size; for transfers s=boundary, op=dir */
-    double t0;          /* transfer start (adapter latency samples) */
+    double t0;          /* op / transfer start */
+    int64_t mb;         /* micro-batch id (-1: None) */
 } sim_ev;
 
 /* ---- DynamicBatchAdapter (src/adapter.py:18-224) ---------------------- */
@@ -936,7 +939,7 @@ static sim_ev heap_pop(sim_heap *H)
 }
 
 typedef struct {
-    int64_t *q_size;
+    int64_t *q_size, *q_mb;
     int *q_it;
     int64_t head, tail;
     int busy;
@@ -980,12 +983,12 @@ static double transfer_end(double start, double bytes, double base_bw, double la
 
 int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
                 const gp_sim_options *opts, gp_sim_report *rep, double *iter_ends,
-                double *makespan_out);
+                gp_op *ops_out, gp_transfer *xf_out, double *makespan_out);
 
 int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
            double *makespan_out)
 {
-    return or_sim_full(T, policy, iterations, trace, NULL, NULL, NULL, makespan_out);
+    return or_sim_full(T, policy, iterations, trace, NULL, NULL, NULL, NULL, NULL, makespan_out);
 }
 
 int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
@@ -998,7 +1001,7 @@ int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
  * asynchronous iterations (:297-314); rep / iter_ends may be NULL. */
 int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
                 const gp_sim_options *opts, gp_sim_report *rep, double *iter_ends,
-                double *makespan_out)
+                gp_op *ops_out, gp_transfer *xf_out, double *makespan_out)
 {
     const int S = (int)T->n_stages;
     if (S < 1 || S > GP_MAX_STAGES || iterations < 1)
@@ -1026,8 +1029,10 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
         A.current[s] = m;
     int64_t *it_fwd_done = (int64_t *)calloc((size_t)iterations, sizeof(int64_t));
     sim_pool *pools = (sim_pool *)calloc((size_t)S * iterations, sizeof(sim_pool));
-    for (int i = 0; i < S * iterations; ++i)
+    for (int i = 0; i < S * iterations; ++i) {
         pools[i].wq = (int64_t *)calloc((size_t)per_it + 1, sizeof(int64_t));
+        pools[i].wq_id = (int64_t *)calloc((size_t)per_it + 1, sizeof(int64_t));
+    }
 #define POOL(s, it) (&pools[(s) * iterations + (it)])
     int cur[GP_MAX_STAGES], busy[GP_MAX_STAGES], closed_cnt = 0;
     int *stages_closed = (int *)calloc((size_t)iterations, sizeof(int));
@@ -1035,6 +1040,7 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
     const int64_t lcap = per_it * iterations + 1;
     for (int l = 0; l < 2 * (S - 1); ++l) {
         links[l].q_size = (int64_t *)calloc((size_t)lcap, sizeof(int64_t));
+        links[l].q_mb = (int64_t *)calloc((size_t)lcap, sizeof(int64_t));
         links[l].q_it = (int *)calloc((size_t)lcap, sizeof(int));
         links[l].head = links[l].tail = 0;
         links[l].busy = 0;
@@ -1059,6 +1065,22 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
         busy[s] = 0;
         ACTIVATE(s, 0);
     }
+    /* ops[s].append(op) at start (src/engine.py:304-330) */
+#define RECORD_OP(e_)                                                                      \
+    do {                                                                                   \
+        if (ops_out) {                                                                     \
+            gp_op *o_ = &ops_out[n_ops];                                                   \
+            o_->start = (e_).t0;                                                           \
+            o_->end = (e_).t;                                                              \
+            o_->size = (int32_t)(e_).size;                                                 \
+            o_->microbatch_id = (int32_t)(e_).mb;                                          \
+            o_->iteration = (uint32_t)(e_).it;                                             \
+            o_->kind = (uint8_t)(e_).op;                                                   \
+            o_->stage = (uint8_t)(e_).s;                                                   \
+            o_->pad = 0;                                                                   \
+        }                                                                                  \
+        n_ops++;                                                                           \
+    } while (0)
 
     /* try_start_link (src/engine.py:276-289) */
 #define TRY_START(tnow, bnd, dir)                                                          \
@@ -1066,13 +1088,14 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
         sim_link *L_ = &links[2 * (bnd) + (dir)];                                           \
         if (!L_->busy && L_->head < L_->tail) {                                            \
             int64_t sz_ = L_->q_size[L_->head];                                            \
+            int64_t mb_ = L_->q_mb[L_->head];                                              \
             int it_ = L_->q_it[L_->head];                                                  \
             L_->head++;                                                                    \
             L_->busy = 1;                                                                  \
             double per_ = (dir) == 0 ? T->act[bnd] : T->grad[bnd];                         \
             double end_ = transfer_end((tnow), per_ * (double)sz_, T->bw[bnd], T->lat[bnd], \
                                        trace, (bnd));                                      \
-            sim_ev e_ = {end_, seq++, 1, (bnd), (dir), it_, sz_, (tnow)};                  \
+            sim_ev e_ = {end_, seq++, 1, (bnd), (dir), it_, sz_, (tnow), mb_};             \
             heap_push(&H, e_);                                                             \
         }                                                                                  \
     } while (0)
@@ -1160,9 +1183,10 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
                     if (remaining > 0 && nx->fwd_avail - nx->fwd_taken >= chunk) {
                         nx->fwd_taken += chunk;
                         busy[s] = 1;
-                        sim_ev e = {now + T->fwd[s] * (double)chunk, seq++, 0, s, 0, it + 1, chunk, now};
+                        sim_ev e = {now + T->fwd[s] * (double)chunk, seq++, 0, s, 0, it + 1, chunk,
+                                    now, nx->fwd_next_id};
                         heap_push(&H, e);
-                        n_ops++;
+                        RECORD_OP(e);
                         progress = 1;
                     }
                     continue;
@@ -1178,9 +1202,11 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
                 default: dur = T->opt[s]; break;
                 }
                 busy[s] = 1;
-                sim_ev e = {now + dur, seq++, 0, s, best_k, it, best_sz, now};
+                int64_t mb = best_k == 0 ? p->fwd_next_id : best_k == 1 ? p->bwd_next_id
+                             : best_k == 2 ? p->wq_id[p->wq_head - 1] : -1;
+                sim_ev e = {now + dur, seq++, 0, s, best_k, it, best_sz, now, mb};
                 heap_push(&H, e);
-                n_ops++;
+                RECORD_OP(e);
                 progress = 1;
             }
         }
@@ -1209,9 +1235,11 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
             }
             if (e.op == 0) {
                 p->fwd_done += e.size;
+                p->fwd_next_id++;
                 if (s < S - 1) {
                     sim_link *L = &links[2 * s + 0];
                     L->q_size[L->tail] = e.size;
+                    L->q_mb[L->tail] = e.mb;
                     L->q_it[L->tail] = it;
                     L->tail++;
                     TRY_START(now, s, 0);
@@ -1224,6 +1252,8 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
                     }
             } else if (e.op == 1) {
                 p->bwd_done += e.size;
+                p->bwd_next_id++;
+                p->wq_id[p->wq_tail] = e.mb;
                 p->wq[p->wq_tail++] = e.size;
                 if (!p->first_bwd) {
                     p->first_bwd = 1;
@@ -1233,6 +1263,7 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
                 if (s > 0) {
                     sim_link *L = &links[2 * (s - 1) + 1];
                     L->q_size[L->tail] = e.size;
+                    L->q_mb[L->tail] = e.mb;
                     L->q_it[L->tail] = it;
                     L->tail++;
                     TRY_START(now, s - 1, 1);
@@ -1258,6 +1289,17 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
                 POOL(bnd + 1, e.it)->fwd_avail += e.size;
             else
                 POOL(bnd, e.it)->bwd_avail += e.size;
+            if (xf_out) {  /* transfers.append(TransferRecord(...)) */
+                gp_transfer *x = &xf_out[n_xfer];
+                x->start = e.t0;
+                x->end = now;
+                x->size = (int32_t)e.size;
+                x->microbatch_id = (int32_t)e.mb;
+                x->iteration = (uint32_t)e.it;
+                x->boundary = (uint8_t)bnd;
+                x->direction = (uint8_t)dir;
+                x->pad = 0;
+            }
             n_xfer++;
             if (adapter)
                 ad_transfer_complete(&A, bnd, dir, now - e.t0, e.size);
@@ -1278,19 +1320,23 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
         rep->n_ops = n_ops;
         rep->n_transfers = n_xfer;
     }
-    for (int i = 0; i < S * iterations; ++i)
+    for (int i = 0; i < S * iterations; ++i) {
         free(pools[i].wq);
+        free(pools[i].wq_id);
+    }
     free(pools);
     free(stages_closed);
     free(it_fwd_done);
     for (int l = 0; l < 2 * (S - 1); ++l) {
         free(links[l].q_size);
+        free(links[l].q_mb);
         free(links[l].q_it);
     }
     free(H.h);
 #undef POOL
 #undef TRY_START
 #undef ACTIVATE
+#undef RECORD_OP
     return status;
 }
 
@@ -1330,7 +1376,8 @@ int or_sim_report_batch(const gp_timing *T, uint64_t n, int policy, int iteratio
         double ms = NAN;
         const gp_trace *tr = traces ? &traces[trace_index ? trace_index[i] : 0] : NULL;
         int st = or_sim_full(&T[i], policy, iterations, tr, opts, &reports[i],
-                             iter_ends ? iter_ends + i * (uint64_t)iterations : NULL, &ms);
+                             iter_ends ? iter_ends + i * (uint64_t)iterations : NULL, NULL, NULL,
+                             &ms);
         if (st != GP_OK)
             reports[i].makespan = NAN;
         status[i] = (uint8_t)st;
@@ -1670,5 +1717,225 @@ int or_group_hierarchy(int D, const double *pt, const double *bw, const double *
     free(mem);
     free(sgo);
     free(tmp);
+    return GP_OK;
+}
+
+
+/* Schedules (ops + transfers) of a batch of timings at the given offsets
+ * (from or_sim_report_batch's counts). */
+int or_sim_schedule_batch(const gp_timing *T, uint64_t n, int policy, int iterations,
+                          const gp_trace *traces, const uint32_t *trace_index,
+                          const gp_sim_options *opts, const uint64_t *op_offset, gp_op *ops,
+                          const uint64_t *xf_offset, gp_transfer *xfers, uint8_t *status)
+{
+    for (uint64_t i = 0; i < n; ++i) {
+        double ms = NAN;
+        gp_sim_report rep;
+        const gp_trace *tr = traces ? &traces[trace_index ? trace_index[i] : 0] : NULL;
+        status[i] = (uint8_t)or_sim_full(&T[i], policy, iterations, tr, opts, &rep, NULL,
+                                         ops + op_offset[i], xfers ? xfers + xf_offset[i] : NULL,
+                                         &ms);
+    }
+    return GP_OK;
+}
+
+/* ========================================================================
+ * validate_schedule + bubble_fraction busy sums (src/schedule.py:95-182)
+ * for one schedule given as gp_op records (stage lists = records of that
+ * stage in array order).  The index dict keeps the first-insertion order
+ * of each key and the last op stored under it, as a Python dict does.
+ * ====================================================================== */
+typedef struct {
+    int s, kind;
+    uint32_t it;
+    int32_t k;
+    uint64_t op;  /* last op with this key */
+} ov_key;
+
+static void ov_emit(gp_violation *out, uint32_t max_v, uint32_t *nv, int code, int stage,
+                    int kind, uint32_t it, int32_t mb, double t)
+{
+    if (*nv < max_v) {
+        gp_violation *v = &out[*nv];
+        memset(v, 0, sizeof(*v));
+        v->code = (uint8_t)code;
+        v->stage = (uint8_t)stage;
+        v->kind = (uint8_t)kind;
+        v->iteration = it;
+        v->microbatch_id = mb;
+        v->t = t;
+    }
+    (*nv)++;
+}
+
+static int64_t ov_find(const ov_key *K, uint64_t nk, int s, int kind, uint32_t it, int32_t k)
+{
+    for (uint64_t i = 0; i < nk; ++i)
+        if (K[i].s == s && K[i].kind == kind && K[i].it == it && K[i].k == k)
+            return (int64_t)K[i].op;
+    return -1;
+}
+
+int or_validate_schedule(const gp_timing *T, const gp_op *ops, uint64_t n, double makespan,
+                         double tol_rel, uint32_t max_v, gp_violation *out, uint32_t *n_v,
+                         double *busy)
+{
+    const int S = (int)T->n_stages;
+    const double tol = tol_rel * (makespan > 1.0 ? makespan : 1.0);
+    uint32_t nv = 0;
+    ov_key *K = (ov_key *)malloc((n + 1) * sizeof(ov_key));
+    uint64_t nk = 0;
+    uint64_t *ord = (uint64_t *)malloc((n + 1) * sizeof(uint64_t));
+    /* 1. end >= start, and the index */
+    for (int s = 0; s < S; ++s)
+        for (uint64_t i = 0; i < n; ++i) {
+            const gp_op *o = &ops[i];
+            if (o->stage != s)
+                continue;
+            if (o->end < o->start - tol)
+                ov_emit(out, max_v, &nv, 0, s, o->kind, 0, 0, 0.0);
+            if (o->microbatch_id >= 0) {
+                uint64_t q;
+                for (q = 0; q < nk; ++q)
+                    if (K[q].s == s && K[q].kind == o->kind && K[q].it == o->iteration &&
+                        K[q].k == o->microbatch_id)
+                        break;
+                if (q == nk) {
+                    K[nk].s = s;
+                    K[nk].kind = o->kind;
+                    K[nk].it = o->iteration;
+                    K[nk].k = o->microbatch_id;
+                    nk++;
+                }
+                K[q].op = i;
+            }
+        }
+    /* 2. overlaps in (start, end) order, stable */
+    for (int s = 0; s < S; ++s) {
+        uint64_t m = 0;
+        for (uint64_t i = 0; i < n; ++i)
+            if (ops[i].stage == s)
+                ord[m++] = i;
+        for (uint64_t i = 1; i < m; ++i) {  /* stable insertion sort */
+            uint64_t v = ord[i];
+            int64_t j = (int64_t)i - 1;
+            while (j >= 0 && (ops[ord[j]].start > ops[v].start ||
+                              (ops[ord[j]].start == ops[v].start && ops[ord[j]].end > ops[v].end))) {
+                ord[j + 1] = ord[j];
+                --j;
+            }
+            ord[j + 1] = v;
+        }
+        int have = 0;
+        double prev_end = 0.0;
+        for (uint64_t i = 0; i < m; ++i) {
+            const gp_op *o = &ops[ord[i]];
+            if (have && o->start < prev_end - tol)
+                ov_emit(out, max_v, &nv, 1, s, 0, 0, 0, o->start);
+            /* prev_end = max(prev_end or op.end, op.end): 0.0 is falsy */
+            double base = (have && prev_end != 0.0) ? prev_end : o->end;
+            prev_end = o->end > base ? o->end : base;
+            have = 1;
+        }
+    }
+    /* 3. dependencies, in index (first-insertion) order */
+    for (uint64_t q = 0; q < nk; ++q) {
+        const int s = K[q].s, kind = K[q].kind;
+        const uint32_t it = K[q].it;
+        const int32_t k = K[q].k;
+        const gp_op *o = &ops[K[q].op];
+        if (kind == 0 && s > 0) {
+            int64_t u = ov_find(K, nk, s - 1, 0, it, k);
+            if (u >= 0) {
+                double arrival = ops[u].end + (T->lat[s - 1] + (T->act[s - 1] * (double)o->size) / T->bw[s - 1]);
+                if (o->start < arrival - tol)
+                    ov_emit(out, max_v, &nv, 2, s, 0, it, k, 0.0);
+            }
+        }
+        if (kind == 1) {
+            int64_t f = ov_find(K, nk, s, 0, it, k);
+            if (f >= 0 && o->start < ops[f].end - tol)
+                ov_emit(out, max_v, &nv, 3, s, 1, it, k, 0.0);
+            if (s < S - 1) {
+                int64_t d = ov_find(K, nk, s + 1, 1, it, k);
+                if (d >= 0) {
+                    double arrival = ops[d].end + (T->lat[s] + (T->grad[s] * (double)o->size) / T->bw[s]);
+                    if (o->start < arrival - tol)
+                        ov_emit(out, max_v, &nv, 4, s, 1, it, k, 0.0);
+                }
+            }
+        }
+        if (kind == 2) {
+            int64_t b = ov_find(K, nk, s, 1, it, k);
+            if (b >= 0 && o->start < ops[b].end - tol)
+                ov_emit(out, max_v, &nv, 5, s, 2, it, k, 0.0);
+        }
+    }
+    /* 4. iteration close per stage, iterations in first-appearance order */
+    uint32_t *its = (uint32_t *)malloc((n + 1) * sizeof(uint32_t));
+    for (int s = 0; s < S; ++s) {
+        uint64_t ni = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            if (ops[i].stage != s)
+                continue;
+            uint64_t q;
+            for (q = 0; q < ni; ++q)
+                if (its[q] == ops[i].iteration)
+                    break;
+            if (q == ni)
+                its[ni++] = ops[i].iteration;
+        }
+        for (uint64_t q = 0; q < ni; ++q) {
+            int n_sync = 0, n_opt = 0, have_w = 0;
+            int64_t sync = -1, opt = -1;
+            double last_w = 0.0;
+            for (uint64_t i = 0; i < n; ++i) {
+                const gp_op *o = &ops[i];
+                if (o->stage != s || o->iteration != its[q])
+                    continue;
+                if (o->kind == 3) { n_sync++; sync = (int64_t)i; }
+                if (o->kind == 4) { n_opt++; opt = (int64_t)i; }
+                if (o->kind == 2) {
+                    if (!have_w || o->end > last_w)
+                        last_w = o->end;
+                    have_w = 1;
+                }
+            }
+            if (n_sync != 1 || n_opt != 1) {
+                ov_emit(out, max_v, &nv, 6, s, 0, its[q], 0, 0.0);
+                continue;
+            }
+            if (ops[sync].start < last_w - tol)
+                ov_emit(out, max_v, &nv, 7, s, 0, its[q], 0, 0.0);
+            if (ops[opt].start < ops[sync].end - tol)
+                ov_emit(out, max_v, &nv, 8, s, 0, its[q], 0, 0.0);
+        }
+    }
+    /* bubble_fraction busy sums */
+    if (busy)
+        for (int s = 0; s < GP_MAX_STAGES; ++s) {
+            double f = 0.0, c = 0.0;
+            int64_t cnt = 0;
+            for (uint64_t i = 0; i < n && s < S; ++i) {
+                if (ops[i].stage != s)
+                    continue;
+                double x = ops[i].end - ops[i].start;
+                if (cnt++ == 0) {
+                    f = 0.0 + x;
+                } else {
+                    double t = f + x;
+                    if (fabs(f) >= fabs(x))
+                        c += (f - t) + x;
+                    else
+                        c += (x - t) + f;
+                    f = t;
+                }
+            }
+            busy[s] = (c != 0.0 && isfinite(c)) ? f + c : f;
+        }
+    *n_v = nv;
+    free(K);
+    free(ord);
+    free(its);
     return GP_OK;
 }

@@ -63,6 +63,13 @@ def lib():
         L.or_sim_report_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, C.c_int,
                                           P(abi.GpTrace), P(C.c_uint32), P(abi.GpSimOptions),
                                           P(abi.GpSimReport), P(C.c_double), P(C.c_uint8)]
+        L.or_sim_schedule_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, C.c_int,
+                                            P(abi.GpTrace), P(C.c_uint32), P(abi.GpSimOptions),
+                                            P(C.c_uint64), P(abi.GpOp), P(C.c_uint64),
+                                            P(abi.GpTransfer), P(C.c_uint8)]
+        L.or_validate_schedule.argtypes = [P(abi.GpTiming), P(abi.GpOp), C.c_uint64, C.c_double,
+                                           C.c_double, C.c_uint32, P(abi.GpViolation),
+                                           P(C.c_uint32), P(C.c_double)]
         L.or_group_hierarchy.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(C.c_double),
                                          C.c_double, C.c_double, P(C.c_uint16), P(C.c_uint16),
                                          P(C.c_uint32), P(C.c_uint32), P(C.c_double),
@@ -214,3 +221,40 @@ def group_hierarchy(pt, bw, pc, thr_net=0.3, thr_comp=0.3):
         return st, None
     return st, Hierarchy(fg_of, sg_of, fi[:nf.value].copy(), fc[:nf.value].copy(),
                          fb[:nf.value].copy(), sc[:ns.value].copy())
+
+
+def sim_schedules(packed_timings, n, policy, iterations=1, traces=None, trace_index=None,
+                  adapter=False, async_iterations=False, degrade=1.2, recover=1.05):
+    """(reports, op_offset, ops, xfer_offset, transfers, status): the full
+    schedules (PipeOp / TransferRecord records) of a batch of timings."""
+    reps, _, st = sim_reports(packed_timings, n, policy, iterations, traces, trace_index,
+                              adapter, async_iterations, degrade, recover)
+    nops = np.array([reps[i].n_ops for i in range(n)], dtype=np.uint64)
+    nxf = np.array([reps[i].n_transfers for i in range(n)], dtype=np.uint64)
+    ooff = np.zeros(n + 1, np.uint64); ooff[1:] = np.cumsum(nops)
+    xoff = np.zeros(n + 1, np.uint64); xoff[1:] = np.cumsum(nxf)
+    ops = (abi.GpOp * max(1, int(ooff[-1])))()
+    xfs = (abi.GpTransfer * max(1, int(xoff[-1])))()
+    opts = abi.GpSimOptions(int(bool(adapter)), int(bool(async_iterations)),
+                            float(degrade), float(recover))
+    ti = None
+    if trace_index is not None:
+        ti = np.ascontiguousarray(trace_index, dtype=np.uint32)
+    st2 = np.empty(n, dtype=np.uint8)
+    u64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))
+    lib().or_sim_schedule_batch(packed_timings, n, int(policy), int(iterations), traces,
+                                ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
+                                C.byref(opts), u64(ooff), ops, u64(xoff), xfs, _u8(st2))
+    return reps, ooff, ops, xoff, xfs, st2
+
+
+def validate_schedule(timing_struct, ops, n, makespan, tol=1e-9, max_violations=4096, first=0):
+    """(violation records, count, busy[16]) of one schedule: gp_op records
+    ops[first : first + n]."""
+    ops = C.cast(C.addressof(ops) + int(first) * C.sizeof(abi.GpOp), C.POINTER(abi.GpOp))
+    out = (abi.GpViolation * max_violations)()
+    nv = C.c_uint32(0)
+    busy = np.zeros(abi.GP_MAX_STAGES)
+    lib().or_validate_schedule(C.byref(timing_struct), ops, int(n), float(makespan), float(tol),
+                               max_violations, out, C.byref(nv), _dp(busy))
+    return [out[i] for i in range(min(nv.value, max_violations))], nv.value, busy

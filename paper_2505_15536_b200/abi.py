@@ -152,3 +152,30 @@ class GpSimReport(C.Structure):
         ("adapter_actions", C.c_uint32), ("n_ops", C.c_uint32),
         ("n_transfers", C.c_uint32), ("pad", C.c_uint32),
     ]
+
+
+class GpOp(C.Structure):
+    _fields_ = [
+        ("start", C.c_double), ("end", C.c_double), ("size", C.c_int32),
+        ("microbatch_id", C.c_int32), ("iteration", C.c_uint32),
+        ("kind", C.c_uint8), ("stage", C.c_uint8), ("pad", C.c_uint16),
+    ]
+
+
+class GpTransfer(C.Structure):
+    _fields_ = [
+        ("start", C.c_double), ("end", C.c_double), ("size", C.c_int32),
+        ("microbatch_id", C.c_int32), ("iteration", C.c_uint32),
+        ("boundary", C.c_uint8), ("direction", C.c_uint8), ("pad", C.c_uint16),
+    ]
+
+
+class GpViolation(C.Structure):
+    _fields_ = [
+        ("t", C.c_double), ("iteration", C.c_uint32), ("microbatch_id", C.c_int32),
+        ("code", C.c_uint8), ("stage", C.c_uint8), ("kind", C.c_uint8), ("pad", C.c_uint8),
+        ("pad2", C.c_uint32),
+    ]
+
+
+OP_KINDS = ("F", "B", "W", "S", "O")

@@ -33,6 +33,7 @@
 #include "k6_snapshots.cuh"
 #include "k5_sim.cuh"
 #include "k7_grouping.cuh"
+#include "k8_validate.cuh"
 
 // ----------------------------------------------------------------------------
 // context
@@ -1235,76 +1236,102 @@ int gp_simulate(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy
     return GP_OK;
 }
 
+// Shared set-up of the full simulator (K5 full): argument checks, timings /
+// traces H2D, queue-scratch sizing from the largest timing of the batch.
+struct SimPlan {
+    gp_sim_options opt;
+    int wcap, lcap, smax;
+    size_t nlinks, per;
+    uint64_t chunk;
+    gp_trace* d_tr;
+    uint32_t* d_ti;
+};
+
+static int sim_prepare(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy,
+                       uint32_t iterations, const gp_trace* traces, uint32_t n_traces,
+                       const uint32_t* trace_index, const gp_sim_options* opts, SimPlan& P) {
+    if (policy > GP_POLICY_ZB_COMPACT) return fail(GP_ERR_INPUT, "unknown policy %u", policy);
+    if (iterations < 1 || iterations > 0xffff) return fail(GP_ERR_INPUT, "iterations out of range");
+    if (traces && n_traces == 0) traces = nullptr;
+    { int st_ = check_traces(traces, n_traces, trace_index, n); if (st_ != GP_OK) return st_; }
+    P.opt = gp_sim_options{0u, 0u, 1.2, 1.05};
+    if (opts) P.opt = *opts;
+    long long bmax = 1;
+    P.smax = 1;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (timings[i].batch > bmax) bmax = timings[i].batch;
+        if ((int)timings[i].n_stages > P.smax && timings[i].n_stages <= GP_MAX_STAGES)
+            P.smax = (int)timings[i].n_stages;
+    }
+    if (bmax >= (1ll << 24) - 2) return fail(GP_ERR_INPUT, "batch %lld too large", bmax);
+    P.wcap = (int)bmax + 1;
+    P.lcap = (int)(2 * bmax + 2);
+    P.nlinks = (size_t)2 * (P.smax > 1 ? P.smax - 1 : 1);
+    P.per = (size_t)P.smax * SIMF_SLOTS * P.wcap * sizeof(uint32_t) + 8 +
+            P.nlinks * P.lcap * sizeof(unsigned long long) +
+            (size_t)P.smax * SIMF_SLOTS * sizeof(SimFPool) + P.nlinks * sizeof(AdWindow);
+    P.chunk = (uint64_t)((1ull << 30) / P.per);  // <= 1 GiB of queue scratch per launch
+    if (P.chunk < 1) P.chunk = 1;
+    if (P.chunk > n) P.chunk = n;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->s_tim.ensure(n));
+    CUDA_TRY(c->s_st.ensure(n));
+    CUDA_TRY(c->s_wq.ensure(P.chunk * (P.per / sizeof(uint32_t) + 1)));  // queues, pools, windows
+    CUDA_TRY(cudaMemcpyAsync(c->s_tim.p, timings, n * sizeof(gp_timing), cudaMemcpyHostToDevice, s));
+    P.d_tr = nullptr;
+    P.d_ti = nullptr;
+    if (traces) {
+        CUDA_TRY(c->s_traces.ensure(n_traces));
+        CUDA_TRY(cudaMemcpyAsync(c->s_traces.p, traces, n_traces * sizeof(gp_trace),
+                                 cudaMemcpyHostToDevice, s));
+        P.d_tr = c->s_traces.p;
+        if (trace_index) {
+            CUDA_TRY(c->s_tidx.ensure(n));
+            CUDA_TRY(cudaMemcpyAsync(c->s_tidx.p, trace_index, n * sizeof(uint32_t),
+                                     cudaMemcpyHostToDevice, s));
+            P.d_ti = c->s_tidx.p;
+        }
+    }
+    return GP_OK;
+}
+
+static SimScratch sim_scratch(gp_ctx* c, const SimPlan& P, uint64_t nc) {
+    SimScratch sc;
+    sc.n = (long long)nc;
+    sc.wcap = P.wcap;
+    sc.lcap = P.lcap;
+    sc.smax = P.smax;
+    sc.wq = c->s_wq.p;
+    // link FIFOs after the W queues, 8-byte aligned (wcap words per queue)
+    size_t wwords = (size_t)P.smax * SIMF_SLOTS * P.wcap * nc;
+    wwords = (wwords + 1) & ~(size_t)1;
+    sc.lq = reinterpret_cast<unsigned long long*>(c->s_wq.p + wwords);
+    sc.pools = reinterpret_cast<SimFPool*>(sc.lq + P.nlinks * P.lcap * nc);
+    sc.win = reinterpret_cast<AdWindow*>(sc.pools + (size_t)P.smax * SIMF_SLOTS * nc);
+    return sc;
+}
+
 int gp_simulate_report(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy,
                        uint32_t iterations, const gp_trace* traces, uint32_t n_traces,
                        const uint32_t* trace_index, const gp_sim_options* opts,
                        gp_sim_report* report, double* iteration_ends, uint8_t* status) {
     if (!c || !timings || !report || !status) return fail(GP_ERR_INPUT, "bad arguments");
-    if (policy > GP_POLICY_ZB_COMPACT) return fail(GP_ERR_INPUT, "unknown policy %u", policy);
-    if (iterations < 1 || iterations > 0xffff) return fail(GP_ERR_INPUT, "iterations out of range");
     if (n == 0) return GP_OK;
-    if (traces && n_traces == 0) traces = nullptr;
-    { int st_ = check_traces(traces, n_traces, trace_index, n); if (st_ != GP_OK) return st_; }
-    gp_sim_options opt{0u, 0u, 1.2, 1.05};
-    if (opts) opt = *opts;
-    // queue capacities from the largest timing of the batch
-    long long bmax = 1;
-    int smax = 1;
-    for (uint64_t i = 0; i < n; ++i) {
-        if (timings[i].batch > bmax) bmax = timings[i].batch;
-        if ((int)timings[i].n_stages > smax && timings[i].n_stages <= GP_MAX_STAGES)
-            smax = (int)timings[i].n_stages;
-    }
-    if (bmax > 0x7fffffffll / 2 - 2) return fail(GP_ERR_INPUT, "batch too large");
-    const int wcap = (int)bmax + 1, lcap = (int)(2 * bmax + 2);
-    const size_t nlinks = (size_t)2 * (smax > 1 ? smax - 1 : 1);
-    const size_t per = (size_t)smax * SIMF_SLOTS * wcap * sizeof(uint32_t) + 8 +
-                       nlinks * lcap * sizeof(unsigned long long) +
-                       (size_t)smax * SIMF_SLOTS * sizeof(SimFPool) + nlinks * sizeof(AdWindow);
-    uint64_t chunk = (uint64_t)((1ull << 30) / per);  // <= 1 GiB of queue scratch per launch
-    if (chunk < 1) chunk = 1;
-    if (chunk > n) chunk = n;
-    CUDA_TRY(cudaSetDevice(c->device));
+    SimPlan P;
+    { int st_ = sim_prepare(c, timings, n, policy, iterations, traces, n_traces, trace_index, opts, P);
+      if (st_ != GP_OK) return st_; }
     cudaStream_t s = c->stream;
-    CUDA_TRY(c->s_tim.ensure(n));
-    CUDA_TRY(c->s_st.ensure(n));
     CUDA_TRY(c->s_rep.ensure(n));
-    if (iteration_ends) CUDA_TRY(c->s_ends.ensure(n * (uint64_t)iterations));
-    CUDA_TRY(c->s_wq.ensure(chunk * (per / sizeof(uint32_t) + 1)));  // queues, pools, windows
-    CUDA_TRY(cudaMemcpyAsync(c->s_tim.p, timings, n * sizeof(gp_timing), cudaMemcpyHostToDevice, s));
-    if (iteration_ends)
+    if (iteration_ends) {
+        CUDA_TRY(c->s_ends.ensure(n * (uint64_t)iterations));
         CUDA_TRY(cudaMemsetAsync(c->s_ends.p, 0, n * (uint64_t)iterations * sizeof(double), s));
-    gp_trace* d_tr = nullptr;
-    uint32_t* d_ti = nullptr;
-    if (traces) {
-        CUDA_TRY(c->s_traces.ensure(n_traces));
-        CUDA_TRY(cudaMemcpyAsync(c->s_traces.p, traces, n_traces * sizeof(gp_trace),
-                                 cudaMemcpyHostToDevice, s));
-        d_tr = c->s_traces.p;
-        if (trace_index) {
-            CUDA_TRY(c->s_tidx.ensure(n));
-            CUDA_TRY(cudaMemcpyAsync(c->s_tidx.p, trace_index, n * sizeof(uint32_t),
-                                     cudaMemcpyHostToDevice, s));
-            d_ti = c->s_tidx.p;
-        }
     }
-    for (uint64_t i0 = 0; i0 < n; i0 += chunk) {
-        const uint64_t nc = (n - i0) < chunk ? (n - i0) : chunk;
-        SimScratch sc;
-        sc.n = (long long)nc;
-        sc.wcap = wcap;
-        sc.lcap = lcap;
-        sc.wq = c->s_wq.p;
-        // link FIFOs after the W queues, 8-byte aligned (wcap words per queue)
-        size_t wwords = (size_t)smax * SIMF_SLOTS * wcap * nc;
-        wwords = (wwords + 1) & ~(size_t)1;
-        sc.lq = reinterpret_cast<unsigned long long*>(c->s_wq.p + wwords);
-        sc.pools = reinterpret_cast<SimFPool*>(sc.lq + nlinks * lcap * nc);
-        sc.win = reinterpret_cast<AdWindow*>(sc.pools + (size_t)smax * SIMF_SLOTS * nc);
-        sc.smax = smax;
+    for (uint64_t i0 = 0; i0 < n; i0 += P.chunk) {
+        const uint64_t nc = (n - i0) < P.chunk ? (n - i0) : P.chunk;
         k5_sim_full<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
-            c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, d_tr,
-            d_ti ? d_ti + i0 : nullptr, opt, sc, c->s_rep.p + i0,
+            c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, P.d_tr,
+            P.d_ti ? P.d_ti + i0 : nullptr, P.opt, sim_scratch(c, P, nc), c->s_rep.p + i0,
             iteration_ends ? c->s_ends.p + i0 * iterations : nullptr, c->s_st.p + i0);
         CUDA_TRY(cudaGetLastError());
     }
@@ -1313,6 +1340,106 @@ int gp_simulate_report(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t
         CUDA_TRY(cudaMemcpyAsync(iteration_ends, c->s_ends.p, n * (uint64_t)iterations * sizeof(double),
                                  cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return GP_OK;
+}
+
+int gp_simulate_schedule(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy,
+                         uint32_t iterations, const gp_trace* traces, uint32_t n_traces,
+                         const uint32_t* trace_index, const gp_sim_options* opts,
+                         const uint64_t* op_offset, gp_op* ops, const uint64_t* xfer_offset,
+                         gp_transfer* transfers, uint8_t* status) {
+    if (!c || !timings || !op_offset || !ops || !status || (transfers && !xfer_offset))
+        return fail(GP_ERR_INPUT, "bad arguments");
+    if (n == 0) return GP_OK;
+    SimPlan P;
+    { int st_ = sim_prepare(c, timings, n, policy, iterations, traces, n_traces, trace_index, opts, P);
+      if (st_ != GP_OK) return st_; }
+    cudaStream_t s = c->stream;
+    const uint64_t n_ops = op_offset[n] - op_offset[0];
+    const uint64_t n_xf = transfers ? xfer_offset[n] - xfer_offset[0] : 0;
+    // one staging buffer: offsets (2 x (n+1) u64), ops, transfers
+    const size_t b_off = 2 * (n + 1) * 8, b_ops = ((n_ops * sizeof(gp_op)) + 255) & ~(size_t)255;
+    CUDA_TRY(c->g_buf.ensure(b_off + 256 + b_ops + n_xf * sizeof(gp_transfer) + 256));
+    uint8_t* base = c->g_buf.p;
+    unsigned long long* d_oo = reinterpret_cast<unsigned long long*>(base);
+    unsigned long long* d_xo = d_oo + (n + 1);
+    gp_op* d_ops = reinterpret_cast<gp_op*>(base + ((b_off + 255) & ~(size_t)255));
+    gp_transfer* d_xf = reinterpret_cast<gp_transfer*>(reinterpret_cast<uint8_t*>(d_ops) + b_ops);
+    // offsets relative to the first timing
+    std::vector<unsigned long long> h_off(2 * (n + 1));
+    for (uint64_t i = 0; i <= n; ++i) {
+        h_off[i] = op_offset[i] - op_offset[0];
+        h_off[n + 1 + i] = transfers ? xfer_offset[i] - xfer_offset[0] : 0;
+    }
+    CUDA_TRY(cudaMemcpyAsync(d_oo, h_off.data(), b_off, cudaMemcpyHostToDevice, s));
+    for (uint64_t i0 = 0; i0 < n; i0 += P.chunk) {
+        const uint64_t nc = (n - i0) < P.chunk ? (n - i0) : P.chunk;
+        k5_sim_schedule<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
+            c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, P.d_tr,
+            P.d_ti ? P.d_ti + i0 : nullptr, P.opt, sim_scratch(c, P, nc), d_oo + i0, d_ops,
+            d_xo + i0, transfers ? d_xf : nullptr, c->s_st.p + i0);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaMemcpyAsync(ops + op_offset[0], d_ops, n_ops * sizeof(gp_op), cudaMemcpyDeviceToHost, s));
+    if (transfers)
+        CUDA_TRY(cudaMemcpyAsync(transfers + xfer_offset[0], d_xf, n_xf * sizeof(gp_transfer),
+                                 cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return GP_OK;
+}
+
+int gp_validate_schedules(gp_ctx* c, const gp_timing* timings, uint64_t n,
+                          const uint64_t* op_offset, const gp_op* ops, const double* makespan,
+                          uint32_t iterations, double tol, uint32_t max_violations,
+                          gp_violation* violations, uint32_t* n_violations, double* busy,
+                          uint8_t* status) {
+    if (!c || !timings || !op_offset || !ops || !makespan || !n_violations || !status ||
+        (max_violations && !violations))
+        return fail(GP_ERR_INPUT, "bad arguments");
+    if (iterations < 1 || iterations > 0xffff) return fail(GP_ERR_INPUT, "iterations out of range");
+    if (n == 0) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    const uint64_t n_ops = op_offset[n] - op_offset[0];
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t nq = (size_t)GP_MAX_STAGES * iterations * 3;
+    const size_t o_tim = 0, o_off = o_tim + al(n * sizeof(gp_timing)), o_ms = o_off + al((n + 1) * 8);
+    const size_t o_ops = o_ms + al(n * 8), o_v = o_ops + al(n_ops * sizeof(gp_op));
+    const size_t o_nv = o_v + al(n * (size_t)max_violations * sizeof(gp_violation));
+    const size_t o_busy = o_nv + al(n * 4), o_st = o_busy + al(n * GP_MAX_STAGES * 8);
+    const size_t o_tab = o_st + al(n), o_idx = o_tab + al(n * nq * 2 * 4);
+    const size_t o_srt = o_idx + al(n_ops * 4), o_its = o_srt + al(n_ops * 4);
+    const size_t total = o_its + al(n * (size_t)GP_MAX_STAGES * iterations * sizeof(K8Iter));
+    CUDA_TRY(c->g_buf.ensure(total));
+    uint8_t* b = c->g_buf.p;
+    std::vector<unsigned long long> h_off(n + 1);
+    for (uint64_t i = 0; i <= n; ++i) h_off[i] = op_offset[i] - op_offset[0];
+    CUDA_TRY(cudaMemcpyAsync(b + o_tim, timings, n * sizeof(gp_timing), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(b + o_off, h_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(b + o_ms, makespan, n * 8, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(b + o_ops, ops + op_offset[0], n_ops * sizeof(gp_op),
+                             cudaMemcpyHostToDevice, s));
+    K8Scratch sc;
+    sc.tab = reinterpret_cast<uint32_t*>(b + o_tab);
+    sc.idx = reinterpret_cast<uint32_t*>(b + o_idx);
+    sc.sorted = reinterpret_cast<uint32_t*>(b + o_srt);
+    sc.its = reinterpret_cast<K8Iter*>(b + o_its);
+    k8_validate<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
+        reinterpret_cast<const gp_timing*>(b + o_tim), (long long)n,
+        reinterpret_cast<const unsigned long long*>(b + o_off), reinterpret_cast<const gp_op*>(b + o_ops),
+        reinterpret_cast<const double*>(b + o_ms), (int)iterations, tol, max_violations,
+        reinterpret_cast<gp_violation*>(b + o_v), reinterpret_cast<uint32_t*>(b + o_nv),
+        busy ? reinterpret_cast<double*>(b + o_busy) : nullptr, b + o_st, sc);
+    CUDA_TRY(cudaGetLastError());
+    if (max_violations)
+        CUDA_TRY(cudaMemcpyAsync(violations, b + o_v, n * (size_t)max_violations * sizeof(gp_violation),
+                                 cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(n_violations, b + o_nv, n * 4, cudaMemcpyDeviceToHost, s));
+    if (busy)
+        CUDA_TRY(cudaMemcpyAsync(busy, b + o_busy, n * GP_MAX_STAGES * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status, b + o_st, n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return GP_OK;
 }

@@ -326,13 +326,14 @@ struct SimFPool {
     long long fwd_avail, fwd_taken, fwd_done, bwd_avail, bwd_taken, bwd_done, w_done;
     int it_tag, wq_head, wq_tail;
     int flags;          // bit0 sync_done, bit1 opt_done, bit2 activated, bit3 first_bwd_done
+    int f_ids, b_ids;   // fwd_next_id / bwd_next_id (ops of a stage never overlap)
 };
 
 struct SimFEv {
     double t, t0;       // t0: start (op duration / transfer latency samples)
     unsigned long long seq;
-    int code;           // kind<<31 | s<<20 | op<<16 | slot<<14 ... iteration kept separately
-    int it;
+    int code;           // kind<<31 | s<<20 | op<<16
+    int it, mb;         // iteration, micro-batch id (-1: None)
     long long size;
 };
 
@@ -356,9 +357,12 @@ struct SimScratch {
 
 __device__ __forceinline__ long long ad_halve(long long v) { return v / 2 > 1 ? v / 2 : 1; }
 
+// Link FIFO entries pack iteration (16 bits), micro-batch id and size (24
+// bits each); the host bounds batch < 2^24 and iterations < 2^16.
 __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp_trace* trace,
                         const gp_sim_options& opt, SimScratch sc, long long tid,
-                        gp_sim_report* rep, double* iter_ends) {
+                        gp_sim_report* rep, double* iter_ends, gp_op* ops_out, long long op_cap,
+                        gp_transfer* xf_out, long long xf_cap) {
     const int S = (int)T.n_stages;
     if (S < 1 || S > GP_MAX_STAGES || iterations < 1 || T.microbatch <= 0) return GP_ERR_TIMING;
     const long long B = T.batch, m = T.microbatch;
@@ -376,6 +380,7 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
             p.w_done = 0;
             p.wq_head = p.wq_tail = 0;
             p.flags = 0;
+            p.f_ids = p.b_ids = 0;
             p.it_tag = it;
         }
         return p;
@@ -480,11 +485,17 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
         bn[s] = 0;
         activate(s, 0);
     }
-    auto push_op = [&](double tnow, double dur, int s, int k, int it, long long size) {
+    auto push_op = [&](double tnow, double dur, int s, int k, int it, long long size, int mb) {
         SimFEv& e = ev[nev++];
         e.t = tnow + dur; e.t0 = tnow; e.seq = seq++;
         e.code = (s << 20) | (k << 16);
-        e.it = it; e.size = size;
+        e.it = it; e.size = size; e.mb = mb;
+        if (ops_out && n_ops < op_cap) {  // ops[s].append(op) at start (src/engine.py:322-330)
+            gp_op o;
+            o.start = e.t0; o.end = e.t; o.size = (int32_t)size; o.microbatch_id = mb;
+            o.iteration = (uint32_t)it; o.kind = (uint8_t)k; o.stage = (uint8_t)s; o.pad = 0;
+            ops_out[n_ops] = o;
+        }
         ++n_ops;
     };
     auto try_start = [&](double tnow, int bnd, int dir) {  // src/engine.py:276-289
@@ -492,18 +503,19 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
         if (l_busy[l] || l_head[l] >= l_tail[l]) return;
         const unsigned long long v = lq_at(l, l_head[l]++);
         l_busy[l] = true;
-        const long long sz = (long long)(v & 0xffffffffull);
+        const long long sz = (long long)(v & 0xffffffull);
         const double per = dir == 0 ? T.act[bnd] : T.grad[bnd];
         SimFEv& e = ev[nev++];
         e.t = transfer_end(tnow, per * (double)sz, T.bw[bnd], T.lat[bnd], trace, bnd);
         e.t0 = tnow; e.seq = seq++;
         e.code = (int)(1u << 31) | (bnd << 20) | (dir << 16);
-        e.it = (int)(v >> 32); e.size = sz;
+        e.it = (int)(v >> 48); e.mb = (int)((v >> 24) & 0xffffffull); e.size = sz;
     };
-    auto enqueue = [&](double tnow, int bnd, int dir, long long size, int it) {
+    auto enqueue = [&](double tnow, int bnd, int dir, long long size, int it, int mb) {
         const int l = 2 * bnd + dir;
         if (l_tail[l] - l_head[l] >= sc.lcap) { overflow = true; return; }
-        lq_at(l, l_tail[l]++) = ((unsigned long long)(unsigned)it << 32) | (unsigned long long)size;
+        lq_at(l, l_tail[l]++) = ((unsigned long long)(unsigned)it << 48) |
+                                ((unsigned long long)(unsigned)mb << 24) | (unsigned long long)size;
         try_start(tnow, bnd, dir);
     };
     double now = 0.0;
@@ -532,22 +544,24 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
                         if (rem > 0 && nx.fwd_avail - nx.fwd_taken >= chunk) {
                             nx.fwd_taken += chunk;
                             busy[s] = true;
-                            push_op(now, T.fwd[s] * (double)chunk, s, 0, it + 1, chunk);
+                            push_op(now, T.fwd[s] * (double)chunk, s, 0, it + 1, chunk, nx.f_ids++);
                             progress = true;
                         }
                     }
                     continue;
                 }
                 double dur;
+                int mb = -1;
                 switch (k) {
-                    case 0: dur = T.fwd[s] * (double)best_sz; p.fwd_taken += best_sz; break;
-                    case 1: dur = T.bwd[s] * (double)best_sz; p.bwd_taken += best_sz; break;
-                    case 2: dur = T.wgt[s] * (double)best_sz; p.wq_head++; break;
+                    case 0: dur = T.fwd[s] * (double)best_sz; p.fwd_taken += best_sz; mb = p.f_ids++; break;
+                    case 1: dur = T.bwd[s] * (double)best_sz; p.bwd_taken += best_sz; mb = p.b_ids++; break;
+                    // W takes the queue head: the B of id wq_head (B ids are dense, FIFO)
+                    case 2: dur = T.wgt[s] * (double)best_sz; mb = p.wq_head++; break;
                     case 3: dur = T.sync[s]; break;
                     default: dur = T.opt[s]; break;
                 }
                 busy[s] = true;
-                push_op(now, dur, s, k, it, best_sz);
+                push_op(now, dur, s, k, it, best_sz, mb);
                 progress = true;
             }
         }
@@ -567,7 +581,7 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
             if (bn[s]++ == 0) bsum[s].start(x); else bsum[s].add(x);
             if (op == 0) {
                 p.fwd_done += e.size;
-                if (s < S - 1) enqueue(now, s, 0, e.size, it);
+                if (s < S - 1) enqueue(now, s, 0, e.size, it, e.mb);
                 const int ks = it_slot(it);
                 it_fwd[ks] += e.size;
                 if (adapter && it_fwd[ks] == (long long)S * B)
@@ -577,7 +591,7 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
                 if (p.wq_tail >= sc.wcap) { overflow = true; break; }
                 wq_at(s, it, p.wq_tail++) = (uint32_t)e.size;
                 if (!(p.flags & 8)) { p.flags |= 8; if (adapter) phase[s] = 1; }
-                if (s > 0) enqueue(now, s - 1, 1, e.size, it);
+                if (s > 0) enqueue(now, s - 1, 1, e.size, it, e.mb);
             } else if (op == 2) {
                 p.w_done += e.size;
             } else if (op == 3) {
@@ -593,12 +607,20 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
             l_busy[2 * sb + op] = false;
             if (op == 0) pool(sb + 1, it).fwd_avail += e.size;
             else pool(sb, it).bwd_avail += e.size;
+            if (xf_out && n_xfer < xf_cap) {  // transfers.append (src/engine.py:388-393)
+                gp_transfer x;
+                x.start = e.t0; x.end = now; x.size = (int32_t)e.size; x.microbatch_id = e.mb;
+                x.iteration = (uint32_t)it; x.boundary = (uint8_t)sb; x.direction = (uint8_t)op;
+                x.pad = 0;
+                xf_out[n_xfer] = x;
+            }
             ++n_xfer;
             if (adapter) on_transfer(sb, op, now - e.t0, e.size);
             try_start(now, sb, op);
         }
     }
     if (overflow) return GP_ERR_CUDA;  // capacity bound broken: never a silent result
+    if ((ops_out && n_ops != op_cap) || (xf_out && n_xfer != xf_cap)) return GP_ERR_INPUT;
     rep->makespan = now;
     for (int s = 0; s < GP_MAX_STAGES; ++s) rep->busy[s] = s < S && bn[s] ? bsum[s].value() : 0.0;
     rep->adapter_actions = actions;
@@ -619,7 +641,8 @@ __global__ void k5_sim_full(const gp_timing* __restrict__ T, long long n, int po
     const gp_trace* tr = traces ? traces + (tidx ? tidx[i] : 0u) : nullptr;
     gp_sim_report r;
     int st = sim_full(T[i], policy, iterations, tr, opt, sc, i, &r,
-                      iter_ends ? iter_ends + i * (long long)iterations : nullptr);
+                      iter_ends ? iter_ends + i * (long long)iterations : nullptr, nullptr, 0,
+                      nullptr, 0);
     if (st != GP_OK && st != GP_ERR_SCHEDULING) {
         r.makespan = NAN;
         for (int s = 0; s < GP_MAX_STAGES; ++s) r.busy[s] = 0.0;
@@ -627,5 +650,25 @@ __global__ void k5_sim_full(const gp_timing* __restrict__ T, long long n, int po
     }
     if (st == GP_ERR_SCHEDULING) r.makespan = NAN;
     rep[i] = r;
+    status[i] = (uint8_t)st;
+}
+
+// Schedules: as k5_sim_full, writing the op / transfer records of timing i
+// at its offsets (sized by a previous report pass).
+__global__ void k5_sim_schedule(const gp_timing* __restrict__ T, long long n, int policy,
+                                int iterations, const gp_trace* __restrict__ traces,
+                                const uint32_t* __restrict__ tidx, gp_sim_options opt, SimScratch sc,
+                                const unsigned long long* __restrict__ op_off, gp_op* __restrict__ ops,
+                                const unsigned long long* __restrict__ xf_off,
+                                gp_transfer* __restrict__ xfers, uint8_t* __restrict__ status) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const gp_trace* tr = traces ? traces + (tidx ? tidx[i] : 0u) : nullptr;
+    gp_sim_report r;
+    const long long o0 = (long long)op_off[i], o1 = (long long)op_off[i + 1];
+    long long x0 = 0, x1 = 0;
+    if (xfers) { x0 = (long long)xf_off[i]; x1 = (long long)xf_off[i + 1]; }
+    int st = sim_full(T[i], policy, iterations, tr, opt, sc, i, &r, nullptr, ops + o0, o1 - o0,
+                      xfers ? xfers + x0 : nullptr, x1 - x0);
     status[i] = (uint8_t)st;
 }

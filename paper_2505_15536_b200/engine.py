@@ -68,6 +68,13 @@ def lib():
         L.gp_simulate_report.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp,
                                          C.c_uint32, P(C.c_uint32), P(abi.GpSimOptions),
                                          P(abi.GpSimReport), P(C.c_double), u8p]
+        u64p = P(C.c_uint64)
+        L.gp_simulate_schedule.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp,
+                                           C.c_uint32, P(C.c_uint32), P(abi.GpSimOptions),
+                                           u64p, P(abi.GpOp), u64p, P(abi.GpTransfer), u8p]
+        L.gp_validate_schedules.argtypes = [vp, vp, C.c_uint64, u64p, P(abi.GpOp),
+                                            P(C.c_double), C.c_uint32, C.c_double, C.c_uint32,
+                                            P(abi.GpViolation), P(C.c_uint32), P(C.c_double), u8p]
         u16p = P(C.c_uint16)
         L.gp_group_snapshots.argtypes = [vp, C.c_uint32, C.c_uint32, P(C.c_double),
                                          P(C.c_double), P(C.c_double), C.c_double, C.c_double,
@@ -249,6 +256,48 @@ class Engine:
                 int(n_traces), ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
                 C.byref(opts), reps, ends.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
         return reps, ends, st
+
+    def simulate_schedule(self, packed_timings, n: int, policy: int, iterations: int,
+                          packed_traces, n_traces: int, trace_index, opts, op_offset, xfer_offset):
+        """(ops, transfers, status) for timings whose op / transfer counts
+        (a previous simulate_report) set the offsets."""
+        op_offset = np.ascontiguousarray(op_offset, dtype=np.uint64)
+        ops = (abi.GpOp * max(1, int(op_offset[-1])))()
+        xfs = None
+        if xfer_offset is not None:
+            xfer_offset = np.ascontiguousarray(xfer_offset, dtype=np.uint64)
+            xfs = (abi.GpTransfer * max(1, int(xfer_offset[-1])))()
+        st = np.empty(n, dtype=np.uint8)
+        ti = None
+        if trace_index is not None:
+            ti = np.ascontiguousarray(trace_index, dtype=np.uint32)
+        u64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))
+        if n:
+            _check(lib().gp_simulate_schedule(
+                self._h, C.cast(packed_timings, C.c_void_p), n, int(policy), int(iterations),
+                C.cast(packed_traces, C.c_void_p) if packed_traces is not None else None,
+                int(n_traces), ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
+                C.byref(opts), u64(op_offset), ops,
+                u64(xfer_offset) if xfs is not None else None, xfs, _u8(st)))
+        return ops, xfs, st
+
+    def validate_schedules(self, packed_timings, n: int, op_offset, ops, makespans,
+                           iterations: int, tol: float = 1e-9, max_violations: int = 64):
+        """(violations[n, max], counts, busy[n, 16], status) - K8."""
+        op_offset = np.ascontiguousarray(op_offset, dtype=np.uint64)
+        ms = np.ascontiguousarray(makespans, dtype=np.float64)
+        viol = (abi.GpViolation * max(1, n * max_violations))()
+        nv = np.zeros(n, np.uint32)
+        busy = np.zeros((n, abi.GP_MAX_STAGES))
+        st = np.empty(n, dtype=np.uint8)
+        if n:
+            _check(lib().gp_validate_schedules(
+                self._h, C.cast(packed_timings, C.c_void_p), n,
+                op_offset.ctypes.data_as(C.POINTER(C.c_uint64)), ops,
+                ms.ctypes.data_as(C.POINTER(C.c_double)), int(iterations), float(tol),
+                int(max_violations), viol, nv.ctypes.data_as(C.POINTER(C.c_uint32)),
+                busy.ctypes.data_as(C.POINTER(C.c_double)), _u8(st)))
+        return viol, nv, busy, st
 
     def group_snapshots(self, p_t, bandwidth, p_c, threshold_net=0.3, threshold_compute=0.3):
         """K7 grouping of ``p_t[n_snap, D, D]`` (rank order); returns the raw

@@ -361,6 +361,7 @@ def main():
     dump_sim_candidates()
     dump_snapshots()
     dump_grouping()
+    dump_schedules()
     dump_regroup_replan()
 
     for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
@@ -464,6 +465,57 @@ def dump_grouping():
         out[name] = rows
     G.save("grouping.json", out)
     print(f"grouping: {time.time() - t0:.1f}s", flush=True)
+
+
+def dump_schedules():
+    """Schedule digests (ops + transfers) of the sim_reports timings under
+    every policy / adapter / async combination, and validate_schedule
+    messages of seeded perturbations (tests/schedule_cases.py)."""
+    gp = geopipe()
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import schedule_cases as SC
+    from geopipe.timing import BoundaryTiming, StageTiming
+    from geopipe.engine import OpKind, PipeOp
+    from geopipe.schedule import Schedule
+    rep = G.load("sim_reports.json")
+    tims = []
+    for d in rep["timings"]:
+        st = tuple(StageTiming(f, b, w, sy, sy, op, 1.0) for f, b, w, sy, op in d["stages"])
+        bd = tuple(BoundaryTiming(f"{i}-{i + 1}", lat, bw, act, grad)
+                   for i, (lat, bw, act, grad) in enumerate(d["boundaries"]))
+        tims.append(gp.PlanTiming(st, bd, d["batch"], d["microbatch"]))
+    kinds = {k.value: k for k in OpKind}
+    out = {"digests": {}, "violations": {}}
+    t0 = time.time()
+    for ad in (0, 1):
+        for asy in (0, 1):
+            for pol in gp.Policy:
+                key = f"{ad}:{asy}:{pol.value}:3"
+                rows, viols = [], []
+                for i, t in enumerate(tims):
+                    tr = gp.NetworkTrace(breakpoints={k: tuple(tuple(p) for p in v)
+                                                      for k, v in rep["traces"][i].items()})
+                    try:
+                        r = gp.simulate_timing(t, pol, tr, adapter_enabled=bool(ad),
+                                               config=gp.SimConfig(iterations=3,
+                                                                   async_iterations=bool(asy)))
+                    except gp.SchedulingBugError:
+                        rows.append(None)
+                        viols.append(None)
+                        continue
+                    rows.append(SC.digest(r.schedule.ops, r.transfers))
+                    pert = SC.perturb(r.schedule.ops, 1000 * i + 7)
+                    sched = Schedule(
+                        ops=tuple(tuple(PipeOp(kinds[k], s_, a, b, z, it, mb)
+                                        for k, s_, a, b, z, it, mb in stage) for stage in pert),
+                        makespan=r.makespan, policy=pol, num_stages=t.num_stages,
+                        micro_count=t.batch // t.microbatch)
+                    msgs = gp.validate_schedule(sched, t)
+                    viols.append([len(msgs), SC.text_digest(msgs), msgs[:3]])
+                out["digests"][key] = rows
+                out["violations"][key] = viols
+    G.save("schedules.json", out)
+    print(f"schedules: {time.time() - t0:.1f}s", flush=True)
 
 
 def dump_regroup_replan():
