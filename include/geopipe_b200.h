@@ -213,6 +213,14 @@ typedef struct gp_transfer {
     uint16_t pad;
 } gp_transfer;
 
+/* One adapter resize (AdapterAction, src/adapter.py:116-124); signal 0
+ * "fill", 1 "drain", 2 "degraded", 3 "recovered". */
+typedef struct gp_action {
+    double t;
+    int32_t stage, old_size, new_size;
+    uint32_t signal;
+} gp_action;
+
 /* One validate_schedule violation (src/schedule.py:95-171); the message
  * text is formatted by the host from these fields.  Codes:
  * 0 op ends before it starts (stage, kind); 1 ops overlap (stage, t);
@@ -372,18 +380,21 @@ int gp_group_snapshots(gp_ctx *ctx, uint32_t D, uint32_t n_snap, const double *p
                        double *fg_min_bw, double *sg_capacity);
 
 /*
- * The schedules themselves (generate_schedule / SimReport.schedule and
- * .transfers): timing i writes its ops, in per-stage start order
- * interleaved by start, to ops[op_offset[i] ..] and its transfers, in
- * completion order, to transfers[xfer_offset[i] ..] (transfers / offsets
- * may be NULL).  Offsets come from gp_simulate_report's n_ops /
- * n_transfers; a timing whose counts disagree reports GP_ERR_INPUT.
+ * The schedules themselves (generate_schedule / SimReport.schedule,
+ * .transfers and .adapter_actions): timing i writes its ops, in per-stage
+ * start order interleaved by start, to ops[op_offset[i] ..], its transfers,
+ * in completion order, to transfers[xfer_offset[i] ..] and its adapter
+ * actions to actions[action_offset[i] ..] (transfers / actions and their
+ * offsets may be NULL).  Offsets come from gp_simulate_report's n_ops /
+ * n_transfers / adapter_actions; a timing whose counts disagree reports
+ * GP_ERR_INPUT.
  */
 int gp_simulate_schedule(gp_ctx *ctx, const gp_timing *timings, uint64_t n, uint32_t policy,
                          uint32_t iterations, const gp_trace *traces, uint32_t n_traces,
                          const uint32_t *trace_index, const gp_sim_options *opts,
                          const uint64_t *op_offset, gp_op *ops, const uint64_t *xfer_offset,
-                         gp_transfer *transfers, uint8_t *status);
+                         gp_transfer *transfers, const uint64_t *action_offset,
+                         gp_action *actions, uint8_t *status);
 
 /*
  * validate_schedule(schedule_i, timings[i], tol) and the per-stage busy sums
@@ -415,6 +426,17 @@ int gp_sim_1f1b_device(gp_ctx *ctx, const gp_timing *d_timings, uint64_t n,
 int gp_sim_candidates(gp_ctx *ctx, uint32_t k, uint64_t n, const uint8_t *order,
                       const uint8_t *counts, const uint8_t *bm, uint32_t iterations,
                       double opt_seconds, double *makespan, uint8_t *status);
+
+/*
+ * PlanTiming of explicit candidates (build_plan_timing(build_plan(...),
+ * topology, model, groups, opt_seconds), src/timing.py:176-231): timings[i]
+ * for the candidate's plan as _evaluate builds it (splits chosen by
+ * choose_intra_split).  status as _evaluate's errors; memory feasibility is
+ * not checked (build_plan_timing does not check it).
+ */
+int gp_plan_timing(gp_ctx *ctx, uint32_t k, uint64_t n, const uint8_t *order,
+                   const uint8_t *counts, const uint8_t *bm, double opt_seconds,
+                   gp_timing *timings, uint8_t *status);
 
 /*
  * Batched re-plan over bandwidth snapshots (kernel K6 + K3): for snapshot i,

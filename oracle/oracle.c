@@ -801,11 +801,22 @@ typedef struct {
     ad_window win[2 * GP_MAX_STAGES];
     double degrade, recover;
     uint32_t actions;           /* len(adapter.actions): _apply with a change */
+    gp_action *out;             /* optional action records */
 } ad_state;
 
-static void ad_apply(ad_state *A, int s, int64_t size)
+/* _apply (src/adapter.py:158-165); signal 0 fill, 1 drain, 2 degraded,
+ * 3 recovered */
+static void ad_apply(ad_state *A, double t, int s, int64_t size, int signal)
 {
     if (size != A->current[s]) {
+        if (A->out) {
+            gp_action *a = &A->out[A->actions];
+            a->t = t;
+            a->stage = s;
+            a->old_size = (int32_t)A->current[s];
+            a->new_size = (int32_t)size;
+            a->signal = (uint32_t)signal;
+        }
         A->actions++;
         A->current[s] = size;
     }
@@ -857,7 +868,7 @@ static int64_t ad_adjust(int64_t current, int64_t configured, int signal, int ph
     return current;
 }
 
-static void ad_iteration_start(ad_state *A, int S, int s)
+static void ad_iteration_start(ad_state *A, double t, int S, int s)
 {
     A->phase[s] = 0;
     int poor = 0;
@@ -865,10 +876,11 @@ static void ad_iteration_start(ad_state *A, int S, int s)
         for (int d = 0; d < 2; ++d)
             if (b >= 0 && b < S - 1 && A->win[2 * b + d].exists && A->win[2 * b + d].degraded)
                 poor = 1;
-    ad_apply(A, s, poor ? (A->configured / 2 > 1 ? A->configured / 2 : 1) : A->configured);
+    ad_apply(A, t, s, poor ? (A->configured / 2 > 1 ? A->configured / 2 : 1) : A->configured, 0);
 }
 
-static void ad_transfer_complete(ad_state *A, int boundary, int dir, double raw, int64_t size)
+static void ad_transfer_complete(ad_state *A, double t, int boundary, int dir, double raw,
+                                 int64_t size)
 {
     int producer = dir == 0 ? boundary : boundary + 1;
     ad_window *w = &A->win[2 * boundary + dir];
@@ -884,7 +896,7 @@ static void ad_transfer_complete(ad_state *A, int boundary, int dir, double raw,
     int64_t ns = ad_adjust(A->current[producer], A->configured, sig, A->phase[producer]);
     if (ns != A->current[producer]) {
         w->since = 0;
-        ad_apply(A, producer, ns);
+        ad_apply(A, t, producer, ns, sig == 1 ? 2 : 3);
     }
 }
 
@@ -983,12 +995,13 @@ static double transfer_end(double start, double bytes, double base_bw, double la
 
 int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
                 const gp_sim_options *opts, gp_sim_report *rep, double *iter_ends,
-                gp_op *ops_out, gp_transfer *xf_out, double *makespan_out);
+                gp_op *ops_out, gp_transfer *xf_out, gp_action *act_out, double *makespan_out);
 
 int or_sim(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
            double *makespan_out)
 {
-    return or_sim_full(T, policy, iterations, trace, NULL, NULL, NULL, NULL, NULL, makespan_out);
+    return or_sim_full(T, policy, iterations, trace, NULL, NULL, NULL, NULL, NULL, NULL,
+                       makespan_out);
 }
 
 int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
@@ -1001,7 +1014,7 @@ int or_sim_1f1b(const gp_timing *T, int iterations, double *makespan_out)
  * asynchronous iterations (:297-314); rep / iter_ends may be NULL. */
 int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *trace,
                 const gp_sim_options *opts, gp_sim_report *rep, double *iter_ends,
-                gp_op *ops_out, gp_transfer *xf_out, double *makespan_out)
+                gp_op *ops_out, gp_transfer *xf_out, gp_action *act_out, double *makespan_out)
 {
     const int S = (int)T->n_stages;
     if (S < 1 || S > GP_MAX_STAGES || iterations < 1)
@@ -1013,6 +1026,7 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
     ad_state A;
     memset(&A, 0, sizeof(A));
     A.configured = m;
+    A.out = act_out;
     A.degrade = opts ? opts->degrade_factor : 1.2;
     A.recover = opts ? opts->recover_factor : 1.05;
     double busy_f[GP_MAX_STAGES], busy_c[GP_MAX_STAGES];
@@ -1048,6 +1062,7 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
     (void)closed_cnt;
     sim_heap H = {NULL, 0, 0};
     uint64_t seq = 0;
+    double now = 0.0;
     /* activate (src/engine.py:259-267) */
 #define ACTIVATE(s_, it_)                                                                  \
     do {                                                                                   \
@@ -1057,7 +1072,7 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
             if ((s_) == 0)                                                                 \
                 q_->fwd_avail = B;                                                         \
             if (adapter)                                                                   \
-                ad_iteration_start(&A, S, (s_));                                           \
+                ad_iteration_start(&A, now, S, (s_));                                      \
         }                                                                                  \
     } while (0)
     for (int s = 0; s < S; ++s) {
@@ -1100,7 +1115,6 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
         }                                                                                  \
     } while (0)
 
-    double now = 0.0;
     int first = 1;
     for (;;) {
         /* dispatch(now) (src/engine.py:335-341) */
@@ -1248,7 +1262,7 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
                 if (adapter && it_fwd_done[it] == (int64_t)S * B)
                     for (int q = 0; q < S; ++q) {  /* on_drain: halve every stage once */
                         A.phase[q] = 2;
-                        ad_apply(&A, q, ad_adjust(A.current[q], A.configured, 0, 2));
+                        ad_apply(&A, now, q, ad_adjust(A.current[q], A.configured, 0, 2), 1);
                     }
             } else if (e.op == 1) {
                 p->bwd_done += e.size;
@@ -1302,7 +1316,7 @@ int or_sim_full(const gp_timing *T, int policy, int iterations, const gp_trace *
             }
             n_xfer++;
             if (adapter)
-                ad_transfer_complete(&A, bnd, dir, now - e.t0, e.size);
+                ad_transfer_complete(&A, now, bnd, dir, now - e.t0, e.size);
             TRY_START(now, bnd, dir);
         }
     }
@@ -1377,7 +1391,7 @@ int or_sim_report_batch(const gp_timing *T, uint64_t n, int policy, int iteratio
         const gp_trace *tr = traces ? &traces[trace_index ? trace_index[i] : 0] : NULL;
         int st = or_sim_full(&T[i], policy, iterations, tr, opts, &reports[i],
                              iter_ends ? iter_ends + i * (uint64_t)iterations : NULL, NULL, NULL,
-                             &ms);
+                             NULL, &ms);
         if (st != GP_OK)
             reports[i].makespan = NAN;
         status[i] = (uint8_t)st;
@@ -1726,7 +1740,8 @@ int or_group_hierarchy(int D, const double *pt, const double *bw, const double *
 int or_sim_schedule_batch(const gp_timing *T, uint64_t n, int policy, int iterations,
                           const gp_trace *traces, const uint32_t *trace_index,
                           const gp_sim_options *opts, const uint64_t *op_offset, gp_op *ops,
-                          const uint64_t *xf_offset, gp_transfer *xfers, uint8_t *status)
+                          const uint64_t *xf_offset, gp_transfer *xfers,
+                          const uint64_t *act_offset, gp_action *acts, uint8_t *status)
 {
     for (uint64_t i = 0; i < n; ++i) {
         double ms = NAN;
@@ -1734,7 +1749,7 @@ int or_sim_schedule_batch(const gp_timing *T, uint64_t n, int policy, int iterat
         const gp_trace *tr = traces ? &traces[trace_index ? trace_index[i] : 0] : NULL;
         status[i] = (uint8_t)or_sim_full(&T[i], policy, iterations, tr, opts, &rep, NULL,
                                          ops + op_offset[i], xfers ? xfers + xf_offset[i] : NULL,
-                                         &ms);
+                                         acts ? acts + act_offset[i] : NULL, &ms);
     }
     return GP_OK;
 }

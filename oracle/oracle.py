@@ -66,7 +66,8 @@ def lib():
         L.or_sim_schedule_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, C.c_int,
                                             P(abi.GpTrace), P(C.c_uint32), P(abi.GpSimOptions),
                                             P(C.c_uint64), P(abi.GpOp), P(C.c_uint64),
-                                            P(abi.GpTransfer), P(C.c_uint8)]
+                                            P(abi.GpTransfer), P(C.c_uint64), P(abi.GpAction),
+                                            P(C.c_uint8)]
         L.or_validate_schedule.argtypes = [P(abi.GpTiming), P(abi.GpOp), C.c_uint64, C.c_double,
                                            C.c_double, C.c_uint32, P(abi.GpViolation),
                                            P(C.c_uint32), P(C.c_double)]
@@ -225,8 +226,9 @@ def group_hierarchy(pt, bw, pc, thr_net=0.3, thr_comp=0.3):
 
 def sim_schedules(packed_timings, n, policy, iterations=1, traces=None, trace_index=None,
                   adapter=False, async_iterations=False, degrade=1.2, recover=1.05):
-    """(reports, op_offset, ops, xfer_offset, transfers, status): the full
-    schedules (PipeOp / TransferRecord records) of a batch of timings."""
+    """(reports, op_offset, ops, xfer_offset, transfers, status, action_offset,
+    actions): the full schedules (PipeOp / TransferRecord / AdapterAction
+    records) of a batch of timings."""
     reps, _, st = sim_reports(packed_timings, n, policy, iterations, traces, trace_index,
                               adapter, async_iterations, degrade, recover)
     nops = np.array([reps[i].n_ops for i in range(n)], dtype=np.uint64)
@@ -235,6 +237,9 @@ def sim_schedules(packed_timings, n, policy, iterations=1, traces=None, trace_in
     xoff = np.zeros(n + 1, np.uint64); xoff[1:] = np.cumsum(nxf)
     ops = (abi.GpOp * max(1, int(ooff[-1])))()
     xfs = (abi.GpTransfer * max(1, int(xoff[-1])))()
+    aoff = np.zeros(n + 1, np.uint64)
+    aoff[1:] = np.cumsum([reps[i].adapter_actions for i in range(n)])
+    acts = (abi.GpAction * max(1, int(aoff[-1])))()
     opts = abi.GpSimOptions(int(bool(adapter)), int(bool(async_iterations)),
                             float(degrade), float(recover))
     ti = None
@@ -244,8 +249,9 @@ def sim_schedules(packed_timings, n, policy, iterations=1, traces=None, trace_in
     u64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))
     lib().or_sim_schedule_batch(packed_timings, n, int(policy), int(iterations), traces,
                                 ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
-                                C.byref(opts), u64(ooff), ops, u64(xoff), xfs, _u8(st2))
-    return reps, ooff, ops, xoff, xfs, st2
+                                C.byref(opts), u64(ooff), ops, u64(xoff), xfs, u64(aoff), acts,
+                                _u8(st2))
+    return reps, ooff, ops, xoff, xfs, st2, aoff, acts
 
 
 def validate_schedule(timing_struct, ops, n, makespan, tol=1e-9, max_violations=4096, first=0):

@@ -170,6 +170,16 @@ class GpTransfer(C.Structure):
     ]
 
 
+class GpAction(C.Structure):
+    _fields_ = [
+        ("t", C.c_double), ("stage", C.c_int32), ("old_size", C.c_int32),
+        ("new_size", C.c_int32), ("signal", C.c_uint32),
+    ]
+
+
+ACTION_SIGNALS = ("fill", "drain", "degraded", "recovered")
+
+
 class GpViolation(C.Structure):
     _fields_ = [
         ("t", C.c_double), ("iteration", C.c_uint32), ("microbatch_id", C.c_int32),

@@ -1348,8 +1348,10 @@ int gp_simulate_schedule(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32
                          uint32_t iterations, const gp_trace* traces, uint32_t n_traces,
                          const uint32_t* trace_index, const gp_sim_options* opts,
                          const uint64_t* op_offset, gp_op* ops, const uint64_t* xfer_offset,
-                         gp_transfer* transfers, uint8_t* status) {
-    if (!c || !timings || !op_offset || !ops || !status || (transfers && !xfer_offset))
+                         gp_transfer* transfers, const uint64_t* action_offset, gp_action* actions,
+                         uint8_t* status) {
+    if (!c || !timings || !op_offset || !ops || !status || (transfers && !xfer_offset) ||
+        (actions && !action_offset))
         return fail(GP_ERR_INPUT, "bad arguments");
     if (n == 0) return GP_OK;
     SimPlan P;
@@ -1358,32 +1360,42 @@ int gp_simulate_schedule(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32
     cudaStream_t s = c->stream;
     const uint64_t n_ops = op_offset[n] - op_offset[0];
     const uint64_t n_xf = transfers ? xfer_offset[n] - xfer_offset[0] : 0;
-    // one staging buffer: offsets (2 x (n+1) u64), ops, transfers
-    const size_t b_off = 2 * (n + 1) * 8, b_ops = ((n_ops * sizeof(gp_op)) + 255) & ~(size_t)255;
-    CUDA_TRY(c->g_buf.ensure(b_off + 256 + b_ops + n_xf * sizeof(gp_transfer) + 256));
+    const uint64_t n_ac = actions ? action_offset[n] - action_offset[0] : 0;
+    // one staging buffer: offsets (3 x (n+1) u64), ops, transfers, actions
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b_off = al(3 * (n + 1) * 8), b_ops = al(n_ops * sizeof(gp_op));
+    const size_t b_xf = al(n_xf * sizeof(gp_transfer));
+    CUDA_TRY(c->g_buf.ensure(b_off + b_ops + b_xf + n_ac * sizeof(gp_action) + 256));
     uint8_t* base = c->g_buf.p;
     unsigned long long* d_oo = reinterpret_cast<unsigned long long*>(base);
     unsigned long long* d_xo = d_oo + (n + 1);
-    gp_op* d_ops = reinterpret_cast<gp_op*>(base + ((b_off + 255) & ~(size_t)255));
-    gp_transfer* d_xf = reinterpret_cast<gp_transfer*>(reinterpret_cast<uint8_t*>(d_ops) + b_ops);
+    unsigned long long* d_ao = d_xo + (n + 1);
+    gp_op* d_ops = reinterpret_cast<gp_op*>(base + b_off);
+    gp_transfer* d_xf = reinterpret_cast<gp_transfer*>(base + b_off + b_ops);
+    gp_action* d_ac = reinterpret_cast<gp_action*>(base + b_off + b_ops + b_xf);
     // offsets relative to the first timing
-    std::vector<unsigned long long> h_off(2 * (n + 1));
+    std::vector<unsigned long long> h_off(3 * (n + 1));
     for (uint64_t i = 0; i <= n; ++i) {
         h_off[i] = op_offset[i] - op_offset[0];
         h_off[n + 1 + i] = transfers ? xfer_offset[i] - xfer_offset[0] : 0;
+        h_off[2 * (n + 1) + i] = actions ? action_offset[i] - action_offset[0] : 0;
     }
-    CUDA_TRY(cudaMemcpyAsync(d_oo, h_off.data(), b_off, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(d_oo, h_off.data(), 3 * (n + 1) * 8, cudaMemcpyHostToDevice, s));
     for (uint64_t i0 = 0; i0 < n; i0 += P.chunk) {
         const uint64_t nc = (n - i0) < P.chunk ? (n - i0) : P.chunk;
         k5_sim_schedule<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
             c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, P.d_tr,
             P.d_ti ? P.d_ti + i0 : nullptr, P.opt, sim_scratch(c, P, nc), d_oo + i0, d_ops,
-            d_xo + i0, transfers ? d_xf : nullptr, c->s_st.p + i0);
+            d_xo + i0, transfers ? d_xf : nullptr, d_ao + i0, actions ? d_ac : nullptr,
+            c->s_st.p + i0);
         CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaMemcpyAsync(ops + op_offset[0], d_ops, n_ops * sizeof(gp_op), cudaMemcpyDeviceToHost, s));
     if (transfers)
         CUDA_TRY(cudaMemcpyAsync(transfers + xfer_offset[0], d_xf, n_xf * sizeof(gp_transfer),
+                                 cudaMemcpyDeviceToHost, s));
+    if (actions)
+        CUDA_TRY(cudaMemcpyAsync(actions + action_offset[0], d_ac, n_ac * sizeof(gp_action),
                                  cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1630,6 +1642,33 @@ int gp_sim_candidates(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* order,
                                                                  c->b_cost.p, c->b_status.p);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(makespan, c->b_cost.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status, c->b_status.p, n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return GP_OK;
+}
+
+int gp_plan_timing(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* order, const uint8_t* counts,
+                   const uint8_t* bm, double opt_seconds, gp_timing* timings, uint8_t* status) {
+    if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    if (k < 1 || k > GP_MAX_STAGES) return fail(GP_ERR_INPUT, "k=%u outside [1,%d]", k, GP_MAX_STAGES);
+    if (!order || !counts || !bm || !timings || !status) return fail(GP_ERR_INPUT, "bad arguments");
+    if (n == 0) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->b_order.ensure(n * k));
+    CUDA_TRY(c->b_counts.ensure(n * k));
+    CUDA_TRY(c->b_bm.ensure(n));
+    CUDA_TRY(c->b_status.ensure(n));
+    CUDA_TRY(c->s_tim.ensure(n));
+    CUDA_TRY(cudaMemcpyAsync(c->b_order.p, order, n * k, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->b_counts.p, counts, n * k, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->b_bm.p, bm, n, cudaMemcpyHostToDevice, s));
+    k5_plan_timing<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(c->view(), (int)k, (long long)n,
+                                                              c->b_order.p, c->b_counts.p,
+                                                              c->b_bm.p, opt_seconds, c->s_tim.p,
+                                                              c->b_status.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(timings, c->s_tim.p, n * sizeof(gp_timing), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->b_status.p, n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return GP_OK;

@@ -240,41 +240,43 @@ __device__ int sim_dev(const gp_timing& T, int policy, int iterations, const gp_
     return GP_OK;
 }
 
-// 1F1B makespan of explicit candidates: the PlanTiming of build_plan_timing
-// (src/timing.py:176-231) assembled from the stage / boundary tables.
-__global__ void k5_sim_candidates(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
-                                  const uint8_t* __restrict__ counts, const uint8_t* __restrict__ bm,
-                                  int iterations, double opt_seconds, double* __restrict__ makespan,
-                                  uint8_t* __restrict__ status) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ncand) return;
+// The PlanTiming of build_plan_timing (src/timing.py:176-231) for one
+// explicit candidate, assembled from the stage / boundary tables; returns the
+// _evaluate status (GP_ERR_NO_FEASIBLE for a memory-infeasible plan unless
+// `any_memory`: build_plan_timing itself does not check memory).
+__device__ int cand_timing(const DevInst& I, int k, const uint8_t* __restrict__ order,
+                           const uint8_t* __restrict__ counts, int b, double opt_seconds,
+                           bool any_memory, gp_timing& T) {
     uint8_t o[GP_MAX_STAGES];
     int p[GP_MAX_STAGES + 1];
     p[0] = 0;
     int st = GP_OK;
     unsigned seen = 0;
     for (int s = 0; s < k; ++s) {
-        o[s] = order[i * k + s];
-        int c = counts[i * k + s];
+        o[s] = order[s];
+        int c = counts[s];
         if (o[s] >= I.F || (seen >> o[s]) & 1u || c == 0) st = GP_ERR_INPUT;
         seen |= 1u << (o[s] & 31);
         p[s + 1] = p[s] + c;
     }
-    int b = bm[i];
     if (b >= I.nb * I.nm || p[k] > I.n) st = GP_ERR_INPUT;
-    int mi = b % I.nm;
+    const int mi = b % I.nm;
     if (st == GP_OK) {
         long long M = I.batch[b / I.nm] / I.micro[mi];
         EvalOut r = eval_tables(I, k, o, p, mi, M);  // feasibility + errors, as _evaluate
         st = r.status;
-        if (st == GP_OK && isinf(r.cost)) st = GP_ERR_NO_FEASIBLE;  // memory-infeasible plan
+        if (st == GP_OK && isinf(r.cost) && !any_memory) st = GP_ERR_NO_FEASIBLE;  // memory-infeasible
     }
-    if (st != GP_OK) { makespan[i] = NAN; status[i] = (uint8_t)st; return; }
+    if (st != GP_OK) return st;
     const size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
-    gp_timing T;
     T.n_stages = (uint32_t)k;
+    T.pad = 0;
     T.batch = I.batch[b / I.nm];
     T.microbatch = I.micro[mi];
+    for (int s = 0; s < GP_MAX_STAGES; ++s) {
+        T.fwd[s] = T.bwd[s] = T.wgt[s] = T.sync[s] = T.opt[s] = 0.0;
+        T.lat[s] = T.bw[s] = T.act[s] = T.grad[s] = 0.0;
+    }
     for (int s = 0; s < k; ++s) {
         double4 v = I.fbws[(size_t)o[s] * N2 + tri_idx(I.n, p[s], p[s + 1])];
         T.fwd[s] = v.x; T.bwd[s] = v.y; T.wgt[s] = v.z; T.sync[s] = v.w; T.opt[s] = opt_seconds;
@@ -285,9 +287,35 @@ __global__ void k5_sim_candidates(DevInst I, int k, long long ncand, const uint8
             T.act[s] = T.grad[s] = I.act[p[s + 1] - 1];
         }
     }
+    return GP_OK;
+}
+
+// 1F1B makespan of explicit candidates.
+__global__ void k5_sim_candidates(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
+                                  const uint8_t* __restrict__ counts, const uint8_t* __restrict__ bm,
+                                  int iterations, double opt_seconds, double* __restrict__ makespan,
+                                  uint8_t* __restrict__ status) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncand) return;
+    gp_timing T;
+    int st = cand_timing(I, k, order + i * k, counts + i * k, bm[i], opt_seconds, false, T);
+    if (st != GP_OK) { makespan[i] = NAN; status[i] = (uint8_t)st; return; }
     double ms = NAN;
     st = sim_dev(T, GP_POLICY_1F1B, iterations, nullptr, &ms);
     makespan[i] = ms;
+    status[i] = (uint8_t)st;
+}
+
+// PlanTiming records of explicit candidates (for the full simulator).
+__global__ void k5_plan_timing(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
+                               const uint8_t* __restrict__ counts, const uint8_t* __restrict__ bm,
+                               double opt_seconds, gp_timing* __restrict__ out,
+                               uint8_t* __restrict__ status) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncand) return;
+    gp_timing T;
+    int st = cand_timing(I, k, order + i * k, counts + i * k, bm[i], opt_seconds, true, T);
+    if (st == GP_OK) out[i] = T;
     status[i] = (uint8_t)st;
 }
 
@@ -362,7 +390,8 @@ __device__ __forceinline__ long long ad_halve(long long v) { return v / 2 > 1 ? 
 __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp_trace* trace,
                         const gp_sim_options& opt, SimScratch sc, long long tid,
                         gp_sim_report* rep, double* iter_ends, gp_op* ops_out, long long op_cap,
-                        gp_transfer* xf_out, long long xf_cap) {
+                        gp_transfer* xf_out, long long xf_cap, gp_action* act_out,
+                        long long act_cap) {
     const int S = (int)T.n_stages;
     if (S < 1 || S > GP_MAX_STAGES || iterations < 1 || T.microbatch <= 0) return GP_ERR_TIMING;
     const long long B = T.batch, m = T.microbatch;
@@ -415,8 +444,19 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
         W[l].head = W[l].len = 0; W[l].baseline = 0.0; W[l].count = W[l].since = 0;
         W[l].degraded = W[l].exists = 0;
     }
-    auto ad_apply = [&](int s, long long size) {
-        if (size != cur_sz[s]) { ++actions; cur_sz[s] = size; }
+    double now = 0.0;
+    // _apply (src/adapter.py:158-165); signal 0 fill, 1 drain, 2 degraded, 3 recovered
+    auto ad_apply = [&](int s, long long size, int signal) {
+        if (size != cur_sz[s]) {
+            if (act_out && actions < act_cap) {
+                gp_action a;
+                a.t = now; a.stage = s; a.old_size = (int32_t)cur_sz[s];
+                a.new_size = (int32_t)size; a.signal = (uint32_t)signal;
+                act_out[actions] = a;
+            }
+            ++actions;
+            cur_sz[s] = size;
+        }
     };
     auto activate = [&](int s, int it) {  // src/engine.py:259-267
         SimFPool& q = pool(s, it);
@@ -429,7 +469,7 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
             for (int b = s - 1; b <= s; ++b)
                 for (int d = 0; d < 2; ++d)
                     if (b >= 0 && b < S - 1 && W[2 * b + d].exists && W[2 * b + d].degraded) poor = true;
-            ad_apply(s, poor ? ad_halve(m) : m);
+            ad_apply(s, poor ? ad_halve(m) : m, 0);
         }
     };
     auto on_transfer = [&](int bnd, int dir, double raw, long long size) {
@@ -463,7 +503,7 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
         long long ns = c;
         if (phase[producer] == 2 || sig == 1) ns = ad_halve(c);
         else ns = c * 2 < m ? c * 2 : m;
-        if (ns != c) { w.since = 0; ad_apply(producer, ns); }
+        if (ns != c) { w.since = 0; ad_apply(producer, ns, sig == 1 ? 2 : 3); }
     };
 
     int cur[GP_MAX_STAGES];
@@ -518,7 +558,6 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
                                 ((unsigned long long)(unsigned)mb << 24) | (unsigned long long)size;
         try_start(tnow, bnd, dir);
     };
-    double now = 0.0;
     while (!overflow) {
         bool progress = true;
         while (progress) {  // dispatch (src/engine.py:335-341)
@@ -585,7 +624,7 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
                 const int ks = it_slot(it);
                 it_fwd[ks] += e.size;
                 if (adapter && it_fwd[ks] == (long long)S * B)
-                    for (int q = 0; q < S; ++q) { phase[q] = 2; ad_apply(q, ad_halve(cur_sz[q])); }
+                    for (int q = 0; q < S; ++q) { phase[q] = 2; ad_apply(q, ad_halve(cur_sz[q]), 1); }
             } else if (op == 1) {
                 p.bwd_done += e.size;
                 if (p.wq_tail >= sc.wcap) { overflow = true; break; }
@@ -620,7 +659,9 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
         }
     }
     if (overflow) return GP_ERR_CUDA;  // capacity bound broken: never a silent result
-    if ((ops_out && n_ops != op_cap) || (xf_out && n_xfer != xf_cap)) return GP_ERR_INPUT;
+    if ((ops_out && n_ops != op_cap) || (xf_out && n_xfer != xf_cap) ||
+        (act_out && (long long)actions != act_cap))
+        return GP_ERR_INPUT;
     rep->makespan = now;
     for (int s = 0; s < GP_MAX_STAGES; ++s) rep->busy[s] = s < S && bn[s] ? bsum[s].value() : 0.0;
     rep->adapter_actions = actions;
@@ -642,7 +683,7 @@ __global__ void k5_sim_full(const gp_timing* __restrict__ T, long long n, int po
     gp_sim_report r;
     int st = sim_full(T[i], policy, iterations, tr, opt, sc, i, &r,
                       iter_ends ? iter_ends + i * (long long)iterations : nullptr, nullptr, 0,
-                      nullptr, 0);
+                      nullptr, 0, nullptr, 0);
     if (st != GP_OK && st != GP_ERR_SCHEDULING) {
         r.makespan = NAN;
         for (int s = 0; s < GP_MAX_STAGES; ++s) r.busy[s] = 0.0;
@@ -660,7 +701,9 @@ __global__ void k5_sim_schedule(const gp_timing* __restrict__ T, long long n, in
                                 const uint32_t* __restrict__ tidx, gp_sim_options opt, SimScratch sc,
                                 const unsigned long long* __restrict__ op_off, gp_op* __restrict__ ops,
                                 const unsigned long long* __restrict__ xf_off,
-                                gp_transfer* __restrict__ xfers, uint8_t* __restrict__ status) {
+                                gp_transfer* __restrict__ xfers,
+                                const unsigned long long* __restrict__ ac_off,
+                                gp_action* __restrict__ acts, uint8_t* __restrict__ status) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const gp_trace* tr = traces ? traces + (tidx ? tidx[i] : 0u) : nullptr;
@@ -668,7 +711,9 @@ __global__ void k5_sim_schedule(const gp_timing* __restrict__ T, long long n, in
     const long long o0 = (long long)op_off[i], o1 = (long long)op_off[i + 1];
     long long x0 = 0, x1 = 0;
     if (xfers) { x0 = (long long)xf_off[i]; x1 = (long long)xf_off[i + 1]; }
+    long long a0 = 0, a1 = 0;
+    if (acts) { a0 = (long long)ac_off[i]; a1 = (long long)ac_off[i + 1]; }
     int st = sim_full(T[i], policy, iterations, tr, opt, sc, i, &r, nullptr, ops + o0, o1 - o0,
-                      xfers ? xfers + x0 : nullptr, x1 - x0);
+                      xfers ? xfers + x0 : nullptr, x1 - x0, acts ? acts + a0 : nullptr, a1 - a0);
     status[i] = (uint8_t)st;
 }

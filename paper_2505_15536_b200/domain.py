@@ -69,6 +69,23 @@ class EmptyClusterError(GeopipeError):
     """Grouping was asked to run on a topology with no devices."""
 
 
+class InvalidMeasurementError(GeopipeError):
+    """A link measurement violates its invariants (src/errors.py:8-9)."""
+
+
+class InvalidBenchmarkError(GeopipeError):
+    """A compute benchmark list is empty or has non-positive times."""
+
+
+class IncompleteTopologyError(GeopipeError):
+    """The link matrix is missing pairs or contains duplicates."""
+
+    def __init__(self, message, missing=(), duplicates=()):
+        super().__init__(message)
+        self.missing = list(missing)
+        self.duplicates = list(duplicates)
+
+
 class SchedulingBugError(GeopipeError):
     """The 1F1B event loop stalled (src/errors.py:57-62)."""
 
@@ -89,11 +106,11 @@ class LayerSpec:
     activation_out_bytes: float
     param_bytes: float
 
-    def __post_init__(self):
-        for v in (self.fwd_flops, self.bwd_input_flops, self.bwd_weight_flops,
-                  self.activation_out_bytes, self.param_bytes):
-            if not v > 0:
-                raise InputFileError("layer fields must be positive")
+    def __post_init__(self):  # src/plans.py:22-26
+        for name in ("fwd_flops", "bwd_input_flops", "bwd_weight_flops",
+                     "activation_out_bytes", "param_bytes"):
+            if getattr(self, name) <= 0:
+                raise InputFileError(f"layer field {name} must be positive")
 
     @property
     def total_flops(self) -> float:
@@ -107,14 +124,17 @@ class ModelSpec:
     global_batch_candidates: Tuple[int, ...] = (128, 256)
     microbatch_candidates: Tuple[int, ...] = (8, 16, 32)
 
-    def __post_init__(self):
+    def __post_init__(self):  # src/plans.py:41-53
         if not self.layers:
             raise InputFileError("model has no layers")
         for b in self.global_batch_candidates:
+            if b <= 0:
+                raise InputFileError("batch candidates must be positive")
             for m in self.microbatch_candidates:
-                if b <= 0 or m <= 0 or b % m:
-                    raise InputFileError(
-                        f"micro-batch {m} must be positive and divide batch {b}")
+                if m <= 0:
+                    raise InputFileError("micro-batch candidates must be positive")
+                if b % m != 0:
+                    raise InputFileError(f"micro-batch {m} does not divide batch {b}")
 
     @property
     def num_layers(self) -> int:
@@ -151,6 +171,21 @@ class ParallelPlan:
     stages: Tuple[StageAssignment, ...]
     batch_b: int
     microbatch_m: int
+
+    def __post_init__(self):  # src/plans.py:106-122
+        if self.batch_b <= 0 or self.microbatch_m <= 0:
+            raise InputFileError("batch and micro-batch must be positive")
+        if self.batch_b % self.microbatch_m != 0:
+            raise InputFileError(
+                f"micro-batch {self.microbatch_m} does not divide batch {self.batch_b}")
+        fgs = [s.fg_id for s in self.stages]
+        if len(set(fgs)) != len(fgs):
+            raise InputFileError("stage order must use distinct first-level groups")
+        pos = 0
+        for s in self.stages:
+            if s.layer_start != pos or s.layer_end <= s.layer_start:
+                raise InputFileError("stage layer ranges must tile the layer list without gaps")
+            pos = s.layer_end
 
     @property
     def micro_count(self) -> int:

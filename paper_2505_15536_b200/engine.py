@@ -71,7 +71,8 @@ def lib():
         u64p = P(C.c_uint64)
         L.gp_simulate_schedule.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, vp,
                                            C.c_uint32, P(C.c_uint32), P(abi.GpSimOptions),
-                                           u64p, P(abi.GpOp), u64p, P(abi.GpTransfer), u8p]
+                                           u64p, P(abi.GpOp), u64p, P(abi.GpTransfer), u64p,
+                                           P(abi.GpAction), u8p]
         L.gp_validate_schedules.argtypes = [vp, vp, C.c_uint64, u64p, P(abi.GpOp),
                                             P(C.c_double), C.c_uint32, C.c_double, C.c_uint32,
                                             P(abi.GpViolation), P(C.c_uint32), P(C.c_double), u8p]
@@ -85,6 +86,8 @@ def lib():
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
+        L.gp_plan_timing.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_double,
+                                     P(abi.GpTiming), u8p]
         _lib = L
         return L
 
@@ -258,15 +261,20 @@ class Engine:
         return reps, ends, st
 
     def simulate_schedule(self, packed_timings, n: int, policy: int, iterations: int,
-                          packed_traces, n_traces: int, trace_index, opts, op_offset, xfer_offset):
-        """(ops, transfers, status) for timings whose op / transfer counts
-        (a previous simulate_report) set the offsets."""
+                          packed_traces, n_traces: int, trace_index, opts, op_offset, xfer_offset,
+                          action_offset=None):
+        """(ops, transfers, actions, status) for timings whose op / transfer /
+        action counts (a previous simulate_report) set the offsets."""
         op_offset = np.ascontiguousarray(op_offset, dtype=np.uint64)
         ops = (abi.GpOp * max(1, int(op_offset[-1])))()
         xfs = None
         if xfer_offset is not None:
             xfer_offset = np.ascontiguousarray(xfer_offset, dtype=np.uint64)
             xfs = (abi.GpTransfer * max(1, int(xfer_offset[-1])))()
+        acts = None
+        if action_offset is not None:
+            action_offset = np.ascontiguousarray(action_offset, dtype=np.uint64)
+            acts = (abi.GpAction * max(1, int(action_offset[-1])))()
         st = np.empty(n, dtype=np.uint8)
         ti = None
         if trace_index is not None:
@@ -278,8 +286,9 @@ class Engine:
                 C.cast(packed_traces, C.c_void_p) if packed_traces is not None else None,
                 int(n_traces), ti.ctypes.data_as(C.POINTER(C.c_uint32)) if ti is not None else None,
                 C.byref(opts), u64(op_offset), ops,
-                u64(xfer_offset) if xfs is not None else None, xfs, _u8(st)))
-        return ops, xfs, st
+                u64(xfer_offset) if xfs is not None else None, xfs,
+                u64(action_offset) if acts is not None else None, acts, _u8(st)))
+        return ops, xfs, acts, st
 
     def validate_schedules(self, packed_timings, n: int, op_offset, ops, makespans,
                            iterations: int, tol: float = 1e-9, max_violations: int = 64):
@@ -322,6 +331,19 @@ class Engine:
                                         u16(fg_of), u16(sg_of), u32(nf), u32(nsg), dp(fi), dp(fc),
                                         dp(fb), dp(sc)))
         return fg_of, sg_of, nf, nsg, fi, fc, fb, sc
+
+    def plan_timing(self, order, counts, bm, opt_seconds: float = 0.0):
+        """(gp_timing array, status) of explicit candidates of the loaded instance."""
+        order = np.ascontiguousarray(order, dtype=np.uint8)
+        counts = np.ascontiguousarray(counts, dtype=np.uint8)
+        bm = np.ascontiguousarray(bm, dtype=np.uint8)
+        n, k = order.shape
+        out = (abi.GpTiming * max(1, n))()
+        st = np.empty(n, dtype=np.uint8)
+        if n:
+            _check(lib().gp_plan_timing(self._h, k, n, _u8(order), _u8(counts), _u8(bm),
+                                        float(opt_seconds), out, _u8(st)))
+        return out, st
 
     def sim_candidates(self, order, counts, bm, iterations: int = 1, opt_seconds: float = 0.0):
         """1F1B makespans of explicit candidates of the loaded instance."""

@@ -60,6 +60,15 @@ class TransferRecord:
 
 
 @dataclass(frozen=True)
+class AdapterAction:
+    t: float
+    stage: int
+    old_size: int
+    new_size: int
+    signal: str
+
+
+@dataclass(frozen=True)
 class Schedule:
     ops: Tuple[Tuple[PipeOp, ...], ...]
     makespan: float
@@ -72,9 +81,11 @@ class Schedule:
 
 
 def generate_schedules(timings: Sequence, policy="1f1b", traces: Sequence = (), trace_index=None,
-                       adapter_enabled: bool = False, config=None, engine=None):
-    """(Schedule, transfers) per timing: ``simulate_timing(...).schedule`` and
-    ``.transfers`` of the reference, computed on the GPU."""
+                       adapter_enabled: bool = False, config=None, engine=None,
+                       with_actions: bool = False):
+    """(Schedule, transfers[, adapter actions]) per timing:
+    ``simulate_timing(...).schedule`` / ``.transfers`` / ``.adapter_actions``
+    of the reference, computed on the GPU."""
     from .engine import default_engine
     eng = engine if engine is not None else default_engine()
     config = config if config is not None else SimConfig()
@@ -95,13 +106,21 @@ def generate_schedules(timings: Sequence, policy="1f1b", traces: Sequence = (), 
     ooff[1:] = np.cumsum([reps[i].n_ops for i in range(n)])
     xoff = np.zeros(n + 1, np.uint64)
     xoff[1:] = np.cumsum([reps[i].n_transfers for i in range(n)])
+    aoff = np.zeros(n + 1, np.uint64)
+    aoff[1:] = np.cumsum([reps[i].adapter_actions for i in range(n)])
     opts = abi.GpSimOptions(int(bool(adapter_enabled)), int(asy), float(deg), float(rec))
-    ops, xfs, st = eng.simulate_schedule(arr, n, code, its, tr, len(traces), trace_index, opts,
-                                         ooff, xoff)
+    ops, xfs, acts, st = eng.simulate_schedule(arr, n, code, its, tr, len(traces), trace_index,
+                                               opts, ooff, xoff, aoff)
     _raise(st)
-    return [records_to_schedule(t, ops, int(ooff[i]), int(ooff[i + 1]), xfs, int(xoff[i]),
-                                int(xoff[i + 1]), float(reps[i].makespan), pol)
-            for i, t in enumerate(timings)]
+    out = []
+    for i, t in enumerate(timings):
+        sched, xf = records_to_schedule(t, ops, int(ooff[i]), int(ooff[i + 1]), xfs, int(xoff[i]),
+                                        int(xoff[i + 1]), float(reps[i].makespan), pol)
+        actions = tuple(AdapterAction(a.t, a.stage, a.old_size, a.new_size,
+                                      abi.ACTION_SIGNALS[a.signal])
+                        for a in (acts[j] for j in range(int(aoff[i]), int(aoff[i + 1]))))
+        out.append((sched, xf) if not with_actions else (sched, xf, actions))
+    return out
 
 
 def records_to_schedule(timing, ops, o0, o1, xfs, x0, x1, makespan, policy):

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import argparse
 import itertools
+import json
 import logging
 import os
 import random
@@ -362,6 +363,7 @@ def main():
     dump_snapshots()
     dump_grouping()
     dump_schedules()
+    dump_cli()
     dump_regroup_replan()
 
     for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
@@ -485,13 +487,13 @@ def dump_schedules():
                    for i, (lat, bw, act, grad) in enumerate(d["boundaries"]))
         tims.append(gp.PlanTiming(st, bd, d["batch"], d["microbatch"]))
     kinds = {k.value: k for k in OpKind}
-    out = {"digests": {}, "violations": {}}
+    out = {"digests": {}, "violations": {}, "actions": {}}
     t0 = time.time()
     for ad in (0, 1):
         for asy in (0, 1):
             for pol in gp.Policy:
                 key = f"{ad}:{asy}:{pol.value}:3"
-                rows, viols = [], []
+                rows, viols, acts = [], [], []
                 for i, t in enumerate(tims):
                     tr = gp.NetworkTrace(breakpoints={k: tuple(tuple(p) for p in v)
                                                       for k, v in rep["traces"][i].items()})
@@ -502,8 +504,10 @@ def dump_schedules():
                     except gp.SchedulingBugError:
                         rows.append(None)
                         viols.append(None)
+                        acts.append(None)
                         continue
                     rows.append(SC.digest(r.schedule.ops, r.transfers))
+                    acts.append(SC.action_digest(r.adapter_actions))
                     pert = SC.perturb(r.schedule.ops, 1000 * i + 7)
                     sched = Schedule(
                         ops=tuple(tuple(PipeOp(kinds[k], s_, a, b, z, it, mb)
@@ -514,8 +518,101 @@ def dump_schedules():
                     viols.append([len(msgs), SC.text_digest(msgs), msgs[:3]])
                 out["digests"][key] = rows
                 out["violations"][key] = viols
+                out["actions"][key] = acts
     G.save("schedules.json", out)
     print(f"schedules: {time.time() - t0:.1f}s", flush=True)
+
+
+def _cli_inputs(d):
+    """cluster / model / trace files for the CLI goldens (tests/golden/cli)."""
+    import itertools as it
+    os.makedirs(d, exist_ok=True)
+    files = {}
+
+    def cluster_doc(pcs_by_clique, intra=0.01, cross=1.0, memory=1e15, bandwidth=1e8,
+                    latency=0.001):  # the reference's tests/test_cli.py fixture shape
+        devices, links, clique_of = [], [], {}
+        for c, pcs in enumerate(pcs_by_clique):
+            for k, p_c in enumerate(pcs):
+                did = f"c{c}d{k}"
+                clique_of[did] = c
+                devices.append({"id": did, "memory_bytes": memory,
+                                "benchmarks": [{"task": "bench", "seconds": 1.0 / p_c}]})
+        ids = [x["id"] for x in devices]
+        for a, b in it.combinations(ids, 2):
+            p_t = intra if clique_of[a] == clique_of[b] else cross
+            links.append({"a": a, "b": b, "alpha_s": p_t, "beta_s": 1e-3, "payload_bytes": 1e6,
+                          "latency_s": latency, "bandwidth_Bps": bandwidth})
+        return {"schema": "cluster/v1", "devices": devices, "links": links}
+
+    def model_doc(layers=6, batches=(8,), micros=(2, 4)):
+        return {"schema": "model/v1",
+                "layers": [{"fwd_flops": 8.0, "activation_out_bytes": 1e5, "param_bytes": 1e6}
+                           for _ in range(layers)],
+                "global_batch_candidates": list(batches), "microbatch_candidates": list(micros)}
+
+    def inst_docs(name):
+        spec = I.config(name, True)
+        devices = [{"id": i, "memory_bytes": mem, "region": f"r{r}",
+                    "benchmarks": [{"task": "bench", "seconds": 1.0 / p_c}]}
+                   for i, r, _, p_c, mem in spec.devices()]
+        links = [{"a": u, "b": v, "alpha_s": I.LINK_PAYLOAD_M / bw, "beta_s": lat,
+                  "payload_bytes": I.LINK_PAYLOAD_M, "latency_s": lat, "bandwidth_Bps": bw}
+                 for u, v, lat, bw in spec.links()]
+        model = {"schema": "model/v1",
+                 "layers": [{"fwd_flops": f, "bwd_input_flops": bi, "bwd_weight_flops": bw_,
+                             "activation_out_bytes": a, "param_bytes": pb}
+                            for f, bi, bw_, a, pb in spec.layers],
+                 "global_batch_candidates": list(spec.batches),
+                 "microbatch_candidates": list(spec.micros)}
+        return {"schema": "cluster/v1", "devices": devices, "links": links}, model
+
+    def put(name, doc):
+        path = os.path.join(d, name)
+        with open(path, "w") as fh:
+            json.dump(doc, fh, indent=1)
+        files[name] = path
+
+    put("small_cluster.json", cluster_doc([[4.0, 4.0], [2.0, 2.0], [1.0, 1.0]], cross=0.5))
+    put("small_model.json", model_doc())
+    put("hetero_cluster.json", cluster_doc([[8.0, 3.0, 3.0], [2.0, 2.0], [5.0]], cross=0.3))
+    put("hetero_model.json", model_doc(layers=9, batches=(8, 16), micros=(2, 4)))
+    for name in ("c1", "c2"):
+        c, m = inst_docs(name)
+        put(f"{name}_cluster.json", c)
+        put(f"{name}_model.json", m)
+    put("trace.json", {"schema": "trace/v1", "events": [
+        {"link": "0-1", "t_s": 0.5, "multiplier": 0.4},
+        {"link": "0-1", "t_s": 3.0, "multiplier": 1.0},
+        {"link": "1-2", "t_s": 1.0, "multiplier": 0.25}]})
+    put("bad_cluster.json", {"schema": "cluster/v1", "devices": [
+        {"id": "x", "benchmarks": [{"task": "b", "seconds": 1.0}]}], "links": []})
+    return files
+
+
+def dump_cli():
+    """Outputs of the reference CLI (src/cli.py) on committed input files."""
+    from cli_cases import cli_commands, run_cli
+    geopipe()
+    from geopipe.cli import main as ref_main
+    d = os.path.join(G.GOLDEN, "cli")
+    _cli_inputs(d)
+    import tempfile
+    out = {}
+    t0 = time.time()
+    with tempfile.TemporaryDirectory() as o:
+        for case, argv in cli_commands():
+            args = [a.replace("{d}", d).replace("{o}", o) for a in argv]
+            rc, so, se = run_cli(ref_main, args)
+            files = {}
+            for a in args:
+                if a.startswith(o) and os.path.exists(a) and "--out" in args and \
+                        args[args.index("--out") + 1] == a:
+                    files[os.path.basename(a)] = open(a).read()
+            out[case] = {"rc": rc, "stdout": so.replace(d, "{d}").replace(o, "{o}"),
+                         "stderr": se.replace(d, "{d}").replace(o, "{o}"), "files": files}
+    G.save("cli_outputs.json", out)
+    print(f"cli: {time.time() - t0:.1f}s", flush=True)
 
 
 def dump_regroup_replan():

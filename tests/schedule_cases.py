@@ -24,6 +24,11 @@ def digest(schedule_ops, transfers):
     return hashlib.sha1(canonical(schedule_ops, transfers).encode()).hexdigest()[:20]
 
 
+def action_digest(actions):
+    return hashlib.sha1(repr([(a.t, a.stage, a.old_size, a.new_size, a.signal)
+                              for a in actions]).encode()).hexdigest()[:20]
+
+
 def text_digest(messages):
     return hashlib.sha1("\n".join(messages).encode()).hexdigest()[:20]
 

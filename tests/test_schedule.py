@@ -46,7 +46,7 @@ def test_oracle_schedules_and_validation(oracle_lib, key):
     ad, asy, pol, it = _opts(key)
     arr = SM.pack_timings(REP_TIMINGS)
     tr = SM.pack_traces(REP["traces"])
-    reps, ooff, ops, xoff, xfs, st = oracle_lib.sim_schedules(
+    reps, ooff, ops, xoff, xfs, st, aoff, acts = oracle_lib.sim_schedules(
         arr, len(REP_TIMINGS), abi.POLICY_CODE[pol], it, tr, np.arange(len(REP_TIMINGS)),
         adapter=ad, async_iterations=asy)
     for i, t in enumerate(REP_TIMINGS):
@@ -57,6 +57,9 @@ def test_oracle_schedules_and_validation(oracle_lib, key):
         sched, xf = SCH.records_to_schedule(t, ops, int(ooff[i]), int(ooff[i + 1]), xfs,
                                             int(xoff[i]), int(xoff[i + 1]), reps[i].makespan, pol)
         assert SC.digest(sched.ops, xf) == exp, i
+        a = [SCH.AdapterAction(x.t, x.stage, x.old_size, x.new_size, abi.ACTION_SIGNALS[x.signal])
+             for x in (acts[j] for j in range(int(aoff[i]), int(aoff[i + 1])))]
+        assert SC.action_digest(a) == GOLD["actions"][key][i], i
         p = _perturbed(sched, 1000 * i + 7)
         off, parr, _ = SCH.pack_schedules([p])
         recs, nv, _ = oracle_lib.validate_schedule(arr[i], parr, int(off[1]), p.makespan)
@@ -74,9 +77,11 @@ def test_k5_schedules_and_k8_validation(engine, key):
     cfg = SM.SimConfig(iterations=it, async_iterations=asy)
     out = SCH.generate_schedules([REP_TIMINGS[i] for i in ok], pol,
                                  [REP["traces"][i] for i in ok], np.arange(len(ok)),
-                                 adapter_enabled=ad, config=cfg, engine=engine)
-    for i, (sched, xf) in zip(ok, out):
+                                 adapter_enabled=ad, config=cfg, engine=engine, with_actions=True)
+    for i, (sched, xf, acts) in zip(ok, out):
         assert SC.digest(sched.ops, xf) == rows[i], i
+        assert SC.action_digest(acts) == GOLD["actions"][key][i], i
+    out = [(s_, x_) for s_, x_, _ in out]
     pert = [_perturbed(sched, 1000 * i + 7) for i, (sched, _) in zip(ok, out)]
     msgs = SCH.validate_schedules(pert, [REP_TIMINGS[i] for i in ok], engine=engine,
                                   max_violations=8)
