@@ -1745,7 +1745,12 @@ extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const 
     const size_t total = o_scr + SB * per_scr;
     CUDA_TRY(c->g_buf.ensure(total));
     uint8_t* b = c->g_buf.p;
-    const size_t smem = k7_smem_bytes((int)D);
+    // small clusters keep the pair tables (and p_t) in shared memory
+    const size_t head = k7_smem_head((int)D), tabs = k7_scratch_bytes((int)D);
+    int smem_mode = 0;
+    size_t smem = head;
+    if (head + tabs + DD * 8 <= (200u << 10)) { smem_mode = 3; smem = head + tabs + DD * 8; }
+    else if (head + tabs <= (200u << 10)) { smem_mode = 1; smem = head + tabs; }
     CUDA_TRY(cudaFuncSetAttribute(k7_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_TRY(cudaMemcpyAsync(b + o_pc, p_c, (size_t)D * 8, cudaMemcpyHostToDevice, s));
     for (uint32_t s0 = 0; s0 < n_snap; s0 += SB) {
@@ -1765,7 +1770,8 @@ extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const 
             (int)D, reinterpret_cast<const double*>(b + o_pt),
             bandwidth ? reinterpret_cast<const double*>(b + o_bw) : nullptr, (long long)DD,
             (long long)DD, reinterpret_cast<const double*>(b + o_pc), threshold_net,
-            threshold_compute, b + o_scr, per_scr, d_fg, d_sg, d_nf, d_ns, d_fi, d_fc, d_fb, d_sc);
+            threshold_compute, b + o_scr, per_scr, smem_mode, d_fg, d_sg, d_nf, d_ns, d_fi, d_fc,
+            d_fb, d_sc);
         CUDA_TRY(cudaGetLastError());
         const size_t o = (size_t)s0 * D;
         CUDA_TRY(cudaMemcpyAsync(fg_of + o, d_fg, (size_t)nb * D * 2, cudaMemcpyDeviceToHost, s));

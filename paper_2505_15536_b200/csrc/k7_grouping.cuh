@@ -28,6 +28,17 @@
 // ----------------------------------------------------------------------------
 #define K7_THREADS 256
 
+// pair tables: keys, members, merge buffer, live flags (16-B aligned)
+__host__ __device__ __forceinline__ size_t k7_scratch_bytes(int D) {
+    size_t b = (size_t)D * D * 8 + (size_t)D * D * 2 + (size_t)D * 2 + (size_t)D * D;
+    return (b + 15) & ~(size_t)15;
+}
+
+// per-slot arrays at the head of dynamic shared memory
+__host__ __device__ __forceinline__ size_t k7_smem_head(int D) {
+    return ((size_t)D * 8 * 2 + (size_t)D * 2 * 5 + (size_t)D + 16 + 15) & ~(size_t)15;
+}
+
 struct K7Shared {
     double* rowkey;     // [n] best live key of row a
     double* intra;      // [n] level 1: _mean_intra_pt cache; level 2: mean_pc
@@ -276,7 +287,8 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
 __global__ void __launch_bounds__(K7_THREADS)
 k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw_all,
          long long pt_stride, long long bw_stride, const double* __restrict__ pc, double thr_net,
-         double thr_comp, uint8_t* __restrict__ scratch, size_t scratch_per, uint16_t* fg_of_all,
+         double thr_comp, uint8_t* __restrict__ scratch, size_t scratch_per, int smem_mode,
+         uint16_t* fg_of_all,
          uint16_t* sg_of_all, uint32_t* n_fg, uint32_t* n_sg, double* fg_intra_all,
          double* fg_cap_all, double* fg_minbw_all, double* sg_cap_all) {
     extern __shared__ __align__(16) uint8_t k7_smem[];
@@ -286,7 +298,14 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
     const int snap = blockIdx.x, tid = threadIdx.x;
     const double* pt = pt_all + (size_t)snap * pt_stride;
     const double* bw = bw_all ? bw_all + (size_t)snap * bw_stride : nullptr;
-    uint8_t* base = scratch + (size_t)snap * scratch_per;
+    // smem_mode bit0: pair tables in shared memory (small D); bit1: p_t too
+    uint8_t* base = (smem_mode & 1) ? k7_smem + k7_smem_head(D)
+                                    : scratch + (size_t)snap * scratch_per;
+    if (smem_mode & 2) {
+        double* pts = reinterpret_cast<double*>(base + k7_scratch_bytes(D));
+        for (int e = tid; e < D * D; e += blockDim.x) pts[e] = pt[e];
+        pt = pts;  // visible after the first __syncthreads below
+    }
     K7Global g;
     g.key = reinterpret_cast<double*>(base);
     g.mem = reinterpret_cast<uint16_t*>(base + (size_t)D * D * 8);
@@ -374,11 +393,4 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
     }
 }
 
-__host__ __forceinline__ size_t k7_scratch_bytes(int D) {
-    size_t b = (size_t)D * D * 8 + (size_t)D * D * 2 + (size_t)D * 2 + (size_t)D * D;
-    return (b + 255) & ~(size_t)255;
-}
 
-__host__ __forceinline__ size_t k7_smem_bytes(int D) {
-    return (size_t)D * 8 * 2 + (size_t)D * 2 * 5 + (size_t)D + 16;
-}
