@@ -24,6 +24,8 @@
 // Every floating-point operation mirrors the reference operation order
 // (src/costmodel.py:56-89, src/timing.py:116-231, src/planner.py:157-253);
 // the file is compiled with -fmad=false.  There is no CPU fallback.
+#include <mutex>
+
 #include "common.cuh"
 #include "k1_tables.cuh"
 #include "k2_eval.cuh"
@@ -583,6 +585,50 @@ int gp_space_size(gp_ctx* c, uint64_t* out) {
 }
 
 // Sweep launch over items [item_lo, item_hi) of (mi * k! + order).
+typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*,
+                     const uint32_t*);
+
+// sweep variant: shared-memory mode x batch sizes per m x (k = 3..6 fixed at
+// compile time in the all-shared-memory mode, else generic)
+static SwFn pick_sweep(int mode, int nb, int k) {
+    static const SwFn table[3][4] = {
+        {k3_sweep<0, 1, 0>, k3_sweep<0, 2, 0>, k3_sweep<0, 3, 0>, k3_sweep<0, 4, 0>},
+        {k3_sweep<1, 1, 0>, k3_sweep<1, 2, 0>, k3_sweep<1, 3, 0>, k3_sweep<1, 4, 0>},
+        {k3_sweep<2, 1, 0>, k3_sweep<2, 2, 0>, k3_sweep<2, 3, 0>, k3_sweep<2, 4, 0>}};
+    static const SwFn fixed[4][4] = {
+        {k3_sweep<2, 1, 3>, k3_sweep<2, 1, 4>, k3_sweep<2, 1, 5>, k3_sweep<2, 1, 6>},
+        {k3_sweep<2, 2, 3>, k3_sweep<2, 2, 4>, k3_sweep<2, 2, 5>, k3_sweep<2, 2, 6>},
+        {k3_sweep<2, 3, 3>, k3_sweep<2, 3, 4>, k3_sweep<2, 3, 5>, k3_sweep<2, 3, 6>},
+        {k3_sweep<2, 4, 3>, k3_sweep<2, 4, 4>, k3_sweep<2, 4, 5>, k3_sweep<2, 4, 6>}};
+    return (mode == 2 && k >= 3 && k <= 6) ? fixed[nb - 1][k - 3] : table[mode][nb - 1];
+}
+
+// cudaFuncSetAttribute + occupancy query, once per (device, kernel, dynamic
+// smem).  The attribute is process-wide per kernel and device, so the cache
+// is too, and the attribute only ever grows (every cached size stays
+// launchable whichever context configured a larger one).
+struct SlotEntry { int device; const void* kern; size_t smem; int threads, per_sm; };
+static std::vector<SlotEntry> g_slot_cache;
+static std::mutex g_slot_mu;
+
+static int kernel_slots(gp_ctx* c, const void* kern, int threads, size_t smem, int* per_sm) {
+    std::lock_guard<std::mutex> lock(g_slot_mu);
+    for (const auto& e : g_slot_cache)
+        if (e.device == c->device && e.kern == kern && e.smem == smem && e.threads == threads) {
+            *per_sm = e.per_sm;
+            return GP_OK;
+        }
+    size_t top = smem;
+    for (const auto& e : g_slot_cache)
+        if (e.device == c->device && e.kern == kern && e.smem > top) top = e.smem;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)top));
+    int ps = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, threads, smem));
+    g_slot_cache.push_back({c->device, kern, smem, threads, ps});
+    *per_sm = ps;
+    return GP_OK;
+}
+
 static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_lo,
                         unsigned long long item_hi, int mode, const uint32_t* dflags) {
     cudaStream_t s = c->stream;
@@ -595,16 +641,10 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     if (mode == 2 && smem2 > (size_t)c->smem_max) mode = 1;
     if (mode == 1 && smem1 > (size_t)c->smem_max) mode = 0;
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
-    typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*,
-                         const uint32_t*);
-    static const SwFn table[3][4] = {
-        {k3_sweep<0, 1>, k3_sweep<0, 2>, k3_sweep<0, 3>, k3_sweep<0, 4>},
-        {k3_sweep<1, 1>, k3_sweep<1, 2>, k3_sweep<1, 3>, k3_sweep<1, 4>},
-        {k3_sweep<2, 1>, k3_sweep<2, 2>, k3_sweep<2, 3>, k3_sweep<2, 4>}};
-    SwFn kern = table[mode][c->nb - 1];
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SwFn kern = pick_sweep(mode, c->nb, k);
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K3S_THREADS, smem));
+    { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
+      if (st_ != GP_OK) return st_; }
     unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
     unsigned long long items = item_hi - item_lo;
     unsigned long long tasks = (c->sweep_W + 31) / 32;
@@ -735,9 +775,9 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
         unsigned long long gmax = (unsigned long long)c->n_sms * 16;  // grid-stride
         if (grid > gmax) grid = gmax;
     } else {
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K3_THREADS, smem));
+        { int st_ = kernel_slots(c, (const void*)kern, K3_THREADS, smem, &per_sm);
+          if (st_ != GP_OK) return st_; }
         unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
         // items = (micro index, order); a range inside one batch block touches
         // a contiguous run of them, a wider range all of them
@@ -1541,16 +1581,10 @@ int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_
         int mode = smem2 <= (size_t)c->smem_max ? 2 : (smem1 <= (size_t)c->smem_max ? 1 : 0);
         if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
         size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
-        typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*,
-                             const uint32_t*);
-        static const SwFn table[3][4] = {
-            {k3_sweep<0, 1>, k3_sweep<0, 2>, k3_sweep<0, 3>, k3_sweep<0, 4>},
-            {k3_sweep<1, 1>, k3_sweep<1, 2>, k3_sweep<1, 3>, k3_sweep<1, 4>},
-            {k3_sweep<2, 1>, k3_sweep<2, 2>, k3_sweep<2, 3>, k3_sweep<2, 4>}};
-        SwFn kern = table[mode][c->nb - 1];
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SwFn kern = pick_sweep(mode, c->nb, k);
         int per_sm = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K3S_THREADS, smem));
+        { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
+          if (st_ != GP_OK) return st_; }
         unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
         unsigned long long cpi = (items * nb) >= resident ? 1 : resident / (items * nb);
         unsigned long long tasks = (c->sweep_W + 31) / 32;
@@ -1751,7 +1785,8 @@ extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const 
     size_t smem = head;
     if (head + tabs + DD * 8 <= (200u << 10)) { smem_mode = 3; smem = head + tabs + DD * 8; }
     else if (head + tabs <= (200u << 10)) { smem_mode = 1; smem = head + tabs; }
-    CUDA_TRY(cudaFuncSetAttribute(k7_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    { int ps_ = 0, st_ = kernel_slots(c, (const void*)k7_group, K7_THREADS, smem, &ps_);
+      if (st_ != GP_OK) return st_; }
     CUDA_TRY(cudaMemcpyAsync(b + o_pc, p_c, (size_t)D * 8, cudaMemcpyHostToDevice, s));
     for (uint32_t s0 = 0; s0 < n_snap; s0 += SB) {
         const uint32_t nb = (n_snap - s0) < SB ? (n_snap - s0) : SB;

@@ -254,12 +254,14 @@ struct SweepGeom {
     const unsigned long long* bnk;  // C(nn, r), nn <= n, r <= k: contiguous [n+1][k+1]
 };
 
-template <int MODE, int NB>
+// KS > 0 fixes the stage count at compile time (cut arrays in registers,
+// no local memory); KS = 0 is the generic kernel.
+template <int MODE, int NB, int KS>
 __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, SweepGeom G, ArgminScratch S,
                                                           const unsigned long long* __restrict__ binom,
                                                           const uint32_t* skip_if_flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int n = I.n, k = G.k;
+    const int n = I.n, k = KS > 0 ? KS : G.k;
     const int ntri = n * (n + 1) / 2;
     const int KB = k + 1;
     const unsigned int per_snap = G.items * (unsigned int)G.cpi;
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
         if ((unsigned long long)t * 32 >= G.W) break;
         if (lane == 0) t_next = atomicAdd(ctr, 1u);  // next task, latency hidden by this one
         const unsigned int u = t * 32 + lane;
-        int len = 0, a = 0, q0 = 0;
+        int len = 0, a = 1, q0 = 2;  // idle lanes keep in-range table addresses
         double fill2 = 0.0, res1 = 0.0, x1 = 0.0;
         double mx1[NB];
         unsigned long long rpre = 0;  // comp rank of (prefix, a, q = a + 1)
@@ -412,29 +414,57 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
         const double* x2p = (MODE >= 1 ? x23s : X23) + (q0 - 1);
         double run_c = INFINITY;
         int run_i = -1, run_b = 0;
+        // candidate q = q0 + i of the run: (cost min over the batch sizes, its batch)
+        auto eval_q = [&](int i, double& cmin, int& bmin) {
+            double2 e2, e3;
+            double x2;
+            if (MODE >= 1) { e2 = e2p[i]; e3 = e3p[i]; x2 = x2p[i]; }
+            else { e2 = __ldg(&e2p[i]); e3 = __ldg(&e3p[i]); x2 = __ldg(&x2p[i]); }
+            // stages k-2 = [a, q) and k-1 = [q, n) (src/costmodel.py:68-81)
+            const double res2 = res1 + max0f(x1 - e2.x);
+            const double fill3 = fill2 + (e2.x + x2);
+            const double res3 = res2 + max0f(x2 - e3.x);
+            cmin = INFINITY;
+            bmin = 0;
+#pragma unroll
+            for (int bi = 0; bi < NB; ++bi) {
+                double t2 = ((fill2 + Mv[bi] * e2.x) + res2) + e2.y;
+                double t3 = ((fill3 + Mv[bi] * e3.x) + res3) + e3.y;
+                double c = gtsel(t2, mx1[bi]);
+                c = gtsel(t3, c);
+                if (bi == 0 || c < cmin) { cmin = c; bmin = bi; }
+            }
+        };
+#if K3_ILP2
+        // two independent halves of the run in flight per lane (ILP): both
+        // evaluations are unconditional (clamped indices) so they interleave;
+        // the first minimum of the run is the first half's unless the second
+        // half's is strictly smaller
+        {
+            const int h = (len + 1) >> 1, lh = (lmax + 1) >> 1;
+            double c1 = INFINITY;
+            int i1 = -1, b1 = 0;
+            for (int i = 0; i < lh; ++i) {
+                const int ia = i < h ? i : (h > 0 ? h - 1 : 0);
+                const int ib = (h + i < len) ? h + i : ia;
+                double ca, cb;
+                int ba, bb;
+                eval_q(ia, ca, ba);
+                eval_q(ib, cb, bb);
+                if (i < h && (run_i < 0 || ca < run_c)) { run_c = ca; run_i = i; run_b = ba; }
+                if (h + i < len && (i1 < 0 || cb < c1)) { c1 = cb; i1 = h + i; b1 = bb; }
+            }
+            if (i1 >= 0 && (run_i < 0 || c1 < run_c)) { run_c = c1; run_i = i1; run_b = b1; }
+        }
+#else
         for (int i = 0; i < lmax; ++i) {
             if (i < len) {
-                double2 e2, e3;
-                double x2;
-                if (MODE >= 1) { e2 = e2p[i]; e3 = e3p[i]; x2 = x2p[i]; }
-                else { e2 = __ldg(&e2p[i]); e3 = __ldg(&e3p[i]); x2 = __ldg(&x2p[i]); }
-                // stages k-2 = [a, q) and k-1 = [q, n) (src/costmodel.py:68-81)
-                const double res2 = res1 + max0f(x1 - e2.x);
-                const double fill3 = fill2 + (e2.x + x2);
-                const double res3 = res2 + max0f(x2 - e3.x);
-                double cmin = INFINITY;
-                int bmin = 0;
-#pragma unroll
-                for (int bi = 0; bi < NB; ++bi) {
-                    double t2 = ((fill2 + Mv[bi] * e2.x) + res2) + e2.y;
-                    double t3 = ((fill3 + Mv[bi] * e3.x) + res3) + e3.y;
-                    double c = gtsel(t2, mx1[bi]);
-                    c = gtsel(t3, c);
-                    if (bi == 0 || c < cmin) { cmin = c; bmin = bi; }
-                }
+                double cmin; int bmin;
+                eval_q(i, cmin, bmin);
                 if (run_i < 0 || cmin < run_c) { run_c = cmin; run_i = i; run_b = bmin; }
             }
         }
+#endif
         if (run_i >= 0 && run_c <= best_c) {
             unsigned long long tk = (rpre + (unsigned long long)(q0 + run_i - a - 1)) * NB + run_b;
             if (run_c < best_c || tk < best_t) { best_c = run_c; best_t = tk; }
