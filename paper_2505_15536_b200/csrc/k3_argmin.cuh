@@ -355,7 +355,9 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
             // prefix cuts p[1..k-3]: colex row `row` (subsets of [1, a-1] come first)
             int p[GP_MAX_STAGES + 1];
             p[0] = 0;
-            if (k > 3) {
+            if (k == 4) {
+                p[1] = (int)row + 1;  // colex 1-subsets of [1, n-3]: row r is {r + 1}
+            } else if (k > 3) {
                 const uint8_t* pr = G.prefixes + (size_t)row * 16;
                 for (int j = 1; j <= k - 3; ++j) p[j] = pr[j - 1];
             }
