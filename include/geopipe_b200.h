@@ -427,6 +427,23 @@ int gp_sim_candidates(gp_ctx *ctx, uint32_t k, uint64_t n, const uint8_t *order,
                       const uint8_t *counts, const uint8_t *bm, uint32_t iterations,
                       double opt_seconds, double *makespan, uint8_t *status);
 
+/* One StageAssignment of an explicit plan (src/plans.py:84-95): group index
+ * (sorted fg id order), layer range, split kind; for ASYMMETRIC_PP the parts
+ * (subgroup index within the group, layer start, layer end). */
+typedef struct gp_plan_stage {
+    uint32_t fg, layer_start, layer_end, kind, n_parts;
+    uint32_t pp_sg[GP_MAX_SGS], pp_start[GP_MAX_SGS], pp_end[GP_MAX_SGS];
+} gp_plan_stage;
+
+/*
+ * plan_cost(plan, topology, model, groups, opt_seconds) (src/costmodel.py:92-100)
+ * of an explicit plan with the splits it carries, and optionally its
+ * build_plan_timing (src/timing.py:176-231) record.  out->stage[s] holds the
+ * StageCost fields; status as build_plan_timing's exceptions.
+ */
+int gp_plan_cost(gp_ctx *ctx, uint32_t k, const gp_plan_stage *stages, int64_t batch,
+                 int64_t microbatch, double opt_seconds, gp_plan_info *out, gp_timing *timing);
+
 /*
  * PlanTiming of explicit candidates (build_plan_timing(build_plan(...),
  * topology, model, groups, opt_seconds), src/timing.py:176-231): timings[i]

@@ -189,3 +189,15 @@ class GpViolation(C.Structure):
 
 
 OP_KINDS = ("F", "B", "W", "S", "O")
+
+
+class GpPlanStage(C.Structure):
+    _fields_ = [
+        ("fg", C.c_uint32), ("layer_start", C.c_uint32), ("layer_end", C.c_uint32),
+        ("kind", C.c_uint32), ("n_parts", C.c_uint32),
+        ("pp_sg", C.c_uint32 * GP_MAX_SGS), ("pp_start", C.c_uint32 * GP_MAX_SGS),
+        ("pp_end", C.c_uint32 * GP_MAX_SGS),
+    ]
+
+
+KIND_CODE = {v: k for k, v in KIND_OF.items()}

@@ -160,3 +160,123 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
     plan_detail_warp(I, k, o, p, bm, &out->info, &out->status);
 }
 
+
+// ---- cost of an explicit plan -------------------------------------------------------
+// plan_cost(plan, topology, model, groups, opt_seconds) (src/costmodel.py:92-100)
+// = Eq. 1 over build_plan_timing(plan) (src/timing.py:176-231) for a plan
+// whose splits are given (not chosen): only the split kind and the
+// ASYMMETRIC_PP parts enter the cost (effective_capacity, collective
+// volume); memory is not checked (plan_cost does not).  One warp: lane s
+// builds stage s, lane 0 runs the Eq. 1 chain.  Optionally emits the
+// PlanTiming record.
+__global__ void k_plan_cost(DevInst I, int k, const gp_plan_stage* __restrict__ stages,
+                            long long batch, long long micro, double opt_seconds,
+                            gp_plan_info* out, gp_timing* timing, int* status) {
+    const int lane = threadIdx.x & 31;
+    const int n = I.n;
+    const double md = (double)micro;
+    double cx = 0.0, cy = 0.0, xs = 0.0;
+    uint8_t code = SC_OK;
+    bool gw_bad = false;
+    if (lane < k) {
+        const gp_plan_stage& g = stages[lane];
+        const int f = (int)g.fg, a = (int)g.layer_start, b = (int)g.layer_end;
+        const int m0 = I.fg_off[f], m1 = I.fg_off[f + 1], nmem = m1 - m0;
+        const int s0 = I.fg_sg_off[f];
+        const double P = Ssum(I, COL_PARAM, a, b);
+        // effective_capacity (src/timing.py:116-143)
+        double cap;
+        if (g.kind == GP_ASYM_PP) {
+            const double tot = Ssum(I, COL_TF, a, b);
+            bool have = false;
+            double best = 0.0;
+            for (int j = 0; j < (int)g.n_parts; ++j) {
+                const int st = (int)g.pp_start[j], en = (int)g.pp_end[j];
+                const double sub = st < en ? Ssum(I, COL_TF, st, en) : 0.0;
+                const double frac = sub / tot;
+                if (frac > 0) {
+                    const double val = I.sg_cap[s0 + g.pp_sg[j]] / frac;
+                    if (!have || val < best) best = val;
+                    have = true;
+                }
+            }
+            cap = best;
+            if (!have) code = SC_DEGENERATE;
+        } else {
+            cap = I.fg_cap[f];
+            if (!(cap > 0)) code = SC_DEGENERATE;
+        }
+        const double Fp = Ssum(I, COL_FWD, a, b) / cap;
+        const double Bp = Ssum(I, COL_BWD, a, b) / cap;
+        const double Wp = Ssum(I, COL_WGT, a, b) / cap;
+        const bool has = I.fg_has_minbw[f] != 0;
+        const double mbw = I.fg_minbw[f];
+        const double sync = (P == 0.0 || !has) ? 0.0 : (mbw > 0 ? P / mbw : NAN);
+        if (code == SC_OK && has && !(mbw > 0) && (nmem >= 2 || P != 0.0)) code = SC_TOPOLOGY;
+        double al = 0.0;
+        if (nmem >= 2) {  // collective_volume / intra_group_seconds (:146-173)
+            double V = 2.0 * P;
+            if (g.kind == GP_ASYM_TP_DP) V = V + I.act[b - 1] * md;
+            if (V != 0.0 && has && mbw > 0) al = V / mbw;
+        }
+        cx = ((Fp + Bp) + Wp) * md;
+        cy = al;
+        if (lane + 1 < k) {  // gateway boundary (src/timing.py:208-224)
+            const int gl = I.gw[f * I.F + (int)stages[lane + 1].fg];
+            const double bwv = I.bw[gl];
+            gw_bad = !(bwv > 0);
+            xs = I.lat[gl] + (I.act[b - 1] * md) / bwv;
+            if (timing) {
+                timing->lat[lane] = I.lat[gl];
+                timing->bw[lane] = bwv;
+                timing->act[lane] = timing->grad[lane] = I.act[b - 1];
+            }
+        }
+        if (timing) {
+            timing->fwd[lane] = Fp; timing->bwd[lane] = Bp; timing->wgt[lane] = Wp;
+            timing->sync[lane] = sync; timing->opt[lane] = opt_seconds;
+        }
+    }
+    // stage errors in stage order, then zero-bandwidth gateways (the
+    // reference builds every StageTiming before the boundaries)
+    const unsigned errs = __ballot_sync(0xffffffffu, lane < k && code != SC_OK);
+    const unsigned gbad = __ballot_sync(0xffffffffu, gw_bad);
+    const int first_err = errs ? __shfl_sync(0xffffffffu, (int)code, __ffs(errs) - 1) : 0;
+    int st = errs ? first_err : (gbad ? GP_ERR_TOPOLOGY : GP_OK);
+    double fill = 0.0, res = 0.0, xprev = 0.0, best = 0.0;
+    const double Md = (double)(batch / micro);
+    for (int s = 0; s < k; ++s) {
+        const double ex = __shfl_sync(0xffffffffu, cx, s);
+        const double ey = __shfl_sync(0xffffffffu, cy, s);
+        const double xv = __shfl_sync(0xffffffffu, xs, s);
+        if (st != GP_OK) continue;
+        if (s > 0) res = res + gpd::max0(xprev - ex);
+        const double run = Md * ex;
+        const double total = ((fill + run) + res) + ey;
+        best = (s == 0 || total > best) ? total : best;
+        if (lane == 0) {
+            out->stage[s].kind = stages[s].kind;
+            out->stage[s].n_parts = stages[s].n_parts;
+            out->stage[s].fill_seconds = fill;
+            out->stage[s].run_seconds = run;
+            out->stage[s].residual_seconds = res;
+            out->stage[s].collective_seconds = ey;
+        }
+        if (s + 1 < k) {
+            fill = fill + (ex + xv);
+            xprev = xv;
+        }
+    }
+    if (lane == 0) {
+        out->k = (uint32_t)k;
+        out->feasible = 1;
+        out->plan_cost = best;
+        if (timing) {
+            timing->n_stages = (uint32_t)k;
+            timing->pad = 0;
+            timing->batch = batch;
+            timing->microbatch = micro;
+        }
+        *status = st;
+    }
+}

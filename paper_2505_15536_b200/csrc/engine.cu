@@ -143,6 +143,7 @@ struct gp_ctx {
     bool capturing = false;
     size_t arena_bytes = 0;
     int force_mode = -1;  // -1 auto; 0/1/2 fast-path variant; 3 generic kernel
+    std::vector<uint32_t> h_fg_sg_count;  // subgroups per group (explicit plans)
     DBuf<unsigned long long> binom;
     DBuf<unsigned int> item_ctr;
     DBuf<uint8_t> tiles;
@@ -328,6 +329,8 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     cudaStream_t s = c->stream;
     uint32_t n = in->n_layers, D = in->n_devices, F = in->n_fgs;
     c->n = (int)n; c->F = (int)F; c->D = (int)D; c->nb = (int)in->n_batch; c->nm = (int)in->n_micro;
+    c->h_fg_sg_count.assign(F, 0u);
+    for (uint32_t f = 0; f < F; ++f) c->h_fg_sg_count[f] = in->fg_sg_offset[f + 1] - in->fg_sg_offset[f];
     c->nsg = (int)nsg;
     c->bf = in->bottleneck_factor;
     c->h_batch.assign(in->batch, in->batch + in->n_batch);
@@ -1705,6 +1708,56 @@ int gp_plan_timing(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* order, cons
     CUDA_TRY(cudaMemcpyAsync(timings, c->s_tim.p, n * sizeof(gp_timing), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->b_status.p, n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    return GP_OK;
+}
+
+int gp_plan_cost(gp_ctx* c, uint32_t k, const gp_plan_stage* stages, int64_t batch,
+                 int64_t microbatch, double opt_seconds, gp_plan_info* out, gp_timing* timing) {
+    if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    if (!stages || !out) return fail(GP_ERR_INPUT, "bad arguments");
+    if (k < 1 || k > GP_MAX_STAGES) return fail(GP_ERR_INPUT, "k=%u outside [1,%d]", k, GP_MAX_STAGES);
+    if (batch <= 0 || microbatch <= 0 || batch % microbatch)
+        return fail(GP_ERR_INPUT, "micro-batch %lld does not divide batch %lld",
+                    (long long)microbatch, (long long)batch);
+    uint32_t pos = 0, seen = 0;
+    for (uint32_t s = 0; s < k; ++s) {
+        const gp_plan_stage& g = stages[s];
+        if (g.fg >= (uint32_t)c->F || ((seen >> g.fg) & 1u))
+            return fail(GP_ERR_INPUT, "stage %u: bad or repeated group %u", s, g.fg);
+        seen |= 1u << g.fg;
+        if (g.layer_start != pos || g.layer_end <= g.layer_start || g.layer_end > (uint32_t)c->n)
+            return fail(GP_ERR_INPUT, "stage layer ranges must tile the layer list without gaps");
+        pos = g.layer_end;
+        if (g.kind > GP_ASYM_TP_DP || g.n_parts > GP_MAX_SGS)
+            return fail(GP_ERR_INPUT, "stage %u: bad split", s);
+        const uint32_t nsg = (uint32_t)(c->h_fg_sg_count[g.fg]);
+        for (uint32_t j = 0; g.kind == GP_ASYM_PP && j < g.n_parts; ++j)
+            if (g.pp_sg[j] >= nsg || g.pp_start[j] > g.pp_end[j] || g.pp_end[j] > (uint32_t)c->n)
+                return fail(GP_ERR_INPUT, "stage %u: bad pipeline part %u", s, j);
+    }
+    if (pos != (uint32_t)c->n) return fail(GP_ERR_INPUT, "plan covers %u of %d layers", pos, c->n);
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t o_st = 0, o_out = al(k * sizeof(gp_plan_stage)), o_tim = o_out + al(sizeof(gp_plan_info));
+    const size_t o_stat = o_tim + al(sizeof(gp_timing));
+    CUDA_TRY(c->g_buf.ensure(o_stat + 16));
+    uint8_t* b = c->g_buf.p;
+    CUDA_TRY(cudaMemcpyAsync(b + o_st, stages, k * sizeof(gp_plan_stage), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(b + o_out, 0, sizeof(gp_plan_info), s));
+    CUDA_TRY(cudaMemsetAsync(b + o_tim, 0, sizeof(gp_timing), s));
+    k_plan_cost<<<1, 32, 0, s>>>(c->view(), (int)k, reinterpret_cast<const gp_plan_stage*>(b + o_st),
+                                 (long long)batch, (long long)microbatch, opt_seconds,
+                                 reinterpret_cast<gp_plan_info*>(b + o_out),
+                                 timing ? reinterpret_cast<gp_timing*>(b + o_tim) : nullptr,
+                                 reinterpret_cast<int*>(b + o_stat));
+    CUDA_TRY(cudaGetLastError());
+    int st = GP_OK;
+    CUDA_TRY(cudaMemcpyAsync(out, b + o_out, sizeof(gp_plan_info), cudaMemcpyDeviceToHost, s));
+    if (timing) CUDA_TRY(cudaMemcpyAsync(timing, b + o_tim, sizeof(gp_timing), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&st, b + o_stat, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (st != GP_OK) return fail(st, "build_plan_timing raised (status %d)", st);
     return GP_OK;
 }
 

@@ -86,6 +86,8 @@ def lib():
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
+        L.gp_plan_cost.argtypes = [vp, C.c_uint32, P(abi.GpPlanStage), C.c_int64, C.c_int64,
+                                   C.c_double, P(abi.GpPlanInfo), P(abi.GpTiming)]
         L.gp_plan_timing.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_double,
                                      P(abi.GpTiming), u8p]
         _lib = L
@@ -331,6 +333,16 @@ class Engine:
                                         u16(fg_of), u16(sg_of), u32(nf), u32(nsg), dp(fi), dp(fc),
                                         dp(fb), dp(sc)))
         return fg_of, sg_of, nf, nsg, fi, fc, fb, sc
+
+    def plan_cost(self, stages, batch: int, micro: int, opt_seconds: float = 0.0,
+                  timing: bool = False):
+        """(GpPlanInfo, GpTiming | None) of an explicit plan (gp_plan_stage array)."""
+        info = abi.GpPlanInfo()
+        tim = abi.GpTiming() if timing else None
+        _check(lib().gp_plan_cost(self._h, len(stages), stages, int(batch), int(micro),
+                                  float(opt_seconds), C.byref(info),
+                                  C.byref(tim) if tim is not None else None))
+        return info, tim
 
     def plan_timing(self, order, counts, bm, opt_seconds: float = 0.0):
         """(gp_timing array, status) of explicit candidates of the loaded instance."""

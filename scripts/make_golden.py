@@ -364,6 +364,7 @@ def main():
     dump_grouping()
     dump_schedules()
     dump_cli()
+    dump_plan_costs()
     dump_regroup_replan()
 
     for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
@@ -585,6 +586,12 @@ def _cli_inputs(d):
         {"link": "0-1", "t_s": 0.5, "multiplier": 0.4},
         {"link": "0-1", "t_s": 3.0, "multiplier": 1.0},
         {"link": "1-2", "t_s": 1.0, "multiplier": 0.25}]})
+    put("hetero_plan_edited.json", {"schema": "plan/v1", "batch": 16, "microbatch": 4, "stages": [
+        {"fg": "fg2", "layers": [0, 3], "split": {"kind": "uniform", "parts": []}},
+        {"fg": "fg0", "layers": [3, 7], "split": {"kind": "asymmetric_pp", "parts": [
+            ["fg0.sg0", 3, 5], ["fg0.sg1", 5, 7]]}},
+        {"fg": "fg1", "layers": [7, 9], "split": {"kind": "asymmetric_dp",
+                                                  "parts": [["fg1.sg0", 1.0]]}}]})
     put("bad_cluster.json", {"schema": "cluster/v1", "devices": [
         {"id": "x", "benchmarks": [{"task": "b", "seconds": 1.0}]}], "links": []})
     return files
@@ -613,6 +620,99 @@ def dump_cli():
                          "stderr": se.replace(d, "{d}").replace(o, "{o}"), "files": files}
     G.save("cli_outputs.json", out)
     print(f"cli: {time.time() - t0:.1f}s", flush=True)
+
+
+def ref_from_doc(doc):
+    """Reference objects (model, topology, groups) from a golden instance doc."""
+    gp = geopipe()
+    from geopipe.profiling import ClusterTopology, CommMetric, ComputeMetric, LinkInfo
+    from geopipe.timing import GroupIndex
+    from geopipe.grouping import FirstLevelGroup, SecondLevelGroup
+    layers = tuple(gp.LayerSpec(*row) for row in doc["layers"])
+    model = gp.ModelSpec(layers=layers, global_batch_candidates=tuple(doc["batches"]),
+                         microbatch_candidates=tuple(doc["micros"]))
+    devices = tuple(gp.DeviceSpec(id=i, memory_bytes=mem, benchmark_times=(("b", 1.0),))
+                    for i, mem, _ in doc["devices"])
+    compute = {i: ComputeMetric(p_c=pc) for i, _, pc in doc["devices"]}
+    links = {frozenset((u, v)): LinkInfo(metric=CommMetric(p_t=pt), latency_seconds=lat,
+                                         bandwidth_bytes_per_s=bw)
+             for u, v, pt, lat, bw in doc["links"]}
+    topo = ClusterTopology(devices=devices, compute=compute, links=links)
+    fgs = [FirstLevelGroup(id=i, member_device_ids=tuple(m), intra_metric=im,
+                           aggregate_capacity=cap, min_intra_bandwidth=mb)
+           for i, m, im, cap, mb in doc["fgs"]]
+    sgs = {f: [SecondLevelGroup(id=i, parent_fg_id=f, member_device_ids=tuple(m),
+                                aggregate_capacity=cap) for i, m, cap in v]
+           for f, v in doc["sgs"].items()}
+    return model, topo, GroupIndex.build(fgs, sgs)
+
+
+PLAN_COST_CASES = ["small", "c1", "c1j", "c2j", "c4", "err_intra_bw", "err_gateway",
+                   "single_fg"] + [f"rand{i}" for i in range(1, 16)]
+
+
+def random_plan(rng, model, groups):
+    """A random explicit plan: subset and order of groups, cuts, batch /
+    micro-batch, split kinds with arbitrary pipeline parts."""
+    gp = geopipe()
+    n = len(model.layers)
+    fg_ids = sorted(groups.fgs)
+    k = rng.randint(1, min(len(fg_ids), n))
+    order = rng.sample(fg_ids, k)
+    cuts = sorted(rng.sample(range(1, n), k - 1)) if k > 1 else []
+    bounds = [0] + cuts + [n]
+    b = rng.choice(model.global_batch_candidates)
+    m = rng.choice([x for x in (1, 2, 4, 8, 16, b) if b % x == 0])
+    stages = []
+    for s, f in enumerate(order):
+        a, e = bounds[s], bounds[s + 1]
+        kind = rng.choice(list(gp.SplitKind))
+        sgs = [sg.id for sg in groups.sgs_by_fg[f]]
+        if kind is gp.SplitKind.ASYMMETRIC_PP:
+            parts = []
+            for _ in range(rng.randint(0, min(4, len(sgs) + 1))):
+                x, y = sorted(rng.sample(range(a, e + 1), 2)) if e - a >= 1 else (a, a)
+                parts.append((rng.choice(sgs), x, y))
+            parts = tuple(parts)
+        elif kind is gp.SplitKind.ASYMMETRIC_DP:
+            parts = tuple((sg, 1.0 / len(sgs)) for sg in sgs)
+        elif kind is gp.SplitKind.ASYMMETRIC_TP_DP:
+            parts = tuple((d, 0.5, 0.5) for d in groups.fgs[f].member_device_ids)
+        else:
+            parts = ()
+        stages.append(gp.StageAssignment(fg_id=f, layer_start=a, layer_end=e,
+                                         intra_split=gp.IntraSplit(kind, parts)))
+    return gp.ParallelPlan(stages=tuple(stages), batch_b=b, microbatch_m=m)
+
+
+def dump_plan_costs():
+    """plan_cost + build_plan_timing of the reference for random explicit
+    plans (arbitrary splits) on the golden instances."""
+    gp = geopipe()
+    from geopipe.fileio import plan_to_dict
+    from geopipe.timing import build_plan_timing
+    out = {}
+    t0 = time.time()
+    for name in PLAN_COST_CASES:
+        doc = G.load(f"{name}.json")["instance"]
+        model, topo, groups = ref_from_doc(doc)
+        rng = random.Random(sum(map(ord, name)) * 7 + 1)
+        rows = []
+        for _ in range(40):
+            plan = random_plan(rng, model, groups)
+            opt = rng.choice([0.0, 0.25])
+            rec = {"plan": plan_to_dict(plan), "opt_seconds": opt}
+            try:
+                bd = gp.plan_cost(plan, topo, model, groups, opt_seconds=opt)
+                rec["cost"] = G.breakdown_to_dict(bd)
+                t = build_plan_timing(plan, topo, model, groups, opt_seconds=opt)
+                rec["timing"] = timing_to_dict(t)
+            except Exception as e:
+                rec["error"] = type(e).__name__
+            rows.append(rec)
+        out[name] = rows
+    G.save("plan_costs.json", out)
+    print(f"plan costs: {time.time() - t0:.1f}s", flush=True)
 
 
 def dump_regroup_replan():

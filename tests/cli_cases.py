@@ -22,6 +22,10 @@ def cli_commands():
                       "{d}/trace.json", "--iterations", "4"]))
         cmds.append((f"{base}:compare", ["compare", c, m, p, "--adapter", "--trace",
                                          "{d}/trace.json"]))
+    hc, hm, he = "{d}/hetero_cluster.json", "{d}/hetero_model.json", "{d}/hetero_plan_edited.json"
+    cmds.append(("hetero:cost-edited", ["cost", hc, hm, he]))
+    cmds.append(("hetero:simulate-edited", ["simulate", hc, hm, he, "--policy", "gpipe"]))
+    cmds.append(("hetero:compare-edited", ["compare", hc, hm, he]))
     cmds.append(("small:plan-seed3", ["plan", "{d}/small_cluster.json", "{d}/small_model.json",
                                       "--seed", "3", "--beam-width", "2", "--max-iter", "5"]))
     cmds.append(("bad:group", ["group", "{d}/bad_cluster.json"]))
