@@ -253,7 +253,7 @@ def extra_sections(eng, packed, total, local, args, world):
     fac = np.where(rng7.random((n7, nreg, nreg)) < 0.5, rng7.uniform(1.0, 3.0, (n7, nreg, nreg)), 1.0)
     fac = np.triu(fac) + np.triu(fac, 1).transpose(0, 2, 1)
     pts = pt4[None] * fac[:, reg][:, :, reg]
-    GR.group_hierarchies(pts[:8], bw4, pc4, engine=eng)
+    GR.group_hierarchies(pts, bw4, pc4, engine=eng)  # warm-up at full size
     t0 = time.perf_counter()
     hs = GR.group_hierarchies(pts, bw4, pc4, engine=eng)
     el = time.perf_counter() - t0
@@ -295,7 +295,8 @@ def extra_sections(eng, packed, total, local, args, world):
     arr5 = simulate.pack_timings(tims)
     tr5 = simulate.pack_traces(traces)
     ti5 = np.arange(n5) % 64
-    eng.simulate_report(arr5, 1000, 3, 3, tr5, 64, ti5[:1000], adapter=True, async_iterations=True)
+    # warm-up at full size (queue-scratch allocation outside the timed call)
+    eng.simulate_report(arr5, n5, 3, 3, tr5, 64, ti5, adapter=True, async_iterations=True)
     t0 = time.perf_counter()
     reps5, _, st5 = eng.simulate_report(arr5, n5, 3, 3, tr5, 64, ti5, adapter=True,
                                         async_iterations=True)
