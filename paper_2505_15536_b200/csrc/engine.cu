@@ -588,6 +588,15 @@ int gp_space_size(gp_ctx* c, uint64_t* out) {
 }
 
 // Sweep launch over items [item_lo, item_hi) of (mi * k! + order).
+// threads per block for one-thread-per-item kernels: 128, or fewer so that a
+// small batch still spreads over every SM (latency-bound loops per thread)
+static int item_tpb(gp_ctx* c, unsigned long long n) {
+    const unsigned long long per = (unsigned long long)c->n_sms * 2;
+    unsigned long long t = (n + per - 1) / per;
+    t = (t + 31) / 32 * 32;
+    return t < 32 ? 32 : (t > 128 ? 128 : (int)t);
+}
+
 typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*,
                      const uint32_t*);
 
@@ -1220,7 +1229,8 @@ int gp_sim_1f1b_device(gp_ctx* c, const gp_timing* d_timings, uint64_t n, uint32
     if (!c) return fail(GP_ERR_INPUT, "null context");
     if (n == 0) return GP_OK;
     CUDA_TRY(cudaSetDevice(c->device));
-    k5_sim_1f1b<<<(unsigned)((n + 127) / 128), 128, 0, c->stream>>>(
+    const int tpb = item_tpb(c, n);
+    k5_sim_1f1b<<<(unsigned)((n + tpb - 1) / tpb), tpb, 0, c->stream>>>(
         d_timings, (long long)n, GP_POLICY_1F1B, (int)iterations, nullptr, nullptr, d_makespan,
         d_status);
     CUDA_TRY(cudaGetLastError());
@@ -1269,7 +1279,8 @@ int gp_simulate(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy
             d_ti = c->s_tidx.p;
         }
     }
-    k5_sim_1f1b<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(c->s_tim.p, (long long)n, (int)policy,
+    const int tpb = item_tpb(c, n);
+    k5_sim_1f1b<<<(unsigned)((n + tpb - 1) / tpb), tpb, 0, s>>>(c->s_tim.p, (long long)n, (int)policy,
                                                            (int)iterations, d_tr, d_ti, c->s_ms.p,
                                                            c->s_st.p);
     CUDA_TRY(cudaGetLastError());
@@ -1372,7 +1383,8 @@ int gp_simulate_report(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t
     }
     for (uint64_t i0 = 0; i0 < n; i0 += P.chunk) {
         const uint64_t nc = (n - i0) < P.chunk ? (n - i0) : P.chunk;
-        k5_sim_full<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
+        const int tpb = item_tpb(c, nc);
+        k5_sim_full<<<(unsigned)((nc + tpb - 1) / tpb), tpb, 0, s>>>(
             c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, P.d_tr,
             P.d_ti ? P.d_ti + i0 : nullptr, P.opt, sim_scratch(c, P, nc), c->s_rep.p + i0,
             iteration_ends ? c->s_ends.p + i0 * iterations : nullptr, c->s_st.p + i0);
@@ -1426,7 +1438,8 @@ int gp_simulate_schedule(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32
     CUDA_TRY(cudaMemcpyAsync(d_oo, h_off.data(), 3 * (n + 1) * 8, cudaMemcpyHostToDevice, s));
     for (uint64_t i0 = 0; i0 < n; i0 += P.chunk) {
         const uint64_t nc = (n - i0) < P.chunk ? (n - i0) : P.chunk;
-        k5_sim_schedule<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
+        const int tpb = item_tpb(c, nc);
+        k5_sim_schedule<<<(unsigned)((nc + tpb - 1) / tpb), tpb, 0, s>>>(
             c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, P.d_tr,
             P.d_ti ? P.d_ti + i0 : nullptr, P.opt, sim_scratch(c, P, nc), d_oo + i0, d_ops,
             d_xo + i0, transfers ? d_xf : nullptr, d_ao + i0, actions ? d_ac : nullptr,
@@ -1465,7 +1478,8 @@ int gp_validate_schedules(gp_ctx* c, const gp_timing* timings, uint64_t n,
     const size_t o_nv = o_v + al(n * (size_t)max_violations * sizeof(gp_violation));
     const size_t o_busy = o_nv + al(n * 4), o_st = o_busy + al(n * GP_MAX_STAGES * 8);
     const size_t o_tab = o_st + al(n), o_idx = o_tab + al(n * nq * 2 * 4);
-    const size_t o_srt = o_idx + al(n_ops * 4), o_its = o_srt + al(n_ops * 4);
+    const size_t o_srt = o_idx + al(n_ops * 4), o_lst = o_srt + al(n_ops * 4);
+    const size_t o_its = o_lst + al(n_ops * 4);
     const size_t total = o_its + al(n * (size_t)GP_MAX_STAGES * iterations * sizeof(K8Iter));
     CUDA_TRY(c->g_buf.ensure(total));
     uint8_t* b = c->g_buf.p;
@@ -1480,8 +1494,10 @@ int gp_validate_schedules(gp_ctx* c, const gp_timing* timings, uint64_t n,
     sc.tab = reinterpret_cast<uint32_t*>(b + o_tab);
     sc.idx = reinterpret_cast<uint32_t*>(b + o_idx);
     sc.sorted = reinterpret_cast<uint32_t*>(b + o_srt);
+    sc.lists = reinterpret_cast<uint32_t*>(b + o_lst);
     sc.its = reinterpret_cast<K8Iter*>(b + o_its);
-    k8_validate<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
+    const int tpb = item_tpb(c, n);
+    k8_validate<<<(unsigned)((n + tpb - 1) / tpb), tpb, 0, s>>>(
         reinterpret_cast<const gp_timing*>(b + o_tim), (long long)n,
         reinterpret_cast<const unsigned long long*>(b + o_off), reinterpret_cast<const gp_op*>(b + o_ops),
         reinterpret_cast<const double*>(b + o_ms), (int)iterations, tol, max_violations,
@@ -1673,7 +1689,8 @@ int gp_sim_candidates(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* order,
     CUDA_TRY(cudaMemcpyAsync(c->b_counts.p, counts, n * k, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(c->b_bm.p, bm, n, cudaMemcpyHostToDevice, s));
     DevInst I = c->view();
-    k5_sim_candidates<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(I, (int)k, (long long)n, c->b_order.p,
+    const int tpb = item_tpb(c, n);
+    k5_sim_candidates<<<(unsigned)((n + tpb - 1) / tpb), tpb, 0, s>>>(I, (int)k, (long long)n, c->b_order.p,
                                                                  c->b_counts.p, c->b_bm.p,
                                                                  (int)iterations, opt_seconds,
                                                                  c->b_cost.p, c->b_status.p);

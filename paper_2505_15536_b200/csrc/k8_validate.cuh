@@ -26,6 +26,7 @@ struct K8Scratch {
     uint32_t* tab;      // [n][S_MAX*iters*3][2]  count, base
     uint32_t* idx;      // [total ops]            table payload
     uint32_t* sorted;   // [total ops]            per-stage sort buffer
+    uint32_t* lists;    // [total ops]            op indices, stage-major, list order
     K8Iter* its;        // [n][S_MAX*iters]
 };
 
@@ -59,6 +60,7 @@ __global__ void k8_validate(const gp_timing* __restrict__ T_all, long long n,
     uint32_t* tab = sc.tab + i * (long long)nq * 2;
     uint32_t* idx = sc.idx + o0;
     uint32_t* srt = sc.sorted + o0;
+    uint32_t* lst = sc.lists + o0;
     K8Iter* its = sc.its + i * (long long)GP_MAX_STAGES * iterations;
     uint32_t nv = 0;
     n_viol[i] = 0;
@@ -94,14 +96,24 @@ __global__ void k8_validate(const gp_timing* __restrict__ T_all, long long n,
         if (k < 0 || (uint32_t)k >= tab[2 * q]) return -1;
         return idx[tab[2 * q + 1] + k];
     };
+    // per-stage op lists (stage-major, list order): every later phase walks
+    // one stage's ops without rescanning the whole schedule
+    int soff[GP_MAX_STAGES + 1];
+    for (int s = 0; s <= S; ++s) soff[s] = 0;
+    for (long long j = 0; j < m; ++j) soff[ops[j].stage + 1]++;
+    for (int s = 0; s < S; ++s) soff[s + 1] += soff[s];
+    {
+        int fillp[GP_MAX_STAGES];
+        for (int s = 0; s < S; ++s) fillp[s] = soff[s];
+        for (long long j = 0; j < m; ++j) lst[fillp[ops[j].stage]++] = (uint32_t)j;
+    }
     const double tol = tol_rel * (makespan[i] > 1.0 ? makespan[i] : 1.0);
     // 1. ops that end before they start; bubble_fraction busy sums
     for (int s = 0; s < S; ++s) {
         NeumaierSum b;
         bool first = true;
-        for (long long j = 0; j < m; ++j) {
-            const gp_op& o = ops[j];
-            if (o.stage != s) continue;
+        for (int q = soff[s]; q < soff[s + 1]; ++q) {
+            const gp_op& o = ops[lst[q]];
             if (o.end < o.start - tol) k8_emit(out, max_v, nv, 0, s, o.kind, 0, 0, 0.0);
             const double x = o.end - o.start;
             if (first) { b.start(x); first = false; } else b.add(x);
@@ -113,8 +125,7 @@ __global__ void k8_validate(const gp_timing* __restrict__ T_all, long long n,
     // 2. overlaps: stable sort by (start, end) per stage
     for (int s = 0; s < S; ++s) {
         long long c = 0;
-        for (long long j = 0; j < m; ++j)
-            if (ops[j].stage == s) srt[c++] = (uint32_t)j;
+        for (int q = soff[s]; q < soff[s + 1]; ++q) srt[c++] = lst[q];
         for (long long a = 1; a < c; ++a) {
             const uint32_t v = srt[a];
             const double vs = ops[v].start, ve = ops[v].end;
@@ -135,9 +146,9 @@ __global__ void k8_validate(const gp_timing* __restrict__ T_all, long long n,
     }
     // 3. dependencies (dict order = stage-major list order)
     for (int s = 0; s < S; ++s)
-        for (long long j = 0; j < m; ++j) {
-            const gp_op& o = ops[j];
-            if (o.stage != s || o.kind > 2) continue;
+        for (int qq = soff[s]; qq < soff[s + 1]; ++qq) {
+            const gp_op& o = ops[lst[qq]];
+            if (o.kind > 2) continue;
             const int32_t k = o.microbatch_id;
             const uint32_t it = o.iteration;
             if (o.kind == 0 && s > 0) {
@@ -172,20 +183,19 @@ __global__ void k8_validate(const gp_timing* __restrict__ T_all, long long n,
             st[q].n_sync = st[q].n_opt = 0; st[q].sync_idx = st[q].opt_idx = -1;
             st[q].have_w = 0; st[q].done = 0; st[q].last_w = 0.0;
         }
-        for (long long j = 0; j < m; ++j) {
+        for (int qq = soff[s]; qq < soff[s + 1]; ++qq) {
+            const int j = (int)lst[qq];
             const gp_op& o = ops[j];
-            if (o.stage != s) continue;
             K8Iter& q = st[o.iteration];
-            if (o.kind == 3) { q.n_sync++; q.sync_idx = (int)j; }
-            if (o.kind == 4) { q.n_opt++; q.opt_idx = (int)j; }
+            if (o.kind == 3) { q.n_sync++; q.sync_idx = j; }
+            if (o.kind == 4) { q.n_opt++; q.opt_idx = j; }
             if (o.kind == 2) {
                 if (!q.have_w || o.end > q.last_w) q.last_w = o.end;
                 q.have_w = 1;
             }
         }
-        for (long long j = 0; j < m; ++j) {
-            const gp_op& o = ops[j];
-            if (o.stage != s) continue;
+        for (int qq = soff[s]; qq < soff[s + 1]; ++qq) {
+            const gp_op& o = ops[lst[qq]];
             K8Iter& q = st[o.iteration];
             if (q.done) continue;
             q.done = 1;
