@@ -101,9 +101,13 @@ __device__ __forceinline__ int tri_idx(int n, int a, int b) { return a * (n + 1)
 
 enum { COL_FWD = 0, COL_BWD = 1, COL_WGT = 2, COL_PARAM = 3, COL_TF = 4 };
 
+// interval-sum table S[col] is stored b-major (transposed) so that K1's
+// per-a sweeps write coalesced
+__device__ __forceinline__ int s_idx(int n, int a, int b) { return b * (n + 1) + a; }
+
 __device__ __forceinline__ double Ssum(const DevInst& I, int col, int a, int b) {
     size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
-    return I.S[col * N2 + tri_idx(I.n, a, b)];
+    return I.S[col * N2 + s_idx(I.n, a, b)];
 }
 
 

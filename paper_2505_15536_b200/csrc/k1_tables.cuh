@@ -7,9 +7,12 @@
 // each interval summed from its own start (never prefix differences).
 __device__ void k1_intervals_block(const DevInst& I, int col) {
     // one CTA per column; the column is staged in shared memory so the
-    // sequential Neumaier sweeps read on-chip values
+    // sequential Neumaier sweeps read on-chip values.  S is stored
+    // transposed (b-major, see Ssum), so the lanes of a warp (consecutive a)
+    // write consecutive addresses at every step of their sweeps.
     __shared__ double col_s[GP_MAX_LAYERS + 1];
-    for (int i = threadIdx.x; i < I.n; i += blockDim.x) {
+    const int n = I.n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
         double x;
         switch (col) {
             case COL_FWD: x = I.fwd[i]; break;
@@ -21,13 +24,15 @@ __device__ void k1_intervals_block(const DevInst& I, int col) {
         col_s[i] = x;
     }
     __syncthreads();
-    size_t N2 = (size_t)(I.n + 1) * (I.n + 1);
+    const size_t N2 = (size_t)(n + 1) * (n + 1);
     double* out = I.S + col * N2;
-    for (int a = threadIdx.x; a < I.n; a += blockDim.x) {
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
         NeumaierSum sm;
-        for (int b = a + 1; b <= I.n; ++b) {
-            if (b == a + 1) sm.start(col_s[b - 1]); else sm.add(col_s[b - 1]);
-            out[tri_idx(I.n, a, b)] = sm.value();
+        sm.start(col_s[a]);
+        out[s_idx(n, a, a + 1)] = sm.value();
+        for (int b = a + 2; b <= n; ++b) {
+            sm.add(col_s[b - 1]);
+            out[s_idx(n, a, b)] = sm.value();
         }
     }
 }
@@ -48,10 +53,16 @@ __device__ __forceinline__ double block_min128(double v, double* red) {
 }
 
 // one 128-thread block per group: members loaded in parallel into shared
-// memory, then the (sequential) factorisation runs on-chip
+// memory; the TP grid factorisation (split_asymmetric_tp_dp,
+// src/planner.py:116-154) checks each candidate shape with every thread
+// (one isclose per thread, block AND) and divides the fractions in parallel;
+// only the short Neumaier sums run on one thread.
 __device__ void k1_group_block(const DevInst& I, int f) {
     __shared__ double caps[GP_MAX_MEMBERS];
     __shared__ double red[4];
+    __shared__ int shp[64];
+    __shared__ int ns_sh;
+    __shared__ double sums[2];
     const int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
     const int nmem = m1 - m0;
     double mn = INFINITY;
@@ -61,13 +72,56 @@ __device__ void k1_group_block(const DevInst& I, int f) {
         const double mm = I.mem[d];
         mn = mm < mn ? mm : mn;
     }
-    mn = block_min128(mn, red);
+    mn = block_min128(mn, red);  // (synchronises: caps visible)
     if (threadIdx.x == 0) {
         I.g_minmem[f] = mn;
-        I.g_tp_ok[f] = gpd::tp_grid(caps, nmem, I.g_rf + m0, I.g_cf + m0) ? 1 : 0;
+        // candidate shapes (r, n/r), r in [2, n), stably sorted by |r - c|
+        int ns = 0;
+        for (int r = 2; r < nmem && ns < 64; ++r)
+            if (nmem % r == 0 && nmem / r >= 2) shp[ns++] = r;
+        for (int i = 1; i < ns; ++i) {
+            int r = shp[i], j = i - 1;
+            int key = r - nmem / r; key = key < 0 ? -key : key;
+            while (j >= 0) {
+                int kj = shp[j] - nmem / shp[j]; kj = kj < 0 ? -kj : kj;
+                if (kj <= key) break;
+                shp[j + 1] = shp[j];
+                --j;
+            }
+            shp[j + 1] = r;
+        }
+        ns_sh = ns;
         const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
         if (s1 > s0) gpd::dp_fractions(I.sg_cap + s0, s1 - s0, I.g_dp + s0);
     }
+    __syncthreads();
+    bool tp_ok = false;
+    for (int q = 0; q < ns_sh; ++q) {
+        const int r = shp[q], c = nmem / r;
+        bool ok = true;
+        for (int t = threadIdx.x; t < r * c; t += blockDim.x) {
+            const int i = t / c, j = t % c;
+            ok = ok && gpd::py_isclose(caps[j * r + i] * caps[0], caps[i] * caps[j * r], 1e-9);
+        }
+        if (!__syncthreads_and(ok)) continue;
+        if (threadIdx.x == 0) {  // rows = grid[i][0] = caps[i]; cols = grid[0][j] = caps[j*r]
+            NeumaierSum rs, cs;
+            rs.start(caps[0]);
+            for (int i = 1; i < r; ++i) rs.add(caps[i]);
+            cs.start(caps[0]);
+            for (int j = 1; j < c; ++j) cs.add(caps[j * r]);
+            sums[0] = rs.value();
+            sums[1] = cs.value();
+        }
+        __syncthreads();
+        for (int kk = threadIdx.x; kk < nmem; kk += blockDim.x) {
+            I.g_rf[m0 + kk] = caps[kk % r] / sums[0];
+            I.g_cf[m0 + kk] = caps[(kk / r) * r] / sums[1];
+        }
+        tp_ok = true;
+        break;
+    }
+    if (threadIdx.x == 0) I.g_tp_ok[f] = tp_ok ? 1 : 0;
     const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
     for (int g = s0; g < s1; ++g) {
         double sm = INFINITY;
@@ -154,17 +208,19 @@ __device__ void k1_stage_t(const DevInst& I, long long t) {
     int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
     int s0 = I.fg_sg_off[f];
     // memory feasibility: bytes_needed > memory_bytes -> infeasible
+    // (no early exit: the loads of every member / part are independent, so
+    // they overlap instead of forming a chain of dependent round trips)
     bool feas = true;
     if (kind == GP_ASYM_PP) {
         int pos = a;
-        for (int j = 0; j < np && feas; ++j) {
+        for (int j = 0; j < np; ++j) {
             double sub = Ssum(I, COL_PARAM, pos, pos + shares[j]);
-            if (I.sg_off[s0 + j + 1] > I.sg_off[s0 + j]) feas = !(sub > I.sg_minmem[s0 + j]);
+            if (I.sg_off[s0 + j + 1] > I.sg_off[s0 + j]) feas = feas & !(sub > I.sg_minmem[s0 + j]);
             pos += shares[j];
         }
     } else if (kind == GP_ASYM_TP_DP) {
-        for (int x = m0; x < m1 && feas; ++x)
-            feas = !(((P * I.g_rf[x]) * I.g_cf[x]) > I.mem[I.fg_mem[x]]);
+        for (int x = m0; x < m1; ++x)
+            feas = feas & !(((P * I.g_rf[x]) * I.g_cf[x]) > I.mem[I.fg_mem[x]]);
     } else {
         feas = !(P > I.g_minmem[f]);
     }
@@ -242,7 +298,8 @@ __device__ void k1_gateway_warp(const DevInst& I, int warp, int lane) {
     bool have = false;
     double bp = 0.0;
     unsigned int bu = 0, bv = 0, ru = 0xffffffffu, rv = 0xffffffffu;
-    for (int t = lane; t < na * nbm; t += 32) {
+#pragma unroll 8
+    for (int t = lane; t < na * nbm; t += 32) {  // unrolled: the member / p_t loads overlap
         const unsigned int u = I.fg_mem[a0 + t / nbm], v = I.fg_mem[b0 + t % nbm];
         const double p = I.p_t[(size_t)u * I.D + v];
         const unsigned int qu = I.id_rank[u], qv = I.id_rank[v];
@@ -277,10 +334,22 @@ __device__ void k1_gateway_warp(const DevInst& I, int warp, int lane);
 
 __global__ void __launch_bounds__(128) k1_phase1(DevInst I) {
     const int b = blockIdx.x;
-    if (b < 5) { k1_intervals_block(I, b); return; }
-    if (b < 5 + I.F) { k1_group_block(I, b - 5); return; }
-    const int warp = (b - 5 - I.F) * 4 + (threadIdx.x >> 5);
-    if (warp < I.F * I.F) k1_gateway_warp(I, warp, threadIdx.x & 31);
+#if defined(K1_PROFILE)
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
+    if (b < 5) k1_intervals_block(I, b);
+    else if (b < 5 + I.F) k1_group_block(I, b - 5);
+    else {
+        const int warp = (b - 5 - I.F) * 4 + (threadIdx.x >> 5);
+        if (warp < I.F * I.F) k1_gateway_warp(I, warp, threadIdx.x & 31);
+    }
+#if defined(K1_PROFILE)
+    __syncthreads();
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (threadIdx.x == 0) printf("k1_phase1 block %d: %llu ns\n", b, t1 - t0);
+#endif
 }
 
 __device__ void k1_boundary_t(const DevInst& I, long long t) {
