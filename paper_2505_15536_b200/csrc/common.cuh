@@ -45,9 +45,6 @@ enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 
 #define K3_THREADS 256
 #define K3_TILE 256
 #define K3_SEG 32
-#ifndef K3_ILP2
-#define K3_ILP2 0
-#endif
 #ifndef K3S_THREADS
 #define K3S_THREADS 256
 #endif

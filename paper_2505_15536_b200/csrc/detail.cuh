@@ -113,8 +113,16 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
     // one warp: decode the arg-min key (cut positions by a 32-wide ballot
     // over the hockey-stick counts), then the warp plan detail
     const int lane = threadIdx.x & 31;
+    // the binomial columns the decode reads, staged once (independent loads
+    // overlap) instead of one dependent global round trip per probe
+    __shared__ unsigned long long bsm[(GP_MAX_LAYERS + 1) * (GP_MAX_STAGES + 1)];
+    for (int q = lane; q < (I.n + 1) * (k + 1); q += 32) {
+        const int nn = q / (k + 1), r = q % (k + 1);
+        bsm[q] = binom[(size_t)nn * (GP_MAX_STAGES + 1) + r];
+    }
     const Key key = *result;
     const unsigned long long e = *err;
+    __syncwarp();
     if (lane == 0) {
         out->key = key;
         out->err = e;
@@ -133,7 +141,7 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
     unsigned long long rem = pc % NC;
     int prev = 0;
     auto C = [&](int nn, int r) -> unsigned long long {
-        return (r < 0 || nn < 0) ? 0ull : binom[(size_t)nn * (GP_MAX_STAGES + 1) + r];
+        return (r < 0 || nn < 0) ? 0ull : bsm[nn * (k + 1) + r];
     };
     for (int j = 1; j < k; ++j) {
         const int r = k - 1 - j, lo = prev + 1;

@@ -437,28 +437,6 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
                 if (bi == 0 || c < cmin) { cmin = c; bmin = bi; }
             }
         };
-#if K3_ILP2
-        // two independent halves of the run in flight per lane (ILP): both
-        // evaluations are unconditional (clamped indices) so they interleave;
-        // the first minimum of the run is the first half's unless the second
-        // half's is strictly smaller
-        {
-            const int h = (len + 1) >> 1, lh = (lmax + 1) >> 1;
-            double c1 = INFINITY;
-            int i1 = -1, b1 = 0;
-            for (int i = 0; i < lh; ++i) {
-                const int ia = i < h ? i : (h > 0 ? h - 1 : 0);
-                const int ib = (h + i < len) ? h + i : ia;
-                double ca, cb;
-                int ba, bb;
-                eval_q(ia, ca, ba);
-                eval_q(ib, cb, bb);
-                if (i < h && (run_i < 0 || ca < run_c)) { run_c = ca; run_i = i; run_b = ba; }
-                if (h + i < len && (i1 < 0 || cb < c1)) { c1 = cb; i1 = h + i; b1 = bb; }
-            }
-            if (i1 >= 0 && (run_i < 0 || c1 < run_c)) { run_c = c1; run_i = i1; run_b = b1; }
-        }
-#else
         for (int i = 0; i < lmax; ++i) {
             if (i < len) {
                 double cmin; int bmin;
@@ -466,7 +444,6 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
                 if (run_i < 0 || cmin < run_c) { run_c = cmin; run_i = i; run_b = bmin; }
             }
         }
-#endif
         if (run_i >= 0 && run_c <= best_c) {
             unsigned long long tk = (rpre + (unsigned long long)(q0 + run_i - a - 1)) * NB + run_b;
             if (run_c < best_c || tk < best_t) { best_c = run_c; best_t = tk; }
