@@ -170,7 +170,7 @@ def extra_sections(eng, packed, total, local, args, world):
         return ev[0].elapsed_time(ev[1]) / reps
 
     # ---- K2: explicit batch of 2x10^7 random C4 candidates (> L2: HBM-bound)
-    N = 20_000_000
+    N = N_K2 = 20_000_000
     rng = np.random.default_rng(4)
     idx = rng.integers(0, total, size=N)
     order, counts, bm = decode_indices(80, 4, idx, composition_table(80, 4))
@@ -197,7 +197,7 @@ def extra_sections(eng, packed, total, local, args, world):
     cost_h = d_cost.cpu().numpy()
     feas = np.nonzero(np.isfinite(cost_h[:5_000_000]))[0][:200_000]
     NS = int(feas.size)
-    eng.sim_candidates(order[feas[:1000]], counts[feas[:1000]], bm[feas[:1000]], 1, 0.0)
+    eng.sim_candidates(order[feas], counts[feas], bm[feas], 1, 0.0)  # warm-up at full size
     t0 = time.perf_counter()
     msk, stk = eng.sim_candidates(order[feas], counts[feas], bm[feas], 1, 0.0)
     el = time.perf_counter() - t0
@@ -214,7 +214,7 @@ def extra_sections(eng, packed, total, local, args, world):
     bws = replan.bandwidth_matrices(p2, [instances.snapshot_multipliers(spec, j)
                                          for j in range(nsnap)])
     e2 = Engine(local).load(p2)
-    e2.replan_snapshots(bws[:64])
+    e2.replan_snapshots(bws)  # warm-up at full size (allocations outside the timed call)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     b2, s2 = e2.replan_snapshots(bws)
@@ -240,6 +240,37 @@ def extra_sections(eng, packed, total, local, args, world):
             O.argmin_range(p3, 0, c2_total, threads=args.cpu_threads or os.cpu_count())
         out["k6_snapshot_replan"]["cpu_port_ms_per_snapshot"] = (time.perf_counter() - t0) / 5 * 1e3
     e2.close()
+
+    # ---- C5: throughput vs batch size N
+    eng.load(packed)
+    sweep = {}
+    for N in (10**3, 10**4, 10**5, 10**6, total):
+        ms3 = timed(lambda: eng.argmin_range_async(0, N), 20)
+        sweep[str(N)] = {"k3_range_ms": ms3, "k3_candidates_per_s": N / (ms3 * 1e-3)}
+        if N <= N_K2:
+            ms2 = timed(lambda: eng.eval_batch_device(4, N, d_o.data_ptr(), d_c.data_ptr(),
+                                                      d_b.data_ptr(), d_cost.data_ptr(),
+                                                      d_st.data_ptr()), 20)
+            sweep[str(N)].update({"k2_explicit_ms": ms2, "k2_candidates_per_s": N / (ms2 * 1e-3)})
+    eng.argmin_fetch()
+    # N = 10^8: C4 under 9 bandwidth snapshots in one K6 launch
+    spec4s = instances.config("c4")
+    bw9 = replan.bandwidth_matrices(packed, [instances.snapshot_multipliers(spec4s, j)
+                                             for j in range(9)])
+    eng.replan_snapshots(bw9)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        eng.replan_snapshots(bw9)
+    el9 = (time.perf_counter() - t0) / 5
+    sweep[str(9 * total)] = {"k6_9_snapshots_host_call_ms": el9 * 1e3,
+                             "candidates_per_s": 9 * total / el9}
+    eng.load(packed)
+    out["c5_batch_sweep"] = {
+        "rows": sweep,
+        "note": "K3 over the first N ranks of C4 (device time per call, L2 warm), K2 over the "
+                "first N of the 2x10^7 random explicit C4 candidates, and N = 9 x C4 through "
+                "K6 (host call incl. H2D of the bandwidth matrices)"}
 
     # ---- K7: regroup C4 (64 devices) per p_t snapshot
     from paper_2505_15536_b200 import grouping as GR
