@@ -413,6 +413,18 @@ int gp_validate_schedules(gp_ctx *ctx, const gp_timing *timings, uint64_t n,
                           gp_violation *violations, uint32_t *n_violations, double *busy,
                           uint8_t *status);
 
+/*
+ * Group statistics and second level for a GIVEN first-level partition
+ * (fg_of_in[d] = group index in sorted-member-tuple order, n_fg_in groups):
+ * the FirstLevelGroup fields as group_first_level would build them and
+ * group_second_level per group (SURVEY App. D region-grouping sweep).
+ * Outputs as gp_group_snapshots for one snapshot.
+ */
+int gp_group_fixed(gp_ctx *ctx, uint32_t D, const double *p_t, const double *bandwidth,
+                   const double *p_c, const uint16_t *fg_of_in, uint32_t n_fg_in,
+                   double threshold_compute, uint16_t *sg_of, uint32_t *n_sg, double *fg_intra,
+                   double *fg_capacity, double *fg_min_bw, double *sg_capacity);
+
 /* Same with device pointers, asynchronous on the context's stream. */
 int gp_sim_1f1b_device(gp_ctx *ctx, const gp_timing *d_timings, uint64_t n,
                        uint32_t iterations, double *d_makespan, uint8_t *d_status);

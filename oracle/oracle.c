@@ -1664,27 +1664,15 @@ static int og_agglomerate(const og_ctx *c, const int *items, int n, double thr, 
     return na;
 }
 
-/* group_first_level + group_second_level (src/grouping.py:146-228) for one
- * topology given in rank order: fg_of[d], sg_of[d] (index within the FG),
- * per FG (index f < *n_fg): intra_metric (NaN for singletons),
- * aggregate_capacity, min_intra_bandwidth (NaN for singletons); per SG in
- * FG-major order: aggregate_capacity.  Returns GP_OK / GP_ERR_INPUT. */
-int or_group_hierarchy(int D, const double *pt, const double *bw, const double *pc,
-                       double thr_net, double thr_comp, uint16_t *fg_of, uint16_t *sg_of,
-                       uint32_t *n_fg, uint32_t *n_sg, double *fg_intra, double *fg_cap,
-                       double *fg_minbw, double *sg_cap)
+/* group statistics + group_second_level for a given first-level partition
+ * gof[d] in sorted-member-tuple order (shared by or_group_hierarchy and the
+ * fixed-partition sweep) */
+static int og_second_levels(int D, const double *pt, const double *bw, const double *pc,
+                            double thr_comp, const int *gof, int nf, uint16_t *fg_of,
+                            uint16_t *sg_of, uint32_t *n_sg, double *fg_intra, double *fg_cap,
+                            double *fg_minbw, double *sg_cap)
 {
-    if (D < 1)
-        return GP_ERR_INPUT;  /* EmptyClusterError */
-    if (!(thr_net > 0 && thr_net < 1) || !(thr_comp > 0 && thr_comp < 1))
-        return GP_ERR_INPUT;  /* ValueError */
     og_ctx c1 = {1, D, pt, pc};
-    int *items = (int *)malloc((size_t)D * sizeof(int));
-    int *gof = (int *)malloc((size_t)D * sizeof(int));
-    for (int d = 0; d < D; ++d)
-        items[d] = d;
-    int nf = og_agglomerate(&c1, items, D, thr_net, gof);
-    *n_fg = (uint32_t)nf;
     uint32_t sg_base = 0;
     int *mem = (int *)malloc((size_t)D * sizeof(int));
     int *sgo = (int *)malloc((size_t)D * sizeof(int));
@@ -1726,12 +1714,55 @@ int or_group_hierarchy(int D, const double *pt, const double *bw, const double *
         sg_base += (uint32_t)ns;
     }
     *n_sg = sg_base;
-    free(items);
-    free(gof);
     free(mem);
     free(sgo);
     free(tmp);
     return GP_OK;
+}
+
+int or_group_fixed(int D, const double *pt, const double *bw, const double *pc, const uint16_t *fg_in,
+                   int nf, double thr_comp, uint16_t *sg_of, uint32_t *n_sg, double *fg_intra,
+                   double *fg_cap, double *fg_minbw, double *sg_cap)
+{
+    if (D < 1 || nf < 1 || !(thr_comp > 0 && thr_comp < 1))
+        return GP_ERR_INPUT;
+    int *gof = (int *)malloc((size_t)D * sizeof(int));
+    uint16_t *fg_of = (uint16_t *)malloc((size_t)D * sizeof(uint16_t));
+    for (int d = 0; d < D; ++d)
+        gof[d] = fg_in[d];
+    int st = og_second_levels(D, pt, bw, pc, thr_comp, gof, nf, fg_of, sg_of, n_sg, fg_intra, fg_cap,
+                              fg_minbw, sg_cap);
+    free(gof);
+    free(fg_of);
+    return st;
+}
+
+/* group_first_level + group_second_level (src/grouping.py:146-228) for one
+ * topology given in rank order: fg_of[d], sg_of[d] (index within the FG),
+ * per FG (index f < *n_fg): intra_metric (NaN for singletons),
+ * aggregate_capacity, min_intra_bandwidth (NaN for singletons); per SG in
+ * FG-major order: aggregate_capacity.  Returns GP_OK / GP_ERR_INPUT. */
+int or_group_hierarchy(int D, const double *pt, const double *bw, const double *pc,
+                       double thr_net, double thr_comp, uint16_t *fg_of, uint16_t *sg_of,
+                       uint32_t *n_fg, uint32_t *n_sg, double *fg_intra, double *fg_cap,
+                       double *fg_minbw, double *sg_cap)
+{
+    if (D < 1)
+        return GP_ERR_INPUT;  /* EmptyClusterError */
+    if (!(thr_net > 0 && thr_net < 1) || !(thr_comp > 0 && thr_comp < 1))
+        return GP_ERR_INPUT;  /* ValueError */
+    og_ctx c1 = {1, D, pt, pc};
+    int *items = (int *)malloc((size_t)D * sizeof(int));
+    int *gof = (int *)malloc((size_t)D * sizeof(int));
+    for (int d = 0; d < D; ++d)
+        items[d] = d;
+    int nf = og_agglomerate(&c1, items, D, thr_net, gof);
+    *n_fg = (uint32_t)nf;
+    int st = og_second_levels(D, pt, bw, pc, thr_comp, gof, nf, fg_of, sg_of, n_sg, fg_intra,
+                               fg_cap, fg_minbw, sg_cap);
+    free(items);
+    free(gof);
+    return st;
 }
 
 

@@ -75,6 +75,10 @@ def lib():
                                          C.c_double, C.c_double, P(C.c_uint16), P(C.c_uint16),
                                          P(C.c_uint32), P(C.c_uint32), P(C.c_double),
                                          P(C.c_double), P(C.c_double), P(C.c_double)]
+        L.or_group_fixed.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(C.c_double),
+                                     P(C.c_uint16), C.c_int, C.c_double, P(C.c_uint16),
+                                     P(C.c_uint32), P(C.c_double), P(C.c_double), P(C.c_double),
+                                     P(C.c_double)]
         _lib = L
     return _lib
 
@@ -264,3 +268,25 @@ def validate_schedule(timing_struct, ops, n, makespan, tol=1e-9, max_violations=
     lib().or_validate_schedule(C.byref(timing_struct), ops, int(n), float(makespan), float(tol),
                                max_violations, out, C.byref(nv), _dp(busy))
     return [out[i] for i in range(min(nv.value, max_violations))], nv.value, busy
+
+
+def group_fixed(pt, bw, pc, fg_of, n_fg, thr_comp=0.3):
+    """(status, grouping.Hierarchy) for a given first-level partition
+    (fg_of in sorted-member-tuple order): group statistics + second level."""
+    from paper_2505_15536_b200.grouping import Hierarchy
+    pt = np.ascontiguousarray(pt, dtype=np.float64)
+    bw = np.ascontiguousarray(bw, dtype=np.float64)
+    pc = np.ascontiguousarray(pc, dtype=np.float64)
+    fg = np.ascontiguousarray(fg_of, dtype=np.uint16)
+    n = len(pc)
+    sg_of = np.zeros(n, np.uint16)
+    ns = C.c_uint32(0)
+    fi = np.zeros(max(n, 1)); fc = np.zeros(max(n, 1)); fb = np.zeros(max(n, 1))
+    sc = np.zeros(max(n, 1))
+    u16 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint16))
+    st = lib().or_group_fixed(n, _dp(pt), _dp(bw), _dp(pc), u16(fg), int(n_fg), float(thr_comp),
+                              u16(sg_of), C.byref(ns), _dp(fi), _dp(fc), _dp(fb), _dp(sc))
+    if st:
+        return st, None
+    return st, Hierarchy(fg.copy(), sg_of, fi[:n_fg].copy(), fc[:n_fg].copy(), fb[:n_fg].copy(),
+                         sc[:ns.value].copy())

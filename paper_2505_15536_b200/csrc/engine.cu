@@ -1821,11 +1821,12 @@ int gp_diag_fp64_peak(int device, double* dadd_per_second) {
 // ----------------------------------------------------------------------------
 // K7: device grouping per topology snapshot
 // ----------------------------------------------------------------------------
-extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_t,
-                                  const double* bandwidth, const double* p_c, double threshold_net,
-                                  double threshold_compute, uint16_t* fg_of, uint16_t* sg_of,
-                                  uint32_t* n_fg, uint32_t* n_sg, double* fg_intra,
-                                  double* fg_capacity, double* fg_min_bw, double* sg_capacity) {
+static int group_launch(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_t,
+                        const double* bandwidth, const double* p_c, double threshold_net,
+                        double threshold_compute, const uint16_t* fixed_fg, uint32_t fixed_nf,
+                        uint16_t* fg_of, uint16_t* sg_of, uint32_t* n_fg, uint32_t* n_sg,
+                        double* fg_intra, double* fg_capacity, double* fg_min_bw,
+                        double* sg_capacity) {
     if (!c || !p_t || !p_c || !fg_of || !sg_of || !n_fg || !n_sg || !fg_intra || !fg_capacity ||
         !fg_min_bw || !sg_capacity)
         return fail(GP_ERR_INPUT, "bad arguments");
@@ -1845,7 +1846,8 @@ extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const 
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t o_pt = 0, o_bw = o_pt + al(SB * DD * 8), o_pc = o_bw + al(bandwidth ? SB * DD * 8 : 8);
     const size_t o_u16 = o_pc + al((size_t)D * 8), o_cnt = o_u16 + al((size_t)SB * D * 2 * 2);
-    const size_t o_dbl = o_cnt + al((size_t)SB * 2 * 4), o_scr = o_dbl + al((size_t)SB * D * 4 * 8);
+    const size_t o_dbl = o_cnt + al((size_t)SB * 2 * 4), o_fix = o_dbl + al((size_t)SB * D * 4 * 8);
+    const size_t o_scr = o_fix + al((size_t)D * 2);
     const size_t total = o_scr + SB * per_scr;
     CUDA_TRY(c->g_buf.ensure(total));
     uint8_t* b = c->g_buf.p;
@@ -1858,6 +1860,7 @@ extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const 
     { int ps_ = 0, st_ = kernel_slots(c, (const void*)k7_group, K7_THREADS, smem, &ps_);
       if (st_ != GP_OK) return st_; }
     CUDA_TRY(cudaMemcpyAsync(b + o_pc, p_c, (size_t)D * 8, cudaMemcpyHostToDevice, s));
+    if (fixed_fg) CUDA_TRY(cudaMemcpyAsync(b + o_fix, fixed_fg, (size_t)D * 2, cudaMemcpyHostToDevice, s));
     for (uint32_t s0 = 0; s0 < n_snap; s0 += SB) {
         const uint32_t nb = (n_snap - s0) < SB ? (n_snap - s0) : SB;
         CUDA_TRY(cudaMemcpyAsync(b + o_pt, p_t + (size_t)s0 * DD, nb * DD * 8, cudaMemcpyHostToDevice, s));
@@ -1875,8 +1878,9 @@ extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const 
             (int)D, reinterpret_cast<const double*>(b + o_pt),
             bandwidth ? reinterpret_cast<const double*>(b + o_bw) : nullptr, (long long)DD,
             (long long)DD, reinterpret_cast<const double*>(b + o_pc), threshold_net,
-            threshold_compute, b + o_scr, per_scr, smem_mode, d_fg, d_sg, d_nf, d_ns, d_fi, d_fc,
-            d_fb, d_sc);
+            threshold_compute, b + o_scr, per_scr, smem_mode,
+            fixed_fg ? reinterpret_cast<const uint16_t*>(b + o_fix) : nullptr, (int)fixed_nf, d_fg,
+            d_sg, d_nf, d_ns, d_fi, d_fc, d_fb, d_sc);
         CUDA_TRY(cudaGetLastError());
         const size_t o = (size_t)s0 * D;
         CUDA_TRY(cudaMemcpyAsync(fg_of + o, d_fg, (size_t)nb * D * 2, cudaMemcpyDeviceToHost, s));
@@ -1890,4 +1894,33 @@ extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const 
         CUDA_TRY(cudaStreamSynchronize(s));  // staging buffers are reused by the next batch
     }
     return GP_OK;
+}
+
+extern "C" int gp_group_snapshots(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_t,
+                                  const double* bandwidth, const double* p_c, double threshold_net,
+                                  double threshold_compute, uint16_t* fg_of, uint16_t* sg_of,
+                                  uint32_t* n_fg, uint32_t* n_sg, double* fg_intra,
+                                  double* fg_capacity, double* fg_min_bw, double* sg_capacity) {
+    return group_launch(c, D, n_snap, p_t, bandwidth, p_c, threshold_net, threshold_compute,
+                        nullptr, 0, fg_of, sg_of, n_fg, n_sg, fg_intra, fg_capacity, fg_min_bw,
+                        sg_capacity);
+}
+
+extern "C" int gp_group_fixed(gp_ctx* c, uint32_t D, const double* p_t, const double* bandwidth,
+                              const double* p_c, const uint16_t* fg_of_in, uint32_t n_fg_in,
+                              double threshold_compute, uint16_t* sg_of, uint32_t* n_sg,
+                              double* fg_intra, double* fg_capacity, double* fg_min_bw,
+                              double* sg_capacity) {
+    if (!fg_of_in || n_fg_in == 0 || n_fg_in > D) return fail(GP_ERR_INPUT, "bad first-level partition");
+    std::vector<uint32_t> cnt(n_fg_in, 0);
+    for (uint32_t d = 0; d < D; ++d) {
+        if (fg_of_in[d] >= n_fg_in) return fail(GP_ERR_INPUT, "device %u: group index out of range", d);
+        cnt[fg_of_in[d]]++;
+    }
+    for (uint32_t f = 0; f < n_fg_in; ++f) if (!cnt[f]) return fail(GP_ERR_INPUT, "group %u is empty", f);
+    std::vector<uint16_t> fg_out(D);
+    uint32_t nf = 0;
+    return group_launch(c, D, 1, p_t, bandwidth, p_c, 0.5, threshold_compute, fg_of_in, n_fg_in,
+                        fg_out.data(), sg_of, &nf, n_sg, fg_intra, fg_capacity, fg_min_bw,
+                        sg_capacity);
 }

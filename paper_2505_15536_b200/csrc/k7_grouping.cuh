@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(K7_THREADS)
 k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw_all,
          long long pt_stride, long long bw_stride, const double* __restrict__ pc, double thr_net,
          double thr_comp, uint8_t* __restrict__ scratch, size_t scratch_per, int smem_mode,
-         uint16_t* fg_of_all,
+         const uint16_t* __restrict__ fixed_fg, int fixed_nf, uint16_t* fg_of_all,
          uint16_t* sg_of_all, uint32_t* n_fg, uint32_t* n_sg, double* fg_intra_all,
          double* fg_cap_all, double* fg_minbw_all, double* sg_cap_all) {
     extern __shared__ __align__(16) uint8_t k7_smem[];
@@ -329,7 +329,16 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
 
     for (int d = tid; d < D; d += blockDim.x) items[d] = (uint16_t)d;
     __syncthreads();
-    const int nf = k7_agglomerate(1, D, items, pt, pc, D, thr_net, g, sh, gof, s_ab, s_red, s_ia);
+    // first level: agglomerated, or given (a fixed partition, e.g. the C2
+    // region-grouping sweep; indices already in sorted-member-tuple order)
+    int nf;
+    if (fixed_fg) {
+        for (int d = tid; d < D; d += blockDim.x) gof[d] = fixed_fg[d];
+        __syncthreads();
+        nf = fixed_nf;
+    } else {
+        nf = k7_agglomerate(1, D, items, pt, pc, D, thr_net, g, sh, gof, s_ab, s_red, s_ia);
+    }
     for (int d = tid; d < D; d += blockDim.x) fg_of[d] = gof[d];
     __syncthreads();
     int sg_base = 0;

@@ -81,6 +81,9 @@ def lib():
                                          P(C.c_double), P(C.c_double), C.c_double, C.c_double,
                                          u16p, u16p, P(C.c_uint32), P(C.c_uint32), P(C.c_double),
                                          P(C.c_double), P(C.c_double), P(C.c_double)]
+        L.gp_group_fixed.argtypes = [vp, C.c_uint32, P(C.c_double), P(C.c_double), P(C.c_double),
+                                     u16p, C.c_uint32, C.c_double, u16p, P(C.c_uint32),
+                                     P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double)]
         L.gp_replan_snapshots.argtypes = [vp, P(C.c_double), C.c_uint32, P(abi.GpBest),
                                           P(C.c_int32)]
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
@@ -356,6 +359,24 @@ class Engine:
             _check(lib().gp_plan_timing(self._h, k, n, _u8(order), _u8(counts), _u8(bm),
                                         float(opt_seconds), out, _u8(st)))
         return out, st
+
+    def group_fixed(self, p_t, bandwidth, p_c, fg_of, n_fg: int, threshold_compute=0.3):
+        """Statistics + second level of a given first-level partition (rank order)."""
+        p_t = np.ascontiguousarray(p_t, dtype=np.float64)
+        D = p_t.shape[0]
+        bw = np.ascontiguousarray(bandwidth, dtype=np.float64) if bandwidth is not None else None
+        pc = np.ascontiguousarray(p_c, dtype=np.float64)
+        fg = np.ascontiguousarray(fg_of, dtype=np.uint16)
+        sg_of = np.zeros(D, np.uint16)
+        ns = C.c_uint32(0)
+        fi, fc, fb, sc = (np.zeros(D) for _ in range(4))
+        P = C.POINTER
+        dp = lambda a: a.ctypes.data_as(P(C.c_double))
+        u16 = lambda a: a.ctypes.data_as(P(C.c_uint16))
+        _check(lib().gp_group_fixed(self._h, D, dp(p_t), dp(bw) if bw is not None else None, dp(pc),
+                                    u16(fg), int(n_fg), float(threshold_compute), u16(sg_of),
+                                    C.byref(ns), dp(fi), dp(fc), dp(fb), dp(sc)))
+        return sg_of, ns.value, fi[:n_fg], fc[:n_fg], fb[:n_fg], sc[:ns.value]
 
     def sim_candidates(self, order, counts, bm, iterations: int = 1, opt_seconds: float = 0.0):
         """1F1B makespans of explicit candidates of the loaded instance."""

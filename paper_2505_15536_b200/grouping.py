@@ -125,3 +125,28 @@ def regroup_snapshots(topology, p_t_snapshots, bandwidth_snapshots=None,
     bws = bw0 if bandwidth_snapshots is None else np.asarray(bandwidth_snapshots, np.float64)
     hs = group_hierarchies(pts, bws, pc, threshold_net, threshold_compute, engine)
     return [to_groups(ids, h) for h in hs]
+
+
+def fixed_hierarchy(topology, blocks: Sequence[Sequence[str]], threshold_compute: float = 0.3,
+                    engine=None):
+    """(fgs, sgs_by_fg, GroupIndex) for a GIVEN partition of the devices into
+    first-level groups (``blocks`` of device ids): FirstLevelGroup fields as
+    ``group_first_level`` builds them (sorted member tuples, ids over the
+    sorted tuples, src/grouping.py:179-189) and ``group_second_level`` per
+    group - on the GPU (SURVEY App. D region-grouping sweep)."""
+    from .engine import default_engine
+    eng = engine if engine is not None else default_engine()
+    ids, pt, bw, pc = topology_arrays(topology)
+    pos = {d: i for i, d in enumerate(ids)}
+    tuples = sorted(tuple(sorted(b)) for b in blocks)
+    fg_of = np.full(len(ids), 0xffff, np.uint16)
+    for f, members in enumerate(tuples):
+        for d in members:
+            if fg_of[pos[d]] != 0xffff:
+                raise D.InputFileError(f"device {d} in two groups")
+            fg_of[pos[d]] = f
+    if (fg_of == 0xffff).any():
+        raise D.InputFileError("partition does not cover every device")
+    sg_of, ns, fi, fc, fb, sc = eng.group_fixed(pt, bw, pc, fg_of, len(tuples), threshold_compute)
+    h = Hierarchy(fg_of, sg_of, fi, fc, fb, sc)
+    return to_groups(ids, h)

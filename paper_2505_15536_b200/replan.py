@@ -123,3 +123,49 @@ def replan_regrouped(model, topology, config, p_t_snapshots, bandwidth_snapshots
         except D.GeopipeError as e:
             out.append((e, gi))
     return out
+
+
+def set_partitions(r: int):
+    """Set partitions of r labelled blocks as restricted-growth strings in
+    lexicographic order ({abc}, {ab|c}, {ac|b}, {a|bc}, {a|b|c} for r = 3)."""
+    out = []
+
+    def rec(prefix, top):
+        if len(prefix) == r:
+            out.append(list(prefix))
+            return
+        for v in range(top + 2):
+            rec(prefix + [v], max(top, v))
+    rec([0], 0)
+    return out
+
+
+def region_grouping_sweep(model, topology, regions: Sequence[Sequence[str]], config,
+                          threshold_compute: float = 0.3, engine: Optional[Engine] = None):
+    """C2 region-grouping sweep: for every set partition of the
+    regions (restricted-growth order), first-level groups = unions of the
+    regions of a block (built as group_first_level would), second level by
+    group_second_level, then one exact exhaustive_plan.  Returns
+    ``(results, best)``: per grouping ``(blocks, SearchResult | exception)``
+    and the index of the sweep optimum, the minimum of
+    ``(cost, grouping index)`` (ties inside a grouping are already broken by
+    exhaustive_plan's key)."""
+    from .grouping import fixed_hierarchy
+    from .planner import exhaustive_plan
+    eng = engine or default_engine()
+    results = []
+    best = None
+    for gi, rgs in enumerate(set_partitions(len(regions))):
+        blocks = [sorted(d for r, b in zip(regions, rgs) if b == v for d in r)
+                  for v in range(max(rgs) + 1)]
+        _, _, groups = fixed_hierarchy(topology, blocks, threshold_compute, engine=eng)
+        try:
+            res = exhaustive_plan(model, topology, groups, config, engine=eng)
+        except D.GeopipeError as e:
+            results.append((blocks, e))
+            continue
+        results.append((blocks, res))
+        key = (res.breakdown.plan_cost, gi)
+        if best is None or key < best[0]:
+            best = (key, gi)
+    return results, (best[1] if best is not None else None)

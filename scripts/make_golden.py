@@ -365,6 +365,7 @@ def main():
     dump_schedules()
     dump_cli()
     dump_plan_costs()
+    dump_region_sweep()
     dump_regroup_replan()
 
     for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
@@ -713,6 +714,45 @@ def dump_plan_costs():
         out[name] = rows
     G.save("plan_costs.json", out)
     print(f"plan costs: {time.time() - t0:.1f}s", flush=True)
+
+
+def dump_region_sweep():
+    """C2 region-grouping sweep with the reference: groups built
+    as group_first_level would for each set partition of the regions, then
+    group_second_level and exhaustive_plan."""
+    gp = geopipe()
+    from geopipe.grouping import FirstLevelGroup, _mean_intra_pt, _min_intra_bw
+    from geopipe.timing import GroupIndex
+    from paper_2505_15536_b200.replan import set_partitions
+    spec = I.config("c2")
+    model, topo, _ = build_reference(spec)
+    regions = {}
+    for i, r, _, _, _ in spec.devices():
+        regions.setdefault(r, []).append(i)
+    regs = [regions[r] for r in sorted(regions)]
+    out = {"regions": regs, "groupings": []}
+    t0 = time.time()
+    for rgs in set_partitions(len(regs)):
+        blocks = [sorted(d for rr, b in zip(regs, rgs) if b == v for d in rr)
+                  for v in range(max(rgs) + 1)]
+        tuples = sorted(tuple(sorted(b)) for b in blocks)
+        fgs = [FirstLevelGroup(id=f"fg{idx}", member_device_ids=m,
+                               intra_metric=_mean_intra_pt(m, topo),
+                               aggregate_capacity=sum(topo.p_c(x) for x in m),
+                               min_intra_bandwidth=_min_intra_bw(m, topo))
+               for idx, m in enumerate(tuples)]
+        sgs = {fg.id: gp.group_second_level(fg, topo, 0.3) for fg in fgs}
+        groups = GroupIndex.build(fgs, sgs)
+        rec = {"rgs": rgs, "blocks": blocks,
+               "fgs": [[fg.id, list(fg.member_device_ids), fg.intra_metric, fg.aggregate_capacity,
+                        fg.min_intra_bandwidth] for fg in fgs],
+               "sgs": {f: [[sg.id, list(sg.member_device_ids), sg.aggregate_capacity] for sg in v]
+                       for f, v in sgs.items()}}
+        rec.update(run_or_error(lambda: gp.exhaustive_plan(model, topo, groups,
+                                                           gp.SearchConfig(seed=0))))
+        out["groupings"].append(rec)
+    G.save("region_sweep.json", out)
+    print(f"region sweep: {time.time() - t0:.1f}s", flush=True)
 
 
 def dump_regroup_replan():

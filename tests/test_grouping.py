@@ -133,3 +133,63 @@ def test_regroup_then_replan_matches_reference(engine):
         assert got["breakdown"] == exp["result"]["breakdown"]
         ks.add(len(gi.fgs))
     assert ks == {3, 4}
+
+
+# ------------------------------------------------ C2 region-grouping sweep --
+SWEEP = G.load("region_sweep.json")
+
+
+def _sweep_arrays():
+    from paper_2505_15536_b200 import instances as I
+    _, topo, _ = I.load("c2")
+    ids, pt, bw, pc = GR.topology_arrays(topo)
+    return topo, ids, pt, bw, pc
+
+
+def test_set_partitions_order():
+    from paper_2505_15536_b200.replan import set_partitions
+    assert set_partitions(3) == [[0, 0, 0], [0, 0, 1], [0, 1, 0], [0, 1, 1], [0, 1, 2]]
+    assert len(set_partitions(4)) == 15 and [g["rgs"] for g in SWEEP["groupings"]] == set_partitions(3)
+
+
+@pytest.mark.parametrize("gi", range(5))
+def test_oracle_fixed_partition_matches_reference(oracle_lib, gi):
+    topo, ids, pt, bw, pc = _sweep_arrays()
+    g = SWEEP["groupings"][gi]
+    pos = {d: i for i, d in enumerate(ids)}
+    fg_of = np.zeros(len(ids), np.uint16)
+    for f, (_, members, *_r) in enumerate(g["fgs"]):
+        for d in members:
+            fg_of[pos[d]] = f
+    st, h = oracle_lib.group_fixed(pt, bw, pc, fg_of, len(g["fgs"]))
+    assert st == 0
+    fgs, sgs, _ = GR.to_groups(ids, h)
+    for fg, (fid, members, intra, cap, mb) in zip(fgs, g["fgs"]):
+        assert (fg.id, list(fg.member_device_ids), fg.aggregate_capacity) == (fid, members, cap)
+        assert (fg.intra_metric, fg.min_intra_bandwidth) == (intra, mb)
+        assert [[s.id, list(s.member_device_ids), s.aggregate_capacity] for s in sgs[fid]] == \
+            g["sgs"][fid]
+
+
+@pytest.mark.gpu
+def test_region_grouping_sweep_matches_reference(engine):
+    from paper_2505_15536_b200 import instances as I
+    from paper_2505_15536_b200.replan import region_grouping_sweep
+    model, topo, _ = I.load("c2")
+    results, best = region_grouping_sweep(model, topo, SWEEP["regions"], D.SearchConfig(seed=0),
+                                          engine=engine)
+    evaluated = 0
+    for (blocks, r), g in zip(results, SWEEP["groupings"]):
+        assert blocks == g["blocks"]
+        if "error" in g:
+            assert type(r).__name__ == g["error"]
+            continue
+        got = G.normalize_result(r)
+        assert got["plan"] == g["result"]["plan"]
+        assert got["breakdown"] == g["result"]["breakdown"]
+        assert r.evaluated == g["result"]["evaluated"]
+        evaluated += r.evaluated
+    assert evaluated == 3 * 372 + 16740
+    costs = [(g["result"]["breakdown"]["plan_cost"], i) for i, g in enumerate(SWEEP["groupings"])
+             if "result" in g]
+    assert best == min(costs)[1]
