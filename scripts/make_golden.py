@@ -366,6 +366,7 @@ def main():
     dump_cli()
     dump_plan_costs()
     dump_region_sweep()
+    dump_search_seeds()
     dump_regroup_replan()
 
     for name, cfg_name, jit in [("c1", "c1", False), ("c1j", "c1", True),
@@ -714,6 +715,21 @@ def dump_plan_costs():
         out[name] = rows
     G.save("plan_costs.json", out)
     print(f"plan costs: {time.time() - t0:.1f}s", flush=True)
+
+
+def dump_search_seeds():
+    """search_plan of the reference for seeds 0-20 on C1-C4 (integer and
+    jittered), the SURVEY §8(c) parity protocol (3)."""
+    gp = geopipe()
+    out = {}
+    t0 = time.time()
+    for name in ("c1", "c1j", "c2", "c2j", "c4", "c4j"):
+        model, topo, groups = build_reference(I.config(name[:2], name.endswith("j")))
+        out[name] = {str(s): run_or_error(lambda: gp.search_plan(model, topo, groups,
+                                                                 gp.SearchConfig(seed=s)))
+                     for s in range(21)}
+        print(f"search seeds {name}: {time.time() - t0:.1f}s", flush=True)
+    G.save("search_seeds.json", out)
 
 
 def dump_region_sweep():

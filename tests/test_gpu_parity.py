@@ -195,3 +195,17 @@ def test_space_overflow_is_an_error(engine):
     engine.load(PackedInstance(model, topo, groups, 1.25))
     with pytest.raises(P.InputFileError):
         engine.space_size()
+
+
+# search_plan for seeds 0-20 on C1-C4 (SURVEY §8(c) parity protocol (3))
+SEEDS = G.load("search_seeds.json")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(SEEDS))
+def test_search_plan_seeds_0_to_20(engine, name):
+    from paper_2505_15536_b200 import instances as I
+    model, topo, groups = I.load(name[:2], name.endswith("j"))
+    for seed, exp in SEEDS[name].items():
+        res = P.search_plan(model, topo, groups, P.SearchConfig(seed=int(seed)), engine=engine)
+        assert G.normalize_result(res) == exp["result"], (name, seed)
