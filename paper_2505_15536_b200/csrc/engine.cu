@@ -615,6 +615,45 @@ static SwFn pick_sweep(int mode, int nb, int k) {
     return (mode == 2 && k >= 3 && k <= 6) ? fixed[nb - 1][k - 3] : table[mode][nb - 1];
 }
 
+// Sweep launch.  With GP_K3_CLUSTER=c (2 or 4, dividing the CTAs per item)
+// the CTAs of one item form a thread-block cluster and the item's tables are
+// fetched once and multicast into every member (TMA .multicast::cluster).
+// Measured on C4 (profiles/README.md): cluster 2 = no change (36.9 us),
+// cluster 4 = 51 us (72 clusters of 4 x 113 KB do not co-schedule in one wave
+// across the GPCs), so the default is a plain launch.
+static cudaError_t launch_sweep_kernel(SwFn kern, unsigned grid, size_t smem, cudaStream_t s,
+                                       SweepGeom& G, const DevInst& I, const ArgminScratch& S,
+                                       const unsigned long long* binom, const uint32_t* flags) {
+    int cs = 1;
+    if (const char* e = getenv("GP_K3_CLUSTER")) cs = atoi(e) > 0 ? atoi(e) : 1;
+    if (cs > 1 && (G.cpi % cs != 0)) cs = 1;
+    G.csize = cs;
+    if (cs == 1) {
+        kern<<<grid, K3S_THREADS, smem, s>>>(I, G, S, binom, flags);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(K3S_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, I, G, S, binom, flags);
+    if (e != cudaSuccess) {  // cluster not schedulable here: plain launch, no multicast
+        (void)cudaGetLastError();
+        G.csize = 1;
+        kern<<<grid, K3S_THREADS, smem, s>>>(I, G, S, binom, flags);
+        e = cudaGetLastError();
+    }
+    return e;
+}
+
 // cudaFuncSetAttribute + occupancy query, once per (device, kernel, dynamic
 // smem).  The attribute is process-wide per kernel and device, so the cache
 // is too, and the attribute only ever grows (every cached size stays
@@ -697,8 +736,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     S.err_idx = c->err_idx.p;
     c->last_geom = R;
     DevInst I = c->view();
-    kern<<<(unsigned)grid, K3S_THREADS, smem, s>>>(I, G, S, c->binom.p, dflags);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_sweep_kernel(kern, (unsigned)grid, smem, s, G, I, S, c->binom.p, dflags));
     return GP_OK;
 }
 
@@ -1632,7 +1670,8 @@ int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_
         S.result = c->z_res.p;
         S.err = nullptr;
         S.err_idx = c->err_idx.p;
-        kern<<<(unsigned)grid, K3S_THREADS, smem, s>>>(I, G, S, c->binom.p, c->z_flags.p);
+        CUDA_TRY(launch_sweep_kernel(kern, (unsigned)grid, smem, s, G, I, S, c->binom.p,
+                                     c->z_flags.p));
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaMemcpyAsync(h_res.data(), c->z_res.p, nb * sizeof(Key), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaMemcpyAsync(h_fl.data(), c->z_flags.p, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));

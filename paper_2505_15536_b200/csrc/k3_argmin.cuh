@@ -252,8 +252,12 @@ struct SweepGeom {
     const double* xt;
     unsigned long long s_tpk, s_tcol, s_xt;  // per-snapshot strides (elements)
     const unsigned long long* bnk;  // C(nn, r), nn <= n, r <= k: contiguous [n+1][k+1]
+    int csize;                      // thread-block cluster size (CTAs of one item), 1 = none
 };
 
+#if defined(K3_PROFILE)
+__device__ __forceinline__ unsigned __nv_smid_k3() { unsigned r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
+#endif
 // KS > 0 fixes the stage count at compile time (cut arrays in registers,
 // no local memory); KS = 0 is the generic kernel.
 template <int MODE, int NB, int KS>
@@ -261,6 +265,9 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
                                                           const unsigned long long* __restrict__ binom,
                                                           const uint32_t* skip_if_flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+#if defined(K3_PROFILE)
+    unsigned long long t0p; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0p));
+#endif
     const int n = I.n, k = KS > 0 ? KS : G.k;
     const int ntri = n * (n + 1) / 2;
     const int KB = k + 1;
@@ -298,29 +305,44 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     double2* row0 = (double2*)(x23s + (MODE >= 1 ? I.nxp : 0));
     double* x01s = (double*)(row0 + (MODE >= 1 ? n : 0));
     double2* tri1 = (double2*)(x01s + (MODE >= 1 ? I.nxp : 0));
+    // every table this CTA reads arrives by bulk async copy on one mbarrier;
+    // with a cluster (the CTAs of one item), the cluster's rank 0 issues each
+    // copy once, multicast into every member's shared memory
+    const uint32_t bn_bytes = (uint32_t)(((size_t)(n + 1) * KB * 8 + 15) & ~(size_t)15);
+    uint32_t bytes = bn_bytes + (uint32_t)G.ngroups * 16;
+    if (MODE >= 1)
+        bytes += (uint32_t)(ntri * 16 + (n + 1) * 16 + 3 * I.nxp * 8 + n * 16) +
+                 (MODE == 2 ? (uint32_t)ntri * 16 : 0u);
+    const bool mc = G.csize > 1;
     if (threadIdx.x == 0) {
-        // every table this CTA reads arrives by bulk async copy on one mbarrier
-        const uint32_t bn_bytes = (uint32_t)(((size_t)(n + 1) * KB * 8 + 15) & ~(size_t)15);
-        uint32_t bytes = bn_bytes + (uint32_t)G.ngroups * 16;
-        if (MODE >= 1)
-            bytes += (uint32_t)(ntri * 16 + (n + 1) * 16 + 3 * I.nxp * 8 + n * 16) +
-                     (MODE == 2 ? (uint32_t)ntri * 16 : 0u);
         mbar_init(bar, 1);
         mbar_expect_tx(bar, bytes);
-        tma_bulk_g2s(bn, G.bnk, bn_bytes, bar);
-        tma_bulk_g2s(grp, G.groups, (uint32_t)G.ngroups * 16, bar);
+    }
+    if (mc) { cluster_arrive(); cluster_wait(); }  // every member's mbarrier is armed
+    if (threadIdx.x == 0 && (!mc || cluster_ctarank() == 0)) {
+        const uint16_t mask = (uint16_t)((1u << G.csize) - 1u);
+        auto copy = [&](void* dst, const void* src, uint32_t nb) {
+            if (mc) tma_bulk_g2s_mc(dst, src, nb, bar, mask);
+            else tma_bulk_g2s(dst, src, nb, bar);
+        };
+        copy(bn, G.bnk, bn_bytes);
+        copy(grp, G.groups, (uint32_t)G.ngroups * 16);
         if (MODE >= 1) {
-            tma_bulk_g2s(tri2, P2, (uint32_t)ntri * 16, bar);
-            tma_bulk_g2s(col3, C3, (uint32_t)(n + 1) * 16, bar);
-            tma_bulk_g2s(x12s, X12, (uint32_t)I.nxp * 8, bar);
-            tma_bulk_g2s(x23s, X23, (uint32_t)I.nxp * 8, bar);
-            tma_bulk_g2s(row0, P0, (uint32_t)n * 16, bar);
-            tma_bulk_g2s(x01s, X01, (uint32_t)I.nxp * 8, bar);
-            if (MODE == 2) tma_bulk_g2s(tri1, P1, (uint32_t)ntri * 16, bar);
+            copy(tri2, P2, (uint32_t)ntri * 16);
+            copy(col3, C3, (uint32_t)(n + 1) * 16);
+            copy(x12s, X12, (uint32_t)I.nxp * 8);
+            copy(x23s, X23, (uint32_t)I.nxp * 8);
+            copy(row0, P0, (uint32_t)n * 16);
+            copy(x01s, X01, (uint32_t)I.nxp * 8);
+            if (MODE == 2) copy(tri1, P1, (uint32_t)ntri * 16);
         }
     }
     __syncthreads();
     mbar_wait(bar, 0);
+    if (mc) cluster_arrive();  // this CTA's copies have landed (waited on before exit)
+#if defined(K3_PROFILE)
+    unsigned long long t1p; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1p));
+#endif
 
     const int lane = threadIdx.x & 31;
     double best_c = INFINITY;
@@ -460,7 +482,15 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     Ss.blk = S.blk + (size_t)snap * per_snap;
     Ss.counter = S.counter + snap;
     Ss.result = S.result + snap;
+#if defined(K3_PROFILE)
+    unsigned long long t2p; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2p));
+#endif
     block_argmin_finish(mine, Ss, per_snap, local);
+    if (mc) cluster_wait();  // no CTA leaves while a multicast into a peer may be in flight
+#if defined(K3_PROFILE)
+    { unsigned long long t3; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
+      if (threadIdx.x == 0) printf("K3P %d %d %llu %llu %llu %llu\n", blockIdx.x, (int)__nv_smid_k3(), t0p, t1p, t2p, t3); }
+#endif
 }
 
 // Tile table: cut positions p[1..k-1] (u8) of every K3_TILE-th composition
