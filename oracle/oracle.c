@@ -370,8 +370,9 @@ int or_evaluate(const gp_instance *I, uint32_t k, const uint8_t *order,
         detail->feasible = feasible;
         for (uint32_t s = 0; s < k; ++s) {
             detail->stage[s].kind = (uint32_t)split[s].kind;
+            /* len(IntraSplit.parts): SGs (PP, DP) or members (TP) */
+            detail->stage[s].n_parts = (uint32_t)split[s].n_parts;
             if (split[s].kind == GP_ASYM_PP) {
-                detail->stage[s].n_parts = (uint32_t)split[s].n_parts;
                 for (int j = 0; j < split[s].n_parts; ++j) {
                     detail->stage[s].pp_sg[j] = (uint32_t)j;
                     detail->stage[s].pp_start[j] = split[s].pp_start[j];

@@ -742,8 +742,10 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
 
 // Generic status-tracking pass that runs only when the device flags are set.
 static int launch_fixup(gp_ctx* c, const RangeGeom& G) {
+    // grid-stride over the range; small grid because the kernel usually only
+    // reads the (clear) flag and exits
     unsigned long long grid = (G.hi - G.lo + 255) / 256;
-    unsigned long long gmax = (unsigned long long)c->n_sms * 16;
+    unsigned long long gmax = (unsigned long long)c->n_sms * 2;
     if (grid > gmax) grid = gmax;
     if (grid < 1) grid = 1;
     CUDA_TRY(c->blk.ensure(grid));
