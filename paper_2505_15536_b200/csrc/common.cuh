@@ -66,6 +66,7 @@ struct DevInst {
     int nb, nm;     // |B|, |M|
     const double *fwd, *bwd_in, *bwd_w, *act, *param;
     const long long *batch, *micro;
+    double* mtab;   // [nb*nm] (double)(batch / micro) per (b, m) index (K1)
     const double *p_c, *mem, *p_t, *lat, *bw;
     const uint32_t* id_rank;
     const uint32_t *fg_off, *fg_mem, *fg_sg_off, *sg_off, *sg_mem;

@@ -85,6 +85,7 @@ struct gp_ctx {
     DBuf<double> S, g_rf, g_cf, g_dp, g_minmem, sg_minmem, C1, xt;
     DBuf<double4> fbws;
     DBuf<double> vtab;
+    DBuf<double> mtab;           // micro-batch counts M per (b, m) index
     DBuf<double2> tpk, tcol;
     DBuf<uint32_t> flagsbuf;
     DBuf<uint8_t> g_tp_ok, scode, skind;
@@ -159,7 +160,7 @@ struct gp_ctx {
         DevInst I;
         I.n = n; I.F = F; I.D = D; I.nb = nb; I.nm = nm;
         I.fwd = fwd.p; I.bwd_in = bwd_in.p; I.bwd_w = bwd_w.p; I.act = act.p; I.param = param.p;
-        I.batch = batch.p; I.micro = micro.p;
+        I.batch = batch.p; I.micro = micro.p; I.mtab = mtab.p;
         I.p_c = p_c.p; I.mem = mem.p; I.p_t = p_t.p; I.lat = lat.p; I.bw = bw.p;
         I.id_rank = id_rank.p;
         I.fg_off = fg_off.p; I.fg_mem = fg_mem.p; I.fg_sg_off = fg_sg_off.p;
@@ -245,6 +246,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     for (auto* b : dd) b->release();
     c->fbws.release();
     c->vtab.release();
+    c->mtab.release();
     c->flagsbuf.release();
     DBuf<uint8_t>* bb[] = {&c->g_tp_ok, &c->scode, &c->skind, &c->b_order, &c->b_counts,
                            &c->b_bm, &c->b_status};
@@ -412,6 +414,7 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     CUDA_TRY(c->C1.ensure((size_t)F * N2));
     CUDA_TRY(c->fbws.ensure((size_t)F * N2));
     CUDA_TRY(c->vtab.ensure((size_t)c->nm * F * ((size_t)n * (n + 1) / 2)));
+    CUDA_TRY(c->mtab.ensure(256));
     CUDA_TRY(c->gw.ensure((size_t)F * F));
     CUDA_TRY(c->xt.ensure((size_t)c->nm * F * F * ((n + 1) & ~1u)));
     CUDA_TRY(c->tpk.ensure((size_t)c->nm * F * ((size_t)n * (n + 1) / 2)));

@@ -338,6 +338,9 @@ __global__ void __launch_bounds__(128) k1_phase1(DevInst I) {
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
 #endif
+    if (b == 0)  // M = batch / micro per (b, m) index, for the per-candidate kernels
+        for (int t = threadIdx.x; t < I.nb * I.nm; t += blockDim.x)
+            I.mtab[t] = (double)(I.batch[t / I.nm] / I.micro[t % I.nm]);
     if (b < 5) k1_intervals_block(I, b);
     else if (b < 5 + I.F) k1_group_block(I, b - 5);
     else {

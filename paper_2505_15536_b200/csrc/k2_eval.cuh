@@ -99,9 +99,8 @@ __global__ void k2_eval_batch(DevInst I, int k, long long ncand, const uint8_t* 
     if (b >= I.nb * I.nm || p[k] > I.n) st = GP_ERR_INPUT;
     if (st != GP_OK) { cost[i] = NAN; status[i] = (uint8_t)st; return; }
     int mi = b % I.nm;
-    long long M = I.batch[b / I.nm] / I.micro[mi];
     if (*I.flags == 0u && p[k] == I.n && k >= 2 && k <= 6) {
-        const double Md = (double)M;
+        const double Md = __ldg(&I.mtab[b]);  // (double)(batch / micro), tabulated by K1
         double c;
         switch (k) {
             case 2: c = eval_fast<2>(I, o, p, mi, Md); break;
@@ -114,7 +113,7 @@ __global__ void k2_eval_batch(DevInst I, int k, long long ncand, const uint8_t* 
         status[i] = GP_OK;
         return;
     }
-    EvalOut r = eval_tables(I, k, o, p, mi, M);
+    EvalOut r = eval_tables(I, k, o, p, mi, I.batch[b / I.nm] / I.micro[mi]);
     cost[i] = r.status == GP_OK ? r.cost : NAN;
     status[i] = (uint8_t)r.status;
 }

@@ -27,3 +27,16 @@ for _ in range(3):
     eng.eval_batch_device(4, N, d_o.data_ptr(), d_c.data_ptr(), d_b.data_ptr(), d_cost.data_ptr(),
                           d_st.data_ptr())
 torch.cuda.synchronize()
+# timing (CUDA events on the engine stream, 20 launches)
+stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+with torch.cuda.stream(stream):
+    a.record(stream)
+for _ in range(20):
+    eng.eval_batch_device(4, N, d_o.data_ptr(), d_c.data_ptr(), d_b.data_ptr(), d_cost.data_ptr(),
+                          d_st.data_ptr())
+with torch.cuda.stream(stream):
+    b.record(stream)
+torch.cuda.synchronize()
+ms = a.elapsed_time(b) / 20
+print(f"K2 2e7: {ms * 1e3:.1f} us per launch, {N / (ms * 1e-3):.3g} candidates/s")
