@@ -36,7 +36,7 @@ __host__ __device__ __forceinline__ size_t k7_scratch_bytes(int D) {
 
 // per-slot arrays at the head of dynamic shared memory
 __host__ __device__ __forceinline__ size_t k7_smem_head(int D) {
-    return ((size_t)D * 8 * 2 + (size_t)D * 2 * 5 + (size_t)D + 16 + 15) & ~(size_t)15;
+    return ((size_t)D * 8 * 2 + (size_t)D * 2 * 5 + (size_t)D * 2 + 16 + 15) & ~(size_t)15;
 }
 
 struct K7Shared {
@@ -45,6 +45,7 @@ struct K7Shared {
     int16_t* rowarg;    // [n] its partner b (-1: row empty)
     int16_t* cnt;       // [n] members of the group in slot a (0: dead slot)
     uint8_t* has;       // [n] intra cache valid (bit0) / singleton (bit1)
+    uint8_t* need;      // [n] row minimum must be rescanned
 };
 
 struct K7Global {
@@ -123,12 +124,46 @@ __device__ __forceinline__ void k7_scan_row(const K7Global& g, const K7Shared& s
     sh.rowarg[a] = (int16_t)bb;
 }
 
+// the same rescan by one warp: lanes take every 32nd column, then a warp
+// arg-min on (key, column) - the first minimal column, as the serial scan
+__device__ __forceinline__ void k7_scan_row_warp(const K7Global& g, const K7Shared& sh, int n,
+                                                 int a, int lane) {
+    double bk = 0.0;
+    int bb = -1;
+    const double* kr = g.key + (size_t)a * n;
+    const uint8_t* lr = g.live + (size_t)a * n;
+    for (int b = a + 1 + lane; b < n; b += 32)
+        if (lr[b] && sh.cnt[b] && (bb < 0 || kr[b] < bk)) { bk = kr[b]; bb = b; }
+    for (int o = 16; o; o >>= 1) {
+        const double k2 = __shfl_down_sync(0xffffffffu, bk, o);
+        const int b2 = __shfl_down_sync(0xffffffffu, bb, o);
+        if (b2 >= 0 && (bb < 0 || k2 < bk || (k2 == bk && b2 < bb))) { bk = k2; bb = b2; }
+    }
+    if (lane == 0) {
+        sh.rowkey[a] = bk;
+        sh.rowarg[a] = (int16_t)bb;
+    }
+}
+
+// rows flagged in sh.need, one warp per row (WARP: the calling warp alone)
+template <bool WARP>
+__device__ __forceinline__ void k7_rescan_flagged(const K7Global& g, const K7Shared& sh, int n) {
+    const int lane = threadIdx.x & 31, wid = WARP ? 0 : threadIdx.x >> 5,
+              nw = WARP ? 1 : blockDim.x >> 5;
+    for (int r = wid; r < n; r += nw)
+        if (sh.need[r]) k7_scan_row_warp(g, sh, n, r, lane);
+}
+
 // CTA arg-min over the row minima: returns (a, b) in s_ab, or a = -1
+// (WARP: the calling warp alone, warp-synchronous)
+template <bool WARP>
 __device__ void k7_pop(const K7Shared& sh, int n, int* s_ab, double* s_red, int* s_ia) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int tid = WARP ? (threadIdx.x & 31) : threadIdx.x, lane = threadIdx.x & 31,
+              wid = threadIdx.x >> 5;
+    const int nt = WARP ? 32 : blockDim.x;
     double bk = 0.0;
     int ba = -1, bb = -1;
-    for (int a = tid; a < n; a += blockDim.x) {
+    for (int a = tid; a < n; a += nt) {
         const int b = sh.rowarg[a];
         if (sh.cnt[a] == 0 || b < 0) continue;
         const double k = sh.rowkey[a];
@@ -139,6 +174,11 @@ __device__ void k7_pop(const K7Shared& sh, int n, int* s_ab, double* s_red, int*
         const int a2 = __shfl_down_sync(0xffffffffu, ba, o);
         const int b2 = __shfl_down_sync(0xffffffffu, bb, o);
         if (a2 >= 0 && (ba < 0 || k7_less(k2, a2, b2, bk, ba, bb))) { bk = k2; ba = a2; bb = b2; }
+    }
+    if (WARP) {
+        if (lane == 0) { s_ab[0] = ba; s_ab[1] = bb; }
+        __syncwarp();
+        return;
     }
     if (lane == 0) { s_red[wid] = bk; s_ia[2 * wid] = ba; s_ia[2 * wid + 1] = bb; }
     __syncthreads();
@@ -158,20 +198,24 @@ __device__ void k7_pop(const K7Shared& sh, int n, int* s_ab, double* s_red, int*
 // _agglomerate over n items (device ranks items[i], sorted): on return
 // group_of[i] = index of the item's group in sorted(alive) order; returns
 // the number of groups.  All threads of the CTA call it.
+template <bool WARP>
 __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const double* __restrict__ pt,
                               const double* __restrict__ pc, int D, double thr, const K7Global& g,
                               const K7Shared& sh, uint16_t* group_of, int* s_ab, double* s_red,
                               int* s_ia) {
-    const int tid = threadIdx.x, nt = blockDim.x;
+    // WARP: one warp runs the whole merge chain with warp barriers (small
+    // groups: the chain is barrier-latency bound)
+    const int tid = WARP ? (threadIdx.x & 31) : threadIdx.x, nt = WARP ? 32 : blockDim.x;
+    auto sync = [] { if (WARP) __syncwarp(); else __syncthreads(); };
     for (int a = tid; a < n; a += nt) {
         sh.cnt[a] = 1;
         g.mem[(size_t)a * n] = items[a];
         sh.has[a] = 0;
     }
-    __syncthreads();
+    sync();
     if (level == 2)
         for (int a = tid; a < n; a += nt) k7_group_value(2, g, sh, n, pt, pc, D, a);
-    __syncthreads();
+    sync();
     for (long long p = tid; p < (long long)n * n; p += nt) {
         const int a = (int)(p / n), b = (int)(p % n);
         if (b > a) {
@@ -179,12 +223,23 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
             g.live[p] = 1;
         }
     }
-    __syncthreads();
-    for (int a = tid; a < n; a += nt) k7_scan_row(g, sh, n, a);
-    __syncthreads();
+    for (int a = tid; a < n; a += nt) sh.need[a] = 1;
+    sync();
+    k7_rescan_flagged<WARP>(g, sh, n);
+    sync();
+#if defined(K7_PROFILE)
+    long long c_pop = 0, c_pred = 0, c_keys = 0, c_rows = 0, c0, c1;
+    int npops = 0;
+#endif
     for (;;) {
-        k7_pop(sh, n, s_ab, s_red, s_ia);
+#if defined(K7_PROFILE)
+        c0 = clock64();
+#endif
+        k7_pop<WARP>(sh, n, s_ab, s_red, s_ia);
         const int a = s_ab[0], b = s_ab[1];
+#if defined(K7_PROFILE)
+        c1 = clock64(); c_pop += c1 - c0; c0 = c1; ++npops;
+#endif
         if (a < 0) break;
         // merge predicate (merge_values + _relative_spread, :154-180, :203-210)
         if (tid == 0) {
@@ -210,7 +265,6 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
             const double spread = top == 0 ? 0.0 : (top - bot) / top;
             if (spread >= thr) {
                 g.live[(size_t)a * n + b] = 0;  // discarded permanently
-                k7_scan_row(g, sh, n, a);
                 s_ab[2] = 0;
             } else {
                 // merged = tuple(sorted(a + b)) into slot a
@@ -229,10 +283,17 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
                 s_ab[2] = 1;
             }
         }
-        __syncthreads();
-        if (!s_ab[2]) continue;
+        sync();
+#if defined(K7_PROFILE)
+        c1 = clock64(); c_pred += c1 - c0; c0 = c1;
+#endif
+        if (!s_ab[2]) {  // discarded: row a loses its minimum
+            if (tid < 32) k7_scan_row_warp(g, sh, n, a, tid & 31);
+            sync();
+            continue;
+        }
         if (level == 2 && tid == 0) k7_group_value(2, g, sh, n, pt, pc, D, a);
-        __syncthreads();
+        sync();
         // pairs of the merged group with every other live group; drop b's
         for (int c = tid; c < n; c += nt) {
             if (c == a || sh.cnt[c] == 0) continue;
@@ -241,14 +302,20 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
             g.live[(size_t)x * n + y] = 1;
             if (c < b) g.live[(size_t)c * n + b] = 0;
         }
-        __syncthreads();
+        // the merged group's _mean_intra_pt, on an otherwise idle thread
+        if (level == 1 && n < nt && tid == nt - 1) k7_group_value(1, g, sh, n, pt, pc, D, a);
+        sync();
+#if defined(K7_PROFILE)
+        c1 = clock64(); c_keys += c1 - c0; c0 = c1;
+#endif
         // row minima: rows that pointed at a or b rescan; rows c < a compare
         // against their new pair (c, a); row a rescans
         for (int c = tid; c < n; c += nt) {
+            sh.need[c] = 0;
             if (sh.cnt[c] == 0) continue;
             const int r = sh.rowarg[c];
             if (c == a || r == a || r == b) {
-                k7_scan_row(g, sh, n, c);
+                sh.need[c] = 1;
             } else if (c < a) {
                 const double k = g.key[(size_t)c * n + a];
                 if (r < 0 || k7_less(k, c, a, sh.rowkey[c], c, r)) {
@@ -257,8 +324,18 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
                 }
             }
         }
-        __syncthreads();
+        sync();
+        k7_rescan_flagged<WARP>(g, sh, n);
+        sync();
+#if defined(K7_PROFILE)
+        c1 = clock64(); c_rows += c1 - c0;
+#endif
     }
+#if defined(K7_PROFILE)
+    if (tid == 0 && blockIdx.x == 0)
+        printf("  level %d n %d pops %d: pop %lld pred %lld keys %lld rows %lld cycles\n", level, n, npops,
+               c_pop, c_pred, c_keys, c_rows);
+#endif
     // sorted(alive): slot order; group index = rank among live slots
     if (tid == 0) {
         int gi = 0;
@@ -278,7 +355,7 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
         }
         s_ab[3] = gi;
     }
-    __syncthreads();
+    sync();
     return s_ab[3];
 }
 
@@ -320,6 +397,7 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
     uint16_t* gof = items + D;          // level-1 group of each device
     uint16_t* sgo = gof + D;            // level-2 group of each FG member
     sh.has = reinterpret_cast<uint8_t*>(sgo + D);
+    sh.need = sh.has + D;
     uint16_t* fg_of = fg_of_all + (size_t)snap * D;
     uint16_t* sg_of = sg_of_all + (size_t)snap * D;
     double* fg_intra = fg_intra_all + (size_t)snap * D;
@@ -329,6 +407,10 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
 
     for (int d = tid; d < D; d += blockDim.x) items[d] = (uint16_t)d;
     __syncthreads();
+#if defined(K7_PROFILE)
+    unsigned long long tp0, tp1, tp2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp0));
+#endif
     // first level: agglomerated, or given (a fixed partition, e.g. the C2
     // region-grouping sweep; indices already in sorted-member-tuple order)
     int nf;
@@ -337,10 +419,13 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
         __syncthreads();
         nf = fixed_nf;
     } else {
-        nf = k7_agglomerate(1, D, items, pt, pc, D, thr_net, g, sh, gof, s_ab, s_red, s_ia);
+        nf = k7_agglomerate<false>(1, D, items, pt, pc, D, thr_net, g, sh, gof, s_ab, s_red, s_ia);
     }
     for (int d = tid; d < D; d += blockDim.x) fg_of[d] = gof[d];
     __syncthreads();
+#if defined(K7_PROFILE)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
+#endif
     int sg_base = 0;
     for (int f = 0; f < nf; ++f) {
         // members of FG f in rank order
@@ -353,7 +438,8 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
         __syncthreads();
         const int nm = s_ab[0];
         __syncthreads();
-        // FG statistics (group_first_level, :176-188)
+        // FG statistics (group_first_level, :176-188): the sums on one thread
+        // (operand order), min_intra_bandwidth as a CTA min (order-free)
         if (tid == 0) {
             NeumaierSum s;
             s.start(pc[items[0]]);
@@ -361,24 +447,45 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
             fg_cap[f] = s.value();
             if (nm < 2) {
                 fg_intra[f] = NAN;
-                fg_minbw[f] = NAN;
             } else {
                 NeumaierSum t;
                 bool first = true;
-                double mb = INFINITY;
                 for (int i = 0; i < nm; ++i)
                     for (int j = i + 1; j < nm; ++j) {
-                        const size_t e = (size_t)items[i] * D + items[j];
-                        if (first) { t.start(pt[e]); first = false; } else t.add(pt[e]);
-                        if (bw && bw[e] < mb) mb = bw[e];
+                        const double v = pt[(size_t)items[i] * D + items[j]];
+                        if (first) { t.start(v); first = false; } else t.add(v);
                     }
                 fg_intra[f] = t.value() / (double)((long long)nm * (nm - 1) / 2);
-                fg_minbw[f] = bw ? mb : NAN;
             }
         }
+        {
+            double mb = INFINITY;
+            if (bw)
+                for (int q = tid; q < nm * nm; q += blockDim.x) {
+                    const int i = q / nm, j = q % nm;
+                    if (j > i) {
+                        const double v = bw[(size_t)items[i] * D + items[j]];
+                        mb = v < mb ? v : mb;
+                    }
+                }
+            for (int o = 16; o; o >>= 1) {
+                const double v = __shfl_down_sync(0xffffffffu, mb, o);
+                mb = v < mb ? v : mb;
+            }
+            if ((tid & 31) == 0) s_red[tid >> 5] = mb;
+            __syncthreads();
+            if (tid == 0) {
+                double r = s_red[0];
+                for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = s_red[w] < r ? s_red[w] : r;
+                fg_minbw[f] = (nm < 2 || !bw) ? NAN : r;
+            }
+            __syncthreads();
+        }
         // second level over the FG's members (local slots 0..nm-1)
-        const int ns = k7_agglomerate(2, nm, items, pt, pc, D, thr_comp, g, sh, sgo, s_ab, s_red,
-                                      s_ia);
+        // (a one-warp variant, k7_agglomerate<true>, measured slower here: the
+        // chain is bound by dependent shared-memory steps, not by barriers)
+        const int ns = k7_agglomerate<false>(2, nm, items, pt, pc, D, thr_comp, g, sh, sgo, s_ab,
+                                             s_red, s_ia);
         for (int i = tid; i < nm; i += blockDim.x) sg_of[items[i]] = sgo[i];
         __syncthreads();
         if (tid == 0) {
@@ -400,6 +507,10 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
         n_fg[snap] = (uint32_t)nf;
         n_sg[snap] = (uint32_t)sg_base;
     }
+#if defined(K7_PROFILE)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp2));
+    if (tid == 0 && snap == 0) printf("K7 level1 %llu ns, level2+stats %llu ns\n", tp1 - tp0, tp2 - tp1);
+#endif
 }
 
 
