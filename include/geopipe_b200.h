@@ -484,6 +484,10 @@ void *gp_ctx_stream(gp_ctx *ctx);
 /* Diagnostics: measured FP64 DADD issue rate of `device` (ops/s), the
  * roofline denominator of the range kernel (bench.py). */
 int gp_diag_fp64_peak(int device, double *dadd_per_second);
+/* Diagnostics: when `enable`, gp_replan brackets its graph launch with CUDA
+ * events; *last_graph_ms (optional) receives the device time of the last
+ * timed graph (-1 before the first). */
+int gp_diag_replan_timing(gp_ctx *ctx, int enable, double *last_graph_ms);
 /* Diagnostics: force the exhaustive kernel variant (-1 auto; 0 tables in
  * L1/L2; 1 one triangle in shared memory; 2 two triangles; 3 generic
  * status-tracking kernel).  Results are identical in every mode. */

@@ -291,6 +291,15 @@ __device__ __forceinline__ bool advance_pair(int* p, int& a, int& q, int s, int 
 
 
 
+// ---- programmatic dependent launch ----------------------------------------------
+// Kernels of the gp_replan graph are launched with programmatic stream
+// serialisation: a dependent grid is scheduled once every CTA of the
+// preceding grid has called pdl_trigger(), and pdl_wait() blocks until the
+// preceding grid has completed and its writes are visible.  Without the
+// launch attribute both are no-ops, so the same kernels serve every path.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- TMA (bulk async copy) helpers ----------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);

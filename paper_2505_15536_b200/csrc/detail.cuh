@@ -21,7 +21,7 @@ struct SolveOut {
     Key key;
     unsigned long long err;
     int status;        // of the detail evaluation
-    uint32_t k, bm, pad;
+    uint32_t k, bm, flags;  // flags: the table-build flags word (FLAG_*)
     uint8_t order[GP_MAX_STAGES];
     uint8_t counts[GP_MAX_STAGES];
     gp_plan_info info;
@@ -120,6 +120,7 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
         const int nn = q / (k + 1), r = q % (k + 1);
         bsm[q] = binom[(size_t)nn * (GP_MAX_STAGES + 1) + r];
     }
+    pdl_wait();  // the arg-min (binom is static: staged before the wait)
     const Key key = *result;
     const unsigned long long e = *err;
     __syncwarp();
@@ -128,6 +129,7 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
         out->err = e;
         out->k = (uint32_t)k;
         out->status = GP_OK;
+        out->flags = *I.flags;  // table flags travel back with the result
     }
     if (e != ~0ull || key.tie == ~0ull) return;
     const int n = I.n;

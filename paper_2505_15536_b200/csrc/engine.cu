@@ -142,6 +142,10 @@ struct gp_ctx {
     RangeGeom graph_geom{};
     unsigned long long graph_lo = 0, graph_hi = 0;
     bool capturing = false;
+    bool pdl = false;  // capturing the gp_replan graph: PDL launches, no memset nodes
+    bool diag_timing = false;          // gp_diag_replan_timing
+    cudaEvent_t t_ev0 = nullptr, t_ev1 = nullptr;
+    float last_graph_ms = -1.0f;
     size_t arena_bytes = 0;
     int force_mode = -1;  // -1 auto; 0/1/2 fast-path variant; 3 generic kernel
     std::vector<uint32_t> h_fg_sg_count;  // subgroups per group (explicit plans)
@@ -196,6 +200,25 @@ static unsigned long long h_binom(int n, int r) {
         if (res > (unsigned __int128)~0ull) return ~0ull;
     }
     return (unsigned long long)res;
+}
+
+// Kernel launch with programmatic stream serialisation (PDL) when `pdl`:
+// the kernel may be scheduled while its predecessor drains and waits in
+// pdl_wait() for the predecessor's results.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                            cudaStream_t s, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(block, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 extern "C" {
@@ -260,6 +283,8 @@ void gp_ctx_destroy(gp_ctx* c) {
     c->dsolve.release(); c->gbest.release(); c->s_tim.release(); c->s_traces.release(); c->s_tidx.release(); c->s_ms.release(); c->s_st.release();
     c->s_rep.release(); c->s_ends.release(); c->g_buf.release(); c->s_wq.release(); c->s_lq.release();
     if (c->flags_ev) cudaEventDestroy(c->flags_ev);
+    if (c->t_ev0) cudaEventDestroy(c->t_ev0);
+    if (c->t_ev1) cudaEventDestroy(c->t_ev1);
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release();
@@ -278,7 +303,8 @@ static int run_tables(gp_ctx* c, bool full) {
     if (full) {
         // interval sums + group constants + gateways (independent) in one launch
         const int gw_blocks = (c->F * c->F + 3) / 4;
-        k1_phase1<<<5 + c->F + gw_blocks, 128, 0, s>>>(I);
+        K1Reset R = {nullptr, nullptr, 0u};
+        k1_phase1<<<5 + c->F + gw_blocks, 128, 0, s>>>(I, R);
     } else {
         k1_gateways<<<(c->F * c->F * 32 + 127) / 128, 128, 0, s>>>(I);
     }
@@ -626,15 +652,13 @@ static SwFn pick_sweep(int mode, int nb, int k) {
 // across the GPCs), so the default is a plain launch.
 static cudaError_t launch_sweep_kernel(SwFn kern, unsigned grid, size_t smem, cudaStream_t s,
                                        SweepGeom& G, const DevInst& I, const ArgminScratch& S,
-                                       const unsigned long long* binom, const uint32_t* flags) {
+                                       const unsigned long long* binom, const uint32_t* flags,
+                                       bool pdl = false) {
     int cs = 1;
     if (const char* e = getenv("GP_K3_CLUSTER")) cs = atoi(e) > 0 ? atoi(e) : 1;
     if (cs > 1 && (G.cpi % cs != 0)) cs = 1;
     G.csize = cs;
-    if (cs == 1) {
-        kern<<<grid, K3S_THREADS, smem, s>>>(I, G, S, binom, flags);
-        return cudaGetLastError();
-    }
+    if (cs == 1) return launch_k(kern, grid, K3S_THREADS, smem, s, pdl, I, G, S, binom, flags);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(K3S_THREADS, 1, 1);
@@ -728,7 +752,8 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     G.gsteps = 1;
     while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
     CUDA_TRY(c->item_ctr.ensure(items));
-    CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
+    if (!c->pdl)  // (the gp_replan graph resets the counters in K1 phase 1)
+        CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
     G.item_ctr = c->item_ctr.p;
     CUDA_TRY(c->blk.ensure(grid));
     ArgminScratch S;
@@ -739,7 +764,8 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     S.err_idx = c->err_idx.p;
     c->last_geom = R;
     DevInst I = c->view();
-    CUDA_TRY(launch_sweep_kernel(kern, (unsigned)grid, smem, s, G, I, S, c->binom.p, dflags));
+    CUDA_TRY(launch_sweep_kernel(kern, (unsigned)grid, smem, s, G, I, S, c->binom.p, dflags,
+                                 c->pdl));
     return GP_OK;
 }
 
@@ -759,8 +785,8 @@ static int launch_fixup(gp_ctx* c, const RangeGeom& G) {
     S.err = nullptr;
     S.err_idx = c->err_idx.p;
     DevInst I = c->view();
-    k3_argmin_generic<<<(unsigned)grid, 256, 0, c->stream>>>(I, G, S, c->flagsbuf.p);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_k(k3_argmin_generic, (unsigned)grid, 256, 0, c->stream, c->pdl, I, G, S,
+                      (const uint32_t*)c->flagsbuf.p));
     return GP_OK;
 }
 
@@ -789,7 +815,8 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     c->last_lo = lo;
     c->last_hi = hi;
     ArgminScratch S;
-    CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));  // = ~0
+    if (!c->pdl)  // (the gp_replan graph resets it in K1 phase 1)
+        CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));  // = ~0
     DevInst I = c->view();
     // table flags (error entries, overflow) force the status-tracking kernel;
     // while the async read-back is pending, launch the fast kernel with a
@@ -1045,9 +1072,9 @@ static int enqueue_solve(gp_ctx* c, uint64_t lo, uint64_t hi) {
     const RangeGeom& G = c->last_geom;
     CUDA_TRY(c->dsolve.ensure(1));
     DevInst I = c->view();
-    k_solve_detail<<<1, 32, 0, c->stream>>>(I, G.k, G.NC, G.NP, G.nbm, c->result.p, c->err_idx.p,
-                                            c->binom.p, c->dsolve.p);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_k(k_solve_detail, 1, 32, 0, c->stream, c->pdl, I, G.k, G.NC, G.NP, G.nbm,
+                      (const Key*)c->result.p, (const unsigned long long*)c->err_idx.p,
+                      (const unsigned long long*)c->binom.p, c->dsolve.p));
     CUDA_TRY(cudaMemcpyAsync(c->h_solve, c->dsolve.p, sizeof(SolveOut), cudaMemcpyDeviceToHost,
                              c->stream));
     return GP_OK;
@@ -1057,6 +1084,8 @@ static int enqueue_solve(gp_ctx* c, uint64_t lo, uint64_t hi) {
 static int finish_solve(gp_ctx* c, gp_best* best, gp_plan_info* info) {
     const RangeGeom& G = c->last_geom;
     const SolveOut& o = *c->h_solve;
+    c->flags = o.flags;  // the table flags as the detail kernel saw them
+    c->flags_known = true;
     memset(best, 0, sizeof(*best));
     best->k = (uint32_t)G.k;
     best->evaluated = c->last_hi - c->last_lo;
@@ -1134,17 +1163,22 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
                                          cudaMemcpyHostToDevice, s);
         int st2 = ce == cudaSuccess ? GP_OK : fail(GP_ERR_CUDA, "capture: %s", cudaGetErrorString(ce));
         if (st2 == GP_OK) {
+            // H2D -> K1 phase 1 (resets flags, err_idx, item counters) -> phase 2
+            // -> sweep -> fix-up -> detail (PDL chain; the table flags return
+            // inside the SolveOut record) -> D2H
             DevInst I = c->view();
-            cudaMemsetAsync(c->flagsbuf.p, 0, sizeof(uint32_t), s);
             const int gw_blocks = (c->F * c->F + 3) / 4;
-            k1_phase1<<<5 + c->F + gw_blocks, 128, 0, s>>>(I);
+            K1Reset R = {c->err_idx.p, c->item_ctr.p, (unsigned)((size_t)c->nm * h_fact(c->F))};
+            ce = launch_k(k1_phase1, 5 + c->F + gw_blocks, 128, 0, s, false, I, R);
             long long ns = (long long)c->F * (c->n + 1) * (c->n + 1);
             long long nx = (long long)c->nm * c->F * c->F * c->n;
-            k1_phase2<<<(unsigned)((ns + nx + 127) / 128), 128, 0, s>>>(I, ns);
-            cudaMemcpyAsync(c->h_flags, c->flagsbuf.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
-            cudaEventRecord(c->flags_ev, s);
+            if (ce == cudaSuccess)
+                ce = launch_k(k1_phase2, (unsigned)((ns + nx + 127) / 128), 128, 0, s, true, I, ns);
+            if (ce != cudaSuccess) st2 = fail(GP_ERR_CUDA, "capture: %s", cudaGetErrorString(ce));
             c->flags_known = false;
-            st2 = enqueue_solve(c, 0, total);
+            c->pdl = true;
+            if (st2 == GP_OK) st2 = enqueue_solve(c, 0, total);
+            c->pdl = false;
         }
         cudaGraph_t g = nullptr;
         cudaError_t ee = cudaStreamEndCapture(s, &g);
@@ -1187,9 +1221,12 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
         c->last_lo = c->graph_lo;
         c->last_hi = c->graph_hi;
     }
+    if (c->diag_timing) CUDA_TRY(cudaEventRecord(c->t_ev0, s));
     CUDA_TRY(cudaGraphLaunch(c->graph_exec, s));
     CUDA_TRY(cudaEventRecord(c->arena_ev, s));
+    if (c->diag_timing) CUDA_TRY(cudaEventRecord(c->t_ev1, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    if (c->diag_timing) CUDA_TRY(cudaEventElapsedTime(&c->last_graph_ms, c->t_ev0, c->t_ev1));
     c->flags_known = false;
     c->loaded = true;
     return finish_solve(c, best, info);
@@ -1825,6 +1862,18 @@ int gp_plan_cost(gp_ctx* c, uint32_t k, const gp_plan_stage* stages, int64_t bat
 int gp_ctx_set_k3_mode(gp_ctx* c, int mode) {
     if (!c || mode < -1 || mode > 4) return fail(GP_ERR_INPUT, "bad mode");
     c->force_mode = mode;
+    return GP_OK;
+}
+
+int gp_diag_replan_timing(gp_ctx* c, int enable, double* last_graph_ms) {
+    if (!c) return fail(GP_ERR_INPUT, "null context");
+    if (enable && !c->t_ev0) {
+        CUDA_TRY(cudaSetDevice(c->device));
+        CUDA_TRY(cudaEventCreate(&c->t_ev0));
+        CUDA_TRY(cudaEventCreate(&c->t_ev1));
+    }
+    c->diag_timing = enable != 0;
+    if (last_graph_ms) *last_graph_ms = (double)c->last_graph_ms;
     return GP_OK;
 }
 

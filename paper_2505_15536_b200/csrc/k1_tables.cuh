@@ -316,10 +316,9 @@ __device__ void k1_gateway_warp(const DevInst& I, int warp, int lane) {
         bool take = oh && (!have || op < bp || (op == bp && (oru < ru || (oru == ru && orv < rv))));
         if (take) { have = true; bp = op; bu = ou; bv = ov; ru = oru; rv = orv; }
     }
-    if (lane == 0) {
-        I.gw[warp] = (int)(bu * I.D + bv);
-        if (fa != fb && !(I.bw[(size_t)bu * I.D + bv] > 0)) atomicOr(I.flags, FLAG_GATEWAY_ERROR);
-    }
+    // (a zero-bandwidth gateway raises FLAG_GATEWAY_ERROR in k1_boundary_t,
+    // so phase 1 never touches the flags word it resets)
+    if (lane == 0) I.gw[warp] = (int)(bu * I.D + bv);
 }
 
 __global__ void k1_gateways(DevInst I) {
@@ -332,8 +331,25 @@ __global__ void k1_gateways(DevInst I) {
 __device__ void k1_intervals_block(const DevInst& I, int col);
 __device__ void k1_gateway_warp(const DevInst& I, int warp, int lane);
 
-__global__ void __launch_bounds__(128) k1_phase1(DevInst I) {
+// Per-run scratch that the gp_replan graph resets inside phase 1 instead of
+// with memset nodes (null pointers: nothing to reset).
+struct K1Reset {
+    unsigned long long* err_idx;  // first erroring candidate -> ~0
+    unsigned int* item_ctr;       // K3 sweep per-item task counters -> 0
+    unsigned int n_items;
+};
+
+__global__ void __launch_bounds__(128) k1_phase1(DevInst I, K1Reset R) {
     const int b = blockIdx.x;
+    pdl_trigger();  // phase 2 may be scheduled now (it waits for this grid)
+    if (b == 0) {
+        if (threadIdx.x == 0) {
+            *I.flags = 0u;
+            if (R.err_idx) *R.err_idx = ~0ull;
+        }
+        for (unsigned int t = threadIdx.x; R.item_ctr && t < R.n_items; t += blockDim.x)
+            R.item_ctr[t] = 0u;
+    }
 #if defined(K1_PROFILE)
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -363,6 +379,8 @@ __device__ void k1_boundary_t(const DevInst& I, long long t) {
     int pair = (int)(r % (I.F * I.F));
     int mi = (int)(r / (I.F * I.F));
     int g = I.gw[pair];
+    if (mi == 0 && j == 0 && pair / I.F != pair % I.F && !(I.bw[g] > 0))
+        atomicOr(I.flags, FLAG_GATEWAY_ERROR);  // zero-bandwidth gateway
     double md = (double)I.micro[mi];
     // transfer_seconds: latency + (act*m)/bandwidth (src/timing.py:91-97)
     I.xt[(size_t)r * I.nxp + j] = I.lat[g] + (I.act[j] * md) / I.bw[g];
@@ -370,6 +388,8 @@ __device__ void k1_boundary_t(const DevInst& I, long long t) {
 
 // K1 phase 2 in one launch: stage table entries, then boundary x entries
 __global__ void k1_phase2(DevInst I, long long n_stage) {
+    pdl_trigger();
+    pdl_wait();  // phase 1's interval sums, group constants and gateways
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < n_stage) k1_stage_t(I, t);
     else k1_boundary_t(I, t - n_stage);

@@ -268,6 +268,8 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
 #if defined(K3_PROFILE)
     unsigned long long t0p; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0p));
 #endif
+    pdl_trigger();
+    pdl_wait();  // K1's tables (gp_replan graph); no-op on plain launches
     const int n = I.n, k = KS > 0 ? KS : G.k;
     const int ntri = n * (n + 1) / 2;
     const int KB = k + 1;
@@ -510,6 +512,8 @@ __global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G,
                                                          const uint32_t* only_if_flags) {
     // fix-up launch behind a fast-path kernel: do nothing unless the table
     // build raised a flag (then this kernel's result replaces the fast one)
+    pdl_trigger();
+    pdl_wait();
     if (only_if_flags && *only_if_flags == 0u) return;
     Key mine{INFINITY, ~0ull};
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;

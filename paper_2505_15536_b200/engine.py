@@ -89,6 +89,7 @@ def lib():
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
+        L.gp_diag_replan_timing.argtypes = [vp, C.c_int, P(C.c_double)]
         L.gp_plan_cost.argtypes = [vp, C.c_uint32, P(abi.GpPlanStage), C.c_int64, C.c_int64,
                                    C.c_double, P(abi.GpPlanInfo), P(abi.GpTiming)]
         L.gp_plan_timing.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_double,
@@ -408,6 +409,13 @@ class Engine:
     def set_k3_mode(self, mode: int) -> None:
         """Force the exhaustive-kernel variant (-1 auto, 0/1/2, 3 generic)."""
         _check(lib().gp_ctx_set_k3_mode(self._h, int(mode)))
+
+    def replan_timing(self, enable: bool = True) -> float:
+        """Turn on/off CUDA-event timing of the gp_replan graph; returns the
+        device milliseconds of the last timed graph (-1 before the first)."""
+        out = C.c_double(-1.0)
+        _check(lib().gp_diag_replan_timing(self._h, int(bool(enable)), C.byref(out)))
+        return out.value
 
     def set_bandwidth(self, bw: np.ndarray) -> None:
         a = np.ascontiguousarray(bw, dtype=np.float64)
