@@ -488,6 +488,14 @@ int gp_diag_fp64_peak(int device, double *dadd_per_second);
  * events; *last_graph_ms (optional) receives the device time of the last
  * timed graph (-1 before the first). */
 int gp_diag_replan_timing(gp_ctx *ctx, int enable, double *last_graph_ms);
+/* Diagnostics: host-side phases of the last timed gp_replan in microseconds:
+ * [0] arena fill (+ shape check), [1] graph launch call, [2] wait for the
+ * graph, [3] result decode. */
+int gp_diag_replan_host(gp_ctx *ctx, double *host_us4);
+/* Diagnostics: drain the per-CTA kernel timeline of a -DGP_TIMELINE build
+ * (records of 40 bytes: u64 entry, after-dependency-wait and exit
+ * globaltimer ns; u32 kernel id, CTA, SM, pad).  Shipped builds return 0. */
+int gp_diag_timeline(void *out, uint32_t cap, uint32_t *n);
 /* Diagnostics: force the exhaustive kernel variant (-1 auto; 0 tables in
  * L1/L2; 1 one triangle in shared memory; 2 two triangles; 3 generic
  * status-tracking kernel).  Results are identical in every mode. */

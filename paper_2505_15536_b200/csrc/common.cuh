@@ -291,6 +291,31 @@ __device__ __forceinline__ bool advance_pair(int* p, int& a, int& q, int s, int 
 
 
 
+// ---- per-CTA timeline (diagnostic builds, -DGP_TIMELINE) --------------------------
+// Thread 0 of each CTA of the instrumented kernels appends {kernel id, CTA,
+// SM, entry, after pdl_wait, exit} (globaltimer ns) to a device log that
+// gp_diag_timeline() drains.  Compiled out of the shipped library.
+struct TlRec { unsigned long long t0, tw, t1; unsigned int kid, blk, smid, pad; };
+#if defined(GP_TIMELINE)
+#define GP_TL_CAP 65536
+__device__ TlRec g_tl[GP_TL_CAP];
+__device__ unsigned int g_tl_n;
+__device__ __forceinline__ unsigned long long tl_now() {
+    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+#define TL_START() const unsigned long long _tl0 = tl_now(); unsigned long long _tlw = _tl0
+#define TL_WAITED() _tlw = tl_now()
+#define TL_STOP(kid) do { if (threadIdx.x == 0) { \
+    unsigned int _i = atomicAdd(&g_tl_n, 1u); unsigned int _sm; \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(_sm)); \
+    if (_i < GP_TL_CAP) g_tl[_i] = TlRec{_tl0, _tlw, tl_now(), (unsigned)(kid), blockIdx.x, _sm, 0u}; \
+    } } while (0)
+#else
+#define TL_START() do {} while (0)
+#define TL_WAITED() do {} while (0)
+#define TL_STOP(kid) do {} while (0)
+#endif
+
 // ---- programmatic dependent launch ----------------------------------------------
 // Kernels of the gp_replan graph are launched with programmatic stream
 // serialisation: a dependent grid is scheduled once every CTA of the

@@ -18,7 +18,7 @@ __global__ void k_plan_detail(DevInst I, int k, const uint8_t* order_in, const u
 // Winner of the last arg-min -> decoded candidate + plan detail, on the
 // device (no host round trip between the arg-min and the breakdown).
 struct SolveOut {
-    Key key;
+    Key key;  // (sizeof is a multiple of 8: copied in 8-byte words)
     unsigned long long err;
     int status;        // of the detail evaluation
     uint32_t k, bm, flags;  // flags: the table-build flags word (FLAG_*)
@@ -26,6 +26,8 @@ struct SolveOut {
     uint8_t counts[GP_MAX_STAGES];
     gp_plan_info info;
 };
+
+static_assert(sizeof(SolveOut) % 8 == 0, "SolveOut is copied in 8-byte words");
 
 // Warp version of plan_detail_dev: lane s prepares stage s (split choice and
 // table loads in parallel), lane 0 runs the short Eq. 1 chain.
@@ -113,6 +115,16 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
     // one warp: decode the arg-min key (cut positions by a 32-wide ballot
     // over the hockey-stick counts), then the warp plan detail
     const int lane = threadIdx.x & 31;
+    TL_START();
+    // the record is assembled in shared memory and leaves in one coalesced
+    // pass (the destination may be mapped host memory)
+    __shared__ __align__(16) SolveOut so;
+    SolveOut* const dst = out;
+    out = &so;
+    {
+        unsigned long long* z = (unsigned long long*)&so;
+        for (int q = lane; q < (int)(sizeof(SolveOut) / 8); q += 32) z[q] = 0ull;
+    }
     // the binomial columns the decode reads, staged once (independent loads
     // overlap) instead of one dependent global round trip per probe
     __shared__ unsigned long long bsm[(GP_MAX_LAYERS + 1) * (GP_MAX_STAGES + 1)];
@@ -121,6 +133,7 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
         bsm[q] = binom[(size_t)nn * (GP_MAX_STAGES + 1) + r];
     }
     pdl_wait();  // the arg-min (binom is static: staged before the wait)
+    TL_WAITED();
     const Key key = *result;
     const unsigned long long e = *err;
     __syncwarp();
@@ -131,7 +144,13 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
         out->status = GP_OK;
         out->flags = *I.flags;  // table flags travel back with the result
     }
-    if (e != ~0ull || key.tie == ~0ull) return;
+    auto flush = [&]() {
+        __syncwarp();
+        const unsigned long long* src = (const unsigned long long*)&so;
+        unsigned long long* d = (unsigned long long*)dst;
+        for (int q = lane; q < (int)(sizeof(SolveOut) / 8); q += 32) d[q] = src[q];
+    };
+    if (e != ~0ull || key.tie == ~0ull) { flush(); TL_STOP(50); return; }
     const int n = I.n;
     const unsigned long long t = key.tie;
     const int bm = (int)(t % (unsigned long long)nbm);
@@ -168,6 +187,8 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
         }
     }
     plan_detail_warp(I, k, o, p, bm, &out->info, &out->status);
+    flush();
+    TL_STOP(50);
 }
 
 

@@ -25,6 +25,7 @@
 // (src/costmodel.py:56-89, src/timing.py:116-231, src/planner.py:157-253);
 // the file is compiled with -fmad=false.  There is no CPU fallback.
 #include <mutex>
+#include <chrono>
 
 #include "common.cuh"
 #include "k1_tables.cuh"
@@ -120,7 +121,8 @@ struct gp_ctx {
     DBuf<uint32_t> s_wq;         // K5 full queue scratch
     DBuf<uint8_t> g_buf;         // K7 inputs, outputs and scratch
     DBuf<unsigned long long> s_lq;
-    SolveOut* h_solve = nullptr;  // pinned
+    SolveOut* h_solve = nullptr;  // pinned, mapped (the gp_replan graph's detail kernel writes it)
+    SolveOut* d_hsolve = nullptr; // device alias of h_solve
     RangeGeom last_geom{};
     bool last_generic = false;
     unsigned long long last_lo = 0, last_hi = 0;
@@ -131,7 +133,8 @@ struct gp_ctx {
     cudaEvent_t arena_ev = nullptr;
     bool flags_known = false;
     // raw instance arena: one pinned staging buffer -> one H2D copy
-    unsigned char* h_arena = nullptr;
+    unsigned char* h_arena = nullptr;   // pinned, mapped
+    const unsigned char* d_harena = nullptr;  // device alias (k_arena_pull reads it)
     size_t h_arena_cap = 0;
     DBuf<unsigned char> arena;
     int cache_n = -1, cache_k = -1;   // (n, k) of the enumeration helpers
@@ -146,6 +149,7 @@ struct gp_ctx {
     bool diag_timing = false;          // gp_diag_replan_timing
     cudaEvent_t t_ev0 = nullptr, t_ev1 = nullptr;
     float last_graph_ms = -1.0f;
+    double host_us[4] = {0, 0, 0, 0};  // gp_replan: arena fill, launch, wait, finish
     size_t arena_bytes = 0;
     int force_mode = -1;  // -1 auto; 0/1/2 fast-path variant; 3 generic kernel
     std::vector<uint32_t> h_fg_sg_count;  // subgroups per group (explicit plans)
@@ -246,7 +250,8 @@ int gp_ctx_create(int device, gp_ctx** out) {
     c->n_sms = prop.multiProcessorCount;
     if (const char* fm = getenv("GP_K3_MODE")) c->force_mode = atoi(fm);
     if (cudaHostAlloc((void**)&c->h_flags, sizeof(uint32_t), cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc((void**)&c->h_solve, sizeof(SolveOut), cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc((void**)&c->h_solve, sizeof(SolveOut), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&c->d_hsolve, c->h_solve, 0) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->flags_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->arena_ev, cudaEventDisableTiming) != cudaSuccess) {
         gp_ctx_destroy(c);
@@ -276,6 +281,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     for (auto* b : bb) b->release();
     c->arena.release();
     if (c->h_arena) cudaFreeHost(c->h_arena);
+    c->d_harena = nullptr;
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->h_solve) cudaFreeHost(c->h_solve);
     c->z_bw.release(); c->z_mbw.release(); c->z_xt.release(); c->z_flags.release();
@@ -393,8 +399,11 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
         if (c->h_arena) cudaFreeHost(c->h_arena);
         c->h_arena = nullptr;
         c->h_arena_cap = 0;
-        CUDA_TRY(cudaHostAlloc((void**)&c->h_arena, off, cudaHostAllocDefault));
+        CUDA_TRY(cudaHostAlloc((void**)&c->h_arena, off, cudaHostAllocMapped));
         c->h_arena_cap = off;
+        void* dp = nullptr;
+        CUDA_TRY(cudaHostGetDevicePointer(&dp, c->h_arena, 0));
+        c->d_harena = (const unsigned char*)dp;
     }
     for (int i = 0; i < ns; ++i)
         if (seg[i].bytes) memcpy(c->h_arena + seg[i].off, seg[i].src, seg[i].bytes);
@@ -1072,9 +1081,13 @@ static int enqueue_solve(gp_ctx* c, uint64_t lo, uint64_t hi) {
     const RangeGeom& G = c->last_geom;
     CUDA_TRY(c->dsolve.ensure(1));
     DevInst I = c->view();
+    // inside the gp_replan graph the record goes straight to the mapped pinned
+    // buffer (no D2H node); elsewhere to device memory + an async copy
+    SolveOut* dst = c->pdl ? c->d_hsolve : c->dsolve.p;
     CUDA_TRY(launch_k(k_solve_detail, 1, 32, 0, c->stream, c->pdl, I, G.k, G.NC, G.NP, G.nbm,
                       (const Key*)c->result.p, (const unsigned long long*)c->err_idx.p,
-                      (const unsigned long long*)c->binom.p, c->dsolve.p));
+                      (const unsigned long long*)c->binom.p, dst));
+    if (c->pdl) return GP_OK;
     CUDA_TRY(cudaMemcpyAsync(c->h_solve, c->dsolve.p, sizeof(SolveOut), cudaMemcpyDeviceToHost,
                              c->stream));
     return GP_OK;
@@ -1136,8 +1149,14 @@ static void instance_shape(const gp_instance* in, unsigned long long* key) {
     key[8] = h;
 }
 
+static inline double now_us() {
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* info) {
     if (!c || !in || !best) return fail(GP_ERR_INPUT, "null argument");
+    const double h0 = c->diag_timing ? now_us() : 0.0;
     unsigned long long key[10];
     instance_shape(in, key);
     memcpy(&key[9], &in->bottleneck_factor, sizeof(double));
@@ -1159,8 +1178,12 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
         CUDA_TRY(c->item_ctr.ensure((size_t)c->nm * h_fact(c->F) + 1));
         c->capturing = true;
         CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-        cudaError_t ce = cudaMemcpyAsync(c->arena.p, c->h_arena, c->arena_bytes,
-                                         cudaMemcpyHostToDevice, s);
+        // the instance arena moves host -> device by a kernel reading the mapped
+        // pinned buffer (no copy-engine node; K1 phase 1 follows by PDL)
+        const unsigned long long n16 = (c->arena_bytes + 15) / 16;
+        const unsigned pull_blocks = (unsigned)((n16 + 255) / 256 < 148 ? (n16 + 255) / 256 : 148);
+        cudaError_t ce = launch_k(k_arena_pull, pull_blocks > 0 ? pull_blocks : 1u, 256, 0, s, false,
+                                  (const uint4*)c->d_harena, (uint4*)c->arena.p, n16);
         int st2 = ce == cudaSuccess ? GP_OK : fail(GP_ERR_CUDA, "capture: %s", cudaGetErrorString(ce));
         if (st2 == GP_OK) {
             // H2D -> K1 phase 1 (resets flags, err_idx, item counters) -> phase 2
@@ -1169,11 +1192,15 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
             DevInst I = c->view();
             const int gw_blocks = (c->F * c->F + 3) / 4;
             K1Reset R = {c->err_idx.p, c->item_ctr.p, (unsigned)((size_t)c->nm * h_fact(c->F))};
-            ce = launch_k(k1_phase1, 5 + c->F + gw_blocks, 128, 0, s, false, I, R);
+            ce = launch_k(k1_phase1, 5 + c->F + gw_blocks, 128, 0, s, true, I, R);
             long long ns = (long long)c->F * (c->n + 1) * (c->n + 1);
             long long nx = (long long)c->nm * c->F * c->F * c->n;
             if (ce == cudaSuccess)
                 ce = launch_k(k1_phase2, (unsigned)((ns + nx + 127) / 128), 128, 0, s, true, I, ns);
+#if defined(GP_TIMELINE)
+            if (getenv("GP_K1_TWICE") && ce == cudaSuccess)  // icache experiment
+                ce = launch_k(k1_phase2, (unsigned)((ns + nx + 127) / 128), 128, 0, s, true, I, ns);
+#endif
             if (ce != cudaSuccess) st2 = fail(GP_ERR_CUDA, "capture: %s", cudaGetErrorString(ce));
             c->flags_known = false;
             c->pdl = true;
@@ -1221,15 +1248,24 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
         c->last_lo = c->graph_lo;
         c->last_hi = c->graph_hi;
     }
+    const double h1 = c->diag_timing ? now_us() : 0.0;
     if (c->diag_timing) CUDA_TRY(cudaEventRecord(c->t_ev0, s));
     CUDA_TRY(cudaGraphLaunch(c->graph_exec, s));
     CUDA_TRY(cudaEventRecord(c->arena_ev, s));
     if (c->diag_timing) CUDA_TRY(cudaEventRecord(c->t_ev1, s));
+    const double h2 = c->diag_timing ? now_us() : 0.0;
     CUDA_TRY(cudaStreamSynchronize(s));
+    const double h3 = c->diag_timing ? now_us() : 0.0;
     if (c->diag_timing) CUDA_TRY(cudaEventElapsedTime(&c->last_graph_ms, c->t_ev0, c->t_ev1));
     c->flags_known = false;
     c->loaded = true;
-    return finish_solve(c, best, info);
+    const int rs = finish_solve(c, best, info);
+    if (c->diag_timing) {
+        const double h4 = now_us();
+        c->host_us[0] = h1 - h0; c->host_us[1] = h2 - h1;
+        c->host_us[2] = h3 - h2; c->host_us[3] = h4 - h3;
+    }
+    return rs;
 }
 
 int gp_plan_detail(gp_ctx* c, uint32_t k, const uint8_t* order, const uint8_t* counts, uint32_t bm,
@@ -1862,6 +1898,31 @@ int gp_plan_cost(gp_ctx* c, uint32_t k, const gp_plan_stage* stages, int64_t bat
 int gp_ctx_set_k3_mode(gp_ctx* c, int mode) {
     if (!c || mode < -1 || mode > 4) return fail(GP_ERR_INPUT, "bad mode");
     c->force_mode = mode;
+    return GP_OK;
+}
+
+int gp_diag_timeline(void* out, uint32_t cap, uint32_t* n_out) {
+    if (!n_out) return fail(GP_ERR_INPUT, "null output");
+    *n_out = 0;
+#if defined(GP_TIMELINE)
+    unsigned int n = 0;
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyFromSymbol(&n, g_tl_n, sizeof(n)));
+    if (n > GP_TL_CAP) n = GP_TL_CAP;
+    if (n > cap) n = cap;
+    if (out && n) CUDA_TRY(cudaMemcpyFromSymbol(out, g_tl, n * sizeof(TlRec)));
+    const unsigned int zero = 0;
+    CUDA_TRY(cudaMemcpyToSymbol(g_tl_n, &zero, sizeof(zero)));
+    *n_out = n;
+#else
+    (void)out; (void)cap;
+#endif
+    return GP_OK;
+}
+
+int gp_diag_replan_host(gp_ctx* c, double* host_us4) {
+    if (!c || !host_us4) return fail(GP_ERR_INPUT, "null argument");
+    memcpy(host_us4, c->host_us, sizeof(c->host_us));
     return GP_OK;
 }
 

@@ -181,6 +181,9 @@ __device__ int choose_split(const DevInst& I, int f, int a, int b, int* shares, 
 // One thread per (group, a, b).  memory_feasible is local to a stage because
 // every group appears in exactly one stage (src/planner.py:226-253).
 __device__ void k1_stage_t(const DevInst& I, long long t) {
+#if defined(GP_TIMELINE)
+    const unsigned long long tt0 = tl_now();
+#endif
     int n = I.n;
     int N1 = n + 1;
     long long total = (long long)I.F * N1 * N1;
@@ -203,6 +206,9 @@ __device__ void k1_stage_t(const DevInst& I, long long t) {
     }
     int shares[GP_MAX_SGS], np;
     int kind = choose_split(I, f, a, b, shares, &np);
+#if defined(GP_TIMELINE)
+    const unsigned long long ttw = tl_now();
+#endif
     I.skind[e] = (uint8_t)kind;
     double P = Ssum(I, COL_PARAM, a, b);
     int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
@@ -284,6 +290,15 @@ __device__ void k1_stage_t(const DevInst& I, long long t) {
     I.scode[e] = feas ? code : SC_INFEASIBLE;
     if (feas && code != SC_OK) atomicOr(I.flags, FLAG_STAGE_ERROR);
     if (overflow) atomicOr(I.flags, FLAG_OVERFLOW);
+#if defined(GP_TIMELINE)
+    {   // per-thread record: kid 22, blk = f<<16 | a<<8 | b, pad = split kind
+        const unsigned long long tt1 = tl_now();
+        unsigned int _i = atomicAdd(&g_tl_n, 1u);
+        if (_i < GP_TL_CAP)
+            g_tl[_i] = TlRec{tt0, ttw, tt1, 22u, (unsigned)((f << 16) | (a << 8) | b), 0u,
+                             (unsigned)kind};
+    }
+#endif
 }
 
 // ---- K1d: gateways and boundary transfer table -------------------------------------
@@ -331,6 +346,18 @@ __global__ void k1_gateways(DevInst I) {
 __device__ void k1_intervals_block(const DevInst& I, int col);
 __device__ void k1_gateway_warp(const DevInst& I, int warp, int lane);
 
+// gp_replan graph head: instance arena host -> device by loads from the
+// mapped pinned staging buffer (16 B per thread, grid-stride)
+__global__ void k_arena_pull(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                             unsigned long long n16) {
+    TL_START();
+    pdl_trigger();
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+    TL_STOP(5);
+}
+
 // Per-run scratch that the gp_replan graph resets inside phase 1 instead of
 // with memset nodes (null pointers: nothing to reset).
 struct K1Reset {
@@ -341,7 +368,10 @@ struct K1Reset {
 
 __global__ void __launch_bounds__(128) k1_phase1(DevInst I, K1Reset R) {
     const int b = blockIdx.x;
+    TL_START();
     pdl_trigger();  // phase 2 may be scheduled now (it waits for this grid)
+    pdl_wait();     // the instance arena (k_arena_pull in the gp_replan graph)
+    TL_WAITED();
     if (b == 0) {
         if (threadIdx.x == 0) {
             *I.flags = 0u;
@@ -350,10 +380,6 @@ __global__ void __launch_bounds__(128) k1_phase1(DevInst I, K1Reset R) {
         for (unsigned int t = threadIdx.x; R.item_ctr && t < R.n_items; t += blockDim.x)
             R.item_ctr[t] = 0u;
     }
-#if defined(K1_PROFILE)
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-#endif
     if (b == 0)  // M = batch / micro per (b, m) index, for the per-candidate kernels
         for (int t = threadIdx.x; t < I.nb * I.nm; t += blockDim.x)
             I.mtab[t] = (double)(I.batch[t / I.nm] / I.micro[t % I.nm]);
@@ -363,11 +389,9 @@ __global__ void __launch_bounds__(128) k1_phase1(DevInst I, K1Reset R) {
         const int warp = (b - 5 - I.F) * 4 + (threadIdx.x >> 5);
         if (warp < I.F * I.F) k1_gateway_warp(I, warp, threadIdx.x & 31);
     }
-#if defined(K1_PROFILE)
+#if defined(GP_TIMELINE)
     __syncthreads();
-    unsigned long long t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    if (threadIdx.x == 0) printf("k1_phase1 block %d: %llu ns\n", b, t1 - t0);
+    TL_STOP(b < 5 ? 10 : (b < 5 + I.F ? 11 : 12));  // intervals / groups / gateways
 #endif
 }
 
@@ -388,10 +412,16 @@ __device__ void k1_boundary_t(const DevInst& I, long long t) {
 
 // K1 phase 2 in one launch: stage table entries, then boundary x entries
 __global__ void k1_phase2(DevInst I, long long n_stage) {
+    TL_START();
     pdl_trigger();
     pdl_wait();  // phase 1's interval sums, group constants and gateways
+    TL_WAITED();
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < n_stage) k1_stage_t(I, t);
     else k1_boundary_t(I, t - n_stage);
+#if defined(GP_TIMELINE)
+    __syncthreads();
+    TL_STOP(blockIdx.x * blockDim.x < n_stage ? 20 : 21);  // stage / boundary blocks
+#endif
 }
 

@@ -268,8 +268,10 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
 #if defined(K3_PROFILE)
     unsigned long long t0p; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0p));
 #endif
+    TL_START();
     pdl_trigger();
     pdl_wait();  // K1's tables (gp_replan graph); no-op on plain launches
+    TL_WAITED();
     const int n = I.n, k = KS > 0 ? KS : G.k;
     const int ntri = n * (n + 1) / 2;
     const int KB = k + 1;
@@ -489,6 +491,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
 #endif
     block_argmin_finish(mine, Ss, per_snap, local);
     if (mc) cluster_wait();  // no CTA leaves while a multicast into a peer may be in flight
+    TL_STOP(30);
 #if defined(K3_PROFILE)
     { unsigned long long t3; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
       if (threadIdx.x == 0) printf("K3P %d %d %llu %llu %llu %llu\n", blockIdx.x, (int)__nv_smid_k3(), t0p, t1p, t2p, t3); }
@@ -512,9 +515,11 @@ __global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G,
                                                          const uint32_t* only_if_flags) {
     // fix-up launch behind a fast-path kernel: do nothing unless the table
     // build raised a flag (then this kernel's result replaces the fast one)
+    TL_START();
     pdl_trigger();
     pdl_wait();
-    if (only_if_flags && *only_if_flags == 0u) return;
+    TL_WAITED();
+    if (only_if_flags && *only_if_flags == 0u) { TL_STOP(40); return; }
     Key mine{INFINITY, ~0ull};
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long t = G.lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;

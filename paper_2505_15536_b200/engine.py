@@ -90,6 +90,7 @@ def lib():
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
         L.gp_diag_replan_timing.argtypes = [vp, C.c_int, P(C.c_double)]
+        L.gp_diag_replan_host.argtypes = [vp, P(C.c_double)]
         L.gp_plan_cost.argtypes = [vp, C.c_uint32, P(abi.GpPlanStage), C.c_int64, C.c_int64,
                                    C.c_double, P(abi.GpPlanInfo), P(abi.GpTiming)]
         L.gp_plan_timing.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_double,
@@ -416,6 +417,13 @@ class Engine:
         out = C.c_double(-1.0)
         _check(lib().gp_diag_replan_timing(self._h, int(bool(enable)), C.byref(out)))
         return out.value
+
+    def replan_host_us(self):
+        """Host phases of the last timed gp_replan (us): arena fill, graph
+        launch call, wait, result decode."""
+        out = (C.c_double * 4)()
+        _check(lib().gp_diag_replan_host(self._h, out))
+        return list(out)
 
     def set_bandwidth(self, bw: np.ndarray) -> None:
         a = np.ascontiguousarray(bw, dtype=np.float64)

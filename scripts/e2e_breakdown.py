@@ -21,7 +21,7 @@ packs = [PackedInstance(*instances.load("c4", snapshot=j), 1.25) for j in range(
 eng = Engine(0)
 for timed in (False, True):
     eng.replan_timing(timed)
-    host, dev = [], []
+    host, dev, ph = [], [], []
     for i in range(400):
         t0 = time.perf_counter()
         best, info = eng.replan(packs[i % 4])
@@ -30,6 +30,11 @@ for timed in (False, True):
             host.append(el * 1e3)
             if timed:
                 dev.append(eng.replan_timing(True))
+                ph.append(eng.replan_host_us())
     print(f"gp_replan C4 host ms ({'with' if timed else 'without'} graph events): {pct(host)}")
     if timed:
         print(f"gp_replan C4 graph device ms: {pct(dev)}")
+        import numpy as np
+        med = np.median(np.array(ph), axis=0)
+        print("host phases p50 us: arena fill %.1f, graph launch %.1f, wait %.1f, decode %.1f"
+              % tuple(med))
