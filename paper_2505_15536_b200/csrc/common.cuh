@@ -56,6 +56,19 @@ enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 
 #endif
 #define BINOM_ROWS 257
 
+// Per-group constants of the stage-table build, one 128-byte record per
+// first-level group written by K1 phase 1 (k1_group_block) so that a phase-2
+// thread reads its group in one round trip.  `fast` = the register path of
+// k1_stage_t applies (<= 2 second-level groups); tp_thr = the TP memory
+// threshold (see tp_threshold), valid when thr_ok.
+struct __align__(16) K1Grp {
+    double cap, mbw, minmem, tp_thr;  // fg capacity, min intra bw, min member memory
+    double sgcap[4], sgmin[4];        // second-level capacities / min memories
+    int nmem, s0, nsg;
+    uint8_t has, tp_ok, thr_ok, sgne;  // sgne bit j: SG j has members
+    int fast, pad[3];
+};
+
 // ----------------------------------------------------------------------------
 // device-side view of one loaded instance
 // ----------------------------------------------------------------------------
@@ -77,6 +90,9 @@ struct DevInst {
     // K1 outputs
     double* S;                   // [5][(n+1)^2]: fwd, bwd_in, bwd_w, param, total_flops
     uint8_t* g_tp_ok;            // [F]
+    K1Grp* grp;                  // [F] packed per-group constants (phase 1 -> phase 2)
+    uint8_t* sshare0;            // [F][(n+1)^2] first ASYMMETRIC_PP share (winner detail)
+    uint8_t* gwbad;              // [F*F] gateway bandwidth not > 0 (winner detail)
     double *g_rf, *g_cf;         // [fg member slots]
     double* g_dp;                // [sg slots]
     double* g_minmem;            // [F]

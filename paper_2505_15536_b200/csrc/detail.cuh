@@ -45,27 +45,40 @@ __device__ void plan_detail_warp(const DevInst& I, int k, const uint8_t* o, cons
     uint8_t code = SC_OK;
     bool gw_bad = false;
     if (lane < k) {
+        // the split of (group, a, b) comes from K1's tables (kind, first PP
+        // share, group sizes); only groups with > 2 second-level groups
+        // re-run choose_intra_split for their PP shares
         const int s = lane;
         gp_stage_info& st = out->stage[s];
-        int shares[GP_MAX_SGS], np;
-        const int kind = choose_split(I, o[s], p[s], p[s + 1], shares, &np);
-        st.kind = (uint32_t)kind;
-        st.n_parts = (uint32_t)np;
-        if (kind == GP_ASYM_PP) {
-            int pos = p[s];
-            for (int j = 0; j < np; ++j) {
-                st.pp_sg[j] = (uint32_t)j;
-                st.pp_start[j] = (uint32_t)pos;
-                st.pp_end[j] = (uint32_t)(pos + shares[j]);
-                pos += shares[j];
-            }
-        }
-        const size_t ei = (size_t)o[s] * N2 + tri_idx(n, p[s], p[s + 1]);
+        const int f = o[s], a = p[s], b = p[s + 1];
+        const size_t ei = (size_t)f * N2 + tri_idx(n, a, b);
+        const int kind = I.skind[ei];
+        const int sh0 = I.sshare0[ei];
+        const K1Grp g = I.grp[f];
         e = T[ei];
         code = I.scode[ei];
         if (s + 1 < k) {
-            x = X[((size_t)o[s] * I.F + o[s + 1]) * I.nxp + (p[s + 1] - 1)];
-            gw_bad = !(I.bw[I.gw[o[s] * I.F + o[s + 1]]] > 0);
+            x = X[((size_t)f * I.F + o[s + 1]) * I.nxp + (b - 1)];
+            gw_bad = I.gwbad[f * I.F + o[s + 1]] != 0;
+        }
+        const int np = kind == GP_UNIFORM ? 0 : (kind == GP_ASYM_TP_DP ? g.nmem : g.nsg);
+        st.kind = (uint32_t)kind;
+        st.n_parts = (uint32_t)np;
+        if (kind == GP_ASYM_PP) {
+            if (g.nsg == 2) {
+                st.pp_sg[0] = 0u; st.pp_start[0] = (uint32_t)a; st.pp_end[0] = (uint32_t)(a + sh0);
+                st.pp_sg[1] = 1u; st.pp_start[1] = (uint32_t)(a + sh0); st.pp_end[1] = (uint32_t)b;
+            } else {
+                int shares[GP_MAX_SGS], np2;
+                choose_split(I, f, a, b, shares, &np2);
+                int pos = a;
+                for (int j = 0; j < np2; ++j) {
+                    st.pp_sg[j] = (uint32_t)j;
+                    st.pp_start[j] = (uint32_t)pos;
+                    st.pp_end[j] = (uint32_t)(pos + shares[j]);
+                    pos += shares[j];
+                }
+            }
         }
     }
     const unsigned infeas = __ballot_sync(0xffffffffu, lane < k && code == SC_INFEASIBLE);

@@ -18,9 +18,12 @@ struct NeumaierSum {
     double f, c;
     __host__ __device__ void start(double x0) { f = 0.0 + x0; c = 0.0; }
     __host__ __device__ void add(double x) {
-        double t = f + x;
-        if (fabs(f) >= fabs(x)) c += (f - t) + x;
-        else c += (x - t) + f;
+        // c += (big - t) + small with big the operand of larger magnitude
+        // (selects instead of a divergent branch; identical arithmetic)
+        const double t = f + x;
+        const bool fb = fabs(f) >= fabs(x);
+        const double big = fb ? f : x, small = fb ? x : f;
+        c += (big - t) + small;
         f = t;
     }
     __host__ __device__ double value() const {

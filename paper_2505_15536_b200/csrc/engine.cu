@@ -90,6 +90,8 @@ struct gp_ctx {
     DBuf<double2> tpk, tcol;
     DBuf<uint32_t> flagsbuf;
     DBuf<uint8_t> g_tp_ok, scode, skind;
+    DBuf<K1Grp> kgrp;
+    DBuf<uint8_t> sshare0, gwbad;
     DBuf<double2> stg;
     DBuf<int> gw;
     // K3 scratch
@@ -176,6 +178,7 @@ struct gp_ctx {
         I.fg_cap = fg_cap.p; I.sg_cap = sg_cap.p;
         I.fg_minbw = fg_minbw.p; I.fg_has_minbw = fg_has.p;
         I.bf = bf;
+        I.grp = kgrp.p; I.sshare0 = sshare0.p; I.gwbad = gwbad.p;
         I.S = S.p; I.g_tp_ok = g_tp_ok.p; I.g_rf = g_rf.p; I.g_cf = g_cf.p; I.g_dp = g_dp.p;
         I.g_minmem = g_minmem.p; I.sg_minmem = sg_minmem.p;
         I.stg = stg.p; I.scode = scode.p; I.skind = skind.p; I.C1 = C1.p; I.fbws = fbws.p; I.vtab = vtab.p;
@@ -273,6 +276,9 @@ void gp_ctx_destroy(gp_ctx* c) {
                           &c->C1, &c->xt, &c->b_cost};
     for (auto* b : dd) b->release();
     c->fbws.release();
+    c->kgrp.release();
+    c->sshare0.release();
+    c->gwbad.release();
     c->vtab.release();
     c->mtab.release();
     c->flagsbuf.release();
@@ -438,6 +444,9 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     size_t N2 = (size_t)(n + 1) * (n + 1);
     CUDA_TRY(c->S.ensure(5 * N2));
     CUDA_TRY(c->g_tp_ok.ensure(F));
+    CUDA_TRY(c->kgrp.ensure(F));
+    CUDA_TRY(c->sshare0.ensure((size_t)F * N2));
+    CUDA_TRY(c->gwbad.ensure((size_t)F * F));
     CUDA_TRY(c->g_rf.ensure(nfm));
     CUDA_TRY(c->g_cf.ensure(nfm));
     CUDA_TRY(c->g_dp.ensure(nsg ? nsg : 1));

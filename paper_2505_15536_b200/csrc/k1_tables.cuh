@@ -52,24 +52,56 @@ __device__ __forceinline__ double block_min128(double v, double* red) {
     return r;
 }
 
+// TP memory threshold of one member: the largest non-NaN double P with
+// !(((P * rf) * cf) > mem), i.e. the member accepts a stage of parameter sum
+// P iff !(P > threshold).  Rounding is monotone, so for 0 < rf, cf < inf the
+// accepted set is a down-set of the doubles and a bisection over their
+// ordered bit patterns finds its top exactly (64 steps).  *ok = false where
+// the monotone argument does not apply (the caller keeps the member loop).
+__device__ double tp_threshold(double rf, double cf, double mem, bool* ok) {
+    *ok = rf > 0.0 && rf < INFINITY && cf > 0.0 && cf < INFINITY;
+    if (!*ok) return 0.0;
+    auto key = [](double d) -> unsigned long long {
+        const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+        return (u >> 63) ? ~u : (u | (1ull << 63));
+    };
+    auto unkey = [](unsigned long long k) -> double {
+        const unsigned long long u = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
+        return __longlong_as_double((long long)u);
+    };
+    auto accept = [&](double P) { return !(((P * rf) * cf) > mem); };
+    if (accept(INFINITY)) return INFINITY;
+    if (!accept(-INFINITY)) { *ok = false; return 0.0; }
+    unsigned long long lo = key(-INFINITY), hi = key(INFINITY);  // accept(lo), !accept(hi)
+    while (hi - lo > 1ull) {
+        const unsigned long long mid = lo + (hi - lo) / 2ull;
+        if (accept(unkey(mid))) lo = mid; else hi = mid;
+    }
+    return unkey(lo);
+}
+
 // one 128-thread block per group: members loaded in parallel into shared
 // memory; the TP grid factorisation (split_asymmetric_tp_dp,
 // src/planner.py:116-154) checks each candidate shape with every thread
 // (one isclose per thread, block AND) and divides the fractions in parallel;
-// only the short Neumaier sums run on one thread.
+// only the short Neumaier sums run on one thread.  Ends with the packed
+// K1Grp record phase 2 reads.
 __device__ void k1_group_block(const DevInst& I, int f) {
     __shared__ double caps[GP_MAX_MEMBERS];
+    __shared__ double memv[GP_MAX_MEMBERS];
     __shared__ double red[4];
     __shared__ int shp[64];
     __shared__ int ns_sh;
     __shared__ double sums[2];
     const int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
     const int nmem = m1 - m0;
+    const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
     double mn = INFINITY;
     for (int j = threadIdx.x; j < nmem; j += blockDim.x) {
         const int d = I.fg_mem[m0 + j];
         caps[j] = I.p_c[d];
         const double mm = I.mem[d];
+        memv[j] = mm;
         mn = mm < mn ? mm : mn;
     }
     mn = block_min128(mn, red);  // (synchronises: caps visible)
@@ -91,11 +123,12 @@ __device__ void k1_group_block(const DevInst& I, int f) {
             shp[j + 1] = r;
         }
         ns_sh = ns;
-        const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
         if (s1 > s0) gpd::dp_fractions(I.sg_cap + s0, s1 - s0, I.g_dp + s0);
     }
     __syncthreads();
     bool tp_ok = false;
+    double thr = INFINITY;
+    bool thr_ok = true;
     for (int q = 0; q < ns_sh; ++q) {
         const int r = shp[q], c = nmem / r;
         bool ok = true;
@@ -115,14 +148,24 @@ __device__ void k1_group_block(const DevInst& I, int f) {
         }
         __syncthreads();
         for (int kk = threadIdx.x; kk < nmem; kk += blockDim.x) {
-            I.g_rf[m0 + kk] = caps[kk % r] / sums[0];
-            I.g_cf[m0 + kk] = caps[(kk / r) * r] / sums[1];
+            const double rf = caps[kk % r] / sums[0], cf = caps[(kk / r) * r] / sums[1];
+            I.g_rf[m0 + kk] = rf;
+            I.g_cf[m0 + kk] = cf;
+            bool okx;
+            const double tx = tp_threshold(rf, cf, memv[kk], &okx);
+            thr_ok = thr_ok && okx;
+            thr = tx < thr ? tx : thr;
         }
         tp_ok = true;
         break;
     }
+    if (tp_ok) {  // (block-uniform)
+        thr = block_min128(thr, red);
+        thr_ok = __syncthreads_and(thr_ok) != 0;
+    }
     if (threadIdx.x == 0) I.g_tp_ok[f] = tp_ok ? 1 : 0;
-    const int s0 = I.fg_sg_off[f], s1 = I.fg_sg_off[f + 1];
+    double sgmin[4] = {0.0, 0.0, 0.0, 0.0};
+    uint8_t sgne = 0;
     for (int g = s0; g < s1; ++g) {
         double sm = INFINITY;
         for (int x = I.sg_off[g] + threadIdx.x; x < (int)I.sg_off[g + 1]; x += blockDim.x) {
@@ -130,7 +173,33 @@ __device__ void k1_group_block(const DevInst& I, int f) {
             sm = mm < sm ? mm : sm;
         }
         sm = block_min128(sm, red);
-        if (threadIdx.x == 0) I.sg_minmem[g] = I.sg_off[g + 1] > I.sg_off[g] ? sm : 0.0;
+        const bool ne = I.sg_off[g + 1] > I.sg_off[g];
+        if (threadIdx.x == 0) I.sg_minmem[g] = ne ? sm : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (g - s0 == j) { sgmin[j] = ne ? sm : 0.0; sgne |= ne ? (uint8_t)(1u << j) : (uint8_t)0; }
+    }
+    if (threadIdx.x == 0) {
+        K1Grp R;
+        R.cap = I.fg_cap[f];
+        R.mbw = 0.0;  // (bandwidth-dependent: phase 2 reads I.fg_minbw)
+        R.minmem = mn;
+        R.tp_thr = thr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            R.sgcap[j] = j < s1 - s0 ? I.sg_cap[s0 + j] : 0.0;
+            R.sgmin[j] = sgmin[j];
+        }
+        R.nmem = nmem;
+        R.s0 = s0;
+        R.nsg = s1 - s0;
+        R.has = 0;
+        R.tp_ok = tp_ok ? 1 : 0;
+        R.thr_ok = tp_ok && thr_ok ? 1 : 0;
+        R.sgne = sgne;
+        R.fast = s1 - s0 <= 2 ? 1 : 0;
+        R.pad[0] = R.pad[1] = R.pad[2] = 0;
+        I.grp[f] = R;
     }
 }
 
@@ -153,7 +222,8 @@ __global__ void k1_minbw(DevInst I, double* out) {
 
 // split choice for one (group, layer range): choose_intra_split
 // (src/planner.py:157-200).  Writes PP shares when kind == ASYM_PP.
-__device__ int choose_split(const DevInst& I, int f, int a, int b, int* shares, int* nparts) {
+__device__ __noinline__ int choose_split(const DevInst& I, int f, int a, int b, int* shares,
+                                         int* nparts) {
     int nmem = I.fg_off[f + 1] - I.fg_off[f];
     int s0 = I.fg_sg_off[f], nsg = I.fg_sg_off[f + 1] - s0;
     *nparts = 0;
@@ -177,39 +247,22 @@ __device__ int choose_split(const DevInst& I, int f, int a, int b, int* shares, 
     return GP_ASYM_DP;
 }
 
-// ---- K1c: stage table -------------------------------------------------------------
-// One thread per (group, a, b).  memory_feasible is local to a stage because
-// every group appears in exactly one stage (src/planner.py:226-253).
-__device__ void k1_stage_t(const DevInst& I, long long t) {
+// ---- K1c: stage table, generic path ---------------------------------------------
+// Generic stage entry (any number of second-level groups): the reference
+// order step by step, reading group data from global memory.
+__device__ __noinline__ void k1_stage_generic(const DevInst& I, int f, int a, int b, size_t e) {
 #if defined(GP_TIMELINE)
     const unsigned long long tt0 = tl_now();
 #endif
-    int n = I.n;
-    int N1 = n + 1;
-    long long total = (long long)I.F * N1 * N1;
-    if (t >= total) return;
-    int f = (int)(t / (N1 * N1));
-    int rem = (int)(t % (N1 * N1));
-    int a = rem / N1, b = rem % N1;
-    size_t N2 = (size_t)N1 * N1;
-    size_t e = (size_t)f * N2 + rem;
-    if (a >= b) {
-        I.scode[e] = SC_INFEASIBLE;
-        I.skind[e] = 0;
-        I.C1[e] = INFINITY;
-        I.fbws[e] = make_double4(NAN, NAN, NAN, NAN);
-        for (int mi = 0; mi < I.nm; ++mi) {
-            I.stg[(size_t)mi * I.F * N2 + e] = make_double2(INFINITY, 0.0);
-            if (a == n && b == n) I.tcol[((size_t)mi * I.F + f) * (n + 1) + n] = make_double2(INFINITY, 0.0);
-        }
-        return;
-    }
+    const int n = I.n;
+    const size_t N2 = (size_t)(n + 1) * (n + 1);
     int shares[GP_MAX_SGS], np;
     int kind = choose_split(I, f, a, b, shares, &np);
 #if defined(GP_TIMELINE)
     const unsigned long long ttw = tl_now();
 #endif
     I.skind[e] = (uint8_t)kind;
+    I.sshare0[e] = kind == GP_ASYM_PP ? (uint8_t)shares[0] : (uint8_t)0;
     double P = Ssum(I, COL_PARAM, a, b);
     int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
     int s0 = I.fg_sg_off[f];
@@ -296,6 +349,185 @@ __device__ void k1_stage_t(const DevInst& I, long long t) {
         unsigned int _i = atomicAdd(&g_tl_n, 1u);
         if (_i < GP_TL_CAP)
             g_tl[_i] = TlRec{tt0, ttw, tt1, 22u, (unsigned)((f << 16) | (a << 8) | b), 0u,
+                             (unsigned)kind};
+    }
+#endif
+}
+
+// proportional_split (src/planner.py:65-87) for exactly two parts with
+// minimum = 1, in registers: the stable sort by (-rem, index) is one compare.
+// Returns 1 ok, 0 where the reference raises InfeasibleSplitError, -1 when
+// an operand is not finite (the caller takes the generic path).
+__device__ __forceinline__ int prop_split2(int total, double w0, double w1, int& s0, int& s1) {
+    NeumaierSum ws;
+    ws.start(w0);
+    ws.add(w1);
+    const double wsum = ws.value();
+    const double raw0 = ((double)total * w0) / wsum, raw1 = ((double)total * w1) / wsum;
+    const double fl0 = floor(raw0), fl1 = floor(raw1);
+    if (!(isfinite(raw0) && isfinite(raw1) && fl0 >= 0.0 && fl1 >= 0.0 && fl0 < 1e9 && fl1 < 1e9))
+        return -1;
+    s0 = (int)fl0;
+    s1 = (int)fl1;
+    const double k0 = -(raw0 - fl0), k1 = -(raw1 - fl1);  // sort keys -rem
+    const long long leftover = (long long)total - ((long long)s0 + s1);
+    const long long take = leftover >= 0 ? (leftover < 2 ? leftover : 2)
+                                         : (2 + leftover > 0 ? 2 + leftover : 0);
+    const int rank0 = k1 < k0 ? 1 : 0, rank1 = k0 <= k1 ? 1 : 0;  // (ties: index order)
+    s0 += rank0 < take ? 1 : 0;
+    s1 += rank1 < take ? 1 : 0;
+    // donation loop (shares are >= 0, so at most one move per part)
+    if (s0 < 1) {
+        if (s1 > s0) { if (s1 <= 1) return 0; s1 -= 1; s0 += 1; }
+        else return 0;  // donor = part 0 itself with share 0 <= minimum
+    }
+    if (s1 < 1) {
+        if (s0 >= s1) { if (s0 <= 1) return 0; s0 -= 1; s1 += 1; }
+        else { return 0; }
+    }
+    return 1;
+}
+
+// ---- K1c: stage table -------------------------------------------------------------
+// One thread per (group, a, b).  memory_feasible is local to a stage because
+// every group appears in exactly one stage (src/planner.py:226-253).  The
+// register path issues every independent load up front (group record, the
+// five interval sums, the micro-batch sizes), keeps the split in registers
+// and stores last, so a thread waits on two round trips instead of a chain of
+// dependent ones; the arithmetic is the generic path's, operation by operation.
+__device__ void k1_stage_t(const DevInst& I, long long t, const double* md_s) {
+    const int n = I.n;
+    const int N1 = n + 1, NN = N1 * N1;
+    if (t >= (long long)I.F * NN) return;
+    const int f = (int)(t / NN);
+    const int rem = (int)(t - (long long)f * NN);
+    const int a = rem / N1, b = rem - a * N1;
+    const size_t N2 = (size_t)NN;
+    const size_t e = (size_t)f * N2 + rem;
+    if (a >= b) {
+        I.scode[e] = SC_INFEASIBLE;
+        I.skind[e] = 0;
+        I.sshare0[e] = 0;
+        I.C1[e] = INFINITY;
+        I.fbws[e] = make_double4(NAN, NAN, NAN, NAN);
+        for (int mi = 0; mi < I.nm; ++mi) {
+            I.stg[(size_t)mi * I.F * N2 + e] = make_double2(INFINITY, 0.0);
+            if (a == n && b == n) I.tcol[((size_t)mi * I.F + f) * (n + 1) + n] = make_double2(INFINITY, 0.0);
+        }
+        return;
+    }
+    const K1Grp g = I.grp[f];
+    if (!g.fast || md_s == nullptr) { k1_stage_generic(I, f, a, b, e); return; }
+#if defined(GP_TIMELINE)
+    const unsigned long long tt0 = tl_now();
+#endif
+    const double* __restrict__ S = I.S;
+    const int si = s_idx(n, a, b);
+    const double sF = S[COL_FWD * N2 + si], sB = S[COL_BWD * N2 + si], sW = S[COL_WGT * N2 + si];
+    const double sP = S[COL_PARAM * N2 + si], sT = S[COL_TF * N2 + si];
+    const double act_b = I.act[b - 1];
+    const double mbw = I.fg_minbw[f];
+    const bool has = I.fg_has_minbw[f] != 0;
+    // choose_intra_split (src/planner.py:157-200)
+    const int nmem = g.nmem;
+    int kind, sh0 = 0, sh1 = 0;
+    double subT0 = 0.0, subT1 = 0.0, subP0 = 0.0, subP1 = 0.0;
+    bool pp = false;
+    if (nmem == 1 || g.nsg == 1) {
+        kind = GP_UNIFORM;
+    } else {
+        if (b - a >= 2) {
+            const int ps = prop_split2(b - a, g.sgcap[0], g.sgcap[1], sh0, sh1);
+            if (ps < 0) { k1_stage_generic(I, f, a, b, e); return; }
+            if (ps == 1) {
+                const int q0 = s_idx(n, a, a + sh0), q1 = s_idx(n, a + sh0, a + sh0 + sh1);
+                subT0 = S[COL_TF * N2 + q0];
+                subT1 = S[COL_TF * N2 + q1];
+                subP0 = S[COL_PARAM * N2 + q0];
+                subP1 = S[COL_PARAM * N2 + q1];
+                const double t0 = subT0 / g.sgcap[0], t1 = subT1 / g.sgcap[1];
+                NeumaierSum ts;
+                ts.start(t0);
+                ts.add(t1);
+                const double mean = ts.value() / 2.0;
+                const double mx = t1 > t0 ? t1 : t0;
+                pp = mx <= I.bf * mean;
+            }
+        }
+        kind = pp ? GP_ASYM_PP : (g.tp_ok ? GP_ASYM_TP_DP : GP_ASYM_DP);
+    }
+    // memory_feasible (src/planner.py:226-253)
+    bool feas;
+    if (kind == GP_ASYM_PP) {
+        feas = !((g.sgne & 1) && subP0 > g.sgmin[0]) && !((g.sgne & 2) && subP1 > g.sgmin[1]);
+    } else if (kind == GP_ASYM_TP_DP) {
+        if (g.thr_ok) {
+            feas = !(sP > g.tp_thr);
+        } else {
+            feas = true;
+            const int m0 = I.fg_off[f];
+            for (int x = m0; x < m0 + nmem; ++x)
+                feas = feas & !(((sP * I.g_rf[x]) * I.g_cf[x]) > I.mem[I.fg_mem[x]]);
+        }
+    } else {
+        feas = !(sP > g.minmem);
+    }
+    // effective_capacity (src/timing.py:116-143)
+    uint8_t code = SC_OK;
+    double cap;
+    if (kind == GP_ASYM_PP) {
+        const double fr0 = subT0 / sT, fr1 = subT1 / sT;
+        bool hv = false;
+        double best = 0.0;
+        if (fr0 > 0) { best = g.sgcap[0] / fr0; hv = true; }
+        if (fr1 > 0) { const double v1 = g.sgcap[1] / fr1; if (!hv || v1 < best) best = v1; hv = true; }
+        cap = best;
+        if (!hv) code = SC_DEGENERATE;
+    } else {
+        cap = g.cap;
+        if (!(cap > 0)) code = SC_DEGENERATE;
+    }
+    const double Fp = sF / cap, Bp = sB / cap, Wp = sW / cap;
+    const double c1 = (Fp + Bp) + Wp;
+    const double sync = (sP == 0.0 || !has) ? 0.0 : (mbw > 0 ? sP / mbw : NAN);
+    if (code == SC_OK && has && !(mbw > 0) && (nmem >= 2 || sP != 0.0)) code = SC_TOPOLOGY;
+#if defined(GP_TIMELINE)
+    const unsigned long long ttw = tl_now();
+#endif
+    I.skind[e] = (uint8_t)kind;
+    I.sshare0[e] = pp ? (uint8_t)sh0 : (uint8_t)0;
+    I.C1[e] = c1;
+    I.fbws[e] = make_double4(Fp, Bp, Wp, sync);
+    const size_t ntri = (size_t)n * (n + 1) / 2;
+    const size_t pk = (size_t)(a * n - a * (a - 1) / 2) + (b - a - 1);
+    bool overflow = false;
+#pragma unroll 1
+    for (int mi = 0; mi < I.nm; ++mi) {
+        const double md = md_s[mi];
+        double al = 0.0;
+        double V = 0.0;
+        if (nmem >= 2) {
+            V = 2.0 * sP;
+            if (kind == GP_ASYM_TP_DP) V = V + act_b * md;
+            if (V != 0.0 && has && mbw > 0) al = V / mbw;
+        }
+        const double cm = c1 * md;
+        if (feas && isinf(cm)) overflow = true;
+        I.vtab[((size_t)mi * I.F + f) * ntri + pk] = V;
+        const double2 v = make_double2(feas ? cm : INFINITY, al);
+        I.stg[(size_t)mi * I.F * N2 + e] = v;
+        I.tpk[((size_t)mi * I.F + f) * ntri + pk] = v;
+        if (b == n) I.tcol[((size_t)mi * I.F + f) * (n + 1) + a] = v;
+    }
+    I.scode[e] = feas ? code : SC_INFEASIBLE;
+    if (feas && code != SC_OK) atomicOr(I.flags, FLAG_STAGE_ERROR);
+    if (overflow) atomicOr(I.flags, FLAG_OVERFLOW);
+#if defined(GP_TIMELINE)
+    {
+        const unsigned long long tt1 = tl_now();
+        unsigned int _i = atomicAdd(&g_tl_n, 1u);
+        if (_i < GP_TL_CAP)
+            g_tl[_i] = TlRec{tt0, ttw, tt1, 23u, (unsigned)((f << 16) | (a << 8) | b), 0u,
                              (unsigned)kind};
     }
 #endif
@@ -403,8 +635,11 @@ __device__ void k1_boundary_t(const DevInst& I, long long t) {
     int pair = (int)(r % (I.F * I.F));
     int mi = (int)(r / (I.F * I.F));
     int g = I.gw[pair];
-    if (mi == 0 && j == 0 && pair / I.F != pair % I.F && !(I.bw[g] > 0))
-        atomicOr(I.flags, FLAG_GATEWAY_ERROR);  // zero-bandwidth gateway
+    if (mi == 0 && j == 0) {
+        const bool bad = !(I.bw[g] > 0);
+        I.gwbad[pair] = bad ? 1 : 0;
+        if (bad && pair / I.F != pair % I.F) atomicOr(I.flags, FLAG_GATEWAY_ERROR);  // zero-bandwidth gateway
+    }
     double md = (double)I.micro[mi];
     // transfer_seconds: latency + (act*m)/bandwidth (src/timing.py:91-97)
     I.xt[(size_t)r * I.nxp + j] = I.lat[g] + (I.act[j] * md) / I.bw[g];
@@ -416,8 +651,11 @@ __global__ void k1_phase2(DevInst I, long long n_stage) {
     pdl_trigger();
     pdl_wait();  // phase 1's interval sums, group constants and gateways
     TL_WAITED();
+    __shared__ double md_s[16];  // (double)micro[mi] for the register path
+    if (threadIdx.x < 16 && threadIdx.x < I.nm) md_s[threadIdx.x] = (double)I.micro[threadIdx.x];
+    __syncthreads();
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < n_stage) k1_stage_t(I, t);
+    if (t < n_stage) k1_stage_t(I, t, I.nm <= 16 ? md_s : nullptr);
     else k1_boundary_t(I, t - n_stage);
 #if defined(GP_TIMELINE)
     __syncthreads();

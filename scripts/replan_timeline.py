@@ -40,6 +40,12 @@ for rep in range(3):
     base = int(tl["t0"].min())
     print(f"--- replan {rep}: graph device {eng.replan_timing(True) * 1e3:.1f} us; "
           f"{len(tl)} CTA records; times in us from the first CTA entry")
+    fs = tl[tl["kid"] == 23]
+    if len(fs):  # register-path stage threads: smid field = clock64 cycles
+        d = (fs["t1"] - fs["t0"]).astype(float)
+        print(f"  fast stage threads: {len(fs)}, p50 {np.median(d) / 1e3:.2f} us, "
+              f"p50 {np.median(fs['smid']):.0f} cycles -> {np.median(fs['smid'] / d) * 1e3:.0f} MHz")
+        tl = tl[tl["kid"] != 23]
     th = tl[tl["kid"] == 22]
     tl = tl[tl["kid"] != 22]
     if len(th):  # per-thread K1 phase-2 stage records (kind = pad)
