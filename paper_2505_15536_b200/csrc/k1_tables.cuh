@@ -30,7 +30,15 @@ __device__ void k1_intervals_block(const DevInst& I, int col) {
         NeumaierSum sm;
         sm.start(col_s[a]);
         out[s_idx(n, a, a + 1)] = sm.value();
-        for (int b = a + 2; b <= n; ++b) {
+        int b = a + 2;
+        for (; b + 3 <= n; b += 4) {  // shared-memory loads of 4 steps issued together
+            const double x0 = col_s[b - 1], x1 = col_s[b], x2 = col_s[b + 1], x3 = col_s[b + 2];
+            sm.add(x0); out[s_idx(n, a, b)] = sm.value();
+            sm.add(x1); out[s_idx(n, a, b + 1)] = sm.value();
+            sm.add(x2); out[s_idx(n, a, b + 2)] = sm.value();
+            sm.add(x3); out[s_idx(n, a, b + 3)] = sm.value();
+        }
+        for (; b <= n; ++b) {
             sm.add(col_s[b - 1]);
             out[s_idx(n, a, b)] = sm.value();
         }
@@ -55,12 +63,12 @@ __device__ __forceinline__ double block_min128(double v, double* red) {
 // TP memory threshold of one member: the largest non-NaN double P with
 // !(((P * rf) * cf) > mem), i.e. the member accepts a stage of parameter sum
 // P iff !(P > threshold).  Rounding is monotone, so for 0 < rf, cf < inf the
-// accepted set is a down-set of the doubles and a bisection over their
-// ordered bit patterns finds its top exactly (64 steps).  *ok = false where
-// the monotone argument does not apply (the caller keeps the member loop).
-__device__ double tp_threshold(double rf, double cf, double mem, bool* ok) {
-    *ok = rf > 0.0 && rf < INFINITY && cf > 0.0 && cf < INFINITY;
-    if (!*ok) return 0.0;
+// accepted set is a down-set of the doubles and its top is found exactly:
+// start from mem / (rf * cf) (a few ulps off) and step ulp by ulp to the
+// boundary; a bisection over the ordered bit patterns covers what the walk
+// cannot (non-finite estimate, > 64 steps).  *ok = false where the monotone
+// argument does not apply (the caller keeps the member loop).
+__device__ __noinline__ double tp_threshold_bisect(double rf, double cf, double mem) {
     auto key = [](double d) -> unsigned long long {
         const unsigned long long u = (unsigned long long)__double_as_longlong(d);
         return (u >> 63) ? ~u : (u | (1ull << 63));
@@ -70,14 +78,33 @@ __device__ double tp_threshold(double rf, double cf, double mem, bool* ok) {
         return __longlong_as_double((long long)u);
     };
     auto accept = [&](double P) { return !(((P * rf) * cf) > mem); };
-    if (accept(INFINITY)) return INFINITY;
-    if (!accept(-INFINITY)) { *ok = false; return 0.0; }
     unsigned long long lo = key(-INFINITY), hi = key(INFINITY);  // accept(lo), !accept(hi)
     while (hi - lo > 1ull) {
         const unsigned long long mid = lo + (hi - lo) / 2ull;
         if (accept(unkey(mid))) lo = mid; else hi = mid;
     }
     return unkey(lo);
+}
+
+__device__ double tp_threshold(double rf, double cf, double mem, bool* ok) {
+    *ok = rf > 0.0 && rf < INFINITY && cf > 0.0 && cf < INFINITY;
+    if (!*ok) return 0.0;
+    auto accept = [&](double P) { return !(((P * rf) * cf) > mem); };
+    if (accept(INFINITY)) return INFINITY;
+    if (!accept(-INFINITY)) { *ok = false; return 0.0; }
+    double P = mem / (rf * cf);
+    if (isfinite(P)) {
+        for (int it = 0; it < 64; ++it) {
+            if (!accept(P)) {
+                P = nextafter(P, -INFINITY);
+            } else {
+                const double up = nextafter(P, INFINITY);
+                if (!accept(up)) return P;
+                P = up;
+            }
+        }
+    }
+    return tp_threshold_bisect(rf, cf, mem);
 }
 
 // one 128-thread block per group: members loaded in parallel into shared
@@ -123,8 +150,8 @@ __device__ void k1_group_block(const DevInst& I, int f) {
             shp[j + 1] = r;
         }
         ns_sh = ns;
-        if (s1 > s0) gpd::dp_fractions(I.sg_cap + s0, s1 - s0, I.g_dp + s0);
     }
+    if (threadIdx.x == 32 && s1 > s0) gpd::dp_fractions(I.sg_cap + s0, s1 - s0, I.g_dp + s0);
     __syncthreads();
     bool tp_ok = false;
     double thr = INFINITY;
@@ -164,22 +191,36 @@ __device__ void k1_group_block(const DevInst& I, int f) {
         thr_ok = __syncthreads_and(thr_ok) != 0;
     }
     if (threadIdx.x == 0) I.g_tp_ok[f] = tp_ok ? 1 : 0;
-    double sgmin[4] = {0.0, 0.0, 0.0, 0.0};
-    uint8_t sgne = 0;
-    for (int g = s0; g < s1; ++g) {
-        double sm = INFINITY;
-        for (int x = I.sg_off[g] + threadIdx.x; x < (int)I.sg_off[g + 1]; x += blockDim.x) {
-            const double mm = I.mem[I.sg_mem[x]];
-            sm = mm < sm ? mm : sm;
+    // second-level minimum memories: one warp per second-level group
+    __shared__ double sgmin_s[4];
+    {
+        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int g = s0 + w; g < s1; g += (int)(blockDim.x >> 5)) {
+            const int x0 = I.sg_off[g], x1 = I.sg_off[g + 1];
+            double sm = INFINITY;
+            for (int x = x0 + lane; x < x1; x += 32) {
+                const double mm = I.mem[I.sg_mem[x]];
+                sm = mm < sm ? mm : sm;
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+                const double o = __shfl_down_sync(0xffffffffu, sm, off);
+                sm = o < sm ? o : sm;
+            }
+            if (lane == 0) {
+                const double v = x1 > x0 ? sm : 0.0;
+                I.sg_minmem[g] = v;
+                if (g - s0 < 4) sgmin_s[g - s0] = v;
+            }
         }
-        sm = block_min128(sm, red);
-        const bool ne = I.sg_off[g + 1] > I.sg_off[g];
-        if (threadIdx.x == 0) I.sg_minmem[g] = ne ? sm : 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (g - s0 == j) { sgmin[j] = ne ? sm : 0.0; sgne |= ne ? (uint8_t)(1u << j) : (uint8_t)0; }
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
+        double sgmin[4] = {0.0, 0.0, 0.0, 0.0};
+        uint8_t sgne = 0;
+        for (int j = 0; j < 4 && j < s1 - s0; ++j) {
+            sgmin[j] = sgmin_s[j];
+            if (I.sg_off[s0 + j + 1] > I.sg_off[s0 + j]) sgne |= (uint8_t)(1u << j);
+        }
         K1Grp R;
         R.cap = I.fg_cap[f];
         R.mbw = 0.0;  // (bandwidth-dependent: phase 2 reads I.fg_minbw)
@@ -604,17 +645,17 @@ __global__ void __launch_bounds__(128) k1_phase1(DevInst I, K1Reset R) {
     pdl_trigger();  // phase 2 may be scheduled now (it waits for this grid)
     pdl_wait();     // the instance arena (k_arena_pull in the gp_replan graph)
     TL_WAITED();
-    if (b == 0) {
+    if (b == (int)gridDim.x - 1) {  // (a gateway block: the shortest role)
         if (threadIdx.x == 0) {
             *I.flags = 0u;
             if (R.err_idx) *R.err_idx = ~0ull;
         }
         for (unsigned int t = threadIdx.x; R.item_ctr && t < R.n_items; t += blockDim.x)
             R.item_ctr[t] = 0u;
-    }
-    if (b == 0)  // M = batch / micro per (b, m) index, for the per-candidate kernels
+        // M = batch / micro per (b, m) index, for the per-candidate kernels
         for (int t = threadIdx.x; t < I.nb * I.nm; t += blockDim.x)
             I.mtab[t] = (double)(I.batch[t / I.nm] / I.micro[t % I.nm]);
+    }
     if (b < 5) k1_intervals_block(I, b);
     else if (b < 5 + I.F) k1_group_block(I, b - 5);
     else {
