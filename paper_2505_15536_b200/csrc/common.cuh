@@ -168,6 +168,23 @@ __device__ unsigned long long d_binom(int n, int r) {
 }
 
 __device__ void d_unrank_perm(int k, unsigned long long r, uint8_t* perm) {
+    if (k <= 12 && r < 479001600ull) {
+        // 32-bit arithmetic (12! < 2^32) and the pool as 4-bit fields of one
+        // register (no local-memory array, no 64-bit division)
+        unsigned long long pool = 0xfedcba9876543210ull;  // field i = i
+        unsigned int f = 1, rr = (unsigned int)r;
+        for (int i = 2; i < k; ++i) f *= (unsigned int)i;     // (k-1)!
+        for (int i = 0; i < k; ++i) {
+            const unsigned int q = rr / f;
+            rr -= q * f;
+            perm[i] = (uint8_t)((pool >> (4 * q)) & 15ull);
+            // remove field q: keep fields below, shift the ones above down
+            const unsigned long long lowmask = q ? ((1ull << (4 * q)) - 1ull) : 0ull;
+            pool = (pool & lowmask) | ((pool >> 4) & ~lowmask);
+            if (k - 1 - i > 0) f /= (unsigned int)(k - 1 - i);
+        }
+        return;
+    }
     uint8_t pool[GP_MAX_STAGES];
     unsigned long long f = 1;
     for (int i = 0; i < k; ++i) { pool[i] = (uint8_t)i; if (i > 0) f *= (unsigned long long)i; }

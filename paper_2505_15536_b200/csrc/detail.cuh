@@ -37,7 +37,7 @@ __device__ void plan_detail_warp(const DevInst& I, int k, const uint8_t* o, cons
     const int n = I.n;
     const size_t N2 = (size_t)(n + 1) * (n + 1);
     const int mi = bm % I.nm;
-    const long long M = I.batch[bm / I.nm] / I.micro[mi];
+    const double Md = I.mtab[bm];  // (double)(batch / micro), K1
     const double2* T = I.stg + (size_t)mi * I.F * N2;
     const double* X = I.xt + (size_t)mi * I.F * I.F * I.nxp;
     double2 e = make_double2(0.0, 0.0);
@@ -93,7 +93,6 @@ __device__ void plan_detail_warp(const DevInst& I, int k, const uint8_t* o, cons
     else if (p[k] != n) st = GP_ERR_TOPOLOGY;
     else if (errs) st = first_err;
     else if (gbad) st = GP_ERR_TOPOLOGY;
-    const double Md = (double)M;
     for (int s = 0; s < k; ++s) {
         const double cx = __shfl_sync(0xffffffffu, e.x, s);
         const double cy = __shfl_sync(0xffffffffu, e.y, s);
@@ -122,57 +121,43 @@ __device__ void plan_detail_warp(const DevInst& I, int k, const uint8_t* o, cons
     }
 }
 
-__global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned long long NP,
-                               int nbm, const Key* result, const unsigned long long* err,
-                               const unsigned long long* __restrict__ binom, SolveOut* out) {
-    // one warp: decode the arg-min key (cut positions by a 32-wide ballot
-    // over the hockey-stick counts), then the warp plan detail
+// Decode of one arg-min key + plan detail into `out` (shared memory); one
+// warp.  Out of line so that the icache warm-up pass and the real pass run
+// the same instructions.
+__device__ __noinline__ void solve_body(const DevInst& I, int k, unsigned long long NC, int nbm,
+                                        Key key, unsigned long long e, uint32_t flags,
+                                        const unsigned long long* bsm, SolveOut* out) {
     const int lane = threadIdx.x & 31;
-    TL_START();
-    // the record is assembled in shared memory and leaves in one coalesced
-    // pass (the destination may be mapped host memory)
-    __shared__ __align__(16) SolveOut so;
-    SolveOut* const dst = out;
-    out = &so;
-    {
-        unsigned long long* z = (unsigned long long*)&so;
-        for (int q = lane; q < (int)(sizeof(SolveOut) / 8); q += 32) z[q] = 0ull;
-    }
-    // the binomial columns the decode reads, staged once (independent loads
-    // overlap) instead of one dependent global round trip per probe
-    __shared__ unsigned long long bsm[(GP_MAX_LAYERS + 1) * (GP_MAX_STAGES + 1)];
-    for (int q = lane; q < (I.n + 1) * (k + 1); q += 32) {
-        const int nn = q / (k + 1), r = q % (k + 1);
-        bsm[q] = binom[(size_t)nn * (GP_MAX_STAGES + 1) + r];
-    }
-    pdl_wait();  // the arg-min (binom is static: staged before the wait)
-    TL_WAITED();
-    const Key key = *result;
-    const unsigned long long e = *err;
-    __syncwarp();
     if (lane == 0) {
         out->key = key;
         out->err = e;
         out->k = (uint32_t)k;
         out->status = GP_OK;
-        out->flags = *I.flags;  // table flags travel back with the result
+        out->flags = flags;  // table flags travel back with the result
     }
-    auto flush = [&]() {
-        __syncwarp();
-        const unsigned long long* src = (const unsigned long long*)&so;
-        unsigned long long* d = (unsigned long long*)dst;
-        for (int q = lane; q < (int)(sizeof(SolveOut) / 8); q += 32) d[q] = src[q];
-    };
-    if (e != ~0ull || key.tie == ~0ull) { flush(); TL_STOP(50); return; }
+    if (e != ~0ull || key.tie == ~0ull) return;
     const int n = I.n;
     const unsigned long long t = key.tie;
-    const int bm = (int)(t % (unsigned long long)nbm);
-    const unsigned long long pc = t / (unsigned long long)nbm;
+    int bm;
+    unsigned long long pc;
+    if (t < (1ull << 32)) {  // 32-bit division when the key fits (every realistic space)
+        bm = (int)((unsigned)t % (unsigned)nbm);
+        pc = (unsigned)t / (unsigned)nbm;
+    } else {
+        bm = (int)(t % (unsigned long long)nbm);
+        pc = t / (unsigned long long)nbm;
+    }
     uint8_t o[GP_MAX_STAGES];
     int p[GP_MAX_STAGES + 1];
-    d_unrank_perm(k, pc / NC, o);
+    unsigned long long rem;
+    if (pc < (1ull << 32) && NC < (1ull << 32)) {
+        d_unrank_perm(k, (unsigned)pc / (unsigned)NC, o);
+        rem = (unsigned)pc % (unsigned)NC;
+    } else {
+        d_unrank_perm(k, pc / NC, o);
+        rem = pc % NC;
+    }
     p[0] = 0;
-    unsigned long long rem = pc % NC;
     int prev = 0;
     auto C = [&](int nn, int r) -> unsigned long long {
         return (r < 0 || nn < 0) ? 0ull : bsm[nn * (k + 1) + r];
@@ -181,12 +166,13 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
         const int r = k - 1 - j, lo = prev + 1;
         const unsigned long long tot = C(n - lo, r + 1), thr = tot - rem;
         int qsel = -1;
-        for (int base = lo; qsel < 0; base += 32) {
+        for (int base = lo; qsel < 0 && base <= n - 1 - r; base += 32) {
             const int qq = base + lane;
             const bool ok = qq <= n - 1 - r && C(n - qq - 1, r + 1) < thr;
             const unsigned m = __ballot_sync(0xffffffffu, ok);
             if (m) qsel = base + __ffs(m) - 1;
         }
+        if (qsel < 0) qsel = n - 1 - r;  // (unreachable for a valid key)
         rem -= tot - C(n - qsel, r + 1);
         p[j] = qsel;
         prev = qsel;
@@ -200,8 +186,58 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
         }
     }
     plan_detail_warp(I, k, o, p, bm, &out->info, &out->status);
-    flush();
+}
+
+__global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned long long NP,
+                               int nbm, const Key* result, const unsigned long long* err,
+                               const unsigned long long* __restrict__ binom, SolveOut* out,
+                               int warm) {
+    // one warp: decode the arg-min key (cut positions by a 32-wide ballot
+    // over the hockey-stick counts), then the warp plan detail
+    (void)NP;
+    const int lane = threadIdx.x & 31;
+    TL_START();
+    pdl_trigger();
+    // the record is assembled in shared memory and leaves in one coalesced
+    // pass (the destination may be mapped host memory)
+    __shared__ __align__(16) SolveOut so;
+    // the binomial columns the decode reads, staged once (independent loads
+    // overlap) instead of one dependent global round trip per probe
+    __shared__ unsigned long long bsm[(GP_MAX_LAYERS + 1) * (GP_MAX_STAGES + 1)];
+    for (int nn = lane; nn <= I.n; nn += 32)
+        for (int r = 0; r <= k; ++r) bsm[nn * (k + 1) + r] = binom[(size_t)nn * (GP_MAX_STAGES + 1) + r];
+    __syncwarp();
+    // inside the gp_replan graph this kernel is scheduled while the arg-min
+    // still runs: one pass over candidate rank 0 (valid for every instance;
+    // the tables it reads are this instance's) pulls the code of the decode
+    // and detail into the instruction cache before the real key exists
+    if (warm) solve_body(I, k, NC, nbm, Key{0.0, 0ull}, ~0ull, 0u, bsm, &so);
+    {
+        __syncwarp();
+        unsigned long long* z = (unsigned long long*)&so;
+        for (int q = lane; q < (int)(sizeof(SolveOut) / 8); q += 32) z[q] = 0ull;
+        __syncwarp();
+    }
+    pdl_wait();  // the arg-min (binom is static: staged before the wait)
+    TL_WAITED();
+#if defined(GP_TIMELINE)
+    const unsigned long long td0 = tl_now();
+#endif
+    solve_body(I, k, NC, nbm, *result, *err, *I.flags, bsm, &so);
+#if defined(GP_TIMELINE)
+    const unsigned long long td1 = tl_now();
+#endif
+    __syncwarp();
+    const unsigned long long* src = (const unsigned long long*)&so;
+    unsigned long long* d = (unsigned long long*)out;
+    for (int q = lane; q < (int)(sizeof(SolveOut) / 8); q += 32) d[q] = src[q];
     TL_STOP(50);
+#if defined(GP_TIMELINE)
+    if (lane == 0) {  // sub-phases: real pass start / detail done / exit
+        unsigned int i2 = atomicAdd(&g_tl_n, 1u);
+        if (i2 < GP_TL_CAP) g_tl[i2] = TlRec{td0, td1, tl_now(), 51u, 0u, 0u, 0u};
+    }
+#endif
 }
 
 

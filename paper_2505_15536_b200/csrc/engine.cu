@@ -1095,7 +1095,7 @@ static int enqueue_solve(gp_ctx* c, uint64_t lo, uint64_t hi) {
     SolveOut* dst = c->pdl ? c->d_hsolve : c->dsolve.p;
     CUDA_TRY(launch_k(k_solve_detail, 1, 32, 0, c->stream, c->pdl, I, G.k, G.NC, G.NP, G.nbm,
                       (const Key*)c->result.p, (const unsigned long long*)c->err_idx.p,
-                      (const unsigned long long*)c->binom.p, dst));
+                      (const unsigned long long*)c->binom.p, dst, c->pdl ? 1 : 0));
     if (c->pdl) return GP_OK;
     CUDA_TRY(cudaMemcpyAsync(c->h_solve, c->dsolve.p, sizeof(SolveOut), cudaMemcpyDeviceToHost,
                              c->stream));

@@ -16,7 +16,7 @@ from paper_2505_15536_b200.layout import PackedInstance  # noqa: E402
 
 REC = np.dtype([("t0", "<u8"), ("tw", "<u8"), ("t1", "<u8"), ("kid", "<u4"), ("blk", "<u4"),
                 ("smid", "<u4"), ("pad", "<u4")])
-NAMES = {10: "k1p1 intervals", 11: "k1p1 groups", 12: "k1p1 gateways", 20: "k1p2 stages",
+NAMES = {51: "detail phases", 5: "arena_pull", 10: "k1p1 intervals", 11: "k1p1 groups", 12: "k1p1 gateways", 20: "k1p2 stages",
          21: "k1p2 boundary", 30: "k3_sweep", 40: "fixup", 50: "solve_detail"}
 
 
