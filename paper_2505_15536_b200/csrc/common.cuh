@@ -239,6 +239,8 @@ struct ArgminScratch {
     Key* result;              // [1]
     int* err;                 // [1] first error (index<<4|code) low 32 bits unused
     unsigned long long* err_idx;
+    unsigned int* rearm = nullptr;  // [nrearm] work counters the group's last CTA zeroes
+    unsigned int nrearm = 0;
 };
 
 // CTA-wide reduction of per-thread keys, then last-block grid reduction.
@@ -284,6 +286,10 @@ __device__ void block_argmin_finish(Key mine, const ArgminScratch& S, unsigned i
         *S.result = r;
         *S.counter = 0;  // re-arm for the next launch
     }
+    // every CTA of the group has finished its last atomicAdd on the work
+    // counters before it reached the group counter: zero them for the next
+    // launch (saves a memset node per launch)
+    for (unsigned int i = threadIdx.x; i < S.nrearm; i += blockDim.x) S.rearm[i] = 0u;
 }
 
 __device__ __forceinline__ void block_argmin_finish(Key mine, const ArgminScratch& S) {

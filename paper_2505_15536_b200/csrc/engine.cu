@@ -154,6 +154,11 @@ struct gp_ctx {
     double host_us[4] = {0, 0, 0, 0};  // gp_replan: arena fill, launch, wait, finish
     size_t arena_bytes = 0;
     int force_mode = -1;  // -1 auto; 0/1/2 fast-path variant; 3 generic kernel
+    // device state known from earlier launches on the stream (memsets skipped):
+    // item counters [0, ctr_armed) are zero (k3_sweep re-arms the ones it
+    // used); err_idx holds ~0 (no launch since its reset could have written it)
+    size_t ctr_armed = 0;
+    bool err_clean = false;
     std::vector<uint32_t> h_fg_sg_count;  // subgroups per group (explicit plans)
     DBuf<unsigned long long> binom;
     DBuf<unsigned int> item_ctr;
@@ -346,6 +351,7 @@ static int known_flags(gp_ctx* c) {
 }
 
 int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
+    if (c) { c->ctr_armed = 0; c->err_clean = false; }  // launches below skip neither reset
     if (!c || !in) return fail(GP_ERR_INPUT, "null argument");
     if (in->n_layers < 1 || in->n_layers > GP_MAX_LAYERS)
         return fail(GP_ERR_INPUT, "n_layers %u outside [1, %d]", in->n_layers, GP_MAX_LAYERS);
@@ -676,6 +682,8 @@ static cudaError_t launch_sweep_kernel(SwFn kern, unsigned grid, size_t smem, cu
     if (const char* e = getenv("GP_K3_CLUSTER")) cs = atoi(e) > 0 ? atoi(e) : 1;
     if (cs > 1 && (G.cpi % cs != 0)) cs = 1;
     G.csize = cs;
+    G.interleave = 1;
+    if (const char* e = getenv("GP_K3_BLOCKMAP")) G.interleave = atoi(e) != 0;
     if (cs == 1) return launch_k(kern, grid, K3S_THREADS, smem, s, pdl, I, G, S, binom, flags);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
@@ -769,9 +777,14 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     G.s_tpk = G.s_tcol = G.s_xt = 0;
     G.gsteps = 1;
     while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
+    if (c->item_ctr.cap < items || !c->item_ctr.p) c->ctr_armed = 0;  // (re)allocation
     CUDA_TRY(c->item_ctr.ensure(items));
-    if (!c->pdl)  // (the gp_replan graph resets the counters in K1 phase 1)
+    // (the gp_replan graph resets the counters in K1 phase 1; the sweep
+    // itself re-arms them at exit)
+    if (!c->pdl && items > c->ctr_armed) {
         CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
+        c->ctr_armed = items;
+    }
     G.item_ctr = c->item_ctr.p;
     CUDA_TRY(c->blk.ensure(grid));
     ArgminScratch S;
@@ -833,8 +846,9 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     c->last_lo = lo;
     c->last_hi = hi;
     ArgminScratch S;
-    if (!c->pdl)  // (the gp_replan graph resets it in K1 phase 1)
+    if (!c->pdl && !c->err_clean)  // (the gp_replan graph resets it in K1 phase 1)
         CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));  // = ~0
+    c->err_clean = false;  // every branch below but the plain sweep may write it
     DevInst I = c->view();
     // table flags (error entries, overflow) force the status-tracking kernel;
     // while the async read-back is pending, launch the fast kernel with a
@@ -864,7 +878,11 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
         c->last_generic = false;
         CUDA_TRY(c->blk.ensure(1));
         int st = launch_sweep(c, G, 0, (unsigned long long)c->nm * G.NP, mode, dflags);
-        if (st != GP_OK || !pending) return st;
+        if (st != GP_OK) return st;
+        if (!pending) {
+            c->err_clean = !c->pdl;  // the sweep never writes err_idx
+            return st;
+        }
         return launch_fixup(c, G);
     }
     if (hi == lo) {
@@ -903,6 +921,7 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
         grid = items * cpi;
         CUDA_TRY(c->item_ctr.ensure(items));
         CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
+        c->ctr_armed = 0;  // k3_argmin leaves its counters non-zero
         G.item_ctr = c->item_ctr.p;
         int ts = ensure_tiles(c);
         if (ts != GP_OK) return ts;
@@ -991,6 +1010,7 @@ int gp_argmin_range(gp_ctx* c, uint64_t lo, uint64_t hi, gp_best* out) {
 }
 
 int gp_argmin_bnb_async(gp_ctx* c) {
+    if (c) { c->ctr_armed = 0; c->err_clean = false; }  // launches below skip neither reset
     if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
     const int k = c->F, n = c->n;
     uint64_t total;
@@ -1032,6 +1052,7 @@ int gp_argmin_bnb_async(gp_ctx* c) {
 }
 
 int gp_argmin_items_async(gp_ctx* c, uint64_t item_lo, uint64_t item_hi) {
+    if (c) { c->ctr_armed = 0; c->err_clean = false; }  // launches below skip neither reset
     if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
     const int k = c->F;
     uint64_t total;
@@ -1164,6 +1185,7 @@ static inline double now_us() {
 }
 
 int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* info) {
+    if (c) { c->ctr_armed = 0; c->err_clean = false; }  // launches below skip neither reset
     if (!c || !in || !best) return fail(GP_ERR_INPUT, "null argument");
     const double h0 = c->diag_timing ? now_us() : 0.0;
     unsigned long long key[10];
@@ -1660,6 +1682,7 @@ int gp_sim_1f1b(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t iterat
 
 int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_best* out,
                         int32_t* status) {
+    if (c) { c->ctr_armed = 0; c->err_clean = false; }  // launches below skip neither reset
     if (!c || !c->loaded || !bandwidth || !out || !status) return fail(GP_ERR_INPUT, "bad arguments");
     if (n_snap == 0) return GP_OK;
     CUDA_TRY(cudaSetDevice(c->device));

@@ -253,6 +253,7 @@ struct SweepGeom {
     unsigned long long s_tpk, s_tcol, s_xt;  // per-snapshot strides (elements)
     const unsigned long long* bnk;  // C(nn, r), nn <= n, r <= k: contiguous [n+1][k+1]
     int csize;                      // thread-block cluster size (CTAs of one item), 1 = none
+    int interleave;                 // CTA -> item map: 1 = item-minor (b % items), 0 = item-major
 };
 
 #if defined(K3_PROFILE)
@@ -277,7 +278,13 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     const int KB = k + 1;
     const unsigned int per_snap = G.items * (unsigned int)G.cpi;
     const unsigned int snap = blockIdx.x / per_snap, local = blockIdx.x % per_snap;
-    const unsigned long long islot = local / G.cpi;
+    // Item-minor map: CTAs are dispatched in blockIdx order, one per SM first,
+    // and the SM's warp scheduler favours its older CTA, so an item-major map
+    // (an item's CTAs adjacent) gives whole items only first-wave or only
+    // second-wave CTAs and they finish ~15 % apart.  Item-minor spreads each
+    // item's CTAs over both waves.  A cluster needs its item's CTAs adjacent.
+    const unsigned long long islot =
+        (G.interleave && G.csize == 1) ? local % G.items : local / G.cpi;
     const unsigned long long item = G.item0 + islot;
     const int mi = (int)(item / G.NP);
     const unsigned long long perm_rank = item % G.NP;
@@ -486,6 +493,8 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     Ss.blk = S.blk + (size_t)snap * per_snap;
     Ss.counter = S.counter + snap;
     Ss.result = S.result + snap;
+    Ss.rearm = ctr - islot;  // this snapshot's item counters
+    Ss.nrearm = G.items;
 #if defined(K3_PROFILE)
     unsigned long long t2p; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2p));
 #endif
