@@ -44,7 +44,12 @@ enum : uint8_t { SC_OK = 0, SC_INFEASIBLE = 1, SC_DEGENERATE = 4, SC_TOPOLOGY = 
 enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 4 };
 #define K3_THREADS 256
 #define K3_TILE 256
+#ifndef K3_SEG
 #define K3_SEG 32
+#endif
+#ifndef K3_QPAIR
+#define K3_QPAIR 1  // k3_sweep: two q steps per iteration where the warp's runs allow
+#endif
 #ifndef K3S_THREADS
 #define K3S_THREADS 256
 #endif

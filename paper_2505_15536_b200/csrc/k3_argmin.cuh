@@ -435,11 +435,13 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
             }
             fill2 = fill + (e1.x + x1);
         }
-        int lmax = len;
+        int lmax = len, lmin = len;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             int o = __shfl_xor_sync(0xffffffffu, lmax, off);
             lmax = o > lmax ? o : lmax;
+            o = __shfl_xor_sync(0xffffffffu, lmin, off);
+            lmin = o < lmin ? o : lmin;
         }
         // walk q: per-run minimum with strict < (ranks increase with q, and
         // with the batch index inside one q), merged into the lane's best
@@ -470,7 +472,21 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
                 if (bi == 0 || c < cmin) { cmin = c; bmin = bi; }
             }
         };
-        for (int i = 0; i < lmax; ++i) {
+        // steps every lane of the warp has (runs are sorted by length, so
+        // usually all of them): two independent q evaluations per iteration
+        // (ILP 2 for the fixed-latency FP64 chains), merged in q order
+        int i0 = 0;
+#if K3_QPAIR
+        for (; i0 + 1 < lmin; i0 += 2) {
+            double c0, c1;
+            int b0, b1;
+            eval_q(i0, c0, b0);
+            eval_q(i0 + 1, c1, b1);
+            if (run_i < 0 || c0 < run_c) { run_c = c0; run_i = i0; run_b = b0; }
+            if (c1 < run_c) { run_c = c1; run_i = i0 + 1; run_b = b1; }
+        }
+#endif
+        for (int i = i0; i < lmax; ++i) {
             if (i < len) {
                 double cmin; int bmin;
                 eval_q(i, cmin, bmin);
