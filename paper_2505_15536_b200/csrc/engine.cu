@@ -2033,7 +2033,8 @@ static int group_launch(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_
     const size_t o_pt = 0, o_bw = o_pt + al(SB * DD * 8), o_pc = o_bw + al(bandwidth ? SB * DD * 8 : 8);
     const size_t o_u16 = o_pc + al((size_t)D * 8), o_cnt = o_u16 + al((size_t)SB * D * 2 * 2);
     const size_t o_dbl = o_cnt + al((size_t)SB * 2 * 4), o_fix = o_dbl + al((size_t)SB * D * 4 * 8);
-    const size_t o_scr = o_fix + al((size_t)D * 2);
+    const size_t o_nsf = o_fix + al((size_t)D * 2), o_stg = o_nsf + al((size_t)SB * D * 4);
+    const size_t o_scr = o_stg + al((size_t)SB * D * 8);
     const size_t total = o_scr + SB * per_scr;
     CUDA_TRY(c->g_buf.ensure(total));
     uint8_t* b = c->g_buf.p;
@@ -2060,13 +2061,30 @@ static int group_launch(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_
         double* d_dbl = reinterpret_cast<double*>(b + o_dbl);
         double *d_fi = d_dbl, *d_fc = d_fi + (size_t)SB * D, *d_fb = d_fc + (size_t)SB * D,
                *d_sc = d_fb + (size_t)SB * D;
-        k7_group<<<nb, K7_THREADS, smem, s>>>(
-            (int)D, reinterpret_cast<const double*>(b + o_pt),
-            bandwidth ? reinterpret_cast<const double*>(b + o_bw) : nullptr, (long long)DD,
-            (long long)DD, reinterpret_cast<const double*>(b + o_pc), threshold_net,
-            threshold_compute, b + o_scr, per_scr, smem_mode,
-            fixed_fg ? reinterpret_cast<const uint16_t*>(b + o_fix) : nullptr, (int)fixed_nf, d_fg,
-            d_sg, d_nf, d_ns, d_fi, d_fc, d_fb, d_sc);
+        uint32_t* d_nsf = reinterpret_cast<uint32_t*>(b + o_nsf);
+        double* d_stg = reinterpret_cast<double*>(b + o_stg);
+        auto launch = [&](unsigned grid, int phase) {
+            k7_group<<<grid, K7_THREADS, smem, s>>>(
+                (int)D, reinterpret_cast<const double*>(b + o_pt),
+                bandwidth ? reinterpret_cast<const double*>(b + o_bw) : nullptr, (long long)DD,
+                (long long)DD, reinterpret_cast<const double*>(b + o_pc), threshold_net,
+                threshold_compute, b + o_scr, per_scr, smem_mode,
+                fixed_fg ? reinterpret_cast<const uint16_t*>(b + o_fix) : nullptr, (int)fixed_nf,
+                d_fg, d_sg, d_nf, d_ns, d_fi, d_fc, d_fb, d_sc, phase, d_nsf, d_stg);
+        };
+        // pair tables in shared memory: the FGs' second levels run as
+        // separate CTAs (phase 2) instead of one after another in the
+        // snapshot's CTA; GP_K7_SPLIT=0 keeps the single-kernel form
+        bool split = (smem_mode & 1) != 0;
+        if (const char* e = getenv("GP_K7_SPLIT")) split = split && atoi(e) != 0;
+        if (split) {
+            launch(nb, 1);
+            launch(nb * D, 2);
+            k7_sg_finish<<<(nb + 127) / 128, 128, 0, s>>>((int)D, (int)nb, d_nf, d_fg, d_nsf, d_stg,
+                                                          d_sc, d_ns);
+        } else {
+            launch(nb, 0);
+        }
         CUDA_TRY(cudaGetLastError());
         const size_t o = (size_t)s0 * D;
         CUDA_TRY(cudaMemcpyAsync(fg_of + o, d_fg, (size_t)nb * D * 2, cudaMemcpyDeviceToHost, s));

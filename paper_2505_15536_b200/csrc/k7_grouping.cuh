@@ -367,12 +367,20 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
          double thr_comp, uint8_t* __restrict__ scratch, size_t scratch_per, int smem_mode,
          const uint16_t* __restrict__ fixed_fg, int fixed_nf, uint16_t* fg_of_all,
          uint16_t* sg_of_all, uint32_t* n_fg, uint32_t* n_sg, double* fg_intra_all,
-         double* fg_cap_all, double* fg_minbw_all, double* sg_cap_all) {
+         double* fg_cap_all, double* fg_minbw_all, double* sg_cap_all, int phase,
+         uint32_t* nsg_f_all, double* sg_stage_all) {
+    // phase 0: one CTA per snapshot runs both levels (the FGs' second levels
+    // one after another); phase 1: first level only (fg_of, n_fg); phase 2:
+    // CTA (snapshot, f) runs FG f's statistics and second level, its SG
+    // capacities staged at the FG's first member slot (k7_sg_finish packs
+    // them).  Phases 1 + 2 need the pair tables in shared memory.
     extern __shared__ __align__(16) uint8_t k7_smem[];
     __shared__ int s_ab[4];
     __shared__ double s_red[K7_THREADS / 32];
     __shared__ int s_ia[2 * (K7_THREADS / 32)];
-    const int snap = blockIdx.x, tid = threadIdx.x;
+    const int snap = phase == 2 ? (int)(blockIdx.x / (unsigned)D) : (int)blockIdx.x, tid = threadIdx.x;
+    const int f_only = phase == 2 ? (int)(blockIdx.x % (unsigned)D) : -1;
+    if (phase == 2 && f_only >= (int)n_fg[snap]) return;
     const double* pt = pt_all + (size_t)snap * pt_stride;
     const double* bw = bw_all ? bw_all + (size_t)snap * bw_stride : nullptr;
     // smem_mode bit0: pair tables in shared memory (small D); bit1: p_t too
@@ -414,26 +422,38 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
     // first level: agglomerated, or given (a fixed partition, e.g. the C2
     // region-grouping sweep; indices already in sorted-member-tuple order)
     int nf;
-    if (fixed_fg) {
+    if (phase == 2) {
+        for (int d = tid; d < D; d += blockDim.x) gof[d] = fg_of[d];
+        __syncthreads();
+        nf = (int)n_fg[snap];
+    } else if (fixed_fg) {
         for (int d = tid; d < D; d += blockDim.x) gof[d] = fixed_fg[d];
         __syncthreads();
         nf = fixed_nf;
     } else {
         nf = k7_agglomerate<false>(1, D, items, pt, pc, D, thr_net, g, sh, gof, s_ab, s_red, s_ia);
     }
-    for (int d = tid; d < D; d += blockDim.x) fg_of[d] = gof[d];
+    if (phase != 2)
+        for (int d = tid; d < D; d += blockDim.x) fg_of[d] = gof[d];
     __syncthreads();
+    if (phase == 1) {
+        if (tid == 0) n_fg[snap] = (uint32_t)nf;
+        return;
+    }
 #if defined(K7_PROFILE)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
 #endif
     int sg_base = 0;
-    for (int f = 0; f < nf; ++f) {
+    for (int f = f_only < 0 ? 0 : f_only; f < (f_only < 0 ? nf : f_only + 1); ++f) {
         // members of FG f in rank order
         if (tid == 0) {
-            int k = 0;
-            for (int d = 0; d < D; ++d)
+            int k = 0, before = 0;
+            for (int d = 0; d < D; ++d) {
                 if (gof[d] == f) items[k++] = (uint16_t)d;
+                before += gof[d] < f;
+            }
             s_ab[0] = k;
+            if (f_only >= 0) sg_base = before;  // staging slot: FG f's first member
         }
         __syncthreads();
         const int nm = s_ab[0];
@@ -497,12 +517,15 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
                         const double v = pc[items[i]];
                         if (first) { s.start(v); first = false; } else s.add(v);
                     }
-                sg_cap[sg_base + q] = s.value();
+                if (f_only >= 0) sg_stage_all[(size_t)snap * D + sg_base + q] = s.value();
+                else sg_cap[sg_base + q] = s.value();
             }
+            if (f_only >= 0) nsg_f_all[(size_t)snap * D + f] = (uint32_t)ns;
         }
         sg_base += ns;
         __syncthreads();
     }
+    if (f_only >= 0) return;
     if (tid == 0) {
         n_fg[snap] = (uint32_t)nf;
         n_sg[snap] = (uint32_t)sg_base;
@@ -513,4 +536,27 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
 #endif
 }
 
-
+// After phase 2: per snapshot, SG capacities in FG order (sg_base = running
+// count of SGs) and n_sg.  One thread per snapshot (<= D FGs).
+__global__ void k7_sg_finish(int D, int n_snap, const uint32_t* __restrict__ n_fg,
+                             const uint16_t* __restrict__ fg_of_all,
+                             const uint32_t* __restrict__ nsg_f_all,
+                             const double* __restrict__ sg_stage_all, double* sg_cap_all,
+                             uint32_t* n_sg) {
+    const int snap = blockIdx.x * blockDim.x + threadIdx.x;
+    if (snap >= n_snap) return;
+    const uint16_t* fg_of = fg_of_all + (size_t)snap * D;
+    const uint32_t* nsg = nsg_f_all + (size_t)snap * D;
+    const double* st = sg_stage_all + (size_t)snap * D;
+    double* out = sg_cap_all + (size_t)snap * D;
+    const int nf = (int)n_fg[snap];
+    int base = 0, first = 0;  // first: member slots of the FGs before f
+    for (int f = 0; f < nf; ++f) {
+        int cnt = 0;
+        for (int d = 0; d < D; ++d) cnt += fg_of[d] == f;
+        for (int q = 0; q < (int)nsg[f]; ++q) out[base + q] = st[first + q];
+        base += (int)nsg[f];
+        first += cnt;
+    }
+    n_sg[snap] = (uint32_t)base;
+}
