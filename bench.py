@@ -49,9 +49,9 @@ ALG_OPS_PER_CAND_C4 = 39
 # inner loop, profiles/r1_k3_sweep.md): 27 per q-step for 2 candidates plus
 # the per-run prefix fold, amortised.
 K3_ISSUED_FP64_PER_CAND = 13.5
-# dram__bytes_read.sum + write of one K3 launch after an L2 flush (ncu,
-# profiles/r1_k3_sweep_ncu_raw.csv)
-K3_DRAM_BYTES = 725504
+# dram__bytes_read.sum + write of one K3 launch after an L2 flush (ncu launch
+# list of this bench, profiles/r1e_launches_bench.csv: 704,256 B read, 0 written)
+K3_DRAM_BYTES = 704256
 
 
 def parse():
