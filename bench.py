@@ -46,9 +46,8 @@ sys.path.insert(0, ROOT)
 # three adds, max) + 5 per boundary (c+x, fill+, x-c', max0, res+).
 ALG_OPS_PER_CAND_C4 = 39
 # FP64 instructions the K3 sweep actually issues per candidate (SASS of the
-# inner loop, profiles/r1_k3_sweep.md): 27 per q-step for 2 candidates plus
-# the per-run prefix fold, amortised.
-K3_ISSUED_FP64_PER_CAND = 13.5
+# paired-q inner loop: 56 DADD/DMUL/DSETP per 2 q steps x 2 batch sizes).
+K3_ISSUED_FP64_PER_CAND = 14
 # dram__bytes_read.sum + write of one K3 launch after an L2 flush (ncu launch
 # list of this bench, profiles/r1e_launches_bench.csv: 704,256 B read, 0 written)
 K3_DRAM_BYTES = 704256
