@@ -581,6 +581,8 @@ int gp_set_bandwidth(gp_ctx* c, const double* bandwidth) {
     return run_tables(c, false);
 }
 
+static int kernel_slots(gp_ctx* c, const void* kern, int threads, size_t smem, int* per_sm);
+
 int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_order,
                          const uint8_t* d_counts, const uint8_t* d_bm, double* d_cost,
                          uint8_t* d_status) {
@@ -589,6 +591,33 @@ int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_ord
     if (n == 0) return GP_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     DevInst I = c->view();
+    // large batches: persistent kernel with the stage codes in shared memory
+    // (GP_K2_SC=0 disables); small ones (search_plan beams): one thread each
+    const size_t sc_bytes = (((size_t)c->F * (c->n + 1) * (c->n + 1)) + 15) & ~(size_t)15;
+    bool sc = n >= (1u << 16) && k >= 2 && k <= 6 && sc_bytes <= (96u << 10) &&
+              ((k != 4) || (((uintptr_t)d_order | (uintptr_t)d_counts) & 3u) == 0);
+    if (const char* e = getenv("GP_K2_SC")) sc = sc && atoi(e) != 0;
+    if (sc) {
+        typedef void (*K2Fn)(DevInst, long long, const uint8_t*, const uint8_t*, const uint8_t*,
+                             double*, uint8_t*);
+        static const K2Fn tab[5] = {k2_eval_batch_sc<2>, k2_eval_batch_sc<3>, k2_eval_batch_sc<4>,
+                                    k2_eval_batch_sc<5>, k2_eval_batch_sc<6>};
+        // k = 4 (and < 2^32 candidates): the warp-compacted variant
+        bool q4 = k == 4 && n < (1ull << 32);
+        if (const char* e = getenv("GP_K2_Q4")) q4 = q4 && atoi(e) != 0;
+        const K2Fn kern = q4 ? k2_eval_batch_q4 : tab[k - 2];
+        const size_t smem_k2 = sc_bytes + (q4 ? (K2Q_THREADS / 32) * 64 * sizeof(uint4) : 0);
+        int per_sm = 0;
+        { int st_ = kernel_slots(c, (const void*)kern, 256, smem_k2, &per_sm);
+          if (st_ != GP_OK) return st_; }
+        unsigned long long grid = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
+        const unsigned long long need = (n + 255) / 256;
+        if (grid > need) grid = need;
+        kern<<<(unsigned)grid, 256, smem_k2, c->stream>>>(I, (long long)n, d_order, d_counts, d_bm,
+                                                          d_cost, d_status);
+        CUDA_TRY(cudaGetLastError());
+        return GP_OK;
+    }
     unsigned blocks = (unsigned)((n + 255) / 256);
     k2_eval_batch<<<blocks, 256, 0, c->stream>>>(I, (int)k, (long long)n, d_order, d_counts, d_bm,
                                                  d_cost, d_status);

@@ -118,3 +118,210 @@ __global__ void k2_eval_batch(DevInst I, int k, long long ncand, const uint8_t* 
     status[i] = (uint8_t)r.status;
 }
 
+
+// ---- K2 for large batches: stage codes in shared memory ---------------------
+// Persistent grid-stride variant for batches of many candidates on tables
+// without error entries.  Every CTA copies the stage-code table scode[f][a][b]
+// (F * (n+1)^2 bytes, 26 KB at C4) into shared memory once; a candidate with a
+// memory-infeasible stage (SC_INFEASIBLE, whose stage-table entry is +inf by
+// construction, so its cost is exactly +inf: no inf - inf can arise) is
+// decided from shared memory, and only the others gather their k stage entries
+// and k-1 boundary values from L2 (84 % of random C4 candidates are
+// infeasible).  k = 4 reads order and counts as one 32-bit word each.
+#ifndef K2_U
+#define K2_U 2
+#endif
+template <int K>
+__global__ void __launch_bounds__(256) k2_eval_batch_sc(DevInst I, long long ncand,
+                                                        const uint8_t* __restrict__ order,
+                                                        const uint8_t* __restrict__ counts,
+                                                        const uint8_t* __restrict__ bm,
+                                                        double* __restrict__ cost,
+                                                        uint8_t* __restrict__ status) {
+    extern __shared__ __align__(16) uint8_t sc_s[];
+    const int n = I.n;
+    const int N2 = (n + 1) * (n + 1);
+    const int nbytes = I.F * N2;
+    {
+        int done = 0;
+        if ((reinterpret_cast<uintptr_t>(I.scode) & 15u) == 0) {
+            const uint4* src = reinterpret_cast<const uint4*>(I.scode);
+            uint4* dst = reinterpret_cast<uint4*>(sc_s);
+            for (int i = threadIdx.x; i < nbytes / 16; i += blockDim.x) dst[i] = __ldg(&src[i]);
+            done = nbytes & ~15;
+        }
+        for (int i = done + threadIdx.x; i < nbytes; i += blockDim.x) sc_s[i] = __ldg(&I.scode[i]);
+    }
+    __syncthreads();
+    const bool fast_tables = *I.flags == 0u;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // K2_U candidates per thread and iteration: their input words are loaded
+    // before any of them is evaluated (memory-level parallelism)
+    for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < ncand;
+         i0 += stride * K2_U) {
+        uint32_t ow[K2_U], cw[K2_U];
+        int bv[K2_U];
+#pragma unroll
+        for (int u = 0; u < K2_U; ++u) {
+            const long long i = i0 + u * stride;
+            ow[u] = cw[u] = 0u;
+            bv[u] = 0;
+            if (i < ncand) {
+                if (K == 4) {
+                    ow[u] = __ldg(reinterpret_cast<const uint32_t*>(order) + i);
+                    cw[u] = __ldg(reinterpret_cast<const uint32_t*>(counts) + i);
+                }
+                bv[u] = __ldg(&bm[i]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < K2_U; ++u) {
+            const long long i = i0 + u * stride;
+            if (i >= ncand) break;
+            uint8_t o[K];
+            int p[K + 1];
+            p[0] = 0;
+            int st = GP_OK;
+            unsigned seen = 0;
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                int c;
+                if (K == 4) {
+                    o[s] = (uint8_t)(ow[u] >> (8 * s));
+                    c = (int)((cw[u] >> (8 * s)) & 0xffu);
+                } else {
+                    o[s] = __ldg(&order[i * K + s]);
+                    c = __ldg(&counts[i * K + s]);
+                }
+                if (o[s] >= I.F || (seen >> o[s]) & 1u || c == 0) st = GP_ERR_INPUT;
+                seen |= 1u << (o[s] & 31);
+                p[s + 1] = p[s] + c;
+            }
+            const int b = bv[u];
+            if (b >= I.nb * I.nm || p[K] > n) st = GP_ERR_INPUT;
+            if (st != GP_OK) { cost[i] = NAN; status[i] = (uint8_t)st; continue; }
+            const int mi = b % I.nm;
+            if (fast_tables && p[K] == n) {
+                bool inf = false;
+#pragma unroll
+                for (int s = 0; s < K; ++s)
+                    inf |= sc_s[o[s] * N2 + tri_idx(n, p[s], p[s + 1])] == SC_INFEASIBLE;
+                double c = INFINITY;
+                if (!inf) c = eval_fast<K>(I, o, p, mi, __ldg(&I.mtab[b]));
+                cost[i] = c;
+                status[i] = GP_OK;
+                continue;
+            }
+            EvalOut r = eval_tables(I, K, o, p, mi, I.batch[b / I.nm] / I.micro[mi]);
+            cost[i] = r.status == GP_OK ? r.cost : NAN;
+            status[i] = (uint8_t)r.status;
+        }
+    }
+}
+
+// ---- K2, k = 4, large batches: warp-compacted evaluation -------------------
+// As k2_eval_batch_sc, but the candidates that need the stage-table gathers
+// (feasible ones, ~16 % of random C4 candidates) are queued per warp in
+// shared memory and evaluated 32 at a time, so eval_fast runs with every lane
+// busy instead of once per warp under a mostly-idle mask.
+#define K2Q_THREADS 256
+__global__ void __launch_bounds__(K2Q_THREADS) k2_eval_batch_q4(DevInst I, long long ncand,
+                                                                const uint8_t* __restrict__ order,
+                                                                const uint8_t* __restrict__ counts,
+                                                                const uint8_t* __restrict__ bm,
+                                                                double* __restrict__ cost,
+                                                                uint8_t* __restrict__ status) {
+    extern __shared__ __align__(16) uint8_t q4_s[];
+    uint4* queue = reinterpret_cast<uint4*>(q4_s);  // [warps][64] {index, order, counts, bm}
+    uint8_t* sc_s = q4_s + (K2Q_THREADS / 32) * 64 * sizeof(uint4);
+    const int n = I.n;
+    const int N2 = (n + 1) * (n + 1);
+    const int nbytes = I.F * N2;
+    {
+        int done = 0;
+        if ((reinterpret_cast<uintptr_t>(I.scode) & 15u) == 0) {
+            const uint4* src = reinterpret_cast<const uint4*>(I.scode);
+            uint4* dst = reinterpret_cast<uint4*>(sc_s);
+            for (int i = threadIdx.x; i < nbytes / 16; i += blockDim.x) dst[i] = __ldg(&src[i]);
+            done = nbytes & ~15;
+        }
+        for (int i = done + threadIdx.x; i < nbytes; i += blockDim.x) sc_s[i] = __ldg(&I.scode[i]);
+    }
+    __syncthreads();
+    const bool fast_tables = *I.flags == 0u;
+    const int lane = threadIdx.x & 31;
+    uint4* wq = queue + (threadIdx.x >> 5) * 64;
+    const unsigned lt = (1u << lane) - 1u;
+    auto decode = [&](uint32_t ow, uint32_t cw, uint8_t* o, int* p) {
+        p[0] = 0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            o[s] = (uint8_t)(ow >> (8 * s));
+            p[s + 1] = p[s] + (int)((cw >> (8 * s)) & 0xffu);
+        }
+    };
+    auto eval_entry = [&](const uint4 e) {
+        uint8_t o[4];
+        int p[5];
+        decode(e.y, e.z, o, p);
+        const int b = (int)e.w;
+        cost[e.x] = eval_fast<4>(I, o, p, b % I.nm, __ldg(&I.mtab[b]));
+    };
+    int q = 0;  // warp-uniform queue length
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < ncand;
+         base += stride) {
+        const long long i = base + lane;
+        const bool valid = i < ncand;
+        uint32_t ow = 0u, cw = 0u;
+        int b = 0;
+        if (valid) {
+            ow = __ldg(reinterpret_cast<const uint32_t*>(order) + i);
+            cw = __ldg(reinterpret_cast<const uint32_t*>(counts) + i);
+            b = __ldg(&bm[i]);
+        }
+        bool need = false;
+        if (valid) {
+            uint8_t o[4];
+            int p[5];
+            decode(ow, cw, o, p);
+            int st = GP_OK;
+            unsigned seen = 0;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                if (o[s] >= I.F || (seen >> o[s]) & 1u || p[s + 1] == p[s]) st = GP_ERR_INPUT;
+                seen |= 1u << (o[s] & 31);
+            }
+            if (b >= I.nb * I.nm || p[4] > n) st = GP_ERR_INPUT;
+            if (st != GP_OK) {
+                cost[i] = NAN;
+                status[i] = (uint8_t)st;
+            } else if (fast_tables && p[4] == n) {
+                bool inf = false;
+#pragma unroll
+                for (int s = 0; s < 4; ++s)
+                    inf |= sc_s[o[s] * N2 + tri_idx(n, p[s], p[s + 1])] == SC_INFEASIBLE;
+                status[i] = GP_OK;
+                if (inf) cost[i] = INFINITY;
+                else need = true;
+            } else {
+                const int mi = b % I.nm;
+                EvalOut r = eval_tables(I, 4, o, p, mi, I.batch[b / I.nm] / I.micro[mi]);
+                cost[i] = r.status == GP_OK ? r.cost : NAN;
+                status[i] = (uint8_t)r.status;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (need) wq[q + __popc(m & lt)] = make_uint4((unsigned)i, ow, cw, (unsigned)b);
+        q += __popc(m);
+        __syncwarp();
+        if (q >= 32) {
+            const uint4 e = wq[q - 32 + lane];
+            __syncwarp();
+            q -= 32;
+            eval_entry(e);
+        }
+    }
+    __syncwarp();
+    if (lane < q) eval_entry(wq[lane]);
+}

@@ -63,6 +63,52 @@ def test_k2_c4_sample_bitwise(engine, oracle_lib, name):
     assert same_bits(cost, gc).all()
 
 
+def _tile(a, reps):
+    return np.concatenate([a] * reps)
+
+
+@pytest.mark.parametrize("name", CASES_ALL)
+def test_k2_large_batch_path_bitwise(engine, name):
+    # >= 2^16 candidates take the persistent kernel with the stage codes in
+    # shared memory (k2_eval_batch_sc); tile every golden case past that and
+    # mix in malformed candidates (status 1, cost NaN)
+    doc, model, topo, groups, packed = _load(engine, name)
+    order, counts, bm = enumerate_encoded(packed)
+    gc, gs = golden_costs(name)
+    if gc.size == 0:
+        return
+    reps = (1 << 16) // gc.size + 1
+    order, counts, bm = _tile(order, reps), _tile(counts, reps), _tile(bm, reps)
+    gc, gs = _tile(gc, reps), _tile(gs, reps).copy()
+    bad = np.arange(7, order.shape[0], 9973)
+    counts = counts.copy()
+    counts[bad, 0] = 0
+    gs[bad] = 1
+    cost, status = engine.eval_batch(order, counts, bm)
+    assert (status == gs).all(), np.nonzero(status != gs)[0][:10]
+    good = gs == 0
+    assert np.isnan(cost[~good]).all()
+    ok = same_bits(cost[good], gc[good])
+    assert ok.all(), (np.nonzero(~ok)[0][:10], cost[good][~ok][:5], gc[good][~ok][:5])
+
+
+@pytest.mark.parametrize("name", ["c4", "c4j"])
+def test_k2_c4_large_batch_path_bitwise(engine, oracle_lib, name):
+    doc, model, topo, groups, packed = _load(engine, name)
+    idx = np.load(f"{G.GOLDEN}/{name}.sample_idx.npy")
+    gc = np.load(f"{G.GOLDEN}/{name}.sample_costs.npy")
+    k = packed.n_fgs
+    order = np.zeros((idx.size, k), np.uint8)
+    counts = np.zeros((idx.size, k), np.uint8)
+    bm = np.zeros(idx.size, np.uint8)
+    for r, i in enumerate(idx):
+        order[r], counts[r], bm[r] = oracle_lib.decode(packed, int(i))
+    reps = 4
+    cost, status = engine.eval_batch(_tile(order, reps), _tile(counts, reps), _tile(bm, reps))
+    assert (status == 0).all()
+    assert same_bits(cost, _tile(gc, reps)).all()
+
+
 def test_k2_rejects_bad_candidates(engine):
     doc, model, topo, groups, packed = _load(engine, "c2")
     order = np.array([[0, 0, 1], [0, 1, 7], [0, 1, 2], [0, 1, 2]], np.uint8)
