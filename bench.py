@@ -189,10 +189,11 @@ def extra_sections(eng, packed, total, local, args, world):
                      "achieved_gbs": N * bytes_per / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
                      "frac": N * bytes_per / (ms * 1e-3) / 1e9 / hbm},
         "note": "360 MB of candidates + results per launch (> 126 MB L2); order/counts/bm u8 "
-                "in, cost f64 + status u8 out. Not HBM-bound in practice: each candidate "
-                "gathers k stage-table entries, k codes and k-1 boundary times at random from "
-                "the L2-resident tables (ncu: L1TEX 73 % of peak, 4.5 L2 sectors and 10 "
-                "long-scoreboard stall cycles per issue; profiles/r1c_k2_eval_batch_ncu_raw.csv)"}
+                "in, cost f64 + status u8 out. k2_eval_batch_q4: stage codes in shared memory "
+                "decide the 85 % memory-infeasible candidates without table gathers; the "
+                "feasible ones are queued per warp and evaluated 32 at a time (stage-table and "
+                "boundary gathers from L2). ncu (profiles/r1e_k2_eval_batch_q4_ncu_raw.csv): "
+                "ALU pipe 57 %, long-scoreboard stalls dominant, DRAM 1.8 TB/s"}
 
     # ---- K5: 1F1B makespans of 10^5 of those C4 candidates
     # feasible candidates only (infeasible ones are rejected before simulating)

@@ -225,7 +225,10 @@ __global__ void __launch_bounds__(256) k2_eval_batch_sc(DevInst I, long long nca
 // shared memory and evaluated 32 at a time, so eval_fast runs with every lane
 // busy instead of once per warp under a mostly-idle mask.
 #define K2Q_THREADS 256
-__global__ void __launch_bounds__(K2Q_THREADS) k2_eval_batch_q4(DevInst I, long long ncand,
+#ifndef K2Q_MINB
+#define K2Q_MINB 1
+#endif
+__global__ void __launch_bounds__(K2Q_THREADS, K2Q_MINB) k2_eval_batch_q4(DevInst I, long long ncand,
                                                                 const uint8_t* __restrict__ order,
                                                                 const uint8_t* __restrict__ counts,
                                                                 const uint8_t* __restrict__ bm,
@@ -269,17 +272,26 @@ __global__ void __launch_bounds__(K2Q_THREADS) k2_eval_batch_q4(DevInst I, long 
     };
     int q = 0;  // warp-uniform queue length
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < ncand;
-         base += stride) {
-        const long long i = base + lane;
-        const bool valid = i < ncand;
-        uint32_t ow = 0u, cw = 0u;
-        int b = 0;
-        if (valid) {
+    // the next iteration's input words are loaded before this one is decided
+    auto load_in = [&](long long i, uint32_t& ow, uint32_t& cw, int& b) {
+        ow = cw = 0u;
+        b = 0;
+        if (i < ncand) {
             ow = __ldg(reinterpret_cast<const uint32_t*>(order) + i);
             cw = __ldg(reinterpret_cast<const uint32_t*>(counts) + i);
             b = __ldg(&bm[i]);
         }
+    };
+    long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    uint32_t ow_n, cw_n;
+    int b_n;
+    load_in(base + lane, ow_n, cw_n, b_n);
+    for (; base < ncand; base += stride) {
+        const long long i = base + lane;
+        const bool valid = i < ncand;
+        const uint32_t ow = ow_n, cw = cw_n;
+        const int b = b_n;
+        load_in(base + stride + lane, ow_n, cw_n, b_n);
         bool need = false;
         if (valid) {
             uint8_t o[4];
