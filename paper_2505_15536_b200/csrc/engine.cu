@@ -2104,7 +2104,9 @@ static int group_launch(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_
         // pair tables in shared memory: the FGs' second levels run as
         // separate CTAs (phase 2) instead of one after another in the
         // snapshot's CTA; GP_K7_SPLIT=0 keeps the single-kernel form
-        bool split = (smem_mode & 1) != 0;
+        // (only while the snapshots alone leave SMs idle: a large batch fills
+        // the GPU with whole-snapshot CTAs already)
+        bool split = (smem_mode & 1) != 0 && nb < 2u * (uint32_t)c->n_sms;
         if (const char* e = getenv("GP_K7_SPLIT")) split = split && atoi(e) != 0;
         if (split) {
             launch(nb, 1);
