@@ -25,6 +25,7 @@ struct SolveOut {
     uint8_t order[GP_MAX_STAGES];
     uint8_t counts[GP_MAX_STAGES];
     gp_plan_info info;
+    unsigned long long seq;  // gp_replan graph: written last, after a system fence
 };
 
 static_assert(sizeof(SolveOut) % 8 == 0, "SolveOut is copied in 8-byte words");
@@ -191,7 +192,7 @@ __device__ __noinline__ void solve_body(const DevInst& I, int k, unsigned long l
 __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned long long NP,
                                int nbm, const Key* result, const unsigned long long* err,
                                const unsigned long long* __restrict__ binom, SolveOut* out,
-                               int warm) {
+                               int warm, unsigned long long* seqctr) {
     // one warp: decode the arg-min key (cut positions by a 32-wide ballot
     // over the hockey-stick counts), then the warp plan detail
     (void)NP;
@@ -230,7 +231,19 @@ __global__ void k_solve_detail(DevInst I, int k, unsigned long long NC, unsigned
     __syncwarp();
     const unsigned long long* src = (const unsigned long long*)&so;
     unsigned long long* d = (unsigned long long*)out;
-    for (int q = lane; q < (int)(sizeof(SolveOut) / 8); q += 32) d[q] = src[q];
+    const int nw = (int)(offsetof(SolveOut, seq) / 8);
+    for (int q = lane; q < nw; q += 32) d[q] = src[q];
+    if (seqctr) {
+        // the host polls `seq` instead of synchronising the stream: the
+        // record's words are fenced to the system before the new number lands
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0) {
+            const unsigned long long v = *seqctr + 1ull;
+            *seqctr = v;
+            *(volatile unsigned long long*)&out->seq = v;
+        }
+    }
     TL_STOP(50);
 #if defined(GP_TIMELINE)
     if (lane == 0) {  // sub-phases: real pass start / detail done / exit

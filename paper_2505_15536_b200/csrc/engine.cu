@@ -25,6 +25,7 @@
 // (src/costmodel.py:56-89, src/timing.py:116-231, src/planner.py:157-253);
 // the file is compiled with -fmad=false.  There is no CPU fallback.
 #include <mutex>
+#include <atomic>
 #include <chrono>
 
 #include "common.cuh"
@@ -125,6 +126,8 @@ struct gp_ctx {
     DBuf<unsigned long long> s_lq;
     SolveOut* h_solve = nullptr;  // pinned, mapped (the gp_replan graph's detail kernel writes it)
     SolveOut* d_hsolve = nullptr; // device alias of h_solve
+    DBuf<unsigned long long> d_seq;        // completed gp_replan graphs (device count)
+    unsigned long long solve_seq = 0;      // launched gp_replan graphs (host count)
     RangeGeom last_geom{};
     bool last_generic = false;
     unsigned long long last_lo = 0, last_hi = 0;
@@ -297,7 +300,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     if (c->h_solve) cudaFreeHost(c->h_solve);
     c->z_bw.release(); c->z_mbw.release(); c->z_xt.release(); c->z_flags.release();
     c->z_tpk.release(); c->z_tcol.release(); c->z_res.release(); c->z_cnt.release();
-    c->dsolve.release(); c->gbest.release(); c->s_tim.release(); c->s_traces.release(); c->s_tidx.release(); c->s_ms.release(); c->s_st.release();
+    c->dsolve.release(); c->d_seq.release(); c->gbest.release(); c->s_tim.release(); c->s_traces.release(); c->s_tidx.release(); c->s_ms.release(); c->s_st.release();
     c->s_rep.release(); c->s_ends.release(); c->g_buf.release(); c->s_wq.release(); c->s_lq.release();
     if (c->flags_ev) cudaEventDestroy(c->flags_ev);
     if (c->t_ev0) cudaEventDestroy(c->t_ev0);
@@ -1145,7 +1148,8 @@ static int enqueue_solve(gp_ctx* c, uint64_t lo, uint64_t hi) {
     SolveOut* dst = c->pdl ? c->d_hsolve : c->dsolve.p;
     CUDA_TRY(launch_k(k_solve_detail, 1, 32, 0, c->stream, c->pdl, I, G.k, G.NC, G.NP, G.nbm,
                       (const Key*)c->result.p, (const unsigned long long*)c->err_idx.p,
-                      (const unsigned long long*)c->binom.p, dst, c->pdl ? 1 : 0));
+                      (const unsigned long long*)c->binom.p, dst, c->pdl ? 1 : 0,
+                      c->pdl ? c->d_seq.p : (unsigned long long*)nullptr));
     if (c->pdl) return GP_OK;
     CUDA_TRY(cudaMemcpyAsync(c->h_solve, c->dsolve.p, sizeof(SolveOut), cudaMemcpyDeviceToHost,
                              c->stream));
@@ -1236,6 +1240,11 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
         // make every buffer the graph touches exist before capturing
         CUDA_TRY(c->dsolve.ensure(1));
         CUDA_TRY(c->item_ctr.ensure((size_t)c->nm * h_fact(c->F) + 1));
+        CUDA_TRY(c->d_seq.ensure(1));
+        CUDA_TRY(cudaMemsetAsync(c->d_seq.p, 0, sizeof(unsigned long long), s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        c->solve_seq = 0;
+        c->h_solve->seq = 0;
         c->capturing = true;
         CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
         // the instance arena moves host -> device by a kernel reading the mapped
@@ -1314,7 +1323,22 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
     CUDA_TRY(cudaEventRecord(c->arena_ev, s));
     if (c->diag_timing) CUDA_TRY(cudaEventRecord(c->t_ev1, s));
     const double h2 = c->diag_timing ? now_us() : 0.0;
-    CUDA_TRY(cudaStreamSynchronize(s));
+    const unsigned long long want = ++c->solve_seq;
+    bool landed = false;
+    if (!c->diag_timing) {
+        // the detail kernel publishes the record with a sequence number in
+        // mapped memory: poll it (the graph's last kernel may still be
+        // exiting); a graph that never publishes falls through to the
+        // stream synchronisation, which reports its error
+        const volatile unsigned long long* seq = &c->h_solve->seq;
+        const double t_end = now_us() + 20000.0;
+        for (unsigned spin = 0;; ++spin) {
+            if (*seq == want) { landed = true; break; }
+            if ((spin & 1023u) == 1023u && now_us() > t_end) break;
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+    }
+    if (!landed) CUDA_TRY(cudaStreamSynchronize(s));
     const double h3 = c->diag_timing ? now_us() : 0.0;
     if (c->diag_timing) CUDA_TRY(cudaEventElapsedTime(&c->last_graph_ms, c->t_ev0, c->t_ev1));
     c->flags_known = false;
