@@ -951,9 +951,12 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
         G.chunk = 0;
         G.chunks_per_item = cpi;
         grid = items * cpi;
+        if (c->item_ctr.cap < items || !c->item_ctr.p) c->ctr_armed = 0;  // (re)allocation
         CUDA_TRY(c->item_ctr.ensure(items));
-        CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
-        c->ctr_armed = 0;  // k3_argmin leaves its counters non-zero
+        if (!c->pdl && items > c->ctr_armed) {  // (k3_argmin re-arms the ones it used)
+            CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, items * sizeof(unsigned int), s));
+            c->ctr_armed = items;
+        }
         G.item_ctr = c->item_ctr.p;
         int ts = ensure_tiles(c);
         if (ts != GP_OK) return ts;
@@ -975,6 +978,7 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
         kern<<<(unsigned)grid, K3_THREADS, smem, s>>>(I, G, S, c->binom.p, dflags);
         CUDA_TRY(cudaGetLastError());
         if (pending) return launch_fixup(c, G);
+        c->err_clean = !c->pdl;  // the tile kernel never writes err_idx
     }
     CUDA_TRY(cudaGetLastError());
     return GP_OK;

@@ -220,7 +220,10 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k3_argmin(DevInst I, Rang
         mine.tie = ((perm_rank * G.NC) + rr) * (unsigned long long)G.nbm +
                    (unsigned long long)(bi * I.nm + mi);
     }
-    block_argmin_finish(mine, S);
+    ArgminScratch Sr = S;  // the launch's item counters, zeroed by the last CTA
+    Sr.rearm = G.item_ctr;
+    Sr.nrearm = (unsigned int)(gridDim.x / G.chunks_per_item);
+    block_argmin_finish(mine, Sr);
 }
 
 // ---------------------------------------------------------------------------
