@@ -150,6 +150,33 @@ def test_k3_random_subranges(engine, name):
         assert got.evaluated == hi - lo
 
 
+def test_k3_interleaved_calls_rearm_state(engine):
+    # the sweep and the sub-range kernel re-arm their work counters and leave
+    # err_idx clean, and the engine skips the resets while it knows the device
+    # state: interleave every entry point that touches that state and check
+    # each answer
+    doc, model, topo, groups, packed = _load(engine, "c2j")
+    gc, gs = golden_costs("c2j")
+    order, counts, bm = enumerate_encoded(packed)
+    N = gc.size
+    rng = random.Random(11)
+    full = _key_argmin(packed, gc, gs, 0, N, order, counts, bm)[1]
+    for rep in range(3):
+        assert engine.argmin_range(0, N).index == full
+        lo, hi = sorted(rng.sample(range(N + 1), 2))
+        if hi > lo:
+            assert engine.argmin_range(lo, hi).index == _key_argmin(
+                packed, gc, gs, lo, hi, order, counts, bm)[1]
+        assert engine.argmin_range(0, N).index == full
+        b, _ = engine.replan(packed)
+        assert b.index == full
+        assert engine.argmin_range(0, N).index == full
+        cost, status = engine.eval_batch(order[:100], counts[:100], bm[:100])
+        assert same_bits(cost, gc[:100]).all()
+        engine.load(packed)
+        assert engine.argmin_range(0, N).index == full
+
+
 @pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("name", ["c1j", "c2", "c2j", "rand5", "rand10", "rand6", "small"])
 def test_k3_all_kernel_variants_agree(engine, name, mode):
