@@ -285,9 +285,11 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     // and the SM's warp scheduler favours its older CTA, so an item-major map
     // (an item's CTAs adjacent) gives whole items only first-wave or only
     // second-wave CTAs and they finish ~15 % apart.  Item-minor spreads each
-    // item's CTAs over both waves.  A cluster needs its item's CTAs adjacent.
+    // item's CTAs over both waves; with clusters the map is cluster-minor (a
+    // cluster's CTAs stay on one item: measured 32.8 vs 30.7 us unclustered).
     const unsigned long long islot =
-        (G.interleave && G.csize == 1) ? local % G.items : local / G.cpi;
+        !G.interleave ? local / G.cpi
+                      : (G.csize == 1 ? local % G.items : (local / G.csize) % G.items);
     const unsigned long long item = G.item0 + islot;
     const int mi = (int)(item / G.NP);
     const unsigned long long perm_rank = item % G.NP;
