@@ -473,11 +473,11 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     CUDA_TRY(c->tpk.ensure((size_t)c->nm * F * ((size_t)n * (n + 1) / 2)));
     CUDA_TRY(c->tcol.ensure((size_t)c->nm * F * (n + 1)));
     CUDA_TRY(c->flagsbuf.ensure(1));
-    CUDA_TRY(c->counter.ensure(1));
-    CUDA_TRY(c->result.ensure(1));
+    CUDA_TRY(c->counter.ensure(3));  // slots: a split range's sweep + 2 edge pieces
+    CUDA_TRY(c->result.ensure(3));
     CUDA_TRY(c->err_idx.ensure(1));
     CUDA_TRY(c->blk.ensure(4096));  // >= the generic fix-up grid (no realloc mid-stream)
-    CUDA_TRY(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned int), s));
+    CUDA_TRY(cudaMemsetAsync(c->counter.p, 0, c->counter.cap * sizeof(unsigned int), s));
     if (!c->binom.p) {
         // C(nn, r) for nn < 257, r <= GP_MAX_STAGES (composition unranking)
         std::vector<unsigned long long> tab((size_t)BINOM_ROWS * (GP_MAX_STAGES + 1), 0ull);
@@ -766,7 +766,8 @@ static int kernel_slots(gp_ctx* c, const void* kern, int threads, size_t smem, i
 }
 
 static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_lo,
-                        unsigned long long item_hi, int mode, const uint32_t* dflags) {
+                        unsigned long long item_hi, int mode, const uint32_t* dflags,
+                        int nb_sel = 0, int b0 = 0, int slot = 0) {
     cudaStream_t s = c->stream;
     const int k = R.k, n = c->n;
     size_t ntri = (size_t)n * (n + 1) / 2;
@@ -777,7 +778,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     if (mode == 2 && smem2 > (size_t)c->smem_max) mode = 1;
     if (mode == 1 && smem1 > (size_t)c->smem_max) mode = 0;
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
-    SwFn kern = pick_sweep(mode, c->nb, k);
+    SwFn kern = pick_sweep(mode, nb_sel > 0 ? nb_sel : c->nb, k);
     int per_sm = 0;
     { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
       if (st_ != GP_OK) return st_; }
@@ -792,6 +793,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "item range too large for one launch");
     SweepGeom G;
     G.k = k;
+    G.b0 = b0;
     G.nbm = R.nbm;
     G.NC = R.NC;
     G.NP = R.NP;
@@ -821,8 +823,8 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     CUDA_TRY(c->blk.ensure(grid));
     ArgminScratch S;
     S.blk = c->blk.p;
-    S.counter = c->counter.p;
-    S.result = c->result.p;
+    S.counter = c->counter.p + slot;
+    S.result = c->result.p + slot;
     S.err = nullptr;
     S.err_idx = c->err_idx.p;
     c->last_geom = R;
@@ -853,8 +855,18 @@ static int launch_fixup(gp_ctx* c, const RangeGeom& G) {
     return GP_OK;
 }
 
+static int range_async(gp_ctx* c, uint64_t lo, uint64_t hi, int slot);
+
 int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
+    return range_async(c, lo, hi, -1);
+}
+
+// slot < 0: a caller's range (resets, and the split below); slot >= 0: an
+// edge piece of a split range, its key into result slot `slot`
+static int range_async(gp_ctx* c, uint64_t lo, uint64_t hi, int slot) {
     if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    const bool top = slot < 0;
+    if (top) slot = 0;
     int k = c->F;
     uint64_t total;
     { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
@@ -875,11 +887,13 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     G.nm = c->nm;
     G.item_ctr = nullptr;
     G.tiles = nullptr;
-    c->last_lo = lo;
-    c->last_hi = hi;
+    if (top) {
+        c->last_lo = lo;
+        c->last_hi = hi;
+        if (!c->pdl && !c->err_clean)  // (the gp_replan graph resets it in K1 phase 1)
+            CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));  // = ~0
+    }
     ArgminScratch S;
-    if (!c->pdl && !c->err_clean)  // (the gp_replan graph resets it in K1 phase 1)
-        CUDA_TRY(cudaMemsetAsync(c->err_idx.p, 0xFF, sizeof(unsigned long long), s));  // = ~0
     c->err_clean = false;  // every branch below but the plain sweep may write it
     DevInst I = c->view();
     // table flags (error entries, overflow) force the status-tracking kernel;
@@ -916,6 +930,42 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
             return st;
         }
         return launch_fixup(c, G);
+    }
+    // a range inside one batch block holding >= 2 whole (micro, order) blocks:
+    // those through the sweep (that batch index only), the edge pieces through
+    // the tile kernel, each key into its own slot, then one combine
+    // (GP_K3_SPLIT=0 disables)
+    bool split = top && !generic && !pending && c->sweep_ok && c->force_mode < 0 && !c->pdl &&
+                 hi > lo;
+    if (split) if (const char* e = getenv("GP_K3_SPLIT")) split = atoi(e) != 0;
+    if (split) {
+        const unsigned long long per_b = (unsigned long long)c->nm * G.NP;
+        const unsigned long long bblk = per_b * G.NC;
+        const unsigned long long b = lo / bblk;
+        const unsigned long long f0 = (lo + G.NC - 1) / G.NC, f1 = hi / G.NC;  // whole blocks
+        if ((hi - 1) / bblk == b && f1 >= f0 + 2) {
+            c->last_generic = false;
+            CUDA_TRY(c->blk.ensure(1));
+            int st = launch_sweep(c, G, f0 - b * per_b, f1 - b * per_b, mode, nullptr, 1, (int)b, 0);
+            if (st != GP_OK) return st;
+            int nslot = 1;
+            if (lo < f0 * G.NC) {
+                st = range_async(c, lo, f0 * G.NC, nslot++);
+                if (st != GP_OK) return st;
+            }
+            if (f1 * G.NC < hi) {
+                st = range_async(c, f1 * G.NC, hi, nslot++);
+                if (st != GP_OK) return st;
+            }
+            if (nslot > 1) {
+                k_key_combine<<<1, 1, 0, s>>>(reinterpret_cast<Key*>(c->result.p), nslot);
+                CUDA_TRY(cudaGetLastError());
+            }
+            c->last_geom = G;
+            c->last_generic = false;
+            c->err_clean = !c->pdl;  // neither kernel writes err_idx
+            return GP_OK;
+        }
     }
     if (hi == lo) {
         generic = true;
@@ -966,8 +1016,8 @@ int gp_argmin_range_async(gp_ctx* c, uint64_t lo, uint64_t hi) {
     if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "range too large for one launch");
     CUDA_TRY(c->blk.ensure(grid));
     S.blk = c->blk.p;
-    S.counter = c->counter.p;
-    S.result = c->result.p;
+    S.counter = c->counter.p + slot;
+    S.result = c->result.p + slot;
     S.err = nullptr;
     S.err_idx = c->err_idx.p;
     c->last_geom = G;
@@ -1818,6 +1868,7 @@ int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_
         unsigned long long grid = (unsigned long long)nb * items * cpi;
         if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "snapshot batch too large");
         SweepGeom G;
+        G.b0 = 0;
         G.k = k; G.nbm = c->nb * c->nm; G.NC = NC; G.NP = NP; G.item0 = 0; G.cpi = cpi;
         G.W = c->sweep_W; G.ngroups = c->ngroups; G.groups = c->groups.p;
         G.prefixes = c->prefixes.p;

@@ -257,6 +257,7 @@ struct SweepGeom {
     const unsigned long long* bnk;  // C(nn, r), nn <= n, r <= k: contiguous [n+1][k+1]
     int csize;                      // thread-block cluster size (CTAs of one item), 1 = none
     int interleave;                 // CTA -> item map: 1 = item-minor (b % items), 0 = item-major
+    int b0;                         // first batch index of the NB evaluated together
 };
 
 #if defined(K3_PROFILE)
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     d_unrank_perm(k, perm_rank, order);
     double Mv[NB];
 #pragma unroll
-    for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[bi] / I.micro[mi]);
+    for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[G.b0 + bi] / I.micro[mi]);
     const double2* TPm = G.tpk + snap * G.s_tpk + (size_t)mi * I.F * ntri;
     const double* X = G.xt + snap * G.s_xt + (size_t)mi * I.F * I.F * I.nxp;
     const int f1 = order[k - 3], f2 = order[k - 2], f3 = order[k - 1];
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
         unsigned long long rr = best_t / NB, bi = best_t % NB;
         mine.cost = best_c;
         mine.tie = ((perm_rank * G.NC) + rr) * (unsigned long long)G.nbm +
-                   (unsigned long long)(bi * I.nm + mi);
+                   (unsigned long long)((G.b0 + bi) * I.nm + mi);
     }
     ArgminScratch Ss = S;
     Ss.blk = S.blk + (size_t)snap * per_snap;
@@ -581,3 +582,9 @@ __global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G,
     block_argmin_finish(mine, S);
 }
 
+// r[0] = the smallest of the keys r[0..n) (range split into launches)
+__global__ void k_key_combine(Key* r, int n) {
+    Key b = r[0];
+    for (int i = 1; i < n; ++i) if (key_less(r[i], b)) b = r[i];
+    r[0] = b;
+}
