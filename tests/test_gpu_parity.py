@@ -210,6 +210,25 @@ def test_k3_c4_variants(engine, mode):
     assert got.cost == doc["oracle_argmin"]["cost"]
 
 
+@pytest.mark.parametrize("name", ["c4", "c4j"])
+def test_k3_c4_split_subranges_vs_oracle(engine, oracle_lib, name):
+    # sub-ranges inside one batch block with whole (micro, order) blocks take
+    # the sweep (single batch index) + tile-kernel edges + combine; b = 1
+    # exercises the batch offset.  The pinned C oracle is the checker.
+    doc, model, topo, groups, packed = _load(engine, name)
+    NC = 79079
+    bblk = 3 * 24 * NC
+    ranges = [(0, 1_000_000), (17, 5 * NC + 3), (bblk + 12_345, bblk + 9 * NC - 1),
+              (2 * bblk - 4 * NC - 5, 2 * bblk), (bblk, bblk + 2 * NC)]
+    for lo, hi in ranges:
+        st, exp = oracle_lib.argmin_range(packed, lo, hi, threads=8)
+        assert st == 0
+        got = engine.argmin_range(lo, hi)
+        assert got.index == exp.index, (lo, hi)
+        assert same_bits(got.cost, exp.cost)
+        assert got.evaluated == hi - lo
+
+
 @pytest.mark.parametrize("name", CASES_ALL)
 def test_exhaustive_plan_matches_reference(engine, name):
     doc, model, topo, groups = load_case(name)
