@@ -364,14 +364,33 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     const int lane = threadIdx.x & 31;
     double best_c = INFINITY;
     unsigned long long best_t = ~0ull;  // R * NB + bi
+#if defined(K3_NOTASK)
+    const bool skip = true;  // diagnostic: staging + reduction only
+#else
     const bool skip = skip_if_flags && skip_if_flags[snap];  // generic kernel decides
+#endif
     unsigned int* const ctr = &G.item_ctr[(size_t)snap * G.items + islot];
     unsigned int t_next = 0;
+#if defined(K3_STATIC)
+    // diagnostic: round-robin tasks over the item's warps, no queue
+    const unsigned int wstride = (unsigned int)G.cpi * (blockDim.x >> 5);
+    const unsigned int wfirst = (unsigned int)((G.interleave && G.csize == 1) ? local / G.items
+                                                                               : local % G.cpi) *
+                                    (blockDim.x >> 5) + (threadIdx.x >> 5);
+    t_next = wfirst;
+#else
     if (lane == 0 && !skip) t_next = atomicAdd(ctr, 1u);
+#endif
     for (; !skip;) {
+#if defined(K3_STATIC)
+        const unsigned int t = t_next;
+        if ((unsigned long long)t * 32 >= G.W) break;
+        t_next += wstride;
+#else
         const unsigned int t = __shfl_sync(0xffffffffu, t_next, 0);
         if ((unsigned long long)t * 32 >= G.W) break;
         if (lane == 0) t_next = atomicAdd(ctr, 1u);  // next task, latency hidden by this one
+#endif
         const unsigned int u = t * 32 + lane;
         int len = 0, a = 1, q0 = 2;  // idle lanes keep in-range table addresses
         double fill2 = 0.0, res1 = 0.0, x1 = 0.0;
@@ -442,6 +461,9 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
             fill2 = fill + (e1.x + x1);
         }
         int lmax = len, lmin = len;
+#if defined(K3_NOLOOP)
+        len = 0; lmax = 0; lmin = 0;  // diagnostic: prologue + staging cost only
+#endif
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             int o = __shfl_xor_sync(0xffffffffu, lmax, off);
