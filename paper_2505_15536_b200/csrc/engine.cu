@@ -789,6 +789,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     unsigned long long cap = (tasks + (K3S_THREADS / 32) - 1) / (K3S_THREADS / 32);
     if (cpi > cap) cpi = cap;
     if (cpi < 1) cpi = 1;
+    if (const char* e = getenv("GP_K3_CPI")) if (atoi(e) > 0) cpi = (unsigned long long)atoi(e);  // diagnostic
     unsigned long long grid = items * cpi;
     if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "item range too large for one launch");
     SweepGeom G;
