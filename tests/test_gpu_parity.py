@@ -63,6 +63,24 @@ def test_k2_c4_sample_bitwise(engine, oracle_lib, name):
     assert same_bits(cost, gc).all()
 
 
+@pytest.mark.parametrize("name", ["c4", "c4j"])
+def test_k2_c4_random_1e5_vs_oracle(engine, oracle_lib, name):
+    # SURVEY §8(c) protocol item (2): 10^5 random C4 candidates bitwise against
+    # the pinned C oracle, through the large-batch path (>= 2^16) and the
+    # small-batch path (the first 1,000)
+    from paper_2505_15536_b200.enumeration import composition_table, decode_indices
+    doc, model, topo, groups, packed = _load(engine, name)
+    total = engine.space_size()
+    idx = np.random.default_rng(2505).integers(0, total, size=100_000)
+    order, counts, bm = decode_indices(80, 4, idx, composition_table(80, 4))
+    ec, es = oracle_lib.eval_batch(packed, order, counts, bm, threads=8)
+    cost, status = engine.eval_batch(order, counts, bm)
+    assert (status == es).all()
+    assert same_bits(cost, ec).all()
+    c1, s1 = engine.eval_batch(order[:1000], counts[:1000], bm[:1000])
+    assert (s1 == es[:1000]).all() and same_bits(c1, ec[:1000]).all()
+
+
 def _tile(a, reps):
     return np.concatenate([a] * reps)
 
