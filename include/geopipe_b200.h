@@ -302,6 +302,10 @@ int gp_argmin_range_async(gp_ctx *ctx, uint64_t lo, uint64_t hi);
  * ranges is the whole exhaustive space).  Read with gp_argmin_fetch; the
  * returned index is the global enumeration index. */
 int gp_argmin_items_async(gp_ctx *ctx, uint64_t item_lo, uint64_t item_hi);
+/* Result of the last asynchronous arg-min.  When a candidate of the range
+ * raises (its status is returned), out->index is the enumeration index of
+ * the first such candidate, so that a multi-GPU caller can order the ranks'
+ * errors as the reference's sequential loop would meet them. */
 int gp_argmin_fetch(gp_ctx *ctx, gp_best *out);
 
 /* One-call exact re-plan: arg-min over [lo, hi) and the winner's splits +
@@ -478,6 +482,22 @@ int gp_plan_timing(gp_ctx *ctx, uint32_t k, uint64_t n, const uint8_t *order,
 int gp_replan_snapshots(gp_ctx *ctx, const double *bandwidth, uint32_t n_snap, gp_best *out,
                         int32_t *status);
 
+/*
+ * Device-pointer, asynchronous form of gp_replan_snapshots (the bench's and
+ * the multi-GPU path's hot loop): d_bandwidth = n_snap D x D matrices in
+ * device memory; per snapshot i, d_keys[2i] = the winner's cost (f64 bits)
+ * and d_keys[2i+1] = its tie rank ((order rank * C(n-1,k-1) + cuts rank) *
+ * |B||M| + (b, m) index; ~0 when empty), d_flags[i] != 0 when the snapshot's
+ * tables raise (then gp_replan_snapshots gives its status).  Needs an
+ * error-free loaded instance with k >= 3 (else GP_ERR_INPUT).
+ */
+int gp_replan_snapshots_async(gp_ctx *ctx, const double *d_bandwidth, uint32_t n_snap,
+                              void *d_keys, uint32_t *d_flags);
+
+/* Restore the loaded instance's link bandwidths and its GroupIndex
+ * min_intra_bandwidth values after gp_set_bandwidth snapshots. */
+int gp_reset_bandwidth(gp_ctx *ctx);
+
 /* Stream the context uses (cudaStream_t), for event timing by callers. */
 void *gp_ctx_stream(gp_ctx *ctx);
 
@@ -500,6 +520,16 @@ int gp_diag_timeline(void *out, uint32_t cap, uint32_t *n);
  * L1/L2; 1 one triangle in shared memory; 2 two triangles; 3 generic
  * status-tracking kernel).  Results are identical in every mode. */
 int gp_ctx_set_k3_mode(gp_ctx *ctx, int mode);
+/* Parity tests (not a production path): until gp_diag_verify_end, every
+ * exhaustive / snapshot launch (K3 sweep, sub-range and generic kernels, the
+ * gp_replan graph, gp_replan_snapshots) uses its verify instantiation - the
+ * same arithmetic source plus a store - and records each evaluated
+ * candidate's cost at position g - lo, g = snapshot * space_size + index,
+ * for g in [lo, lo + n).  Error candidates record a NaN whose low 4 bits are
+ * the status code; unwritten slots hold the all-ones NaN pattern.
+ * gp_diag_verify_end copies the n slots to `out` (may be NULL). */
+int gp_diag_verify_begin(gp_ctx *ctx, uint64_t lo, uint64_t n);
+int gp_diag_verify_end(gp_ctx *ctx, double *out);
 
 #ifdef __cplusplus
 }

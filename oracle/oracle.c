@@ -726,6 +726,60 @@ int or_eval_batch(const gp_instance *I, uint32_t k, uint64_t n, const uint8_t *o
     return GP_OK;
 }
 
+/* Every candidate of the enumeration range [lo, hi): cost[i - lo] and
+ * status[i - lo] as _evaluate gives them (NaN cost where it raises); the
+ * per-candidate reference for the engine's verify sink. */
+typedef struct {
+    const gp_instance *I;
+    uint64_t lo, hi, base;
+    double *cost;
+    uint8_t *status;
+} erange_job;
+
+static void *erange_worker(void *arg)
+{
+    erange_job *J = (erange_job *)arg;
+    uint32_t k = J->I->n_fgs;
+    for (uint64_t idx = J->lo; idx < J->hi; ++idx) {
+        uint8_t order[GP_MAX_STAGES], counts[GP_MAX_STAGES];
+        uint32_t bm;
+        double c = NAN;
+        or_decode(J->I, idx, order, counts, &bm);
+        int st = or_evaluate(J->I, k, order, counts, bm, &c, NULL);
+        J->cost[idx - J->base] = st == GP_OK ? c : NAN;
+        J->status[idx - J->base] = (uint8_t)st;
+    }
+    return NULL;
+}
+
+int or_eval_range(const gp_instance *I, uint64_t lo, uint64_t hi, double *cost,
+                  uint8_t *status, int threads)
+{
+    uint32_t k = I->n_fgs;
+    if (k < 1 || k > GP_MAX_STAGES || k > I->n_layers)
+        return GP_ERR_INFEASIBLE_SPLIT;
+    if (threads < 1)
+        threads = 1;
+    if (threads > 256)
+        threads = 256;
+    erange_job jobs[256];
+    pthread_t tid[256];
+    uint64_t span = hi > lo ? hi - lo : 0;
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = (erange_job){I, lo + span * (uint64_t)t / (uint64_t)threads,
+                               lo + span * (uint64_t)(t + 1) / (uint64_t)threads, lo, cost,
+                               status};
+        if (threads == 1)
+            erange_worker(&jobs[0]);
+        else
+            pthread_create(&tid[t], NULL, erange_worker, &jobs[t]);
+    }
+    if (threads > 1)
+        for (int t = 0; t < threads; ++t)
+            pthread_join(tid[t], NULL);
+    return GP_OK;
+}
+
 /* Per-group constants of the TP/DP splits (they depend on the group only):
  * split_asymmetric_tp_dp on device p_c in member order and
  * split_asymmetric_dp on second-level capacities (src/planner.py:188-200). */

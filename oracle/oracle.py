@@ -53,6 +53,8 @@ def lib():
         L.or_eval_batch.argtypes = [P(abi.GpInstance), C.c_uint32, C.c_uint64,
                                     P(C.c_uint8), P(C.c_uint8), P(C.c_uint8),
                                     P(C.c_double), P(C.c_uint8), C.c_int]
+        L.or_eval_range.argtypes = [P(abi.GpInstance), C.c_uint64, C.c_uint64, P(C.c_double),
+                                    P(C.c_uint8), C.c_int]
         L.or_group_detail.argtypes = [P(abi.GpInstance), C.c_uint32, P(abi.GpGroupInfo)]
         L.or_sim_1f1b.argtypes = [P(abi.GpTiming), C.c_int, P(C.c_double)]
         L.or_sim_batch.argtypes = [P(abi.GpTiming), C.c_uint64, C.c_int, P(C.c_double),
@@ -139,6 +141,18 @@ def eval_batch(packed, order, counts, bm, threads=1):
     status = np.empty(n, dtype=np.uint8)
     lib().or_eval_batch(C.byref(packed.struct), k, n, _u8(order), _u8(counts),
                         _u8(bm), _dp(cost), _u8(status), int(threads))
+    return cost, status
+
+
+def eval_range(packed, lo, hi, threads=1):
+    """(cost, status) of every candidate with enumeration index in [lo, hi)."""
+    n = max(0, int(hi) - int(lo))
+    cost = np.empty(n, dtype=np.float64)
+    status = np.empty(n, dtype=np.uint8)
+    if n:
+        st = lib().or_eval_range(C.byref(packed.struct), int(lo), int(hi), _dp(cost), _u8(status),
+                                 int(threads))
+        abi.raise_for(st, "bad instance")
     return cost, status
 
 

@@ -16,7 +16,7 @@ from typing import Optional
 from . import abi
 from . import domain as D
 from .engine import Engine, default_engine
-from .layout import PackedInstance
+from .layout import PackedInstance, packed_instance
 
 
 def _stages(plan, packed: PackedInstance):
@@ -42,7 +42,7 @@ def _stages(plan, packed: PackedInstance):
 
 
 def _evaluate(plan, topology, model, groups, opt_seconds, engine, timing):
-    packed = PackedInstance(model, topology, groups, 1.25)
+    packed = packed_instance(model, topology, groups, 1.25)
     eng = (engine if engine is not None else default_engine()).load(packed)
     return eng.plan_cost(_stages(plan, packed), plan.batch_b, plan.microbatch_m, opt_seconds,
                          timing)

@@ -147,6 +147,24 @@ __device__ __forceinline__ double gtsel(double a, double b) {
 
 
 // ----------------------------------------------------------------------------
+// Verify sink (parity tests): when `out` is set, the verify instantiations of
+// the K3 / K6 kernels store every evaluated candidate's cost at its global
+// position g = snapshot * stride + enumeration index, g in [lo, lo + n).
+// Production launches carry out = nullptr and use the plain instantiations
+// (same arithmetic source, no stores).  Error candidates (generic kernel)
+// store a quiet NaN whose low bits hold the status code.
+// ----------------------------------------------------------------------------
+struct VerifySink {
+    double* out = nullptr;
+    unsigned long long lo = 0, n = 0, stride = 0;
+};
+__device__ __forceinline__ void vput(const VerifySink& V, unsigned long long snap,
+                                     unsigned long long idx, double c) {
+    const unsigned long long g = snap * V.stride + idx;
+    if (g - V.lo < V.n) V.out[g - V.lo] = c;
+}
+
+// ----------------------------------------------------------------------------
 // K3: exhaustive argmin over an enumeration-index range
 // ----------------------------------------------------------------------------
 struct RangeGeom {
@@ -163,16 +181,17 @@ struct RangeGeom {
     int items_mode;                    // generic kernel: [lo, hi) indexes (b, item, comp)
     unsigned long long it_lo, it_span; // item range of items_mode
     int nm;                            // |M| (items_mode decode)
+    VerifySink vs;                     // parity tests only (out = nullptr otherwise)
 };
 
-__device__ unsigned long long d_binom(int n, int r) {
+static __device__ unsigned long long d_binom(int n, int r) {
     if (r < 0 || r > n) return 0ull;
     unsigned long long res = 1;
     for (int i = 1; i <= r; ++i) res = res * (unsigned long long)(n - r + i) / (unsigned long long)i;
     return res;
 }
 
-__device__ void d_unrank_perm(int k, unsigned long long r, uint8_t* perm) {
+static __device__ void d_unrank_perm(int k, unsigned long long r, uint8_t* perm) {
     if (k <= 12 && r < 479001600ull) {
         // 32-bit arithmetic (12! < 2^32) and the pool as 4-bit fields of one
         // register (no local-memory array, no 64-bit division)
@@ -206,7 +225,7 @@ __device__ void d_unrank_perm(int k, unsigned long long r, uint8_t* perm) {
 }
 
 // composition rank -> cut positions p[1..k-1] (lexicographic in counts)
-__device__ void d_unrank_cuts(int n, int k, unsigned long long r, int* p) {
+static __device__ void d_unrank_cuts(int n, int k, unsigned long long r, int* p) {
     p[0] = 0;
     int prev = 0;
     for (int j = 1; j < k; ++j) {
@@ -252,7 +271,7 @@ struct ArgminScratch {
 // Reduction over a group of `nblk` CTAs (the whole grid, or one snapshot's
 // CTAs): CTA `bidx` of the group writes its key; the last one to finish
 // reduces the group's keys into *S.result and re-arms the counter.
-__device__ void block_argmin_finish(Key mine, const ArgminScratch& S, unsigned int nblk,
+static __device__ void block_argmin_finish(Key mine, const ArgminScratch& S, unsigned int nblk,
                                     unsigned int bidx) {
     __shared__ Key wbest[32];
     __shared__ bool last;

@@ -38,6 +38,7 @@
 #include "k5_sim.cuh"
 #include "k7_grouping.cuh"
 #include "k8_validate.cuh"
+#include "verify.h"
 
 // ----------------------------------------------------------------------------
 // context
@@ -145,7 +146,11 @@ struct gp_ctx {
     int cache_n = -1, cache_k = -1;   // (n, k) of the enumeration helpers
     // gp_replan: CUDA graph of H2D + K1 + K3 + detail + D2H for one shape
     cudaGraphExec_t graph_exec = nullptr;
-    unsigned long long graph_key[10] = {0};
+    unsigned long long graph_key[11] = {0};
+    // shape key of the instance the context tables currently hold (set by
+    // gp_ctx_load and gp_replan): the graph replays only while it equals
+    // graph_key, i.e. no load of another shape came in between
+    unsigned long long loaded_key[11] = {0};
     unsigned long long graph_gen = 0;
     RangeGeom graph_geom{};
     unsigned long long graph_lo = 0, graph_hi = 0;
@@ -156,7 +161,13 @@ struct gp_ctx {
     float last_graph_ms = -1.0f;
     double host_us[4] = {0, 0, 0, 0};  // gp_replan: arena fill, launch, wait, finish
     size_t arena_bytes = 0;
+    size_t bw_off = 0;  // offset of the loaded bandwidth matrix in the arena
     int force_mode = -1;  // -1 auto; 0/1/2 fast-path variant; 3 generic kernel
+    // parity tests: every K3 / K6 launch uses the VER instantiation and
+    // stores each candidate's cost into vbuf (gp_diag_verify_begin / _end)
+    bool verify = false;
+    VerifySink vs;
+    DBuf<double> vbuf;
     // device state known from earlier launches on the stream (memsets skipped):
     // item counters [0, ctr_armed) are zero (k3_sweep re-arms the ones it
     // used); err_idx holds ~0 (no launch since its reset could have written it)
@@ -311,7 +322,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
     c->counter.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
-    c->ginfo.release(); c->dstatus.release();
+    c->ginfo.release(); c->dstatus.release(); c->vbuf.release();
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -353,8 +364,11 @@ static int known_flags(gp_ctx* c) {
     return -1;
 }
 
+static void replan_key(const gp_ctx* c, const gp_instance* in, unsigned long long* key);
+
 int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     if (c) { c->ctr_armed = 0; c->err_clean = false; }  // launches below skip neither reset
+    if (c) memset(c->loaded_key, 0, sizeof(c->loaded_key));  // valid again once this load succeeds
     if (!c || !in) return fail(GP_ERR_INPUT, "null argument");
     if (in->n_layers < 1 || in->n_layers > GP_MAX_LAYERS)
         return fail(GP_ERR_INPUT, "n_layers %u outside [1, %d]", in->n_layers, GP_MAX_LAYERS);
@@ -487,9 +501,11 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
     }
     int st = run_tables(c, true);
     if (st != GP_OK) return st;
+    c->bw_off = seg[i_bw].off;
     // enumeration helpers depend on (n, k) only: rebuild when those change
     if (c->cache_n == (int)n && c->cache_k == (int)F) {
         c->loaded = true;
+        replan_key(c, in, c->loaded_key);
         return GP_OK;
     }
     c->cache_n = (int)n;
@@ -553,6 +569,7 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
         }
     }
     c->loaded = true;
+    replan_key(c, in, c->loaded_key);
     return GP_OK;
 }
 
@@ -581,6 +598,22 @@ int gp_set_bandwidth(gp_ctx* c, const double* bandwidth) {
     DevInst I = c->view();
     k1_minbw<<<(c->F + 31) / 32, 32, 0, c->stream>>>(I, c->fg_minbw.p);
     CUDA_TRY(cudaGetLastError());
+    return run_tables(c, false);
+}
+
+// Restore the loaded instance's bandwidth matrix and its GroupIndex
+// min_intra_bandwidth values (not re-derived from the matrix: a hierarchy
+// read from file may carry other values), then the boundary/AL tables.
+int gp_reset_bandwidth(gp_ctx* c) {
+    if (!c || !c->loaded) return fail(GP_ERR_INPUT, "context not loaded");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->arena_ev) CUDA_TRY(cudaEventSynchronize(c->arena_ev));  // pinned arena = loaded instance
+    const size_t DD = (size_t)c->D * c->D;
+    CUDA_TRY(cudaMemcpyAsync(c->bw.p, c->h_arena + c->bw_off, DD * sizeof(double),
+                             cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->fg_minbw.p, c->fg_minbw_in.p, (size_t)c->F * sizeof(double),
+                             cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaEventRecord(c->arena_ev, c->stream));
     return run_tables(c, false);
 }
 
@@ -682,9 +715,6 @@ static int item_tpb(gp_ctx* c, unsigned long long n) {
     return t < 32 ? 32 : (t > 128 ? 128 : (int)t);
 }
 
-typedef void (*SwFn)(DevInst, SweepGeom, ArgminScratch, const unsigned long long*,
-                     const uint32_t*);
-
 // sweep variant: shared-memory mode x batch sizes per m x (k = 3..6 fixed at
 // compile time in the all-shared-memory mode, else generic)
 static SwFn pick_sweep(int mode, int nb, int k) {
@@ -778,7 +808,8 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     if (mode == 2 && smem2 > (size_t)c->smem_max) mode = 1;
     if (mode == 1 && smem1 > (size_t)c->smem_max) mode = 0;
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
-    SwFn kern = pick_sweep(mode, nb_sel > 0 ? nb_sel : c->nb, k);
+    SwFn kern = c->verify ? pick_sweep_verify(mode, nb_sel > 0 ? nb_sel : c->nb, k)
+                          : pick_sweep(mode, nb_sel > 0 ? nb_sel : c->nb, k);
     int per_sm = 0;
     { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
       if (st_ != GP_OK) return st_; }
@@ -812,6 +843,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     G.s_tpk = G.s_tcol = G.s_xt = 0;
     G.gsteps = 1;
     while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
+    if (c->verify) G.vs = c->vs;
     if (c->item_ctr.cap < items || !c->item_ctr.p) c->ctr_armed = 0;  // (re)allocation
     CUDA_TRY(c->item_ctr.ensure(items));
     // (the gp_replan graph resets the counters in K1 phase 1; the sweep
@@ -914,13 +946,13 @@ static int range_async(gp_ctx* c, uint64_t lo, uint64_t hi, int slot) {
     int mode = smem2 <= (size_t)c->smem_max ? 2 : (smem1 <= (size_t)c->smem_max ? 1 : 0);
     if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
-    typedef void (*K3Fn)(DevInst, RangeGeom, ArgminScratch, const unsigned long long*,
-                         const uint32_t*);
     static const K3Fn table[3][4] = {
         {k3_argmin<0, 1>, k3_argmin<0, 2>, k3_argmin<0, 3>, k3_argmin<0, 4>},
         {k3_argmin<1, 1>, k3_argmin<1, 2>, k3_argmin<1, 3>, k3_argmin<1, 4>},
         {k3_argmin<2, 1>, k3_argmin<2, 2>, k3_argmin<2, 3>, k3_argmin<2, 4>}};
-    K3Fn kern = generic ? nullptr : table[mode][c->nb - 1];
+    K3Fn kern = generic ? nullptr
+                        : (c->verify ? pick_argmin_verify(mode, c->nb) : table[mode][c->nb - 1]);
+    if (c->verify) G.vs = c->vs;
     if (!generic && lo == 0 && hi == total && hi > 0 && c->sweep_ok && c->force_mode != 4) {
         c->last_generic = false;
         CUDA_TRY(c->blk.ensure(1));
@@ -1075,6 +1107,7 @@ int gp_argmin_fetch(gp_ctx* c, gp_best* out) {
     out->evaluated = c->last_hi - c->last_lo;
     if (err != ~0ull) {
         int code = (int)(err & 15ull);
+        out->index = err >> 4;  // first erroring candidate (enumeration order)
         return fail(code, "candidate %llu raises status %d", err >> 4, code);
     }
     if (r.tie == ~0ull) return fail(GP_ERR_NO_FEASIBLE, "empty candidate range");
@@ -1162,6 +1195,7 @@ int gp_argmin_items_async(gp_ctx* c, uint64_t item_lo, uint64_t item_hi) {
     G.it_span = item_hi > item_lo ? item_hi - item_lo : 1;
     G.lo = 0;
     G.hi = (unsigned long long)c->nb * (item_hi - item_lo) * NC;
+    if (c->verify) G.vs = c->vs;
     c->last_lo = 0;
     c->last_hi = G.hi;
     c->last_geom = G;
@@ -1267,6 +1301,12 @@ static void instance_shape(const gp_instance* in, unsigned long long* key) {
     key[8] = h;
 }
 
+static void replan_key(const gp_ctx* c, const gp_instance* in, unsigned long long* key) {
+    instance_shape(in, key);
+    memcpy(&key[9], &in->bottleneck_factor, sizeof(double));
+    key[10] = (unsigned long long)(long long)c->force_mode;
+}
+
 static inline double now_us() {
     return std::chrono::duration<double, std::micro>(
                std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -1276,10 +1316,10 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
     if (c) { c->ctr_armed = 0; c->err_clean = false; }  // launches below skip neither reset
     if (!c || !in || !best) return fail(GP_ERR_INPUT, "null argument");
     const double h0 = c->diag_timing ? now_us() : 0.0;
-    unsigned long long key[10];
-    instance_shape(in, key);
-    memcpy(&key[9], &in->bottleneck_factor, sizeof(double));
+    unsigned long long key[11];
+    replan_key(c, in, key);
     const bool same = c->graph_exec && memcmp(key, c->graph_key, sizeof(key)) == 0 &&
+                      memcmp(key, c->loaded_key, sizeof(key)) == 0 &&
                       c->graph_gen == __atomic_load_n(&g_alloc_gen, __ATOMIC_RELAXED);
     cudaStream_t s = c->stream;
     if (!same) {
@@ -1788,6 +1828,136 @@ int gp_sim_1f1b(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t iterat
     return GP_OK;
 }
 
+// K6 for nb snapshots whose bandwidth matrices are at d_bw (device memory):
+// patch the per-snapshot tables, then one sweep over (snapshot, item); the
+// arg-min key of snapshot i goes to d_keys[i] and its table flags (errors
+// that need the status-tracking path) to d_flags[i].  Asynchronous on the
+// context stream.  `vsnap0` = global index of the first snapshot (verify sink).
+static int snap_enqueue(gp_ctx* c, const double* d_bw, uint32_t nb, Key* d_keys,
+                        uint32_t* d_flags, unsigned long long vsnap0) {
+    cudaStream_t s = c->stream;
+    const int k = c->F, n = c->n;
+    uint64_t total;
+    { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
+    const unsigned long long NP = h_fact(k), NC = h_binom(n - 1, k - 1);
+    const unsigned long long items = (unsigned long long)c->nm * NP;
+    const size_t ntri = (size_t)n * (n + 1) / 2, nxp = (size_t)((n + 1) & ~1);
+    const size_t s_tpk = (size_t)c->nm * c->F * ntri, s_tcol = (size_t)c->nm * c->F * (n + 1);
+    const size_t s_xt = (size_t)c->nm * c->F * c->F * nxp;
+    CUDA_TRY(c->z_mbw.ensure((size_t)nb * c->F));
+    CUDA_TRY(c->z_tpk.ensure((size_t)nb * s_tpk));
+    CUDA_TRY(c->z_tcol.ensure((size_t)nb * s_tcol));
+    CUDA_TRY(c->z_xt.ensure((size_t)nb * s_xt));
+    CUDA_TRY(c->z_cnt.ensure(nb));
+    CUDA_TRY(cudaMemsetAsync(d_flags, 0, nb * sizeof(uint32_t), s));
+    CUDA_TRY(cudaMemsetAsync(c->z_cnt.p, 0, nb * sizeof(unsigned int), s));
+    SnapGeom Z;
+    Z.nsnap = (int)nb;
+    Z.bw = d_bw; Z.mbw = c->z_mbw.p; Z.flags = d_flags;
+    Z.tpk = c->z_tpk.p; Z.tcol = c->z_tcol.p; Z.xt = c->z_xt.p;
+    Z.s_tpk = s_tpk; Z.s_tcol = s_tcol; Z.s_xt = s_xt;
+    DevInst I = c->view();
+    k6_minbw<<<(unsigned)((nb * c->F + 127) / 128), 128, 0, s>>>(I, Z);
+    const long long work = (long long)(s_tpk + (size_t)c->nm * c->F * c->F * n);
+    dim3 pg((unsigned)((work + 255) / 256), nb);
+    k6_patch<<<pg, 256, 0, s>>>(I, Z);
+    CUDA_TRY(cudaGetLastError());
+    // sweep over (snapshot, item)
+    size_t smem0 = 16 + (((size_t)(n + 1) * (k + 1) * 8 + 15) & ~(size_t)15) + (size_t)c->ngroups * 16;
+    size_t smem1 = smem0 + ntri * 16 + (n + 1) * 16 + 3 * nxp * 8 + (size_t)n * 16;
+    size_t smem2 = smem1 + ntri * 16;
+    int mode = smem2 <= (size_t)c->smem_max ? 2 : (smem1 <= (size_t)c->smem_max ? 1 : 0);
+    if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
+    size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
+    SwFn kern = c->verify ? pick_sweep_verify(mode, c->nb, k) : pick_sweep(mode, c->nb, k);
+    int per_sm = 0;
+    { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
+      if (st_ != GP_OK) return st_; }
+    unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
+    unsigned long long cpi = (items * nb) >= resident ? 1 : resident / (items * nb);
+    unsigned long long tasks = (c->sweep_W + 31) / 32;
+    unsigned long long cap = (tasks + (K3S_THREADS / 32) - 1) / (K3S_THREADS / 32);
+    if (cpi > cap) cpi = cap;
+    if (cpi < 1) cpi = 1;
+    unsigned long long grid = (unsigned long long)nb * items * cpi;
+    if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "snapshot batch too large");
+    SweepGeom G;
+    G.b0 = 0;
+    G.k = k; G.nbm = c->nb * c->nm; G.NC = NC; G.NP = NP; G.item0 = 0; G.cpi = cpi;
+    G.W = c->sweep_W; G.ngroups = c->ngroups; G.groups = c->groups.p;
+    G.prefixes = c->prefixes.p;
+    G.bnk = c->bnk.p;
+    G.gsteps = 1;
+    while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
+    G.items = (unsigned int)items;
+    G.tpk = c->z_tpk.p; G.tcol = c->z_tcol.p; G.xt = c->z_xt.p;
+    G.s_tpk = s_tpk; G.s_tcol = s_tcol; G.s_xt = s_xt;
+    if (c->verify) {  // global position = (vsnap0 + snap) * total + index
+        G.vs = c->vs;
+        G.vs.lo = c->vs.lo - vsnap0 * total;
+    }
+    if (c->item_ctr.cap < (size_t)nb * items || !c->item_ctr.p) c->ctr_armed = 0;
+    CUDA_TRY(c->item_ctr.ensure((size_t)nb * items));
+    CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, (size_t)nb * items * sizeof(unsigned int), s));
+    G.item_ctr = c->item_ctr.p;
+    CUDA_TRY(c->blk.ensure(grid > 4096 ? grid : 4096));
+    ArgminScratch S;
+    S.blk = c->blk.p;
+    S.counter = c->z_cnt.p;
+    S.result = d_keys;
+    S.err = nullptr;
+    S.err_idx = c->err_idx.p;
+    CUDA_TRY(launch_sweep_kernel(kern, (unsigned)grid, smem, s, G, I, S, c->binom.p, d_flags));
+    CUDA_TRY(cudaGetLastError());
+    return GP_OK;
+}
+
+// per-snapshot batch size: keep the per-snapshot tables around 256 MB
+static uint32_t snap_batch(gp_ctx* c) {
+    const int n = c->n;
+    const size_t ntri = (size_t)n * (n + 1) / 2, nxp = (size_t)((n + 1) & ~1);
+    const size_t per = ((size_t)c->nm * c->F * ntri + (size_t)c->nm * c->F * (n + 1)) * 16 +
+                       (size_t)c->nm * c->F * c->F * nxp * 8 + (size_t)c->D * c->D * 8;
+    uint32_t SB = (uint32_t)((256ull << 20) / (per ? per : 1));
+    if (SB < 1) SB = 1;
+    if (SB > 4096) SB = 4096;
+    return SB;
+}
+
+// the fast (table-patch + sweep) path applies: error-free base tables, k >= 3
+static int snap_fast_ok(gp_ctx* c, bool* ok) {
+    uint64_t total;
+    { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
+    int fl = known_flags(c);
+    if (fl < 0) {
+        CUDA_TRY(cudaEventSynchronize(c->flags_ev));
+        fl = known_flags(c);
+    }
+    *ok = fl == 0 && c->F >= 3 && c->sweep_ok && c->nb <= 4 && total > 0 && c->force_mode != 3 &&
+          c->force_mode != 4;
+    return GP_OK;
+}
+
+int gp_replan_snapshots_async(gp_ctx* c, const double* d_bandwidth, uint32_t n_snap, void* d_keys,
+                              uint32_t* d_flags) {
+    if (c) { c->ctr_armed = 0; c->err_clean = false; }
+    if (!c || !c->loaded || !d_bandwidth || !d_keys || !d_flags) return fail(GP_ERR_INPUT, "bad arguments");
+    if (n_snap == 0) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    bool ok = false;
+    { int st_ = snap_fast_ok(c, &ok); if (st_ != GP_OK) return st_; }
+    if (!ok) return fail(GP_ERR_INPUT, "device snapshot path needs error-free tables and k >= 3 "
+                                       "(use gp_replan_snapshots)");
+    const uint32_t SB = snap_batch(c);
+    const size_t DD = (size_t)c->D * c->D;
+    for (uint32_t b0 = 0; b0 < n_snap; b0 += SB) {
+        const uint32_t nb = (n_snap - b0) < SB ? (n_snap - b0) : SB;
+        int st = snap_enqueue(c, d_bandwidth + (size_t)b0 * DD, nb, (Key*)d_keys + b0, d_flags + b0, b0);
+        if (st != GP_OK) return st;
+    }
+    return GP_OK;
+}
+
 int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_best* out,
                         int32_t* status) {
     if (c) { c->ctr_armed = 0; c->err_clean = false; }  // launches below skip neither reset
@@ -1799,99 +1969,27 @@ int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_
     uint64_t total;
     { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
     const unsigned long long NP = h_fact(k), NC = h_binom(n - 1, k - 1);
-    const unsigned long long items = (unsigned long long)c->nm * NP;
     const size_t DD = (size_t)c->D * c->D;
-    const size_t ntri = (size_t)n * (n + 1) / 2, nxp = (size_t)((n + 1) & ~1);
-    const size_t s_tpk = (size_t)c->nm * c->F * ntri, s_tcol = (size_t)c->nm * c->F * (n + 1);
-    const size_t s_xt = (size_t)c->nm * c->F * c->F * nxp;
-    int fl_sync = known_flags(c);
-    if (fl_sync < 0) {  // base tables must be error-free for the per-snapshot fast path
-        CUDA_TRY(cudaEventSynchronize(c->flags_ev));
-        fl_sync = known_flags(c);
-    }
-    const bool fast = k >= 3 && c->sweep_ok && c->nb <= 4 && total > 0 && c->force_mode != 3 &&
-                      c->force_mode != 4;
-    // batch size: keep the per-snapshot tables around 256 MB
-    size_t per = (s_tpk + s_tcol) * 16 + s_xt * 8 + DD * 8;
-    uint32_t SB = (uint32_t)((256ull << 20) / (per ? per : 1));
-    if (SB < 1) SB = 1;
-    if (SB > 4096) SB = 4096;
+    bool fast = false;
+    { int st_ = snap_fast_ok(c, &fast); if (st_ != GP_OK) return st_; }
+    uint32_t SB = snap_batch(c);
     if (SB > n_snap) SB = n_snap;
     std::vector<uint32_t> h_fl(SB);
     std::vector<Key> h_res(SB);
     std::vector<uint32_t> slow;
     for (uint32_t b0 = 0; b0 < n_snap; b0 += SB) {
         const uint32_t nb = (n_snap - b0) < SB ? (n_snap - b0) : SB;
-        if (!(fast && fl_sync == 0)) {
+        if (!fast) {
             for (uint32_t i = 0; i < nb; ++i) slow.push_back(b0 + i);
             continue;
         }
         CUDA_TRY(c->z_bw.ensure((size_t)SB * DD));
-        CUDA_TRY(c->z_mbw.ensure((size_t)SB * c->F));
         CUDA_TRY(c->z_flags.ensure(SB));
-        CUDA_TRY(c->z_tpk.ensure((size_t)SB * s_tpk));
-        CUDA_TRY(c->z_tcol.ensure((size_t)SB * s_tcol));
-        CUDA_TRY(c->z_xt.ensure((size_t)SB * s_xt));
         CUDA_TRY(c->z_res.ensure(SB));
-        CUDA_TRY(c->z_cnt.ensure(SB));
         CUDA_TRY(cudaMemcpyAsync(c->z_bw.p, bandwidth + (size_t)b0 * DD, (size_t)nb * DD * 8,
                                  cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemsetAsync(c->z_flags.p, 0, nb * sizeof(uint32_t), s));
-        CUDA_TRY(cudaMemsetAsync(c->z_cnt.p, 0, nb * sizeof(unsigned int), s));
-        SnapGeom Z;
-        Z.nsnap = (int)nb;
-        Z.bw = c->z_bw.p; Z.mbw = c->z_mbw.p; Z.flags = c->z_flags.p;
-        Z.tpk = c->z_tpk.p; Z.tcol = c->z_tcol.p; Z.xt = c->z_xt.p;
-        Z.s_tpk = s_tpk; Z.s_tcol = s_tcol; Z.s_xt = s_xt;
-        DevInst I = c->view();
-        k6_minbw<<<(unsigned)((nb * c->F + 127) / 128), 128, 0, s>>>(I, Z);
-        const long long work = (long long)(s_tpk + (size_t)c->nm * c->F * c->F * n);
-        dim3 pg((unsigned)((work + 255) / 256), nb);
-        k6_patch<<<pg, 256, 0, s>>>(I, Z);
-        CUDA_TRY(cudaGetLastError());
-        // sweep over (snapshot, item)
-        size_t smem0 = 16 + (((size_t)(n + 1) * (k + 1) * 8 + 15) & ~(size_t)15) + (size_t)c->ngroups * 16;
-        size_t smem1 = smem0 + ntri * 16 + (n + 1) * 16 + 3 * nxp * 8 + (size_t)n * 16;
-        size_t smem2 = smem1 + ntri * 16;
-        int mode = smem2 <= (size_t)c->smem_max ? 2 : (smem1 <= (size_t)c->smem_max ? 1 : 0);
-        if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
-        size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
-        SwFn kern = pick_sweep(mode, c->nb, k);
-        int per_sm = 0;
-        { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
-          if (st_ != GP_OK) return st_; }
-        unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
-        unsigned long long cpi = (items * nb) >= resident ? 1 : resident / (items * nb);
-        unsigned long long tasks = (c->sweep_W + 31) / 32;
-        unsigned long long cap = (tasks + (K3S_THREADS / 32) - 1) / (K3S_THREADS / 32);
-        if (cpi > cap) cpi = cap;
-        if (cpi < 1) cpi = 1;
-        unsigned long long grid = (unsigned long long)nb * items * cpi;
-        if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "snapshot batch too large");
-        SweepGeom G;
-        G.b0 = 0;
-        G.k = k; G.nbm = c->nb * c->nm; G.NC = NC; G.NP = NP; G.item0 = 0; G.cpi = cpi;
-        G.W = c->sweep_W; G.ngroups = c->ngroups; G.groups = c->groups.p;
-        G.prefixes = c->prefixes.p;
-        G.bnk = c->bnk.p;
-        G.gsteps = 1;
-        while (G.gsteps * 2 <= c->ngroups) G.gsteps *= 2;
-        G.items = (unsigned int)items;
-        G.tpk = c->z_tpk.p; G.tcol = c->z_tcol.p; G.xt = c->z_xt.p;
-        G.s_tpk = s_tpk; G.s_tcol = s_tcol; G.s_xt = s_xt;
-        CUDA_TRY(c->item_ctr.ensure((size_t)nb * items));
-        CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, (size_t)nb * items * sizeof(unsigned int), s));
-        G.item_ctr = c->item_ctr.p;
-        CUDA_TRY(c->blk.ensure(grid > 4096 ? grid : 4096));
-        ArgminScratch S;
-        S.blk = c->blk.p;
-        S.counter = c->z_cnt.p;
-        S.result = c->z_res.p;
-        S.err = nullptr;
-        S.err_idx = c->err_idx.p;
-        CUDA_TRY(launch_sweep_kernel(kern, (unsigned)grid, smem, s, G, I, S, c->binom.p,
-                                     c->z_flags.p));
-        CUDA_TRY(cudaGetLastError());
+        int st = snap_enqueue(c, c->z_bw.p, nb, c->z_res.p, c->z_flags.p, b0);
+        if (st != GP_OK) return st;
         CUDA_TRY(cudaMemcpyAsync(h_res.data(), c->z_res.p, nb * sizeof(Key), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaMemcpyAsync(h_fl.data(), c->z_flags.p, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -1916,15 +2014,15 @@ int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_
     }
     if (!slow.empty()) {
         // exact status-tracking path, one snapshot at a time on the context
-        std::vector<double> base((size_t)DD);
-        CUDA_TRY(cudaMemcpyAsync(base.data(), c->bw.p, DD * 8, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
+        const VerifySink vs0 = c->vs;
         for (uint32_t sn : slow) {
             int st = gp_set_bandwidth(c, bandwidth + (size_t)sn * DD);
+            c->vs.lo = vs0.lo - (unsigned long long)sn * total;  // snapshot sn's slots
             if (st == GP_OK) st = gp_argmin_range(c, 0, total, &out[sn]);
             status[sn] = st;
         }
-        int st = gp_set_bandwidth(c, base.data());
+        c->vs = vs0;
+        int st = gp_reset_bandwidth(c);
         if (st != GP_OK) return st;
     }
     return GP_OK;
@@ -2033,6 +2131,41 @@ int gp_plan_cost(gp_ctx* c, uint32_t k, const gp_plan_stage* stages, int64_t bat
     CUDA_TRY(cudaMemcpyAsync(&st, b + o_stat, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (st != GP_OK) return fail(st, "build_plan_timing raised (status %d)", st);
+    return GP_OK;
+}
+
+// Parity tests: from now on every K3 / K6 launch (sweep, sub-range tile
+// kernel, generic kernel, the gp_replan graph, snapshot batches) uses the
+// verify instantiation and stores each evaluated candidate's cost at global
+// position g = snapshot * space_size + enumeration index, for g in
+// [lo, lo + n).  Unwritten slots keep an all-ones NaN pattern.
+int gp_diag_verify_begin(gp_ctx* c, uint64_t lo, uint64_t n) {
+    if (!c || !c->loaded || n == 0) return fail(GP_ERR_INPUT, "context not loaded / empty sink");
+    CUDA_TRY(cudaSetDevice(c->device));
+    uint64_t total;
+    { int st_ = gp_space_size(c, &total); if (st_ != GP_OK) return st_; }
+    CUDA_TRY(c->vbuf.ensure(n));
+    CUDA_TRY(cudaMemsetAsync(c->vbuf.p, 0xFF, n * sizeof(double), c->stream));
+    c->vs.out = c->vbuf.p;
+    c->vs.lo = lo;
+    c->vs.n = n;
+    c->vs.stride = total;
+    c->verify = true;
+    if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+    return GP_OK;
+}
+
+// Ends verify mode and copies the sink (n doubles) to host memory `out`.
+int gp_diag_verify_end(gp_ctx* c, double* out) {
+    if (!c || !c->verify) return fail(GP_ERR_INPUT, "verify mode not active");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const uint64_t n = c->vs.n;
+    c->verify = false;
+    c->vs = VerifySink();
+    if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+    if (out) CUDA_TRY(cudaMemcpyAsync(out, c->vbuf.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                      c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
     return GP_OK;
 }
 

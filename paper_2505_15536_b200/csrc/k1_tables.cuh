@@ -5,7 +5,7 @@
 // ---- K1a: interval sums -----------------------------------------------------
 // sum(model.layers[i].<field> for i in range(a, b)) for every 0 <= a < b <= n,
 // each interval summed from its own start (never prefix differences).
-__device__ void k1_intervals_block(const DevInst& I, int col) {
+static __device__ void k1_intervals_block(const DevInst& I, int col) {
     // one CTA per column; the column is staged in shared memory so the
     // sequential Neumaier sweeps read on-chip values.  S is stored
     // transposed (b-major, see Ssum), so the lanes of a warp (consecutive a)
@@ -68,7 +68,7 @@ __device__ __forceinline__ double block_min128(double v, double* red) {
 // boundary; a bisection over the ordered bit patterns covers what the walk
 // cannot (non-finite estimate, > 64 steps).  *ok = false where the monotone
 // argument does not apply (the caller keeps the member loop).
-__device__ __noinline__ double tp_threshold_bisect(double rf, double cf, double mem) {
+static __device__ __noinline__ double tp_threshold_bisect(double rf, double cf, double mem) {
     auto key = [](double d) -> unsigned long long {
         const unsigned long long u = (unsigned long long)__double_as_longlong(d);
         return (u >> 63) ? ~u : (u | (1ull << 63));
@@ -86,7 +86,7 @@ __device__ __noinline__ double tp_threshold_bisect(double rf, double cf, double 
     return unkey(lo);
 }
 
-__device__ double tp_threshold(double rf, double cf, double mem, bool* ok) {
+static __device__ double tp_threshold(double rf, double cf, double mem, bool* ok) {
     *ok = rf > 0.0 && rf < INFINITY && cf > 0.0 && cf < INFINITY;
     if (!*ok) return 0.0;
     auto accept = [&](double P) { return !(((P * rf) * cf) > mem); };
@@ -113,7 +113,7 @@ __device__ double tp_threshold(double rf, double cf, double mem, bool* ok) {
 // (one isclose per thread, block AND) and divides the fractions in parallel;
 // only the short Neumaier sums run on one thread.  Ends with the packed
 // K1Grp record phase 2 reads.
-__device__ void k1_group_block(const DevInst& I, int f) {
+static __device__ void k1_group_block(const DevInst& I, int f) {
     __shared__ double caps[GP_MAX_MEMBERS];
     __shared__ double memv[GP_MAX_MEMBERS];
     __shared__ double red[4];
@@ -246,7 +246,7 @@ __device__ void k1_group_block(const DevInst& I, int f) {
 
 // recompute min_intra_bandwidth over member pairs (bandwidth snapshots;
 // src/grouping.py:69-75 on the rebuilt topology)
-__global__ void k1_minbw(DevInst I, double* out) {
+static __global__ void k1_minbw(DevInst I, double* out) {
     int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= I.F) return;
     int m0 = I.fg_off[f], m1 = I.fg_off[f + 1];
@@ -263,7 +263,7 @@ __global__ void k1_minbw(DevInst I, double* out) {
 
 // split choice for one (group, layer range): choose_intra_split
 // (src/planner.py:157-200).  Writes PP shares when kind == ASYM_PP.
-__device__ __noinline__ int choose_split(const DevInst& I, int f, int a, int b, int* shares,
+static __device__ __noinline__ int choose_split(const DevInst& I, int f, int a, int b, int* shares,
                                          int* nparts) {
     int nmem = I.fg_off[f + 1] - I.fg_off[f];
     int s0 = I.fg_sg_off[f], nsg = I.fg_sg_off[f + 1] - s0;
@@ -291,7 +291,7 @@ __device__ __noinline__ int choose_split(const DevInst& I, int f, int a, int b, 
 // ---- K1c: stage table, generic path ---------------------------------------------
 // Generic stage entry (any number of second-level groups): the reference
 // order step by step, reading group data from global memory.
-__device__ __noinline__ void k1_stage_generic(const DevInst& I, int f, int a, int b, size_t e) {
+static __device__ __noinline__ void k1_stage_generic(const DevInst& I, int f, int a, int b, size_t e) {
 #if defined(GP_TIMELINE)
     const unsigned long long tt0 = tl_now();
 #endif
@@ -436,7 +436,7 @@ __device__ __forceinline__ int prop_split2(int total, double w0, double w1, int&
 // five interval sums, the micro-batch sizes), keeps the split in registers
 // and stores last, so a thread waits on two round trips instead of a chain of
 // dependent ones; the arithmetic is the generic path's, operation by operation.
-__device__ void k1_stage_t(const DevInst& I, long long t, const double* md_s) {
+static __device__ void k1_stage_t(const DevInst& I, long long t, const double* md_s) {
     const int n = I.n;
     const int N1 = n + 1, NN = N1 * N1;
     if (t >= (long long)I.F * NN) return;
@@ -577,7 +577,7 @@ __device__ void k1_stage_t(const DevInst& I, long long t, const double* md_s) {
 // ---- K1d: gateways and boundary transfer table -------------------------------------
 // gateway_link (src/timing.py:104-113): argmin over (p_t, u, v) with string
 // order of ids, u in the upstream group, v in the downstream group.
-__device__ void k1_gateway_warp(const DevInst& I, int warp, int lane) {
+static __device__ void k1_gateway_warp(const DevInst& I, int warp, int lane) {
     // one warp per ordered pair (fa, fb); lanes scan member pairs, then a
     // warp argmin on the key (p_t, rank(u), rank(v))
     const int fa = warp / I.F, fb = warp % I.F;
@@ -609,7 +609,7 @@ __device__ void k1_gateway_warp(const DevInst& I, int warp, int lane) {
     if (lane == 0) I.gw[warp] = (int)(bu * I.D + bv);
 }
 
-__global__ void k1_gateways(DevInst I) {
+static __global__ void k1_gateways(DevInst I) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (warp < I.F * I.F) k1_gateway_warp(I, warp, threadIdx.x & 31);
 }
@@ -621,7 +621,7 @@ __device__ void k1_gateway_warp(const DevInst& I, int warp, int lane);
 
 // gp_replan graph head: instance arena host -> device by loads from the
 // mapped pinned staging buffer (16 B per thread, grid-stride)
-__global__ void k_arena_pull(const uint4* __restrict__ src, uint4* __restrict__ dst,
+static __global__ void k_arena_pull(const uint4* __restrict__ src, uint4* __restrict__ dst,
                              unsigned long long n16) {
     TL_START();
     pdl_trigger();
@@ -639,7 +639,7 @@ struct K1Reset {
     unsigned int n_items;
 };
 
-__global__ void __launch_bounds__(128) k1_phase1(DevInst I, K1Reset R) {
+static __global__ void __launch_bounds__(128) k1_phase1(DevInst I, K1Reset R) {
     const int b = blockIdx.x;
     TL_START();
     pdl_trigger();  // phase 2 may be scheduled now (it waits for this grid)
@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(128) k1_phase1(DevInst I, K1Reset R) {
 #endif
 }
 
-__device__ void k1_boundary_t(const DevInst& I, long long t) {
+static __device__ void k1_boundary_t(const DevInst& I, long long t) {
     long long total = (long long)I.nm * I.F * I.F * I.n;
     if (t >= total) return;
     int j = (int)(t % I.n);
@@ -687,7 +687,7 @@ __device__ void k1_boundary_t(const DevInst& I, long long t) {
 }
 
 // K1 phase 2 in one launch: stage table entries, then boundary x entries
-__global__ void k1_phase2(DevInst I, long long n_stage) {
+static __global__ void k1_phase2(DevInst I, long long n_stage) {
     TL_START();
     pdl_trigger();
     pdl_wait();  // phase 1's interval sums, group constants and gateways

@@ -11,7 +11,7 @@ struct EvalOut {
 };
 
 // p[0..k] are cut positions (p[0] = 0); order[s] group of stage s.
-__device__ EvalOut eval_tables(const DevInst& I, int k, const uint8_t* order, const int* p,
+static __device__ EvalOut eval_tables(const DevInst& I, int k, const uint8_t* order, const int* p,
                                int mi, long long M) {
     int n = I.n;
     size_t N2 = (size_t)(n + 1) * (n + 1);
@@ -78,7 +78,7 @@ __device__ __forceinline__ double eval_fast(const DevInst& I, const uint8_t* o, 
     return best;
 }
 
-__global__ void k2_eval_batch(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
+static __global__ void k2_eval_batch(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
                               const uint8_t* __restrict__ counts, const uint8_t* __restrict__ bm,
                               double* __restrict__ cost, uint8_t* __restrict__ status) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) k2_eval_batch_sc(DevInst I, long long nca
 #ifndef K2Q_MINB
 #define K2Q_MINB 1
 #endif
-__global__ void __launch_bounds__(K2Q_THREADS, K2Q_MINB) k2_eval_batch_q4(DevInst I, long long ncand,
+static __global__ void __launch_bounds__(K2Q_THREADS, K2Q_MINB) k2_eval_batch_q4(DevInst I, long long ncand,
                                                                 const uint8_t* __restrict__ order,
                                                                 const uint8_t* __restrict__ counts,
                                                                 const uint8_t* __restrict__ bm,

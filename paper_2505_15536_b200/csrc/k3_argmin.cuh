@@ -16,7 +16,7 @@
 //     stage k-1 = [q, n)        column of group order[k-1]
 // MODE 2: T1 and T2 triangles, the column and both boundary rows in shared
 // memory; MODE 1: T1 from L1/L2; MODE 0: everything from L1/L2.
-template <int MODE, int NB>
+template <int MODE, int NB, bool VER = false>
 __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k3_argmin(DevInst I, RangeGeom G, ArgminScratch S,
                                                            const unsigned long long* __restrict__ binom,
                                                            const uint32_t* skip_if_flags) {
@@ -205,6 +205,8 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k3_argmin(DevInst I, Rang
                         double c = (k > 3) ? gtsel(t1, mx[bi]) : t1;
                         c = gtsel(t2, c);
                         c = gtsel(t3, c);
+                        if constexpr (VER)
+                            vput(G.vs, 0, (((unsigned long long)bi * I.nm + mi) * G.NP + perm_rank) * G.NC + rabs, c);
                         unsigned long long tk = rabs * NB + bi;
                         if (c < best_c || (c == best_c && tk < best_t)) { best_c = c; best_t = tk; }
                     }
@@ -258,6 +260,7 @@ struct SweepGeom {
     int csize;                      // thread-block cluster size (CTAs of one item), 1 = none
     int interleave;                 // CTA -> item map: 1 = item-minor (b % items), 0 = item-major
     int b0;                         // first batch index of the NB evaluated together
+    VerifySink vs;                  // parity tests only (VER instantiations)
 };
 
 #if defined(K3_PROFILE)
@@ -265,7 +268,7 @@ __device__ __forceinline__ unsigned __nv_smid_k3() { unsigned r; asm volatile("m
 #endif
 // KS > 0 fixes the stage count at compile time (cut arrays in registers,
 // no local memory); KS = 0 is the generic kernel.
-template <int MODE, int NB, int KS>
+template <int MODE, int NB, int KS, bool VER = false>
 __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, SweepGeom G, ArgminScratch S,
                                                           const unsigned long long* __restrict__ binom,
                                                           const uint32_t* skip_if_flags) {
@@ -497,6 +500,10 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
                 double t3 = ((fill3 + Mv[bi] * e3.x) + res3) + e3.y;
                 double c = gtsel(t2, mx1[bi]);
                 c = gtsel(t3, c);
+                if constexpr (VER)
+                    vput(G.vs, snap,
+                         ((((unsigned long long)(G.b0 + bi) * I.nm + mi) * G.NP + perm_rank) * G.NC) +
+                             rpre + (unsigned long long)(q0 + i - a - 1), c);
                 if (bi == 0 || c < cmin) { cmin = c; bmin = bi; }
             }
         };
@@ -553,7 +560,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
 
 // Tile table: cut positions p[1..k-1] (u8) of every K3_TILE-th composition
 // rank (16-byte records); depends on (n, k) only.
-__global__ void k_tiles(int n, int k, unsigned long long ntiles, uint8_t* out) {
+static __global__ void k_tiles(int n, int k, unsigned long long ntiles, uint8_t* out) {
     unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles) return;
     int p[GP_MAX_STAGES + 1];
@@ -564,7 +571,7 @@ __global__ void k_tiles(int n, int k, unsigned long long ntiles, uint8_t* out) {
 
 // Generic range kernel (status-tracking): one thread per index; records the
 // first erroring candidate in enumeration order.
-__global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G, ArgminScratch S,
+static __global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G, ArgminScratch S,
                                                          const uint32_t* only_if_flags) {
     // fix-up launch behind a fast-path kernel: do nothing unless the table
     // build raised a flag (then this kernel's result replaces the fast one)
@@ -594,6 +601,9 @@ __global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G,
         int mi = bmi % I.nm;
         long long M = I.batch[bmi / I.nm] / I.micro[mi];
         EvalOut e = eval_tables(I, G.k, order, p, mi, M);
+        if (G.vs.out)
+            vput(G.vs, 0, idx, e.status != GP_OK
+                 ? __longlong_as_double(0x7ff8000000000000ll | (long long)e.status) : e.cost);
         if (e.status != GP_OK) {
             atomicMin(S.err_idx, (idx << 4) | (unsigned long long)e.status);
         } else {
@@ -605,7 +615,7 @@ __global__ void __launch_bounds__(256) k3_argmin_generic(DevInst I, RangeGeom G,
 }
 
 // r[0] = the smallest of the keys r[0..n) (range split into launches)
-__global__ void k_key_combine(Key* r, int n) {
+static __global__ void k_key_combine(Key* r, int n) {
     Key b = r[0];
     for (int i = 1; i < n; ++i) if (key_less(r[i], b)) b = r[i];
     r[0] = b;

@@ -1,15 +1,21 @@
-"""Multi-GPU exhaustive re-plan: item sharding + a 16-byte tuple arg-min.
+"""Multi-GPU re-planning: candidates and snapshots sharded over ranks.
 
 One process per GPU (torch.distributed; NCCL on B200s, gloo for the CPU
-tests).  The exhaustive space of `exhaustive_plan` (src/planner.py:389-392)
-is partitioned into (micro-batch, stage order) ITEMS, each covering every
-batch size and every layer cut; rank r evaluates the contiguous item range
-``shard_items(n_items, world, r)`` on its own GPU (K3 sweep) with no
-data-path communication.  The only exchange is the final arg-min of one
-``(cost bits, tie)`` pair per rank, where ``tie`` orders candidates exactly
-as the reference's key ``(cost, (order, cuts))`` with earliest-(b, m)
-tie-break does: non-negative doubles and +inf order like
-their IEEE bit patterns, so the pair compares as two int64.
+tests); the units shard with no data-path communication:
+
+* one exhaustive re-plan (`exhaustive_plan`, src/planner.py:389-392): the
+  space is partitioned into (micro-batch, stage order) ITEMS, each covering
+  every batch size and every layer cut; rank r sweeps the contiguous item
+  range ``shard_items(n_items, world, r)`` on its own GPU (K3).  The only
+  exchange is the final arg-min of one ``(first error, cost bits, tie)``
+  triple per rank, where ``tie`` orders candidates exactly as the
+  reference's key ``(cost, (order, cuts))`` with earliest-(b, m) tie-break
+  does: non-negative doubles and +inf order like their
+  IEEE bit patterns, so the key compares as int64s.  An erroring candidate
+  on any rank makes every rank raise the error with the smallest index;
+* a batch of bandwidth snapshots (the adapter's re-planning loop): snapshot
+  j goes to the rank whose contiguous shard holds j (K6 per rank); the
+  per-snapshot records (cost bits, winner index, status) are all-gathered.
 """
 
 from __future__ import annotations
@@ -60,31 +66,113 @@ def _bits_cost(bits: int) -> float:
     return struct.unpack("<d", struct.pack("<q", bits))[0]
 
 
-def reduce_key(key: Tuple[float, int], group=None, device=None) -> Tuple[float, int]:
-    """All-gather one (cost, tie) per rank and return the global minimum."""
+NO_ERR = (1 << 63) - 1
+
+
+def reduce_key(key: Tuple[float, int], group=None, device=None, err=None) -> Tuple[float, int]:
+    """All-gather one (cost, tie) per rank - plus its first error, if any -
+    and return the global minimum key.  When any rank met an erroring
+    candidate, every rank raises the error of the smallest enumeration index
+    (the one the reference's sequential loop meets first,
+    src/planner.py:389-399), so no rank is left waiting in a collective."""
     import torch
     import torch.distributed as dist
+    ek = NO_ERR if err is None else (int(err[0]) << 4) | int(err[1])
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
-        return key
-    t = torch.tensor([_cost_bits(key[0]), key[1]], dtype=torch.int64, device=device)
-    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(out, t, group=group)
-    keys = [(int(o[0]), int(o[1])) for o in out]
-    bits, tie = min(keys)
+        keys = [(ek, _cost_bits(key[0]), key[1])]
+    else:
+        t = torch.tensor([ek, _cost_bits(key[0]), key[1]], dtype=torch.int64, device=device)
+        out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(out, t, group=group)
+        keys = [(int(o[0]), int(o[1]), int(o[2])) for o in out]
+    e = min(k[0] for k in keys)
+    if e != NO_ERR:
+        from . import abi
+        abi.raise_for(e & 15, f"candidate {e >> 4} raises status {e & 15}")
+    bits, tie = min((k[1], k[2]) for k in keys)
     return _bits_cost(bits), tie
 
 
-def sharded_argmin(evaluate_items: Callable[[int, int], Tuple[float, int]], n_items: int,
+def sharded_argmin(evaluate_items: Callable[[int, int], tuple], n_items: int,
                    group=None, device=None) -> Tuple[float, int]:
     """Global (cost, tie) arg-min; ``evaluate_items(lo, hi)`` is this rank's
-    local arg-min over items [lo, hi) (the engine on a GPU, the oracle in
-    CPU tests)."""
+    local arg-min over items [lo, hi) as ``(cost, tie)`` or ``(cost, tie,
+    err)`` with ``err = (first erroring index, status)`` or None (the engine
+    on a GPU, the oracle in CPU tests)."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     lo, hi = shard_items(n_items, world, rank)
-    key = evaluate_items(lo, hi) if hi > lo else NO_KEY
-    return reduce_key(key, group, device)
+    r = evaluate_items(lo, hi) if hi > lo else NO_KEY
+    key, err = (r[0], r[1]), (r[2] if len(r) > 2 else None)
+    return reduce_key(key, group, device, err)
+
+
+def gather_snapshot_records(local: np.ndarray, n_total: int, group=None, device=None) -> np.ndarray:
+    """All-gather the per-snapshot records ``[n_local, 3]`` int64 (cost bits,
+    enumeration index, status) of contiguous snapshot shards into the full
+    ``[n_total, 3]`` table on every rank."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return local
+    world = dist.get_world_size(group)
+    width = -(-n_total // world)
+    buf = torch.zeros((width, 3), dtype=torch.int64, device=device)
+    if local.shape[0]:
+        buf[:local.shape[0]] = torch.from_numpy(np.ascontiguousarray(local)).to(device)
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    rows = []
+    for r in range(world):
+        lo, hi = shard_items(n_total, world, r)
+        rows.append(out[r][:hi - lo].cpu().numpy())
+    return np.concatenate(rows) if rows else local
+
+
+def replan_snapshots_sharded(model, topology, groups, config, bandwidths: np.ndarray,
+                             engine=None, group=None):
+    """Exact re-plan per bandwidth snapshot (replan.replan_snapshots), the
+    snapshots partitioned by index over the ranks of ``group`` (contiguous
+    shards); every rank returns the full list, one
+    ``(cost, order_ids, counts, b, m)`` tuple or exception per snapshot."""
+    import torch
+    import torch.distributed as dist
+    from . import abi
+    from .engine import default_engine
+    from .layout import packed_instance
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    packed = packed_instance(model, topology, groups, config.bottleneck_factor)
+    eng = (engine or default_engine(torch.cuda.current_device())).load(packed)
+    S = bandwidths.shape[0]
+    lo, hi = shard_items(S, world, rank)
+    rec = np.zeros((hi - lo, 3), dtype=np.int64)
+    if hi > lo:
+        bests, status = eng.replan_snapshots(bandwidths[lo:hi])
+        for i in range(hi - lo):
+            rec[i] = (_cost_bits(bests[i].cost), int(bests[i].index), int(status[i]))
+    allrec = gather_snapshot_records(rec, S, group, torch.device("cuda"))
+    return decode_snapshot_records(packed, allrec)
+
+
+def decode_snapshot_records(packed, rec: np.ndarray):
+    """Per-snapshot records -> ``(cost, order_ids, counts, b, m)`` or the
+    exception the reference would raise (replan.replan_snapshots format)."""
+    from . import abi
+    k, n = packed.n_fgs, packed.n_layers
+    NC, NP, _ = space_dims(n, k, len(packed.batches), len(packed.micros))
+    nbm = len(packed.batches) * len(packed.micros)
+    nm = len(packed.micros)
+    out = []
+    for j, (bits, index, st) in enumerate(rec.tolist()):
+        if st != abi.GP_OK:
+            out.append(abi._ERRORS.get(st, D.GeopipeError)(f"snapshot {j}: status {st}"))
+            continue
+        order, counts, bm = decode_candidate(tie_of_index(index, NC, NP, nbm), NC, NP, nbm, n, k)
+        out.append((_bits_cost(bits), [packed.fg_ids[f] for f in order], counts,
+                    packed.batches[bm // nm], packed.micros[bm % nm]))
+    return out
 
 
 def decode_candidate(tie: int, NC: int, NP: int, nbm: int, n_layers: int, k: int):
@@ -119,9 +207,9 @@ def exhaustive_plan_sharded(model, topology, groups, config, engine=None, group=
     same SearchResult (the reference's, bit for bit)."""
     import torch
     from .engine import default_engine
-    from .layout import PackedInstance
+    from .layout import packed_instance
     from .planner import assemble
-    packed = PackedInstance(model, topology, groups, config.bottleneck_factor)
+    packed = packed_instance(model, topology, groups, config.bottleneck_factor)
     eng = (engine or default_engine(torch.cuda.current_device())).load(packed)
     k = packed.n_fgs
     NC, NP, n_items = space_dims(packed.n_layers, k, len(packed.batches), len(packed.micros))
@@ -130,8 +218,13 @@ def exhaustive_plan_sharded(model, topology, groups, config, engine=None, group=
         raise D.NoFeasiblePlanError("no feasible plan in exhaustive sweep")
 
     def local(lo, hi):
-        b = eng.argmin_items(lo, hi)
-        return b.cost, tie_of_index(b.index, NC, NP, nbm)
+        from . import abi
+        st, b, msg = eng.argmin_items_status(lo, hi)
+        if st == abi.GP_OK:
+            return b.cost, tie_of_index(b.index, NC, NP, nbm), None
+        if st == abi.GP_ERR_NO_FEASIBLE:  # empty item range
+            return NO_KEY[0], NO_KEY[1], None
+        return NO_KEY[0], NO_KEY[1], (int(b.index), st)
 
     cost, tie = sharded_argmin(local, n_items, group, device=torch.device("cuda"))
     order, counts, bm = decode_candidate(tie, NC, NP, nbm, packed.n_layers, k)

@@ -60,6 +60,9 @@ def lib():
         L.gp_replan.argtypes = [vp, P(abi.GpInstance), P(abi.GpBest), P(abi.GpPlanInfo)]
         L.gp_group_splits.argtypes = [vp, C.c_uint32, P(abi.GpGroupInfo)]
         L.gp_set_bandwidth.argtypes = [vp, P(C.c_double)]
+        L.gp_reset_bandwidth.argtypes = [vp]
+        L.gp_diag_verify_begin.argtypes = [vp, C.c_uint64, C.c_uint64]
+        L.gp_diag_verify_end.argtypes = [vp, P(C.c_double)]
         L.gp_diag_fp64_peak.argtypes = [C.c_int, P(C.c_double)]
         L.gp_sim_1f1b.argtypes = [vp, vp, C.c_uint64, C.c_uint32, P(C.c_double), u8p]
         L.gp_sim_1f1b_device.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp]
@@ -86,6 +89,7 @@ def lib():
                                      P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double)]
         L.gp_replan_snapshots.argtypes = [vp, P(C.c_double), C.c_uint32, P(abi.GpBest),
                                           P(C.c_int32)]
+        L.gp_replan_snapshots_async.argtypes = [vp, vp, C.c_uint32, vp, vp]
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
@@ -205,6 +209,19 @@ class Engine:
         best = abi.GpBest()
         _check(lib().gp_argmin_fetch(self._h, C.byref(best)))
         return best
+
+    def argmin_fetch_status(self):
+        """(status, GpBest, message) without raising: on a per-candidate
+        error, GpBest.index is the first erroring candidate's index."""
+        best = abi.GpBest()
+        st = lib().gp_argmin_fetch(self._h, C.byref(best))
+        msg = lib().gp_last_error().decode(errors="replace") if st else ""
+        return st, best, msg
+
+    def argmin_items_status(self, item_lo: int, item_hi: int):
+        """argmin_items without raising (multi-GPU shards): (status, GpBest, message)."""
+        _check(lib().gp_argmin_items_async(self._h, int(item_lo), int(item_hi)))
+        return self.argmin_fetch_status()
 
     def plan_detail(self, order, counts, bm: int) -> abi.GpPlanInfo:
         o = np.ascontiguousarray(order, dtype=np.uint8)
@@ -407,6 +424,13 @@ class Engine:
                                              out, st.ctypes.data_as(C.POINTER(C.c_int32))))
         return out, st
 
+    def replan_snapshots_async(self, d_bandwidth: int, n_snap: int, d_keys: int,
+                               d_flags: int) -> None:
+        """Device pointers (ints), asynchronous on :attr:`stream`: per snapshot
+        the arg-min key (cost bits, tie) -> d_keys[2i:2i+2] (int64) and the
+        table flags -> d_flags[i] (gp_replan_snapshots_async)."""
+        _check(lib().gp_replan_snapshots_async(self._h, d_bandwidth, int(n_snap), d_keys, d_flags))
+
     def set_k3_mode(self, mode: int) -> None:
         """Force the exhaustive-kernel variant (-1 auto, 0/1/2, 3 generic)."""
         _check(lib().gp_ctx_set_k3_mode(self._h, int(mode)))
@@ -428,6 +452,22 @@ class Engine:
     def set_bandwidth(self, bw: np.ndarray) -> None:
         a = np.ascontiguousarray(bw, dtype=np.float64)
         _check(lib().gp_set_bandwidth(self._h, a.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def reset_bandwidth(self) -> None:
+        """Back to the loaded instance's bandwidths and min_intra_bandwidth values."""
+        _check(lib().gp_reset_bandwidth(self._h))
+
+    def verify_begin(self, lo: int, n: int) -> None:
+        """Parity tests: record every evaluated candidate's cost at global
+        position g - lo (g = snapshot * space_size + index, lo <= g < lo + n)
+        until :meth:`verify_end` (gp_diag_verify_begin)."""
+        self._verify_n = int(n)
+        _check(lib().gp_diag_verify_begin(self._h, int(lo), int(n)))
+
+    def verify_end(self) -> np.ndarray:
+        out = np.empty(self._verify_n, dtype=np.float64)
+        _check(lib().gp_diag_verify_end(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
 
 
 def fp64_peak(device: int = 0) -> float:

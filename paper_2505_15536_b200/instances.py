@@ -144,6 +144,28 @@ def config(name: str, jitter: bool = False) -> InstanceSpec:
     raise KeyError(name)
 
 
+def many_group_config(k: int, n: int, seed: int, batches=(64, 128), micros=(8, 16),
+                      jitter: bool = True) -> InstanceSpec:
+    """k-region instances (k first-level groups) for the k >= 5 regime where
+    the exhaustive space C(n-1, k-1) * k! explodes: each region holds one or
+    two tiers of 1-2 devices (random p_c / memory), random intra-region
+    bandwidth and latency, 100 Mb/s cross-region links at 30 ms."""
+    rng = random.Random(seed)
+    regions = []
+    for _ in range(k):
+        tiers = [[(rng.choice([3.5e13, 7.1e13, 1.65e14, 9.89e14]), rng.choice([8e9, 24e9, 80e9]))]
+                 * rng.randint(1, 2)]
+        if rng.random() < 0.5:
+            tiers.append([(rng.choice([2.0e13, 3.12e14]), 24e9)])
+        regions.append(tiers)
+    layers = transformer_layers(n, 2048, 5504, 1024, 32000, d_kv=2048,
+                                jitter_seed=seed if jitter else None)
+    return InstanceSpec(f"k{k}n{n}s{seed}", layers, tuple(batches), tuple(micros), regions,
+                        intra_bw=[rng.uniform(1e9, 5e10) for _ in range(k)],
+                        intra_lat=[rng.uniform(1e-5, 1e-3) for _ in range(k)],
+                        cross_bw=1.25e7, cross_lat=0.03, jitter_seed=seed)
+
+
 def snapshot_multipliers(spec: InstanceSpec, j: int) -> Dict[Tuple[str, str], float]:
     """C3 snapshot ``j``: bandwidth multiplier per unordered device pair.
 

@@ -22,6 +22,7 @@ to HBM (and what the test-only oracle consumes).
 from __future__ import annotations
 
 import ctypes as C
+from collections import OrderedDict
 from typing import Dict, List
 
 import numpy as np
@@ -32,6 +33,29 @@ from . import domain as D
 
 def _ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(C.POINTER(ctype))
+
+
+_CACHE: "OrderedDict[tuple, PackedInstance]" = OrderedDict()
+_CACHE_SIZE = 16
+
+
+def packed_instance(model, topology, groups, bottleneck_factor: float = 1.25) -> "PackedInstance":
+    """PackedInstance of a (model, topology, groups) triple, cached by object
+    identity.  The reference's inputs are frozen and shareable
+    (SURVEY.md §8(b)), so a triple seen before packs to the same arrays; the
+    cache holds strong references, so an id is never reused while cached.
+    This is what makes repeated drop-in calls on the same objects (the
+    planner's and the adapter's re-plan loop) cost microseconds on the host."""
+    key = (id(model), id(topology), id(groups), float(bottleneck_factor))
+    hit = _CACHE.get(key)
+    if hit is not None and hit.model is model and hit.topology is topology and hit.groups is groups:
+        _CACHE.move_to_end(key)
+        return hit
+    p = PackedInstance(model, topology, groups, bottleneck_factor)
+    _CACHE[key] = p
+    while len(_CACHE) > _CACHE_SIZE:
+        _CACHE.popitem(last=False)
+    return p
 
 
 class PackedInstance:
@@ -77,13 +101,19 @@ class PackedInstance:
         self.p_t = np.zeros((Dn, Dn), dtype=np.float64)
         self.lat = np.zeros((Dn, Dn), dtype=np.float64)
         self.bw = np.zeros((Dn, Dn), dtype=np.float64)
-        for key, info in topology.links.items():
-            u, v = tuple(key)
-            i, j = dev_index[u], dev_index[v]
-            for (a, b) in ((i, j), (j, i)):
-                self.p_t[a, b] = info.metric.p_t
-                self.lat[a, b] = info.latency_seconds
-                self.bw[a, b] = info.bandwidth_bytes_per_s
+        links = topology.links
+        nl = len(links)
+        if nl:
+            ends = [tuple(k) for k in links]
+            infos = list(links.values())
+            ii = np.fromiter((dev_index[e[0]] for e in ends), np.intp, nl)
+            jj = np.fromiter((dev_index[e[-1]] for e in ends), np.intp, nl)
+            for mat, vals in ((self.p_t, (x.metric.p_t for x in infos)),
+                              (self.lat, (x.latency_seconds for x in infos)),
+                              (self.bw, (x.bandwidth_bytes_per_s for x in infos))):
+                v = np.fromiter(vals, np.float64, nl)
+                mat[ii, jj] = v
+                mat[jj, ii] = v
 
         # groups in sorted-id (string) order
         self.fg_ids: List[str] = sorted(groups.fgs)

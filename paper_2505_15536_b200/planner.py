@@ -30,7 +30,7 @@ import numpy as np
 from . import abi
 from . import domain as D
 from .engine import Engine, default_engine
-from .layout import PackedInstance
+from .layout import PackedInstance, packed_instance
 
 log = logging.getLogger(__name__)
 
@@ -179,7 +179,7 @@ def assemble(packed: PackedInstance, eng: Engine, order_idx, counts, bm: int, in
 
 def exhaustive_plan(model, topology, groups, config, engine: Engine = None) -> D.SearchResult:
     """GPU replacement for ``exhaustive_plan`` (src/planner.py:374-403)."""
-    packed = PackedInstance(model, topology, groups, config.bottleneck_factor)
+    packed = packed_instance(model, topology, groups, config.bottleneck_factor)
     eng = engine if engine is not None else default_engine()
     k, n = packed.n_fgs, packed.n_layers
     space = (len(packed.batches) * len(packed.micros) * math.factorial(k) *
@@ -205,7 +205,7 @@ def exhaustive_plan(model, topology, groups, config, engine: Engine = None) -> D
 
 def search_plan(model, topology, groups, config, engine: Engine = None) -> D.SearchResult:
     """GPU-batched replacement for ``search_plan`` (src/planner.py:330-371)."""
-    packed = PackedInstance(model, topology, groups, config.bottleneck_factor)
+    packed = packed_instance(model, topology, groups, config.bottleneck_factor)
     eng = _engine_for(packed, engine)
     fgs = sorted(groups.fgs.values(), key=lambda g: g.id)
     pairs = packed.bm_pairs()

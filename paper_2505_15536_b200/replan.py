@@ -20,7 +20,7 @@ import numpy as np
 from . import abi
 from . import domain as D
 from .engine import Engine, default_engine
-from .layout import PackedInstance
+from .layout import PackedInstance, packed_instance
 from .planner import assemble
 
 
@@ -50,7 +50,7 @@ def replan_snapshots(model, topology, groups, config, bandwidths: np.ndarray,
     topology returns them) or the tuple ``(cost, order_ids, counts, b, m)``;
     snapshots whose re-plan raises carry the exception instance instead.
     """
-    packed = PackedInstance(model, topology, groups, config.bottleneck_factor)
+    packed = packed_instance(model, topology, groups, config.bottleneck_factor)
     eng = (engine or default_engine()).load(packed)
     bests, status = eng.replan_snapshots(bandwidths)
     out: List = []
@@ -79,7 +79,7 @@ def replan_snapshots(model, topology, groups, config, bandwidths: np.ndarray,
             out.append(D.SearchResult(plan=plan, breakdown=breakdown, best_cost_trace=[b.cost],
                                       evaluated=int(b.evaluated)))
     if detail:
-        eng.set_bandwidth(packed.bw)
+        eng.reset_bandwidth()
     return out
 
 

@@ -17,7 +17,12 @@ Cases
                      tests/test_acceptance.py:_random_instance)
   err_*              error behaviour: all-infeasible memory, zero intra-group
                      bandwidth, zero-bandwidth gateway
-Usage: python scripts/make_golden.py [--skip-c4]
+  k5n9 .. k8n9       k = 5..8 stage groups (instances.many_group_config):
+                     every candidate's reference cost, exhaustive_plan, search
+  k5n24 .. k6n40     k = 5..8, larger spaces (up to 1.66e9 candidates, the
+                     K4 regime): a 2,000-candidate reference sample that pins
+                     the oracle on that instance, then the oracle's arg-min
+Usage: python scripts/make_golden.py [--skip-c4] [--only many:k5n9]
 """
 
 from __future__ import annotations
@@ -333,6 +338,74 @@ def dump_snapshots():
     print(f"snapshots: {time.time() - t0:.1f}s", flush=True)
 
 
+# k >= 5 stage groups (the regime exhaustive_plan hands to K4 above 5e8
+# candidates): small spaces with every candidate's reference cost, larger
+# ones with the pinned oracle's arg-min (pinned on a reference sample).
+MANY_SMALL = [("k5n9", 5, 9, 51, (64, 128), (8, 16)), ("k6n8", 6, 8, 61, (64, 128), (8, 16)),
+              ("k7n8", 7, 8, 71, (64, 128), (8,)), ("k8n9", 8, 9, 81, (64, 128), (16,))]
+MANY_BIG = [("k5n24", 5, 24, 100, (64, 128), (8, 16)), ("k6n20", 6, 20, 100, (64, 128), (8, 16)),
+            ("k7n16", 7, 16, 72, (64, 128), (8,)), ("k8n14", 8, 14, 82, (64, 128), (16,)),
+            ("k6n40", 6, 40, 100, (64, 128), (8, 16))]
+
+
+def _many_ref(k, n, seed, batches, micros):
+    spec = I.many_group_config(k, n, seed, batches, micros)
+    model, topo, groups = build_reference(spec)
+    assert len(groups.fgs) == k, (k, n, seed, len(groups.fgs))
+    return model, topo, groups
+
+
+def dump_many(which=None):
+    for name, k, n, seed, bs, ms in MANY_SMALL:
+        if which and name != which:
+            continue
+        model, topo, groups = _many_ref(k, n, seed, bs, ms)
+        dump_case(name, model, topo, groups, seeds=[0, 1])
+    from oracle import oracle as O
+    gp = geopipe()
+    from geopipe.planner import Candidate
+    for name, k, n, seed, bs, ms in MANY_BIG:
+        if which and name != which:
+            continue
+        model, topo, groups = _many_ref(k, n, seed, bs, ms)
+        doc = {"instance": G.instance_to_dict(model, topo, groups)}
+        packed = PackedInstance(model, topo, groups, 1.25)
+        total = O.space_size(packed)
+        idx = sorted(random.Random(seed).sample(range(total), 2000))
+        cfg = gp.SearchConfig(seed=0)
+        fg_ids = sorted(groups.fgs)
+        costs, stats = [], []
+        t = time.time()
+        for i in idx:
+            o, c, bm = O.decode(packed, i)
+            b = model.global_batch_candidates[bm // len(model.microbatch_candidates)]
+            m = model.microbatch_candidates[bm % len(model.microbatch_candidates)]
+            cand = Candidate(tuple(fg_ids[x] for x in o), tuple(int(x) for x in c))
+            cv, sv = ref_cost(model, topo, groups, cand, b, m, cfg)
+            st_o, v_o = O.evaluate(packed, o, c, bm)
+            assert st_o == sv and (sv != 0 or np.float64(v_o).view(np.uint64) ==
+                                   np.float64(cv).view(np.uint64)), (name, i)
+            costs.append(cv)
+            stats.append(sv)
+        doc["sample"] = {"index": idx, "cost": [G._f(x) for x in costs], "status": stats}
+        print(f"{name}: reference sample {time.time() - t:.1f}s (oracle pinned)", flush=True)
+        t = time.time()
+        st, best = O.argmin_range(packed, 0, total, threads=os.cpu_count())
+        doc["oracle_argmin"] = {"status": st, "cost": best.cost, "index": best.index,
+                                "order": list(best.order[:best.k]),
+                                "counts": list(best.counts[:best.k]),
+                                "batch_index": best.batch_index, "micro_index": best.micro_index,
+                                "evaluated": total,
+                                "cpu_seconds": time.time() - t, "threads": os.cpu_count()}
+        print(f"{name}: oracle argmin over {total} candidates {time.time() - t:.1f}s", flush=True)
+        doc["search"] = {}
+        for s_ in (0,):
+            doc["search"][str(s_)] = run_or_error(
+                lambda: gp.search_plan(model, topo, groups, gp.SearchConfig(seed=s_)))
+        doc["search_config"] = {"beam_width": 8, "max_iter": 20}
+        G.save(f"{name}.json", doc)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c4", action="store_true")
@@ -346,6 +419,9 @@ def main():
     import conftest as rc  # reference test fixtures (read-only import)
     os.makedirs(G.GOLDEN, exist_ok=True)
     if args.only:
+        if args.only.startswith("many:"):
+            dump_many(args.only[5:])
+            return
         globals()["dump_" + args.only]()
         return
     ap_only = args.only_sim

@@ -1,0 +1,64 @@
+"""torchrun worker for tests/test_multigpu.py (one rank per GPU, NCCL).
+
+Runs the sharded product paths on every rank and writes rank 0's answers to
+the JSON file named by argv[1]:
+  exhaustive  distributed.exhaustive_plan_sharded on golden cases
+  errors      the exception class every rank raised for erroring instances
+  snapshots   distributed.replan_snapshots_sharded over C3 snapshots of C2
+"""
+
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import golden_io as G
+    from cases import load_case
+    import paper_2505_15536_b200 as P
+    from paper_2505_15536_b200 import distributed as DI
+    from paper_2505_15536_b200 import instances as I
+    from paper_2505_15536_b200 import replan as R
+    from paper_2505_15536_b200.engine import Engine
+    from paper_2505_15536_b200.layout import PackedInstance
+    eng = Engine(local)
+    out = {"world": dist.get_world_size(), "exhaustive": {}, "errors": {}}
+    for name in ["c1j", "c2", "c2j", "rand10", "k5n9", "k6n8", "k8n9", "c4", "c4j"]:
+        doc, model, topo, groups = load_case(name)
+        res = DI.exhaustive_plan_sharded(model, topo, groups, P.SearchConfig(seed=0), engine=eng)
+        out["exhaustive"][name] = G.normalize_result(res)
+    for name in ["err_gateway", "err_intra_bw"]:
+        doc, model, topo, groups = load_case(name)
+        try:
+            DI.exhaustive_plan_sharded(model, topo, groups, P.SearchConfig(seed=0), engine=eng)
+            out["errors"][name] = None
+        except Exception as e:
+            out["errors"][name] = type(e).__name__
+    spec = I.config("c2")
+    model, topo, groups = I.build(spec)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    bws = R.bandwidth_matrices(packed, [I.snapshot_multipliers(spec, j) for j in range(37)])
+    res = DI.replan_snapshots_sharded(model, topo, groups, P.SearchConfig(seed=0), bws, engine=eng)
+    out["snapshots"] = [r if isinstance(r, tuple) else type(r).__name__ for r in res]
+    gathered = [None] * dist.get_world_size()
+    dist.all_gather_object(gathered, out)
+    if dist.get_rank() == 0:
+        out["all_ranks_equal"] = all(g == gathered[0] for g in gathered)
+        with open(sys.argv[1], "w") as f:
+            json.dump(out, f)
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,7 +1,5 @@
 """K4 branch-and-bound == exhaustive arg-min (same cost, same winner index)."""
 
-import random
-
 import pytest
 
 from cases import CASES_ALL, load_case
@@ -31,21 +29,7 @@ def test_bnb_equals_exhaustive_golden(engine, name):
 
 
 def _many_group_instance(k, n, seed, jitter=True):
-    rng = random.Random(seed)
-    regions = []
-    for r in range(k):
-        tiers = [[(rng.choice([3.5e13, 7.1e13, 1.65e14, 9.89e14]), rng.choice([8e9, 24e9, 80e9]))]
-                 * rng.randint(1, 2)]
-        if rng.random() < 0.5:
-            tiers.append([(rng.choice([2.0e13, 3.12e14]), 24e9)])
-        regions.append(tiers)
-    layers = I.transformer_layers(n, 2048, 5504, 1024, 32000, d_kv=2048,
-                                  jitter_seed=seed if jitter else None)
-    spec = I.InstanceSpec(f"k{k}", layers, (64, 128), (8, 16), regions,
-                          intra_bw=[rng.uniform(1e9, 5e10) for _ in range(k)],
-                          intra_lat=[rng.uniform(1e-5, 1e-3) for _ in range(k)],
-                          cross_bw=1.25e7, cross_lat=0.03, jitter_seed=seed)
-    return I.build(spec)
+    return I.build(I.many_group_config(k, n, seed, jitter=jitter))
 
 
 @pytest.mark.parametrize("k,n,seed", [(5, 20, 1), (5, 24, 2), (6, 16, 3), (6, 20, 4), (6, 40, 5),

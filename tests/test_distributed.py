@@ -19,19 +19,23 @@ from paper_2505_15536_b200.layout import PackedInstance
 
 
 def _oracle_items(O, packed, lo, hi):
+    """Rank-local (cost, tie, first error) over items [lo, hi), oracle-evaluated."""
     k = packed.n_fgs
     NC, NP, n_items = DI.space_dims(packed.n_layers, k, len(packed.batches), len(packed.micros))
     nbm = len(packed.batches) * len(packed.micros)
     nm = len(packed.micros)
-    best = DI.NO_KEY
+    best, err = DI.NO_KEY, None
     for bi in range(len(packed.batches)):
         a, b = (bi * nm * NP + lo) * NC, (bi * nm * NP + hi) * NC
-        st, r = O.argmin_range(packed, a, b, threads=1)
-        assert st in (0, 3)
-        if st == 0:
-            key = (r.cost, DI.tie_of_index(r.index, NC, NP, nbm))
-            best = min(best, key)
-    return best
+        cost, status = O.eval_range(packed, a, b, threads=1)
+        bad = np.nonzero(status)[0]
+        if bad.size:
+            if err is None or a + int(bad[0]) < err[0]:
+                err = (a + int(bad[0]), int(status[bad[0]]))
+            continue
+        for j in range(cost.size):
+            best = min(best, (float(cost[j]), DI.tie_of_index(a + j, NC, NP, nbm)))
+    return best[0], best[1], err
 
 
 def _worker(rank, world, port, name, out):
@@ -44,24 +48,87 @@ def _worker(rank, world, port, name, out):
     packed = PackedInstance(model, topo, groups, 1.25)
     k = packed.n_fgs
     NC, NP, n_items = DI.space_dims(packed.n_layers, k, len(packed.batches), len(packed.micros))
-    key = DI.sharded_argmin(lambda lo, hi: _oracle_items(O, packed, lo, hi), n_items)
-    out[rank] = key
+    try:
+        out[rank] = DI.sharded_argmin(lambda lo, hi: _oracle_items(O, packed, lo, hi), n_items)
+    except Exception as e:  # every rank must raise the same error, none may hang
+        out[rank] = type(e).__name__
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["c2", "c2j", "rand10", "small"])
-def test_gloo_two_ranks_match_exhaustive(name):
+def _spawn(target, world, *args):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
     port = 29500 + random.randint(0, 2000)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, out)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, world, port) + args + (out,))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(120)
+        p.join(180)
         assert p.exitcode == 0
+    return dict(out)
+
+
+@pytest.mark.parametrize("name", ["err_gateway", "err_intra_bw"])
+def test_gloo_two_ranks_raise_reference_error(name):
+    """A rank whose shard raises does not leave the others in the collective:
+    all ranks raise the error of the smallest index, as the reference does."""
+    out = _spawn(_worker, 2, name)
+    doc, model, topo, groups = load_case(name)
+    exp = doc["exhaustive"]["error"]
+    assert out[0] == out[1] == exp
+
+
+def _snap_worker(rank, world, port, n_snap, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    from paper_2505_15536_b200 import instances as I
+    spec = I.config("c1")
+    lo, hi = DI.shard_items(n_snap, world, rank)
+    rec = np.zeros((hi - lo, 3), np.int64)
+    for i, j in enumerate(range(lo, hi)):
+        m, t, g = I.build(spec, I.snapshot_multipliers(spec, j))
+        p = PackedInstance(m, t, g, 1.25)
+        st, b = O.argmin_range(p, 0, O.space_size(p), threads=1)
+        rec[i] = (DI._cost_bits(b.cost), b.index, st)
+    allrec = DI.gather_snapshot_records(rec, n_snap, device=torch.device("cpu"))
+    m, t, g = I.build(spec)
+    out[rank] = DI.decode_snapshot_records(PackedInstance(m, t, g, 1.25), allrec)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_snapshot_shards_gather_every_result(world):
+    """Snapshots partitioned by index; every rank ends with all results,
+    each equal to the single-process re-plan of that snapshot."""
+    from oracle import oracle as O
+    from paper_2505_15536_b200 import instances as I
+    n_snap = 7
+    out = _spawn(_snap_worker, world, n_snap)
+    spec = I.config("c1")
+    for r in range(1, world):
+        assert out[r] == out[0]
+    for j in range(n_snap):
+        m, t, g = I.build(spec, I.snapshot_multipliers(spec, j))
+        p = PackedInstance(m, t, g, 1.25)
+        st, b = O.argmin_range(p, 0, O.space_size(p), threads=1)
+        cost, order, counts, bb, mm = out[0][j]
+        assert cost == b.cost
+        assert [p.fg_pos[f] for f in order] == list(b.order[:b.k])
+        assert counts == list(b.counts[:b.k])
+        assert (bb, mm) == (p.batches[b.batch_index], p.micros[b.micro_index])
+
+
+@pytest.mark.parametrize("name", ["c2", "c2j", "rand10", "small"])
+def test_gloo_two_ranks_match_exhaustive(name):
+    out = _spawn(_worker, 2, name)
     assert out[0] == out[1]
     doc, model, topo, groups = load_case(name)
     packed = PackedInstance(model, topo, groups, 1.25)

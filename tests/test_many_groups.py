@@ -1,0 +1,177 @@
+"""k = 5..8 stage groups: the regime where exhaustive_plan's space explodes
+and the drop-in hands spaces above BNB_THRESHOLD to K4 (branch-and-bound).
+
+Golden instances (scripts/make_golden.py, instances.many_group_config, the
+reference's own group_first_level):
+  k5n9 k6n8 k7n8 k8n9      every candidate's reference cost, the reference
+                           exhaustive_plan / search_plan results (these also
+                           run through every test parametrised by CASES_ALL)
+  k5n24 k6n20 k7n16 k8n14  4e6 .. 1.4e8 candidates, and k6n40 with 1.66e9
+                           (> BNB_THRESHOLD: the drop-in's K4 route): a
+                           2,000-candidate reference sample (pins the oracle on
+                           that very instance) and the oracle's full arg-min
+
+Every exhaustive kernel is checked against these answers, never only
+against another GPU kernel: the sweep with k fixed at compile time (k = 5, 6)
+and the generic sweep (k = 7, 8, and modes 0 / 1 for every k), the
+status-tracking generic kernel, the sub-range tile kernel, K4, K2, and the
+drop-in exhaustive_plan / search_plan.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from cases import golden_costs, load_case, same_bits
+import paper_2505_15536_b200 as P
+from paper_2505_15536_b200 import planner as PL
+from paper_2505_15536_b200.layout import PackedInstance
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["k5n9", "k6n8", "k7n8", "k8n9"]
+BIG = ["k5n24", "k6n20", "k7n16", "k8n14", "k6n40"]
+
+
+def _load(engine, name):
+    doc, model, topo, groups = load_case(name)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    engine.load(packed)
+    return doc, model, topo, groups, packed
+
+
+def _golden_argmin(packed, gc, gs):
+    """(index, cost) of the reference key (cost, (order, cuts)) minimum with
+    the earliest (b, m) - the tie rank order of SURVEY App. C."""
+    k, n = packed.n_fgs, packed.n_layers
+    NP, NC = math.factorial(k), math.comb(n - 1, k - 1)
+    nbm = len(packed.batches) * len(packed.micros)
+    idx = np.arange(gc.size, dtype=np.int64)
+    tie = ((idx // NC) % NP * NC + idx % NC) * nbm + idx // (NP * NC)
+    order = np.lexsort((tie, gc))
+    i = int(order[0])
+    return i, gc[i]
+
+
+@pytest.mark.parametrize("mode", [-1, 0, 1, 2, 3, 4])
+@pytest.mark.parametrize("name", SMALL)
+def test_small_argmin_every_kernel(engine, name, mode):
+    doc, model, topo, groups, packed = _load(engine, name)
+    gc, gs = golden_costs(name)
+    assert not gs.any()
+    i, c = _golden_argmin(packed, gc, gs)
+    total = engine.space_size()
+    engine.set_k3_mode(mode)
+    try:
+        got = engine.argmin_range(0, total)
+    finally:
+        engine.set_k3_mode(-1)
+    assert got.index == i and same_bits(got.cost, c)
+    exp = doc["exhaustive"]["result"]["breakdown"]["plan_cost"]
+    assert got.cost == exp
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_small_bnb_vs_reference(engine, name):
+    doc, model, topo, groups, packed = _load(engine, name)
+    gc, gs = golden_costs(name)
+    i, c = _golden_argmin(packed, gc, gs)
+    got = engine.argmin_bnb()
+    assert got.index == i and same_bits(got.cost, c)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_small_exhaustive_plan_via_bnb_vs_reference(engine, name, monkeypatch):
+    monkeypatch.setattr(PL, "BNB_THRESHOLD", 0)
+    doc, model, topo, groups = load_case(name)
+    res = P.exhaustive_plan(model, topo, groups, P.SearchConfig(seed=0), engine=engine)
+    assert G.normalize_result(res) == doc["exhaustive"]["result"]
+
+
+@pytest.mark.parametrize("name", BIG)
+def test_big_sample_k2_vs_reference(engine, oracle_lib, name):
+    doc, model, topo, groups, packed = _load(engine, name)
+    smp = doc["sample"]
+    idx = smp["index"]
+    k = packed.n_fgs
+    order = np.zeros((len(idx), k), np.uint8)
+    counts = np.zeros((len(idx), k), np.uint8)
+    bm = np.zeros(len(idx), np.uint8)
+    for r, i in enumerate(idx):
+        order[r], counts[r], bm[r] = oracle_lib.decode(packed, int(i))
+    cost, status = engine.eval_batch(order, counts, bm)
+    assert list(status) == smp["status"]
+    exp = np.array([G._uf(x) if x is not None else np.nan for x in smp["cost"]])
+    ok = status == 0
+    assert same_bits(cost[ok], exp[ok]).all()
+
+
+@pytest.mark.parametrize("mode", [-1, 0, 1, 3])
+@pytest.mark.parametrize("name", BIG)
+def test_big_argmin_vs_oracle(engine, name, mode):
+    doc, model, topo, groups, packed = _load(engine, name)
+    exp = doc["oracle_argmin"]
+    total = engine.space_size()
+    assert total == exp["evaluated"]
+    if mode == 3 and total > 2e8:
+        pytest.skip("generic kernel on 1.7e9 candidates: covered by the sweep modes")
+    engine.set_k3_mode(mode)
+    try:
+        got = engine.argmin_range(0, total)
+    finally:
+        engine.set_k3_mode(-1)
+    assert got.index == exp["index"] and got.cost == exp["cost"]
+    assert list(got.order[:got.k]) == exp["order"]
+    assert list(got.counts[:got.k]) == exp["counts"]
+
+
+@pytest.mark.parametrize("name", BIG)
+def test_big_bnb_vs_oracle(engine, name):
+    doc, model, topo, groups, packed = _load(engine, name)
+    exp = doc["oracle_argmin"]
+    got = engine.argmin_bnb()
+    assert got.index == exp["index"] and got.cost == exp["cost"]
+
+
+@pytest.mark.parametrize("name", ["k5n24", "k6n20", "k7n16"])
+def test_big_sweep_costs_at_reference_sample(engine, name):
+    """The sweep's own per-candidate costs (verify sink) at the positions the
+    reference evaluated."""
+    doc, model, topo, groups, packed = _load(engine, name)
+    total = engine.space_size()
+    engine.verify_begin(0, total)
+    engine.argmin_range(0, total)
+    v = engine.verify_end()
+    smp = doc["sample"]
+    idx = np.array(smp["index"], dtype=np.int64)
+    exp = np.array([G._uf(x) if x is not None else np.nan for x in smp["cost"]])
+    assert same_bits(v[idx], exp).all()
+    assert not (v.view(np.uint64) == np.uint64(0xFFFFFFFFFFFFFFFF)).any()
+
+
+@pytest.mark.parametrize("name", BIG)
+def test_big_exhaustive_plan_dropin(engine, name):
+    """The drop-in routes spaces above BNB_THRESHOLD (k6n40) to K4 and the
+    rest to the sweep; either way the reference key's winner."""
+    doc, model, topo, groups = load_case(name)
+    exp = doc["oracle_argmin"]
+    res = P.exhaustive_plan(model, topo, groups, P.SearchConfig(seed=0), engine=engine)
+    assert res.breakdown.plan_cost == exp["cost"]
+    assert res.evaluated == exp["evaluated"]
+    fg = sorted(groups.fgs)
+    assert [s.fg_id for s in res.plan.stages] == [fg[i] for i in exp["order"]]
+    assert [s.layer_end - s.layer_start for s in res.plan.stages] == exp["counts"]
+    assert res.plan.batch_b == model.global_batch_candidates[exp["batch_index"]]
+    assert res.plan.microbatch_m == model.microbatch_candidates[exp["micro_index"]]
+    if exp["evaluated"] > PL.BNB_THRESHOLD:
+        assert name == "k6n40"
+
+
+@pytest.mark.parametrize("name", BIG)
+def test_big_search_plan_vs_reference(engine, name):
+    doc, model, topo, groups = load_case(name)
+    for seed, exp in doc["search"].items():
+        res = P.search_plan(model, topo, groups, P.SearchConfig(seed=int(seed)), engine=engine)
+        assert G.normalize_result(res) == exp["result"]

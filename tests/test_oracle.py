@@ -98,6 +98,22 @@ def test_oracle_c4_sample_bitwise(oracle_lib, name):
     assert same_bits(cost, gc[:3000]).all()
 
 
+@pytest.mark.parametrize("name", ["k5n24", "k6n20", "k7n16", "k8n14", "k6n40"])
+def test_oracle_many_group_sample_bitwise(oracle_lib, name):
+    """k = 5..8 instances too large for a full reference sweep: the oracle
+    whose arg-min the GPU tests use equals the reference on 2,000 samples."""
+    doc, model, topo, groups = load_case(name)
+    packed = PackedInstance(model, topo, groups, 1.25)
+    smp = doc["sample"]
+    for i, c, s in zip(smp["index"], smp["cost"], smp["status"]):
+        o, n, bm = oracle_lib.decode(packed, int(i))
+        st, v = oracle_lib.evaluate(packed, o, n, bm)
+        assert st == s
+        if s == 0:
+            assert same_bits(v, G._uf(c))
+    assert doc["oracle_argmin"]["evaluated"] == oracle_lib.space_size(packed)
+
+
 @pytest.mark.parametrize("name", CASES_ALL)
 def test_oracle_exhaustive_argmin(oracle_lib, name):
     doc, model, topo, groups = load_case(name)
