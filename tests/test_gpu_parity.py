@@ -319,3 +319,68 @@ def test_search_plan_seeds_0_to_20(engine, name):
     for seed, exp in SEEDS[name].items():
         res = P.search_plan(model, topo, groups, P.SearchConfig(seed=int(seed)), engine=engine)
         assert G.normalize_result(res) == exp["result"], (name, seed)
+
+
+def test_replan_graph_after_loads_of_other_shapes(engine):
+    """gp_replan replays its captured graph only while the context holds an
+    instance of the graph's shape: replan(A), then loads / searches / K4 on
+    smaller instances B, then replan(A') must still give A's golden answer
+    (stale run groups, prefixes and host geometry otherwise)."""
+    from paper_2505_15536_b200 import instances as I
+    docA, mA, tA, gA = load_case("c2j")
+    pA = PackedInstance(mA, tA, gA, 1.25)
+    expA = docA["exhaustive"]["result"]["breakdown"]["plan_cost"]
+    gc, gs = golden_costs("c2j")
+    for other in ["rand10", "small", "k5n9", "c1", "rand12"]:
+        b, _ = engine.replan(pA)
+        assert b.cost == expA
+        docB, mB, tB, gB = load_case(other)
+        pB = PackedInstance(mB, tB, gB, 1.25)
+        engine.load(pB)
+        if pB.n_fgs >= 2:
+            engine.argmin_bnb()
+        P.search_plan(mB, tB, gB, P.SearchConfig(seed=1), engine=engine)
+        pA2 = PackedInstance(mA, tA, gA, 1.25)  # a different object of A's shape
+        b, info = engine.replan(pA2)
+        assert b.cost == expA, other
+        assert info.plan_cost == expA
+        total = engine.space_size()
+        assert total == gc.size
+        assert engine.argmin_range(0, total).cost == expA
+    # and K6 snapshots in between
+    spec = I.config("c2")
+    m2, t2, g2 = I.build(spec)
+    p2 = PackedInstance(m2, t2, g2, 1.25)
+    engine.load(p2)
+    from paper_2505_15536_b200 import replan as R
+    engine.replan_snapshots(R.bandwidth_matrices(p2, [I.snapshot_multipliers(spec, 3)]))
+    b, _ = engine.replan(pA)
+    assert b.cost == expA
+
+
+def test_reset_bandwidth_restores_groupindex_min_bw(engine):
+    """After snapshots, the loaded GroupIndex min_intra_bandwidth values come
+    back (not min(bw) re-derived from the matrix): use a hierarchy whose
+    stored min bandwidth differs from the matrix minimum."""
+    import dataclasses
+    doc, model, topo, groups = load_case("c2j")
+    fg = sorted(groups.fgs)[0]
+    g0 = groups.fgs[fg]
+    fgs = dict(groups.fgs)
+    fgs[fg] = dataclasses.replace(g0, min_intra_bandwidth=g0.min_intra_bandwidth * 0.5)
+    groups2 = dataclasses.replace(groups, fgs=fgs)
+    packed = PackedInstance(model, topo, groups2, 1.25)
+    engine.load(packed)
+    total = engine.space_size()
+
+    def costs():
+        engine.verify_begin(0, total)
+        engine.argmin_range(0, total)
+        return engine.verify_end()
+
+    before = costs()
+    engine.set_bandwidth(packed.bw)  # snapshot = same matrix: min bw re-derived from it
+    derived = costs()
+    assert not same_bits(derived, before).all()  # the stored value really differs
+    engine.reset_bandwidth()
+    assert same_bits(costs(), before).all()
