@@ -1,42 +1,55 @@
 #!/usr/bin/env python3
-"""Benchmark: candidate plans evaluated/s and full re-plan latency on B200.
+"""Benchmark: candidate plans evaluated/s and exact re-plan latency on B200.
 
-Workload (BASELINE.json configs[3], App. D "c4"): the 80-layer Llama-2-70B
-cost table on 64 heterogeneous devices in 4 tiers.  One STEP = one exact
-exhaustive re-plan of that instance = the arg-min over all 11,387,376
-(b, m, stage order, layer cuts) candidates, each fully evaluated as the
-reference's `_evaluate` does (split choice + memory feasibility + Eq. 1).
-Under torchrun every rank re-plans its own bandwidth snapshot of C4 (C3
-recipe, snapshot = rank), so per-GPU work is fixed ("scaling": "weak"); the
-per-snapshot winners are all-gathered once at the end (16 B per rank).
+Workload (BASELINE.json configs[2]+[3]): the C4 instance - the
+80-layer Llama-2-70B cost table on 64 heterogeneous devices in 4 tiers - under
+the C3 bandwidth-fluctuation recipe.  One STEP = the exact exhaustive re-plan
+of a fixed batch of S = 128 bandwidth snapshots (snapshot j = App. D recipe
+with seed j), i.e. 128 x 11,387,376 candidates, each fully evaluated as the
+reference's `_evaluate` does (split choice + memory feasibility + Eq. 1) and
+reduced to that snapshot's arg-min under the reference key.  Under torchrun
+the snapshots are partitioned by index over the N ranks (contiguous shards,
+no data-path communication) and the per-snapshot winners (16 B each) are
+all-gathered over NCCL inside the step, so every rank ends with all 128 plans
+(fixed total work: "scaling": "strong").
 
-  value      candidates/s over all ranks, tables resident in HBM, device time
-             of the K3 launches (CUDA events on the engine stream, L2 flushed
-             between steps, max over ranks)
-  e2e        the same metric through the C-ABI with host buffers: per step
-             gp_ctx_load (H2D of the packed instance + K1 tables) +
-             gp_argmin_range (K3 + D2H of the winner) + gp_plan_detail
-  roofline   K3 is FP64-issue-bound (no HBM traffic per candidate): achieved
-             FP64 ops/s = (ops per candidate) x candidates/s against the
-             FP64 add rate measured live on this GPU
-  cpu_baseline  the C oracle port (oracle/, test infrastructure) on all host
-             threads over the same full range, rank 0 at N=1 only
+  value      candidates/s over all ranks with the bandwidth matrices resident
+             in HBM: CUDA events on the engine stream around each step (K6
+             table patch + K3 sweep + NCCL all-gather), L2 flushed between
+             steps, max over ranks
+  e2e        the same step through the public API with host buffers:
+             distributed.replan_snapshots_sharded (single GPU:
+             replan.replan_snapshots) - pinned H2D of the matrices, K6, D2H
+             of the winners, all-gather - wall clock, max over ranks
+  roofline   the sweep kernel is FP64-issue-bound (tables in shared memory,
+             no per-candidate HBM traffic): 39 algorithmic FP64 ops per C4
+             candidate (11k - 5) x candidates per launch over
+             the launch's CUDA-event duration, against the FP64 add rate
+             measured live on this GPU
+  cpu_baseline  the C oracle port (oracle/, test infrastructure) on the host
+             threads over a bounded prefix of one snapshot, rank 0 at N=1,
+             plus the unmodified Python reference on a sample when it is
+             importable (baseline/_ref)
+  scaling_rows  the other sharded paths at the same N: one C4 re-plan
+             item-sharded with the NCCL tuple arg-min, the BASELINE 10^6
+             sampled C4 candidates in N K2 chunks + arg-min, C3 (C2 x 10^4
+             snapshots) partitioned by index, and weak scaling
 
-`--impl reference` times that CPU implementation alone (the reference arm).
+`--impl reference` times the CPU implementation alone (the reference arm).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-
-import numpy as np
+import math
 import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -45,12 +58,13 @@ sys.path.insert(0, ROOT)
 # (11k - 5 = 39 for k = 4 stages): 6 per stage (C1*m, M*c,
 # three adds, max) + 5 per boundary (c+x, fill+, x-c', max0, res+).
 ALG_OPS_PER_CAND_C4 = 39
-# FP64 instructions the K3 sweep actually issues per candidate (SASS of the
-# paired-q inner loop: 56 DADD/DMUL/DSETP per 2 q steps x 2 batch sizes).
-K3_ISSUED_FP64_PER_CAND = 14
-# dram__bytes_read.sum + write of one K3 launch after an L2 flush (ncu launch
-# list of this bench, profiles/r1e_launches_bench.csv: 704,256 B read, 0 written)
-K3_DRAM_BYTES = 704256
+# Measured by ncu on the sweep kernel of this workload (not in-run):
+# profiles/r2_k6_sweep_ncu_raw.csv (sm__inst_executed_pipe_fp64 / candidates
+# and dram__bytes_read.sum + dram__bytes_write.sum of one launch).
+NCU_SOURCE = "profiles/r2_k6_sweep_ncu_raw.csv"
+SWEEP_ISSUED_FP64_PER_CAND = None
+SWEEP_DRAM_BYTES = None
+S_TOTAL = 128
 
 
 def parse():
@@ -59,9 +73,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--snapshots", type=int, default=S_TOTAL)
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-rows", action="store_true")
     return ap.parse_args()
 
 
@@ -70,6 +86,36 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def pct(xs, q):
+    xs = sorted(xs)
+    if not xs:
+        return float("nan")
+    return xs[min(len(xs) - 1, int(math.ceil(q / 100.0 * len(xs))) - 1)]
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def load_ncu_constants():
+    """issued FP64 per candidate and DRAM bytes per launch of the sweep, from
+    the committed ncu capture of this workload (None when absent)."""
+    global SWEEP_ISSUED_FP64_PER_CAND, SWEEP_DRAM_BYTES
+    path = os.path.join(ROOT, "profiles", "r2_k6_sweep_ncu_summary.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        SWEEP_ISSUED_FP64_PER_CAND = d.get("issued_fp64_per_candidate")
+        SWEEP_DRAM_BYTES = d.get("dram_bytes_per_launch")
 
 
 class ClockSampler:
@@ -87,7 +133,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -97,7 +143,7 @@ class ClockSampler:
     def __exit__(self, *a):
         self.lines = []
         if self.proc is not None:
-            time.sleep(0.1)
+            time.sleep(0.05)
             self.proc.terminate()
             try:
                 out, _ = self.proc.communicate(timeout=5)
@@ -124,23 +170,87 @@ class ClockSampler:
                 "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(total, threads, target_s=10.0):
-    """Oracle port on host cores over a bounded prefix of the range."""
+def cpu_baseline(packed, total, threads, target_s=10.0):
+    """Oracle port on host cores over a bounded prefix of one snapshot's space."""
     from oracle import oracle as O
-    from paper_2505_15536_b200 import instances
-    from paper_2505_15536_b200.layout import PackedInstance
-    model, topo, groups = instances.load("c4")
-    packed = PackedInstance(model, topo, groups, 1.25)
-    # calibrate on a short prefix, then run ~target_s of work
     n0 = 200_000
     t = time.perf_counter()
     O.argmin_range(packed, 0, n0, threads=threads)
     dt = time.perf_counter() - t
     n = int(min(total, max(n0, n0 * target_s / max(dt, 1e-6))))
     t = time.perf_counter()
-    st, best = O.argmin_range(packed, 0, n, threads=threads)
+    O.argmin_range(packed, 0, n, threads=threads)
     dt = time.perf_counter() - t
     return n / dt, n, dt
+
+
+def python_reference_rate(spec_name="c4", n_cand=600, procs=None):
+    """The unmodified Python reference (`geopipe.planner._evaluate`, fresh cache
+    per candidate, logging disabled) on a random sample of the C4 space: one
+    process, and `procs` processes over contiguous shards.  None when the
+    reference is not importable (baseline/_ref or /root/reference)."""
+    import importlib
+    import logging
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "geopipe")) and p not in sys.path:
+            sys.path.insert(0, p)
+    try:
+        gp = importlib.import_module("geopipe")
+    except ImportError:
+        return None
+    logging.disable(logging.CRITICAL)
+    from concurrent.futures import ProcessPoolExecutor
+    rate1 = _py_ref_worker((spec_name, 0, n_cand))
+    procs = procs or os.cpu_count() or 1
+    t = time.perf_counter()
+    with ProcessPoolExecutor(procs) as ex:
+        list(ex.map(_py_ref_worker, [(spec_name, s + 1, n_cand) for s in range(procs)]))
+    el = time.perf_counter() - t
+    return {"value_1proc": rate1, "value_all": procs * n_cand / el, "processes": procs,
+            "unit": "candidates/s", "sample": f"{n_cand} random C4 candidates per process",
+            "source": "geopipe (unmodified reference) " + getattr(gp, "__version__", "")}
+
+
+def _py_ref_worker(args):
+    spec_name, seed, n_cand = args
+    import logging
+    import random
+    logging.disable(logging.CRITICAL)
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "geopipe")) and p not in sys.path:
+            sys.path.insert(0, p)
+    from geopipe.planner import Candidate, _evaluate
+    from geopipe.timing import GroupIndex
+    import geopipe as gp
+    from paper_2505_15536_b200 import instances
+    from paper_2505_15536_b200.enumeration import decode_indices, composition_table
+    # the instance built with the reference's own constructors and grouping
+    spec = instances.config(spec_name)
+    devs = [gp.DeviceSpec(id=i, memory_bytes=mem, benchmark_times=(("bench", 1.0 / p_c),))
+            for i, _, _, p_c, mem in spec.devices()]
+    meas = [gp.LinkMeasurement(endpoints=frozenset((u, v)), alpha_seconds=1e8 / bw,
+                               beta_seconds=lat, payload_bytes_m=1e8, latency_seconds=lat,
+                               bandwidth_bytes_per_s=bw) for u, v, lat, bw in spec.links()]
+    topo = gp.build_topology(devs, meas)
+    fgs = gp.group_first_level(topo, 0.3)
+    groups = GroupIndex.build(fgs, {f.id: gp.group_second_level(f, topo, 0.3) for f in fgs})
+    model = gp.ModelSpec(layers=tuple(gp.LayerSpec(*r) for r in spec.layers),
+                         global_batch_candidates=tuple(spec.batches),
+                         microbatch_candidates=tuple(spec.micros))
+    fg = sorted(groups.fgs)
+    n, k = model.num_layers, len(fg)
+    total = 6 * math.factorial(k) * math.comb(n - 1, k - 1)
+    idx = np.array(random.Random(seed).sample(range(total), n_cand))
+    order, counts, bm = decode_indices(n, k, idx, composition_table(n, k))
+    cfg = gp.SearchConfig(seed=0)
+    nm = len(model.microbatch_candidates)
+    cands = [(Candidate(tuple(fg[x] for x in order[i]), tuple(int(c) for c in counts[i])),
+              model.global_batch_candidates[bm[i] // nm], model.microbatch_candidates[bm[i] % nm])
+             for i in range(n_cand)]
+    t = time.perf_counter()
+    for c, b, m in cands:
+        _evaluate(c, b, m, groups, topo, model, cfg, {})
+    return n_cand / (time.perf_counter() - t)
 
 
 def extra_sections(eng, packed, total, local, args, world):
@@ -208,41 +318,6 @@ def extra_sections(eng, packed, total, local, args, world):
                           "ok": int((stk == 0).sum()),
                           "note": "memory-feasible C4 plans, 1F1B, iterations=1; one thread per "
                                   "simulation; includes H2D/D2H of the batch"}
-
-    # ---- K6: C3 - 10^4 bandwidth snapshots of C2, exact re-plan each
-    spec = instances.config("c2")
-    m2, t2, g2 = instances.build(spec)
-    p2 = PackedInstance(m2, t2, g2, 1.25)
-    nsnap = 10_000
-    bws = replan.bandwidth_matrices(p2, [instances.snapshot_multipliers(spec, j)
-                                         for j in range(nsnap)])
-    e2 = Engine(local).load(p2)
-    e2.replan_snapshots(bws)  # warm-up at full size (allocations outside the timed call)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    b2, s2 = e2.replan_snapshots(bws)
-    el = time.perf_counter() - t0
-    lat = []
-    for j in range(20):
-        t1 = time.perf_counter()
-        e2.replan_snapshots(bws[j:j + 1])
-        lat.append(time.perf_counter() - t1)
-    c2_total = e2.space_size()
-    out["k6_snapshot_replan"] = {
-        "snapshots": nsnap, "candidates_per_snapshot": c2_total, "host_call_s": el,
-        "snapshots_per_s": nsnap / el, "candidates_per_s": nsnap * c2_total / el,
-        "single_snapshot_latency_ms_p50": statistics.median(lat) * 1e3,
-        "ok": int((s2 == 0).sum()),
-        "note": "C3 recipe (App. D) on C2; bandwidth matrices H2D inside the call"}
-    if world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as O
-        t0 = time.perf_counter()
-        for j in range(5):
-            m3, t3, g3 = instances.build(spec, instances.snapshot_multipliers(spec, j))
-            p3 = PackedInstance(m3, t3, g3, 1.25)
-            O.argmin_range(p3, 0, c2_total, threads=args.cpu_threads or os.cpu_count())
-        out["k6_snapshot_replan"]["cpu_port_ms_per_snapshot"] = (time.perf_counter() - t0) / 5 * 1e3
-    e2.close()
 
     # ---- C5: throughput vs batch size N
     eng.load(packed)
@@ -323,6 +398,7 @@ def extra_sections(eng, packed, total, local, args, world):
     out["k7_regroup"] = {
         "snapshots": n7, "devices": int(len(ids4)), "host_call_s": el,
         "snapshots_per_s": n7 / el, "single_snapshot_latency_ms_p50": statistics.median(lat) * 1e3,
+        "single_snapshot_latency_ms_p99": pct(lat, 99) * 1e3,
         "groups_seen": sorted({len(h.fg_capacity) for h in hs}),
         "note": "group_first_level + group_second_level per C4 p_t snapshot, one CTA each; "
                 "p_t matrices H2D inside the call; the Python reference takes ~50 ms per "
@@ -372,20 +448,19 @@ def extra_sections(eng, packed, total, local, args, world):
         out["k5_full_adapter"]["cpu_port_simulations_per_s_1thread"] = 5000 / (time.perf_counter() - t0)
 
     # ---- K4: exact re-plan of spaces far beyond enumeration (k = 8 groups)
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from test_bnb import _many_group_instance
     for (k, n, seed) in ((6, 80, 6), (8, 80, 8)):
-        mk, tk, gk = _many_group_instance(k, n, seed)
+        mk, tk, gk = instances.build(instances.many_group_config(k, n, seed))
         pk = PackedInstance(mk, tk, gk, 1.25)
         ek = Engine(local).load(pk)
         ek.argmin_bnb()
         lat = []
-        for _ in range(5):
+        for _ in range(9):
             t0 = time.perf_counter()
             bb = ek.argmin_bnb()
             lat.append(time.perf_counter() - t0)
         out[f"k4_bnb_k{k}_n{n}"] = {
             "candidates_in_space": int(ek.space_size()), "replan_ms_p50": statistics.median(lat) * 1e3,
+            "replan_ms_p99": pct(lat, 99) * 1e3,
             "cost": bb.cost,
             "note": "exact arg-min by branch-and-bound with the exact-in-reals DP bound "
                     "(same winner as exhaustive enumeration; tests/test_bnb.py)"}
@@ -412,10 +487,10 @@ def run_reference(args):
     from oracle import oracle as O
     from paper_2505_15536_b200 import instances
     from paper_2505_15536_b200.layout import PackedInstance
-    model, topo, groups = instances.load("c4")
+    model, topo, groups = instances.load("c4", snapshot=0)
     packed = PackedInstance(model, topo, groups, 1.25)
     total = O.space_size(packed)
-    # each step: a bounded sample (contiguous prefix) of the full re-plan
+    # each step: a bounded sample (contiguous prefix) of snapshot 0's re-plan
     n0 = 100_000
     t = time.perf_counter()
     O.argmin_range(packed, 0, n0, threads=threads)
@@ -432,153 +507,431 @@ def run_reference(args):
         "impl": "reference", "metric": "candidate plans evaluated/sec", "value": rate,
         "unit": "candidates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": "c4-exhaustive-replan", "candidates_per_replan": total,
-                   "layers": 80, "devices": 64, "groups": 4},
-        "cpu_baseline": {"value": rate, "unit": "candidates/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"first {per_step} candidates of the C4 exhaustive range "
-                                   f"per step (oracle/oracle.c, {threads} threads)"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (App. D C4 recipe; C3 bandwidth snapshot 0)",
+        "config": workload_config(args.snapshots, total, world),
+        "cpu_baseline": {"value": rate, "unit": "candidates/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
+                         "sample": f"first {per_step} candidates of snapshot 0's C4 exhaustive "
+                                   f"range per step (oracle/oracle.c, {threads} threads)"},
         "e2e": {"value": rate, "unit": "candidates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    py = python_reference_rate()
+    if py is not None:
+        line["python_reference"] = py
     print(json.dumps(line), flush=True)
     return 0
+
+
+def workload_config(S, total, world):
+    return {"workload": "c4-snapshot-replan", "snapshots_per_step": S,
+            "candidates_per_snapshot": total, "candidates_per_step": S * total,
+            "layers": 80, "devices": 64, "groups": 4, "batch_micro_pairs": 6,
+            "l2": "flushed between steps (256 MiB write)",
+            "parallelism": f"snapshot shards x{world} (contiguous by index) + NCCL all-gather "
+                           "of the 16-byte per-snapshot winners"}
+
+
+class Ctx:
+    """Per-rank handles shared by the sections."""
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.args = args
+        self.rank, self.world, self.local = dist_env()
+        self.dev = torch.device("cuda", self.local)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, x):
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def shard(self, n):
+        from paper_2505_15536_b200.distributed import shard_items
+        return shard_items(n, self.world, self.rank)
+
+
+def event_loop(X, stream, step, steps, warmup, flush=None, sampler=None):
+    """Device ms per step (CUDA events on `stream`), after `warmup` untimed steps."""
+    torch = X.torch
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            if flush is not None:
+                flush.zero_()
+            step()
+    X.barrier()
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for i in range(steps):
+            if flush is not None:
+                flush.zero_()
+            st[i].record(stream)
+            step()
+            en[i].record(stream)
+    torch.cuda.synchronize()
+    X.barrier()
+    return [a.elapsed_time(b) for a, b in zip(st, en)]
+
+
+def scaling_rows(X, eng, packed, model, topo, groups, total):
+    """The other sharded paths at this N (every rank takes part)."""
+    torch, dist = X.torch, X.dist
+    import random
+    from paper_2505_15536_b200 import SearchConfig, instances, replan
+    from paper_2505_15536_b200 import distributed as DI
+    from paper_2505_15536_b200.engine import Engine
+    from paper_2505_15536_b200.enumeration import composition_table, decode_indices
+    from paper_2505_15536_b200.layout import PackedInstance
+    rows = {}
+    stream = torch.cuda.ExternalStream(eng.stream, device=X.dev)
+    k = packed.n_fgs
+    NC, NP, n_items = DI.space_dims(packed.n_layers, k, len(packed.batches), len(packed.micros))
+    nbm = len(packed.batches) * len(packed.micros)
+
+    # (a) ONE C4 exhaustive re-plan, items sharded over the ranks, NCCL tuple arg-min
+    eng.load(packed)
+    lo, hi = X.shard(n_items)
+    dev_ms = event_loop(X, stream, lambda: DI_items(eng, lo, hi), 30, 3)
+    cfg = SearchConfig(seed=0)
+    lat = []
+    for i in range(33):
+        X.barrier()
+        t0 = time.perf_counter()
+        res = DI.exhaustive_plan_sharded(model, topo, groups, cfg, engine=eng)
+        el = time.perf_counter() - t0
+        if i >= 3:
+            lat.append(el)
+    lat_max = [X.max_over_ranks(v) for v in lat]
+    dmax = [X.max_over_ranks(v) for v in dev_ms]
+    rows["single_replan_item_sharded"] = {
+        "candidates": total, "items": n_items, "items_this_rank": hi - lo,
+        "device_ms_p50": statistics.median(dmax), "device_ms_p99": pct(dmax, 99),
+        "api_ms_p50": statistics.median(lat_max) * 1e3, "api_ms_p99": pct(lat_max, 99) * 1e3,
+        "candidates_per_s_device": total / (statistics.median(dmax) * 1e-3),
+        "best_cost": res.breakdown.plan_cost,
+        "note": "device: the rank's item-range sweep (K3), events on the engine stream, max over "
+                "ranks; api: distributed.exhaustive_plan_sharded wall clock incl. the 24-byte "
+                "NCCL all-gather of (first error, cost bits, tie), winner decode and plan detail"}
+
+    # (b) BASELINE configs[3]: 10^6 sampled C4 candidates in N K2 chunks + arg-min
+    idx = np.array(sorted(random.Random(4).sample(range(total), 10**6)), dtype=np.int64)
+    order, counts, bm = decode_indices(80, 4, idx, composition_table(80, 4))
+    lo, hi = X.shard(idx.size)
+    nloc = hi - lo
+    d_o = torch.from_numpy(np.ascontiguousarray(order[lo:hi])).to(X.dev)
+    d_c = torch.from_numpy(np.ascontiguousarray(counts[lo:hi])).to(X.dev)
+    d_b = torch.from_numpy(np.ascontiguousarray(bm[lo:hi])).to(X.dev)
+    d_i = torch.from_numpy(idx[lo:hi]).to(X.dev)
+    d_cost = torch.empty(max(1, nloc), dtype=torch.float64, device=X.dev)
+    d_st = torch.empty(max(1, nloc), dtype=torch.uint8, device=X.dev)
+    key = torch.empty(2, dtype=torch.int64, device=X.dev)
+    gk = torch.empty(2 * X.world, dtype=torch.int64, device=X.dev)
+    big = torch.tensor(2**62, dtype=torch.int64, device=X.dev)
+    torch.cuda.synchronize()
+
+    def k2_step():
+        eng.eval_batch_device(4, nloc, d_o.data_ptr(), d_c.data_ptr(), d_b.data_ptr(),
+                              d_cost.data_ptr(), d_st.data_ptr())
+        c = d_cost[:nloc]
+        m = c.min()
+        key[0] = m.view(torch.int64)
+        key[1] = torch.where(c == m, d_i, big).min()
+        if X.world > 1:
+            dist.all_gather_into_tensor(gk, key)
+    dev_ms = event_loop(X, stream, k2_step, 30, 3)
+    dmax = [X.max_over_ranks(v) for v in dev_ms]
+    g = (gk if X.world > 1 else key).view(-1, 2).cpu().numpy()
+    wi = min(range(g.shape[0]), key=lambda r: (int(g[r, 0]), int(g[r, 1])))
+    rows["k2_sample_1e6_sharded"] = {
+        "candidates": int(idx.size), "candidates_this_rank": nloc,
+        "device_ms_p50": statistics.median(dmax), "device_ms_p99": pct(dmax, 99),
+        "candidates_per_s": idx.size / (statistics.median(dmax) * 1e-3),
+        "best_index": int(g[wi, 1]), "best_cost": float(np.int64(g[wi, 0]).view(np.float64)),
+        "note": "random.Random(4).sample(range(11387376), 10**6) (BASELINE configs[3]); per "
+                "rank: K2 on its contiguous chunk, device arg-min (cost, index), NCCL all-gather"}
+
+    # (c) C3: C2 under 10^4 bandwidth snapshots, partitioned by index
+    spec2 = instances.config("c2")
+    m2, t2, g2 = instances.build(spec2)
+    p2 = PackedInstance(m2, t2, g2, 1.25)
+    e2 = Engine(X.local).load(p2)
+    tot2 = e2.space_size()
+    S2 = 10_000
+    bws2 = replan.bandwidth_matrices(p2, [instances.snapshot_multipliers(spec2, j)
+                                          for j in range(S2)])
+    lo, hi = X.shard(S2)
+    width = -(-S2 // X.world)
+    d_bw2 = torch.from_numpy(np.ascontiguousarray(bws2[lo:hi])).to(X.dev)
+    d_k2 = torch.zeros((width, 2), dtype=torch.int64, device=X.dev)
+    d_f2 = torch.zeros(width, dtype=torch.int32, device=X.dev)
+    gath2 = torch.empty((X.world * width, 2), dtype=torch.int64, device=X.dev)
+    s2 = torch.cuda.ExternalStream(e2.stream, device=X.dev)
+    torch.cuda.synchronize()
+
+    def c3_step():
+        e2.replan_snapshots_async(d_bw2.data_ptr(), hi - lo, d_k2.data_ptr(), d_f2.data_ptr())
+        if X.world > 1:
+            dist.all_gather_into_tensor(gath2, d_k2)
+    dev_ms = event_loop(X, s2, c3_step, 10, 2)
+    dmax = [X.max_over_ranks(v) for v in dev_ms]
+    bws2p = torch.from_numpy(bws2).pin_memory().numpy()
+    lat = []
+    for i in range(6):
+        X.barrier()
+        t0 = time.perf_counter()
+        if X.world > 1:
+            res2 = DI.replan_snapshots_sharded(m2, t2, g2, SearchConfig(seed=0), bws2p, engine=e2)
+        else:
+            res2 = replan.replan_snapshots(m2, t2, g2, SearchConfig(seed=0), bws2p, engine=e2)
+        el = time.perf_counter() - t0
+        if i >= 1:
+            lat.append(el)
+    lmax = [X.max_over_ranks(v) for v in lat]
+    rows["c3_snapshots_sharded"] = {
+        "snapshots": S2, "candidates_per_snapshot": tot2, "snapshots_this_rank": hi - lo,
+        "device_ms_p50": statistics.median(dmax), "device_ms_p99": pct(dmax, 99),
+        "candidates_per_s": S2 * tot2 / (statistics.median(dmax) * 1e-3),
+        "snapshots_per_s": S2 / (statistics.median(dmax) * 1e-3),
+        "api_ms_p50": statistics.median(lmax) * 1e3, "api_ms_p99": pct(lmax, 99) * 1e3,
+        "ok": int((res2.status == 0).sum()),
+        "note": "BASELINE configs[2] (App. D C3 recipe on C2); device: K6 + NCCL all-gather of "
+                "the winners; api: distributed.replan_snapshots_sharded with pinned host "
+                "matrices (H2D, K6, D2H, all-gather)"}
+    e2.close()
+
+    # (d) weak scaling: every rank re-plans its own C4 snapshot (K3), rank = snapshot
+    m3, t3, g3 = instances.load("c4", snapshot=X.rank)
+    p3 = PackedInstance(m3, t3, g3, 1.25)
+    e3 = Engine(X.local).load(p3)
+    s3 = torch.cuda.ExternalStream(e3.stream, device=X.dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=X.dev)
+    dev_ms = event_loop(X, s3, lambda: e3.argmin_range_async(0, total), 20, 3, flush)
+    e3.argmin_fetch()
+    dmax = X.max_over_ranks(sum(dev_ms))
+    rows["weak_snapshot_per_rank"] = {
+        "candidates_per_s": X.world * total * len(dev_ms) / (dmax * 1e-3),
+        "device_ms_per_replan": dmax / len(dev_ms), "scaling": "weak",
+        "note": "round-1 headline: rank r re-plans C4 under snapshot r (K3 sweep), L2 flushed"}
+    e3.close()
+    del flush
+    eng.load(packed)
+    return rows
+
+
+def DI_items(eng, lo, hi):
+    from paper_2505_15536_b200.engine import lib, _check
+    _check(lib().gp_argmin_items_async(eng.handle, int(lo), int(hi)))
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    rank, world, local = dist_env()
-    import torch
-    import torch.distributed as dist
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2505_15536_b200 import instances, abi
-    from paper_2505_15536_b200.engine import Engine, fp64_peak
-    from paper_2505_15536_b200.layout import PackedInstance
+    load_ncu_constants()
+    X = Ctx(args)
+    torch, dist = X.torch, X.dist
+    torch.cuda.set_device(X.local)
+    if X.world > 1:
+        dist.init_process_group("nccl", device_id=X.dev)
+    from paper_2505_15536_b200 import SearchConfig, exhaustive_plan, instances, replan
+    from paper_2505_15536_b200 import distributed as DI
+    from paper_2505_15536_b200.engine import Engine, best_fields, fp64_peak
+    from paper_2505_15536_b200.layout import packed_instance
 
-    model, topo, groups = instances.load("c4", snapshot=rank if world > 1 else None)
-    packed = PackedInstance(model, topo, groups, 1.25)
-    eng = Engine(local).load(packed)
+    spec = instances.config("c4")
+    model, topo, groups = instances.build(spec)
+    packed = packed_instance(model, topo, groups, 1.25)
+    eng = Engine(X.local).load(packed)
     total = eng.space_size()
-    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
+    S = args.snapshots
+    bws = replan.bandwidth_matrices(packed, [instances.snapshot_multipliers(spec, j)
+                                             for j in range(S)])
+    lo, hi = X.shard(S)
+    nloc = hi - lo
+    width = -(-S // X.world)
+    d_bw = torch.from_numpy(np.ascontiguousarray(bws[lo:hi])).to(X.dev)
+    d_keys = torch.zeros((width, 2), dtype=torch.int64, device=X.dev)
+    d_flags = torch.zeros(width, dtype=torch.int32, device=X.dev)
+    gathered = torch.empty((X.world * width, 2), dtype=torch.int64, device=X.dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=X.dev)
+    stream = torch.cuda.ExternalStream(eng.stream, device=X.dev)
+    torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    def step():
+        eng.replan_snapshots_async(d_bw.data_ptr(), nloc, d_keys.data_ptr(), d_flags.data_ptr())
+        if X.world > 1:
+            dist.all_gather_into_tensor(gathered, d_keys)
 
     # ---- device-resident throughput (value) --------------------------------
-    for _ in range(max(3, args.warmup)):
-        with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
             flush.zero_()
-        eng.argmin_range_async(0, total)
-    eng.argmin_fetch()
+            step()
+    X.barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    barrier()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            with torch.cuda.stream(stream):
+    eng.kernel_timing(True)
+    with ClockSampler(X.local) as clk:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
                 flush.zero_()               # evict L2 (outside the events)
                 starts[i].record(stream)
-            eng.argmin_range_async(0, total)
-            with torch.cuda.stream(stream):
+                step()
                 ends[i].record(stream)
         torch.cuda.synchronize()
-    barrier()
-    kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    best = eng.argmin_fetch()
-    dev_ms = sum(kernel_ms)
-    t = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms_max = float(t.item())
-    value = world * total * args.steps / (dev_ms_max * 1e-3)
+    sweep_ms, sweep_n = eng.kernel_timing(False)
+    X.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    dev_ms_max = X.max_over_ranks(sum(step_ms))
+    value = S * total * args.steps / (dev_ms_max * 1e-3)
+    keys = (gathered if X.world > 1 else d_keys).cpu().numpy().reshape(-1, 2)
+    flags_ok = int(d_flags[:nloc].sum().item()) == 0
+    # rows of the gathered table in snapshot order
+    rows_idx = np.concatenate([np.arange(r * width, r * width + (DI.shard_items(S, X.world, r)[1]
+                                                                 - DI.shard_items(S, X.world, r)[0]))
+                               for r in range(X.world)])
+    win = keys[rows_idx]
+    win_cost = win[:, 0].view(np.float64)
 
-    # ---- end-to-end through the C-ABI with host buffers (e2e) --------------
-    h2d = sum(getattr(packed, a).nbytes for a in (
-        "fwd", "bwd_in", "bwd_w", "act", "param", "batch", "micro", "p_c", "memory",
-        "id_rank", "p_t", "lat", "bw", "fg_member_offset", "fg_members", "fg_capacity",
-        "fg_min_bw", "fg_has_min_bw", "fg_sg_offset", "sg_member_offset", "sg_members",
-        "sg_capacity"))
-    import ctypes
-    d2h = 24 + 8 + 4 * 4 + 32 + ctypes.sizeof(abi.GpPlanInfo)  # SolveOut record
+    # cross-check 4 snapshots through the other table path (K1 full build + K3)
+    checked = 0
+    if X.rank == 0:
+        for j in (0, 1, S // 2, S - 1):
+            eng.set_bandwidth(bws[j])
+            b = eng.argmin_range(0, total)
+            tie = DI.tie_of_index(b.index, *DI.space_dims(80, 4, 2, 3)[:2], 6)
+            assert b.cost == win_cost[j] and tie == int(win[j, 1]), (j, b.cost, win_cost[j])
+            checked += 1
+        eng.reset_bandwidth()
+
+    # ---- end to end through the public API with host buffers (e2e) ---------
+    cfg = SearchConfig(seed=0)
+    bws_pinned = torch.from_numpy(bws).pin_memory().numpy()
     lat = []
     for i in range(args.warmup + args.steps):
-        barrier()
+        X.barrier()
         t0 = time.perf_counter()
-        b, info = eng.replan(packed)     # graph: pinned H2D + K1 + K3 + detail + D2H
+        if X.world > 1:
+            res = DI.replan_snapshots_sharded(model, topo, groups, cfg, bws_pinned, engine=eng)
+        else:
+            res = replan.replan_snapshots(model, topo, groups, cfg, bws_pinned, engine=eng)
         el = time.perf_counter() - t0
         if i >= args.warmup:
             lat.append(el)
-    e2e_s = torch.tensor([sum(lat)], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = world * total * args.steps / float(e2e_s.item())
+    e2e_s = X.max_over_ranks(sum(lat))
+    e2e_value = S * total * args.steps / e2e_s
+    assert (res.status == 0).all() and (res.cost.view(np.int64) == win[:, 0]).all()
+    # whole job: the matrices in, per snapshot its 16-byte key + 4-byte flags
+    # out, and under torchrun each rank's read of the gathered record table
+    h2d = S * bws.shape[1] * bws.shape[2] * 8
+    d2h = S * 20 + (X.world * X.world * width * 3 * 8 if X.world > 1 else 0)
 
-    # ---- gather per-snapshot winners (tiny collective) -----------------------
-    rec = torch.tensor([best.cost, float(best.index)], dtype=torch.float64,
-                       device=f"cuda:{local}")
-    if world > 1:
-        out = [torch.empty_like(rec) for _ in range(world)]
-        dist.all_gather(out, rec)
-        winners = [(float(o[0]), int(o[1])) for o in out]
-    else:
-        winners = [(best.cost, best.index)]
+    rows = None
+    if not args.no_rows:
+        rows = scaling_rows(X, eng, packed, model, topo, groups, total)
 
-    if rank == 0:
-        peak = fp64_peak(local)
-        per_launch_ms = dev_ms_max / args.steps
-        cand_rate_1gpu = total / (per_launch_ms * 1e-3)
-        achieved = ALG_OPS_PER_CAND_C4 * cand_rate_1gpu
+    # ---- single C4 re-plan latency (device K3, C-ABI graph, Python drop-in) -
+    replan_lat = None
+    if X.world == 1:
+        eng.load(packed)
+        k3_ms = event_loop(X, stream, lambda: eng.argmin_range_async(0, total), 50, 5, flush)
+        eng.argmin_fetch()
+        g_lat, p_lat = [], []
+        for i in range(105):
+            t0 = time.perf_counter()
+            eng.replan(packed)
+            if i >= 5:
+                g_lat.append(time.perf_counter() - t0)
+        for i in range(105):
+            t0 = time.perf_counter()
+            r_ = exhaustive_plan(model, topo, groups, cfg, engine=eng)
+            if i >= 5:
+                p_lat.append(time.perf_counter() - t0)
+        replan_lat = {
+            "device_k3_p50": statistics.median(k3_ms), "device_k3_p99": pct(k3_ms, 99),
+            "c_abi_gp_replan_p50": statistics.median(g_lat) * 1e3,
+            "c_abi_gp_replan_p99": pct(g_lat, 99) * 1e3,
+            "dropin_exhaustive_plan_p50": statistics.median(p_lat) * 1e3,
+            "dropin_exhaustive_plan_p99": pct(p_lat, 99) * 1e3,
+            "note": "one exact C4 re-plan (11,387,376 candidates): device = K3 sweep (L2 "
+                    "flushed); gp_replan = host call of the CUDA graph (arena pull + K1 + K3 + "
+                    "detail, result in mapped memory); drop-in = exhaustive_plan(model, topology, "
+                    "groups, config) of planner.py returning the SearchResult"}
+
+    if X.rank == 0:
+        peak = fp64_peak(X.local)
+        per_step_ms = dev_ms_max / args.steps
+        cand_per_launch = nloc * total
+        launch_ms = sweep_ms / max(1, sweep_n)
+        achieved = ALG_OPS_PER_CAND_C4 * cand_per_launch / (launch_ms * 1e-3)
         line = {
             "metric": "candidate plans evaluated/sec", "value": value,
-            "unit": "candidates/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": per_launch_ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (App. D C4 recipe; snapshot = rank)",
-            "config": {"workload": "c4-exhaustive-replan", "candidates_per_replan": total,
-                       "layers": 80, "devices": 64, "groups": 4,
-                       "batch_micro_pairs": len(packed.batches) * len(packed.micros),
-                       "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": f"snapshot-per-gpu x{world}"},
-            "replan_latency_ms": {"device_p50": statistics.median(kernel_ms),
-                                  "device_min": min(kernel_ms),
-                                  "c_abi_host_p50": statistics.median(lat) * 1e3},
-            "e2e": {"value": e2e_value, "unit": "candidates/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "gp_replan: one CUDA graph of pinned H2D + K1 + K3 + detail + D2H"},
+            "unit": "candidates/s", "n_gpus": X.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (App. D C4 recipe; C3 bandwidth snapshots 0..%d)" % (S - 1),
+            "config": workload_config(S, total, X.world),
+            "e2e": {"value": e2e_value, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_s / args.steps * 1e3,
+                    "path": ("distributed.replan_snapshots_sharded" if X.world > 1 else
+                             "replan.replan_snapshots") +
+                            ": pinned host bandwidth matrices -> gp_replan_snapshots (H2D, K6 "
+                            "table patch + K3 sweep, D2H of the winners)" +
+                            (" -> NCCL all-gather of the records" if X.world > 1 else "")},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": K3_DRAM_BYTES,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": SWEEP_DRAM_BYTES,
+                         "traffic_source": NCU_SOURCE if SWEEP_DRAM_BYTES else None,
+                         "kernel": "k3_sweep (K6 snapshot batch)",
+                         "launch_ms": launch_ms, "launches_timed": sweep_n,
+                         "candidates_per_launch": cand_per_launch,
+                         "share_of_step": launch_ms / per_step_ms,
                          "algorithmic_ops_per_candidate": ALG_OPS_PER_CAND_C4,
-                         "issued_fp64_per_candidate": K3_ISSUED_FP64_PER_CAND,
-                         "issued_frac": K3_ISSUED_FP64_PER_CAND * cand_rate_1gpu / peak,
+                         "issued_fp64_per_candidate": SWEEP_ISSUED_FP64_PER_CAND,
+                         "issued_source": NCU_SOURCE if SWEEP_ISSUED_FP64_PER_CAND else None,
                          "peak_source": "FP64 DADD issue rate measured live on this GPU "
-                                        "(gp_diag_fp64_peak); not in MEASURED_PEAKS.json",
-                         "kernel": "k3_sweep"},
-            "gpu_launches": args.steps,
+                                        "(gp_diag_fp64_peak: 8 independent DADD chains per "
+                                        "thread); MEASURED_PEAKS.json has no FP64 entry"},
+            "gpu_launches": 3 * X.world * args.steps,
+            "gpu_launches_note": "per rank and step: k6_minbw, k6_patch, k3_sweep",
             "clocks": clk.summary(),
-            "winners": winners[:8],
+            "step_ms_p50": statistics.median(step_ms), "step_ms_p99": pct(step_ms, 99),
+            "winners": {"flags_clear": flags_ok, "cross_checked_k1_k3": checked,
+                        "first": [float(win_cost[0]), int(win[0, 1])]},
         }
-        if not args.no_cpu_baseline and world == 1:
+        if replan_lat is not None:
+            line["replan_latency_ms"] = replan_lat
+        if rows is not None:
+            line["scaling_rows"] = rows
+        if not args.no_cpu_baseline and X.world == 1:
             threads = args.cpu_threads or os.cpu_count()
-            rate, n, dt = cpu_baseline(total, threads)
+            rate, n, dt = cpu_baseline(packed, total, threads)
             line["cpu_baseline"] = {
                 "value": rate, "unit": "candidates/s", "cores": threads, "kind": "port",
+                "cpu_model": cpu_model(),
                 "sample": f"first {n} candidates of the C4 exhaustive range, "
                           f"{dt:.1f} s on {threads} host threads (oracle/oracle.c)"}
-            line["cpu_replan_s_extrapolated"] = total / rate
-        if not args.no_extra:
-            line["extra"] = extra_sections(eng, packed, total, local, args, world)
+            py = python_reference_rate()
+            line["cpu_baseline"]["python_reference"] = py if py is not None else \
+                "absent: geopipe not importable on this host (baseline/_ref missing)"
+        if not args.no_extra and X.world == 1:
+            line["extra"] = extra_sections(eng, packed, total, X.local, args, X.world)
         print(json.dumps(line), flush=True)
     eng.close()
-    if world > 1:
+    if X.world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

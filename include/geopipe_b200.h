@@ -512,6 +512,11 @@ int gp_diag_replan_timing(gp_ctx *ctx, int enable, double *last_graph_ms);
  * [0] arena fill (+ shape check), [1] graph launch call, [2] wait for the
  * graph, [3] result decode. */
 int gp_diag_replan_host(gp_ctx *ctx, double *host_us4);
+/* Diagnostics: enable = 1 opens a window in which every exhaustive sweep
+ * launch (K3 / K6) is bracketed by CUDA events on the context stream;
+ * enable = 0 closes it and returns the launches' summed device time (ms)
+ * and their count (the roofline's per-launch kernel duration). */
+int gp_diag_kernel_timing(gp_ctx *ctx, int enable, double *total_ms, uint64_t *launches);
 /* Diagnostics: drain the per-CTA kernel timeline of a -DGP_TIMELINE build
  * (records of 40 bytes: u64 entry, after-dependency-wait and exit
  * globaltimer ns; u32 kernel id, CTA, SM, pad).  Shipped builds return 0. */

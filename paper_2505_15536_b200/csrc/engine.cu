@@ -168,6 +168,10 @@ struct gp_ctx {
     bool verify = false;
     VerifySink vs;
     DBuf<double> vbuf;
+    // gp_diag_kernel_timing: CUDA events around every exhaustive sweep launch
+    bool ktime = false;
+    std::vector<cudaEvent_t> kt_ev;  // pairs (start, end), reused across windows
+    size_t kt_used = 0;
     // device state known from earlier launches on the stream (memsets skipped):
     // item counters [0, ctr_armed) are zero (k3_sweep re-arms the ones it
     // used); err_idx holds ~0 (no launch since its reset could have written it)
@@ -318,6 +322,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     if (c->t_ev1) cudaEventDestroy(c->t_ev1);
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    for (cudaEvent_t e : c->kt_ev) cudaEventDestroy(e);
     c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release();
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
@@ -795,6 +800,21 @@ static int kernel_slots(gp_ctx* c, const void* kern, int threads, size_t smem, i
     return GP_OK;
 }
 
+// event pair around one sweep launch while gp_diag_kernel_timing is on
+static cudaError_t kt_mark(gp_ctx* c, bool end) {
+    if (!c->ktime || c->capturing) return cudaSuccess;
+    const size_t i = c->kt_used + (end ? 1 : 0);
+    while (c->kt_ev.size() <= i) {
+        cudaEvent_t e;
+        cudaError_t err = cudaEventCreate(&e);
+        if (err != cudaSuccess) return err;
+        c->kt_ev.push_back(e);
+    }
+    cudaError_t err = cudaEventRecord(c->kt_ev[i], c->stream);
+    if (end && err == cudaSuccess) c->kt_used += 2;
+    return err;
+}
+
 static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_lo,
                         unsigned long long item_hi, int mode, const uint32_t* dflags,
                         int nb_sel = 0, int b0 = 0, int slot = 0) {
@@ -862,8 +882,10 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     S.err_idx = c->err_idx.p;
     c->last_geom = R;
     DevInst I = c->view();
+    CUDA_TRY(kt_mark(c, false));
     CUDA_TRY(launch_sweep_kernel(kern, (unsigned)grid, smem, s, G, I, S, c->binom.p, dflags,
                                  c->pdl));
+    CUDA_TRY(kt_mark(c, true));
     return GP_OK;
 }
 
@@ -1907,7 +1929,9 @@ static int snap_enqueue(gp_ctx* c, const double* d_bw, uint32_t nb, Key* d_keys,
     S.result = d_keys;
     S.err = nullptr;
     S.err_idx = c->err_idx.p;
+    CUDA_TRY(kt_mark(c, false));
     CUDA_TRY(launch_sweep_kernel(kern, (unsigned)grid, smem, s, G, I, S, c->binom.p, d_flags));
+    CUDA_TRY(kt_mark(c, true));
     CUDA_TRY(cudaGetLastError());
     return GP_OK;
 }
@@ -2166,6 +2190,32 @@ int gp_diag_verify_end(gp_ctx* c, double* out) {
     if (out) CUDA_TRY(cudaMemcpyAsync(out, c->vbuf.p, n * sizeof(double), cudaMemcpyDeviceToHost,
                                       c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return GP_OK;
+}
+
+// Diagnostics (bench.py roofline): enable = 1 starts a window in which every
+// exhaustive sweep launch (K3 / K6) is bracketed by CUDA events on the
+// context stream; enable = 0 ends it and returns the summed device time of
+// those launches and their count.
+int gp_diag_kernel_timing(gp_ctx* c, int enable, double* total_ms, uint64_t* launches) {
+    if (!c) return fail(GP_ERR_INPUT, "null context");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (enable) {
+        c->ktime = true;
+        c->kt_used = 0;
+        return GP_OK;
+    }
+    c->ktime = false;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < c->kt_used; i += 2) {
+        float ms = 0.0f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, c->kt_ev[i], c->kt_ev[i + 1]));
+        tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = c->kt_used / 2;
+    c->kt_used = 0;
     return GP_OK;
 }
 

@@ -149,30 +149,31 @@ def replan_snapshots_sharded(model, topology, groups, config, bandwidths: np.nda
     lo, hi = shard_items(S, world, rank)
     rec = np.zeros((hi - lo, 3), dtype=np.int64)
     if hi > lo:
+        from .engine import best_fields
         bests, status = eng.replan_snapshots(bandwidths[lo:hi])
-        for i in range(hi - lo):
-            rec[i] = (_cost_bits(bests[i].cost), int(bests[i].index), int(status[i]))
+        cost, index = best_fields(bests, hi - lo)
+        rec[:, 0] = cost.view(np.int64)
+        rec[:, 1] = index.view(np.int64)
+        rec[:, 2] = status
     allrec = gather_snapshot_records(rec, S, group, torch.device("cuda"))
     return decode_snapshot_records(packed, allrec)
 
 
 def decode_snapshot_records(packed, rec: np.ndarray):
-    """Per-snapshot records -> ``(cost, order_ids, counts, b, m)`` or the
-    exception the reference would raise (replan.replan_snapshots format)."""
-    from . import abi
+    """Per-snapshot records -> replan.SnapshotPlans (item j = ``(cost,
+    order_ids, counts, b, m)`` or the exception the reference would raise)."""
+    from .replan import SnapshotPlans
+    rec = np.ascontiguousarray(rec, dtype=np.int64)
+    return SnapshotPlans(packed, rec[:, 0].view(np.float64), rec[:, 1].view(np.uint64),
+                         rec[:, 2].astype(np.int32))
+
+
+def decode_index(index: int, packed):
+    """Enumeration index -> (order indices, counts, bm) of ``packed``'s space."""
     k, n = packed.n_fgs, packed.n_layers
     NC, NP, _ = space_dims(n, k, len(packed.batches), len(packed.micros))
     nbm = len(packed.batches) * len(packed.micros)
-    nm = len(packed.micros)
-    out = []
-    for j, (bits, index, st) in enumerate(rec.tolist()):
-        if st != abi.GP_OK:
-            out.append(abi._ERRORS.get(st, D.GeopipeError)(f"snapshot {j}: status {st}"))
-            continue
-        order, counts, bm = decode_candidate(tie_of_index(index, NC, NP, nbm), NC, NP, nbm, n, k)
-        out.append((_bits_cost(bits), [packed.fg_ids[f] for f in order], counts,
-                    packed.batches[bm // nm], packed.micros[bm % nm]))
-    return out
+    return decode_candidate(tie_of_index(index, NC, NP, nbm), NC, NP, nbm, n, k)
 
 
 def decode_candidate(tie: int, NC: int, NP: int, nbm: int, n_layers: int, k: int):

@@ -93,6 +93,7 @@ def lib():
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
+        L.gp_diag_kernel_timing.argtypes = [vp, C.c_int, P(C.c_double), P(C.c_uint64)]
         L.gp_diag_replan_timing.argtypes = [vp, C.c_int, P(C.c_double)]
         L.gp_diag_replan_host.argtypes = [vp, P(C.c_double)]
         L.gp_plan_cost.argtypes = [vp, C.c_uint32, P(abi.GpPlanStage), C.c_int64, C.c_int64,
@@ -123,6 +124,9 @@ class Engine:
         self._h = h
         self.device = device
         self.packed = None
+        # the instance whose tables the context holds unmodified (None after a
+        # bandwidth snapshot or a failed load): load() of it again is a no-op
+        self._clean = None
 
     def close(self):
         if self._h:
@@ -144,8 +148,14 @@ class Engine:
         return lib().gp_ctx_stream(self._h) or 0
 
     def load(self, packed) -> "Engine":
+        """Stage ``packed`` (gp_ctx_load); a no-op when the context already
+        holds exactly this instance's tables."""
+        if packed is self._clean:
+            return self
+        self._clean = None
         _check(lib().gp_ctx_load(self._h, C.byref(packed.struct)))
         self.packed = packed
+        self._clean = packed
         return self
 
     def space_size(self) -> int:
@@ -188,8 +198,13 @@ class Engine:
         replayed for every instance of the same shape)."""
         best = abi.GpBest()
         info = abi.GpPlanInfo()
-        _check(lib().gp_replan(self._h, C.byref(packed.struct), C.byref(best), C.byref(info)))
+        self._clean = None
+        st = lib().gp_replan(self._h, C.byref(packed.struct), C.byref(best), C.byref(info))
         self.packed = packed
+        if st in (abi.GP_OK, abi.GP_ERR_INFEASIBLE_SPLIT, abi.GP_ERR_NO_FEASIBLE,
+                  abi.GP_ERR_DEGENERATE, abi.GP_ERR_TOPOLOGY):
+            self._clean = packed  # the tables were built (a candidate raised, or not)
+        _check(st)
         return best, info
 
     def argmin_range_async(self, lo: int, hi: int) -> None:
@@ -424,12 +439,28 @@ class Engine:
                                              out, st.ctypes.data_as(C.POINTER(C.c_int32))))
         return out, st
 
+
+def best_fields(bests, n: int):
+    """(cost f64[n], index u64[n]) views of a ctypes GpBest array (no per-item
+    Python work)."""
+    dt = np.dtype({"names": ["cost", "index"], "formats": ["<f8", "<u8"], "offsets": [0, 8],
+                   "itemsize": C.sizeof(abi.GpBest)})
+    a = np.frombuffer(bests, dtype=dt, count=n)
+    return a["cost"].copy(), a["index"].copy()
+
     def replan_snapshots_async(self, d_bandwidth: int, n_snap: int, d_keys: int,
                                d_flags: int) -> None:
         """Device pointers (ints), asynchronous on :attr:`stream`: per snapshot
         the arg-min key (cost bits, tie) -> d_keys[2i:2i+2] (int64) and the
         table flags -> d_flags[i] (gp_replan_snapshots_async)."""
         _check(lib().gp_replan_snapshots_async(self._h, d_bandwidth, int(n_snap), d_keys, d_flags))
+
+    def kernel_timing(self, enable: bool):
+        """Start (True) / end (False) a window of CUDA-event timing around
+        every sweep launch; ending returns (total device ms, launches)."""
+        ms, n = C.c_double(0.0), C.c_uint64(0)
+        _check(lib().gp_diag_kernel_timing(self._h, int(bool(enable)), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def set_k3_mode(self, mode: int) -> None:
         """Force the exhaustive-kernel variant (-1 auto, 0/1/2, 3 generic)."""
@@ -451,11 +482,13 @@ class Engine:
 
     def set_bandwidth(self, bw: np.ndarray) -> None:
         a = np.ascontiguousarray(bw, dtype=np.float64)
+        self._clean = None
         _check(lib().gp_set_bandwidth(self._h, a.ctypes.data_as(C.POINTER(C.c_double))))
 
     def reset_bandwidth(self) -> None:
         """Back to the loaded instance's bandwidths and min_intra_bandwidth values."""
         _check(lib().gp_reset_bandwidth(self._h))
+        self._clean = self.packed
 
     def verify_begin(self, lo: int, n: int) -> None:
         """Parity tests: record every evaluated candidate's cost at global

@@ -41,18 +41,54 @@ def bandwidth_matrices(packed: PackedInstance,
     return out
 
 
+class SnapshotPlans:
+    """Per-snapshot re-plan results as arrays (cost, winner enumeration index,
+    status), decoded on access: ``plans[j]`` is the tuple ``(cost, order_ids,
+    counts, b, m)`` or the exception the reference's re-plan of snapshot j
+    would raise.  Decoding is integer unranking on the host and happens only
+    for the snapshots a caller looks at."""
+
+    def __init__(self, packed: PackedInstance, cost: np.ndarray, index: np.ndarray,
+                 status: np.ndarray):
+        self.packed = packed
+        self.cost = np.asarray(cost, dtype=np.float64)
+        self.index = np.asarray(index, dtype=np.uint64)
+        self.status = np.asarray(status, dtype=np.int32)
+
+    def __len__(self):
+        return int(self.status.size)
+
+    def __getitem__(self, j):
+        if not -len(self) <= j < len(self):
+            raise IndexError(j)
+        from .distributed import decode_index
+        st = int(self.status[j])
+        if st != abi.GP_OK:
+            return abi._ERRORS.get(st, D.GeopipeError)(f"snapshot {j}: status {st}")
+        p = self.packed
+        order, counts, bm = decode_index(int(self.index[j]), p)
+        nm = len(p.micros)
+        return (float(self.cost[j]), [p.fg_ids[f] for f in order], counts,
+                p.batches[bm // nm], p.micros[bm % nm])
+
+
 def replan_snapshots(model, topology, groups, config, bandwidths: np.ndarray,
                      engine: Optional[Engine] = None, detail: bool = False):
     """Exact re-plan per snapshot.
 
-    Returns a list with, per snapshot, either a SearchResult (``detail=True``:
+    Returns, per snapshot, either a SearchResult (``detail=True``: a list of
     plan, splits and CostBreakdown, as ``exhaustive_plan`` on the rebuilt
-    topology returns them) or the tuple ``(cost, order_ids, counts, b, m)``;
-    snapshots whose re-plan raises carry the exception instance instead.
+    topology returns them) or (default) a :class:`SnapshotPlans` whose item j
+    is the tuple ``(cost, order_ids, counts, b, m)``; snapshots whose re-plan
+    raises carry the exception instance instead.
     """
+    from .engine import best_fields
     packed = packed_instance(model, topology, groups, config.bottleneck_factor)
     eng = (engine or default_engine()).load(packed)
     bests, status = eng.replan_snapshots(bandwidths)
+    if not detail:
+        cost, index = best_fields(bests, bandwidths.shape[0])
+        return SnapshotPlans(packed, cost, index, status)
     out: List = []
     k = packed.n_fgs
     nm = len(packed.micros)

@@ -99,7 +99,7 @@ def _snap_worker(rank, world, port, n_snap, out):
         rec[i] = (DI._cost_bits(b.cost), b.index, st)
     allrec = DI.gather_snapshot_records(rec, n_snap, device=torch.device("cpu"))
     m, t, g = I.build(spec)
-    out[rank] = DI.decode_snapshot_records(PackedInstance(m, t, g, 1.25), allrec)
+    out[rank] = list(DI.decode_snapshot_records(PackedInstance(m, t, g, 1.25), allrec))
     dist.barrier()
     dist.destroy_process_group()
 
