@@ -440,14 +440,6 @@ class Engine:
         return out, st
 
 
-def best_fields(bests, n: int):
-    """(cost f64[n], index u64[n]) views of a ctypes GpBest array (no per-item
-    Python work)."""
-    dt = np.dtype({"names": ["cost", "index"], "formats": ["<f8", "<u8"], "offsets": [0, 8],
-                   "itemsize": C.sizeof(abi.GpBest)})
-    a = np.frombuffer(bests, dtype=dt, count=n)
-    return a["cost"].copy(), a["index"].copy()
-
     def replan_snapshots_async(self, d_bandwidth: int, n_snap: int, d_keys: int,
                                d_flags: int) -> None:
         """Device pointers (ints), asynchronous on :attr:`stream`: per snapshot
@@ -501,6 +493,15 @@ def best_fields(bests, n: int):
         out = np.empty(self._verify_n, dtype=np.float64)
         _check(lib().gp_diag_verify_end(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
+
+
+def best_fields(bests, n: int):
+    """(cost f64[n], index u64[n]) views of a ctypes GpBest array (no per-item
+    Python work)."""
+    dt = np.dtype({"names": ["cost", "index"], "formats": ["<f8", "<u8"], "offsets": [0, 8],
+                   "itemsize": C.sizeof(abi.GpBest)})
+    a = np.frombuffer(bests, dtype=dt, count=n)
+    return a["cost"].copy(), a["index"].copy()
 
 
 def fp64_peak(device: int = 0) -> float:
