@@ -54,10 +54,20 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Algorithmic FP64 ops per candidate in the reference's operation order
-# (11k - 5 = 39 for k = 4 stages): 6 per stage (C1*m, M*c,
-# three adds, max) + 5 per boundary (c+x, fill+, x-c', max0, res+).
-ALG_OPS_PER_CAND_C4 = 39
+# FP64 ops per candidate of independent evaluation in the reference's operation
+# order (11k - 5 = 39 for k = 4 stages): 6 per stage (C1*m,
+# M*c, three adds, max) + 5 per boundary (c+x, fill+, x-c', max0, res+).
+REF_OPS_PER_CAND_C4 = 39
+# FP64 ops per candidate the sweep's algorithm needs: a run
+# fixes stages 0..k-3, so only the last two stages vary along q.  Per q,
+# shared by the NB batch sizes: res2 = res1 + max0(x1 - e2.c), fill3 = fill2 +
+# (e2.c + x2), res3 = res2 + max0(x2 - e3.c) = 6 adds; per (q, b): M*e2.c,
+# M*e3.c, 6 adds for t2 and t3, 2 max compares = 10; per (q, b) the run-min
+# compare = 1.  NB = 2: (6 + 2 * 11) / 2 = 14 per candidate.  39 x rate
+# exceeds the FP64 pipe peak (the prefix work is shared), so the roofline
+# uses this count; the reference-order equivalent rate is reported beside it.
+def sweep_ops_per_candidate(nb):
+    return (6 + 11 * nb) / nb
 # Measured by ncu on the sweep kernel of this workload (not in-run):
 # profiles/r2_k6_sweep_ncu_raw.csv (sm__inst_executed_pipe_fp64 / candidates
 # and dram__bytes_read.sum + dram__bytes_write.sum of one launch).
@@ -184,7 +194,7 @@ def cpu_baseline(packed, total, threads, target_s=10.0):
     return n / dt, n, dt
 
 
-def python_reference_rate(spec_name="c4", n_cand=600, procs=None):
+def python_reference_rate(spec_name="c4", n_cand=2000, procs=None):
     """The unmodified Python reference (`geopipe.planner._evaluate`, fresh cache
     per candidate, logging disabled) on a random sample of the C4 space: one
     process, and `procs` processes over contiguous shards.  None when the
@@ -200,19 +210,23 @@ def python_reference_rate(spec_name="c4", n_cand=600, procs=None):
         return None
     logging.disable(logging.CRITICAL)
     from concurrent.futures import ProcessPoolExecutor
-    rate1 = _py_ref_worker((spec_name, 0, n_cand))
+    t0, t1 = _py_ref_worker((spec_name, 0, n_cand, 0.0))
+    rate1 = n_cand / (t1 - t0)
     procs = procs or os.cpu_count() or 1
-    t = time.perf_counter()
+    start = time.time() + 6.0  # every worker has built its instance by then
     with ProcessPoolExecutor(procs) as ex:
-        list(ex.map(_py_ref_worker, [(spec_name, s + 1, n_cand) for s in range(procs)]))
-    el = time.perf_counter() - t
+        spans = list(ex.map(_py_ref_worker, [(spec_name, s + 1, n_cand, start)
+                                             for s in range(procs)]))
+    el = max(b for _, b in spans) - min(a for a, _ in spans)
     return {"value_1proc": rate1, "value_all": procs * n_cand / el, "processes": procs,
-            "unit": "candidates/s", "sample": f"{n_cand} random C4 candidates per process",
+            "unit": "candidates/s",
+            "sample": f"{n_cand} random C4 candidates per process (fresh _evaluate cache each, "
+                      "logging disabled); all processes start together",
             "source": "geopipe (unmodified reference) " + getattr(gp, "__version__", "")}
 
 
 def _py_ref_worker(args):
-    spec_name, seed, n_cand = args
+    spec_name, seed, n_cand, start = args
     import logging
     import random
     logging.disable(logging.CRITICAL)
@@ -247,10 +261,12 @@ def _py_ref_worker(args):
     cands = [(Candidate(tuple(fg[x] for x in order[i]), tuple(int(c) for c in counts[i])),
               model.global_batch_candidates[bm[i] // nm], model.microbatch_candidates[bm[i] % nm])
              for i in range(n_cand)]
-    t = time.perf_counter()
+    while time.time() < start:
+        time.sleep(0.001)
+    t = time.time()
     for c, b, m in cands:
         _evaluate(c, b, m, groups, topo, model, cfg, {})
-    return n_cand / (time.perf_counter() - t)
+    return t, time.time()
 
 
 def extra_sections(eng, packed, total, local, args, world):
@@ -873,7 +889,8 @@ def main():
         per_step_ms = dev_ms_max / args.steps
         cand_per_launch = nloc * total
         launch_ms = sweep_ms / max(1, sweep_n)
-        achieved = ALG_OPS_PER_CAND_C4 * cand_per_launch / (launch_ms * 1e-3)
+        alg_ops = sweep_ops_per_candidate(len(packed.batches))
+        achieved = alg_ops * cand_per_launch / (launch_ms * 1e-3)
         line = {
             "metric": "candidate plans evaluated/sec", "value": value,
             "unit": "candidates/s", "n_gpus": X.world, "steps": args.steps,
@@ -898,7 +915,12 @@ def main():
                          "launch_ms": launch_ms, "launches_timed": sweep_n,
                          "candidates_per_launch": cand_per_launch,
                          "share_of_step": launch_ms / per_step_ms,
-                         "algorithmic_ops_per_candidate": ALG_OPS_PER_CAND_C4,
+                         "algorithmic_ops_per_candidate": alg_ops,
+                         "algorithm": "prefix-sharing sweep (DESIGN.md §4): 14 FP64 ops per "
+                                      "C4 candidate",
+                         "reference_order_ops_per_candidate": REF_OPS_PER_CAND_C4,
+                         "reference_equivalent_tflops": REF_OPS_PER_CAND_C4 * cand_per_launch
+                         / (launch_ms * 1e-3) / 1e12,
                          "issued_fp64_per_candidate": SWEEP_ISSUED_FP64_PER_CAND,
                          "issued_source": NCU_SOURCE if SWEEP_ISSUED_FP64_PER_CAND else None,
                          "peak_source": "FP64 DADD issue rate measured live on this GPU "
