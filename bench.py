@@ -58,23 +58,18 @@ sys.path.insert(0, ROOT)
 # order (11k - 5 = 39 for k = 4 stages): 6 per stage (C1*m,
 # M*c, three adds, max) + 5 per boundary (c+x, fill+, x-c', max0, res+).
 REF_OPS_PER_CAND_C4 = 39
-# FP64 ops per candidate the sweep's algorithm needs: a run
-# fixes stages 0..k-3, so only the last two stages vary along q.  Per q,
-# shared by the NB batch sizes: res2 = res1 + max0(x1 - e2.c), fill3 = fill2 +
-# (e2.c + x2), res3 = res2 + max0(x2 - e3.c) = 6 adds; per (q, b): M*e2.c,
-# M*e3.c, 6 adds for t2 and t3, 2 max compares = 10; per (q, b) the run-min
-# compare = 1.  NB = 2: (6 + 2 * 11) / 2 = 14 per candidate.  39 x rate
-# exceeds the FP64 pipe peak (the prefix work is shared), so the roofline
-# uses this count; the reference-order equivalent rate is reported beside it.
+# FP64 ops per candidate the sweep's algorithm needs.  A run
+# fixes stages 0..k-3, so only the last two stages vary along q, and the
+# record sweep (k3_sweep_rec, the K6 batch kernel) tabulates per item the
+# terms that depend on (a, q) or q alone (D2 = max0(x1 - c2), G2 = c2 + x2,
+# D3 = max0(x2 - c3)).  Per q, shared by the NB batch sizes: res2, fill3, res3
+# = 3 adds; per (q, b): M*c2, M*c3, 6 adds for t2 and t3, 2 max compares and
+# the run-min compare = 11.  NB = 2: (3 + 2 * 11) / 2 = 12.5 per candidate
+# (the per-item tables add ~0.1).  39 x rate exceeds the FP64 pipe peak (the
+# prefix work is shared), so the roofline uses this count; the reference-
+# order equivalent rate is reported beside it.
 def sweep_ops_per_candidate(nb):
-    return (6 + 11 * nb) / nb
-# Measured by ncu on the sweep kernel of this workload (not in-run):
-# profiles/r2_k6_sweep_ncu_raw.csv (sm__inst_executed_pipe_fp64 / candidates
-# and dram__bytes_read.sum + dram__bytes_write.sum of one launch).
-NCU_SOURCE = "profiles/r2_k6_sweep_ncu_raw.csv"
-SWEEP_ISSUED_FP64_PER_CAND = None
-SWEEP_DRAM_BYTES = None
-S_TOTAL = 128
+    return (3 + 11 * nb) / nb
 
 
 def parse():
@@ -911,13 +906,13 @@ def main():
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": SWEEP_DRAM_BYTES,
                          "traffic_source": NCU_SOURCE if SWEEP_DRAM_BYTES else None,
-                         "kernel": "k3_sweep (K6 snapshot batch)",
+                         "kernel": "k3_sweep_rec<2,4> (K6 snapshot batch)",
                          "launch_ms": launch_ms, "launches_timed": sweep_n,
                          "candidates_per_launch": cand_per_launch,
                          "share_of_step": launch_ms / per_step_ms,
                          "algorithmic_ops_per_candidate": alg_ops,
-                         "algorithm": "prefix-sharing sweep (DESIGN.md §4): 14 FP64 ops per "
-                                      "C4 candidate",
+                         "algorithm": "prefix-sharing record sweep (DESIGN.md §4): 12.5 FP64 "
+                                      "ops per C4 candidate",
                          "reference_order_ops_per_candidate": REF_OPS_PER_CAND_C4,
                          "reference_equivalent_tflops": REF_OPS_PER_CAND_C4 * cand_per_launch
                          / (launch_ms * 1e-3) / 1e12,

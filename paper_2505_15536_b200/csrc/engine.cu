@@ -32,6 +32,7 @@
 #include "k1_tables.cuh"
 #include "k2_eval.cuh"
 #include "k3_argmin.cuh"
+#include "k3_sweep_rec.cuh"
 #include "detail.cuh"
 #include "k4_bnb.cuh"
 #include "k6_snapshots.cuh"
@@ -185,7 +186,8 @@ struct gp_ctx {
     DBuf<uint4> groups;       // K3 sweep run groups
     DBuf<uint8_t> prefixes;   // colex (k-3)-subsets for the sweep
     DBuf<unsigned long long> bnk;  // binomial sub-table [n+1][k+1] (TMA-staged)
-    int ngroups = 0;
+    int ngroups = 0;  // uint4 slots of `groups`: the run groups, then the task table
+    int ng = 0;       // run groups
     unsigned int sweep_W = 0;
     bool sweep_ok = false;
 
@@ -567,8 +569,21 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
             for (int a = 0; a <= nn; ++a)
                 for (int r = 0; r <= k; ++r) bk[(size_t)a * (k + 1) + r] = h_binom(a, r);
             CUDA_TRY(upload(s, c->bnk, bk.data(), bk.size()));
+            // task t (runs 32t .. 32t+31) -> group of its first run, u16,
+            // appended after the groups (one staged block)
+            const int ng = (int)g.size();
+            const unsigned long long ntask = (start + 31) / 32;
+            std::vector<uint16_t> tg((size_t)ntask + 8, 0);
+            for (unsigned long long t = 0, gi = 0; t < ntask; ++t) {
+                while (gi + 1 < g.size() && g[gi + 1].x <= t * 32) ++gi;
+                tg[t] = (uint16_t)gi;
+            }
+            const size_t tslots = ((size_t)ntask * 2 + 15) / 16;
+            g.resize(g.size() + tslots);
+            memcpy(&g[ng], tg.data(), tslots * 16 <= tg.size() * 2 ? tslots * 16 : tg.size() * 2);
             CUDA_TRY(upload(s, c->groups, g.data(), g.size()));
             c->ngroups = (int)g.size();
+            c->ng = ng;
             c->sweep_W = (unsigned)start;
             c->sweep_ok = true;
         }
@@ -735,6 +750,25 @@ static SwFn pick_sweep(int mode, int nb, int k) {
     return (mode == 2 && k >= 3 && k <= 6) ? fixed[nb - 1][k - 3] : table[mode][nb - 1];
 }
 
+// record sweep (k3_sweep_rec.cuh) for k = 3..6, when its shared memory fits
+// and each CTA owns a whole item (the per-item record build is then paid
+// once per item; GP_K3_REC=0 disables, force_mode 5 forces it); nullptr
+// otherwise
+static SwFn pick_sweep_rec(gp_ctx* c, int nb, int k, size_t* smem) {
+    static const SwFn table[4][4] = {
+        {k3_sweep_rec<1, 3>, k3_sweep_rec<1, 4>, k3_sweep_rec<1, 5>, k3_sweep_rec<1, 6>},
+        {k3_sweep_rec<2, 3>, k3_sweep_rec<2, 4>, k3_sweep_rec<2, 5>, k3_sweep_rec<2, 6>},
+        {k3_sweep_rec<3, 3>, k3_sweep_rec<3, 4>, k3_sweep_rec<3, 5>, k3_sweep_rec<3, 6>},
+        {k3_sweep_rec<4, 3>, k3_sweep_rec<4, 4>, k3_sweep_rec<4, 5>, k3_sweep_rec<4, 6>}};
+    static const int enabled = [] { const char* e = getenv("GP_K3_REC"); return e ? atoi(e) : 1; }();
+    if (!enabled || k < 3 || k > 6 || nb < 1 || nb > 4) return nullptr;
+    if (c->force_mode >= 0 && c->force_mode != 5) return nullptr;  // diagnostics pick a variant
+    const size_t need = k3r_smem(c->n, k, c->ngroups);
+    if (need > (size_t)c->smem_max) return nullptr;
+    *smem = need;
+    return c->verify ? pick_sweep_rec_verify(nb, k) : table[nb - 1][k - 3];
+}
+
 // Sweep launch.  With GP_K3_CLUSTER=c (2 or 4, dividing the CTAs per item)
 // the CTAs of one item form a thread-block cluster and the item's tables are
 // fetched once and multicast into every member (TMA .multicast::cluster).
@@ -830,6 +864,8 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
     SwFn kern = c->verify ? pick_sweep_verify(mode, nb_sel > 0 ? nb_sel : c->nb, k)
                           : pick_sweep(mode, nb_sel > 0 ? nb_sel : c->nb, k);
+    if (c->force_mode == 5)  // whole items per CTA only in large batches (K6)
+        if (SwFn r = pick_sweep_rec(c, nb_sel > 0 ? nb_sel : c->nb, k, &smem)) kern = r;
     int per_sm = 0;
     { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
       if (st_ != GP_OK) return st_; }
@@ -853,6 +889,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     G.cpi = cpi;
     G.W = c->sweep_W;
     G.ngroups = c->ngroups;
+    G.ng = c->ng;
     G.groups = c->groups.p;
     G.prefixes = c->prefixes.p;
     G.bnk = c->bnk.p;
@@ -1879,7 +1916,7 @@ static int snap_enqueue(gp_ctx* c, const double* d_bw, uint32_t nb, Key* d_keys,
     Z.tpk = c->z_tpk.p; Z.tcol = c->z_tcol.p; Z.xt = c->z_xt.p;
     Z.s_tpk = s_tpk; Z.s_tcol = s_tcol; Z.s_xt = s_xt;
     DevInst I = c->view();
-    k6_minbw<<<(unsigned)((nb * c->F + 127) / 128), 128, 0, s>>>(I, Z);
+    k6_minbw<<<(unsigned)((nb * c->F * 32 + 127) / 128), 128, 0, s>>>(I, Z);
     const long long work = (long long)(s_tpk + (size_t)c->nm * c->F * c->F * n);
     dim3 pg((unsigned)((work + 255) / 256), nb);
     k6_patch<<<pg, 256, 0, s>>>(I, Z);
@@ -1892,6 +1929,8 @@ static int snap_enqueue(gp_ctx* c, const double* d_bw, uint32_t nb, Key* d_keys,
     if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
     SwFn kern = c->verify ? pick_sweep_verify(mode, c->nb, k) : pick_sweep(mode, c->nb, k);
+    if ((mode == 2 && items * nb >= 2ull * c->n_sms) || c->force_mode == 5)
+        if (SwFn r = pick_sweep_rec(c, c->nb, k, &smem)) kern = r;
     int per_sm = 0;
     { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
       if (st_ != GP_OK) return st_; }
@@ -1906,7 +1945,7 @@ static int snap_enqueue(gp_ctx* c, const double* d_bw, uint32_t nb, Key* d_keys,
     SweepGeom G;
     G.b0 = 0;
     G.k = k; G.nbm = c->nb * c->nm; G.NC = NC; G.NP = NP; G.item0 = 0; G.cpi = cpi;
-    G.W = c->sweep_W; G.ngroups = c->ngroups; G.groups = c->groups.p;
+    G.W = c->sweep_W; G.ngroups = c->ngroups; G.ng = c->ng; G.groups = c->groups.p;
     G.prefixes = c->prefixes.p;
     G.bnk = c->bnk.p;
     G.gsteps = 1;
@@ -2220,7 +2259,7 @@ int gp_diag_kernel_timing(gp_ctx* c, int enable, double* total_ms, uint64_t* lau
 }
 
 int gp_ctx_set_k3_mode(gp_ctx* c, int mode) {
-    if (!c || mode < -1 || mode > 4) return fail(GP_ERR_INPUT, "bad mode");
+    if (!c || mode < -1 || mode > 5) return fail(GP_ERR_INPUT, "bad mode");
     c->force_mode = mode;
     return GP_OK;
 }

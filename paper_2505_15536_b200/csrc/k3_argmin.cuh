@@ -245,8 +245,9 @@ struct SweepGeom {
     unsigned long long item0;       // first (mi * NP + perm) item
     unsigned long long cpi;         // CTAs per item
     unsigned int W;                 // runs per item
-    int ngroups;
-    const uint4* groups;            // [ngroups]
+    int ngroups;                    // uint4 slots staged: the run groups + the task table
+    int ng;                         // run groups
+    const uint4* groups;            // [ng] groups, then u16 task -> group of its first run
     unsigned int* item_ctr;         // per-item task counters
     const uint8_t* prefixes;        // colex-ordered (k-3)-subsets, 16-byte records
     int gsteps;                     // largest power of two <= ngroups
@@ -400,18 +401,18 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
         double mx1[NB];
         unsigned long long rpre = 0;  // comp rank of (prefix, a, q = a + 1)
         if (u < G.W) {
-            // run id -> group (fixed-trip binary search), prefix row, segment
-            int gi = 0;
-            for (int step = G.gsteps; step > 0; step >>= 1) {
-                int mid = gi + step;
-                if (mid < G.ngroups && grp[mid].x <= u) gi = mid;
-            }
+            // run id -> group (from the task's first group, a few steps at
+            // most), prefix row, segment; full-length groups are segment-major
+            // so the lanes of a warp share (a, q) and read the same shared-
+            // memory words (broadcast)
+            int gi = ((const uint16_t*)(grp + G.ng))[t];
+            while (gi + 1 < G.ng && grp[gi + 1].x <= u) ++gi;
             const uint4 g = grp[gi];
             const unsigned int local = u - g.x;
             a = (int)(g.y & 0xffffu);
             len = (int)(g.y >> 16);
             unsigned int row;
-            if (g.w) { row = local / g.w; q0 = a + 1 + (int)(local % g.w) * K3_SEG; }
+            if (g.w) { const unsigned seg = local / g.z; row = local - seg * g.z; q0 = a + 1 + (int)seg * K3_SEG; }
             else { row = local; q0 = n - len; }
             // prefix cuts p[1..k-3]: colex row `row` (subsets of [1, a-1] come first)
             int p[GP_MAX_STAGES + 1];

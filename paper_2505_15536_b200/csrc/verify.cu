@@ -4,6 +4,7 @@
 // (gp_diag_verify_begin / _end).  A separate translation unit so that the
 // doubled instantiation set compiles in parallel with engine.cu.
 #include "k3_argmin.cuh"
+#include "k3_sweep_rec.cuh"
 #include "verify.h"
 
 SwFn pick_sweep_verify(int mode, int nb, int k) {
@@ -25,4 +26,13 @@ K3Fn pick_argmin_verify(int mode, int nb) {
         {k3_argmin<1, 1, true>, k3_argmin<1, 2, true>, k3_argmin<1, 3, true>, k3_argmin<1, 4, true>},
         {k3_argmin<2, 1, true>, k3_argmin<2, 2, true>, k3_argmin<2, 3, true>, k3_argmin<2, 4, true>}};
     return table[mode][nb - 1];
+}
+
+SwFn pick_sweep_rec_verify(int nb, int k) {
+    static const SwFn table[4][4] = {
+        {k3_sweep_rec<1, 3, true>, k3_sweep_rec<1, 4, true>, k3_sweep_rec<1, 5, true>, k3_sweep_rec<1, 6, true>},
+        {k3_sweep_rec<2, 3, true>, k3_sweep_rec<2, 4, true>, k3_sweep_rec<2, 5, true>, k3_sweep_rec<2, 6, true>},
+        {k3_sweep_rec<3, 3, true>, k3_sweep_rec<3, 4, true>, k3_sweep_rec<3, 5, true>, k3_sweep_rec<3, 6, true>},
+        {k3_sweep_rec<4, 3, true>, k3_sweep_rec<4, 4, true>, k3_sweep_rec<4, 5, true>, k3_sweep_rec<4, 6, true>}};
+    return table[nb - 1][k - 3];
 }

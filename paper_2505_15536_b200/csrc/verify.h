@@ -9,3 +9,4 @@ typedef void (*K3Fn)(DevInst, RangeGeom, ArgminScratch, const unsigned long long
                      const uint32_t*);
 SwFn pick_sweep_verify(int mode, int nb, int k);
 K3Fn pick_argmin_verify(int mode, int nb);
+SwFn pick_sweep_rec_verify(int nb, int k);

@@ -195,7 +195,7 @@ def test_k3_interleaved_calls_rearm_state(engine):
         assert engine.argmin_range(0, N).index == full
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("name", ["c1j", "c2", "c2j", "rand5", "rand10", "rand6", "small"])
 def test_k3_all_kernel_variants_agree(engine, name, mode):
     doc, model, topo, groups, packed = _load(engine, name)
@@ -216,7 +216,7 @@ def test_k3_all_kernel_variants_agree(engine, name, mode):
         engine.set_k3_mode(-1)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
 def test_k3_c4_variants(engine, mode):
     doc, model, topo, groups, packed = _load(engine, "c4j")
     try:

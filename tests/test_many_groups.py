@@ -55,7 +55,7 @@ def _golden_argmin(packed, gc, gs):
     return i, gc[i]
 
 
-@pytest.mark.parametrize("mode", [-1, 0, 1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [-1, 0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("name", SMALL)
 def test_small_argmin_every_kernel(engine, name, mode):
     doc, model, topo, groups, packed = _load(engine, name)
@@ -108,7 +108,7 @@ def test_big_sample_k2_vs_reference(engine, oracle_lib, name):
     assert same_bits(cost[ok], exp[ok]).all()
 
 
-@pytest.mark.parametrize("mode", [-1, 0, 1, 3])
+@pytest.mark.parametrize("mode", [-1, 0, 1, 2, 3, 5])
 @pytest.mark.parametrize("name", BIG)
 def test_big_argmin_vs_oracle(engine, name, mode):
     doc, model, topo, groups, packed = _load(engine, name)

@@ -75,7 +75,7 @@ def _load(engine, name):
     return doc, packed
 
 
-@pytest.mark.parametrize("mode", [-1, 0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [-1, 0, 1, 2, 3, 5])
 @pytest.mark.parametrize("name", CASES_ALL)
 def test_every_candidate_full_space(engine, name, mode):
     doc, packed = _load(engine, name)
