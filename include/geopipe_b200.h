@@ -525,6 +525,10 @@ int gp_diag_timeline(void *out, uint32_t cap, uint32_t *n);
  * L1/L2; 1 one triangle in shared memory; 2 two triangles; 3 generic
  * status-tracking kernel).  Results are identical in every mode. */
 int gp_ctx_set_k3_mode(gp_ctx *ctx, int mode);
+/* Checked builds (make checked: -DGP_CHECKS, the device-side stand-in for
+ * compute-sanitizer): *line = first failing device check's source line since
+ * the last call (0 = none), then cleared; other builds set 0xFFFFFFFF. */
+int gp_diag_checks(gp_ctx *ctx, uint32_t *line);
 /* Parity tests (not a production path): until gp_diag_verify_end, every
  * exhaustive / snapshot launch (K3 sweep, sub-range and generic kernels, the
  * gp_replan graph, gp_replan_snapshots) uses its verify instantiation - the

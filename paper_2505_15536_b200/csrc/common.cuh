@@ -38,6 +38,20 @@ static int fail(int code, const char* fmt, ...) {
                         cudaGetErrorString(e_), __FILE__, __LINE__);          \
     } while (0)
 
+// ----------------------------------------------------------------------------
+// checked build (make checked -> libgeopipe_b200_chk.so, -DGP_CHECKS): device
+// index / invariant checks record the first failing source line in a device
+// word instead of trapping (a trap would leave the context unusable);
+// gp_diag_checks() reads and clears it.  The stand-in for compute-sanitizer,
+// which this GPU pool does not allow.  Production builds compile them out.
+// ----------------------------------------------------------------------------
+#if defined(GP_CHECKS)
+static __device__ unsigned int g_chk_line = 0u;
+#define GP_DCHECK(cond) do { if (!(cond)) atomicCAS(&g_chk_line, 0u, (unsigned)__LINE__); } while (0)
+#else
+#define GP_DCHECK(cond) do {} while (0)
+#endif
+
 // stage-table codes (per group, layer range)
 enum : uint8_t { SC_OK = 0, SC_INFEASIBLE = 1, SC_DEGENERATE = 4, SC_TOPOLOGY = 5 };
 // context flags that force the generic (status-tracking) range kernel

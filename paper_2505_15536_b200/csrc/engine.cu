@@ -2258,6 +2258,25 @@ int gp_diag_kernel_timing(gp_ctx* c, int enable, double* total_ms, uint64_t* lau
     return GP_OK;
 }
 
+// Checked builds (-DGP_CHECKS): first failing device check line of either
+// translation unit since the last call (0 = none), then cleared.  Other
+// builds report 0xFFFFFFFF (checks compiled out).
+int gp_diag_checks(gp_ctx* c, uint32_t* line) {
+    if (!c || !line) return fail(GP_ERR_INPUT, "null argument");
+#if defined(GP_CHECKS)
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    unsigned int v = 0, z = 0;
+    CUDA_TRY(cudaMemcpyFromSymbol(&v, g_chk_line, sizeof(v)));
+    CUDA_TRY(cudaMemcpyToSymbol(g_chk_line, &z, sizeof(z)));
+    const unsigned int w = verify_tu_checks();
+    *line = v ? v : w;
+#else
+    *line = 0xFFFFFFFFu;
+#endif
+    return GP_OK;
+}
+
 int gp_ctx_set_k3_mode(gp_ctx* c, int mode) {
     if (!c || mode < -1 || mode > 5) return fail(GP_ERR_INPUT, "bad mode");
     c->force_mode = mode;

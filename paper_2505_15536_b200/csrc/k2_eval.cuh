@@ -17,6 +17,8 @@ static __device__ EvalOut eval_tables(const DevInst& I, int k, const uint8_t* or
     size_t N2 = (size_t)(n + 1) * (n + 1);
     EvalOut out{0.0, GP_OK};
     bool feas = true;
+    GP_DCHECK(k >= 1 && k <= I.F && p[0] == 0 && mi >= 0 && mi < I.nm);
+    for (int s = 0; s < k; ++s) GP_DCHECK(order[s] < I.F && p[s] < p[s + 1] && p[s + 1] <= n);
     for (int s = 0; s < k; ++s)
         if (I.scode[(size_t)order[s] * N2 + tri_idx(n, p[s], p[s + 1])] == SC_INFEASIBLE)
             feas = false;

@@ -424,6 +424,9 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
                 for (int j = 1; j <= k - 3; ++j) p[j] = pr[j - 1];
             }
             p[k - 2] = a;
+            GP_DCHECK(gi < G.ng && a >= k - 2 && a <= n - 2 && len >= 1 && len <= K3_SEG &&
+                      q0 >= a + 1 && q0 + len - 1 <= n - 1);
+            for (int j = 1; j <= k - 2; ++j) GP_DCHECK(p[j - 1] < p[j]);
             // rank prefix: sum_j C(n - p[j-1] - 1, k - j) - C(n - p[j], k - j), j <= k-2
             for (int j = 1; j <= k - 2; ++j)
                 rpre += bn[(n - p[j - 1] - 1) * KB + (k - j)] - bn[(n - p[j]) * KB + (k - j)];
@@ -485,6 +488,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
         int run_i = -1, run_b = 0;
         // candidate q = q0 + i of the run: (cost min over the batch sizes, its batch)
         auto eval_q = [&](int i, double& cmin, int& bmin) {
+            GP_DCHECK(i >= 0 && i < len && rowoff(n, a) - a - 1 + q0 + i < ntri && q0 + i <= n);
             double2 e2, e3;
             double x2;
             if (MODE >= 1) { e2 = e2p[i]; e3 = e3p[i]; x2 = x2p[i]; }
@@ -537,6 +541,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     Key mine{INFINITY, ~0ull};
     if (best_t != ~0ull) {
         unsigned long long rr = best_t / NB, bi = best_t % NB;
+        GP_DCHECK(rr < G.NC);
         mine.cost = best_c;
         mine.tie = ((perm_rank * G.NC) + rr) * (unsigned long long)G.nbm +
                    (unsigned long long)((G.b0 + bi) * I.nm + mi);

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
             const double2* prow = P2 + (rowoff(n, a) - a - 1);
             K3RowRec* rr = rrec + (k3r_rowbase(n, A0, a) - a - 1);
             for (int q = a + 1 + lane; q <= n - 1; q += 32) {
+                GP_DCHECK(k3r_rowbase(n, A0, a) - a - 1 + q < nrec);
                 const double2 e2 = __ldg(&prow[q]);
                 const double x2 = __ldg(&X23[q - 1]);
                 K3RowRec r;
@@ -172,6 +173,8 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
                 for (int j = 1; j <= k - 3; ++j) p[j] = pr[j - 1];
             }
             p[k - 2] = a;
+            GP_DCHECK(gi < G.ng && a >= k - 2 && a <= n - 2 && len >= 1 && len <= K3_SEG &&
+                      q0 >= a + 1 && q0 + len - 1 <= n - 1);
 #pragma unroll
             for (int j = 1; j <= k - 2; ++j)
                 rpre += bn[(n - p[j - 1] - 1) * KB + (k - j)] - bn[(n - p[j]) * KB + (k - j)];
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
 #pragma unroll
         for (int bi = 0; bi < NB; ++bi) { run_c[bi] = INFINITY; run_q[bi] = 0; }
         auto eval_q = [&](int i) {
+            GP_DCHECK(i >= 0 && i < len && k3r_rowbase(n, A0, a) - a - 1 + q0 + i < nrec);
             const K3RowRec R = rp[i];
             const K3ColRec Cq = cp[i];
             const double res2 = res1 + R.D2;
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
     Key mine{INFINITY, ~0ull};
     if (best_t != ~0ull) {
         unsigned long long rr = best_t / NB, bi = best_t % NB;
+        GP_DCHECK(rr < G.NC);
         mine.cost = best_c;
         mine.tie = ((perm_rank * G.NC) + rr) * (unsigned long long)G.nbm +
                    (unsigned long long)((G.b0 + bi) * I.nm + mi);

@@ -42,6 +42,7 @@ __global__ void k6_minbw(DevInst I, SnapGeom Z) {
         while (x > 0 && x * (2 * nmem - x - 1) / 2 > t) --x;
         while ((x + 1) * (2 * nmem - x - 2) / 2 <= t) ++x;
         const int y = x + 1 + (t - x * (2 * nmem - x - 1) / 2);
+        GP_DCHECK(x >= 0 && x < y && y < nmem);
         const double v = bw[(size_t)I.fg_mem[m0 + x] * I.D + I.fg_mem[m0 + y]];
         mn = v < mn ? v : mn;
     }
@@ -86,6 +87,7 @@ __global__ void k6_patch(DevInst I, SnapGeom Z) {
         while (a > 0 && rowoff(n, a) > e) --a;
         while (a + 1 < n && rowoff(n, a + 1) <= e) ++a;
         const int b = a + 1 + (e - rowoff(n, a));
+        GP_DCHECK(a >= 0 && a < n && b > a && b <= n && rowoff(n, a) + (b - a - 1) == e);
         double2 v = I.tpk[t];
         const double V = I.vtab[t];
         const double mb = mbw[f];

@@ -36,3 +36,14 @@ SwFn pick_sweep_rec_verify(int nb, int k) {
         {k3_sweep_rec<4, 3, true>, k3_sweep_rec<4, 4, true>, k3_sweep_rec<4, 5, true>, k3_sweep_rec<4, 6, true>}};
     return table[nb - 1][k - 3];
 }
+
+unsigned int verify_tu_checks() {
+#if defined(GP_CHECKS)
+    unsigned int v = 0, z = 0;
+    if (cudaMemcpyFromSymbol(&v, g_chk_line, sizeof(v)) != cudaSuccess) return 0xFFFFFFFEu;
+    cudaMemcpyToSymbol(g_chk_line, &z, sizeof(z));
+    return v;
+#else
+    return 0;
+#endif
+}

@@ -10,3 +10,6 @@ typedef void (*K3Fn)(DevInst, RangeGeom, ArgminScratch, const unsigned long long
 SwFn pick_sweep_verify(int mode, int nb, int k);
 K3Fn pick_argmin_verify(int mode, int nb);
 SwFn pick_sweep_rec_verify(int nb, int k);
+// checked builds: first failing device check line of verify.cu's kernels
+// (0 = none), cleared on read
+unsigned int verify_tu_checks();

@@ -93,6 +93,7 @@ def lib():
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]
+        L.gp_diag_checks.argtypes = [vp, P(C.c_uint32)]
         L.gp_diag_kernel_timing.argtypes = [vp, C.c_int, P(C.c_double), P(C.c_uint64)]
         L.gp_diag_replan_timing.argtypes = [vp, C.c_int, P(C.c_double)]
         L.gp_diag_replan_host.argtypes = [vp, P(C.c_double)]
@@ -446,6 +447,13 @@ class Engine:
         the arg-min key (cost bits, tie) -> d_keys[2i:2i+2] (int64) and the
         table flags -> d_flags[i] (gp_replan_snapshots_async)."""
         _check(lib().gp_replan_snapshots_async(self._h, d_bandwidth, int(n_snap), d_keys, d_flags))
+
+    def device_checks(self) -> int:
+        """Checked builds: first failing device check line since the last
+        call (0 none); 0xFFFFFFFF when the checks are compiled out."""
+        v = C.c_uint32(0)
+        _check(lib().gp_diag_checks(self._h, C.byref(v)))
+        return v.value
 
     def kernel_timing(self, enable: bool):
         """Start (True) / end (False) a window of CUDA-event timing around

@@ -23,8 +23,17 @@ def oracle_lib():
 
 
 @pytest.fixture(scope="session")
-def engine():
+def _engine_session():
     from paper_2505_15536_b200.engine import Engine
     eng = Engine(0)
     yield eng
     eng.close()
+
+
+@pytest.fixture
+def engine(_engine_session):
+    """The session's engine context; on a checked build (GP_ENGINE_LIB =
+    libgeopipe_b200_chk.so) every test also fails on a device check."""
+    yield _engine_session
+    line = _engine_session.device_checks()
+    assert line in (0, 0xFFFFFFFF), f"device check failed at source line {line}"
