@@ -204,7 +204,17 @@ def exhaustive_plan(model, topology, groups, config, engine: Engine = None) -> D
 
 
 def search_plan(model, topology, groups, config, engine: Engine = None) -> D.SearchResult:
-    """GPU-batched replacement for ``search_plan`` (src/planner.py:330-371)."""
+    """GPU-batched replacement for ``search_plan`` (src/planner.py:330-371).
+
+    The (b, m) passes advance in lock-step (one K2 batch per beam iteration
+    over every active pass); what the caller observes is then replayed in the
+    reference's sequential pass order: the per-plan memory warnings
+    (src/planner.py:321) and per-pass "no feasible plan" warnings (:367) in
+    that order, and - if a candidate raises - the exception of the first
+    erroring candidate in sequential (pass, iteration, position) order.  A
+    pass that errors stops; passes after it in the sequential order are not
+    needed any more, passes before it run on until they finish or error.
+    """
     packed = packed_instance(model, topology, groups, config.bottleneck_factor)
     eng = _engine_for(packed, engine)
     fgs = sorted(groups.fgs.values(), key=lambda g: g.id)
@@ -214,18 +224,24 @@ def search_plan(model, topology, groups, config, engine: Engine = None) -> D.Sea
     for bm, (b, m) in enumerate(pairs):
         rng = random.Random(f"{config.seed}:{b}:{m}")
         beam = initial_candidates(model, fgs, config.beam_width, rng.randrange(2 ** 30))
-        passes.append({"bm": bm, "rng": rng, "beam": beam, "tops": []})
+        passes.append({"bm": bm, "rng": rng, "beam": beam, "tops": [], "iters": [],
+                       "err": None})
     cache: Dict[tuple, float] = {}
+    errors: Dict[tuple, int] = {}  # key -> status of candidates that raise
+    first_err = len(passes)        # smallest pass index that raised so far
     for _ in range(config.max_iter):
+        live = [ps for ps in passes[:first_err] if ps["err"] is None]
+        if not live:
+            break
         expanded = []
         todo_c, todo_bm, todo_keys = [], [], []
-        for ps in passes:
+        for ps in live:
             ex = expand_candidates(ps["beam"], ps["rng"])
             expanded.append(ex)
             b, m = pairs[ps["bm"]]
             for c in ex:
                 key = (c.order, c.counts, b, m)
-                if key not in cache:
+                if key not in cache and key not in errors:
                     cache[key] = None
                     todo_c.append(c)
                     todo_bm.append(ps["bm"])
@@ -233,22 +249,43 @@ def search_plan(model, topology, groups, config, engine: Engine = None) -> D.Sea
         if todo_c:
             o, cn, bmv = packed.encode(todo_c, todo_bm)
             cost, status = eng.eval_batch(o, cn, bmv)
-            bad = np.nonzero(status)[0]
-            if bad.size:
-                first = int(bad[0])
-                abi.raise_for(int(status[first]), f"candidate {todo_keys[first]} failed")
-            for key, c in zip(todo_keys, cost.tolist()):
-                cache[key] = c
-        for ps, ex in zip(passes, expanded):
+            for key, c, st in zip(todo_keys, cost.tolist(), status.tolist()):
+                if st:
+                    del cache[key]
+                    errors[key] = int(st)
+                else:
+                    cache[key] = c
+        for ps, ex in zip(live, expanded):
             b, m = pairs[ps["bm"]]
+            ps["iters"].append(ex)
+            bad = next((j for j, c in enumerate(ex) if (c.order, c.counts, b, m) in errors), None)
+            if bad is not None:
+                ps["err"] = (len(ps["iters"]) - 1, bad)
+                first_err = min(first_err, passes.index(ps))
+                continue
             scored = [(cache[(c.order, c.counts, b, m)], (c.order, c.counts), c) for c in ex]
             scored.sort(key=lambda x: (x[0], x[1]))
             ps["beam"] = [x[2] for x in scored[:config.beam_width]]
             ps["tops"].append((scored[0][0], scored[0][1]))
-    # replay best / trace in the reference's sequential pass order
+    # replay in the reference's sequential order: warnings, trace, best, errors
     best = None
     trace: List[float] = []
+    warn = log.isEnabledFor(logging.WARNING)
     for ps in passes:
+        b, m = pairs[ps["bm"]]
+        seen = set()
+        for it, ex in enumerate(ps["iters"]):
+            stop = ps["err"][1] if ps["err"] is not None and ps["err"][0] == it else len(ex)
+            for c in ex[:stop]:
+                key = (c.order, c.counts, b, m)
+                if key not in seen:
+                    seen.add(key)
+                    if warn and cache[key] == INFEASIBLE:
+                        log.warning("plan %s exceeds device memory; penalized", key)
+            if stop < len(ex):
+                c = ex[stop]
+                key = (c.order, c.counts, b, m)
+                abi.raise_for(errors[key], f"candidate {key} failed")
         incumbent = math.inf
         for top_cost, top_key in ps["tops"]:
             incumbent = min(incumbent, top_cost)
@@ -256,10 +293,7 @@ def search_plan(model, topology, groups, config, engine: Engine = None) -> D.Sea
                 best = (top_cost, top_key, ps["bm"])
             trace.append(min(incumbent, best[0]))
         if incumbent == math.inf:
-            log.warning("no feasible plan for batch=%d micro=%d", *pairs[ps["bm"]])
-    n_inf = sum(1 for v in cache.values() if v == math.inf)
-    if n_inf:
-        log.warning("%d evaluated plans exceed device memory; penalized", n_inf)
+            log.warning("no feasible plan for batch=%d micro=%d", b, m)
     if best is None or best[0] == INFEASIBLE:
         raise D.NoFeasiblePlanError("all (batch, micro-batch) pairs infeasible")
     order_ids, counts = best[1]

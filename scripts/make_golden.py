@@ -808,6 +808,43 @@ def dump_search_seeds():
     G.save("search_seeds.json", out)
 
 
+def dump_search_warnings():
+    """The warnings search_plan logs (src/planner.py:321, :367), in order,
+    and the exception it raises, for golden cases x seeds (logging enabled,
+    records captured from the `geopipe.planner` logger)."""
+    import logging as lg
+    gp = geopipe()
+    lg.disable(lg.NOTSET)
+    out = {}
+
+    class Cap(lg.Handler):
+        def __init__(self):
+            super().__init__()
+            self.msgs = []
+
+        def emit(self, rec):
+            self.msgs.append(rec.getMessage())
+    logger = lg.getLogger("geopipe.planner")
+    for name in ("c1", "c2j", "small", "rand10", "err_memory", "err_gateway", "err_intra_bw",
+                 "k5n9", "c4"):
+        doc = G.load(f"{name}.json")
+        model, topo, groups = G.instance_from_dict(doc["instance"])
+        out[name] = {}
+        for seed in ((0,) if name == "c4" else (0, 1, 2)):
+            h = Cap()
+            logger.addHandler(h)
+            logger.propagate = False
+            try:
+                gp.search_plan(model, topo, groups, gp.SearchConfig(seed=seed))
+                err = None
+            except Exception as e:
+                err = type(e).__name__
+            logger.removeHandler(h)
+            out[name][str(seed)] = {"warnings": h.msgs, "error": err}
+    lg.disable(lg.CRITICAL)
+    G.save("search_warnings.json", out)
+
+
 def dump_region_sweep():
     """C2 region-grouping sweep with the reference: groups built
     as group_first_level would for each set partition of the regions, then

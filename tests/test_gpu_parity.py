@@ -384,3 +384,37 @@ def test_reset_bandwidth_restores_groupindex_min_bw(engine):
     assert not same_bits(derived, before).all()  # the stored value really differs
     engine.reset_bandwidth()
     assert same_bits(costs(), before).all()
+
+
+WARN = G.load("search_warnings.json")
+
+
+@pytest.mark.parametrize("name", sorted(WARN))
+def test_search_plan_warnings_and_errors_in_reference_order(engine, name):
+    """search_plan logs one warning per memory-infeasible plan when it is first
+    evaluated (src/planner.py:321) and one per infeasible (b, m) pass (:367),
+    in the reference's sequential pass order, and raises the first error in
+    that order - although the passes run in lock-step on the GPU."""
+    import logging
+    doc, model, topo, groups = load_case(name)
+    logger = logging.getLogger("paper_2505_15536_b200.planner")
+    for seed, exp in WARN[name].items():
+        msgs = []
+
+        class Cap(logging.Handler):
+            def emit(self, rec):
+                msgs.append(rec.getMessage())
+        h = Cap()
+        logger.addHandler(h)
+        old = logger.propagate
+        logger.propagate = False
+        try:
+            P.search_plan(model, topo, groups, P.SearchConfig(seed=int(seed)), engine=engine)
+            err = None
+        except P.GeopipeError as e:
+            err = type(e).__name__
+        finally:
+            logger.removeHandler(h)
+            logger.propagate = old
+        assert err == exp["error"], (name, seed)
+        assert msgs == exp["warnings"], (name, seed)
