@@ -661,6 +661,24 @@ int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_ord
         // k = 4 (and < 2^32 candidates): the warp-compacted variant
         bool q4 = k == 4 && n < (1ull << 32);
         if (const char* e = getenv("GP_K2_Q4")) q4 = q4 && atoi(e) != 0;
+        // k = 4 with 16-byte aligned arrays: the TMA-fed chunk kernel
+        // (GP_K2_TMA=0 disables)
+        bool t4 = q4 && ((((uintptr_t)d_order | (uintptr_t)d_counts | (uintptr_t)d_bm) & 15u) == 0) &&
+                  k2t_smem(sc_bytes) <= (size_t)c->smem_max;
+        if (const char* e = getenv("GP_K2_TMA")) t4 = t4 && atoi(e) != 0;
+        if (t4) {
+            const size_t smem_t = k2t_smem(sc_bytes);
+            int per_sm = 0;
+            { int st_ = kernel_slots(c, (const void*)k2_eval_batch_t4, K2T_THREADS, smem_t, &per_sm);
+              if (st_ != GP_OK) return st_; }
+            unsigned long long grid = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
+            const unsigned long long chunks = (n + K2T_CHUNK - 1) / K2T_CHUNK;
+            if (grid > chunks) grid = chunks;
+            k2_eval_batch_t4<<<(unsigned)grid, K2T_THREADS, smem_t, c->stream>>>(
+                I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status, (unsigned)sc_bytes);
+            CUDA_TRY(cudaGetLastError());
+            return GP_OK;
+        }
         const K2Fn kern = q4 ? k2_eval_batch_q4 : tab[k - 2];
         const size_t smem_k2 = sc_bytes + (q4 ? (K2Q_THREADS / 32) * 64 * sizeof(uint4) : 0);
         int per_sm = 0;

@@ -339,3 +339,192 @@ static __global__ void __launch_bounds__(K2Q_THREADS, K2Q_MINB) k2_eval_batch_q4
     __syncwarp();
     if (lane < q) eval_entry(wq[lane]);
 }
+
+// ---- K2, k = 4, large batches: TMA-fed chunks --------------------------------
+// Persistent CTAs own chunks of K2T_CHUNK candidates (chunk = blockIdx + j *
+// gridDim).  One elected thread streams each chunk's order / counts / bm
+// arrays into a K2T_STAGES-deep shared-memory ring with bulk async copies
+// (cp.async.bulk + mbarrier complete_tx), so the input loads leave the
+// warps' critical path.  A warp classifies 32 candidates at a time from
+// shared memory with SIMD byte arithmetic on the packed words (range,
+// distinctness and zero checks on all four bytes at once, the cut positions
+// as the byte-wise prefix sums of counts * 0x01010101) and the stage codes
+// (also in shared memory): errors and memory-infeasible candidates (+inf)
+// are written at once, the feasible ones queued per warp and evaluated 32 at
+// a time (eval_fast: k stage entries + k-1 boundary values from L2), as in
+// k2_eval_batch_q4.  One CTA barrier per chunk releases its ring slot.
+#ifndef K2T_CHUNK
+#define K2T_CHUNK 2048
+#endif
+#ifndef K2T_STAGES
+#define K2T_STAGES 3
+#endif
+#define K2T_THREADS 256
+#define K2T_SLOT (K2T_CHUNK * 9)  // order u32 + counts u32 + bm u8 per candidate
+
+__host__ __device__ inline size_t k2t_smem(size_t sc_bytes) {
+    return 64 + sc_bytes + (size_t)K2T_STAGES * K2T_SLOT + (K2T_THREADS / 32) * 64 * 16;
+}
+
+static __global__ void __launch_bounds__(K2T_THREADS, 2) k2_eval_batch_t4(DevInst I, long long ncand,
+                                                              const uint8_t* __restrict__ order,
+                                                              const uint8_t* __restrict__ counts,
+                                                              const uint8_t* __restrict__ bm,
+                                                              double* __restrict__ cost,
+                                                              uint8_t* __restrict__ status,
+                                                              unsigned sc_bytes) {
+    extern __shared__ __align__(16) uint8_t t4_s[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(t4_s);                // [K2T_STAGES]
+    uint8_t* sc_s = t4_s + 64;
+    uint8_t* ring = sc_s + sc_bytes;                                  // [K2T_STAGES][K2T_SLOT]
+    uint4* wq = reinterpret_cast<uint4*>(ring + (size_t)K2T_STAGES * K2T_SLOT) + (threadIdx.x >> 5) * 64;
+    const int n = I.n;
+    const int N2 = (n + 1) * (n + 1);
+    const long long nchunks = (ncand + K2T_CHUNK - 1) / K2T_CHUNK;
+    auto issue = [&](long long c, int slot) {
+        const long long left = ncand - c * K2T_CHUNK;
+        const int cnt = (left < K2T_CHUNK ? (int)left : K2T_CHUNK) & ~15;  // ragged tail: direct loads
+        uint8_t* dst = ring + (size_t)slot * K2T_SLOT;
+        mbar_expect_tx(&bar[slot], (uint32_t)cnt * 9u);
+        if (cnt) {
+            tma_bulk_g2s(dst, order + c * K2T_CHUNK * 4, (uint32_t)cnt * 4, &bar[slot]);
+            tma_bulk_g2s(dst + K2T_CHUNK * 4, counts + c * K2T_CHUNK * 4, (uint32_t)cnt * 4, &bar[slot]);
+            tma_bulk_g2s(dst + K2T_CHUNK * 8, bm + c * K2T_CHUNK, (uint32_t)cnt, &bar[slot]);
+        }
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < K2T_STAGES; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < K2T_STAGES; ++s) {
+            const long long c = blockIdx.x + (long long)s * gridDim.x;
+            if (c < nchunks) issue(c, s);
+        }
+    }
+    {
+        const unsigned nbytes = (unsigned)(I.F * N2);
+        const uint4* src = reinterpret_cast<const uint4*>(I.scode);
+        uint4* dst = reinterpret_cast<uint4*>(sc_s);
+        for (unsigned i = threadIdx.x; i < nbytes / 16; i += blockDim.x) dst[i] = __ldg(&src[i]);
+        for (unsigned i = (nbytes & ~15u) + threadIdx.x; i < nbytes; i += blockDim.x)
+            sc_s[i] = __ldg(&I.scode[i]);
+    }
+    __syncthreads();
+    const bool fast_tables = *I.flags == 0u;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int nbm = I.nb * I.nm;
+    auto eval_entry = [&](const uint4 e) {
+        uint8_t o[4];
+        int p[5];
+        const unsigned pw = e.z * 0x01010101u;  // byte-wise prefix sums of the counts
+        p[0] = 0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            o[s] = (uint8_t)(e.y >> (8 * s));
+            p[s + 1] = (int)((pw >> (8 * s)) & 0xffu);
+        }
+        const int b = (int)e.w;
+        cost[e.x] = eval_fast<4>(I, o, p, b % I.nm, __ldg(&I.mtab[b]));
+    };
+    int q = 0;  // warp-uniform queue length
+    int j = 0;
+    for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, ++j) {
+        const int slot = j % K2T_STAGES;
+        mbar_wait(&bar[slot], (uint32_t)((j / K2T_STAGES) & 1));
+        const uint32_t* so = reinterpret_cast<const uint32_t*>(ring + (size_t)slot * K2T_SLOT);
+        const uint32_t* scn = so + K2T_CHUNK;
+        const uint8_t* sb = reinterpret_cast<const uint8_t*>(so + 2 * K2T_CHUNK);
+        const long long c0 = c * K2T_CHUNK;
+        const long long left = ncand - c0;
+        const int cnt = left < K2T_CHUNK ? (int)left : K2T_CHUNK;
+        const int cnt16 = cnt & ~15;
+        double* cc = cost + c0;
+        uint8_t* sc = status + c0;
+        // one candidate: write its result or queue it for the warp's batch
+        auto classify = [&](int r, uint32_t ow, uint32_t cw, int b) -> bool {
+            // input checks on the packed words: groups < F and distinct (a
+            // 4-bit set of 4 members), counts > 0 (no zero byte), sum of
+            // counts <= n, (b, m) index in range
+            const unsigned o0 = ow & 0xffu, o1 = (ow >> 8) & 0xffu, o2 = (ow >> 16) & 0xffu,
+                           o3 = ow >> 24;
+            const unsigned msk = (1u << (o0 & 31u)) | (1u << (o1 & 31u)) | (1u << (o2 & 31u)) |
+                                 (1u << (o3 & 31u));
+            const bool ok = ((ow & 0xE0E0E0E0u) == 0u) && (__popc(msk) == 4) &&
+                            ((msk >> I.F) == 0u) &&
+                            (((cw - 0x01010101u) & ~cw & 0x80808080u) == 0u);
+            const int total = (int)__vsadu4(cw, 0u);
+            if (!ok || b >= nbm || total > n) {
+                cc[r] = NAN;
+                sc[r] = (uint8_t)GP_ERR_INPUT;
+                return false;
+            }
+            if (fast_tables && total == n) {
+                const unsigned pw = cw * 0x01010101u;  // p1..p4 (exact: sums <= n <= 255)
+                const int p1 = (int)(pw & 0xffu), p2 = (int)((pw >> 8) & 0xffu),
+                          p3 = (int)((pw >> 16) & 0xffu);
+                const bool inf = (sc_s[(int)o0 * N2 + p1] == SC_INFEASIBLE) |
+                                 (sc_s[(int)o1 * N2 + tri_idx(n, p1, p2)] == SC_INFEASIBLE) |
+                                 (sc_s[(int)o2 * N2 + tri_idx(n, p2, p3)] == SC_INFEASIBLE) |
+                                 (sc_s[(int)o3 * N2 + tri_idx(n, p3, n)] == SC_INFEASIBLE);
+                sc[r] = GP_OK;
+                if (inf) cc[r] = INFINITY;
+                return !inf;
+            }
+            uint8_t o[4];
+            int p[5];
+            p[0] = 0;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                o[s] = (uint8_t)(ow >> (8 * s));
+                p[s + 1] = p[s] + (int)((cw >> (8 * s)) & 0xffu);
+            }
+            const int mi = b % I.nm;
+            EvalOut e = eval_tables(I, 4, o, p, mi, I.batch[b / I.nm] / I.micro[mi]);
+            cc[r] = e.status == GP_OK ? e.cost : NAN;
+            sc[r] = (uint8_t)e.status;
+            return false;
+        };
+        auto enqueue = [&](bool need, int r, uint32_t ow, uint32_t cw, int b) {
+            const unsigned m = __ballot_sync(0xffffffffu, need);
+            if (need) wq[q + __popc(m & lt)] = make_uint4((unsigned)(c0 + r), ow, cw, (unsigned)b);
+            q += __popc(m);
+            __syncwarp();
+            if (q >= 32) {
+                const uint4 e = wq[q - 32 + lane];
+                __syncwarp();
+                q -= 32;
+                eval_entry(e);
+            }
+        };
+        if (cnt == K2T_CHUNK) {  // full chunk: every input word in shared memory
+#pragma unroll 2
+            for (int r = threadIdx.x; r < K2T_CHUNK; r += K2T_THREADS) {
+                const uint32_t ow = so[r], cw = scn[r];
+                const int b = sb[r];
+                enqueue(classify(r, ow, cw, b), r, ow, cw, b);
+            }
+        } else {
+            for (int r = threadIdx.x; r < ((cnt + 31) & ~31); r += blockDim.x) {
+                bool need = false;
+                uint32_t ow = 0, cw = 0;
+                int b = 0;
+                if (r < cnt) {
+                    if (r < cnt16) { ow = so[r]; cw = scn[r]; b = sb[r]; }
+                    else {
+                        ow = __ldg(reinterpret_cast<const uint32_t*>(order) + c0 + r);
+                        cw = __ldg(reinterpret_cast<const uint32_t*>(counts) + c0 + r);
+                        b = __ldg(&bm[c0 + r]);
+                    }
+                    need = classify(r, ow, cw, b);
+                }
+                enqueue(need, r, ow, cw, b);
+            }
+        }
+        __syncthreads();  // every warp is done with the slot
+        if (threadIdx.x == 0) {
+            const long long cn = c + (long long)K2T_STAGES * gridDim.x;
+            if (cn < nchunks) issue(cn, slot);
+        }
+    }
+    __syncwarp();
+    if (lane < q) eval_entry(wq[lane]);
+}
