@@ -672,7 +672,8 @@ int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_ord
             { int st_ = kernel_slots(c, (const void*)k2_eval_batch_t4, K2T_THREADS, smem_t, &per_sm);
               if (st_ != GP_OK) return st_; }
             unsigned long long grid = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
-            const unsigned long long chunks = (n + K2T_CHUNK - 1) / K2T_CHUNK;
+            const unsigned long long chunks = (n + (unsigned long long)K2T_WCHUNK * K2T_WARPS - 1) /
+                                              ((unsigned long long)K2T_WCHUNK * K2T_WARPS);
             if (grid > chunks) grid = chunks;
             k2_eval_batch_t4<<<(unsigned)grid, K2T_THREADS, smem_t, c->stream>>>(
                 I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status, (unsigned)sc_bytes);

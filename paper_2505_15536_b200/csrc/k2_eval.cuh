@@ -341,32 +341,40 @@ static __global__ void __launch_bounds__(K2Q_THREADS, K2Q_MINB) k2_eval_batch_q4
 }
 
 // ---- K2, k = 4, large batches: TMA-fed chunks --------------------------------
-// Persistent CTAs own chunks of K2T_CHUNK candidates (chunk = blockIdx + j *
-// gridDim).  One elected thread streams each chunk's order / counts / bm
-// arrays into a K2T_STAGES-deep shared-memory ring with bulk async copies
-// (cp.async.bulk + mbarrier complete_tx), so the input loads leave the
-// warps' critical path.  A warp classifies 32 candidates at a time from
-// shared memory with SIMD byte arithmetic on the packed words (range,
-// distinctness and zero checks on all four bytes at once, the cut positions
-// as the byte-wise prefix sums of counts * 0x01010101) and the stage codes
-// (also in shared memory): errors and memory-infeasible candidates (+inf)
-// are written at once, the feasible ones queued per warp and evaluated 32 at
-// a time (eval_fast: k stage entries + k-1 boundary values from L2), as in
-// k2_eval_batch_q4.  One CTA barrier per chunk releases its ring slot.
-#ifndef K2T_CHUNK
-#define K2T_CHUNK 2048
+// Every warp owns a private pipeline: chunks of K2T_WCHUNK candidates (warp
+// chunk = global warp id + j * total warps), streamed by the warp's lane 0
+// into the warp's own K2T_STAGES-deep shared-memory ring with bulk async
+// copies (cp.async.bulk + mbarrier complete_tx), so input loads leave the
+// warps' critical path and no CTA-wide barrier paces the warps.  A warp
+// classifies 32 candidates at a time from shared memory with SIMD byte
+// arithmetic on the packed words (range, distinctness and zero checks on all
+// four bytes at once, the cut positions as the byte-wise prefix sums of
+// counts * 0x01010101) and the stage codes (shared by the CTA, in shared
+// memory): errors and memory-infeasible candidates (+inf) are written at
+// once, the feasible ones queued and evaluated 32 at a time (eval_fast: k
+// stage entries + k-1 boundary values from L2), as in k2_eval_batch_q4.
+#ifndef K2T_WCHUNK
+#define K2T_WCHUNK 256
 #endif
 #ifndef K2T_STAGES
 #define K2T_STAGES 3
 #endif
 #define K2T_THREADS 256
-#define K2T_SLOT (K2T_CHUNK * 9)  // order u32 + counts u32 + bm u8 per candidate
+#ifndef K2T_MINB
+#define K2T_MINB 2
+#endif
+#ifndef K2T_ILP
+#define K2T_ILP 4
+#endif
+#define K2T_WARPS (K2T_THREADS / 32)
+#define K2T_SLOT (K2T_WCHUNK * 9)  // order u32 + counts u32 + bm u8 per candidate
 
 __host__ __device__ inline size_t k2t_smem(size_t sc_bytes) {
-    return 64 + sc_bytes + (size_t)K2T_STAGES * K2T_SLOT + (K2T_THREADS / 32) * 64 * 16;
+    return 16 * K2T_WARPS * K2T_STAGES / 2 + 64 + sc_bytes +
+           (size_t)K2T_WARPS * K2T_STAGES * K2T_SLOT + (size_t)K2T_WARPS * 64 * 16;
 }
 
-static __global__ void __launch_bounds__(K2T_THREADS, 2) k2_eval_batch_t4(DevInst I, long long ncand,
+static __global__ void __launch_bounds__(K2T_THREADS, K2T_MINB) k2_eval_batch_t4(DevInst I, long long ncand,
                                                               const uint8_t* __restrict__ order,
                                                               const uint8_t* __restrict__ counts,
                                                               const uint8_t* __restrict__ bm,
@@ -374,28 +382,33 @@ static __global__ void __launch_bounds__(K2T_THREADS, 2) k2_eval_batch_t4(DevIns
                                                               uint8_t* __restrict__ status,
                                                               unsigned sc_bytes) {
     extern __shared__ __align__(16) uint8_t t4_s[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(t4_s);                // [K2T_STAGES]
-    uint8_t* sc_s = t4_s + 64;
-    uint8_t* ring = sc_s + sc_bytes;                                  // [K2T_STAGES][K2T_SLOT]
-    uint4* wq = reinterpret_cast<uint4*>(ring + (size_t)K2T_STAGES * K2T_SLOT) + (threadIdx.x >> 5) * 64;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t bar_bytes = ((size_t)K2T_WARPS * K2T_STAGES * 8 + 63) & ~(size_t)63;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(t4_s) + warp * K2T_STAGES;  // this warp's
+    uint8_t* sc_s = t4_s + bar_bytes;
+    uint8_t* ring = sc_s + sc_bytes + (size_t)warp * K2T_STAGES * K2T_SLOT;
+    uint4* wq = reinterpret_cast<uint4*>(sc_s + sc_bytes + (size_t)K2T_WARPS * K2T_STAGES * K2T_SLOT) +
+                warp * 64;
     const int n = I.n;
     const int N2 = (n + 1) * (n + 1);
-    const long long nchunks = (ncand + K2T_CHUNK - 1) / K2T_CHUNK;
-    auto issue = [&](long long c, int slot) {
-        const long long left = ncand - c * K2T_CHUNK;
-        const int cnt = (left < K2T_CHUNK ? (int)left : K2T_CHUNK) & ~15;  // ragged tail: direct loads
+    const long long nchunks = (ncand + K2T_WCHUNK - 1) / K2T_WCHUNK;
+    const long long wstride = (long long)gridDim.x * K2T_WARPS;
+    const long long wfirst = (long long)blockIdx.x * K2T_WARPS + warp;
+    auto issue = [&](long long c, int slot) {  // lane 0
+        const long long left = ncand - c * K2T_WCHUNK;
+        const int cnt = (left < K2T_WCHUNK ? (int)left : K2T_WCHUNK) & ~15;  // ragged tail: direct loads
         uint8_t* dst = ring + (size_t)slot * K2T_SLOT;
         mbar_expect_tx(&bar[slot], (uint32_t)cnt * 9u);
         if (cnt) {
-            tma_bulk_g2s(dst, order + c * K2T_CHUNK * 4, (uint32_t)cnt * 4, &bar[slot]);
-            tma_bulk_g2s(dst + K2T_CHUNK * 4, counts + c * K2T_CHUNK * 4, (uint32_t)cnt * 4, &bar[slot]);
-            tma_bulk_g2s(dst + K2T_CHUNK * 8, bm + c * K2T_CHUNK, (uint32_t)cnt, &bar[slot]);
+            tma_bulk_g2s(dst, order + c * K2T_WCHUNK * 4, (uint32_t)cnt * 4, &bar[slot]);
+            tma_bulk_g2s(dst + K2T_WCHUNK * 4, counts + c * K2T_WCHUNK * 4, (uint32_t)cnt * 4, &bar[slot]);
+            tma_bulk_g2s(dst + K2T_WCHUNK * 8, bm + c * K2T_WCHUNK, (uint32_t)cnt, &bar[slot]);
         }
     };
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
         for (int s = 0; s < K2T_STAGES; ++s) mbar_init(&bar[s], 1);
         for (int s = 0; s < K2T_STAGES; ++s) {
-            const long long c = blockIdx.x + (long long)s * gridDim.x;
+            const long long c = wfirst + (long long)s * wstride;
             if (c < nchunks) issue(c, s);
         }
     }
@@ -409,7 +422,6 @@ static __global__ void __launch_bounds__(K2T_THREADS, 2) k2_eval_batch_t4(DevIns
     }
     __syncthreads();
     const bool fast_tables = *I.flags == 0u;
-    const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const int nbm = I.nb * I.nm;
     auto eval_entry = [&](const uint4 e) {
@@ -427,19 +439,19 @@ static __global__ void __launch_bounds__(K2T_THREADS, 2) k2_eval_batch_t4(DevIns
     };
     int q = 0;  // warp-uniform queue length
     int j = 0;
-    for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, ++j) {
+    for (long long c = wfirst; c < nchunks; c += wstride, ++j) {
         const int slot = j % K2T_STAGES;
         mbar_wait(&bar[slot], (uint32_t)((j / K2T_STAGES) & 1));
         const uint32_t* so = reinterpret_cast<const uint32_t*>(ring + (size_t)slot * K2T_SLOT);
-        const uint32_t* scn = so + K2T_CHUNK;
-        const uint8_t* sb = reinterpret_cast<const uint8_t*>(so + 2 * K2T_CHUNK);
-        const long long c0 = c * K2T_CHUNK;
+        const uint32_t* scn = so + K2T_WCHUNK;
+        const uint8_t* sb = reinterpret_cast<const uint8_t*>(so + 2 * K2T_WCHUNK);
+        const long long c0 = c * K2T_WCHUNK;
         const long long left = ncand - c0;
-        const int cnt = left < K2T_CHUNK ? (int)left : K2T_CHUNK;
+        const int cnt = left < K2T_WCHUNK ? (int)left : K2T_WCHUNK;
         const int cnt16 = cnt & ~15;
         double* cc = cost + c0;
         uint8_t* sc = status + c0;
-        // one candidate: write its result or queue it for the warp's batch
+        // one candidate: write its result or report it for the warp's batch
         auto classify = [&](int r, uint32_t ow, uint32_t cw, int b) -> bool {
             // input checks on the packed words: groups < F and distinct (a
             // 4-bit set of 4 members), counts > 0 (no zero byte), sum of
@@ -495,15 +507,26 @@ static __global__ void __launch_bounds__(K2T_THREADS, 2) k2_eval_batch_t4(DevIns
                 eval_entry(e);
             }
         };
-        if (cnt == K2T_CHUNK) {  // full chunk: every input word in shared memory
-#pragma unroll 2
-            for (int r = threadIdx.x; r < K2T_CHUNK; r += K2T_THREADS) {
-                const uint32_t ow = so[r], cw = scn[r];
-                const int b = sb[r];
-                enqueue(classify(r, ow, cw, b), r, ow, cw, b);
+        if (cnt == K2T_WCHUNK) {  // full chunk: every input word in shared memory
+            // K2T_ILP candidates per lane classified together (independent
+            // chains: shared-memory round trips overlap), then queued in order
+            for (int r0 = lane; r0 < K2T_WCHUNK; r0 += 32 * K2T_ILP) {
+                uint32_t ow[K2T_ILP], cw[K2T_ILP];
+                int b[K2T_ILP];
+                bool need[K2T_ILP];
+#pragma unroll
+                for (int u = 0; u < K2T_ILP; ++u) {
+                    ow[u] = so[r0 + 32 * u];
+                    cw[u] = scn[r0 + 32 * u];
+                    b[u] = sb[r0 + 32 * u];
+                }
+#pragma unroll
+                for (int u = 0; u < K2T_ILP; ++u) need[u] = classify(r0 + 32 * u, ow[u], cw[u], b[u]);
+#pragma unroll
+                for (int u = 0; u < K2T_ILP; ++u) enqueue(need[u], r0 + 32 * u, ow[u], cw[u], b[u]);
             }
         } else {
-            for (int r = threadIdx.x; r < ((cnt + 31) & ~31); r += blockDim.x) {
+            for (int r = lane; r < ((cnt + 31) & ~31); r += 32) {
                 bool need = false;
                 uint32_t ow = 0, cw = 0;
                 int b = 0;
@@ -519,9 +542,9 @@ static __global__ void __launch_bounds__(K2T_THREADS, 2) k2_eval_batch_t4(DevIns
                 enqueue(need, r, ow, cw, b);
             }
         }
-        __syncthreads();  // every warp is done with the slot
-        if (threadIdx.x == 0) {
-            const long long cn = c + (long long)K2T_STAGES * gridDim.x;
+        __syncwarp();  // the warp is done with the slot
+        if (lane == 0) {
+            const long long cn = c + (long long)K2T_STAGES * wstride;
             if (cn < nchunks) issue(cn, slot);
         }
     }
