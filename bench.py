@@ -72,6 +72,16 @@ def sweep_ops_per_candidate(nb):
     return (3 + 11 * nb) / nb
 
 
+# Measured by ncu on the sweep kernel of this workload (not in-run):
+# profiles/r2_k6_sweep_ncu_summary.json (issued FP64 per candidate from the
+# FP64 pipe activity, and dram__bytes_read.sum + dram__bytes_write.sum of one
+# launch; raw metrics in the .csv of the same name).
+NCU_SOURCE = "profiles/r2_k6_sweep_ncu_summary.json"
+SWEEP_ISSUED_FP64_PER_CAND = None
+SWEEP_DRAM_BYTES = None
+S_TOTAL = 128
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)

@@ -240,6 +240,166 @@ __device__ int sim_dev(const gp_timing& T, int policy, int iterations, const gp_
     return GP_OK;
 }
 
+// ----------------------------------------------------------------------------
+// Register-resident specialisation of sim_dev for S <= SMAX stages, one
+// iteration and a constant trace (the common case: ranking candidate plans
+// by their simulated 1F1B makespan).  The event list becomes fixed slots -
+// one pending op per stage, one pending transfer per link direction - so the
+// (time, seq) pop is an unrolled comparison over 3*SMAX-2 slots, every loop
+// over stages is unrolled with compile-time indices, and the state (counters
+// as 32-bit ints, event times) lives in registers instead of a 5 KB local
+// frame.  Event order, dispatch order and every floating-point operation are
+// sim_dev's (src/engine.py:230-406), so makespans are bit-identical.
+// ----------------------------------------------------------------------------
+template <int SMAX>
+__device__ int sim_regs(const gp_timing& T, int policy, double* makespan) {
+    const int S = (int)T.n_stages;
+    const long long B = T.batch, m = T.microbatch;
+    const long long nchunk = (B + m - 1) / m;
+    constexpr int L = 2 * (SMAX - 1) > 0 ? 2 * (SMAX - 1) : 1;
+    long long fa[SMAX], ft[SMAX], fd[SMAX], ba[SMAX], bt[SMAX], bd[SMAX], wd[SMAX];
+    int wh[SMAX], wtl[SMAX];
+    bool syncd[SMAX], optd[SMAX], busy[SMAX];
+    double ot[SMAX];
+    unsigned oseq[SMAX];
+    int ok[SMAX];
+    long long osz[SMAX];
+    long long lenq[L], lst[L], xsz[L];
+    bool lbusy[L];
+    double xt[L];
+    unsigned xseq[L];
+    double fwd[SMAX], bwd[SMAX], wgt[SMAX], syn[SMAX], opt[SMAX];
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) {
+        fa[s] = ft[s] = fd[s] = ba[s] = bt[s] = bd[s] = wd[s] = 0;
+        wh[s] = wtl[s] = 0;
+        syncd[s] = optd[s] = false;
+        busy[s] = s >= S;  // absent stages never dispatch
+        ot[s] = INFINITY;
+        oseq[s] = 0u;
+        ok[s] = 0;
+        osz[s] = 0;
+        fwd[s] = T.fwd[s]; bwd[s] = T.bwd[s]; wgt[s] = T.wgt[s]; syn[s] = T.sync[s]; opt[s] = T.opt[s];
+    }
+    fa[0] = B;
+#pragma unroll
+    for (int l = 0; l < L; ++l) { lenq[l] = lst[l] = xsz[l] = 0; lbusy[l] = false; xt[l] = INFINITY; xseq[l] = 0u; }
+    unsigned seq = 0u;
+    auto chunk_size = [&](long long j) -> long long {
+        long long r = B - (j % nchunk) * m;
+        return r < m ? r : m;
+    };
+    // try_start_link (src/engine.py:271-289), boundary bnd and direction dir
+    // compile-time after unrolling
+    auto try_start = [&](double tnow, int bnd, int dir) {
+        const int l = 2 * bnd + dir;
+        if (lbusy[l] || lst[l] >= lenq[l]) return;
+        const long long j = lst[l]++;
+        lbusy[l] = true;
+        const long long sz = chunk_size(j);
+        const double per = dir == 0 ? T.act[bnd] : T.grad[bnd];
+        const double bytes = per * (double)sz;
+        const double bw = T.bw[bnd] * 1.0;
+        xt[l] = (tnow + bytes / bw) + T.lat[bnd];
+        xseq[l] = seq++;
+        xsz[l] = sz;
+    };
+    double now = 0.0;
+    for (;;) {
+        bool progress = true;
+        while (progress) {
+            progress = false;
+#pragma unroll
+            for (int s = 0; s < SMAX; ++s) {
+                if (busy[s] || optd[s]) continue;
+                const bool wq_any = wh[s] < wtl[s];
+                long long best_sz;
+                const int best_k = ready_op(policy, S, s, B, m, m, fa[s], ft[s], fd[s], ba[s], bt[s],
+                                            bd[s], wd[s], wq_any, wq_any ? chunk_size(wh[s]) : 0,
+                                            syncd[s], optd[s], &best_sz);
+                if (best_k < 0) continue;
+                double dur;
+                switch (best_k) {
+                    case 0: dur = fwd[s] * (double)best_sz; ft[s] += best_sz; break;
+                    case 1: dur = bwd[s] * (double)best_sz; bt[s] += best_sz; break;
+                    case 2: dur = wgt[s] * (double)best_sz; wh[s]++; break;
+                    case 3: dur = syn[s]; break;
+                    default: dur = opt[s]; break;
+                }
+                busy[s] = true;
+                ot[s] = now + dur;
+                oseq[s] = seq++;
+                ok[s] = best_k;
+                osz[s] = best_sz;
+                progress = true;
+            }
+        }
+        // pop the (time, seq) minimum over the pending slots
+        double bt_ = INFINITY;
+        unsigned bs_ = ~0u;
+        int slot = -1;
+#pragma unroll
+        for (int s = 0; s < SMAX; ++s)
+            if (s < S && busy[s] && !optd[s] && (ot[s] < bt_ || (ot[s] == bt_ && oseq[s] < bs_))) {
+                bt_ = ot[s]; bs_ = oseq[s]; slot = s;
+            }
+#pragma unroll
+        for (int l = 0; l < L; ++l)
+            if (lbusy[l] && (xt[l] < bt_ || (xt[l] == bt_ && xseq[l] < bs_))) {
+                bt_ = xt[l]; bs_ = xseq[l]; slot = SMAX + l;
+            }
+        if (slot < 0) break;
+        now = bt_;
+#pragma unroll
+        for (int s = 0; s < SMAX; ++s) {
+            if (slot != s) continue;
+            // finish_op (src/engine.py:343-378)
+            busy[s] = false;
+            const long long sz = osz[s];
+            switch (ok[s]) {
+                case 0:
+                    fd[s] += sz;
+                    if (s < SMAX - 1 && s < S - 1) { lenq[2 * s]++; try_start(now, s, 0); }
+                    break;
+                case 1:
+                    bd[s] += sz;
+                    wtl[s]++;
+                    if (s > 0) { lenq[2 * (s - 1) + 1]++; try_start(now, s - 1, 1); }
+                    break;
+                case 2: wd[s] += sz; break;
+                case 3: syncd[s] = true; break;
+                default: optd[s] = true; busy[s] = true; break;  // iteration done: never dispatch
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            if (slot != SMAX + l) continue;
+            // finish_transfer (src/engine.py:380-396)
+            lbusy[l] = false;
+            const int bnd = l / 2, dir = l % 2;
+            if (dir == 0) fa[bnd + 1] += xsz[l];
+            else ba[bnd] += xsz[l];
+            try_start(now, bnd, dir);
+        }
+    }
+    *makespan = now;
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s)
+        if (s < S && !optd[s]) return GP_ERR_SCHEDULING;
+    return GP_OK;
+}
+
+// sim_dev or, when it applies, its register-resident specialisation
+__device__ __forceinline__ int sim_any(const gp_timing& T, int policy, int iterations,
+                                       const gp_trace* trace, double* makespan) {
+    const int S = (int)T.n_stages;
+#if !defined(K5_NO_REGS)
+    if (iterations == 1 && !trace && S >= 1 && S <= 4 && T.microbatch > 0 && T.batch > 0)
+        return sim_regs<4>(T, policy, makespan);
+#endif
+    return sim_dev(T, policy, iterations, trace, makespan);
+}
+
 // The PlanTiming of build_plan_timing (src/timing.py:176-231) for one
 // explicit candidate, assembled from the stage / boundary tables; returns the
 // _evaluate status (GP_ERR_NO_FEASIBLE for a memory-infeasible plan unless
@@ -301,7 +461,7 @@ __global__ void k5_sim_candidates(DevInst I, int k, long long ncand, const uint8
     int st = cand_timing(I, k, order + i * k, counts + i * k, bm[i], opt_seconds, false, T);
     if (st != GP_OK) { makespan[i] = NAN; status[i] = (uint8_t)st; return; }
     double ms = NAN;
-    st = sim_dev(T, GP_POLICY_1F1B, iterations, nullptr, &ms);
+    st = sim_any(T, GP_POLICY_1F1B, iterations, nullptr, &ms);
     makespan[i] = ms;
     status[i] = (uint8_t)st;
 }
@@ -326,7 +486,7 @@ __global__ void k5_sim_1f1b(const gp_timing* __restrict__ T, long long n, int po
     if (i >= n) return;
     double ms = NAN;
     const gp_trace* tr = traces ? traces + (tidx ? tidx[i] : 0u) : nullptr;
-    int st = sim_dev(T[i], policy, iterations, tr, &ms);
+    int st = sim_any(T[i], policy, iterations, tr, &ms);
     makespan[i] = ms;
     status[i] = (uint8_t)st;
 }
