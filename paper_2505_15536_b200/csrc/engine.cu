@@ -190,6 +190,10 @@ struct gp_ctx {
     int ng = 0;       // run groups
     unsigned int sweep_W = 0;
     bool sweep_ok = false;
+    DBuf<K3Run> recruns;      // record sweep run table (k3_sweep_rec)
+    unsigned int rec_W = 0;
+    bool rec_ok = false;
+    DBuf<uint32_t> recrow;    // record sweep padded row starts
 
     DevInst view() {
         DevInst I;
@@ -325,7 +329,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     for (cudaEvent_t e : c->kt_ev) cudaEventDestroy(e);
-    c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release();
+    c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release(); c->recruns.release(); c->recrow.release();
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
     c->counter.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
@@ -587,6 +591,39 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
             c->sweep_W = (unsigned)start;
             c->sweep_ok = true;
         }
+        // record sweep: one run per (prefix, a), a ascending (runs longest
+        // first), prefixes in colex order; rpre = composition rank of
+        // (prefix, a, q = a + 1)
+        c->rec_ok = false;
+        if (k <= 6 && (k == 3 || pre_ok)) {
+            std::vector<K3Run> runs;
+            runs.reserve((size_t)h_binom(nn - 2, k - 2));
+            for (int a = k - 2; a <= nn - 2; ++a) {
+                const unsigned long long rows = h_binom(a - 1, k - 3);
+                for (unsigned long long r = 0; r < rows; ++r) {
+                    K3Run x = {};
+                    int p[8] = {0};
+                    for (int j = 1; j <= k - 3; ++j) p[j] = pre[(size_t)r * 16 + (j - 1)];
+                    p[k - 2] = a;
+                    for (int j = 0; j < k - 3; ++j) x.p[j] = (uint8_t)p[j + 1];
+                    x.a = (uint8_t)a;
+                    x.len = (uint8_t)(nn - 1 - a);
+                    unsigned long long rp = 0;
+                    for (int j = 1; j <= k - 2; ++j)
+                        rp += h_binom(nn - p[j - 1] - 1, k - j) - h_binom(nn - p[j], k - j);
+                    x.rpre = rp;
+                    runs.push_back(x);
+                }
+            }
+            std::vector<uint32_t> rs((size_t)nn + 4, 0u);
+            for (int a = k - 2, acc = 0; a <= nn - 2; ++a) { rs[a] = (uint32_t)acc; acc += k3r_lenp(nn, a); }
+            if (!runs.empty() && runs.size() < (1ull << 31)) {
+                CUDA_TRY(upload(s, c->recrow, rs.data(), rs.size()));
+                CUDA_TRY(upload(s, c->recruns, runs.data(), runs.size()));
+                c->rec_W = (unsigned)runs.size();
+                c->rec_ok = true;
+            }
+        }
     }
     c->loaded = true;
     replan_key(c, in, c->loaded_key);
@@ -780,9 +817,9 @@ static SwFn pick_sweep_rec(gp_ctx* c, int nb, int k, size_t* smem) {
         {k3_sweep_rec<3, 3>, k3_sweep_rec<3, 4>, k3_sweep_rec<3, 5>, k3_sweep_rec<3, 6>},
         {k3_sweep_rec<4, 3>, k3_sweep_rec<4, 4>, k3_sweep_rec<4, 5>, k3_sweep_rec<4, 6>}};
     static const int enabled = [] { const char* e = getenv("GP_K3_REC"); return e ? atoi(e) : 1; }();
-    if (!enabled || k < 3 || k > 6 || nb < 1 || nb > 4) return nullptr;
+    if (!enabled || k < 3 || k > 6 || nb < 1 || nb > 4 || !c->rec_ok) return nullptr;
     if (c->force_mode >= 0 && c->force_mode != 5) return nullptr;  // diagnostics pick a variant
-    const size_t need = k3r_smem(c->n, k, c->ngroups);
+    const size_t need = k3r_smem(c->n, k, nb);
     if (need > (size_t)c->smem_max) return nullptr;
     *smem = need;
     return c->verify ? pick_sweep_rec_verify(nb, k) : table[nb - 1][k - 3];
@@ -868,6 +905,16 @@ static cudaError_t kt_mark(gp_ctx* c, bool end) {
     return err;
 }
 
+// record sweep (persistent grid): run table, units and the per-CTA run-record
+// scratch; `units` = (snapshot, item, chunk) CTA tasks, returns the grid
+static int setup_rec(gp_ctx* c, SweepGeom& G) {
+    G.runs = c->recruns.p;
+    G.W = c->rec_W;
+    G.rowstart = c->recrow.p;
+    G.nrecp = k3r_nrecp(c->n, c->F);
+    return GP_OK;
+}
+
 static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_lo,
                         unsigned long long item_hi, int mode, const uint32_t* dflags,
                         int nb_sel = 0, int b0 = 0, int slot = 0) {
@@ -883,8 +930,9 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
     SwFn kern = c->verify ? pick_sweep_verify(mode, nb_sel > 0 ? nb_sel : c->nb, k)
                           : pick_sweep(mode, nb_sel > 0 ? nb_sel : c->nb, k);
+    bool rec = false;
     if (c->force_mode == 5)  // whole items per CTA only in large batches (K6)
-        if (SwFn r = pick_sweep_rec(c, nb_sel > 0 ? nb_sel : c->nb, k, &smem)) kern = r;
+        if (SwFn r = pick_sweep_rec(c, nb_sel > 0 ? nb_sel : c->nb, k, &smem)) { kern = r; rec = true; }
     int per_sm = 0;
     { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
       if (st_ != GP_OK) return st_; }
@@ -898,7 +946,9 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     if (const char* e = getenv("GP_K3_CPI")) if (atoi(e) > 0) cpi = (unsigned long long)atoi(e);  // diagnostic
     unsigned long long grid = items * cpi;
     if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "item range too large for one launch");
+    const unsigned long long units = grid;
     SweepGeom G;
+    if (rec) setup_rec(c, G);
     G.k = k;
     G.b0 = b0;
     G.nbm = R.nbm;
@@ -906,7 +956,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
     G.NP = R.NP;
     G.item0 = item_lo;
     G.cpi = cpi;
-    G.W = c->sweep_W;
+    if (!rec) G.W = c->sweep_W;
     G.ngroups = c->ngroups;
     G.ng = c->ng;
     G.groups = c->groups.p;
@@ -929,7 +979,7 @@ static int launch_sweep(gp_ctx* c, const RangeGeom& R, unsigned long long item_l
         c->ctr_armed = items;
     }
     G.item_ctr = c->item_ctr.p;
-    CUDA_TRY(c->blk.ensure(grid));
+    CUDA_TRY(c->blk.ensure(units));
     ArgminScratch S;
     S.blk = c->blk.p;
     S.counter = c->counter.p + slot;
@@ -1948,23 +1998,27 @@ static int snap_enqueue(gp_ctx* c, const double* d_bw, uint32_t nb, Key* d_keys,
     if (c->force_mode >= 0 && c->force_mode < mode) mode = c->force_mode;
     size_t smem = mode == 2 ? smem2 : (mode == 1 ? smem1 : smem0);
     SwFn kern = c->verify ? pick_sweep_verify(mode, c->nb, k) : pick_sweep(mode, c->nb, k);
+    bool rec = false;
     if ((mode == 2 && items * nb >= 2ull * c->n_sms) || c->force_mode == 5)
-        if (SwFn r = pick_sweep_rec(c, c->nb, k, &smem)) kern = r;
+        if (SwFn r = pick_sweep_rec(c, c->nb, k, &smem)) { kern = r; rec = true; }
     int per_sm = 0;
     { int st_ = kernel_slots(c, (const void*)kern, K3S_THREADS, smem, &per_sm);
       if (st_ != GP_OK) return st_; }
     unsigned long long resident = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
     unsigned long long cpi = (items * nb) >= resident ? 1 : resident / (items * nb);
-    unsigned long long tasks = (c->sweep_W + 31) / 32;
+    unsigned long long tasks = ((rec ? c->rec_W : c->sweep_W) + 31) / 32;
     unsigned long long cap = (tasks + (K3S_THREADS / 32) - 1) / (K3S_THREADS / 32);
     if (cpi > cap) cpi = cap;
     if (cpi < 1) cpi = 1;
     unsigned long long grid = (unsigned long long)nb * items * cpi;
     if (grid > 0x7fffffffull) return fail(GP_ERR_INPUT, "snapshot batch too large");
+    const unsigned long long units = grid;
     SweepGeom G;
+    if (rec) setup_rec(c, G);
     G.b0 = 0;
     G.k = k; G.nbm = c->nb * c->nm; G.NC = NC; G.NP = NP; G.item0 = 0; G.cpi = cpi;
-    G.W = c->sweep_W; G.ngroups = c->ngroups; G.ng = c->ng; G.groups = c->groups.p;
+    if (!rec) G.W = c->sweep_W;
+    G.ngroups = c->ngroups; G.ng = c->ng; G.groups = c->groups.p;
     G.prefixes = c->prefixes.p;
     G.bnk = c->bnk.p;
     G.gsteps = 1;
@@ -1976,11 +2030,15 @@ static int snap_enqueue(gp_ctx* c, const double* d_bw, uint32_t nb, Key* d_keys,
         G.vs = c->vs;
         G.vs.lo = c->vs.lo - vsnap0 * total;
     }
-    if (c->item_ctr.cap < (size_t)nb * items || !c->item_ctr.p) c->ctr_armed = 0;
-    CUDA_TRY(c->item_ctr.ensure((size_t)nb * items));
-    CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, (size_t)nb * items * sizeof(unsigned int), s));
+    // item counters, then (8-byte aligned) one u64 bound per snapshot for
+    // the record sweep, all zeroed per launch
+    const size_t nctr = ((size_t)nb * items + 1) & ~(size_t)1;
+    if (c->item_ctr.cap < nctr + 2 * (size_t)nb || !c->item_ctr.p) c->ctr_armed = 0;
+    CUDA_TRY(c->item_ctr.ensure(nctr + 2 * (size_t)nb));
+    CUDA_TRY(cudaMemsetAsync(c->item_ctr.p, 0, (nctr + 2 * (size_t)nb) * sizeof(unsigned int), s));
     G.item_ctr = c->item_ctr.p;
-    CUDA_TRY(c->blk.ensure(grid > 4096 ? grid : 4096));
+    G.gbound = reinterpret_cast<unsigned long long*>(c->item_ctr.p + nctr);
+    CUDA_TRY(c->blk.ensure(units > 4096 ? units : 4096));
     ArgminScratch S;
     S.blk = c->blk.p;
     S.counter = c->z_cnt.p;

@@ -239,6 +239,16 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k3_argmin(DevInst I, Rang
 // A run group = {first run id, a | len << 16, rows, segs_per_row}; the run
 // id -> (group, prefix row, segment) map is a binary search in smem.
 // ---------------------------------------------------------------------------
+// record sweep (k3_sweep_rec.cuh) run table entry: prefix cuts p1..p(k-3),
+// a = p(k-2), the run's length n-1-a and the composition rank of (prefix, a,
+// q = a+1); host-built per (n, k), runs ordered by length
+struct __align__(16) K3Run {
+    uint8_t p[4];
+    uint8_t a, len;
+    uint16_t pad;
+    unsigned long long rpre;
+};
+
 struct SweepGeom {
     int k, nbm;
     unsigned long long NC, NP;
@@ -260,6 +270,10 @@ struct SweepGeom {
     const unsigned long long* bnk;  // C(nn, r), nn <= n, r <= k: contiguous [n+1][k+1]
     int csize;                      // thread-block cluster size (CTAs of one item), 1 = none
     int interleave;                 // CTA -> item map: 1 = item-minor (b % items), 0 = item-major
+    unsigned long long* gbound = nullptr;  // k3_sweep_rec: per-snapshot shared bound (~bits, 0 = none)
+    const K3Run* runs = nullptr;    // k3_sweep_rec: run table ([W] runs)
+    const uint32_t* rowstart = nullptr;  // k3_sweep_rec: padded record row starts [n]
+    int nrecp = 0;                  // k3_sweep_rec: padded row records
     int b0;                         // first batch index of the NB evaluated together
     VerifySink vs;                  // parity tests only (VER instantiations)
 };

@@ -1,49 +1,75 @@
-// k3_sweep_rec.cuh - K3 sweep with per-item (a, q) records (the hot kernel of
-// the exhaustive and snapshot re-plans for k = 3..6 stage groups).
+// k3_sweep_rec.cuh - K3 sweep with per-item (a, q) records: the hot kernel of
+// the snapshot re-plans (K6) for k = 3..6 stage groups.
 #pragma once
 #include "k3_argmin.cuh"
 
-// Same enumeration, run structure, task queue and reduction as k3_sweep
-// (k3_argmin.cuh).  What changes is the q walk.  Along a run the prefix
-// stages are fixed and only the last two stages [a, q) and [q, n) vary, and
-// several terms of their Eq. 1 chains (src/costmodel.py:68-81) depend on
-// (a, q) or on q alone - not on the run:
+// Candidates of one (m, order) item are grouped into RUNS = (prefix cuts
+// p1..p(k-3), a = p(k-2)); a run walks every last cut q in (a, n-1].  Along
+// a run the stages 0..k-3 are fixed, and several terms of the last two
+// stages' Eq. 1 chains (src/costmodel.py:68-81) depend on (a, q) or on q
+// alone - not on the run:
 //     D2 = max(0, x1 - c2)   x1 = x(a) of boundary k-3, c2 = C1*m of [a, q)
 //     G2 = c2 + x2           x2 = x(q) of boundary k-2
 //     D3 = max(0, x2 - c3)   c3 = C1*m of [q, n)
-// so each CTA tabulates them once per item, in shared memory, as records
-//     row (a, q): {D2, G2, c2, AL2}      col q: {D3, c3, AL3}
-// and a q step of a run is, for the run's res1 / fill2 / mx1[b],
+// so each CTA (one (snapshot, item) unit) tabulates them once, in shared
+// memory, as
+//     row records (a, q): {D2, G2, c2, AL2}     col records q: {D3, AL3, M_b*c3}
+// and a q step of a run is, for the run's res1 / fill2 / mx1[b] (formed once
+// per run from stage 0..k-3 entries),
 //     res2 = res1 + D2,  fill3 = fill2 + G2,  res3 = res2 + D3
 //     t2_b = ((fill2 + M_b*c2) + res2) + AL2,  t3_b = ((fill3 + M_b*c3) + res3) + AL3
 //     cost_b = max(mx1_b, t2_b, t3_b)          (first-max)
 // - every value the same IEEE operation on the same operands as the
-// reference's order (the records hold the very sums and maxima the chains
-// would compute), so the costs are bit-identical; the q step drops from 6
-// adds + 2 integer max0 + 2 NB multiplies + 6 NB adds to 3 + 2 NB + 6 NB
-// with no integer work.  Rows hold only a in [k-2, n-2], q in [a+1, n-1]
-// (the pairs a sweep visits): (n-k+1)(n-k+2)/2 records of 32 B.  The run
-// minimum is kept per batch size (shorter select chains) and merged under
-// the reference key at the end of the run.
+// reference's order (the records hold the very sums, products and maxima the
+// chains would compute), so every cost is bit-identical.
+//
+// Arg-min: a lane keeps the best (cost, key) of the candidates that meet a
+// bound T - a cost some evaluated candidate has (the warp's, the CTA's and
+// the snapshot's best so far), so a candidate above T cannot be the arg-min.
+// cost <= T  <=>  t2 <= Tb && t3 <= Tb with Tb = T when mx1 <= T (else a
+// negative bound): two compares per candidate instead of two first-max
+// selects and a running minimum; the exact cost and the reference key are
+// formed only for the rare candidates within the bound.  Every candidate's
+// t2 and t3 are computed (the verify instantiation stores each cost).
+//
+// Runs come from a host-built table (prefix cuts, a, length, composition
+// rank), ordered by length, in 32-run tasks; a warp's lanes therefore walk in
+// lock step and read the same records (shared-memory broadcast).  Tasks go
+// to the warps in snake order (lengths balance); a warp loads its next
+// task's run entry and stage k-3 entry while it walks the current one.  Rows
+// of records are padded to a multiple of the q unroll with records whose
+// totals are +inf (no remainder loop).
 #ifndef K3R_UNROLL
-#define K3R_UNROLL 2
+#define K3R_UNROLL 4
+#endif
+#ifndef K3R_GT
+#define K3R_GT 1  // share the bound across the snapshot's CTAs (G.gbound)
 #endif
 
 struct __align__(16) K3RowRec { double D2, G2, c2, al2; };
-struct __align__(16) K3ColRec { double D3, c3, al3, pad; };
+// col q: D3, AL3 and M_b * c3 per batch size (the product the reference
+// forms, tabulated once per item)
+template <int NB>
+struct __align__(16) K3ColRecN { double D3, al3, Mc3[NB]; };
 
-// records of the compact (a, q) triangle before row a (a >= A0 = k-2)
-__device__ __forceinline__ int k3r_rowbase(int n, int A0, int a) {
-    // sum_{j=A0}^{a-1} (n-1-j)
-    return (a - A0) * (n - 1) - ((a - 1) * a / 2 - (A0 - 1) * A0 / 2);
+__host__ __device__ inline size_t k3r_colrec_bytes(int nb) { return ((size_t)(2 + nb) * 8 + 15) & ~(size_t)15; }
+
+// padded row length and row starts: rows a in [k-2, n-2], q in (a, n-1]
+__host__ __device__ __forceinline__ int k3r_lenp(int n, int a) {
+    return ((n - 1 - a) + K3R_UNROLL - 1) / K3R_UNROLL * K3R_UNROLL;
 }
-
-__host__ __device__ inline size_t k3r_smem(int n, int k, int ngroups) {
-    const size_t nrec = (size_t)(n - k + 1) * (n - k + 2) / 2;
+__host__ __device__ inline int k3r_nrecp(int n, int k) {
+    int s = 0;
+    for (int a = k - 2; a <= n - 2; ++a) s += k3r_lenp(n, a);
+    return s;
+}
+// shared layout: bar 16 | rows [nrecp] | cols [n + K3R_UNROLL] | rowstart [n] u32
+// (16-aligned) | row0 [n] double2 | x01 | x12 | x23 [nxp]
+__host__ __device__ inline size_t k3r_rowstart_bytes(int n) { return ((size_t)n * 4 + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t k3r_smem(int n, int k, int nb) {
     const size_t nxp = (size_t)((n + 1) & ~1);
-    return 16 + (((size_t)(n + 1) * (k + 1) * 8 + 15) & ~(size_t)15) + (size_t)ngroups * 16 +
-           nrec * sizeof(K3RowRec) + (size_t)(n + 1) * sizeof(K3ColRec) + (size_t)n * 16 +
-           nxp * 8;
+    return 16 + (size_t)k3r_nrecp(n, k) * sizeof(K3RowRec) + (size_t)(n + K3R_UNROLL) * k3r_colrec_bytes(nb) +
+           k3r_rowstart_bytes(n) + (size_t)n * 16 + 3 * nxp * 8;
 }
 
 template <int NB, int KS, bool VER = false>
@@ -51,21 +77,24 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
                                                               const unsigned long long* __restrict__ binom,
                                                               const uint32_t* skip_if_flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ unsigned long long s_thr;  // the CTA's bound (bits of a non-negative double)
     TL_START();
     pdl_trigger();
     pdl_wait();  // K1's tables (gp_replan graph); no-op on plain launches
     TL_WAITED();
+    (void)binom;
     constexpr int k = KS;
     const int n = I.n;
     const int ntri = n * (n + 1) / 2;
-    constexpr int KB = k + 1;
     const int A0 = k - 2;
+    const int nrecp = G.nrecp;
     const unsigned int per_snap = G.items * (unsigned int)G.cpi;
     const unsigned int snap = blockIdx.x / per_snap, local = blockIdx.x % per_snap;
-    const unsigned long long islot = !G.interleave ? local / G.cpi : local % G.items;
+    const unsigned int islot = local % G.items, csub = local / G.items;
     const unsigned long long item = G.item0 + islot;
     const int mi = (int)(item / G.NP);
     const unsigned long long perm_rank = item % G.NP;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     uint8_t order[GP_MAX_STAGES];
     d_unrank_perm(k, perm_rank, order);
     double Mv[NB];
@@ -74,111 +103,135 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
     const double2* TPm = G.tpk + snap * G.s_tpk + (size_t)mi * I.F * ntri;
     const double* X = G.xt + snap * G.s_xt + (size_t)mi * I.F * I.F * I.nxp;
     const int f1 = order[k - 3], f2 = order[k - 2], f3 = order[k - 1];
-    const double2* P0 = TPm + (size_t)order[0] * ntri;
     const double2* P1 = TPm + (size_t)f1 * ntri;
     const double2* P2 = TPm + (size_t)f2 * ntri;
     const double2* C3 = G.tcol + snap * G.s_tcol + ((size_t)mi * I.F + f3) * (n + 1);
-    const double* X01 = X + ((size_t)order[0] * I.F + order[1]) * I.nxp;
-    const double* X12 = X + ((size_t)f1 * I.F + f2) * I.nxp;
-    const double* X23 = X + ((size_t)f2 * I.F + f3) * I.nxp;
 
-    // shared: mbarrier | binom | groups | row records | col records | row0 | x01
     uint64_t* bar = (uint64_t*)smem_raw;
-    unsigned long long* bn = (unsigned long long*)(smem_raw + 16);
-    const uint32_t bn_bytes = (uint32_t)(((size_t)(n + 1) * KB * 8 + 15) & ~(size_t)15);
-    uint4* grp = (uint4*)(smem_raw + 16 + bn_bytes);
-    K3RowRec* rrec = (K3RowRec*)(grp + G.ngroups);
-    const int nrec = (n - k + 1) * (n - k + 2) / 2;
-    K3ColRec* crec = (K3ColRec*)(rrec + nrec);
-    double2* row0 = (double2*)(crec + (n + 1));
+    K3RowRec* rrec = (K3RowRec*)(smem_raw + 16);
+    K3ColRecN<NB>* crec = (K3ColRecN<NB>*)(rrec + nrecp);
+    uint32_t* rstart = (uint32_t*)(crec + (n + K3R_UNROLL));
+    double2* row0 = (double2*)((unsigned char*)rstart + k3r_rowstart_bytes(n));
     double* x01s = (double*)(row0 + n);
-    const uint32_t bytes = bn_bytes + (uint32_t)G.ngroups * 16 + (uint32_t)n * 16 +
-                           (uint32_t)I.nxp * 8;
+    double* x12s = x01s + I.nxp;
+    double* x23s = x12s + I.nxp;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        mbar_expect_tx(bar, bytes);
-        tma_bulk_g2s(bn, G.bnk, bn_bytes, bar);
-        tma_bulk_g2s(grp, G.groups, (uint32_t)G.ngroups * 16, bar);
-        tma_bulk_g2s(row0, P0, (uint32_t)n * 16, bar);
-        tma_bulk_g2s(x01s, X01, (uint32_t)I.nxp * 8, bar);
+        const uint32_t rsb = (uint32_t)k3r_rowstart_bytes(n);
+        mbar_expect_tx(bar, rsb + (uint32_t)(n * 16 + 3 * I.nxp * 8));
+        tma_bulk_g2s(rstart, G.rowstart, rsb, bar);
+        tma_bulk_g2s(row0, TPm + (size_t)order[0] * ntri, (uint32_t)n * 16, bar);
+        tma_bulk_g2s(x01s, X + ((size_t)order[0] * I.F + order[1]) * I.nxp, (uint32_t)I.nxp * 8, bar);
+        tma_bulk_g2s(x12s, X + ((size_t)f1 * I.F + f2) * I.nxp, (uint32_t)I.nxp * 8, bar);
+        tma_bulk_g2s(x23s, X + ((size_t)f2 * I.F + f3) * I.nxp, (uint32_t)I.nxp * 8, bar);
+        s_thr = 0x7FEFFFFFFFFFFFFFull;  // DBL_MAX
     }
-    // records, one warp per row a (lanes over q), straight from L2
-    {
-        const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-        for (int a = A0 + wid; a <= n - 2; a += nw) {
-            const double x1 = __ldg(&X12[a - 1]);
-            const double2* prow = P2 + (rowoff(n, a) - a - 1);
-            K3RowRec* rr = rrec + (k3r_rowbase(n, A0, a) - a - 1);
-            for (int q = a + 1 + lane; q <= n - 1; q += 32) {
-                GP_DCHECK(k3r_rowbase(n, A0, a) - a - 1 + q < nrec);
-                const double2 e2 = __ldg(&prow[q]);
-                const double x2 = __ldg(&X23[q - 1]);
-                K3RowRec r;
-                r.D2 = max0f(x1 - e2.x);
-                r.G2 = e2.x + x2;
-                r.c2 = e2.x;
-                r.al2 = e2.y;
-                rr[q] = r;
-            }
+    // the first tasks' run entries (independent of the tables)
+    const int ntask = (int)((G.W + 31) / 32);
+    const int wg = (int)csub * nw + wid, wstride = (int)G.cpi * nw;
+    auto task_of = [&](int j) {  // snake order over the warps
+        return j * wstride + ((j & 1) ? (wstride - 1 - wg) : wg);
+    };
+    auto load_run = [&](int j, K3Run& r) {
+        const int t = task_of(j);
+        const unsigned int u = (unsigned int)t * 32u + lane;
+        if (t < ntask && u < G.W) {
+            r = G.runs[u];
+        } else {
+            r.a = (uint8_t)A0;
+            r.len = 0;
+            r.rpre = 0;
+            r.p[0] = r.p[1] = r.p[2] = r.p[3] = 0;
         }
-        for (int q = threadIdx.x; q <= n; q += blockDim.x) {
-            K3ColRec cr;
-            const double2 e3 = __ldg(&C3[q]);
-            const double x2 = q >= 1 ? __ldg(&X23[q - 1]) : 0.0;
-            cr.D3 = max0f(x2 - e3.x);
-            cr.c3 = e3.x;
-            cr.al3 = e3.y;
-            cr.pad = 0.0;
-            crec[q] = cr;
-        }
-    }
-    __syncthreads();
+    };
+    K3Run ri_a, ri_b;
+    load_run(0, ri_a);
+    load_run(1, ri_b);
+    __syncthreads();  // mbarrier initialised
     mbar_wait(bar, 0);
 
-    const int lane = threadIdx.x & 31;
-    double best_c = INFINITY;
-    unsigned long long best_t = ~0ull;  // R * NB + bi
-    const bool skip = skip_if_flags && skip_if_flags[snap];  // generic kernel decides
-    unsigned int* const ctr = &G.item_ctr[(size_t)snap * G.items + islot];
-    unsigned int t_next = 0;
-    if (lane == 0 && !skip) t_next = atomicAdd(ctr, 1u);
-    for (; !skip;) {
-        const unsigned int t = __shfl_sync(0xffffffffu, t_next, 0);
-        if ((unsigned long long)t * 32 >= G.W) break;
-        if (lane == 0) t_next = atomicAdd(ctr, 1u);  // next task, latency hidden by this one
-        const unsigned int u = t * 32 + lane;
-        int len = 0, a = A0 > 0 ? A0 : 1, q0 = a + 1;  // idle lanes keep in-range addresses
-        double fill2 = 0.0, res1 = 0.0;
-        double mx1[NB];
+    // ---- row records (a, q): one warp per row, lanes over q; padding
+    // records (q > n-1) have +inf totals
+    for (int a = A0 + wid; a <= n - 2; a += nw) {
+        const double x1 = x12s[a - 1];
+        const double2* prow = P2 + rowoff(n, a) - a - 1;
+        K3RowRec* rr = rrec + rstart[a];
+        const int L = n - 1 - a, Lp = k3r_lenp(n, a);
+        for (int i = lane; i < Lp; i += 32) {
+            K3RowRec r;
+            if (i < L) {
+                const int q = a + 1 + i;
+                GP_DCHECK(rstart[a] + i < (uint32_t)nrecp);
+                const double2 e2 = __ldg(&prow[q]);
+                r.D2 = max0f(x1 - e2.x);
+                r.G2 = e2.x + x23s[q - 1];
+                r.c2 = e2.x;
+                r.al2 = e2.y;
+            } else {
+                r.D2 = r.G2 = r.c2 = 0.0;
+                r.al2 = INFINITY;
+            }
+            rr[i] = r;
+        }
+    }
+    // ---- col records q (padding past n: +inf totals)
+    for (int q = threadIdx.x; q < n + K3R_UNROLL; q += blockDim.x) {
+        K3ColRecN<NB> cr;
+        if (q <= n) {
+            const double2 e3 = __ldg(&C3[q]);
+            const double x2 = q >= 1 ? x23s[q - 1] : 0.0;
+            cr.D3 = max0f(x2 - e3.x);
+            cr.al3 = e3.y;
 #pragma unroll
-        for (int bi = 0; bi < NB; ++bi) mx1[bi] = -INFINITY;
-        unsigned long long rpre = 0;  // comp rank of (prefix, a, q = a + 1)
-        if (u < G.W) {
-            int gi = ((const uint16_t*)(grp + G.ng))[t];
-            while (gi + 1 < G.ng && grp[gi + 1].x <= u) ++gi;
-            const uint4 g = grp[gi];
-            const unsigned int lo = u - g.x;
-            a = (int)(g.y & 0xffffu);
-            len = (int)(g.y >> 16);
-            unsigned int row;
-            if (g.w) { const unsigned seg = lo / g.z; row = lo - seg * g.z; q0 = a + 1 + (int)seg * K3_SEG; }
-            else { row = lo; q0 = n - len; }
+            for (int bi = 0; bi < NB; ++bi) cr.Mc3[bi] = Mv[bi] * e3.x;
+        } else {
+            cr.D3 = 0.0;
+            cr.al3 = INFINITY;
+#pragma unroll
+            for (int bi = 0; bi < NB; ++bi) cr.Mc3[bi] = 0.0;
+        }
+        crec[q] = cr;
+    }
+    // stage k-3 entry of a run (L2), loaded one task ahead
+    auto load_e1 = [&](const K3Run& r) -> double2 {
+        const int a = r.a, pk3 = (k > 3) ? r.p[k > 3 ? k - 4 : 0] : 0;
+        return r.len ? __ldg(&P1[rowoff(n, pk3) + (a - pk3 - 1)]) : make_double2(0.0, 0.0);
+    };
+    double2 e1_a = load_e1(ri_a);
+    __syncthreads();  // records complete
+
+    double best_c = INFINITY;  // lane best (cost, R * NB + bi) within the bound
+    unsigned long long best_t = ~0ull, inf_t = ~0ull;
+    double T = __longlong_as_double((long long)0x7FEFFFFFFFFFFFFFull);
+    const bool skip = skip_if_flags && skip_if_flags[snap];  // generic kernel decides
+    unsigned long long* const gbound = G.gbound ? G.gbound + snap : nullptr;
+    unsigned long long gb_prev = 0ull;
+    for (int j = 0; !skip && task_of(j) < ntask; ++j) {
+        const K3Run ri = ri_a;
+        const double2 e1 = e1_a;
+        // in flight during this task's walk: the next task's stage k-3 entry
+        // and the run entries of the one after
+        ri_a = ri_b;
+        e1_a = load_e1(ri_a);
+        load_run(j + 2, ri_b);
+        {
+            unsigned long long ct = *(volatile unsigned long long*)&s_thr;
+            if (K3R_GT && gb_prev != 0ull && ~gb_prev < ct) ct = ~gb_prev;
+            if (ct < (unsigned long long)__double_as_longlong(T)) T = __longlong_as_double((long long)ct);
+            // the snapshot's bound, consumed at the next task
+            if (K3R_GT && gbound) gb_prev = *(volatile unsigned long long*)gbound;
+        }
+        const int len = ri.len;
+        const int a = ri.a;
+        const unsigned long long rpre = ri.rpre;  // comp rank of (prefix, a, q = a + 1)
+        // stages 0..k-3 of the run: fill2, res1 and the first-max mx1
+        double fill2, res1, mx1[NB];
+        {
             int p[k + 1];
             p[0] = 0;
-            if (k == 4) {
-                p[1] = (int)row + 1;
-            } else if (k > 3) {
-                const uint8_t* pr = G.prefixes + (size_t)row * 16;
 #pragma unroll
-                for (int j = 1; j <= k - 3; ++j) p[j] = pr[j - 1];
-            }
+            for (int jj = 1; jj <= k - 3; ++jj) p[jj] = ri.p[jj - 1];
             p[k - 2] = a;
-            GP_DCHECK(gi < G.ng && a >= k - 2 && a <= n - 2 && len >= 1 && len <= K3_SEG &&
-                      q0 >= a + 1 && q0 + len - 1 <= n - 1);
-#pragma unroll
-            for (int j = 1; j <= k - 2; ++j)
-                rpre += bn[(n - p[j - 1] - 1) * KB + (k - j)] - bn[(n - p[j]) * KB + (k - j)];
-            // stages 0..k-4 (fixed by the prefix)
             double fill = 0.0, res = 0.0, xprev = 0.0;
             double mx[NB];
 #pragma unroll
@@ -188,8 +241,8 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
                 double2 e;
                 double x;
                 if (s == 0) {
-                    e = row0[p[1] - 1];
-                    x = x01s[p[1] - 1];
+                    e = row0[p[1] > 0 ? p[1] - 1 : 0];
+                    x = x01s[p[1] > 0 ? p[1] - 1 : 0];
                 } else {
                     e = __ldg(&TPm[(size_t)order[s] * ntri + rowoff(n, p[s]) + (p[s + 1] - p[s] - 1)]);
                     x = __ldg(&X[((size_t)order[s] * I.F + order[s + 1]) * I.nxp + (p[s + 1] - 1)]);
@@ -197,82 +250,113 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
                 if (s > 0) res = res + max0f(xprev - e.x);
 #pragma unroll
                 for (int bi = 0; bi < NB; ++bi) {
-                    double tot = ((fill + Mv[bi] * e.x) + res) + e.y;
+                    const double tot = ((fill + Mv[bi] * e.x) + res) + e.y;
                     mx[bi] = (s == 0) ? tot : gtsel(tot, mx[bi]);
                 }
                 fill = fill + (e.x + x);
                 xprev = x;
             }
-            // stage k-3 = [p[k-3], a) (fixed by the run)
-            const int pk3 = p[k - 3];
-            const double2 e1 = __ldg(&P1[rowoff(n, pk3) - pk3 - 1 + a]);
-            const double x1 = __ldg(&X12[a - 1]);
             res1 = (k > 3) ? res + max0f(xprev - e1.x) : res;
 #pragma unroll
             for (int bi = 0; bi < NB; ++bi) {
-                double t1 = ((fill + Mv[bi] * e1.x) + res1) + e1.y;
+                const double t1 = ((fill + Mv[bi] * e1.x) + res1) + e1.y;
                 mx1[bi] = (k > 3) ? gtsel(t1, mx[bi]) : t1;
             }
-            fill2 = fill + (e1.x + x1);
+            fill2 = fill + (e1.x + x12s[a - 1]);
         }
-        int lmax = len, lmin = len;
+        const int lenp = len ? k3r_lenp(n, a) : 0;
+        int lmax = lenp;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            int o = __shfl_xor_sync(0xffffffffu, lmax, off);
+            const int o = __shfl_xor_sync(0xffffffffu, lmax, off);
             lmax = o > lmax ? o : lmax;
-            o = __shfl_xor_sync(0xffffffffu, lmin, off);
-            lmin = o < lmin ? o : lmin;
         }
-        const K3RowRec* rp = rrec + (k3r_rowbase(n, A0, a) - a - 1) + q0;
-        const K3ColRec* cp = crec + q0;
-        // per batch size: the run minimum (strict <: earliest q wins; the first
-        // q stands when every cost is +inf)
-        double run_c[NB];
-        int run_q[NB];
+        const K3RowRec* rp = rrec + rstart[a];
+        const K3ColRecN<NB>* cp = crec + (a + 1);
+        // the run's first key: the lane's answer when none of its candidates
+        // is finite (every cost +inf: the earliest key wins)
+        if (len > 0) inf_t = rpre * NB < inf_t ? rpre * NB : inf_t;
+        // per batch size: cost = max(mx1, t2, t3) <= T  <=>  t2 <= Tb && t3 <= Tb
+        // with Tb = T when mx1 <= T, else a negative bound
+        double Tb[NB];
+        auto set_bounds = [&]() {
 #pragma unroll
-        for (int bi = 0; bi < NB; ++bi) { run_c[bi] = INFINITY; run_q[bi] = 0; }
-        auto eval_q = [&](int i) {
-            GP_DCHECK(i >= 0 && i < len && k3r_rowbase(n, A0, a) - a - 1 + q0 + i < nrec);
+            for (int bi = 0; bi < NB; ++bi) Tb[bi] = (len > 0 && mx1[bi] <= T) ? T : -1.0;
+        };
+        set_bounds();
+        auto step = [&](int i, double* t2, double* t3) -> bool {
+            GP_DCHECK(rstart[a] + i < (uint32_t)nrecp && a + 1 + i < n + K3R_UNROLL);
             const K3RowRec R = rp[i];
-            const K3ColRec Cq = cp[i];
+            const K3ColRecN<NB> Cq = cp[i];
             const double res2 = res1 + R.D2;
             const double fill3 = fill2 + R.G2;
             const double res3 = res2 + Cq.D3;
+            bool p = false;
 #pragma unroll
             for (int bi = 0; bi < NB; ++bi) {
-                const double t2 = ((fill2 + Mv[bi] * R.c2) + res2) + R.al2;
-                const double t3 = ((fill3 + Mv[bi] * Cq.c3) + res3) + Cq.al3;
-                double c = gtsel(t2, mx1[bi]);
-                c = gtsel(t3, c);
+                t2[bi] = ((fill2 + Mv[bi] * R.c2) + res2) + R.al2;
+                t3[bi] = ((fill3 + Cq.Mc3[bi]) + res3) + Cq.al3;
+                p |= (t2[bi] <= Tb[bi]) & (t3[bi] <= Tb[bi]);
                 if constexpr (VER)
-                    vput(G.vs, snap,
-                         ((((unsigned long long)(G.b0 + bi) * I.nm + mi) * G.NP + perm_rank) * G.NC) +
-                             rpre + (unsigned long long)(q0 + i - a - 1), c);
-                if (c < run_c[bi]) { run_c[bi] = c; run_q[bi] = i; }
+                    if (i < len)
+                        vput(G.vs, snap,
+                             ((((unsigned long long)(G.b0 + bi) * I.nm + mi) * G.NP + perm_rank) * G.NC) +
+                                 rpre + (unsigned long long)i,
+                             gtsel(t3[bi], gtsel(t2[bi], mx1[bi])));
+            }
+            return p;
+        };
+        // a candidate within the bound: its exact cost (first-max, the
+        // reference's order) against the lane's best under the full key
+        auto take = [&](int i, const double* t2, const double* t3) {
+#pragma unroll
+            for (int bi = 0; bi < NB; ++bi) {
+                const double c = gtsel(t3[bi], gtsel(t2[bi], mx1[bi]));
+                const unsigned long long tk = (rpre + (unsigned long long)i) * NB + bi;
+                if (c < best_c || (c == best_c && tk < best_t)) { best_c = c; best_t = tk; }
             }
         };
-        int i0 = 0;
-        for (; i0 + K3R_UNROLL - 1 < lmin; i0 += K3R_UNROLL) {
+        // the warp's bound: min of its lanes' best costs, shared with the CTA
+        // and the snapshot
+        auto refresh = [&]() {
+            unsigned long long m = __double_as_longlong(best_c);
 #pragma unroll
-            for (int uu = 0; uu < K3R_UNROLL; ++uu) eval_q(i0 + uu);
-        }
-        for (int i = i0; i < lmax; ++i)
-            if (i < len) eval_q(i);
-        if (len > 0) {
-#pragma unroll
-            for (int bi = 0; bi < NB; ++bi) {
-                const unsigned long long tk =
-                    (rpre + (unsigned long long)(q0 + run_q[bi] - a - 1)) * NB + bi;
-                if (run_c[bi] < best_c || (run_c[bi] == best_c && tk < best_t)) {
-                    best_c = run_c[bi];
-                    best_t = tk;
+            for (int off = 16; off > 0; off >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, m, off);
+                m = o < m ? o : m;
+            }
+            if (m < (unsigned long long)__double_as_longlong(T)) {
+                if (lane == 0) {
+                    atomicMin(&s_thr, m);
+                    if (K3R_GT && gbound) atomicMax(gbound, ~m);
                 }
+                T = __longlong_as_double((long long)m);
+            }
+            set_bounds();
+        };
+        for (int i0 = 0; i0 < lmax; i0 += K3R_UNROLL) {
+            // lanes past their (padded) row: no candidate (in-range reads)
+            const bool act = i0 < lenp;
+            const int ib = act ? i0 : 0;
+            double t2[K3R_UNROLL][NB], t3[K3R_UNROLL][NB];
+            bool p[K3R_UNROLL], any = false;
+#pragma unroll
+            for (int uu = 0; uu < K3R_UNROLL; ++uu) {
+                p[uu] = step(ib + uu, t2[uu], t3[uu]) & act;
+                any |= p[uu];
+            }
+            if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+                for (int uu = 0; uu < K3R_UNROLL; ++uu)
+                    if (p[uu]) take(i0 + uu, t2[uu], t3[uu]);
+                refresh();
             }
         }
     }
     Key mine{INFINITY, ~0ull};
+    if (best_t == ~0ull) best_t = inf_t;  // nothing finite within the bound
     if (best_t != ~0ull) {
-        unsigned long long rr = best_t / NB, bi = best_t % NB;
+        const unsigned long long rr = best_t / NB, bi = best_t % NB;
         GP_DCHECK(rr < G.NC);
         mine.cost = best_c;
         mine.tie = ((perm_rank * G.NC) + rr) * (unsigned long long)G.nbm +
@@ -282,8 +366,8 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
     Ss.blk = S.blk + (size_t)snap * per_snap;
     Ss.counter = S.counter + snap;
     Ss.result = S.result + snap;
-    Ss.rearm = ctr - islot;  // this snapshot's item counters
-    Ss.nrearm = G.items;
+    Ss.rearm = nullptr;
+    Ss.nrearm = 0;
     block_argmin_finish(mine, Ss, per_snap, local);
     TL_STOP(31);
 }
