@@ -59,7 +59,7 @@ enum : uint32_t { FLAG_STAGE_ERROR = 1, FLAG_OVERFLOW = 2, FLAG_GATEWAY_ERROR = 
 #define K3_THREADS 256
 #define K3_TILE 256
 #ifndef K3_SEG
-#define K3_SEG 128
+#define K3_SEG 32
 #endif
 #ifndef K3_QPAIR
 #define K3_QPAIR 1  // k3_sweep: two q steps per iteration where the warp's runs allow
