@@ -615,6 +615,11 @@ int gp_ctx_load(gp_ctx* c, const gp_instance* in) {
                     runs.push_back(x);
                 }
             }
+            for (size_t t0 = 0; t0 < runs.size(); t0 += 32) {
+                int mx = 0;
+                for (size_t u = t0; u < runs.size() && u < t0 + 32; ++u) mx = std::max(mx, k3r_lenp(nn, runs[u].a));
+                for (size_t u = t0; u < runs.size() && u < t0 + 32; ++u) runs[u].tmax = (uint8_t)mx;
+            }
             std::vector<uint32_t> rs((size_t)nn + 4, 0u);
             for (int a = k - 2, acc = 0; a <= nn - 2; ++a) { rs[a] = (uint32_t)acc; acc += k3r_lenp(nn, a); }
             if (!runs.empty() && runs.size() < (1ull << 31)) {

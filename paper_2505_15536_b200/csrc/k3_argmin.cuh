@@ -240,12 +240,14 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k3_argmin(DevInst I, Rang
 // id -> (group, prefix row, segment) map is a binary search in smem.
 // ---------------------------------------------------------------------------
 // record sweep (k3_sweep_rec.cuh) run table entry: prefix cuts p1..p(k-3),
-// a = p(k-2), the run's length n-1-a and the composition rank of (prefix, a,
-// q = a+1); host-built per (n, k), runs ordered by length
+// a = p(k-2), the run's length n-1-a, the longest padded length in its 32-run
+// task and the composition rank of (prefix, a, q = a+1); host-built per
+// (n, k), runs ordered by length
 struct __align__(16) K3Run {
     uint8_t p[4];
     uint8_t a, len;
-    uint16_t pad;
+    uint8_t tmax;  // longest padded run of its 32-run task
+    uint8_t pad;
     unsigned long long rpre;
 };
 

@@ -42,6 +42,9 @@
 #ifndef K3R_UNROLL
 #define K3R_UNROLL 4
 #endif
+#ifndef K3R_RB
+#define K3R_RB 4  // row-record (row, lane chunk) pairs per warp in flight
+#endif
 #ifndef K3R_GT
 #define K3R_GT 1  // share the bound across the snapshot's CTAs (G.gbound)
 #endif
@@ -140,6 +143,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
         } else {
             r.a = (uint8_t)A0;
             r.len = 0;
+            r.tmax = 0;
             r.rpre = 0;
             r.p[0] = r.p[1] = r.p[2] = r.p[3] = 0;
         }
@@ -152,27 +156,44 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
 
     // ---- row records (a, q): one warp per row, lanes over q; padding
     // records (q > n-1) have +inf totals
-    for (int a = A0 + wid; a <= n - 2; a += nw) {
-        const double x1 = x12s[a - 1];
-        const double2* prow = P2 + rowoff(n, a) - a - 1;
-        K3RowRec* rr = rrec + rstart[a];
-        const int L = n - 1 - a, Lp = k3r_lenp(n, a);
-        for (int i = lane; i < Lp; i += 32) {
-            K3RowRec r;
-            if (i < L) {
-                const int q = a + 1 + i;
-                GP_DCHECK(rstart[a] + i < (uint32_t)nrecp);
-                const double2 e2 = __ldg(&prow[q]);
-                r.D2 = max0f(x1 - e2.x);
-                r.G2 = e2.x + x23s[q - 1];
-                r.c2 = e2.x;
-                r.al2 = e2.y;
-            } else {
-                r.D2 = r.G2 = r.c2 = 0.0;
-                r.al2 = INFINITY;
+    // (the (row, lane-chunk) pairs of a warp in batches of K3R_RB, loads
+    // first: several L2 round trips in flight)
+    {
+        const int rows = n - 1 - A0;
+        int a = A0 + wid, i = lane;  // the warp's first pair
+        while (a <= n - 2) {
+            int ba[K3R_RB], bi[K3R_RB];
+            double2 e2[K3R_RB];
+#pragma unroll
+            for (int v = 0; v < K3R_RB; ++v) {
+                ba[v] = a;
+                bi[v] = i;
+                if (a <= n - 2 && i < n - 1 - a) e2[v] = __ldg(&P2[rowoff(n, a) + i]);
+                // next pair: next lane chunk of this row, else the warp's next row
+                if (a <= n - 2) {
+                    i += 32;
+                    if (i >= k3r_lenp(n, a)) { a += nw; i = lane; }
+                }
             }
-            rr[i] = r;
+#pragma unroll
+            for (int v = 0; v < K3R_RB; ++v) {
+                const int ra = ba[v], ri_ = bi[v];
+                if (ra > n - 2 || ri_ >= k3r_lenp(n, ra)) continue;
+                GP_DCHECK(rstart[ra] + ri_ < (uint32_t)nrecp);
+                K3RowRec r;
+                if (ri_ < n - 1 - ra) {
+                    r.D2 = max0f(x12s[ra - 1] - e2[v].x);
+                    r.G2 = e2[v].x + x23s[ra + ri_];
+                    r.c2 = e2[v].x;
+                    r.al2 = e2[v].y;
+                } else {
+                    r.D2 = r.G2 = r.c2 = 0.0;
+                    r.al2 = INFINITY;
+                }
+                rrec[rstart[ra] + ri_] = r;
+            }
         }
+        (void)rows;
     }
     // ---- col records q (padding past n: +inf totals)
     for (int q = threadIdx.x; q < n + K3R_UNROLL; q += blockDim.x) {
@@ -265,12 +286,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
             fill2 = fill + (e1.x + x12s[a - 1]);
         }
         const int lenp = len ? k3r_lenp(n, a) : 0;
-        int lmax = lenp;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const int o = __shfl_xor_sync(0xffffffffu, lmax, off);
-            lmax = o > lmax ? o : lmax;
-        }
+        const int lmax = __shfl_sync(0xffffffffu, ri.tmax, 0);  // the task's longest (lane 0 holds a run)
         const K3RowRec* rp = rrec + rstart[a];
         const K3ColRecN<NB>* cp = crec + (a + 1);
         // the run's first key: the lane's answer when none of its candidates
