@@ -62,14 +62,15 @@ REF_OPS_PER_CAND_C4 = 39
 # fixes stages 0..k-3, so only the last two stages vary along q, and the
 # record sweep (k3_sweep_rec, the K6 batch kernel) tabulates per item the
 # terms that depend on (a, q) or q alone (D2 = max0(x1 - c2), G2 = c2 + x2,
-# D3 = max0(x2 - c3)).  Per q, shared by the NB batch sizes: res2, fill3, res3
-# = 3 adds; per (q, b): M*c2, M*c3, 6 adds for t2 and t3, 2 max compares and
-# the run-min compare = 11.  NB = 2: (3 + 2 * 11) / 2 = 12.5 per candidate
-# (the per-item tables add ~0.1).  39 x rate exceeds the FP64 pipe peak (the
-# prefix work is shared), so the roofline uses this count; the reference-
-# order equivalent rate is reported beside it.
+# D3 = max0(x2 - c3), M_b*c3).  Per q, shared by the NB batch sizes: res2,
+# fill3, res3 = 3 adds; per (q, b): M_b*c2, 6 adds for t2 and t3 and the two
+# compares against the arg-min bound (cost = max(mx1, t2, t3) <= T) = 9.
+# NB = 2: (3 + 2 * 9) / 2 = 10.5 per candidate (the per-run and per-item
+# work adds ~0.3).  39 x rate exceeds the FP64 pipe peak (the prefix work is
+# shared), so the roofline uses this count; the reference-order equivalent
+# rate is reported beside it.
 def sweep_ops_per_candidate(nb):
-    return (3 + 11 * nb) / nb
+    return (3 + 9 * nb) / nb
 
 
 # Measured by ncu on the sweep kernel of this workload (not in-run):
@@ -924,8 +925,8 @@ def main():
                          "candidates_per_launch": cand_per_launch,
                          "share_of_step": launch_ms / per_step_ms,
                          "algorithmic_ops_per_candidate": alg_ops,
-                         "algorithm": "prefix-sharing record sweep (DESIGN.md §4): 12.5 FP64 "
-                                      "ops per C4 candidate",
+                         "algorithm": "prefix-sharing record sweep with a bound-filtered arg-min "
+                                      "(DESIGN.md §4): 10.5 FP64 ops per C4 candidate",
                          "reference_order_ops_per_candidate": REF_OPS_PER_CAND_C4,
                          "reference_equivalent_tflops": REF_OPS_PER_CAND_C4 * cand_per_launch
                          / (launch_ms * 1e-3) / 1e12,
