@@ -708,6 +708,25 @@ int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_ord
         bool t4 = q4 && ((((uintptr_t)d_order | (uintptr_t)d_counts | (uintptr_t)d_bm) & 15u) == 0) &&
                   k2t_smem(sc_bytes) <= (size_t)c->smem_max;
         if (const char* e = getenv("GP_K2_TMA")) t4 = t4 && atoi(e) != 0;
+        // vector-lane variant: 32-byte aligned costs, 4-byte aligned status
+        // (GP_K2_V4=0 disables)
+        bool v4 = t4 && ((((uintptr_t)d_cost) & 31u) == 0) && ((((uintptr_t)d_status) & 3u) == 0) &&
+                  k2v_smem(sc_bytes) <= (size_t)c->smem_max;
+        if (const char* e = getenv("GP_K2_V4")) v4 = v4 && atoi(e) != 0;
+        if (v4) {
+            const size_t smem_v = k2v_smem(sc_bytes);
+            int per_sm = 0;
+            { int st_ = kernel_slots(c, (const void*)k2_eval_batch_v4, K2V_THREADS, smem_v, &per_sm);
+              if (st_ != GP_OK) return st_; }
+            unsigned long long grid = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
+            const unsigned long long chunks = (n + (unsigned long long)K2V_WCHUNK * K2V_WARPS - 1) /
+                                              ((unsigned long long)K2V_WCHUNK * K2V_WARPS);
+            if (grid > chunks) grid = chunks;
+            k2_eval_batch_v4<<<(unsigned)grid, K2V_THREADS, smem_v, c->stream>>>(
+                I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status, (unsigned)sc_bytes);
+            CUDA_TRY(cudaGetLastError());
+            return GP_OK;
+        }
         if (t4) {
             const size_t smem_t = k2t_smem(sc_bytes);
             int per_sm = 0;

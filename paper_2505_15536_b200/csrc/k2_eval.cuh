@@ -551,3 +551,239 @@ static __global__ void __launch_bounds__(K2T_THREADS, K2T_MINB) k2_eval_batch_t4
     __syncwarp();
     if (lane < q) eval_entry(wq[lane]);
 }
+
+// ---- K2, k = 4, large batches: vector lanes -----------------------------------
+// As k2_eval_batch_t4 (per-warp TMA rings of input chunks, feasible
+// candidates queued and evaluated 32 at a time), but a lane classifies FOUR
+// CONSECUTIVE candidates per round: their order / counts words arrive in one
+// 16-byte shared-memory load each and their four bm bytes in one 32-bit
+// load, the classification is branch-free, and the four costs and four
+// status bytes leave in two 16-byte and one 4-byte store.  Memory-infeasible
+// stages come from a bit table (one bit per (group, a, b), 3.3 KB at C4,
+// built from the stage codes by each CTA) instead of the byte table, so more
+// CTAs fit an SM.  Queued (feasible) candidates get a placeholder cost in the
+// vector store and their cost from eval_fast later (same warp, after a
+// __syncwarp); candidates the fast tables cannot decide (an error status may
+// follow) go through eval_tables.
+#ifndef K2V_WCHUNK
+#define K2V_WCHUNK 256
+#endif
+#ifndef K2V_STAGES
+#define K2V_STAGES 2
+#endif
+#define K2V_QCAP 160  // queue entries per warp: < 32 left + 128 of one round
+#define K2V_THREADS 256
+#ifndef K2V_MINB
+#define K2V_MINB 3
+#endif
+#define K2V_WARPS (K2V_THREADS / 32)
+#define K2V_SLOT (K2V_WCHUNK * 9)  // order u32 | counts u32 | bm u8 per candidate
+
+__host__ __device__ inline size_t k2v_bits_bytes(size_t sc_bytes) { return ((sc_bytes + 31) / 32 * 4 + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t k2v_smem(size_t sc_bytes) {
+    return (((size_t)K2V_WARPS * K2V_STAGES * 8 + 63) & ~(size_t)63) + k2v_bits_bytes(sc_bytes) +
+           (size_t)K2V_WARPS * K2V_STAGES * K2V_SLOT + (size_t)K2V_WARPS * K2V_QCAP * 16;
+}
+
+static __global__ void __launch_bounds__(K2V_THREADS, K2V_MINB) k2_eval_batch_v4(DevInst I, long long ncand,
+                                                              const uint8_t* __restrict__ order,
+                                                              const uint8_t* __restrict__ counts,
+                                                              const uint8_t* __restrict__ bm,
+                                                              double* __restrict__ cost,
+                                                              uint8_t* __restrict__ status,
+                                                              unsigned sc_bytes) {
+    extern __shared__ __align__(16) uint8_t v4_s[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t bar_bytes = ((size_t)K2V_WARPS * K2V_STAGES * 8 + 63) & ~(size_t)63;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(v4_s) + warp * K2V_STAGES;
+    uint32_t* ibits = reinterpret_cast<uint32_t*>(v4_s + bar_bytes);
+    uint8_t* ring = v4_s + bar_bytes + k2v_bits_bytes(sc_bytes) + (size_t)warp * K2V_STAGES * K2V_SLOT;
+    uint4* wq = reinterpret_cast<uint4*>(v4_s + bar_bytes + k2v_bits_bytes(sc_bytes) +
+                                         (size_t)K2V_WARPS * K2V_STAGES * K2V_SLOT) + warp * K2V_QCAP;
+    const int n = I.n;
+    const int N2 = (n + 1) * (n + 1);
+    const long long nchunks = (ncand + K2V_WCHUNK - 1) / K2V_WCHUNK;
+    const long long wstride = (long long)gridDim.x * K2V_WARPS;
+    const long long wfirst = (long long)blockIdx.x * K2V_WARPS + warp;
+    auto issue = [&](long long c, int slot) {  // lane 0
+        const long long left = ncand - c * K2V_WCHUNK;
+        const int cnt = (left < K2V_WCHUNK ? (int)left : K2V_WCHUNK) & ~15;  // ragged tail: direct loads
+        uint8_t* dst = ring + (size_t)slot * K2V_SLOT;
+        mbar_expect_tx(&bar[slot], (uint32_t)cnt * 9u);
+        if (cnt) {
+            tma_bulk_g2s(dst, order + c * K2V_WCHUNK * 4, (uint32_t)cnt * 4, &bar[slot]);
+            tma_bulk_g2s(dst + K2V_WCHUNK * 4, counts + c * K2V_WCHUNK * 4, (uint32_t)cnt * 4, &bar[slot]);
+            tma_bulk_g2s(dst + K2V_WCHUNK * 8, bm + c * K2V_WCHUNK, (uint32_t)cnt, &bar[slot]);
+        }
+    };
+    if (lane == 0) {
+        for (int s = 0; s < K2V_STAGES; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < K2V_STAGES; ++s) {
+            const long long c = wfirst + (long long)s * wstride;
+            if (c < nchunks) issue(c, s);
+        }
+    }
+    {   // infeasible-stage bits: bit j of word w <=> scode[32 w + j] == SC_INFEASIBLE
+        const unsigned nbytes = (unsigned)(I.F * N2), nwords = (nbytes + 31) / 32;
+        const bool al = (reinterpret_cast<uintptr_t>(I.scode) & 15u) == 0;
+        for (unsigned w = threadIdx.x; w < nwords; w += blockDim.x) {
+            uint32_t bits = 0;
+            if (al && 32 * w + 32 <= nbytes) {
+                const uint4* src = reinterpret_cast<const uint4*>(I.scode + 32 * w);
+                const uint4 v[2] = {__ldg(src), __ldg(src + 1)};
+                const uint32_t* b = reinterpret_cast<const uint32_t*>(v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        bits |= (uint32_t)(((b[j] >> (8 * t)) & 0xffu) == SC_INFEASIBLE) << (4 * j + t);
+            } else {
+                for (unsigned j = 0; j < 32 && 32 * w + j < nbytes; ++j)
+                    bits |= (uint32_t)(__ldg(&I.scode[32 * w + j]) == SC_INFEASIBLE) << j;
+            }
+            ibits[w] = bits;
+        }
+    }
+    __syncthreads();
+    const bool fast_tables = *I.flags == 0u;
+    const unsigned lt = (1u << lane) - 1u;
+    const int nbm = I.nb * I.nm;
+    auto infeasible = [&](int idx) -> uint32_t { return (ibits[idx >> 5] >> (idx & 31)) & 1u; };
+    auto eval_entry = [&](const uint4 e) {
+        uint8_t o[4];
+        int p[5];
+        const unsigned pw = e.z * 0x01010101u;  // byte-wise prefix sums of the counts
+        p[0] = 0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            o[s] = (uint8_t)(e.y >> (8 * s));
+            p[s + 1] = (int)((pw >> (8 * s)) & 0xffu);
+        }
+        const int b = (int)e.w;
+        cost[e.x] = eval_fast<4>(I, o, p, b % I.nm, __ldg(&I.mtab[b]));
+    };
+    int q = 0;  // warp-uniform queue length
+    auto push = [&](bool need, long long gi, uint32_t ow, uint32_t cw, int b) {
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (need) wq[q + __popc(m & lt)] = make_uint4((unsigned)gi, ow, cw, (unsigned)b);
+        q += __popc(m);
+    };
+    auto drain = [&]() {  // full batches of 32 (one eval site: small code)
+        __syncwarp();
+        while (q >= 32) {
+            const uint4 e = wq[q - 32 + lane];
+            __syncwarp();
+            q -= 32;
+            eval_entry(e);
+        }
+    };
+    // one candidate, branch-free: 0 = error, 1 = +inf, 2 = queue (feasible),
+    // 3 = status-tracking evaluation
+    auto classify = [&](uint32_t ow, uint32_t cw, int b) -> int {
+        const unsigned o0 = ow & 0xffu, o1 = (ow >> 8) & 0xffu, o2 = (ow >> 16) & 0xffu, o3 = ow >> 24;
+        const unsigned msk = (1u << (o0 & 31u)) | (1u << (o1 & 31u)) | (1u << (o2 & 31u)) | (1u << (o3 & 31u));
+        const int total = (int)__vsadu4(cw, 0u);
+        const bool ok = ((ow & 0xE0E0E0E0u) == 0u) & (__popc(msk) == 4) & ((msk >> I.F) == 0u) &
+                        ((((cw - 0x01010101u) & ~cw & 0x80808080u) == 0u)) & (b < nbm) & (total <= n);
+        const bool fast = ok & fast_tables & (total == n);
+        const unsigned pw = cw * 0x01010101u;  // p1..p4 (exact: sums <= n <= 255)
+        const int p1 = (int)(pw & 0xffu), p2 = (int)((pw >> 8) & 0xffu), p3 = (int)((pw >> 16) & 0xffu);
+        const int np = n + 1;
+        const uint32_t inf = fast ? (infeasible((int)o0 * N2 + p1) | infeasible((int)o1 * N2 + p1 * np + p2) |
+                                     infeasible((int)o2 * N2 + p2 * np + p3) |
+                                     infeasible((int)o3 * N2 + p3 * np + n))
+                                  : 0u;
+        return !ok ? 0 : (!fast ? 3 : (inf ? 1 : 2));
+    };
+    auto slow_eval = [&](long long gi, uint32_t ow, uint32_t cw, int b) {
+        uint8_t o[4];
+        int p[5];
+        p[0] = 0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            o[s] = (uint8_t)(ow >> (8 * s));
+            p[s + 1] = p[s] + (int)((cw >> (8 * s)) & 0xffu);
+        }
+        const int mi = b % I.nm;
+        EvalOut e = eval_tables(I, 4, o, p, mi, I.batch[b / I.nm] / I.micro[mi]);
+        cost[gi] = e.status == GP_OK ? e.cost : NAN;
+        status[gi] = (uint8_t)e.status;
+    };
+    int j = 0;
+    for (long long c = wfirst; c < nchunks; c += wstride, ++j) {
+        const int slot = j % K2V_STAGES;
+        mbar_wait(&bar[slot], (uint32_t)((j / K2V_STAGES) & 1));
+        const uint8_t* sl = ring + (size_t)slot * K2V_SLOT;
+        const long long c0 = c * K2V_WCHUNK;
+        const long long left = ncand - c0;
+        const int cnt = left < K2V_WCHUNK ? (int)left : K2V_WCHUNK;
+        if (cnt == K2V_WCHUNK) {
+#pragma unroll 1
+            for (int r = 0; r < K2V_WCHUNK / 128; ++r) {
+                const int i0 = 128 * r + 4 * lane;  // this lane's four candidates
+                const uint4 ow4 = *reinterpret_cast<const uint4*>(sl + 4 * i0);
+                const uint4 cw4 = *reinterpret_cast<const uint4*>(sl + K2V_WCHUNK * 4 + 4 * i0);
+                const uint32_t bw4 = *reinterpret_cast<const uint32_t*>(sl + K2V_WCHUNK * 8 + i0);
+                const uint32_t ow[4] = {ow4.x, ow4.y, ow4.z, ow4.w};
+                const uint32_t cw[4] = {cw4.x, cw4.y, cw4.z, cw4.w};
+                int cl[4];
+#pragma unroll
+                for (int s = 0; s < 4; ++s) cl[s] = classify(ow[s], cw[s], (int)((bw4 >> (8 * s)) & 0xffu));
+                double cv[4];
+                uint32_t sv = 0;
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    cv[s] = cl[s] == 0 ? NAN : (cl[s] == 1 ? INFINITY : 0.0);
+                    sv |= (uint32_t)(cl[s] == 0 ? GP_ERR_INPUT : GP_OK) << (8 * s);
+                }
+                double2* cd = reinterpret_cast<double2*>(cost + c0 + i0);
+                cd[0] = make_double2(cv[0], cv[1]);
+                cd[1] = make_double2(cv[2], cv[3]);
+                *reinterpret_cast<uint32_t*>(status + c0 + i0) = sv;
+                if ((cl[0] == 3) | (cl[1] == 3) | (cl[2] == 3) | (cl[3] == 3)) {
+#pragma unroll
+                    for (int s = 0; s < 4; ++s)
+                        if (cl[s] == 3) slow_eval(c0 + i0 + s, ow[s], cw[s], (int)((bw4 >> (8 * s)) & 0xffu));
+                }
+#pragma unroll
+                for (int s = 0; s < 4; ++s)
+                    push(cl[s] == 2, c0 + i0 + s, ow[s], cw[s], (int)((bw4 >> (8 * s)) & 0xffu));
+                drain();
+            }
+        } else {  // ragged last chunk: one candidate per lane per round
+            const int cnt16 = cnt & ~15;
+            for (int r = lane; r < ((cnt + 31) & ~31); r += 32) {
+                int cl = -1;
+                uint32_t ow = 0, cw = 0;
+                int b = 0;
+                if (r < cnt) {
+                    if (r < cnt16) {
+                        ow = reinterpret_cast<const uint32_t*>(sl)[r];
+                        cw = reinterpret_cast<const uint32_t*>(sl + K2V_WCHUNK * 4)[r];
+                        b = sl[K2V_WCHUNK * 8 + r];
+                    } else {
+                        ow = __ldg(reinterpret_cast<const uint32_t*>(order) + c0 + r);
+                        cw = __ldg(reinterpret_cast<const uint32_t*>(counts) + c0 + r);
+                        b = __ldg(&bm[c0 + r]);
+                    }
+                    cl = classify(ow, cw, b);
+                    if (cl == 3) {
+                        slow_eval(c0 + r, ow, cw, b);
+                    } else {
+                        cost[c0 + r] = cl == 0 ? NAN : (cl == 1 ? INFINITY : 0.0);
+                        status[c0 + r] = (uint8_t)(cl == 0 ? GP_ERR_INPUT : GP_OK);
+                    }
+                }
+                push(cl == 2, c0 + r, ow, cw, b);
+                drain();
+            }
+        }
+        __syncwarp();  // the warp is done with the slot
+        if (lane == 0) {
+            const long long cn = c + (long long)K2V_STAGES * wstride;
+            if (cn < nchunks) issue(cn, slot);
+        }
+    }
+    __syncwarp();
+    if (lane < q) eval_entry(wq[lane]);
+}
