@@ -125,6 +125,8 @@ struct gp_ctx {
     DBuf<double> s_ends;
     DBuf<uint32_t> s_wq;         // K5 full queue scratch
     DBuf<uint8_t> g_buf;         // K7 inputs, outputs and scratch
+    uint8_t* h_stage = nullptr;  // pinned host staging (K7: one H2D, one D2H per batch)
+    size_t h_stage_cap = 0;
     DBuf<unsigned long long> s_lq;
     SolveOut* h_solve = nullptr;  // pinned, mapped (the gp_replan graph's detail kernel writes it)
     SolveOut* d_hsolve = nullptr; // device alias of h_solve
@@ -315,6 +317,7 @@ void gp_ctx_destroy(gp_ctx* c) {
                            &c->b_bm, &c->b_status};
     for (auto* b : bb) b->release();
     c->arena.release();
+    if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h_arena) cudaFreeHost(c->h_arena);
     c->d_harena = nullptr;
     if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -2458,6 +2461,16 @@ int gp_diag_fp64_peak(int device, double* dadd_per_second) {
 // ----------------------------------------------------------------------------
 // K7: device grouping per topology snapshot
 // ----------------------------------------------------------------------------
+static int ensure_stage(gp_ctx* c, size_t bytes) {
+    if (bytes <= c->h_stage_cap && c->h_stage) return GP_OK;
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    c->h_stage = nullptr;
+    c->h_stage_cap = 0;
+    CUDA_TRY(cudaHostAlloc((void**)&c->h_stage, bytes, cudaHostAllocDefault));
+    c->h_stage_cap = bytes;
+    return GP_OK;
+}
+
 static int group_launch(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_t,
                         const double* bandwidth, const double* p_c, double threshold_net,
                         double threshold_compute, const uint16_t* fixed_fg, uint32_t fixed_nf,
@@ -2495,16 +2508,24 @@ static int group_launch(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_
     size_t smem = head;
     if (head + tabs + DD * 8 <= (200u << 10)) { smem_mode = 3; smem = head + tabs + DD * 8; }
     else if (head + tabs <= (200u << 10)) { smem_mode = 1; smem = head + tabs; }
-    { int ps_ = 0, st_ = kernel_slots(c, (const void*)k7_group, K7_THREADS, smem, &ps_);
+    typedef decltype(&k7_group<0>) K7Fn;
+    const K7Fn k7fn = smem_mode == 3 ? k7_group<3> : (smem_mode == 1 ? k7_group<1> : k7_group<0>);
+    { int ps_ = 0, st_ = kernel_slots(c, (const void*)k7fn, K7_THREADS, smem, &ps_);
       if (st_ != GP_OK) return st_; }
-    CUDA_TRY(cudaMemcpyAsync(b + o_pc, p_c, (size_t)D * 8, cudaMemcpyHostToDevice, s));
-    if (fixed_fg) CUDA_TRY(cudaMemcpyAsync(b + o_fix, fixed_fg, (size_t)D * 2, cudaMemcpyHostToDevice, s));
+    // inputs [o_pt, o_u16) and outputs [o_u16, o_fix) travel through one
+    // pinned staging buffer: one H2D and one D2H per batch
+    { int st_ = ensure_stage(c, o_scr); if (st_ != GP_OK) return st_; }
+    uint8_t* hs = c->h_stage;
+    memcpy(hs + o_pc, p_c, (size_t)D * 8);
+    if (fixed_fg) memcpy(hs + o_fix, fixed_fg, (size_t)D * 2);
+    CUDA_TRY(cudaMemcpyAsync(b + o_pc, hs + o_pc, o_u16 - o_pc, cudaMemcpyHostToDevice, s));
+    if (fixed_fg) CUDA_TRY(cudaMemcpyAsync(b + o_fix, hs + o_fix, (size_t)D * 2, cudaMemcpyHostToDevice, s));
     for (uint32_t s0 = 0; s0 < n_snap; s0 += SB) {
         const uint32_t nb = (n_snap - s0) < SB ? (n_snap - s0) : SB;
-        CUDA_TRY(cudaMemcpyAsync(b + o_pt, p_t + (size_t)s0 * DD, nb * DD * 8, cudaMemcpyHostToDevice, s));
-        if (bandwidth)
-            CUDA_TRY(cudaMemcpyAsync(b + o_bw, bandwidth + (size_t)s0 * DD, nb * DD * 8,
-                                     cudaMemcpyHostToDevice, s));
+        memcpy(hs + o_pt, p_t + (size_t)s0 * DD, nb * DD * 8);
+        if (bandwidth) memcpy(hs + o_bw, bandwidth + (size_t)s0 * DD, nb * DD * 8);
+        CUDA_TRY(cudaMemcpyAsync(b + o_pt, hs + o_pt, (bandwidth ? o_bw + nb * DD * 8 : nb * DD * 8),
+                                 cudaMemcpyHostToDevice, s));
         uint16_t* d_fg = reinterpret_cast<uint16_t*>(b + o_u16);
         uint16_t* d_sg = d_fg + (size_t)SB * D;
         uint32_t* d_nf = reinterpret_cast<uint32_t*>(b + o_cnt);
@@ -2515,7 +2536,7 @@ static int group_launch(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_
         uint32_t* d_nsf = reinterpret_cast<uint32_t*>(b + o_nsf);
         double* d_stg = reinterpret_cast<double*>(b + o_stg);
         auto launch = [&](unsigned grid, int phase) {
-            k7_group<<<grid, K7_THREADS, smem, s>>>(
+            k7fn<<<grid, K7_THREADS, smem, s>>>(
                 (int)D, reinterpret_cast<const double*>(b + o_pt),
                 bandwidth ? reinterpret_cast<const double*>(b + o_bw) : nullptr, (long long)DD,
                 (long long)DD, reinterpret_cast<const double*>(b + o_pc), threshold_net,
@@ -2540,15 +2561,17 @@ static int group_launch(gp_ctx* c, uint32_t D, uint32_t n_snap, const double* p_
         }
         CUDA_TRY(cudaGetLastError());
         const size_t o = (size_t)s0 * D;
-        CUDA_TRY(cudaMemcpyAsync(fg_of + o, d_fg, (size_t)nb * D * 2, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(sg_of + o, d_sg, (size_t)nb * D * 2, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(n_fg + s0, d_nf, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(n_sg + s0, d_ns, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(fg_intra + o, d_fi, (size_t)nb * D * 8, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(fg_capacity + o, d_fc, (size_t)nb * D * 8, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(fg_min_bw + o, d_fb, (size_t)nb * D * 8, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(sg_capacity + o, d_sc, (size_t)nb * D * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(hs + o_u16, b + o_u16, o_fix - o_u16, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));  // staging buffers are reused by the next batch
+        auto hp = [&](const void* dptr) { return hs + ((const uint8_t*)dptr - b); };
+        memcpy(fg_of + o, hp(d_fg), (size_t)nb * D * 2);
+        memcpy(sg_of + o, hp(d_sg), (size_t)nb * D * 2);
+        memcpy(n_fg + s0, hp(d_nf), (size_t)nb * 4);
+        memcpy(n_sg + s0, hp(d_ns), (size_t)nb * 4);
+        memcpy(fg_intra + o, hp(d_fi), (size_t)nb * D * 8);
+        memcpy(fg_capacity + o, hp(d_fc), (size_t)nb * D * 8);
+        memcpy(fg_min_bw + o, hp(d_fb), (size_t)nb * D * 8);
+        memcpy(sg_capacity + o, hp(d_sc), (size_t)nb * D * 8);
     }
     return GP_OK;
 }

@@ -158,6 +158,28 @@ __device__ __forceinline__ void k7_rescan_flagged(const K7Global& g, const K7Sha
 // (WARP: the calling warp alone, warp-synchronous)
 template <bool WARP>
 __device__ void k7_pop(const K7Shared& sh, int n, int* s_ab, double* s_red, int* s_ia) {
+    if (!WARP && n <= 128) {  // warp 0 alone (<= 4 rows per lane), one barrier
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            double bk = 0.0;
+            int ba = -1, bb = -1;
+            for (int a = lane; a < n; a += 32) {
+                const int b = sh.rowarg[a];
+                if (sh.cnt[a] == 0 || b < 0) continue;
+                const double k = sh.rowkey[a];
+                if (ba < 0 || k7_less(k, a, b, bk, ba, bb)) { bk = k; ba = a; bb = b; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double k2 = __shfl_down_sync(0xffffffffu, bk, o);
+                const int a2 = __shfl_down_sync(0xffffffffu, ba, o);
+                const int b2 = __shfl_down_sync(0xffffffffu, bb, o);
+                if (a2 >= 0 && (ba < 0 || k7_less(k2, a2, b2, bk, ba, bb))) { bk = k2; ba = a2; bb = b2; }
+            }
+            if (lane == 0) { s_ab[0] = ba; s_ab[1] = bb; }
+        }
+        __syncthreads();
+        return;
+    }
     const int tid = WARP ? (threadIdx.x & 31) : threadIdx.x, lane = threadIdx.x & 31,
               wid = threadIdx.x >> 5;
     const int nt = WARP ? 32 : blockDim.x;
@@ -267,23 +289,42 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
                 g.live[(size_t)a * n + b] = 0;  // discarded permanently
                 s_ab[2] = 0;
             } else {
-                // merged = tuple(sorted(a + b)) into slot a
-                const uint16_t* ma = g.mem + (size_t)a * n;
-                const uint16_t* mb = g.mem + (size_t)b * n;
-                const int na = sh.cnt[a], nb = sh.cnt[b];
-                int i = 0, j = 0, k = 0;
-                while (i < na || j < nb)
-                    g.tmp[k++] = (j >= nb || (i < na && ma[i] < mb[j])) ? ma[i++] : mb[j++];
-                uint16_t* md = g.mem + (size_t)a * n;
-                for (int q = 0; q < k; ++q) md[q] = g.tmp[q];
-                sh.cnt[a] = (int16_t)k;
-                sh.cnt[b] = 0;
-                g.live[(size_t)a * n + b] = 0;
-                sh.has[a] = 0;
                 s_ab[2] = 1;
             }
         }
         sync();
+        if (s_ab[2]) {
+            // merged = tuple(sorted(a + b)) into slot a: member lists are
+            // sorted and disjoint, so an element's place is its index plus
+            // the number of the other list's members below it (binary search)
+            const uint16_t* ma = g.mem + (size_t)a * n;
+            const uint16_t* mb = g.mem + (size_t)b * n;
+            const int na = sh.cnt[a], nb = sh.cnt[b];
+            uint16_t v = 0;
+            int pos = -1;
+            for (int t = tid; t < na + nb; t += nt) {  // na + nb <= n <= nt in practice
+                const bool in_a = t < na;
+                v = in_a ? ma[t] : mb[t - na];
+                const uint16_t* other = in_a ? mb : ma;
+                int lo = 0, hi = in_a ? nb : na;  // first index with other[idx] > v
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (other[mid] < v) lo = mid + 1; else hi = mid;
+                }
+                pos = (in_a ? t : t - na) + lo;
+                g.tmp[pos] = v;
+            }
+            sync();
+            for (int t = tid; t < na + nb; t += nt) g.mem[(size_t)a * n + t] = g.tmp[t];
+            if (tid == 0) {
+                sh.cnt[a] = (int16_t)(na + nb);
+                sh.cnt[b] = 0;
+                g.live[(size_t)a * n + b] = 0;
+                sh.has[a] = 0;
+            }
+            sync();
+            (void)pos;
+        }
 #if defined(K7_PROFILE)
         c1 = clock64(); c_pred += c1 - c0; c0 = c1;
 #endif
@@ -361,6 +402,10 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
 
 // One CTA per snapshot.  Outputs (stride D per snapshot): fg_of, sg_of,
 // fg_intra / fg_cap / fg_minbw per FG, sg_cap per SG (FG-major); n_fg, n_sg.
+// SM = smem_mode as a template parameter, so that with the tables in shared
+// memory every table access compiles to a shared-memory load (LDS) rather
+// than a generic one
+template <int SM>
 __global__ void __launch_bounds__(K7_THREADS)
 k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw_all,
          long long pt_stride, long long bw_stride, const double* __restrict__ pc, double thr_net,
@@ -384,9 +429,9 @@ k7_group(int D, const double* __restrict__ pt_all, const double* __restrict__ bw
     const double* pt = pt_all + (size_t)snap * pt_stride;
     const double* bw = bw_all ? bw_all + (size_t)snap * bw_stride : nullptr;
     // smem_mode bit0: pair tables in shared memory (small D); bit1: p_t too
-    uint8_t* base = (smem_mode & 1) ? k7_smem + k7_smem_head(D)
-                                    : scratch + (size_t)snap * scratch_per;
-    if (smem_mode & 2) {
+    (void)smem_mode;
+    uint8_t* base = (SM & 1) ? k7_smem + k7_smem_head(D) : scratch + (size_t)snap * scratch_per;
+    if constexpr ((SM & 2) != 0) {
         double* pts = reinterpret_cast<double*>(base + k7_scratch_bytes(D));
         for (int e = tid; e < D * D; e += blockDim.x) pts[e] = pt[e];
         pt = pts;  // visible after the first __syncthreads below
