@@ -323,11 +323,13 @@ def extra_sections(eng, packed, total, local, args, world):
                      "achieved_gbs": N * bytes_per / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
                      "frac": N * bytes_per / (ms * 1e-3) / 1e9 / hbm},
         "note": "360 MB of candidates + results per launch (> 126 MB L2); order/counts/bm u8 "
-                "in, cost f64 + status u8 out. k2_eval_batch_q4: stage codes in shared memory "
-                "decide the 85 % memory-infeasible candidates without table gathers; the "
-                "feasible ones are queued per warp and evaluated 32 at a time (stage-table and "
-                "boundary gathers from L2). ncu (profiles/r1e_k2_eval_batch_q4_ncu_raw.csv): "
-                "ALU pipe 57 %, long-scoreboard stalls dominant, DRAM 1.8 TB/s"}
+                "in, cost f64 + status u8 out. k2_eval_batch_v4<16, true>: per-warp TMA rings "
+                "of input chunks, four consecutive candidates per lane classified branch-free "
+                "against infeasible-stage bit rows in shared memory (85 % are +inf without "
+                "table reads), feasible ones queued and evaluated 32 at a time with the first- "
+                "and last-stage and boundary tables in shared memory (two L2 gathers per "
+                "candidate), vector stores. Diagnostic builds: streaming alone 78 us, "
+                "classification 104 us per 2e7 (profiles/README.md)"}
 
     # ---- K5: 1F1B makespans of 10^5 of those C4 candidates
     # feasible candidates only (infeasible ones are rejected before simulating)

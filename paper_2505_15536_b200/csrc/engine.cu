@@ -714,19 +714,29 @@ int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_ord
         // vector-lane variant: 32-byte aligned costs, 4-byte aligned status
         // (GP_K2_V4=0 disables)
         bool v4 = t4 && ((((uintptr_t)d_cost) & 31u) == 0) && ((((uintptr_t)d_status) & 3u) == 0) &&
-                  k2v_smem(sc_bytes) <= (size_t)c->smem_max;
+                  c->n + 1 <= 128 && k2v_smem(c->F, c->n, c->nm, I.nxp, 8, false) <= (size_t)c->smem_max;
         if (const char* e = getenv("GP_K2_V4")) v4 = v4 && atoi(e) != 0;
         if (v4) {
-            const size_t smem_v = k2v_smem(sc_bytes);
+            // 16 warps with the first/last-stage and boundary tables in shared
+            // memory when they fit (GP_K2_SMT=0 disables), else 8 warps
+            bool smt = k2v_smem(c->F, c->n, c->nm, I.nxp, 16, true) <= (size_t)c->smem_max;
+            if (const char* e = getenv("GP_K2_SMT")) smt = smt && atoi(e) != 0;
+            const int nw = smt ? 16 : 8;
+            const void* kfn = smt ? (const void*)k2_eval_batch_v4<16, true> : (const void*)k2_eval_batch_v4<8, false>;
+            const size_t smem_v = k2v_smem(c->F, c->n, c->nm, I.nxp, nw, smt);
             int per_sm = 0;
-            { int st_ = kernel_slots(c, (const void*)k2_eval_batch_v4, K2V_THREADS, smem_v, &per_sm);
+            { int st_ = kernel_slots(c, kfn, nw * 32, smem_v, &per_sm);
               if (st_ != GP_OK) return st_; }
             unsigned long long grid = (unsigned long long)(per_sm > 0 ? per_sm : 1) * c->n_sms;
-            const unsigned long long chunks = (n + (unsigned long long)K2V_WCHUNK * K2V_WARPS - 1) /
-                                              ((unsigned long long)K2V_WCHUNK * K2V_WARPS);
+            const unsigned long long chunks = (n + (unsigned long long)K2V_WCHUNK * nw - 1) /
+                                              ((unsigned long long)K2V_WCHUNK * nw);
             if (grid > chunks) grid = chunks;
-            k2_eval_batch_v4<<<(unsigned)grid, K2V_THREADS, smem_v, c->stream>>>(
-                I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status, (unsigned)sc_bytes);
+            if (smt)
+                k2_eval_batch_v4<16, true><<<(unsigned)grid, 512, smem_v, c->stream>>>(
+                    I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status);
+            else
+                k2_eval_batch_v4<8, false><<<(unsigned)grid, 256, smem_v, c->stream>>>(
+                    I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status);
             CUDA_TRY(cudaGetLastError());
             return GP_OK;
         }

@@ -569,42 +569,56 @@ static __global__ void __launch_bounds__(K2T_THREADS, K2T_MINB) k2_eval_batch_t4
 #define K2V_WCHUNK 256
 #endif
 #ifndef K2V_STAGES
-#define K2V_STAGES 2
+#define K2V_STAGES 3
 #endif
 #define K2V_QCAP 160  // queue entries per warp: < 32 left + 128 of one round
 #define K2V_THREADS 256
 #ifndef K2V_MINB
-#define K2V_MINB 3
+#define K2V_MINB 2
 #endif
 #define K2V_WARPS (K2V_THREADS / 32)
 #define K2V_SLOT (K2V_WCHUNK * 9)  // order u32 | counts u32 | bm u8 per candidate
 
-__host__ __device__ inline size_t k2v_bits_bytes(size_t sc_bytes) { return ((sc_bytes + 31) / 32 * 4 + 15) & ~(size_t)15; }
-__host__ __device__ inline size_t k2v_smem(size_t sc_bytes) {
-    return (((size_t)K2V_WARPS * K2V_STAGES * 8 + 63) & ~(size_t)63) + k2v_bits_bytes(sc_bytes) +
-           (size_t)K2V_WARPS * K2V_STAGES * K2V_SLOT + (size_t)K2V_WARPS * K2V_QCAP * 16;
+// infeasible-stage bit rows: row (f, a) = 4 words, bit b <=> stage [a, b) of
+// group f is memory-infeasible (n + 1 <= 128)
+__host__ __device__ inline size_t k2v_bits_bytes(int F, int n) { return (size_t)F * (n + 1) * 16; }
+// SMT: the first-stage rows [0, b), last-stage columns [a, n) and boundary
+// rows of every (micro-batch, group) in shared memory, so a feasible
+// candidate gathers only its two middle stage entries from L2
+__host__ __device__ inline size_t k2v_tab_bytes(int F, int n, int nm, int nxp) {
+    return (size_t)nm * F * (n + 1) * 16 * 2 + (((size_t)nm * F * F * nxp * 8 + 15) & ~(size_t)15);
+}
+__host__ __device__ inline size_t k2v_smem(int F, int n, int nm, int nxp, int nwarps, bool smt) {
+    return (((size_t)nwarps * K2V_STAGES * 8 + 63) & ~(size_t)63) + k2v_bits_bytes(F, n) +
+           (smt ? k2v_tab_bytes(F, n, nm, nxp) : 0) + (size_t)nwarps * K2V_STAGES * K2V_SLOT +
+           (size_t)nwarps * K2V_QCAP * 16;
 }
 
-static __global__ void __launch_bounds__(K2V_THREADS, K2V_MINB) k2_eval_batch_v4(DevInst I, long long ncand,
+template <int NW, bool SMT>
+static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_eval_batch_v4(DevInst I, long long ncand,
                                                               const uint8_t* __restrict__ order,
                                                               const uint8_t* __restrict__ counts,
                                                               const uint8_t* __restrict__ bm,
                                                               double* __restrict__ cost,
-                                                              uint8_t* __restrict__ status,
-                                                              unsigned sc_bytes) {
+                                                              uint8_t* __restrict__ status) {
     extern __shared__ __align__(16) uint8_t v4_s[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t bar_bytes = ((size_t)K2V_WARPS * K2V_STAGES * 8 + 63) & ~(size_t)63;
+    const int n = I.n, np = n + 1, F = I.F;
+    const int nm = I.nm, nxp = I.nxp;
+    const size_t bar_bytes = ((size_t)NW * K2V_STAGES * 8 + 63) & ~(size_t)63;
+    const size_t bits_bytes = k2v_bits_bytes(F, n) + (SMT ? k2v_tab_bytes(F, n, nm, nxp) : 0);
     uint64_t* bar = reinterpret_cast<uint64_t*>(v4_s) + warp * K2V_STAGES;
     uint32_t* ibits = reinterpret_cast<uint32_t*>(v4_s + bar_bytes);
-    uint8_t* ring = v4_s + bar_bytes + k2v_bits_bytes(sc_bytes) + (size_t)warp * K2V_STAGES * K2V_SLOT;
-    uint4* wq = reinterpret_cast<uint4*>(v4_s + bar_bytes + k2v_bits_bytes(sc_bytes) +
-                                         (size_t)K2V_WARPS * K2V_STAGES * K2V_SLOT) + warp * K2V_QCAP;
-    const int n = I.n;
-    const int N2 = (n + 1) * (n + 1);
+    double2* t0s = reinterpret_cast<double2*>(v4_s + bar_bytes + k2v_bits_bytes(F, n));  // [nm][F][np]
+    double2* t3s = t0s + (size_t)nm * F * np;                                              // [nm][F][np]
+    double* xs = reinterpret_cast<double*>(t3s + (size_t)nm * F * np);                   // [nm][F][F][nxp]
+    uint8_t* ring = v4_s + bar_bytes + bits_bytes + (size_t)warp * K2V_STAGES * K2V_SLOT;
+    uint4* wq = reinterpret_cast<uint4*>(v4_s + bar_bytes + bits_bytes +
+                                         (size_t)NW * K2V_STAGES * K2V_SLOT) + warp * K2V_QCAP;
+    const int N2 = np * np;
     const long long nchunks = (ncand + K2V_WCHUNK - 1) / K2V_WCHUNK;
-    const long long wstride = (long long)gridDim.x * K2V_WARPS;
-    const long long wfirst = (long long)blockIdx.x * K2V_WARPS + warp;
+    const long long wstride = (long long)gridDim.x * NW;
+    const long long wfirst = (long long)blockIdx.x * NW + warp;
     auto issue = [&](long long c, int slot) {  // lane 0
         const long long left = ncand - c * K2V_WCHUNK;
         const int cnt = (left < K2V_WCHUNK ? (int)left : K2V_WCHUNK) & ~15;  // ragged tail: direct loads
@@ -623,44 +637,97 @@ static __global__ void __launch_bounds__(K2V_THREADS, K2V_MINB) k2_eval_batch_v4
             if (c < nchunks) issue(c, s);
         }
     }
-    {   // infeasible-stage bits: bit j of word w <=> scode[32 w + j] == SC_INFEASIBLE
-        const unsigned nbytes = (unsigned)(I.F * N2), nwords = (nbytes + 31) / 32;
-        const bool al = (reinterpret_cast<uintptr_t>(I.scode) & 15u) == 0;
-        for (unsigned w = threadIdx.x; w < nwords; w += blockDim.x) {
-            uint32_t bits = 0;
-            if (al && 32 * w + 32 <= nbytes) {
-                const uint4* src = reinterpret_cast<const uint4*>(I.scode + 32 * w);
-                const uint4 v[2] = {__ldg(src), __ldg(src + 1)};
-                const uint32_t* b = reinterpret_cast<const uint32_t*>(v);
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        bits |= (uint32_t)(((b[j] >> (8 * t)) & 0xffu) == SC_INFEASIBLE) << (4 * j + t);
-            } else {
-                for (unsigned j = 0; j < 32 && 32 * w + j < nbytes; ++j)
-                    bits |= (uint32_t)(__ldg(&I.scode[32 * w + j]) == SC_INFEASIBLE) << j;
-            }
-            ibits[w] = bits;
+    // bit rows from the stage codes (word w of row r: b = 32 w .. 32 w + 31)
+    for (int rw = threadIdx.x; rw < F * np * 4; rw += blockDim.x) {
+        const int r = rw >> 2, w = rw & 3;  // r = f * np + a
+        const uint8_t* src = I.scode + (size_t)(r / np) * N2 + (size_t)(r % np) * np;
+        uint32_t bits = 0;
+        for (int j = 0; j < 32; ++j) {
+            const int b = 32 * w + j;
+            if (b <= n) bits |= (uint32_t)(__ldg(&src[b]) == SC_INFEASIBLE) << j;
         }
+        ibits[rw] = bits;
+    }
+    if constexpr (SMT) {
+        for (int e = threadIdx.x; e < nm * F * np; e += blockDim.x) {
+            const int a = e % np, mf = e / np;  // (mi, f) = mf
+            const double2* T = I.stg + (size_t)mf * N2;
+            t0s[e] = __ldg(&T[a]);                            // stage [0, a)
+            t3s[e] = __ldg(&T[(size_t)a * np + n]);           // stage [a, n)
+        }
+        for (int e = threadIdx.x; e < nm * F * F * nxp; e += blockDim.x) xs[e] = __ldg(&I.xt[e]);
     }
     __syncthreads();
     const bool fast_tables = *I.flags == 0u;
     const unsigned lt = (1u << lane) - 1u;
     const int nbm = I.nb * I.nm;
-    auto infeasible = [&](int idx) -> uint32_t { return (ibits[idx >> 5] >> (idx & 31)) & 1u; };
-    auto eval_entry = [&](const uint4 e) {
-        uint8_t o[4];
-        int p[5];
+    const unsigned fmask = F >= 32 ? 0xffffffffu : ((1u << F) - 1u);
+    // bit b of row (f, a)
+    auto inf_bit = [&](unsigned f, unsigned a, unsigned b) -> unsigned {
+        const uint32_t w = ibits[((f * (unsigned)np + a) << 2) + (b >> 5)];
+        return __funnelshift_r(w, 0u, b) & 1u;
+    };
+    // feasible candidates, 32 at a time, software-pipelined: a batch's table
+    // entries (k stage entries, k-1 boundary values, M) are loaded when it
+    // leaves the queue and its cost formed when the next batch leaves (or at
+    // the end), so the L2 round trip overlaps the next round's classification
+    bool pend = false;
+    unsigned pidx = 0;
+    double2 pe[4];
+    double px[3], pM = 0.0;
+    auto load_entry = [&](const uint4 e) {
         const unsigned pw = e.z * 0x01010101u;  // byte-wise prefix sums of the counts
+        int p[5];
         p[0] = 0;
 #pragma unroll
+        for (int s = 0; s < 4; ++s) p[s + 1] = (int)((pw >> (8 * s)) & 0xffu);
+        const int b = (int)e.w, mi = b % I.nm;
+        const double2* T = I.stg + (size_t)mi * F * N2;
+        const double* X = I.xt + (size_t)mi * F * F * I.nxp;
+#if !defined(K2V_NOLOAD)
+#pragma unroll
         for (int s = 0; s < 4; ++s) {
-            o[s] = (uint8_t)(e.y >> (8 * s));
-            p[s + 1] = (int)((pw >> (8 * s)) & 0xffu);
+            const unsigned os = (e.y >> (8 * s)) & 0xffu;
+            if (SMT && s == 0) pe[s] = t0s[((size_t)mi * F + os) * np + p[1]];
+            else if (SMT && s == 3) pe[s] = t3s[((size_t)mi * F + os) * np + p[3]];
+            else pe[s] = __ldg(&T[(size_t)os * N2 + tri_idx(n, p[s], p[s + 1])]);
+            if (s < 3) {
+                const unsigned on = (e.y >> (8 * (s + 1))) & 0xffu;
+                px[s] = SMT ? xs[(((size_t)mi * F + os) * F + on) * nxp + (p[s + 1] - 1)]
+                            : __ldg(&X[((size_t)os * F + on) * I.nxp + (p[s + 1] - 1)]);
+            }
         }
-        const int b = (int)e.w;
-        cost[e.x] = eval_fast<4>(I, o, p, b % I.nm, __ldg(&I.mtab[b]));
+#else
+        (void)T; (void)X;
+#endif
+        pM = __ldg(&I.mtab[b]);
+#if defined(K2V_NOLOAD)  // diagnostic build: no table gathers
+        pe[0] = pe[1] = pe[2] = pe[3] = make_double2(pM, pM);
+        px[0] = px[1] = px[2] = pM;
+#endif
+        pidx = e.x;
+        pend = true;
+    };
+    auto finish_entry = [&]() {  // eval_fast's arithmetic on the loaded entries
+        if (!pend) return;
+        double fill = 0.0, res = 0.0, best = 0.0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            if (s > 0) res = res + max0f(px[s - 1] - pe[s].x);
+            const double total = ((fill + pM * pe[s].x) + res) + pe[s].y;
+            best = (s == 0 || total > best) ? total : best;
+            if (s + 1 < 4) fill = fill + (pe[s].x + px[s]);
+        }
+#if defined(K2V_NOSTORE)  // diagnostic build: evaluate, store only an impossible value
+        if (best == -1.0) cost[pidx] = best;
+#else
+        cost[pidx] = best;
+#endif
+        pend = false;
+    };
+    auto eval_entry = [&](const uint4 e) {
+        finish_entry();
+        load_entry(e);
     };
     int q = 0;  // warp-uniform queue length
     auto push = [&](bool need, long long gi, uint32_t ow, uint32_t cw, int b) {
@@ -674,25 +741,34 @@ static __global__ void __launch_bounds__(K2V_THREADS, K2V_MINB) k2_eval_batch_v4
             const uint4 e = wq[q - 32 + lane];
             __syncwarp();
             q -= 32;
+#if !defined(K2V_NOEVAL)  // diagnostic build: queue without evaluation
             eval_entry(e);
+#else
+            (void)e;
+#endif
         }
     };
-    // one candidate, branch-free: 0 = error, 1 = +inf, 2 = queue (feasible),
-    // 3 = status-tracking evaluation
-    auto classify = [&](uint32_t ow, uint32_t cw, int b) -> int {
-        const unsigned o0 = ow & 0xffu, o1 = (ow >> 8) & 0xffu, o2 = (ow >> 16) & 0xffu, o3 = ow >> 24;
+    // one candidate: 0 = error, 1 = +inf, 2 = queue (feasible), 3 =
+    // status-tracking evaluation.  Packed-word checks: groups < F and
+    // distinct (a 4-member bit set), no zero count, sum of counts <= n, (b, m)
+    // index in range; the cut positions are the byte-wise prefix sums.
+    auto classify = [&](uint32_t ow, uint32_t cw, unsigned b) -> int {
+        const unsigned o0 = ow & 0xffu, o1 = __byte_perm(ow, 0u, 0x4441), o2 = __byte_perm(ow, 0u, 0x4442),
+                       o3 = ow >> 24;
         const unsigned msk = (1u << (o0 & 31u)) | (1u << (o1 & 31u)) | (1u << (o2 & 31u)) | (1u << (o3 & 31u));
-        const int total = (int)__vsadu4(cw, 0u);
-        const bool ok = ((ow & 0xE0E0E0E0u) == 0u) & (__popc(msk) == 4) & ((msk >> I.F) == 0u) &
-                        ((((cw - 0x01010101u) & ~cw & 0x80808080u) == 0u)) & (b < nbm) & (total <= n);
-        const bool fast = ok & fast_tables & (total == n);
-        const unsigned pw = cw * 0x01010101u;  // p1..p4 (exact: sums <= n <= 255)
-        const int p1 = (int)(pw & 0xffu), p2 = (int)((pw >> 8) & 0xffu), p3 = (int)((pw >> 16) & 0xffu);
-        const int np = n + 1;
-        const uint32_t inf = fast ? (infeasible((int)o0 * N2 + p1) | infeasible((int)o1 * N2 + p1 * np + p2) |
-                                     infeasible((int)o2 * N2 + p2 * np + p3) |
-                                     infeasible((int)o3 * N2 + p3 * np + n))
+        const unsigned total = __vsadu4(cw, 0u);
+        const bool ok = ((ow & 0xE0E0E0E0u) == 0u) & (__popc(msk) == 4) & ((msk & ~fmask) == 0u) &
+                        ((((cw - 0x01010101u) & ~cw & 0x80808080u) == 0u)) & (b < (unsigned)nbm) &
+                        (total <= (unsigned)n);
+        const bool fast = ok & fast_tables & (total == (unsigned)n);
+        const unsigned pw = cw * 0x01010101u;  // p1..p3 (exact: sums <= n <= 127)
+        const unsigned p1 = pw & 0xffu, p2 = __byte_perm(pw, 0u, 0x4441), p3 = __byte_perm(pw, 0u, 0x4442);
+        const unsigned inf = fast ? (inf_bit(o0, 0u, p1) | inf_bit(o1, p1, p2) | inf_bit(o2, p2, p3) |
+                                     inf_bit(o3, p3, (unsigned)n))
                                   : 0u;
+#if defined(K2V_STREAM)  // diagnostic build: inputs in, outputs out, no classification
+        return ((ow ^ cw ^ b) & 1u) ? 1 : 1;
+#endif
         return !ok ? 0 : (!fast ? 3 : (inf ? 1 : 2));
     };
     auto slow_eval = [&](long long gi, uint32_t ow, uint32_t cw, int b) {
@@ -726,9 +802,11 @@ static __global__ void __launch_bounds__(K2V_THREADS, K2V_MINB) k2_eval_batch_v4
                 const uint32_t bw4 = *reinterpret_cast<const uint32_t*>(sl + K2V_WCHUNK * 8 + i0);
                 const uint32_t ow[4] = {ow4.x, ow4.y, ow4.z, ow4.w};
                 const uint32_t cw[4] = {cw4.x, cw4.y, cw4.z, cw4.w};
+                const unsigned bb[4] = {bw4 & 0xffu, __byte_perm(bw4, 0u, 0x4441), __byte_perm(bw4, 0u, 0x4442),
+                                        bw4 >> 24};
                 int cl[4];
 #pragma unroll
-                for (int s = 0; s < 4; ++s) cl[s] = classify(ow[s], cw[s], (int)((bw4 >> (8 * s)) & 0xffu));
+                for (int s = 0; s < 4; ++s) cl[s] = classify(ow[s], cw[s], bb[s]);
                 double cv[4];
                 uint32_t sv = 0;
 #pragma unroll
@@ -743,11 +821,10 @@ static __global__ void __launch_bounds__(K2V_THREADS, K2V_MINB) k2_eval_batch_v4
                 if ((cl[0] == 3) | (cl[1] == 3) | (cl[2] == 3) | (cl[3] == 3)) {
 #pragma unroll
                     for (int s = 0; s < 4; ++s)
-                        if (cl[s] == 3) slow_eval(c0 + i0 + s, ow[s], cw[s], (int)((bw4 >> (8 * s)) & 0xffu));
+                        if (cl[s] == 3) slow_eval(c0 + i0 + s, ow[s], cw[s], (int)bb[s]);
                 }
 #pragma unroll
-                for (int s = 0; s < 4; ++s)
-                    push(cl[s] == 2, c0 + i0 + s, ow[s], cw[s], (int)((bw4 >> (8 * s)) & 0xffu));
+                for (int s = 0; s < 4; ++s) push(cl[s] == 2, c0 + i0 + s, ow[s], cw[s], (int)bb[s]);
                 drain();
             }
         } else {  // ragged last chunk: one candidate per lane per round
@@ -766,7 +843,7 @@ static __global__ void __launch_bounds__(K2V_THREADS, K2V_MINB) k2_eval_batch_v4
                         cw = __ldg(reinterpret_cast<const uint32_t*>(counts) + c0 + r);
                         b = __ldg(&bm[c0 + r]);
                     }
-                    cl = classify(ow, cw, b);
+                    cl = classify(ow, cw, (unsigned)b);
                     if (cl == 3) {
                         slow_eval(c0 + r, ow, cw, b);
                     } else {
@@ -785,5 +862,9 @@ static __global__ void __launch_bounds__(K2V_THREADS, K2V_MINB) k2_eval_batch_v4
         }
     }
     __syncwarp();
-    if (lane < q) eval_entry(wq[lane]);
+    finish_entry();
+    if (lane < q) {
+        load_entry(wq[lane]);
+        finish_entry();
+    }
 }
