@@ -196,6 +196,8 @@ struct gp_ctx {
     unsigned int rec_W = 0;
     bool rec_ok = false;
     DBuf<uint32_t> recrow;    // record sweep padded row starts
+    DBuf<uint32_t> k5_perm;   // K5: candidates grouped by (b, m) index
+    DBuf<uint32_t> k5_hist;
 
     DevInst view() {
         DevInst I;
@@ -332,7 +334,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     for (cudaEvent_t e : c->kt_ev) cudaEventDestroy(e);
-    c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release(); c->recruns.release(); c->recrow.release();
+    c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release(); c->recruns.release(); c->recrow.release(); c->k5_perm.release(); c->k5_hist.release();
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
     c->counter.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
@@ -2223,10 +2225,27 @@ int gp_sim_candidates(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* order,
     CUDA_TRY(cudaMemcpyAsync(c->b_bm.p, bm, n, cudaMemcpyHostToDevice, s));
     DevInst I = c->view();
     const int tpb = item_tpb(c, n);
+    // group the candidates by (b, m) index (equal micro-batch counts per
+    // warp; GP_K5_SORT=0 disables)
+    uint32_t* perm = nullptr;
+    static const int sort_on = [] { const char* e = getenv("GP_K5_SORT"); return e ? atoi(e) : 1; }();
+    const int nbm = c->nb * c->nm;
+    if (sort_on && n >= 1024 && n < (1ull << 32) && nbm <= 256) {
+        CUDA_TRY(c->k5_perm.ensure(n));
+        CUDA_TRY(c->k5_hist.ensure(260));
+        CUDA_TRY(cudaMemsetAsync(c->k5_hist.p, 0, 260 * sizeof(uint32_t), s));
+        unsigned hb = (unsigned)((n + 255) / 256);
+        if (hb > 2u * (unsigned)c->n_sms) hb = 2u * (unsigned)c->n_sms;
+        k5_bm_hist<<<hb, 256, 0, s>>>((long long)n, c->b_bm.p, nbm, c->k5_hist.p);
+        k5_bm_scan<<<1, 1, 0, s>>>(nbm, c->k5_hist.p);
+        k5_bm_scatter<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((long long)n, c->b_bm.p, nbm, c->k5_hist.p,
+                                                                 c->k5_perm.p);
+        perm = c->k5_perm.p;
+    }
     k5_sim_candidates<<<(unsigned)((n + tpb - 1) / tpb), tpb, 0, s>>>(I, (int)k, (long long)n, c->b_order.p,
                                                                  c->b_counts.p, c->b_bm.p,
                                                                  (int)iterations, opt_seconds,
-                                                                 c->b_cost.p, c->b_status.p);
+                                                                 c->b_cost.p, c->b_status.p, perm);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(makespan, c->b_cost.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->b_status.p, n, cudaMemcpyDeviceToHost, s));

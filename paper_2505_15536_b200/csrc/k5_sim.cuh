@@ -450,13 +450,43 @@ __device__ int cand_timing(const DevInst& I, int k, const uint8_t* __restrict__ 
     return GP_OK;
 }
 
-// 1F1B makespan of explicit candidates.
+// Candidates grouped by their (b, m) index before simulating: the event
+// count of a 1F1B run grows with the micro-batch count M = b / m, so a warp
+// of equal-M candidates walks its event loops in lock step (counting sort:
+// histogram, exclusive scan, scatter of candidate indices).
+__global__ void k5_bm_hist(long long n, const uint8_t* __restrict__ bm, int nbm, uint32_t* hist) {
+    __shared__ uint32_t h[257];
+    for (int j = threadIdx.x; j <= nbm; j += blockDim.x) h[j] = 0;
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int b = bm[i] < nbm ? bm[i] : nbm;
+        atomicAdd(&h[b], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j <= nbm; j += blockDim.x)
+        if (h[j]) atomicAdd(&hist[j], h[j]);
+}
+__global__ void k5_bm_scan(int nbm, uint32_t* hist) {  // one thread: <= 257 buckets
+    uint32_t acc = 0;
+    for (int j = 0; j <= nbm; ++j) { const uint32_t v = hist[j]; hist[j] = acc; acc += v; }
+}
+__global__ void k5_bm_scatter(long long n, const uint8_t* __restrict__ bm, int nbm, uint32_t* offs,
+                              uint32_t* __restrict__ perm) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int b = bm[i] < nbm ? bm[i] : nbm;
+    perm[atomicAdd(&offs[b], 1u)] = (uint32_t)i;
+}
+
+// 1F1B makespan of explicit candidates (thread t simulates candidate
+// perm[t], or t without a permutation).
 __global__ void k5_sim_candidates(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
                                   const uint8_t* __restrict__ counts, const uint8_t* __restrict__ bm,
                                   int iterations, double opt_seconds, double* __restrict__ makespan,
-                                  uint8_t* __restrict__ status) {
+                                  uint8_t* __restrict__ status, const uint32_t* __restrict__ perm) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= ncand) return;
+    if (perm) i = perm[i];
     gp_timing T;
     int st = cand_timing(I, k, order + i * k, counts + i * k, bm[i], opt_seconds, false, T);
     if (st != GP_OK) { makespan[i] = NAN; status[i] = (uint8_t)st; return; }
