@@ -1699,6 +1699,26 @@ int gp_sim_1f1b_device(gp_ctx* c, const gp_timing* d_timings, uint64_t n, uint32
     return GP_OK;
 }
 
+// Timings grouped by (stage count, micro-batch count): a permutation in
+// c->k5_perm (nullptr when not worth it; GP_K5_SORT=0 disables)
+static int k5_sort_timings(gp_ctx* c, const gp_timing* d_T, uint64_t n, uint32_t** perm) {
+    static const int sort_on = [] { const char* e = getenv("GP_K5_SORT"); return e ? atoi(e) : 1; }();
+    *perm = nullptr;
+    if (!sort_on || n < 1024 || n >= (1ull << 32)) return GP_OK;
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->k5_perm.ensure(n));
+    CUDA_TRY(c->k5_hist.ensure(K5_NKEYS));
+    CUDA_TRY(cudaMemsetAsync(c->k5_hist.p, 0, K5_NKEYS * sizeof(uint32_t), s));
+    unsigned hb = (unsigned)((n + 255) / 256);
+    if (hb > 2u * (unsigned)c->n_sms) hb = 2u * (unsigned)c->n_sms;
+    k5_key_hist<<<hb, 256, 0, s>>>((long long)n, d_T, c->k5_hist.p);
+    k5_key_scan<<<1, 256, 0, s>>>(c->k5_hist.p);
+    k5_key_scatter<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((long long)n, d_T, c->k5_hist.p, c->k5_perm.p);
+    CUDA_TRY(cudaGetLastError());
+    *perm = c->k5_perm.p;
+    return GP_OK;
+}
+
 // Validation shared by the trace-taking simulators.
 static int check_traces(const gp_trace* traces, uint32_t n_traces, const uint32_t* trace_index,
                         uint64_t n) {
@@ -1742,9 +1762,11 @@ int gp_simulate(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t policy
         }
     }
     const int tpb = item_tpb(c, n);
+    uint32_t* perm = nullptr;
+    { int st_ = k5_sort_timings(c, c->s_tim.p, n, &perm); if (st_ != GP_OK) return st_; }
     k5_sim_1f1b<<<(unsigned)((n + tpb - 1) / tpb), tpb, 0, s>>>(c->s_tim.p, (long long)n, (int)policy,
                                                            (int)iterations, d_tr, d_ti, c->s_ms.p,
-                                                           c->s_st.p);
+                                                           c->s_st.p, perm);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(makespan, c->s_ms.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status, c->s_st.p, n, cudaMemcpyDeviceToHost, s));
@@ -1843,13 +1865,21 @@ int gp_simulate_report(gp_ctx* c, const gp_timing* timings, uint64_t n, uint32_t
         CUDA_TRY(c->s_ends.ensure(n * (uint64_t)iterations));
         CUDA_TRY(cudaMemsetAsync(c->s_ends.p, 0, n * (uint64_t)iterations * sizeof(double), s));
     }
+    uint32_t* perm = nullptr;
+    { int st_ = k5_sort_timings(c, c->s_tim.p, n, &perm); if (st_ != GP_OK) return st_; }
     for (uint64_t i0 = 0; i0 < n; i0 += P.chunk) {
         const uint64_t nc = (n - i0) < P.chunk ? (n - i0) : P.chunk;
         const int tpb = item_tpb(c, nc);
-        k5_sim_full<<<(unsigned)((nc + tpb - 1) / tpb), tpb, 0, s>>>(
-            c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, P.d_tr,
-            P.d_ti ? P.d_ti + i0 : nullptr, P.opt, sim_scratch(c, P, nc), c->s_rep.p + i0,
-            iteration_ends ? c->s_ends.p + i0 * iterations : nullptr, c->s_st.p + i0);
+        if (perm)  // chunk = the permuted positions [i0, i0 + nc); timings by global index
+            k5_sim_full<<<(unsigned)((nc + tpb - 1) / tpb), tpb, 0, s>>>(
+                c->s_tim.p, (long long)nc, (int)policy, (int)iterations, P.d_tr, P.d_ti, P.opt,
+                sim_scratch(c, P, nc), c->s_rep.p, iteration_ends ? c->s_ends.p : nullptr, c->s_st.p,
+                perm + i0);
+        else
+            k5_sim_full<<<(unsigned)((nc + tpb - 1) / tpb), tpb, 0, s>>>(
+                c->s_tim.p + i0, (long long)nc, (int)policy, (int)iterations, P.d_tr,
+                P.d_ti ? P.d_ti + i0 : nullptr, P.opt, sim_scratch(c, P, nc), c->s_rep.p + i0,
+                iteration_ends ? c->s_ends.p + i0 * iterations : nullptr, c->s_st.p + i0);
         CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaMemcpyAsync(report, c->s_rep.p, n * sizeof(gp_sim_report), cudaMemcpyDeviceToHost, s));

@@ -478,6 +478,47 @@ __global__ void k5_bm_scatter(long long n, const uint8_t* __restrict__ bm, int n
     perm[atomicAdd(&offs[b], 1u)] = (uint32_t)i;
 }
 
+// Timings grouped by (stage count, micro-batch count) before simulating
+// (the event count grows with both): key = (S - 1) * 256 + min(M, 255).
+#define K5_NKEYS (GP_MAX_STAGES * 256)
+__device__ __forceinline__ int k5_tkey(const gp_timing& T) {
+    const long long mb = T.microbatch > 0 ? T.microbatch : 1;
+    long long M = T.batch > 0 ? (T.batch + mb - 1) / mb : 0;
+    if (M > 255) M = 255;
+    const int S = T.n_stages >= 1 && T.n_stages <= GP_MAX_STAGES ? (int)T.n_stages : 1;
+    return (S - 1) * 256 + (int)M;
+}
+__global__ void k5_key_hist(long long n, const gp_timing* __restrict__ T, uint32_t* hist) {
+    __shared__ uint32_t h[K5_NKEYS];
+    for (int j = threadIdx.x; j < K5_NKEYS; j += blockDim.x) h[j] = 0;
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        atomicAdd(&h[k5_tkey(T[i])], 1u);
+    __syncthreads();
+    for (int j = threadIdx.x; j < K5_NKEYS; j += blockDim.x)
+        if (h[j]) atomicAdd(&hist[j], h[j]);
+}
+__global__ void k5_key_scan(uint32_t* hist) {  // one block of 256 threads, 8 keys each
+    __shared__ uint32_t part[256];
+    const int t = threadIdx.x;
+    uint32_t v[K5_NKEYS / 256], acc = 0;
+#pragma unroll
+    for (int j = 0; j < K5_NKEYS / 256; ++j) { v[j] = hist[t * (K5_NKEYS / 256) + j]; acc += v[j]; }
+    part[t] = acc;
+    __syncthreads();
+    if (t == 0) { uint32_t run = 0; for (int j = 0; j < 256; ++j) { const uint32_t x = part[j]; part[j] = run; run += x; } }
+    __syncthreads();
+    uint32_t run = part[t];
+#pragma unroll
+    for (int j = 0; j < K5_NKEYS / 256; ++j) { hist[t * (K5_NKEYS / 256) + j] = run; run += v[j]; }
+}
+__global__ void k5_key_scatter(long long n, const gp_timing* __restrict__ T, uint32_t* offs,
+                               uint32_t* __restrict__ perm) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    perm[atomicAdd(&offs[k5_tkey(T[i])], 1u)] = (uint32_t)i;
+}
+
 // 1F1B makespan of explicit candidates (thread t simulates candidate
 // perm[t], or t without a permutation).
 __global__ void k5_sim_candidates(DevInst I, int k, long long ncand, const uint8_t* __restrict__ order,
@@ -511,9 +552,11 @@ __global__ void k5_plan_timing(DevInst I, int k, long long ncand, const uint8_t*
 
 __global__ void k5_sim_1f1b(const gp_timing* __restrict__ T, long long n, int policy, int iterations,
                             const gp_trace* __restrict__ traces, const uint32_t* __restrict__ tidx,
-                            double* __restrict__ makespan, uint8_t* __restrict__ status) {
+                            double* __restrict__ makespan, uint8_t* __restrict__ status,
+                            const uint32_t* __restrict__ perm = nullptr) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (perm) i = perm[i];
     double ms = NAN;
     const gp_trace* tr = traces ? traces + (tidx ? tidx[i] : 0u) : nullptr;
     int st = sim_any(T[i], policy, iterations, tr, &ms);
@@ -866,12 +909,14 @@ __device__ int sim_full(const gp_timing& T, int policy, int iterations, const gp
 __global__ void k5_sim_full(const gp_timing* __restrict__ T, long long n, int policy, int iterations,
                             const gp_trace* __restrict__ traces, const uint32_t* __restrict__ tidx,
                             gp_sim_options opt, SimScratch sc, gp_sim_report* __restrict__ rep,
-                            double* __restrict__ iter_ends, uint8_t* __restrict__ status) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+                            double* __restrict__ iter_ends, uint8_t* __restrict__ status,
+                            const uint32_t* __restrict__ perm = nullptr) {
+    const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // scratch slot
+    if (slot >= n) return;
+    const long long i = perm ? (long long)perm[slot] : slot;  // timing (perm: global index)
     const gp_trace* tr = traces ? traces + (tidx ? tidx[i] : 0u) : nullptr;
     gp_sim_report r;
-    int st = sim_full(T[i], policy, iterations, tr, opt, sc, i, &r,
+    int st = sim_full(T[i], policy, iterations, tr, opt, sc, slot, &r,
                       iter_ends ? iter_ends + i * (long long)iterations : nullptr, nullptr, 0,
                       nullptr, 0, nullptr, 0);
     if (st != GP_OK && st != GP_ERR_SCHEDULING) {
