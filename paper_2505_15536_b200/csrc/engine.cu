@@ -196,6 +196,8 @@ struct gp_ctx {
     unsigned int rec_W = 0;
     bool rec_ok = false;
     DBuf<uint32_t> recrow;    // record sweep padded row starts
+    DBuf<uint8_t> k2img;      // K2: shared-memory image of the current tables
+    unsigned long long tables_gen = 1, k2img_gen = 0;  // table builds / image's build
     DBuf<uint32_t> k5_perm;   // K5: candidates grouped by (b, m) index
     DBuf<uint32_t> k5_hist;
 
@@ -344,6 +346,7 @@ void gp_ctx_destroy(gp_ctx* c) {
 }
 
 static int run_tables(gp_ctx* c, bool full) {
+    ++c->tables_gen;
     DevInst I = c->view();
     cudaStream_t s = c->stream;
     CUDA_TRY(cudaMemsetAsync(c->flagsbuf.p, 0, sizeof(uint32_t), s));
@@ -733,12 +736,23 @@ int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_ord
             const unsigned long long chunks = (n + (unsigned long long)K2V_WCHUNK * nw - 1) /
                                               ((unsigned long long)K2V_WCHUNK * nw);
             if (grid > chunks) grid = chunks;
+            const uint8_t* img = nullptr;
+            if (smt) {  // the shared-memory image of this table generation
+                const size_t ib = k2v_bits_bytes(c->F, c->n) + k2v_tab_bytes(c->F, c->n, c->nm, I.nxp);
+                if (c->k2img_gen != c->tables_gen || !c->k2img.p) {
+                    CUDA_TRY(c->k2img.ensure(ib));
+                    k2_image_build<<<c->n_sms, 256, 0, c->stream>>>(I, c->k2img.p);
+                    CUDA_TRY(cudaGetLastError());
+                    c->k2img_gen = c->tables_gen;
+                }
+                img = c->k2img.p;
+            }
             if (smt)
                 k2_eval_batch_v4<16, true><<<(unsigned)grid, 512, smem_v, c->stream>>>(
-                    I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status);
+                    I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status, img);
             else
                 k2_eval_batch_v4<8, false><<<(unsigned)grid, 256, smem_v, c->stream>>>(
-                    I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status);
+                    I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status, nullptr);
             CUDA_TRY(cudaGetLastError());
             return GP_OK;
         }
@@ -1581,6 +1595,7 @@ int gp_replan(gp_ctx* c, const gp_instance* in, gp_best* best, gp_plan_info* inf
     }
     const double h1 = c->diag_timing ? now_us() : 0.0;
     if (c->diag_timing) CUDA_TRY(cudaEventRecord(c->t_ev0, s));
+    ++c->tables_gen;  // the graph rebuilds the tables
     CUDA_TRY(cudaGraphLaunch(c->graph_exec, s));
     CUDA_TRY(cudaEventRecord(c->arena_ev, s));
     if (c->diag_timing) CUDA_TRY(cudaEventRecord(c->t_ev1, s));

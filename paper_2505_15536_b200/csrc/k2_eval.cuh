@@ -588,8 +588,9 @@ __host__ __device__ inline size_t k2v_bits_bytes(int F, int n) { return (size_t)
 __host__ __device__ inline size_t k2v_tab_bytes(int F, int n, int nm, int nxp) {
     return (size_t)nm * F * (n + 1) * 16 * 2 + (((size_t)nm * F * F * nxp * 8 + 15) & ~(size_t)15);
 }
+__host__ __device__ inline size_t k2v_bar_bytes(int nwarps) { return ((size_t)nwarps * K2V_STAGES * 8 + 8 + 63) & ~(size_t)63; }
 __host__ __device__ inline size_t k2v_smem(int F, int n, int nm, int nxp, int nwarps, bool smt) {
-    return (((size_t)nwarps * K2V_STAGES * 8 + 63) & ~(size_t)63) + k2v_bits_bytes(F, n) +
+    return k2v_bar_bytes(nwarps) + k2v_bits_bytes(F, n) +
            (smt ? k2v_tab_bytes(F, n, nm, nxp) : 0) + (size_t)nwarps * K2V_STAGES * K2V_SLOT +
            (size_t)nwarps * K2V_QCAP * 16;
 }
@@ -600,12 +601,14 @@ static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_
                                                               const uint8_t* __restrict__ counts,
                                                               const uint8_t* __restrict__ bm,
                                                               double* __restrict__ cost,
-                                                              uint8_t* __restrict__ status) {
+                                                              uint8_t* __restrict__ status,
+                                                              const uint8_t* __restrict__ img) {
     extern __shared__ __align__(16) uint8_t v4_s[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = I.n, np = n + 1, F = I.F;
     const int nm = I.nm, nxp = I.nxp;
-    const size_t bar_bytes = ((size_t)NW * K2V_STAGES * 8 + 63) & ~(size_t)63;
+    const size_t bar_bytes = k2v_bar_bytes(NW);
+    uint64_t* img_bar = reinterpret_cast<uint64_t*>(v4_s) + NW * K2V_STAGES;
     const size_t bits_bytes = k2v_bits_bytes(F, n) + (SMT ? k2v_tab_bytes(F, n, nm, nxp) : 0);
     uint64_t* bar = reinterpret_cast<uint64_t*>(v4_s) + warp * K2V_STAGES;
     uint32_t* ibits = reinterpret_cast<uint32_t*>(v4_s + bar_bytes);
@@ -637,7 +640,15 @@ static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_
             if (c < nchunks) issue(c, s);
         }
     }
-    // bit rows from the stage codes (word w of row r: b = 32 w .. 32 w + 31)
+    // bit rows (and SMT tables): one bulk copy of the image k2_image_build
+    // made from this table generation, else from the stage codes
+    const uint32_t img_bytes = (uint32_t)bits_bytes;
+    if (img && threadIdx.x == 0) {
+        mbar_init(img_bar, 1);
+        mbar_expect_tx(img_bar, img_bytes);
+        tma_bulk_g2s(ibits, img, img_bytes, img_bar);
+    }
+    if (!img)
     for (int rw = threadIdx.x; rw < F * np * 4; rw += blockDim.x) {
         const int r = rw >> 2, w = rw & 3;  // r = f * np + a
         const uint8_t* src = I.scode + (size_t)(r / np) * N2 + (size_t)(r % np) * np;
@@ -648,7 +659,7 @@ static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_
         }
         ibits[rw] = bits;
     }
-    if constexpr (SMT) {
+    if (SMT && !img) {
         for (int e = threadIdx.x; e < nm * F * np; e += blockDim.x) {
             const int a = e % np, mf = e / np;  // (mi, f) = mf
             const double2* T = I.stg + (size_t)mf * N2;
@@ -657,7 +668,8 @@ static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_
         }
         for (int e = threadIdx.x; e < nm * F * F * nxp; e += blockDim.x) xs[e] = __ldg(&I.xt[e]);
     }
-    __syncthreads();
+    __syncthreads();  // (img_bar initialised)
+    if (img) mbar_wait(img_bar, 0);
     const bool fast_tables = *I.flags == 0u;
     const unsigned lt = (1u << lane) - 1u;
     const int nbm = I.nb * I.nm;
@@ -866,5 +878,36 @@ static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_
     if (lane < q) {
         load_entry(wq[lane]);
         finish_entry();
+    }
+}
+
+// The shared-memory image of k2_eval_batch_v4<*, true>: infeasible-stage bit
+// rows, first-stage rows, last-stage columns, boundary rows - built once per
+// table generation, bulk-copied by every CTA.
+static __global__ void k2_image_build(DevInst I, uint8_t* __restrict__ img) {
+    const int n = I.n, np = n + 1, F = I.F, nm = I.nm, nxp = I.nxp, N2 = np * np;
+    uint32_t* bits = reinterpret_cast<uint32_t*>(img);
+    double2* t0 = reinterpret_cast<double2*>(img + k2v_bits_bytes(F, n));
+    double2* t3 = t0 + (size_t)nm * F * np;
+    double* xs = reinterpret_cast<double*>(t3 + (size_t)nm * F * np);
+    const long long nb = (long long)F * np * 4, nt = (long long)nm * F * np, nx = (long long)nm * F * F * nxp;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nb + nt + nx;
+         e += (long long)gridDim.x * blockDim.x) {
+        if (e < nb) {
+            const int r = (int)(e >> 2), w = (int)(e & 3);
+            const uint8_t* src = I.scode + (size_t)(r / np) * N2 + (size_t)(r % np) * np;
+            uint32_t b = 0;
+            for (int j = 0; j < 32; ++j)
+                if (32 * w + j <= n) b |= (uint32_t)(src[32 * w + j] == SC_INFEASIBLE) << j;
+            bits[e] = b;
+        } else if (e < nb + nt) {
+            const long long q = e - nb;
+            const int a = (int)(q % np);
+            const double2* T = I.stg + (size_t)(q / np) * N2;
+            t0[q] = T[a];
+            t3[q] = T[(size_t)a * np + n];
+        } else {
+            xs[e - nb - nt] = I.xt[e - nb - nt];
+        }
     }
 }

@@ -15,7 +15,7 @@ from paper_2505_15536_b200.layout import PackedInstance  # noqa: E402
 m, t, g = instances.load("c4")
 eng = Engine(0).load(PackedInstance(m, t, g, 1.25))
 total = eng.space_size()
-N = 20_000_000
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 20_000_000
 idx = np.random.default_rng(4).integers(0, total, size=N)
 order, counts, bm = decode_indices(80, 4, idx, composition_table(80, 4))
 dev = torch.device("cuda", 0)
@@ -38,5 +38,5 @@ with torch.cuda.stream(stream):
 torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1]) / 20
 digest = int(np.bitwise_xor.reduce(ref))
-print(f"{os.environ.get('GP_ENGINE_LIB', 'default')}: K2 {ms * 1e3:.1f} us per 2e7 -> "
+print(f"{os.environ.get('GP_ENGINE_LIB', 'default')}: K2 {ms * 1e3:.1f} us per {N:.0e} -> "
       f"{N / (ms * 1e-3):.3e} cand/s; cost digest {digest:#x}, feasible {np.isfinite(d_cost.cpu().numpy()).mean():.3f}")
