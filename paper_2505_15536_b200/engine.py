@@ -248,8 +248,21 @@ class Engine:
         return info
 
     def group_splits(self, f: int) -> abi.GpGroupInfo:
+        """TP grid tiles / DP fractions of group f of the loaded instance (a
+        function of the instance's capacities and membership only: cached on
+        the PackedInstance, which is immutable)."""
+        cache = getattr(self.packed, "_group_splits", None) if self.packed is not None else None
+        if cache is not None and f in cache:
+            return cache[f]
         g = abi.GpGroupInfo()
         _check(lib().gp_group_splits(self._h, int(f), C.byref(g)))
+        if self.packed is not None:
+            if cache is None:
+                try:
+                    cache = self.packed._group_splits = {}
+                except AttributeError:  # slotted instance: no cache
+                    return g
+            cache[f] = g
         return g
 
     def sim_1f1b(self, packed_timings, n: int, iterations: int = 1):
