@@ -915,6 +915,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s / args.steps * 1e3,
+                    "ms_p50": statistics.median(lat) * 1e3, "ms_p99": pct(lat, 99) * 1e3,
                     "path": ("distributed.replan_snapshots_sharded" if X.world > 1 else
                              "replan.replan_snapshots") +
                             ": pinned host bandwidth matrices -> gp_replan_snapshots (H2D, K6 "
