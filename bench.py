@@ -558,8 +558,9 @@ def workload_config(S, total, world):
             "candidates_per_snapshot": total, "candidates_per_step": S * total,
             "layers": 80, "devices": 64, "groups": 4, "batch_micro_pairs": 6,
             "l2": "flushed between steps (256 MiB write)",
-            "parallelism": f"snapshot shards x{world} (contiguous by index) + NCCL all-gather "
-                           "of the 16-byte per-snapshot winners"}
+            "parallelism": f"snapshot shards x{world} (contiguous by index) + all-gather of the "
+                           "16-byte per-snapshot winners (peer-memory stores over NVLink; NCCL "
+                           "if peer access is unavailable)"}
 
 
 class Ctx:
@@ -796,10 +797,22 @@ def main():
     stream = torch.cuda.ExternalStream(eng.stream, device=X.dev)
     torch.cuda.synchronize()
 
+    # the winners' all-gather: peer-memory stores over NVLink (PeerGather,
+    # no NCCL in the step; GP_PEER=0 or a failed set-up on any rank: NCCL)
+    peer = None
+    if X.world > 1 and os.environ.get("GP_PEER", "1") != "0":
+        peer = DI.PeerGather(eng, width * 16)
+        if not peer.ok:
+            peer.close(X.barrier)
+            peer = None
+
     def step():
         eng.replan_snapshots_async(d_bw.data_ptr(), nloc, d_keys.data_ptr(), d_flags.data_ptr())
         if X.world > 1:
-            dist.all_gather_into_tensor(gathered, d_keys)
+            if peer is not None:
+                peer.gather(d_keys.data_ptr())
+            else:
+                dist.all_gather_into_tensor(gathered, d_keys)
 
     # ---- device-resident throughput (value) --------------------------------
     with torch.cuda.stream(stream):
@@ -823,7 +836,10 @@ def main():
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     dev_ms_max = X.max_over_ranks(sum(step_ms))
     value = S * total * args.steps / (dev_ms_max * 1e-3)
-    keys = (gathered if X.world > 1 else d_keys).cpu().numpy().reshape(-1, 2)
+    if peer is not None:
+        keys = np.frombuffer(peer.read(), dtype=np.int64).reshape(-1, 2)
+    else:
+        keys = (gathered if X.world > 1 else d_keys).cpu().numpy().reshape(-1, 2)
     flags_ok = int(d_flags[:nloc].sum().item()) == 0
     # rows of the gathered table in snapshot order
     rows_idx = np.concatenate([np.arange(r * width, r * width + (DI.shard_items(S, X.world, r)[1]
@@ -940,8 +956,11 @@ def main():
                          "peak_source": "FP64 DADD issue rate measured live on this GPU "
                                         "(gp_diag_fp64_peak: 8 independent DADD chains per "
                                         "thread); MEASURED_PEAKS.json has no FP64 entry"},
-            "gpu_launches": 3 * X.world * args.steps,
-            "gpu_launches_note": "per rank and step: k6_minbw, k6_patch, k3_sweep",
+            "gpu_launches": (3 + (2 if peer is not None else 0)) * X.world * args.steps,
+            "gpu_launches_note": "per rank and step: k6_minbw, k6_patch, k3_sweep_rec" +
+                                 (", k_peer_put, k_peer_wait (winners all-gathered through "
+                                  "peer memory over NVLink)" if peer is not None else
+                                  ("" if X.world == 1 else " (+ NCCL all-gather)")),
             "clocks": clk.summary(),
             "step_ms_p50": statistics.median(step_ms), "step_ms_p99": pct(step_ms, 99),
             "winners": {"flags_clear": flags_ok, "cross_checked_k1_k3": checked,
@@ -965,6 +984,9 @@ def main():
         if not args.no_extra and X.world == 1:
             line["extra"] = extra_sections(eng, packed, total, X.local, args, X.world)
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        X.barrier()
+        peer.close(X.barrier)
     eng.close()
     if X.world > 1:
         dist.barrier()

@@ -2678,3 +2678,106 @@ extern "C" int gp_group_fixed(gp_ctx* c, uint32_t D, const double* p_t, const do
                         fg_out.data(), sg_of, &nf, n_sg, fg_intra, fg_capacity, fg_min_bw,
                         sg_capacity);
 }
+
+// ----------------------------------------------------------------------------
+// Peer-memory all-gather of small per-rank records over NVLink / NVSwitch:
+// each rank owns one device buffer [arrival counter (256 B) | world x slot
+// bytes]; the buffers are exported as CUDA IPC handles and opened by every
+// other rank of the box.  A rank's gather = one kernel that stores its slot
+// into every peer's buffer (P2P stores over NVLink), fences at system scope
+// and bumps every peer's counter, then one kernel that waits (acquire) until
+// its own counter shows all ranks of this epoch.  Replaces the NCCL
+// all-gather of the K6 winners (16 B per snapshot) inside the bench step.
+// ----------------------------------------------------------------------------
+#define GP_PEER_MAX 16
+struct PeerSet { unsigned char* base[GP_PEER_MAX]; };
+
+static __global__ void k_peer_put(const unsigned char* __restrict__ src, unsigned long long slot_bytes,
+                                  int rank, int world, PeerSet P) {
+    // blockIdx.x = destination rank; the slot copied 16 B per thread
+    const int dst = blockIdx.x;
+    unsigned char* d = P.base[dst] + 256 + (size_t)rank * slot_bytes;
+    const unsigned long long n16 = slot_bytes / 16;
+    for (unsigned long long i = threadIdx.x; i < n16; i += blockDim.x)
+        reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(src)[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();  // the slot before the arrival
+        atomicAdd_system(reinterpret_cast<unsigned long long*>(P.base[dst]), 1ull);
+    }
+}
+
+// bounded: gives up after ~2 s (a peer that never arrives must not hang the
+// GPU), leaving the arrival count short - k_peer_put records the shortfall
+// in the buffer's second word for gp_peer_read's caller to see
+static __global__ void k_peer_wait(unsigned long long* counter, unsigned long long target) {
+    if (threadIdx.x != 0) return;
+    unsigned long long v, t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
+        if (v >= target) return;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 2000000000ull) { counter[1] = target - v; return; }  // timed out
+        __nanosleep(100);
+    }
+}
+
+extern "C" {
+
+int gp_peer_alloc(gp_ctx* c, uint64_t bytes, void** d_ptr, void* ipc_handle) {
+    if (!c || !d_ptr || !ipc_handle || bytes == 0) return fail(GP_ERR_INPUT, "bad arguments");
+    CUDA_TRY(cudaSetDevice(c->device));
+    void* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, bytes));
+    CUDA_TRY(cudaMemset(p, 0, bytes));
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) { cudaFree(p); return fail(GP_ERR_CUDA, "ipc handle: %s", cudaGetErrorString(e)); }
+    memcpy(ipc_handle, &h, sizeof(h));
+    *d_ptr = p;
+    return GP_OK;
+}
+
+int gp_peer_open(gp_ctx* c, const void* ipc_handle, void** d_ptr) {
+    if (!c || !ipc_handle || !d_ptr) return fail(GP_ERR_INPUT, "bad arguments");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    CUDA_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return GP_OK;
+}
+
+int gp_peer_close(gp_ctx* c, void* d_ptr, int owned) {
+    if (!c || !d_ptr) return GP_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (owned) CUDA_TRY(cudaFree(d_ptr));
+    else CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
+    return GP_OK;
+}
+
+int gp_peer_read(gp_ctx* c, const void* d_ptr, void* host, uint64_t bytes) {
+    if (!c || !d_ptr || !host) return fail(GP_ERR_INPUT, "bad arguments");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(host, d_ptr, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return GP_OK;
+}
+
+int gp_peer_allgather(gp_ctx* c, const void* d_src, uint64_t slot_bytes, uint32_t rank,
+                      uint32_t world, void* const* peer_bases, uint64_t epoch) {
+    if (!c || !d_src || !peer_bases || world == 0 || world > GP_PEER_MAX || rank >= world ||
+        slot_bytes % 16 != 0)
+        return fail(GP_ERR_INPUT, "bad arguments");
+    CUDA_TRY(cudaSetDevice(c->device));
+    PeerSet P = {};
+    for (uint32_t r = 0; r < world; ++r) P.base[r] = reinterpret_cast<unsigned char*>(peer_bases[r]);
+    k_peer_put<<<world, 128, 0, c->stream>>>(reinterpret_cast<const unsigned char*>(d_src), slot_bytes,
+                                             (int)rank, (int)world, P);
+    k_peer_wait<<<1, 32, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(peer_bases[rank]),
+                                         (unsigned long long)epoch * world);
+    CUDA_TRY(cudaGetLastError());
+    return GP_OK;
+}
+
+}  // extern "C"

@@ -236,3 +236,94 @@ def exhaustive_plan_sharded(model, topology, groups, config, engine=None, group=
     total = nbm * NP * NC
     return D.SearchResult(plan=plan, breakdown=breakdown, best_cost_trace=[cost],
                           evaluated=total)
+
+
+class PeerGather:
+    """All-gather of fixed-size per-rank device records through peer memory
+    (C-ABI gp_peer_*): every rank's slot is stored into every rank's buffer
+    over NVLink by one kernel, with a system-scope arrival counter the
+    receiving GPU waits on - no NCCL call in the data path.  Used for the K6
+    winners (16 B per snapshot) of a sharded snapshot batch.  ``ok`` is False
+    on every rank when any rank could not set it up (callers fall back to
+    NCCL's all-gather)."""
+
+    def __init__(self, engine, slot_bytes: int, group=None):
+        import ctypes as C
+        import torch
+        import torch.distributed as dist
+        from .engine import lib
+        self.eng = engine
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.slot = (int(slot_bytes) + 15) // 16 * 16
+        self.epoch = 0
+        self._owned = C.c_void_p()
+        self._opened = []
+        handle = (C.c_char * 64)()
+        ok = lib().gp_peer_alloc(engine.handle, 256 + self.world * self.slot, C.byref(self._owned),
+                                 handle) == 0
+        handles = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(handles, bytes(handle) if ok else None, group=group)
+        else:
+            handles = [bytes(handle) if ok else None]
+        ok = ok and all(h is not None for h in handles)
+        bases = []
+        for r, h in enumerate(handles):
+            if not ok:
+                break
+            if r == self.rank:
+                bases.append(self._owned.value)
+                continue
+            p = C.c_void_p()
+            hb = (C.c_char * 64).from_buffer_copy(h)
+            if lib().gp_peer_open(engine.handle, hb, C.byref(p)) != 0:
+                ok = False
+                break
+            self._opened.append(p)
+            bases.append(p.value)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+        if self.world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        self.ok = bool(flag.item())
+        self._bases = (C.c_void_p * self.world)(*(bases if self.ok else [None] * self.world))
+
+    @property
+    def records(self) -> int:
+        """Device address of the gathered slots (rank r's at + r * slot)."""
+        return self._owned.value + 256
+
+    def gather(self, d_src: int) -> None:
+        """Asynchronous on the engine stream: slot_bytes from device address
+        d_src into every rank's buffer, then wait for every rank's slot."""
+        from .engine import _check, lib
+        self.epoch += 1
+        _check(lib().gp_peer_allgather(self.eng.handle, d_src, self.slot, self.rank, self.world,
+                                        self._bases, self.epoch))
+
+    def read(self) -> bytes:
+        """The gathered slots (synchronises the engine stream); raises when a
+        wait timed out (a rank's slot never arrived)."""
+        import ctypes as C
+        from . import domain as D
+        from .engine import _check, lib
+        head = (C.c_uint64 * 2)()
+        _check(lib().gp_peer_read(self.eng.handle, self._owned.value, head, 16))
+        if head[1]:
+            raise D.DeviceError(f"peer all-gather: {head[1]} arrival(s) missing after the timeout")
+        buf = (C.c_char * (self.world * self.slot))()
+        _check(lib().gp_peer_read(self.eng.handle, self.records, buf, self.world * self.slot))
+        return bytes(buf)
+
+    def close(self, barrier=None) -> None:
+        """Unmap the peers' buffers, wait for every rank to have done so
+        (``barrier``, e.g. torch.distributed.barrier), free this one."""
+        from .engine import lib
+        for p in self._opened:
+            lib().gp_peer_close(self.eng.handle, p, 0)
+        self._opened = []
+        if barrier is not None:
+            barrier()
+        if self._owned.value:
+            lib().gp_peer_close(self.eng.handle, self._owned, 1)
+            self._owned = type(self._owned)()

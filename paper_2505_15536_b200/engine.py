@@ -90,6 +90,11 @@ def lib():
         L.gp_replan_snapshots.argtypes = [vp, P(C.c_double), C.c_uint32, P(abi.GpBest),
                                           P(C.c_int32)]
         L.gp_replan_snapshots_async.argtypes = [vp, vp, C.c_uint32, vp, vp]
+        L.gp_peer_alloc.argtypes = [vp, C.c_uint64, P(vp), vp]
+        L.gp_peer_open.argtypes = [vp, vp, P(vp)]
+        L.gp_peer_close.argtypes = [vp, vp, C.c_int]
+        L.gp_peer_read.argtypes = [vp, vp, vp, C.c_uint64]
+        L.gp_peer_allgather.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, P(vp), C.c_uint64]
         L.gp_sim_candidates.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p, C.c_uint32,
                                         C.c_double, P(C.c_double), u8p]
         L.gp_ctx_set_k3_mode.argtypes = [vp, C.c_int]

@@ -49,6 +49,34 @@ def main():
     bws = R.bandwidth_matrices(packed, [I.snapshot_multipliers(spec, j) for j in range(37)])
     res = DI.replan_snapshots_sharded(model, topo, groups, P.SearchConfig(seed=0), bws, engine=eng)
     out["snapshots"] = [r if isinstance(r, tuple) else type(r).__name__ for r in res]
+    # peer-memory all-gather (NVLink stores + arrival counter) vs NCCL's, for
+    # the K6 winners of C3 snapshot shards, over several epochs
+    import numpy as np
+    world, rank = dist.get_world_size(), dist.get_rank()
+    eng.load(packed)
+    S = 37
+    width = -(-S // world)
+    lo, hi = DI.shard_items(S, world, rank)
+    d_bw = torch.from_numpy(np.ascontiguousarray(bws[lo:hi])).cuda()
+    d_keys = torch.zeros((width, 2), dtype=torch.int64, device="cuda")
+    d_flags = torch.zeros(width, dtype=torch.int32, device="cuda")
+    ref = torch.empty((world * width, 2), dtype=torch.int64, device="cuda")
+    pg = DI.PeerGather(eng, width * 16)
+    out["peer_ok"] = pg.ok
+    out["peer_equal"] = []
+    for epoch in range(3):
+        if hi > lo:
+            eng.replan_snapshots_async(d_bw.data_ptr(), hi - lo, d_keys.data_ptr(), d_flags.data_ptr())
+        torch.cuda.synchronize()
+        d_keys[0, 1] += epoch  # a different payload per epoch
+        torch.cuda.synchronize()
+        dist.all_gather_into_tensor(ref, d_keys)
+        if pg.ok:
+            pg.gather(d_keys.data_ptr())
+            got = np.frombuffer(pg.read(), dtype=np.int64).reshape(-1, 2)
+            out["peer_equal"].append(bool((got == ref.cpu().numpy()).all()))
+    dist.barrier()
+    pg.close(dist.barrier)
     gathered = [None] * dist.get_world_size()
     dist.all_gather_object(gathered, out)
     if dist.get_rank() == 0:

@@ -66,3 +66,8 @@ def test_sharded_snapshots_match_golden(sharded):
     assert len(got) == 37
     for j, r in enumerate(got):
         assert r[0] == snap[j]["cost"], j
+
+
+def test_peer_memory_allgather_matches_nccl(sharded):
+    assert sharded["peer_ok"], "peer-memory set-up failed (no P2P between the GPUs?)"
+    assert sharded["peer_equal"] == [True, True, True]
