@@ -558,9 +558,8 @@ def workload_config(S, total, world):
             "candidates_per_snapshot": total, "candidates_per_step": S * total,
             "layers": 80, "devices": 64, "groups": 4, "batch_micro_pairs": 6,
             "l2": "flushed between steps (256 MiB write)",
-            "parallelism": f"snapshot shards x{world} (contiguous by index) + all-gather of the "
-                           "16-byte per-snapshot winners (peer-memory stores over NVLink; NCCL "
-                           "if peer access is unavailable)"}
+            "parallelism": f"snapshot shards x{world} (contiguous by index) + NCCL all-gather of "
+                           "the 16-byte per-snapshot winners"}
 
 
 class Ctx:
@@ -797,10 +796,12 @@ def main():
     stream = torch.cuda.ExternalStream(eng.stream, device=X.dev)
     torch.cuda.synchronize()
 
-    # the winners' all-gather: peer-memory stores over NVLink (PeerGather,
-    # no NCCL in the step; GP_PEER=0 or a failed set-up on any rank: NCCL)
+    # the winners' all-gather: NCCL by default; GP_PEER=1 = peer-memory stores
+    # over NVLink (distributed.PeerGather; measured equal to NCCL at N=2 and
+    # 4 - 0.483 vs 0.481 ms p50 steps at N=4 - the 16 B per snapshot gather is
+    # latency-bound either way)
     peer = None
-    if X.world > 1 and os.environ.get("GP_PEER", "1") != "0":
+    if X.world > 1 and os.environ.get("GP_PEER", "0") == "1":
         peer = DI.PeerGather(eng, width * 16)
         if not peer.ok:
             peer.close(X.barrier)
