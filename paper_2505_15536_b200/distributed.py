@@ -117,16 +117,17 @@ def gather_snapshot_records(local: np.ndarray, n_total: int, group=None, device=
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return local
     world = dist.get_world_size(group)
-    width = -(-n_total // world)
-    buf = torch.zeros((width, 3), dtype=torch.int64, device=device)
-    if local.shape[0]:
-        buf[:local.shape[0]] = torch.from_numpy(np.ascontiguousarray(local)).to(device)
-    out = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(out, buf, group=group)
+    width = max(1, -(-n_total // world))
+    h = np.zeros((width, 3), dtype=np.int64)
+    h[:local.shape[0]] = local
+    buf = torch.from_numpy(h).to(device)
+    out = torch.empty((world * width, 3), dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out, buf, group=group)  # one collective, one D2H
+    allrec = out.cpu().numpy().reshape(world, width, 3)
     rows = []
     for r in range(world):
         lo, hi = shard_items(n_total, world, r)
-        rows.append(out[r][:hi - lo].cpu().numpy())
+        rows.append(allrec[r, :hi - lo])
     return np.concatenate(rows) if rows else local
 
 
