@@ -172,7 +172,7 @@ typedef struct gp_timing {
 /* schedule policies (src/engine.py:48-52) */
 enum { GP_POLICY_GPIPE = 0, GP_POLICY_1F1B = 1, GP_POLICY_ZB_ORIGINAL = 2, GP_POLICY_ZB_COMPACT = 3 };
 
-#define GP_MAX_BREAKPOINTS 32
+#define GP_MAX_BREAKPOINTS 256
 /* NetworkTrace (src/nettrace.py:12-45) restricted to the plan's boundary
  * links "b-(b+1)": per boundary b, n_points[b] breakpoints (t, multiplier)
  * sorted by strictly increasing t; the multiplier before the first one is 1. */

@@ -128,7 +128,7 @@ class GpTiming(C.Structure):
 
 GP_POLICY_GPIPE, GP_POLICY_1F1B, GP_POLICY_ZB_ORIGINAL, GP_POLICY_ZB_COMPACT = 0, 1, 2, 3
 POLICY_CODE = {"gpipe": 0, "1f1b": 1, "zb_original": 2, "zb_compact": 3}
-GP_MAX_BREAKPOINTS = 32
+GP_MAX_BREAKPOINTS = 256
 
 
 class GpTrace(C.Structure):

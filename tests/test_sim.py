@@ -281,3 +281,36 @@ def test_k5_full_without_options_equals_fast_path(engine):
         fast = SM.simulate_makespans_policy(tims, pol, 2, engine=engine)
         full = SM.simulate_timings(tims, pol, config=SM.SimConfig(iterations=2), engine=engine)
         assert (np.array([o.makespan for o in full]).view(np.uint64) == fast.view(np.uint64)).all()
+
+
+@pytest.mark.gpu
+def test_k5_full_long_traces_match_oracle(engine, oracle_lib):
+    """Traces with up to 200 breakpoints per link (the reference has no
+    limit; the ABI holds GP_MAX_BREAKPOINTS = 256): device reports equal the
+    oracle's bit for bit."""
+    from paper_2505_15536_b200 import abi
+    assert abi.GP_MAX_BREAKPOINTS >= 200
+    rng = random.Random(9)
+    tims = _random_timings(2000, 44)
+    traces = []
+    for t in tims:
+        bps = {}
+        for b in range(len(t.stages) - 1):
+            pts = sorted(set(round(rng.uniform(0.0, 200.0), 4) for _ in range(rng.randint(50, 200))))
+            bps[f"{b}-{b + 1}"] = [[x, rng.choice([0.25, 0.5, 0.75, 1.0, 1.25])] for x in pts]
+        traces.append(bps)
+    arr = SM.pack_timings(tims)
+    tr = SM.pack_traces(traces)
+    idx = np.arange(len(tims))
+    for ad, asy in ((False, False), (True, True)):
+        reps, ends, st = engine.simulate_report(arr, len(tims), abi.POLICY_CODE["1f1b"], 3, tr,
+                                                len(traces), idx, adapter=ad, async_iterations=asy)
+        oreps, oends, ost = oracle_lib.sim_reports(arr, len(tims), abi.POLICY_CODE["1f1b"], 3, tr,
+                                                   idx, adapter=ad, async_iterations=asy)
+        assert (st == ost).all()
+        okm = st == 0
+        a = np.frombuffer(reps, dtype=np.uint8).reshape(len(tims), -1)
+        b = np.frombuffer(oreps, dtype=np.uint8).reshape(len(tims), -1)
+        assert okm.mean() > 0.9
+        assert (a[okm] == b[okm]).all()
+        assert (ends.view(np.uint64)[okm] == oends.view(np.uint64)[okm]).all()
