@@ -220,24 +220,99 @@ def python_reference_rate(spec_name="c4", n_cand=2000, procs=None):
     from concurrent.futures import ProcessPoolExecutor
     t0, t1 = _py_ref_worker((spec_name, 0, n_cand, 0.0))
     rate1 = n_cand / (t1 - t0)
+    t0, t1 = _py_ref_worker((spec_name, 0, n_cand, 0.0, True))
+    rate_log = n_cand / (t1 - t0)
+    logging.disable(logging.CRITICAL)
     procs = procs or os.cpu_count() or 1
     start = time.time() + 6.0  # every worker has built its instance by then
     with ProcessPoolExecutor(procs) as ex:
         spans = list(ex.map(_py_ref_worker, [(spec_name, s + 1, n_cand, start)
                                              for s in range(procs)]))
     el = max(b for _, b in spans) - min(a for a, _ in spans)
-    return {"value_1proc": rate1, "value_all": procs * n_cand / el, "processes": procs,
+    return {"value_1proc": rate1, "value_1proc_as_shipped_logging": rate_log,
+            "value_all": procs * n_cand / el, "processes": procs,
             "unit": "candidates/s",
             "sample": f"{n_cand} random C4 candidates per process (fresh _evaluate cache each, "
                       "logging disabled); all processes start together",
             "source": "geopipe (unmodified reference) " + getattr(gp, "__version__", "")}
 
 
+def _ref_import():
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "geopipe")) and p not in sys.path:
+            sys.path.insert(0, p)
+    import geopipe as gp
+    return gp
+
+
+def _ref_instance(gp, spec, multipliers=None):
+    """(model, topology, groups) built with the reference's own constructors
+    and grouping from an App. D spec (bandwidth x multiplier per pair)."""
+    from geopipe.timing import GroupIndex
+    devs = [gp.DeviceSpec(id=i, memory_bytes=mem, benchmark_times=(("bench", 1.0 / p_c),))
+            for i, _, _, p_c, mem in spec.devices()]
+    meas = []
+    for u, v, lat, bw in spec.links():
+        if multipliers is not None:
+            bw = bw * multipliers[(min(u, v), max(u, v))]
+        meas.append(gp.LinkMeasurement(endpoints=frozenset((u, v)), alpha_seconds=1e8 / bw,
+                                       beta_seconds=lat, payload_bytes_m=1e8, latency_seconds=lat,
+                                       bandwidth_bytes_per_s=bw))
+    topo = gp.build_topology(devs, meas)
+    fgs = gp.group_first_level(topo, 0.3)
+    groups = GroupIndex.build(fgs, {f.id: gp.group_second_level(f, topo, 0.3) for f in fgs})
+    model = gp.ModelSpec(layers=tuple(gp.LayerSpec(*r) for r in spec.layers),
+                         global_batch_candidates=tuple(spec.batches),
+                         microbatch_candidates=tuple(spec.micros))
+    return model, topo, groups
+
+
+def python_reference_replan(n_search=5, n_exhaustive=2):
+    """The unmodified Python reference's re-plan per C3 bandwidth snapshot of
+    C2: rebuild the topology from the scaled link
+    measurements, regroup, then search_plan (p50 over ``n_search`` snapshots)
+    and exhaustive_plan (p50 over ``n_exhaustive``); logging disabled.  None
+    when the reference is not importable."""
+    import logging
+    try:
+        gp = _ref_import()
+    except ImportError:
+        return None
+    from paper_2505_15536_b200 import instances
+    logging.disable(logging.CRITICAL)
+    spec = instances.config("c2")
+    ts, te = [], []
+    for j in range(max(n_search, n_exhaustive)):
+        mult = instances.snapshot_multipliers(spec, j)
+        if j < n_search:
+            t0 = time.perf_counter()
+            m, t, g = _ref_instance(gp, spec, mult)
+            gp.search_plan(m, t, g, gp.SearchConfig(seed=0))
+            ts.append(time.perf_counter() - t0)
+        if j < n_exhaustive:
+            t0 = time.perf_counter()
+            m, t, g = _ref_instance(gp, spec, mult)
+            gp.exhaustive_plan(m, t, g, gp.SearchConfig(seed=0))
+            te.append(time.perf_counter() - t0)
+    logging.disable(logging.NOTSET)
+    return {"c3_search_plan_s_p50": statistics.median(ts), "snapshots_search": len(ts),
+            "c3_exhaustive_plan_s_p50": statistics.median(te), "snapshots_exhaustive": len(te),
+            "note": "per C3 snapshot of C2: topology rebuilt from the scaled link measurements, "
+                    "group_first_level / group_second_level, then the planner (one process)"}
+
+
 def _py_ref_worker(args):
-    spec_name, seed, n_cand, start = args
+    spec_name, seed, n_cand, start = args[:4]
+    as_shipped = len(args) > 4 and args[4]
     import logging
     import random
-    logging.disable(logging.CRITICAL)
+    root = logging.getLogger()
+    saved = root.handlers[:]
+    if as_shipped:  # the reference's per-plan warnings formatted and written (to /dev/null)
+        logging.disable(logging.NOTSET)
+        root.handlers[:] = [logging.StreamHandler(open(os.devnull, "w"))]
+    else:
+        logging.disable(logging.CRITICAL)
     for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
         if os.path.isdir(os.path.join(p, "geopipe")) and p not in sys.path:
             sys.path.insert(0, p)
@@ -274,7 +349,10 @@ def _py_ref_worker(args):
     t = time.time()
     for c, b, m in cands:
         _evaluate(c, b, m, groups, topo, model, cfg, {})
-    return t, time.time()
+    t1 = time.time()
+    root.handlers[:] = saved
+    logging.disable(logging.CRITICAL)
+    return t, t1
 
 
 def extra_sections(eng, packed, total, local, args, world):
@@ -982,6 +1060,9 @@ def main():
             py = python_reference_rate()
             line["cpu_baseline"]["python_reference"] = py if py is not None else \
                 "absent: geopipe not importable on this host (baseline/_ref missing)"
+            rp = python_reference_replan()
+            if rp is not None:
+                line["cpu_baseline"]["python_reference_replan"] = rp
         if not args.no_extra and X.world == 1:
             line["extra"] = extra_sections(eng, packed, total, X.local, args, X.world)
         print(json.dumps(line), flush=True)
