@@ -92,7 +92,15 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
     const int A0 = k - 2;
     const int nrecp = G.nrecp;
     const unsigned int per_snap = G.items * (unsigned int)G.cpi;
-    const unsigned int snap = blockIdx.x / per_snap, local = blockIdx.x % per_snap;
+    // CTA -> (snapshot, unit): snapshot-minor (K3R_SNAPMINOR), so a
+    // snapshot's items run in different waves and the later ones start from
+    // the bound the earlier ones published (fewer slow-path steps)
+#ifndef K3R_SNAPMINOR
+#define K3R_SNAPMINOR 1
+#endif
+    const unsigned int nsnap = gridDim.x / per_snap;
+    const unsigned int snap = K3R_SNAPMINOR ? blockIdx.x % nsnap : blockIdx.x / per_snap;
+    const unsigned int local = K3R_SNAPMINOR ? blockIdx.x / nsnap : blockIdx.x % per_snap;
     const unsigned int islot = local % G.items, csub = local / G.items;
     const unsigned long long item = G.item0 + islot;
     const int mi = (int)(item / G.NP);
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
     double T = __longlong_as_double((long long)0x7FEFFFFFFFFFFFFFull);
     const bool skip = skip_if_flags && skip_if_flags[snap];  // generic kernel decides
     unsigned long long* const gbound = G.gbound ? G.gbound + snap : nullptr;
-    unsigned long long gb_prev = 0ull;
+    unsigned long long gb_prev = (K3R_GT && gbound) ? *(volatile unsigned long long*)gbound : 0ull;
     for (int j = 0; !skip && task_of(j) < ntask; ++j) {
         const K3Run ri = ri_a;
         const double2 e1 = e1_a;
