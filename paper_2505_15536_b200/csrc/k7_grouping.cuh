@@ -344,7 +344,9 @@ __device__ int k7_agglomerate(int level, int n, const uint16_t* items, const dou
             if (c < b) g.live[(size_t)c * n + b] = 0;
         }
         // the merged group's _mean_intra_pt, on an otherwise idle thread
+#if !defined(K7_LAZY_INTRA)
         if (level == 1 && n < nt && tid == nt - 1) k7_group_value(1, g, sh, n, pt, pc, D, a);
+#endif
         sync();
 #if defined(K7_PROFILE)
         c1 = clock64(); c_keys += c1 - c0; c0 = c1;
