@@ -36,14 +36,18 @@
 // rank), ordered by length, in 32-run tasks; a warp's lanes therefore walk in
 // lock step and read the same records (shared-memory broadcast).  Tasks go
 // to the warps in snake order (lengths balance); a warp loads its next
-// task's run entry and stage k-3 entry while it walks the current one.  Rows
-// of records are padded to a multiple of the q unroll with records whose
-// totals are +inf (no remainder loop).
+// task's run entry and stage k-3 entry while it walks the current one, and
+// the next q step's records while it computes the current one.  Rows of
+// records are padded to a multiple of the q unroll with records whose totals
+// are +inf (no remainder loop).
 #ifndef K3R_UNROLL
-#define K3R_UNROLL 4
+#define K3R_UNROLL 2
 #endif
 #ifndef K3R_RB
 #define K3R_RB 4  // row-record (row, lane chunk) pairs per warp in flight
+#endif
+#ifndef K3R_PF
+#define K3R_PF 1  // next iteration's records loaded while this one computes
 #endif
 #ifndef K3R_GT
 #define K3R_GT 1  // share the bound across the snapshot's CTAs (G.gbound)
@@ -308,10 +312,7 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
             for (int bi = 0; bi < NB; ++bi) Tb[bi] = (len > 0 && mx1[bi] <= T) ? T : -1.0;
         };
         set_bounds();
-        auto step = [&](int i, double* t2, double* t3) -> bool {
-            GP_DCHECK(rstart[a] + i < (uint32_t)nrecp && a + 1 + i < n + K3R_UNROLL);
-            const K3RowRec R = rp[i];
-            const K3ColRecN<NB> Cq = cp[i];
+        auto step_rc = [&](int i, const K3RowRec& R, const K3ColRecN<NB>& Cq, double* t2, double* t3) -> bool {
             const double res2 = res1 + R.D2;
             const double fill3 = fill2 + R.G2;
             const double res3 = res2 + Cq.D3;
@@ -329,6 +330,10 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
                              gtsel(t3[bi], gtsel(t2[bi], mx1[bi])));
             }
             return p;
+        };
+        auto step = [&](int i, double* t2, double* t3) -> bool {
+            GP_DCHECK(rstart[a] + i < (uint32_t)nrecp && a + 1 + i < n + K3R_UNROLL);
+            return step_rc(i, rp[i], cp[i], t2, t3);
         };
         // a candidate within the bound: its exact cost (first-max, the
         // reference's order) against the lane's best under the full key
@@ -358,17 +363,44 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep_rec(DevInst I,
             }
             set_bounds();
         };
+#if K3R_PF
+        // records of the next iteration loaded while this one computes
+        K3RowRec Rn[K3R_UNROLL];
+        K3ColRecN<NB> Cn[K3R_UNROLL];
+#pragma unroll
+        for (int uu = 0; uu < K3R_UNROLL; ++uu) { Rn[uu] = rp[uu]; Cn[uu] = cp[uu]; }
+#endif
         for (int i0 = 0; i0 < lmax; i0 += K3R_UNROLL) {
             // lanes past their (padded) row: no candidate (in-range reads)
             const bool act = i0 < lenp;
             const int ib = act ? i0 : 0;
             double t2[K3R_UNROLL][NB], t3[K3R_UNROLL][NB];
             bool p[K3R_UNROLL], any = false;
+#if K3R_PF
+            K3RowRec Rc[K3R_UNROLL];
+            K3ColRecN<NB> Cc[K3R_UNROLL];
+#pragma unroll
+            for (int uu = 0; uu < K3R_UNROLL; ++uu) { Rc[uu] = Rn[uu]; Cc[uu] = Cn[uu]; }
+            {
+                const int inx = i0 + K3R_UNROLL;
+                const int ibn = inx < lenp ? inx : 0;
+                if (inx < lmax) {
+#pragma unroll
+                    for (int uu = 0; uu < K3R_UNROLL; ++uu) { Rn[uu] = rp[ibn + uu]; Cn[uu] = cp[ibn + uu]; }
+                }
+            }
+#pragma unroll
+            for (int uu = 0; uu < K3R_UNROLL; ++uu) {
+                p[uu] = step_rc(ib + uu, Rc[uu], Cc[uu], t2[uu], t3[uu]) & act;
+                any |= p[uu];
+            }
+#else
 #pragma unroll
             for (int uu = 0; uu < K3R_UNROLL; ++uu) {
                 p[uu] = step(ib + uu, t2[uu], t3[uu]) & act;
                 any |= p[uu];
             }
+#endif
             if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
                 for (int uu = 0; uu < K3R_UNROLL; ++uu)
