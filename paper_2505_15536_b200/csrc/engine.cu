@@ -724,10 +724,10 @@ int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_ord
         if (v4) {
             // 16 warps with the first/last-stage and boundary tables in shared
             // memory when they fit (GP_K2_SMT=0 disables), else 8 warps
-            bool smt = k2v_smem(c->F, c->n, c->nm, I.nxp, 16, true) <= (size_t)c->smem_max;
+            bool smt = k2v_smem(c->F, c->n, c->nm, I.nxp, K2V_NW, true) <= (size_t)c->smem_max;
             if (const char* e = getenv("GP_K2_SMT")) smt = smt && atoi(e) != 0;
-            const int nw = smt ? 16 : 8;
-            const void* kfn = smt ? (const void*)k2_eval_batch_v4<16, true> : (const void*)k2_eval_batch_v4<8, false>;
+            const int nw = smt ? K2V_NW : 8;
+            const void* kfn = smt ? (const void*)k2_eval_batch_v4<K2V_NW, true> : (const void*)k2_eval_batch_v4<8, false>;
             const size_t smem_v = k2v_smem(c->F, c->n, c->nm, I.nxp, nw, smt);
             int per_sm = 0;
             { int st_ = kernel_slots(c, kfn, nw * 32, smem_v, &per_sm);
@@ -748,7 +748,7 @@ int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_ord
                 img = c->k2img.p;
             }
             if (smt)
-                k2_eval_batch_v4<16, true><<<(unsigned)grid, 512, smem_v, c->stream>>>(
+                k2_eval_batch_v4<K2V_NW, true><<<(unsigned)grid, K2V_NW * 32, smem_v, c->stream>>>(
                     I, (long long)n, d_order, d_counts, d_bm, d_cost, d_status, img);
             else
                 k2_eval_batch_v4<8, false><<<(unsigned)grid, 256, smem_v, c->stream>>>(

@@ -569,10 +569,13 @@ static __global__ void __launch_bounds__(K2T_THREADS, K2T_MINB) k2_eval_batch_t4
 #define K2V_WCHUNK 256
 #endif
 #ifndef K2V_STAGES
-#define K2V_STAGES 3
+#define K2V_STAGES 2
 #endif
 #define K2V_QCAP 160  // queue entries per warp: < 32 left + 128 of one round
 #define K2V_THREADS 256
+#ifndef K2V_NW
+#define K2V_NW 16  // warps per CTA of the shared-memory-table variant
+#endif
 #ifndef K2V_MINB
 #define K2V_MINB 2
 #endif
