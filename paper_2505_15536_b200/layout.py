@@ -199,6 +199,19 @@ class PackedInstance:
         return s
 
     # ---- candidate encoding ----
+    def encode_keys(self, keys, bm_index):
+        """``(order ids, counts)`` tuples -> (order u8[n,k], counts u8[n,k], bm u8[n])."""
+        n = len(keys)
+        k = len(keys[0][0]) if n else self.n_fgs
+        pos = self.fg_pos
+        order = np.array([[pos[f] for f in o] for o, _ in keys], dtype=np.uint8).reshape(n, k)
+        counts = np.array([c for _, c in keys], dtype=np.uint8).reshape(n, k)
+        if np.isscalar(bm_index):
+            bm = np.full(n, bm_index, dtype=np.uint8)
+        else:
+            bm = np.asarray(bm_index, dtype=np.uint8)
+        return order, counts, bm
+
     def encode(self, cands, bm_index):
         """Candidates -> (order u8[n,k], counts u8[n,k], bm u8[n])."""
         n = len(cands)

@@ -120,6 +120,35 @@ def expand_candidates(cands, rng: random.Random) -> List[D.Candidate]:
     return list(seen.values())
 
 
+def _expand_keys(cands, rng: random.Random) -> List[tuple]:
+    """expand_candidates on ``(order, counts)`` tuples (the beam driver's
+    internal form): the same variants in the same first-seen order and the
+    same RNG draws (one ``rng.sample(range(k), 2)`` per candidate with k > 1),
+    without building a Candidate per variant."""
+    seen: Dict[tuple, None] = {}
+    add = seen.setdefault
+    for order, counts in cands:
+        k = len(order)
+        add((order, counts), None)
+        if k > 1:
+            i, j = rng.sample(range(k), 2)
+            o = list(order)
+            o[i], o[j] = o[j], o[i]
+            add((tuple(o), counts), None)
+        for b in range(k - 1):
+            if counts[b] > 1:
+                c = list(counts)
+                c[b] -= 1
+                c[b + 1] += 1
+                add((order, tuple(c)), None)
+            if counts[b + 1] > 1:
+                c = list(counts)
+                c[b + 1] -= 1
+                c[b] += 1
+                add((order, tuple(c)), None)
+    return list(seen)
+
+
 # --------------------------------------------------------------------------
 # result assembly from the engine's plan detail
 # --------------------------------------------------------------------------
@@ -223,7 +252,8 @@ def search_plan(model, topology, groups, config, engine: Engine = None) -> D.Sea
     passes = []
     for bm, (b, m) in enumerate(pairs):
         rng = random.Random(f"{config.seed}:{b}:{m}")
-        beam = initial_candidates(model, fgs, config.beam_width, rng.randrange(2 ** 30))
+        beam = [(c.order, c.counts) for c in
+                initial_candidates(model, fgs, config.beam_width, rng.randrange(2 ** 30))]
         passes.append({"bm": bm, "rng": rng, "beam": beam, "tops": [], "iters": [],
                        "err": None})
     cache: Dict[tuple, float] = {}
@@ -236,18 +266,18 @@ def search_plan(model, topology, groups, config, engine: Engine = None) -> D.Sea
         expanded = []
         todo_c, todo_bm, todo_keys = [], [], []
         for ps in live:
-            ex = expand_candidates(ps["beam"], ps["rng"])
+            ex = _expand_keys(ps["beam"], ps["rng"])
             expanded.append(ex)
             b, m = pairs[ps["bm"]]
             for c in ex:
-                key = (c.order, c.counts, b, m)
+                key = c + (b, m)
                 if key not in cache and key not in errors:
                     cache[key] = None
                     todo_c.append(c)
                     todo_bm.append(ps["bm"])
                     todo_keys.append(key)
         if todo_c:
-            o, cn, bmv = packed.encode(todo_c, todo_bm)
+            o, cn, bmv = packed.encode_keys(todo_c, todo_bm)
             cost, status = eng.eval_batch(o, cn, bmv)
             for key, c, st in zip(todo_keys, cost.tolist(), status.tolist()):
                 if st:
@@ -258,14 +288,14 @@ def search_plan(model, topology, groups, config, engine: Engine = None) -> D.Sea
         for ps, ex in zip(live, expanded):
             b, m = pairs[ps["bm"]]
             ps["iters"].append(ex)
-            bad = next((j for j, c in enumerate(ex) if (c.order, c.counts, b, m) in errors), None)
+            bad = next((j for j, c in enumerate(ex) if c + (b, m) in errors), None) if errors else None
             if bad is not None:
                 ps["err"] = (len(ps["iters"]) - 1, bad)
                 first_err = min(first_err, passes.index(ps))
                 continue
-            scored = [(cache[(c.order, c.counts, b, m)], (c.order, c.counts), c) for c in ex]
-            scored.sort(key=lambda x: (x[0], x[1]))
-            ps["beam"] = [x[2] for x in scored[:config.beam_width]]
+            scored = [(cache[c + (b, m)], c) for c in ex]
+            scored.sort()
+            ps["beam"] = [x[1] for x in scored[:config.beam_width]]
             ps["tops"].append((scored[0][0], scored[0][1]))
     # replay in the reference's sequential order: warnings, trace, best, errors
     best = None
@@ -277,14 +307,13 @@ def search_plan(model, topology, groups, config, engine: Engine = None) -> D.Sea
         for it, ex in enumerate(ps["iters"]):
             stop = ps["err"][1] if ps["err"] is not None and ps["err"][0] == it else len(ex)
             for c in ex[:stop]:
-                key = (c.order, c.counts, b, m)
+                key = c + (b, m)
                 if key not in seen:
                     seen.add(key)
                     if warn and cache[key] == INFEASIBLE:
                         log.warning("plan %s exceeds device memory; penalized", key)
             if stop < len(ex):
-                c = ex[stop]
-                key = (c.order, c.counts, b, m)
+                key = ex[stop] + (b, m)
                 abi.raise_for(errors[key], f"candidate {key} failed")
         incumbent = math.inf
         for top_cost, top_key in ps["tops"]:
