@@ -53,3 +53,21 @@ def test_driver_matches_reference(name):
             beam_o, beam_r = eo[:8], er[:8]
     for total, w in [(7, [1.0, 2.0, 4.0]), (80, [3.3, 1.1, 7.7, 0.5]), (5, [2.0, 3.0])]:
         assert P.proportional_split(total, w, 1) == RP.proportional_split(total, w, 1)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_tuple_expansion_matches_candidate_expansion(name):
+    """The beam driver's tuple form (_expand_keys) yields the variants of
+    expand_candidates in the same order and leaves the RNG in the same state."""
+    m, t, g = I.load(name, jitter=True)
+    fgs = sorted(g.fgs.values(), key=lambda f: f.id)
+    for seed in range(10):
+        beam = P.initial_candidates(m, fgs, 8, seed)
+        keys = [(c.order, c.counts) for c in beam]
+        r1, r2 = random.Random(seed), random.Random(seed)
+        for _ in range(6):
+            ec = P.expand_candidates(beam, r1)
+            ek = P._expand_keys(keys, r2)
+            assert [(c.order, c.counts) for c in ec] == ek
+            assert r1.getstate() == r2.getstate()
+            beam, keys = ec[3:11], ek[3:11]
