@@ -816,6 +816,46 @@ def scaling_rows(X, eng, packed, model, topo, groups, total):
                 "matrices (H2D, K6, D2H, all-gather)"}
     e2.close()
 
+    # (e) BASELINE configs[4]: batch-size sweep at this N - the first N
+    # enumeration ranks of C4 split into contiguous rank ranges (K3 range
+    # kernel per rank), and N = 9 x C4 as 9 bandwidth snapshots split by index
+    # (K6); device time per call, max over ranks (L2 warm)
+    eng.load(packed)
+    c5 = {}
+    for N in (10**3, 10**4, 10**5, 10**6, total):
+        lo_r, hi_r = X.shard(N)
+
+        def c5_step(lo_r=lo_r, hi_r=hi_r):
+            if hi_r > lo_r:
+                eng.argmin_range_async(lo_r, hi_r)
+        ms = event_loop(X, stream, c5_step, 20, 3)
+        if hi_r > lo_r:
+            eng.argmin_fetch()
+        dmax = X.max_over_ranks(statistics.median(ms))
+        c5[str(N)] = {"device_ms_p50": dmax, "candidates_per_s": N / (dmax * 1e-3),
+                      "candidates_this_rank": hi_r - lo_r}
+    spec4 = instances.config("c4")
+    bw9 = replan.bandwidth_matrices(packed, [instances.snapshot_multipliers(spec4, j) for j in range(9)])
+    lo9, hi9 = X.shard(9)
+    d_bw9 = torch.from_numpy(np.ascontiguousarray(bw9[lo9:hi9])).to(X.dev)
+    d_k9 = torch.zeros((max(1, hi9 - lo9), 2), dtype=torch.int64, device=X.dev)
+    d_f9 = torch.zeros(max(1, hi9 - lo9), dtype=torch.int32, device=X.dev)
+    torch.cuda.synchronize()
+
+    def c5_k6():
+        if hi9 > lo9:
+            eng.replan_snapshots_async(d_bw9.data_ptr(), hi9 - lo9, d_k9.data_ptr(), d_f9.data_ptr())
+    ms = event_loop(X, stream, c5_k6, 10, 2)
+    dmax = X.max_over_ranks(statistics.median(ms))
+    c5[str(9 * total)] = {"device_ms_p50": dmax, "candidates_per_s": 9 * total / (dmax * 1e-3),
+                          "snapshots_this_rank": hi9 - lo9}
+    rows["c5_batch_sweep_sharded"] = {
+        "rows": c5,
+        "note": "BASELINE configs[4]: the first N ranks of C4 in contiguous rank ranges per rank "
+                "(K3 range kernel), N = 9 x C4 as 9 snapshots split by index (K6); device time "
+                "per call, max over ranks; small N are launch-latency bound"}
+    eng.load(packed)
+
     # (d) weak scaling: every rank re-plans its own C4 snapshot (K3), rank = snapshot
     m3, t3, g3 = instances.load("c4", snapshot=X.rank)
     p3 = PackedInstance(m3, t3, g3, 1.25)
