@@ -127,6 +127,45 @@ def test_k2_c4_large_batch_path_bitwise(engine, oracle_lib, name):
     assert same_bits(cost, _tile(gc, reps)).all()
 
 
+def test_k2_c4_malformed_large_batch_vs_oracle(engine, oracle_lib):
+    # the k = 4 vector-lane kernel's packed-word input checks (byte-SIMD group
+    # range / distinctness, zero counts, count sums, (b, m) range) and the
+    # slow path (sums < n) against the oracle's or_evaluate, candidate by
+    # candidate, on a batch past 2^16
+    doc, model, topo, groups, packed = _load(engine, "c4")
+    from paper_2505_15536_b200.enumeration import composition_table, decode_indices
+    rng = np.random.default_rng(17)
+    N = 140_000
+    total = engine.space_size()
+    order, counts, bm = decode_indices(packed.n_layers, 4, rng.integers(0, total, size=N),
+                                       composition_table(packed.n_layers, 4))
+    order, counts, bm = order.copy(), counts.copy(), bm.copy()
+    kind = rng.integers(0, 12, size=N)
+    col = rng.integers(0, 4, size=N)
+    rows = np.arange(N)
+    m = kind == 1  # duplicate group
+    order[m, col[m]] = order[m, (col[m] + 1) % 4]
+    for j, g in ((2, 4), (3, 15), (4, 16), (5, 31), (6, 200)):  # group out of range
+        m = kind == j
+        order[m, col[m]] = g
+    m = kind == 7  # zero count
+    counts[m, col[m]] = 0
+    m = (kind == 8) & (counts[rows, col] > 1)  # sum < n (slow path)
+    counts[m, col[m]] -= 1
+    m = (kind == 9) & (counts[rows, col] < 250)  # sum > n
+    counts[m, col[m]] += 1
+    m = kind == 10  # (b, m) index out of range
+    bm[m] = rng.integers(len(packed.batches) * len(packed.micros), 256, size=int(m.sum()))
+    cost, status = engine.eval_batch(order, counts, bm)
+    ocost, ostatus = oracle_lib.eval_batch(packed, order, counts, bm)
+    assert (status == ostatus).all(), np.nonzero(status != ostatus)[0][:10]
+    good = ostatus == 0
+    assert np.isnan(cost[~good]).all()
+    ok = same_bits(cost[good], ocost[good])
+    assert ok.all(), np.nonzero(~ok)[0][:10]
+    assert (~good).sum() > N // 2 and good.sum() > N // 10
+
+
 def test_k2_rejects_bad_candidates(engine):
     doc, model, topo, groups, packed = _load(engine, "c2")
     order = np.array([[0, 0, 1], [0, 1, 7], [0, 1, 2], [0, 1, 2]], np.uint8)
