@@ -166,6 +166,40 @@ def test_k2_c4_malformed_large_batch_vs_oracle(engine, oracle_lib):
     assert (~good).sum() > N // 2 and good.sum() > N // 10
 
 
+def test_k2_image_follows_table_changes(engine, oracle_lib):
+    """The k = 4 large-batch kernel bulk-copies a shared-memory image of the
+    tables built once per table generation: a bandwidth snapshot
+    (gp_set_bandwidth), a gp_replan graph replay and a reload must each give
+    a fresh image (results equal to the oracle on the instance then loaded)."""
+    from paper_2505_15536_b200 import instances as I
+    from paper_2505_15536_b200.enumeration import composition_table, decode_indices
+    spec = I.config("c4")
+    base = PackedInstance(*I.build(spec), 1.25)
+    snaps = [PackedInstance(*I.build(spec, I.snapshot_multipliers(spec, j)), 1.25) for j in (1, 2)]
+    engine.load(base)
+    total = engine.space_size()
+    idx = np.random.default_rng(23).integers(0, total, size=70_000)
+    order, counts, bm = decode_indices(base.n_layers, 4, idx, composition_table(base.n_layers, 4))
+
+    def check(packed):
+        cost, status = engine.eval_batch(order, counts, bm)
+        ocost, ostatus = oracle_lib.eval_batch(packed, order, counts, bm)
+        assert (status == ostatus).all()
+        assert same_bits(cost, ocost).all()
+        return cost
+
+    c0 = check(base)
+    engine.set_bandwidth(snaps[0].bw)
+    c1 = check(snaps[0])
+    assert not same_bits(c0, c1).all()  # the snapshot changes costs
+    engine.reset_bandwidth()
+    check(base)
+    engine.replan(snaps[1])  # graph path: K1 inside the replayed graph
+    check(snaps[1])
+    engine.load(base)
+    check(base)
+
+
 def test_k2_rejects_bad_candidates(engine):
     doc, model, topo, groups, packed = _load(engine, "c2")
     order = np.array([[0, 0, 1], [0, 1, 7], [0, 1, 2], [0, 1, 2]], np.uint8)
