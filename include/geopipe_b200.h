@@ -497,13 +497,15 @@ int gp_replan_snapshots_async(gp_ctx *ctx, const double *d_bandwidth, uint32_t n
 /* Peer-memory all-gather of small per-rank records between the GPUs of one
  * box (replaces the NCCL all-gather of the per-snapshot winners of
  * gp_replan_snapshots_async).  Each rank allocates one
- * buffer of 256 + world * slot_bytes bytes (gp_peer_alloc: device pointer +
- * a 64-byte CUDA IPC handle to share), opens every other rank's handle
- * (gp_peer_open), then per gather (gp_peer_allgather, asynchronous on the
- * context stream) stores its slot_bytes (multiple of 16) from d_src into
- * slot `rank` of every rank's buffer over NVLink, fences at system scope,
- * bumps each buffer's arrival counter (the first 8 bytes), and waits on the
- * device until its own counter reaches epoch * world (epoch = 1, 2, ...).
+ * buffer of 256 + 2 * world * slot_bytes bytes (gp_peer_alloc: device
+ * pointer + a 64-byte CUDA IPC handle to share), opens every other rank's
+ * handle (gp_peer_open), then per gather (gp_peer_allgather, asynchronous on
+ * the context stream) stores its slot_bytes (multiple of 16) from d_src into
+ * slot `rank` of table (epoch & 1) of every rank's buffer over NVLink (table t
+ * at byte 256 + t * world * slot_bytes), fences at system scope, bumps each
+ * buffer's arrival counter (the first 8 bytes), and waits on the device until
+ * its own counter reaches epoch * world (epoch = 1, 2, ...).  A rank must
+ * consume epoch e's table (in stream order) before its gather of e + 1.
  * peer_bases[r] = rank r's buffer as seen from this rank. */
 int gp_peer_alloc(gp_ctx *ctx, uint64_t bytes, void **d_ptr, void *ipc_handle);
 int gp_peer_open(gp_ctx *ctx, const void *ipc_handle, void **d_ptr);

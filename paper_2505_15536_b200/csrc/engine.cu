@@ -2681,22 +2681,26 @@ extern "C" int gp_group_fixed(gp_ctx* c, uint32_t D, const double* p_t, const do
 
 // ----------------------------------------------------------------------------
 // Peer-memory all-gather of small per-rank records over NVLink / NVSwitch:
-// each rank owns one device buffer [arrival counter (256 B) | world x slot
-// bytes]; the buffers are exported as CUDA IPC handles and opened by every
-// other rank of the box.  A rank's gather = one kernel that stores its slot
-// into every peer's buffer (P2P stores over NVLink), fences at system scope
-// and bumps every peer's counter, then one kernel that waits (acquire) until
-// its own counter shows all ranks of this epoch.  Replaces the NCCL
-// all-gather of the K6 winners (16 B per snapshot) inside the bench step.
+// each rank owns one device buffer [arrival counter (256 B) | 2 x world x
+// slot bytes]; the buffers are exported as CUDA IPC handles and opened by
+// every other rank of the box.  A rank's gather = one kernel that stores its
+// slot into every peer's buffer (P2P stores over NVLink), fences at system
+// scope and bumps every peer's counter, then one kernel that waits (acquire)
+// until its own counter shows all ranks of this epoch.  Epochs alternate
+// between the two tables: a peer already at epoch e + 1 writes the other
+// table while this rank still reads epoch e's, and it cannot reach e + 2
+// before this rank's own epoch-(e + 1) store, which this rank issues after
+// consuming epoch e in stream order.  Replaces the NCCL all-gather of the K6
+// winners (16 B per snapshot) inside the bench step.
 // ----------------------------------------------------------------------------
 #define GP_PEER_MAX 16
 struct PeerSet { unsigned char* base[GP_PEER_MAX]; };
 
 static __global__ void k_peer_put(const unsigned char* __restrict__ src, unsigned long long slot_bytes,
-                                  int rank, int world, PeerSet P) {
+                                  int rank, int world, int table, PeerSet P) {
     // blockIdx.x = destination rank; the slot copied 16 B per thread
     const int dst = blockIdx.x;
-    unsigned char* d = P.base[dst] + 256 + (size_t)rank * slot_bytes;
+    unsigned char* d = P.base[dst] + 256 + ((size_t)table * world + rank) * slot_bytes;
     const unsigned long long n16 = slot_bytes / 16;
     for (unsigned long long i = threadIdx.x; i < n16; i += blockDim.x)
         reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(src)[i];
@@ -2708,8 +2712,8 @@ static __global__ void k_peer_put(const unsigned char* __restrict__ src, unsigne
 }
 
 // bounded: gives up after ~2 s (a peer that never arrives must not hang the
-// GPU), leaving the arrival count short - k_peer_put records the shortfall
-// in the buffer's second word for gp_peer_read's caller to see
+// GPU) and records the shortfall in the buffer's second word for
+// gp_peer_read's caller to see
 static __global__ void k_peer_wait(unsigned long long* counter, unsigned long long target) {
     if (threadIdx.x != 0) return;
     unsigned long long v, t0, t;
@@ -2773,7 +2777,7 @@ int gp_peer_allgather(gp_ctx* c, const void* d_src, uint64_t slot_bytes, uint32_
     PeerSet P = {};
     for (uint32_t r = 0; r < world; ++r) P.base[r] = reinterpret_cast<unsigned char*>(peer_bases[r]);
     k_peer_put<<<world, 128, 0, c->stream>>>(reinterpret_cast<const unsigned char*>(d_src), slot_bytes,
-                                             (int)rank, (int)world, P);
+                                             (int)rank, (int)world, (int)(epoch & 1), P);
     k_peer_wait<<<1, 32, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(peer_bases[rank]),
                                          (unsigned long long)epoch * world);
     CUDA_TRY(cudaGetLastError());

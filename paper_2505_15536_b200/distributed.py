@@ -261,7 +261,7 @@ class PeerGather:
         self._owned = C.c_void_p()
         self._opened = []
         handle = (C.c_char * 64)()
-        ok = lib().gp_peer_alloc(engine.handle, 256 + self.world * self.slot, C.byref(self._owned),
+        ok = lib().gp_peer_alloc(engine.handle, 256 + 2 * self.world * self.slot, C.byref(self._owned),
                                  handle) == 0
         handles = [None] * self.world
         if self.world > 1:
@@ -291,8 +291,11 @@ class PeerGather:
 
     @property
     def records(self) -> int:
-        """Device address of the gathered slots (rank r's at + r * slot)."""
-        return self._owned.value + 256
+        """Device address of the latest gather's slots (rank r's at + r *
+        slot).  Epochs alternate between two tables, so the table stays valid
+        until this rank's next-but-one gather; consume it (in stream order)
+        before the next gather."""
+        return self._owned.value + 256 + (self.epoch & 1) * self.world * self.slot
 
     def gather(self, d_src: int) -> None:
         """Asynchronous on the engine stream: slot_bytes from device address

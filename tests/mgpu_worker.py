@@ -75,6 +75,35 @@ def main():
             pg.gather(d_keys.data_ptr())
             got = np.frombuffer(pg.read(), dtype=np.int64).reshape(-1, 2)
             out["peer_equal"].append(bool((got == ref.cpu().numpy()).all()))
+    # back-to-back epochs in stream order (no host sync between gathers) with
+    # rank 0 delayed before it consumes each table: the alternating tables
+    # keep epoch e's table intact until its owner has copied it out
+    out["peer_pipelined_equal"] = []
+    if pg.ok:
+        class _Cai:  # a torch view of a raw device address
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8",
+                                                 "data": (ptr, False), "version": 3}
+        n = world * width * 2
+        E = 6
+        pay = [d_keys.clone() for _ in range(E)]
+        for e in range(E):
+            pay[e][:, 1] += 1000 * (e + 1) + rank
+        outs = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(E)]
+        torch.cuda.synchronize()
+        dist.barrier()
+        est = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", torch.cuda.current_device()))
+        with torch.cuda.stream(est):
+            for e in range(E):
+                pg.gather(pay[e].data_ptr())
+                if rank == 0:
+                    torch.cuda._sleep(2_000_000)
+                outs[e].copy_(torch.as_tensor(_Cai(pg.records, n), device="cuda"))
+        torch.cuda.synchronize()
+        for e in range(E):
+            dist.all_gather_into_tensor(ref, pay[e])
+            out["peer_pipelined_equal"].append(bool((outs[e].cpu().numpy() ==
+                                                     ref.cpu().numpy().reshape(-1)).all()))
     dist.barrier()
     pg.close(dist.barrier)
     gathered = [None] * dist.get_world_size()

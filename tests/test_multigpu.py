@@ -71,3 +71,4 @@ def test_sharded_snapshots_match_golden(sharded):
 def test_peer_memory_allgather_matches_nccl(sharded):
     assert sharded["peer_ok"], "peer-memory set-up failed (no P2P between the GPUs?)"
     assert sharded["peer_equal"] == [True, True, True]
+    assert sharded["peer_pipelined_equal"] == [True] * 6
