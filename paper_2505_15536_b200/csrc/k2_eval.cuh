@@ -587,21 +587,13 @@ static __global__ void __launch_bounds__(K2T_THREADS, K2T_MINB) k2_eval_batch_t4
 // last-stage columns of 4 words: bit a of column f <=> stage [a, n) of group f
 // is infeasible (4F consecutive words: a conflict-free lookup for F <= 8).
 __host__ __device__ inline size_t k2v_bits_bytes(int F, int n) { return (size_t)F * (n + 2) * 16; }
-#ifndef K2V_SIMDCHK
-#define K2V_SIMDCHK 1
-#endif
-#ifndef K2V_SWZ
-#define K2V_SWZ 0  // XOR-swizzled row words (fewer bank conflicts, more ALU: 114.4 vs 111.2 us)
-#endif
-__device__ __forceinline__ unsigned k2v_row_word(unsigned r, unsigned w) {
-    return (r << 2) + (K2V_SWZ ? (w ^ ((r >> 3) & 3u)) : w);
-}
+__device__ __forceinline__ unsigned k2v_row_word(unsigned r, unsigned w) { return (r << 2) + w; }
 // word e of the bit image (rows, then columns) from the stage codes
 __device__ inline uint32_t k2v_bits_word(const DevInst& I, int e) {
     const int n = I.n, np = n + 1, N2 = np * np;
     uint32_t bits = 0;
     if (e < I.F * np * 4) {
-        const int r = e >> 2, w = K2V_SWZ ? (e & 3) ^ ((r >> 3) & 3) : (e & 3);  // r = f * np + a
+        const int r = e >> 2, w = e & 3;  // r = f * np + a
         const uint8_t* src = I.scode + (size_t)(r / np) * N2 + (size_t)(r % np) * np;
         for (int j = 0; j < 32; ++j) {
             const int b = 32 * w + j;
@@ -699,10 +691,7 @@ static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_
     const bool fast_tables = *I.flags == 0u;
     const unsigned lt = (1u << lane) - 1u;
     const int nbm = I.nb * I.nm;
-    const unsigned fmask = F >= 32 ? 0xffffffffu : ((1u << F) - 1u);
-#if K2V_SIMDCHK
     const unsigned fbias = (unsigned)(128 - (F < 128 ? F : 128)) * 0x01010101u;
-#endif
     // bit b of row (f, a)
     auto inf_bit = [&](unsigned f, unsigned a, unsigned b) -> unsigned {
         const uint32_t w = ibits[k2v_row_word(f * (unsigned)np + a, b >> 5)];
@@ -798,15 +787,10 @@ static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_
     // distinct (a 4-member bit set), no zero count, sum of counts <= n, (b, m)
     // index in range; the cut positions are the byte-wise prefix sums.
     auto classify = [&](uint32_t ow, uint32_t cw, unsigned b) -> int {
-#if K2V_SIMDCHK
         const unsigned om = ow & 0x0f0f0f0fu;  // groups < 16: in-range table rows for any input
-#else
-        const unsigned om = ow;
-#endif
         const unsigned o0 = om & 0xffu, o1 = __byte_perm(om, 0u, 0x4441), o2 = __byte_perm(om, 0u, 0x4442),
                        o3 = om >> 24;
         const unsigned total = __vsadu4(cw, 0u);
-#if K2V_SIMDCHK
         // groups: every byte < F (bytes < 128 first, then byte + 128 - F has
         // its top bit clear), pairwise distinct (no zero byte in the
         // differences to the byte-rotated words: the 6 pairs)
@@ -815,24 +799,13 @@ static __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : K2V_MINB)) k2_
         const unsigned z = ((d8 - 0x01010101u) & ~d8) | ((d16 - 0x01010101u) & ~d16) |
                            (cw - 0x01010101u) & ~cw | (ow & 0x80808080u) | (ow + fbias);
         const bool ok = ((z & 0x80808080u) == 0u) & (b < (unsigned)nbm) & (total <= (unsigned)n);
-#else
-        const unsigned msk = (1u << (o0 & 31u)) | (1u << (o1 & 31u)) | (1u << (o2 & 31u)) | (1u << (o3 & 31u));
-        const bool ok = ((ow & 0xE0E0E0E0u) == 0u) & (__popc(msk) == 4) & ((msk & ~fmask) == 0u) &
-                        ((((cw - 0x01010101u) & ~cw & 0x80808080u) == 0u)) & (b < (unsigned)nbm) &
-                        (total <= (unsigned)n);
-#endif
         const bool fast = ok & fast_tables & (total == (unsigned)n);
         // p1..p3 (exact when fast: sums <= n <= 127)
-        const unsigned pw = (cw * 0x01010101u) & (K2V_SIMDCHK ? 0x7f7f7f7fu : 0xffffffffu);
+        const unsigned pw = (cw * 0x01010101u) & 0x7f7f7f7fu;
         const unsigned p1 = pw & 0xffu, p2 = __byte_perm(pw, 0u, 0x4441), p3 = __byte_perm(pw, 0u, 0x4442);
-#if K2V_SIMDCHK  // unconditional lookups (rows < 16 * 128, in the allocation), no branches
+        // unconditional lookups (rows < 16 * 128, in the allocation), no branches
         const unsigned inf = (inf_bit(o0, 0u, p1) | inf_bit(o1, p1, p2) | inf_bit(o2, p2, p3) |
                               inf_last(o3, p3)) & (unsigned)fast;
-#else
-        const unsigned inf = fast ? (inf_bit(o0, 0u, p1) | inf_bit(o1, p1, p2) | inf_bit(o2, p2, p3) |
-                                     inf_last(o3, p3))
-                                  : 0u;
-#endif
 #if defined(K2V_STREAM)  // diagnostic build: inputs in, outputs out, no classification
         return ((ow ^ cw ^ b) & 1u) ? 1 : 1;
 #endif
