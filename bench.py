@@ -19,13 +19,15 @@ all-gathered over NCCL inside the step, so every rank ends with all 128 plans
              steps, max over ranks
   e2e        the same step through the public API with host buffers:
              distributed.replan_snapshots_sharded (single GPU:
-             replan.replan_snapshots) - pinned H2D of the matrices, K6, D2H
-             of the winners, all-gather - wall clock, max over ranks
+             replan.replan_snapshots) - pinned H2D of the matrices, K6,
+             all-gather of the winners from device memory, one D2H - wall
+             clock, max over ranks
   roofline   the sweep kernel is FP64-issue-bound (tables in shared memory,
-             no per-candidate HBM traffic): 39 algorithmic FP64 ops per C4
-             candidate (11k - 5) x candidates per launch over
-             the launch's CUDA-event duration, against the FP64 add rate
-             measured live on this GPU
+             no per-candidate HBM traffic): the record sweep's 10.5
+             algorithmic FP64 ops per C4 candidate (sweep_ops_per_candidate;
+             the reference order's 11k - 5 = 39 is reported beside it) x
+             candidates per launch over the launch's CUDA-event duration,
+             against the FP64 add rate measured live on this GPU
   cpu_baseline  the C oracle port (oracle/, test infrastructure) on the host
              threads over a bounded prefix of one snapshot, rank 0 at N=1,
              plus the unmodified Python reference on a sample when it is
@@ -995,10 +997,11 @@ def main():
     e2e_s = X.max_over_ranks(sum(lat))
     e2e_value = S * total * args.steps / e2e_s
     assert (res.status == 0).all() and (res.cost.view(np.int64) == win[:, 0]).all()
-    # whole job: the matrices in, per snapshot its 16-byte key + 4-byte flags
-    # out, and under torchrun each rank's read of the gathered record table
+    # whole job: the matrices in; out, per snapshot its 16-byte key + 4-byte
+    # flags (one GPU) or under torchrun each rank's read of the gathered
+    # [world x width x 3] int64 record table
     h2d = S * bws.shape[1] * bws.shape[2] * 8
-    d2h = S * 20 + (X.world * X.world * width * 3 * 8 if X.world > 1 else 0)
+    d2h = X.world * X.world * width * 3 * 8 if X.world > 1 else S * 20
 
     rows = None
     if not args.no_rows:
@@ -1053,9 +1056,12 @@ def main():
                     "ms_p50": statistics.median(lat) * 1e3, "ms_p99": pct(lat, 99) * 1e3,
                     "path": ("distributed.replan_snapshots_sharded" if X.world > 1 else
                              "replan.replan_snapshots") +
-                            ": pinned host bandwidth matrices -> gp_replan_snapshots (H2D, K6 "
-                            "table patch + K3 sweep, D2H of the winners)" +
-                            (" -> NCCL all-gather of the records" if X.world > 1 else "")},
+                            (": pinned host bandwidth matrices -> per rank H2D of its shard, "
+                             "gp_replan_snapshots_async (K6 table patch + K3 sweep) into device "
+                             "keys, NCCL all-gather of the records from device memory, one D2H"
+                             if X.world > 1 else
+                             ": pinned host bandwidth matrices -> gp_replan_snapshots (H2D, K6 "
+                             "table patch + K3 sweep, D2H of the winners)")},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": SWEEP_DRAM_BYTES,

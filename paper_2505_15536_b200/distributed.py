@@ -148,6 +148,10 @@ def replan_snapshots_sharded(model, topology, groups, config, bandwidths: np.nda
     eng = (engine or default_engine(torch.cuda.current_device())).load(packed)
     S = bandwidths.shape[0]
     lo, hi = shard_items(S, world, rank)
+    if world > 1 and S >= world and packed.n_fgs >= 3:
+        allrec = _replan_shard_device(eng, packed, bandwidths, S, lo, hi, world, group)
+        if allrec is not None:
+            return decode_snapshot_records(packed, allrec)
     rec = np.zeros((hi - lo, 3), dtype=np.int64)
     if hi > lo:
         from .engine import best_fields
@@ -158,6 +162,79 @@ def replan_snapshots_sharded(model, topology, groups, config, bandwidths: np.nda
         rec[:, 2] = status
     allrec = gather_snapshot_records(rec, S, group, torch.device("cuda"))
     return decode_snapshot_records(packed, allrec)
+
+
+def _replan_shard_device(eng, packed, bandwidths, S, lo, hi, world, group):
+    """The device-resident form of the sharded snapshot re-plan: this rank's
+    matrices H2D, gp_replan_snapshots_async (K6) into device keys + flags,
+    one NCCL all-gather of the [width, 3] records straight from device
+    memory and one D2H - no host round trip between the sweep and the
+    collective.  Snapshots whose tables raise (flags) are redone by their
+    owner through the status-tracking gp_replan_snapshots and shared with a
+    second gather (every rank sees the same flags, so the collectives stay
+    matched).  None when the loaded instance needs the status path for
+    every snapshot (gp_replan_snapshots_async refuses it on every rank)."""
+    import torch
+    import torch.distributed as dist
+    from . import abi
+    from .engine import best_fields
+    n = hi - lo
+    width = -(-S // world)
+    Dn = bandwidths.shape[1]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    key = (width, Dn, world)
+    bufs = getattr(eng, "_shard_bufs", None)
+    if bufs is None or bufs[0] != key:
+        bufs = (key, torch.empty((width, Dn, Dn), dtype=torch.float64, device=dev),
+                torch.zeros((width, 2), dtype=torch.int64, device=dev),
+                torch.zeros(width, dtype=torch.int32, device=dev),
+                torch.zeros((width, 3), dtype=torch.int64, device=dev),
+                torch.empty((world * width, 3), dtype=torch.int64, device=dev))
+        eng._shard_bufs = bufs
+    _, d_bw, d_keys, d_flags, d_rec, d_out = bufs
+    cur = torch.cuda.current_stream(dev)
+    d_bw[:n].copy_(torch.from_numpy(np.ascontiguousarray(bandwidths[lo:hi], dtype=np.float64)),
+                   non_blocking=True)
+    est = torch.cuda.ExternalStream(eng.stream, device=dev)
+    est.wait_stream(cur)
+    ok = 1
+    try:
+        eng.replan_snapshots_async(d_bw.data_ptr(), n, d_keys.data_ptr(), d_flags.data_ptr())
+    except D.GeopipeError:
+        ok = 0  # the instance itself needs the status path (same on every rank)
+    cur.wait_stream(est)
+    if not ok:
+        return None
+    d_rec[:n, :2].copy_(d_keys[:n])
+    d_rec[:n, 2].copy_(d_flags[:n])
+    dist.all_gather_into_tensor(d_out, d_rec, group=group)
+    allrec = d_out.cpu().numpy().reshape(world, width, 3)
+    NC, NP, _ = space_dims(packed.n_layers, packed.n_fgs, len(packed.batches), len(packed.micros))
+    nbm = len(packed.batches) * len(packed.micros)
+    rows = []
+    for r in range(world):
+        rlo, rhi = shard_items(S, world, r)
+        rows.append(allrec[r, :rhi - rlo])
+    recs = np.concatenate(rows)
+    flags = recs[:, 2] != 0
+    tie = recs[:, 1].view(np.uint64)
+    empty = tie == np.uint64(0xFFFFFFFFFFFFFFFF)
+    t = np.where(empty, np.uint64(0), tie)
+    bm, pc = t % np.uint64(nbm), t // np.uint64(nbm)
+    index = (bm * np.uint64(NP) + pc // np.uint64(NC)) * np.uint64(NC) + pc % np.uint64(NC)
+    out = np.zeros((S, 3), dtype=np.int64)
+    out[:, 0] = np.where(empty, 0, recs[:, 0])
+    out[:, 1] = index.view(np.int64)
+    out[:, 2] = np.where(empty, abi.GP_ERR_NO_FEASIBLE, abi.GP_OK)
+    if flags.any():  # the owners redo their flagged snapshots with status tracking
+        mine = [j for j in range(lo, hi) if flags[j]]
+        loc = out[lo:hi].copy()
+        for j in mine:
+            bests, status = eng.replan_snapshots(bandwidths[j:j + 1])
+            cost, idx = best_fields(bests, 1)
+            loc[j - lo] = (cost.view(np.int64)[0], idx.view(np.int64)[0], status[0])
+        out = gather_snapshot_records(loc, S, group, dev)
+    return out
 
 
 def decode_snapshot_records(packed, rec: np.ndarray):

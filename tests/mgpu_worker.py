@@ -49,6 +49,20 @@ def main():
     bws = R.bandwidth_matrices(packed, [I.snapshot_multipliers(spec, j) for j in range(37)])
     res = DI.replan_snapshots_sharded(model, topo, groups, P.SearchConfig(seed=0), bws, engine=eng)
     out["snapshots"] = [r if isinstance(r, tuple) else type(r).__name__ for r in res]
+    # snapshots whose tables raise (a device cut off from every link): the
+    # device-resident sharded path hands them to their owners' status path;
+    # the answers must equal the single-engine re-plan's
+    import numpy as np
+    bws2 = bws.copy()
+    for j in (3, 11, 20, 36):
+        d = 1 + j % 5
+        bws2[j][d, :] = 0.0
+        bws2[j][:, d] = 0.0
+    fix = lambda rr: [r if isinstance(r, tuple) else type(r).__name__ for r in rr]  # noqa: E731
+    got = fix(DI.replan_snapshots_sharded(model, topo, groups, P.SearchConfig(seed=0), bws2, engine=eng))
+    exp = fix(R.replan_snapshots(model, topo, groups, P.SearchConfig(seed=0), bws2, engine=eng))
+    out["flagged_equal"] = got == exp
+    out["flagged_errors"] = sum(not isinstance(r, (tuple, list)) for r in got)
     # peer-memory all-gather (NVLink stores + arrival counter) vs NCCL's, for
     # the K6 winners of C3 snapshot shards, over several epochs
     import numpy as np

@@ -68,6 +68,11 @@ def test_sharded_snapshots_match_golden(sharded):
         assert r[0] == snap[j]["cost"], j
 
 
+def test_sharded_snapshots_with_raising_tables(sharded):
+    assert sharded["flagged_equal"]
+    assert sharded["flagged_errors"] >= 1
+
+
 def test_peer_memory_allgather_matches_nccl(sharded):
     assert sharded["peer_ok"], "peer-memory set-up failed (no P2P between the GPUs?)"
     assert sharded["peer_equal"] == [True, True, True]
