@@ -157,7 +157,9 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
-        time.sleep(0.2)
+        # nvidia-smi's NVML start-up takes driver locks for a few hundred ms;
+        # let it reach its steady polling before the timed region starts
+        time.sleep(1.0)
         return self
 
     def __exit__(self, *a):
