@@ -747,16 +747,13 @@ def scaling_rows(X, eng, packed, model, topo, groups, total):
     d_st = torch.empty(max(1, nloc), dtype=torch.uint8, device=X.dev)
     key = torch.empty(2, dtype=torch.int64, device=X.dev)
     gk = torch.empty(2 * X.world, dtype=torch.int64, device=X.dev)
-    big = torch.tensor(2**62, dtype=torch.int64, device=X.dev)
     torch.cuda.synchronize()
 
     def k2_step():
         eng.eval_batch_device(4, nloc, d_o.data_ptr(), d_c.data_ptr(), d_b.data_ptr(),
                               d_cost.data_ptr(), d_st.data_ptr())
-        c = d_cost[:nloc]
-        m = c.min()
-        key[0] = m.view(torch.int64)
-        key[1] = torch.where(c == m, d_i, big).min()
+        eng.argmin_batch_device(nloc, d_cost.data_ptr(), d_st.data_ptr(), d_i.data_ptr(),
+                                key.data_ptr())
         if X.world > 1:
             dist.all_gather_into_tensor(gk, key)
     dev_ms = event_loop(X, stream, k2_step, 30, 3)
@@ -769,7 +766,8 @@ def scaling_rows(X, eng, packed, model, topo, groups, total):
         "candidates_per_s": idx.size / (statistics.median(dmax) * 1e-3),
         "best_index": int(g[wi, 1]), "best_cost": float(np.int64(g[wi, 0]).view(np.float64)),
         "note": "random.Random(4).sample(range(11387376), 10**6) (BASELINE configs[3]); per "
-                "rank: K2 on its contiguous chunk, device arg-min (cost, index), NCCL all-gather"}
+                "rank: K2 on its contiguous chunk, gp_argmin_batch_device (cost, index), NCCL "
+                "all-gather"}
 
     # (c) C3: C2 under 10^4 bandwidth snapshots, partitioned by index
     spec2 = instances.config("c2")

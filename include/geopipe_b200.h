@@ -287,6 +287,19 @@ int gp_eval_batch_device(gp_ctx *ctx, uint32_t k, uint64_t n,
  * (cost, (order, cuts)) with earliest-index tie-break.
  * gp_space_size() gives the total count.
  */
+/*
+ * Arg-min over a batch evaluated by gp_eval_batch_device (device pointers,
+ * asynchronous on the context stream): the least (cost, key) over the n
+ * candidates with status 0, key = d_keys[i] (u64; e.g. the enumeration
+ * index of a sampled candidate) or i when d_keys is NULL, written to d_out
+ * as {cost bits, key} (2 x u64, device memory); {+inf bits, ~0} when no
+ * candidate has status 0.  The min over a candidate list the reference
+ * takes in _evaluate's callers (src/planner.py:313-327), keyed for a
+ * deterministic tie-break across shards.
+ */
+int gp_argmin_batch_device(gp_ctx *ctx, uint64_t n, const double *d_cost, const uint8_t *d_status,
+                           const uint64_t *d_keys, uint64_t *d_out);
+
 int gp_space_size(gp_ctx *ctx, uint64_t *out);
 int gp_argmin_range(gp_ctx *ctx, uint64_t lo, uint64_t hi, gp_best *out);
 /* Same result as gp_argmin_range over the whole space, by exact

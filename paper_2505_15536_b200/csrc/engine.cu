@@ -100,6 +100,8 @@ struct gp_ctx {
     // K3 scratch
     DBuf<Key> blk, result;
     DBuf<unsigned int> counter;
+    DBuf<Key> bam_blk;              // gp_argmin_batch_device: per-CTA keys
+    DBuf<unsigned int> bam_ctr;     //   and its CTA counter (re-armed by the last CTA)
     DBuf<unsigned long long> err_idx;
     DBuf<int> err_dummy;
     // K2 staging
@@ -339,7 +341,7 @@ void gp_ctx_destroy(gp_ctx* c) {
     c->binom.release(); c->item_ctr.release(); c->tiles.release(); c->groups.release(); c->prefixes.release(); c->bnk.release(); c->recruns.release(); c->recrow.release(); c->k5_perm.release(); c->k5_hist.release();
     c->tpk.release(); c->tcol.release();
     c->stg.release(); c->gw.release(); c->blk.release(); c->result.release();
-    c->counter.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
+    c->counter.release(); c->bam_blk.release(); c->bam_ctr.release(); c->err_idx.release(); c->err_dummy.release(); c->info.release();
     c->ginfo.release(); c->dstatus.release(); c->vbuf.release();
     cudaStreamDestroy(c->stream);
     delete c;
@@ -688,6 +690,31 @@ int gp_reset_bandwidth(gp_ctx* c) {
 }
 
 static int kernel_slots(gp_ctx* c, const void* kern, int threads, size_t smem, int* per_sm);
+
+int gp_argmin_batch_device(gp_ctx* c, uint64_t n, const double* d_cost, const uint8_t* d_status,
+                           const uint64_t* d_keys, uint64_t* d_out) {
+    if (!c || (n && (!d_cost || !d_status)) || !d_out) return fail(GP_ERR_INPUT, "bad arguments");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const unsigned long long gmax = 2ull * (unsigned long long)c->n_sms;
+    if (!c->bam_ctr.p) {
+        CUDA_TRY(c->bam_ctr.ensure(1));
+        CUDA_TRY(c->bam_blk.ensure(gmax));  // fixed capacity: never reallocated under a launch
+        CUDA_TRY(cudaMemsetAsync(c->bam_ctr.p, 0, sizeof(unsigned int), c->stream));
+    }
+    unsigned long long grid = (n + 1023) / 1024;
+    if (grid > gmax) grid = gmax;
+    if (grid < 1) grid = 1;
+    ArgminScratch S;
+    S.blk = c->bam_blk.p;
+    S.counter = c->bam_ctr.p;
+    S.result = reinterpret_cast<Key*>(d_out);
+    S.err = nullptr;
+    S.err_idx = nullptr;
+    k2_batch_argmin<<<(unsigned)grid, 256, 0, c->stream>>>((unsigned long long)n, d_cost, d_status,
+                                                          reinterpret_cast<const unsigned long long*>(d_keys), S);
+    CUDA_TRY(cudaGetLastError());
+    return GP_OK;
+}
 
 int gp_eval_batch_device(gp_ctx* c, uint32_t k, uint64_t n, const uint8_t* d_order,
                          const uint8_t* d_counts, const uint8_t* d_bm, double* d_cost,

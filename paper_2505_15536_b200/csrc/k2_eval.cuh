@@ -934,3 +934,22 @@ static __global__ void k2_image_build(DevInst I, uint8_t* __restrict__ img) {
         }
     }
 }
+
+// Arg-min over an evaluated batch (gp_argmin_batch_device): the least
+// (cost, key) over the candidates with status 0, key = keys[i] (e.g. the
+// enumeration index of a sampled candidate) or i; {+inf, ~0} when none.
+// Grid-stride scan, then the CTA / last-CTA reduction of common.cuh.
+static __global__ void __launch_bounds__(256) k2_batch_argmin(unsigned long long n,
+                                                               const double* __restrict__ cost,
+                                                               const uint8_t* __restrict__ status,
+                                                               const unsigned long long* __restrict__ keys,
+                                                               ArgminScratch S) {
+    Key mine{INFINITY, ~0ull};
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        if (__ldg(&status[i])) continue;
+        const Key o{__ldg(&cost[i]), keys ? __ldg(&keys[i]) : i};
+        if (key_less(o, mine)) mine = o;
+    }
+    block_argmin_finish(mine, S);
+}

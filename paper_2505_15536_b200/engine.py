@@ -48,6 +48,7 @@ def lib():
         L.gp_eval_batch.argtypes = [vp, C.c_uint32, C.c_uint64, u8p, u8p, u8p,
                                     P(C.c_double), u8p]
         L.gp_eval_batch_device.argtypes = [vp, C.c_uint32, C.c_uint64, vp, vp, vp, vp, vp]
+        L.gp_argmin_batch_device.argtypes = [vp, C.c_uint64, vp, vp, vp, vp]
         L.gp_space_size.argtypes = [vp, P(C.c_uint64)]
         L.gp_argmin_range.argtypes = [vp, C.c_uint64, C.c_uint64, P(abi.GpBest)]
         L.gp_argmin_range_async.argtypes = [vp, C.c_uint64, C.c_uint64]
@@ -186,6 +187,12 @@ class Engine:
         """Device-pointer variant (ints), asynchronous on :attr:`stream`."""
         _check(lib().gp_eval_batch_device(self._h, k, n, d_order, d_counts, d_bm,
                                           d_cost, d_status))
+
+    def argmin_batch_device(self, n, d_cost, d_status, d_keys, d_out):
+        """Device-pointer arg-min of an evaluated batch (ints; d_keys may be
+        0), asynchronous on :attr:`stream`: d_out[0:2] (u64) = (cost bits,
+        key) of the least (cost, key) with status 0 (gp_argmin_batch_device)."""
+        _check(lib().gp_argmin_batch_device(self._h, int(n), d_cost, d_status, d_keys or None, d_out))
 
     def argmin_range(self, lo: int, hi: int) -> abi.GpBest:
         best = abi.GpBest()

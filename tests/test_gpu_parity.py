@@ -200,6 +200,57 @@ def test_k2_image_follows_table_changes(engine, oracle_lib):
     check(base)
 
 
+def test_k2_batch_argmin_device(engine, oracle_lib):
+    """gp_argmin_batch_device: least (cost, key) over the status-0 candidates
+    of an evaluated batch - against numpy on a K2-evaluated C4 sample (keys =
+    enumeration indices, malformed candidates mixed in) and on synthetic
+    batches full of cost ties, +inf, errors, no keys, empty and all-invalid."""
+    import torch
+    from paper_2505_15536_b200.enumeration import composition_table, decode_indices
+    doc, model, topo, groups, packed = _load(engine, "c4")
+    dev = torch.device("cuda", engine.device)
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def run(cost, status, keys):
+        n = cost.size
+        dc = torch.from_numpy(cost).to(dev) if n else torch.zeros(1, dtype=torch.float64, device=dev)
+        ds = torch.from_numpy(status).to(dev) if n else torch.zeros(1, dtype=torch.uint8, device=dev)
+        dk = torch.from_numpy(keys.view(np.int64)).to(dev) if keys is not None and n else None
+        torch.cuda.synchronize()
+        engine.argmin_batch_device(n, dc.data_ptr(), ds.data_ptr(), dk.data_ptr() if dk is not None else 0,
+                                   out.data_ptr())
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        return o[0], np.uint64(o[1])
+
+    def expect(cost, status, keys):
+        k = keys if keys is not None else np.arange(cost.size, dtype=np.uint64)
+        ok = np.nonzero(status == 0)[0]
+        if ok.size == 0:
+            return np.float64(np.inf).view(np.int64), np.uint64(0xFFFFFFFFFFFFFFFF)
+        j = ok[np.lexsort((k[ok], cost[ok]))[0]]
+        return cost[j].view(np.int64), k[j]
+
+    total = engine.space_size()
+    rng = np.random.default_rng(31)
+    idx = rng.integers(0, total, size=300_000).astype(np.uint64)
+    order, counts, bm = decode_indices(packed.n_layers, 4, idx.astype(np.int64),
+                                       composition_table(packed.n_layers, 4))
+    counts = counts.copy()
+    counts[::97, 0] = 0
+    cost, status = engine.eval_batch(order, counts, bm)
+    assert run(cost, status, idx) == expect(cost, status, idx)
+    assert run(cost, status, None) == expect(cost, status, None)
+    for n in (0, 1, 7, 1000, 70_001):
+        c = rng.integers(0, 5, size=n).astype(np.float64)
+        c[rng.random(n) < 0.2] = np.inf
+        st = (rng.random(n) < 0.3).astype(np.uint8)
+        keys = rng.permutation(n).astype(np.uint64) * np.uint64(3)
+        assert run(c, st, keys) == expect(c, st, keys), n
+        assert run(c, st, None) == expect(c, st, None), n
+        assert run(c, np.ones(n, np.uint8), keys) == expect(c, np.ones(n, np.uint8), keys), n
+
+
 def test_k2_rejects_bad_candidates(engine):
     doc, model, topo, groups, packed = _load(engine, "c2")
     order = np.array([[0, 0, 1], [0, 1, 7], [0, 1, 2], [0, 1, 2]], np.uint8)
