@@ -82,9 +82,9 @@ def reduce_key(key: Tuple[float, int], group=None, device=None, err=None) -> Tup
         keys = [(ek, _cost_bits(key[0]), key[1])]
     else:
         t = torch.tensor([ek, _cost_bits(key[0]), key[1]], dtype=torch.int64, device=device)
-        out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
-        dist.all_gather(out, t, group=group)
-        keys = [(int(o[0]), int(o[1]), int(o[2])) for o in out]
+        out = torch.empty(3 * dist.get_world_size(group), dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(out, t, group=group)  # one collective, one D2H
+        keys = [tuple(int(x) for x in row) for row in out.cpu().numpy().reshape(-1, 3)]
     e = min(k[0] for k in keys)
     if e != NO_ERR:
         from . import abi
