@@ -172,8 +172,9 @@ def _replan_shard_device(eng, packed, bandwidths, S, lo, hi, world, group):
     collective.  Snapshots whose tables raise (flags) are redone by their
     owner through the status-tracking gp_replan_snapshots and shared with a
     second gather (every rank sees the same flags, so the collectives stay
-    matched).  None when the loaded instance needs the status path for
-    every snapshot (gp_replan_snapshots_async refuses it on every rank)."""
+    matched).  None on every rank when any rank's asynchronous re-plan was
+    refused (its records carry -1 flags through the same all-gather); the
+    caller then takes the host-staged path on all ranks."""
     import torch
     import torch.distributed as dist
     from . import abi
@@ -197,18 +198,21 @@ def _replan_shard_device(eng, packed, bandwidths, S, lo, hi, world, group):
                    non_blocking=True)
     est = torch.cuda.ExternalStream(eng.stream, device=dev)
     est.wait_stream(cur)
-    ok = 1
+    ok = True
     try:
         eng.replan_snapshots_async(d_bw.data_ptr(), n, d_keys.data_ptr(), d_flags.data_ptr())
     except D.GeopipeError:
-        ok = 0  # the instance itself needs the status path (same on every rank)
+        ok = False  # e.g. an instance that needs the status path for every snapshot
     cur.wait_stream(est)
-    if not ok:
-        return None
-    d_rec[:n, :2].copy_(d_keys[:n])
-    d_rec[:n, 2].copy_(d_flags[:n])
+    if ok:
+        d_rec[:n, :2].copy_(d_keys[:n])
+        d_rec[:n, 2].copy_(d_flags[:n])
+    else:
+        d_rec[:, 2].fill_(-1)  # tells every rank: all take the host-staged path
     dist.all_gather_into_tensor(d_out, d_rec, group=group)
     allrec = d_out.cpu().numpy().reshape(world, width, 3)
+    if (allrec[:, 0, 2] == -1).any():
+        return None
     NC, NP, _ = space_dims(packed.n_layers, packed.n_fgs, len(packed.batches), len(packed.micros))
     nbm = len(packed.batches) * len(packed.micros)
     rows = []

@@ -62,6 +62,15 @@ def main():
     got = fix(DI.replan_snapshots_sharded(model, topo, groups, P.SearchConfig(seed=0), bws2, engine=eng))
     exp = fix(R.replan_snapshots(model, topo, groups, P.SearchConfig(seed=0), bws2, engine=eng))
     out["flagged_equal"] = got == exp
+    # an instance whose own tables raise: the asynchronous path is refused on
+    # every rank, all ranks take the host-staged path together
+    docE, mE, tE, gE = load_case("err_gateway")
+    pE = PackedInstance(mE, tE, gE, 1.25)
+    bwE = np.stack([pE.bw] * 5)
+    gotE = fix(DI.replan_snapshots_sharded(mE, tE, gE, P.SearchConfig(seed=0), bwE, engine=eng))
+    expE = fix(R.replan_snapshots(mE, tE, gE, P.SearchConfig(seed=0), bwE, engine=eng))
+    out["refused_equal"] = gotE == expE
+    out["refused_kinds"] = sorted(set(gotE))
     out["flagged_errors"] = sum(not isinstance(r, (tuple, list)) for r in got)
     # peer-memory all-gather (NVLink stores + arrival counter) vs NCCL's, for
     # the K6 winners of C3 snapshot shards, over several epochs

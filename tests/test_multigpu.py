@@ -71,6 +71,7 @@ def test_sharded_snapshots_match_golden(sharded):
 def test_sharded_snapshots_with_raising_tables(sharded):
     assert sharded["flagged_equal"]
     assert sharded["flagged_errors"] >= 1
+    assert sharded["refused_equal"], sharded["refused_kinds"]
 
 
 def test_peer_memory_allgather_matches_nccl(sharded):
