@@ -1060,8 +1060,10 @@ def main():
                              "gp_replan_snapshots_async (K6 table patch + K3 sweep) into device "
                              "keys, NCCL all-gather of the records from device memory, one D2H"
                              if X.world > 1 else
-                             ": pinned host bandwidth matrices -> gp_replan_snapshots (H2D, K6 "
-                             "table patch + K3 sweep, D2H of the winners)")},
+                             ": pinned host bandwidth matrices -> gp_replan_snapshots (the K6 "
+                             "patch kernels read the member-pair and gateway entries of the "
+                             "pinned matrices in place over PCIe - zero-copy - then the K3 "
+                             "sweep, D2H of the winners)")},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": SWEEP_DRAM_BYTES,

@@ -490,7 +490,10 @@ int gp_plan_timing(gp_ctx *ctx, uint32_t k, uint64_t n, const uint8_t *order,
  * latency unchanged) and out[i] receives exhaustive_plan's arg-min on that
  * topology (min_intra_bandwidth re-derived as group_first_level would).
  * status[i] = GP_OK or the error exhaustive_plan would raise.  The loaded
- * instance is left unchanged.
+ * instance is left unchanged.  When `bandwidth` lies in pinned (mapped) host
+ * memory the device reads the entries it needs in place (zero-copy);
+ * pageable memory is copied to the device first.  The buffer must not change
+ * until the call returns (it is synchronous).
  */
 int gp_replan_snapshots(gp_ctx *ctx, const double *bandwidth, uint32_t n_snap, gp_best *out,
                         int32_t *status);

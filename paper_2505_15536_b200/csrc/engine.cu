@@ -2228,18 +2228,35 @@ int gp_replan_snapshots(gp_ctx* c, const double* bandwidth, uint32_t n_snap, gp_
     std::vector<uint32_t> h_fl(SB);
     std::vector<Key> h_res(SB);
     std::vector<uint32_t> slow;
+    // matrices in pinned (mapped) host memory are read in place by the
+    // patch kernels - only the member-pair and gateway entries cross PCIe
+    // (about a quarter of each matrix at C4) - instead of a full H2D copy
+    // (GP_SNAP_ZEROCOPY=0 disables)
+    const double* zc = nullptr;
+    {
+        cudaPointerAttributes pa;
+        const char* e = getenv("GP_SNAP_ZEROCOPY");
+        if ((!e || atoi(e) != 0) && cudaPointerGetAttributes(&pa, bandwidth) == cudaSuccess &&
+            pa.type == cudaMemoryTypeHost && pa.devicePointer)
+            zc = static_cast<const double*>(pa.devicePointer);
+        (void)cudaGetLastError();  // (pageable memory: not an error here)
+    }
     for (uint32_t b0 = 0; b0 < n_snap; b0 += SB) {
         const uint32_t nb = (n_snap - b0) < SB ? (n_snap - b0) : SB;
         if (!fast) {
             for (uint32_t i = 0; i < nb; ++i) slow.push_back(b0 + i);
             continue;
         }
-        CUDA_TRY(c->z_bw.ensure((size_t)SB * DD));
         CUDA_TRY(c->z_flags.ensure(SB));
         CUDA_TRY(c->z_res.ensure(SB));
-        CUDA_TRY(cudaMemcpyAsync(c->z_bw.p, bandwidth + (size_t)b0 * DD, (size_t)nb * DD * 8,
-                                 cudaMemcpyHostToDevice, s));
-        int st = snap_enqueue(c, c->z_bw.p, nb, c->z_res.p, c->z_flags.p, b0);
+        const double* d_bw = zc ? zc + (size_t)b0 * DD : nullptr;
+        if (!zc) {
+            CUDA_TRY(c->z_bw.ensure((size_t)SB * DD));
+            CUDA_TRY(cudaMemcpyAsync(c->z_bw.p, bandwidth + (size_t)b0 * DD, (size_t)nb * DD * 8,
+                                     cudaMemcpyHostToDevice, s));
+            d_bw = c->z_bw.p;
+        }
+        int st = snap_enqueue(c, d_bw, nb, c->z_res.p, c->z_flags.p, b0);
         if (st != GP_OK) return st;
         CUDA_TRY(cudaMemcpyAsync(h_res.data(), c->z_res.p, nb * sizeof(Key), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaMemcpyAsync(h_fl.data(), c->z_flags.p, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
