@@ -62,6 +62,10 @@ def main():
     got = fix(DI.replan_snapshots_sharded(model, topo, groups, P.SearchConfig(seed=0), bws2, engine=eng))
     exp = fix(R.replan_snapshots(model, topo, groups, P.SearchConfig(seed=0), bws2, engine=eng))
     out["flagged_equal"] = got == exp
+    # pinned host matrices (the bench's e2e input)
+    pinned = torch.from_numpy(np.ascontiguousarray(bws2)).pin_memory().numpy()
+    out["pinned_equal"] = fix(DI.replan_snapshots_sharded(model, topo, groups, P.SearchConfig(seed=0),
+                                                          pinned, engine=eng)) == exp
     # an instance whose own tables raise: the asynchronous path is refused on
     # every rank, all ranks take the host-staged path together
     docE, mE, tE, gE = load_case("err_gateway")

@@ -72,6 +72,7 @@ def test_sharded_snapshots_with_raising_tables(sharded):
     assert sharded["flagged_equal"]
     assert sharded["flagged_errors"] >= 1
     assert sharded["refused_equal"], sharded["refused_kinds"]
+    assert sharded["pinned_equal"]
 
 
 def test_peer_memory_allgather_matches_nccl(sharded):

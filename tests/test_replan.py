@@ -50,6 +50,21 @@ def test_k6_replan_200_snapshots(engine):
 
 
 @pytest.mark.gpu
+def test_k6_replan_pinned_matrices_read_in_place(engine):
+    """Pinned (mapped) host matrices are read in place by the patch kernels
+    (zero-copy) - same winners as the golden composition."""
+    import torch
+    spec, model, topo, groups, packed, bws = _setup(60)
+    pinned = torch.from_numpy(bws).pin_memory().numpy()
+    engine.load(packed)
+    bests, status = engine.replan_snapshots(pinned)
+    assert (status == 0).all()
+    for j, rec in enumerate(SNAP["snapshots"][:60]):
+        assert bests[j].cost == rec["cost"], j
+        assert bests[j].index == rec["index"], j
+
+
+@pytest.mark.gpu
 def test_k6_replan_detail_matches_reference(engine):
     from paper_2505_15536_b200 import SearchConfig
     spec, model, topo, groups, packed, bws = _setup(3)
