@@ -55,8 +55,11 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# rank 0 prints exactly one JSON line on stdout (no NCCL banner)
-os.environ.setdefault("NCCL_DEBUG", "WARN")
+# rank 0 prints exactly one JSON line on stdout: NCCL's version banner (the
+# GPU boxes export NCCL_DEBUG=VERSION) and warnings go to stderr
+if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+    os.environ["NCCL_DEBUG"] = "WARN"
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 # FP64 ops per candidate of independent evaluation in the reference's operation
 # order (11k - 5 = 39 for k = 4 stages): 6 per stage (C1*m,
