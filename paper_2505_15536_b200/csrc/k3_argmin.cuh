@@ -316,9 +316,6 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
     const unsigned long long perm_rank = item % G.NP;
     uint8_t order[GP_MAX_STAGES];
     d_unrank_perm(k, perm_rank, order);
-    double Mv[NB];
-#pragma unroll
-    for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[G.b0 + bi] / I.micro[mi]);
     const double2* TPm = G.tpk + snap * G.s_tpk + (size_t)mi * I.F * ntri;
     const double* X = G.xt + snap * G.s_xt + (size_t)mi * I.F * I.F * I.nxp;
     const int f1 = order[k - 3], f2 = order[k - 2], f3 = order[k - 1];
@@ -374,6 +371,11 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
             if (MODE == 2) copy(tri1, P1, (uint32_t)ntri * 16);
         }
     }
+    // micro-batch counts M = B / m (loaded after the copies are issued: on a
+    // cold L2 their latency would otherwise delay the TMA issue)
+    double Mv[NB];
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[G.b0 + bi] / I.micro[mi]);
     __syncthreads();
     mbar_wait(bar, 0);
     if (mc) cluster_arrive();  // this CTA's copies have landed (waited on before exit)
