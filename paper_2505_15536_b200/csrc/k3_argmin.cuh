@@ -371,18 +371,6 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
             if (MODE == 2) copy(tri1, P1, (uint32_t)ntri * 16);
         }
     }
-    // micro-batch counts M = B / m (loaded after the copies are issued: on a
-    // cold L2 their latency would otherwise delay the TMA issue)
-    double Mv[NB];
-#pragma unroll
-    for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[G.b0 + bi] / I.micro[mi]);
-    __syncthreads();
-    mbar_wait(bar, 0);
-    if (mc) cluster_arrive();  // this CTA's copies have landed (waited on before exit)
-#if defined(K3_PROFILE)
-    unsigned long long t1p; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1p));
-#endif
-
     const int lane = threadIdx.x & 31;
     double best_c = INFINITY;
     unsigned long long best_t = ~0ull;  // R * NB + bi
@@ -401,8 +389,20 @@ __global__ void __launch_bounds__(K3S_THREADS, K3S_MINB) k3_sweep(DevInst I, Swe
                                     (blockDim.x >> 5) + (threadIdx.x >> 5);
     t_next = wfirst;
 #else
-    if (lane == 0 && !skip) t_next = atomicAdd(ctr, 1u);
+    if (lane == 0 && !skip) t_next = atomicAdd(ctr, 1u);  // (its latency overlaps the staging)
 #endif
+    // micro-batch counts M = B / m (loaded after the copies are issued: on a
+    // cold L2 their latency would otherwise delay the TMA issue)
+    double Mv[NB];
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi) Mv[bi] = (double)(I.batch[G.b0 + bi] / I.micro[mi]);
+    __syncthreads();
+    mbar_wait(bar, 0);
+    if (mc) cluster_arrive();  // this CTA's copies have landed (waited on before exit)
+#if defined(K3_PROFILE)
+    unsigned long long t1p; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1p));
+#endif
+
     for (; !skip;) {
 #if defined(K3_STATIC)
         const unsigned int t = t_next;
